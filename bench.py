@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark of the per-batch update of r neighborhood-sampling estimators (bulkUpdateAll,
+PAPER.md:494-505) on B200.
+
+One step = one tc_push_batch of the next w edges of the synthetic stream (all §8(a) rows: staging,
+incidence index, edge-pair hash, fused Steps 1-3 + partial sums).  Default workload = BASELINE.json
+configs[1] (C2: R-MAT scale 20, ~15.7M edges, r = w = 2^20): the full stream is 15 batches, so the
+default --steps 15 times one whole stream through a fresh estimator set.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+Multi-GPU (torchrun, one process per GPU): estimators are sharded by global id; rank 0 holds the
+stream and broadcasts each batch over NCCL inside the timed region; the estimate all-reduces the
+per-rank exact partial sums.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import CONFIGS, config_stream  # noqa: E402
+
+METRIC = "edges/s and estimator-updates/s per batch; fraction of HBM roofline"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=15)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--w", type=int, default=0, help="override the batch size (C5 sweep)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# --------------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return None
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(config):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(config)
+    return None
+
+
+# --------------------------------------------------------------------------------------------------
+def algorithmic_bytes(phase, w, R, D, fresh, r2old):
+    """Algorithmic bytes per launch: what each phase must move at minimum.
+
+    update : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
+             (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
+             index probes are L2 traffic at C2 and not counted.
+    stage  : read 8 B/edge; write E 8 + arc record 16 + pair slot 16 B/edge; 16 B per vertex slot.
+    segment: 24 B per distinct vertex.   scatter: 16 + 8 B/edge.   sort: 8 + 8 + 16 B/edge.
+    """
+    if phase == "update":
+        return 24 * (R - fresh) + 36 * fresh + 16 * r2old
+    if phase == "stage":
+        return 48 * w + 16 * D
+    if phase == "segment":
+        return 24 * D
+    if phase == "scatter":
+        return 24 * w
+    if phase == "sort":
+        return 32 * w
+    raise KeyError(phase)
+
+
+def run_b200(args):
+    import torch
+    world, rank, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    from paper_1308_2166_b200 import TriangleCounter, build as libbuild
+    libbuild.build()
+
+    cfg = dict(CONFIGS[args.config])
+    r = cfg["r"]
+    w = args.w or cfg["w"]
+    stream = config_stream(args.config)
+    m_total = len(stream)
+    nb = (m_total + w - 1) // w
+    first = rank * r // world
+    count = (rank + 1) * r // world - first
+
+    # stream resident in HBM before timing ("excluding I/O"); rank 0 owns it
+    dstream = torch.from_numpy(stream.view(np.int32)).to(dev) if rank == 0 else None
+    bbuf = torch.empty((w, 2), dtype=torch.int32, device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+
+    def batch(k, ext=None):
+        lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
+        if world == 1:
+            return dstream[lo:hi]
+        n = hi - lo
+        cur = torch.cuda.current_stream()
+        if ext is not None:
+            cur.wait_stream(ext)  # the previous batch's kernels are done reading bbuf
+        if rank == 0:
+            bbuf[:n].copy_(dstream[lo:hi])
+        torch.distributed.broadcast(bbuf[:n], src=0)  # NCCL over NVLink: the per-batch exchange
+        if ext is not None:
+            ext.wait_stream(cur)  # the library stream sees the broadcast batch
+        return bbuf[:n]
+
+    def make():
+        tc = TriangleCounter(r, args.seed, first=first, count=count, device=dev.index, w_max_hint=w)
+        tc.set_async(True)
+        return tc
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- warm-up (untimed) ----
+    tc = make()
+    for k in range(args.warmup):
+        if k and k % nb == 0:
+            tc = make()
+        ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
+        tc.push_batch(batch(k, ext))
+    assert tc.sync() == 0
+    del tc
+
+    # ---- timed: K steps, each bracketed by CUDA events on the library's stream; L2 flushed between ----
+    tc = make()
+    tc.profile(True)
+    ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
+    evs = []
+    launches = 0
+    edges_done = 0
+    counters_for_bytes = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        t_wall = time.perf_counter()
+        for k in range(args.steps):
+            if k and k % nb == 0:  # stream exhausted: a fresh estimator set (creation untimed)
+                assert tc.sync() == 0
+                counters_for_bytes.append(tc)
+                tc = make()
+                tc.profile(True)
+                ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
+            with torch.cuda.stream(ext):
+                flush.fill_(k)  # > L2: every step starts with a cold cache
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(ext)
+            b = batch(k, ext)
+            tc.push_batch(b)
+            with torch.cuda.stream(ext):
+                e1.record(ext)
+            evs.append((e0, e1))
+            launches += tc.last_launches()
+            edges_done += b.shape[0]
+        assert tc.sync() == 0
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall
+    barrier()
+    counters_for_bytes.append(tc)
+    ms = sum(a.elapsed_time(b) for a, b in evs)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms = float(t.item())
+    secs = ms / 1e3
+
+    # per-phase device time (library events) and the dominant kernel's roofline
+    prof = {}
+    for c in counters_for_bytes:
+        for p, (pms, n) in c.profile_read().items():
+            a = prof.setdefault(p, [0.0, 0])
+            a[0] += pms
+            a[1] += n
+    stats = [c.stats() for c in counters_for_bytes]
+    fresh = sum(s["fresh"] for s in stats)
+    r2old = sum(s["r2_replaced_retained"] for s in stats)
+    D = sum(s["vertices"] for s in stats)
+    dom = max(prof, key=lambda p: prof[p][0])
+    peak, peak_src = measured_peaks()
+    nsteps = args.steps
+    total_alg = {
+        "update": algorithmic_bytes("update", 0, count * nsteps, 0, fresh, r2old),
+        "stage": algorithmic_bytes("stage", edges_done, 0, D, 0, 0),
+        "segment": algorithmic_bytes("segment", 0, 0, D, 0, 0),
+        "scatter": algorithmic_bytes("scatter", edges_done, 0, 0, 0, 0),
+        "sort": algorithmic_bytes("sort", edges_done, 0, 0, 0, 0),
+    }
+    kernels_in = {"stage": 1, "segment": 1, "scatter": 1, "sort": 3, "update": 1}
+    dom_secs = prof[dom][0] / 1e3
+    achieved = total_alg[dom] / dom_secs / 1e9 if dom_secs > 0 else None
+    upd_secs = prof["update"][0] / 1e3
+    upd_ach = total_alg["update"] / upd_secs / 1e9 if upd_secs > 0 else None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak if achieved else None,
+                "traffic": committed_traffic(args.config), "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": total_alg[dom] / max(1, nsteps),
+                "launch_ms": prof[dom][0] / max(1, nsteps),
+                "update_kernel": {"achieved": upd_ach, "frac": upd_ach / peak if upd_ach else None,
+                                  "launch_ms": prof["update"][0] / max(1, nsteps)},
+                "phase_ms_per_step": {p: prof[p][0] / max(1, nsteps) for p in prof},
+                "phase_share": {p: prof[p][0] / max(1e-12, sum(v[0] for v in prof.values())) for p in prof}}
+
+    value = edges_done / secs
+    out = {
+        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded R-MAT/ER/Chung-Lu stand-ins; the paper's SNAP datasets are not available)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w, "stream_edges": m_total,
+                   "batches_per_stream": nb, "estimators_per_gpu": count, "parallelism": f"estimator-shard x{world}",
+                   "l2": "flushed before every step (256 MiB write, outside the step's events)",
+                   "timing": "CUDA events on the library stream around each tc_push_batch, summed; max over ranks"},
+        "estimator_updates_per_s": edges_done * r / secs,
+        "batch_estimator_updates_per_s": nsteps * r / secs,
+        "gpu_launches": launches,
+        "roofline": roofline,
+        "wall_s_timed_region": t_wall,
+    }
+    clk = clocks.summary()
+    out["clocks"] = clk
+
+    # ---- e2e: the public API with HOST (pinned) buffers, H2D + result D2H inside every step ----
+    if not args.no_e2e and world == 1:
+        host = torch.from_numpy(stream.view(np.int32)).pin_memory()
+        tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+        ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
+        for k in range(min(args.warmup, nb)):
+            tc2.push_batch(host[k * w:(k + 1) * w])
+        del tc2
+        tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+        ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
+        e_ms, e_edges, h2d = 0.0, 0, 0
+        for k in range(args.steps):
+            if k and k % nb == 0:
+                tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+                ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
+            lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
+            with torch.cuda.stream(ext2):
+                flush.fill_(k)
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(ext2)
+            tc2.push_batch(host[lo:hi])  # strict mode: H2D, kernels, 4-byte status D2H
+            est = tc2.estimate()  # 8-byte S D2H: the step's result
+            with torch.cuda.stream(ext2):
+                a1.record(ext2)
+            a1.synchronize()
+            e_ms += a0.elapsed_time(a1)
+            e_edges += hi - lo
+            h2d += 8 * (hi - lo)
+        out["e2e"] = {"value": e_edges / (e_ms / 1e3), "unit": "edges/s",
+                      "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 12,
+                      "note": "tc_push_batch(pinned host edges) + tc_estimate per step; CUDA events on the library stream"}
+        out["e2e_last_estimate"] = est
+
+    # ---- CPU baseline: the oracle as it stands, on this host's cores (rank 0, N = 1 only) ----
+    if not args.no_cpu_baseline and world == 1:
+        out["cpu_baseline"] = cpu_baseline(stream, r, w, args.seed, nbatches=min(8, nb))
+
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def cpu_baseline(stream, r, w, seed, nbatches):
+    from oracle.indexed import IndexedOracle, threads
+    o = IndexedOracle(r, seed)
+    t0 = time.perf_counter()
+    edges = 0
+    for k in range(nbatches):
+        W = stream[k * w:(k + 1) * w]
+        assert o.push_batch(W) == 0
+        edges += len(W)
+    dt = time.perf_counter() - t0
+    return {"value": edges / dt, "unit": "edges/s", "cores": threads(), "kind": "oracle",
+            "sample": f"first {nbatches} batches ({edges} edges) of the same stream at full r={r}, w={w}; "
+                      f"oracle/indexed.c (qsort + binary-search multisearch, OpenMP over estimators), {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (this tier's reference arm) timed on the host cores."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.indexed import IndexedOracle, threads
+    cfg = dict(CONFIGS[args.config])
+    r = cfg["r"]
+    w = args.w or cfg["w"]
+    stream = config_stream(args.config)
+    nb = (len(stream) + w - 1) // w
+    o = IndexedOracle(r, args.seed)
+    for k in range(args.warmup):
+        if k and k % nb == 0:
+            o = IndexedOracle(r, args.seed)
+        o.push_batch(stream[(k % nb) * w:(k % nb) * w + w])
+    o = IndexedOracle(r, args.seed)
+    t0 = time.perf_counter()
+    edges = 0
+    for k in range(args.steps):
+        if k and k % nb == 0:
+            o = IndexedOracle(r, args.seed)
+        W = stream[(k % nb) * w:(k % nb) * w + w]
+        assert o.push_batch(W) == 0
+        edges += len(W)
+    dt = time.perf_counter() - t0
+    v = edges / dt
+    cb = {"value": v, "unit": "edges/s", "cores": threads(), "kind": "oracle",
+          "sample": f"{args.steps} whole batches (w={w}) of {args.config} at full r={r}"}
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                      "data": "synthetic", "config": {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w},
+                      "cpu_baseline": cb,
+                      "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_b200(a)

@@ -1,0 +1,150 @@
+/*
+ * tc.h -- C ABI of the B200 bulk neighborhood-sampling triangle estimator
+ *         (Tangwongsan, Pavan, Tirthapura, arXiv:1308.2166; "coordinated bulk parallel").
+ *
+ * The library maintains r independent estimators, each a tuple (f1, f2, f3, chi) satisfying
+ * the neighborhood sampling invariant NBSI (§3.1), over a stream of undirected
+ * simple-graph edges that arrives in batches W (§4.1).  One call to
+ * tc_push_batch() is one run of bulkUpdateAll: Step 1 level-1 reservoir
+ * (PAPER.md:520-538), Step 2 level-2 edges and chi, Step 3 closing edges
+ * (PAPER.md:835-845), for all estimators of this handle, on the GPU.
+ *
+ * Conventions (all calls):
+ *  - Vertex ids are uint32; 0xFFFFFFFF is reserved (it encodes "empty") and is rejected.
+ *    The paper's batch is "an array of a pair of int's".
+ *  - Estimator ids are global, 0 .. r-1; a handle owns a contiguous shard [first, first+count)
+ *    (tc_create owns all of them).  All randomness is Philox4x32-10 keyed by (seed) with counter
+ *    (id, batch index, draw word) -- DESIGN.md reading R7 -- so a shard's states do not depend on
+ *    how the estimators are split across handles / GPUs.
+ *  - Errors: functions returning int return TC_OK (0) or a negative TC_E* code.  A rejected batch
+ *    leaves every estimator and the counters unchanged (all-or-nothing).
+ *  - Not thread-safe per handle (single writer); distinct handles are independent.
+ *  - Stream: every handle owns one CUDA stream on its device; all device work is issued on it.
+ */
+#ifndef TC_B200_H
+#define TC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tc_ctx tc_ctx; /* opaque, owned by the library */
+
+/* One stream element: an undirected edge {u, v}, any orientation.  8 bytes, layout == CUDA uint2. */
+typedef struct {
+    uint32_t u, v;
+} tc_edge;
+
+enum {
+    TC_OK = 0,
+    TC_EINVAL = -1,      /* bad argument, or a vertex id 0xFFFFFFFF in the batch            */
+    TC_ENOMEM = -2,      /* device or host allocation failed                                */
+    TC_ESELFLOOP = -3,   /* u == v in the batch (the graph is simple)          */
+    TC_EDUP = -4,        /* the same undirected pair twice in one batch  */
+    TC_EOVERFLOW = -5,   /* m would exceed 2^31-1: chi <= m must fit 31 bits (reading R13)  */
+    TC_ECUDA = -6,       /* a CUDA call failed; the handle is poisoned                      */
+    TC_ESTATE = -8       /* handle poisoned by an earlier asynchronous error               */
+};
+
+/* tc_create -- r estimators (ids 0..r-1) on the current CUDA device, all "empty" (f1 = f2 = f3 =
+ * empty, chi = 0), m = 0.  seed keys the Philox stream.  Returns NULL on failure (r == 0, no device,
+ * out of memory); tc_last_error() then says why. */
+tc_ctx *tc_create(uint64_t r, uint64_t seed);
+
+/* tc_create_shard -- estimators [first, first+count) of r, on CUDA device `device` (-1 = current).
+ * w_max_hint preallocates the per-batch index for batches up to that many edges (0 = grow on
+ * demand).  count may be 0 (an idle shard still tracks m).  NULL on failure. */
+tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t count, int device,
+                        uint64_t w_max_hint);
+
+/* tc_push_batch -- bulkUpdateAll on the next w edges of the stream.
+ *  edges: w tc_edge in arrival order.  Host memory (pageable or pinned) or device memory on the
+ *         handle's device.  Host buffers are copied before the call returns; a device buffer must
+ *         stay valid and unmodified until the next synchronising call (tc_sync, tc_estimate*,
+ *         tc_get_state) when asynchronous errors are enabled, else until this call returns.
+ *  w == 0: no-op (the batch index does not advance).
+ *  Rejects the whole batch (state and counters unchanged) with, in this priority order:
+ *  TC_EINVAL (an id 0xFFFFFFFF), TC_ESELFLOOP, TC_EDUP, TC_EOVERFLOW.  Edges that repeat an edge of
+ *  an EARLIER batch are not detected (each edge arrives once).
+ *  In the default strict mode the call synchronises and returns the batch's status; with
+ *  tc_set_async(ctx, 1) it returns TC_OK after enqueueing, a failure is reported by the next
+ *  synchronising call, and the handle is then poisoned (TC_ESTATE) -- its state stays that of the
+ *  last accepted batch. */
+int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w);
+
+/* tc_estimate -- the mean of the coarse estimates X_i = chi_i * m if f3_i != empty else 0
+ * (Lemma unbiased-est), over ALL r estimators, computed as
+ * (double)m * (double)S / (double)r with S = sum of chi_i over this handle's closed estimators
+ * (exact uint64).  For a shard (count < r) this is the shard's contribution; shards add up.
+ * Synchronises.  0.0 before any edge. */
+int tc_estimate(tc_ctx *ctx, double *out);
+
+/* tc_destroy -- frees the handle and its device memory; NULL-safe. */
+void tc_destroy(tc_ctx *ctx);
+
+/* ------------------------------------------------------------------------------------------- */
+/* Extensions: shards, state readback, aggregation, streams, profiling.                         */
+
+/* tc_closed_sum -- S for this handle (exact uint64; shards all-reduce it).  Synchronises. */
+int tc_closed_sum(tc_ctx *ctx, uint64_t *S);
+
+/* tc_estimate_mom -- median of means over `groups` contiguous groups of the handle's estimators,
+ * group g = local ids [floor(g*count/G), floor((g+1)*count/G)), lower median; PAPER.md:373-376,
+ * 887-888 (reading R9).  1 <= groups <= count.  Synchronises. */
+int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out);
+
+/* tc_group_sums -- S_g for the same contiguous groups (exact uint64, host array of `groups`). */
+int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g);
+
+/* tc_get_state -- copy local estimators [first, first+count) to HOST arrays (SoA):
+ *  r1, r2: 2*count uint32 (lo, hi) with lo < hi, (0xFFFFFFFF, 0xFFFFFFFF) = empty;
+ *  p1, p2: count uint64 0-based global stream positions (UINT64_MAX = empty);
+ *  c: count uint32 chi;  closed: count uint8 (f3 != empty).  Any pointer may be NULL.
+ * Synchronises. */
+int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint64_t *p1,
+                 uint32_t *r2, uint64_t *p2, uint32_t *c, uint8_t *closed);
+
+/* tc_counters -- m (edges accepted so far) and the number of accepted non-empty batches. */
+int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches);
+
+/* tc_set_async -- 0 = strict (default: each push synchronises and reports its status);
+ * 1 = asynchronous (sticky error, reported at the next synchronising call). */
+int tc_set_async(tc_ctx *ctx, int async_errors);
+
+/* tc_sync -- wait for all queued work; returns the first asynchronous error, if any. */
+int tc_sync(tc_ctx *ctx);
+
+/* tc_stream -- the handle's cudaStream_t (as void*), for events recorded by the caller. */
+void *tc_stream(tc_ctx *ctx);
+
+/* Profiling: when enabled, CUDA events bracket each kernel phase of every push.
+ * tc_profile_read fills, for phase p < n (TC_PHASE_*): total milliseconds and launch count since
+ * the last reset, and returns the number of phases.  Synchronises. */
+enum {
+    TC_PHASE_STAGE = 0,   /* a1+a3: staging, validation, vertex table, edge-pair hash           */
+    TC_PHASE_SEGMENT = 1, /* a2: segment starts                                                 */
+    TC_PHASE_SCATTER = 2, /* a2: arc placement                                                  */
+    TC_PHASE_SORT = 3,    /* a2: in-segment arrival order (small + big segments)                */
+    TC_PHASE_UPDATE = 4,  /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)       */
+    TC_NPHASES = 5
+};
+int tc_profile(tc_ctx *ctx, int enable);
+int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n);
+
+/* tc_stats -- event counts since the last tc_profile() call (for the bench's byte model):
+ * out[0] estimators whose f1 was replaced, out[1] retained-f1 estimators whose f2 was replaced,
+ * out[2] sum over batches of the number of distinct vertices in W, out[3] batches.  Returns 4. */
+int tc_stats(tc_ctx *ctx, uint64_t *out, int n);
+
+/* Number of kernel launches issued by the last successful push (for the bench's gpu_launches). */
+int tc_last_launches(tc_ctx *ctx, uint32_t *launches);
+
+const char *tc_strerror(int code);
+int tc_last_error(void); /* thread-local code of the last failed tc_create* */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TC_B200_H */

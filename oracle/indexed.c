@@ -213,18 +213,15 @@ int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
     qsort(F, (size_t)nF, sizeof(arc_rec), cmp_src_posdesc);
     {   /* App. B loop: out[i] = sum; if A[i] is the reset: sum = 0 else sum += 1, where the reset
            marks the last record of each src group (reading R14). */
-        uint32_t sum = 0, maxdeg = 0;
+        uint32_t sum = 0;
         for (int64_t i = 0; i < nF; ++i) {
             F[i].rank = sum;
             int last = (i + 1 == nF) || F[i + 1].src != F[i].src;
-            if (last) { if (sum + 1 > maxdeg) maxdeg = sum + 1; sum = 0; } else sum += 1;
-        }
-        if (code == ORC_OK) {  /* overflow guard (reading R13) */
-            uint64_t maxc = 0;
-            for (uint64_t i = 0; i < o->count; ++i) if (o->c[i] > maxc) maxc = o->c[i];
-            if (maxc + 2ull * maxdeg > C_MAX) code = ORC_EOVERFLOW;
+            if (last) sum = 0; else sum += 1;
         }
     }
+    /* overflow guard (reading R13): chi <= m always, and chi must fit 31 bits */
+    if (code == ORC_OK && o->m + w > C_MAX) code = ORC_EOVERFLOW;
     if (code != ORC_OK) { free(E); free(S); free(F); free(idx); return code; }
 
     const uint64_t m_prev = o->m, seed = o->seed, first = o->first;

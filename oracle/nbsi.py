@@ -196,13 +196,8 @@ class BruteOracle:
         E_W = [normalize(u, v) for (u, v) in W]
         E_lo = np.array([e[0] for e in E_W], dtype=np.int64)
         E_hi = np.array([e[1] for e in E_W], dtype=np.int64)
-        # overflow guard (reading R13): c <= max c + 2*max deg_W can only exceed 2^31-1 this way
-        maxc = max((e.c for e in self.ests), default=0)
-        deg = {}
-        for (u, v) in E_W:
-            deg[u] = deg.get(u, 0) + 1
-            deg[v] = deg.get(v, 0) + 1
-        if maxc + 2 * max(deg.values()) > C_MAX:
+        # overflow guard (reading R13): chi <= m always, and chi must fit 31 bits
+        if self.m + len(W) > C_MAX:
             return TC_EOVERFLOW
         m_prev = self.m
         ids = np.arange(self.first, self.first + self.count, dtype=np.uint64)
@@ -245,16 +240,21 @@ def coarse_estimates(state, m):
     return [int(c) * m if cl else 0 for c, cl in zip(state["c"], state["closed"])]
 
 
-def median_of_means(X, groups):
-    """Median-of-means: contiguous groups g = [floor(g*r/G), floor((g+1)*r/G)),
-    lower median of the group means (reading R9)."""
-    r = len(X)
-    if not (1 <= groups <= r):
-        raise ValueError("groups must be in [1, r]")
+def median_of_means(state, m, groups):
+    """Median-of-means (the paper's aggregate, 887-888) of the coarse estimates
+    X_i = c_i*m (closed) else 0.  Reading R9: contiguous groups g = [floor(g*n/G), floor((g+1)*n/G)),
+    group mean = (double)m * (double)S_g / (double)|g| with S_g the exact sum of c over the group's
+    closed estimators, and the lower median of the G means."""
+    c = [int(x) for x in state["c"]]
+    cl = [int(x) for x in state["closed"]]
+    n = len(c)
+    if not (1 <= groups <= n):
+        raise ValueError("groups must be in [1, n]")
     means = []
     for g in range(groups):
-        lo, hi = g * r // groups, (g + 1) * r // groups
-        means.append(float(sum(X[lo:hi])) / float(hi - lo))
+        lo, hi = g * n // groups, (g + 1) * n // groups
+        S_g = sum(c[i] for i in range(lo, hi) if cl[i])
+        means.append(float(m) * float(S_g) / float(hi - lo))
     means.sort()
     return means[(groups - 1) // 2]
 

@@ -1,0 +1,160 @@
+"""paper_1308_2166_b200 -- B200 (sm_100a) bulk neighborhood-sampling triangle estimator.
+
+Thin Python binding of the C ABI in include/tc.h (``libtc_b200.so``).  The binding only marshals
+arguments; the whole per-batch update (Steps 1-3 of bulkUpdateAll) runs in the
+library's CUDA kernels.  PyTorch, when used, only supplies device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from ._lib import PHASES, TCError
+
+__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library"]
+
+
+def load_library():
+    return _lib.load()
+
+
+def _edges_ptr(edges):
+    """(pointer, w, keepalive) for a numpy (host) or torch (host / cuda) array of shape (w, 2) uint32."""
+    mod = type(edges).__module__
+    if mod.startswith("torch"):
+        import torch
+        t = edges
+        if t.dtype not in (torch.int32, torch.uint32):
+            raise TypeError("edges must be a uint32/int32 tensor of shape (w, 2)")
+        if t.dim() != 2 or t.shape[1] != 2 or not t.is_contiguous():
+            raise ValueError("edges must be contiguous with shape (w, 2)")
+        return C.c_void_p(t.data_ptr()), t.shape[0], t
+    a = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+    return a.ctypes.data_as(C.c_void_p), a.shape[0], a
+
+
+class TriangleCounter:
+    """r estimators (or the shard [first, first+count) of them) on one GPU.
+
+    tc_create(r, seed) / tc_create_shard(...), tc_push_batch, tc_estimate, tc_destroy (include/tc.h).
+    """
+
+    def __init__(self, r: int, seed: int, first: int = 0, count: int | None = None, device: int = -1,
+                 w_max_hint: int = 0):
+        L = _lib.load()
+        self.r, self.seed, self.first = int(r), int(seed), int(first)
+        self.count = self.r - self.first if count is None else int(count)
+        self._h = L.tc_create_shard(self.r, self.seed, self.first, self.count, int(device), int(w_max_hint))
+        if not self._h:
+            raise TCError(L.tc_last_error(), "tc_create_shard")
+
+    # -- lifecycle -------------------------------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.load().tc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- the path ------------------------------------------------------------------------------
+    def push_batch(self, edges, check: bool = True) -> int:
+        ptr, w, keep = _edges_ptr(edges)
+        rc = _lib.load().tc_push_batch(self._h, ptr, int(w))
+        del keep
+        if check and rc != 0:
+            raise TCError(rc, "tc_push_batch")
+        return rc
+
+    def push_batch_ptr(self, ptr: int, w: int) -> int:
+        """Raw pointer form (device or host address of w tc_edge); returns the status code."""
+        return _lib.load().tc_push_batch(self._h, C.c_void_p(ptr), int(w))
+
+    def estimate(self) -> float:
+        out = C.c_double()
+        self._ck(_lib.load().tc_estimate(self._h, C.byref(out)), "tc_estimate")
+        return out.value
+
+    def closed_sum(self) -> int:
+        out = C.c_uint64()
+        self._ck(_lib.load().tc_closed_sum(self._h, C.byref(out)), "tc_closed_sum")
+        return int(out.value)
+
+    def estimate_mom(self, groups: int) -> float:
+        out = C.c_double()
+        self._ck(_lib.load().tc_estimate_mom(self._h, int(groups), C.byref(out)), "tc_estimate_mom")
+        return out.value
+
+    def group_sums(self, groups: int) -> np.ndarray:
+        out = np.zeros(int(groups), np.uint64)
+        self._ck(_lib.load().tc_group_sums(self._h, int(groups), out.ctypes.data_as(C.c_void_p)), "tc_group_sums")
+        return out
+
+    def state(self, first: int = 0, count: int | None = None) -> dict:
+        n = self.count - first if count is None else count
+        r1 = np.empty((n, 2), np.uint32)
+        r2 = np.empty((n, 2), np.uint32)
+        p1 = np.empty(n, np.uint64)
+        p2 = np.empty(n, np.uint64)
+        c = np.empty(n, np.uint32)
+        closed = np.empty(n, np.uint8)
+        P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._ck(_lib.load().tc_get_state(self._h, int(first), int(n), P(r1), P(p1), P(r2), P(p2), P(c), P(closed)),
+                 "tc_get_state")
+        return dict(r1=r1, p1=p1, r2=r2, p2=p2, c=c, closed=closed)
+
+    def counters(self):
+        m, b = C.c_uint64(), C.c_uint32()
+        self._ck(_lib.load().tc_counters(self._h, C.byref(m), C.byref(b)), "tc_counters")
+        return int(m.value), int(b.value)
+
+    def set_async(self, on: bool = True):
+        self._ck(_lib.load().tc_set_async(self._h, 1 if on else 0), "tc_set_async")
+
+    def sync(self) -> int:
+        return _lib.load().tc_sync(self._h)
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(_lib.load().tc_stream(self._h) or 0)
+
+    def profile(self, on: bool = True):
+        self._ck(_lib.load().tc_profile(self._h, 1 if on else 0), "tc_profile")
+
+    def profile_read(self):
+        ms = np.zeros(_lib.TC_NPHASES, np.float64)
+        n = np.zeros(_lib.TC_NPHASES, np.uint64)
+        rc = _lib.load().tc_profile_read(self._h, ms.ctypes.data_as(C.c_void_p), n.ctypes.data_as(C.c_void_p),
+                                         _lib.TC_NPHASES)
+        if rc < 0:
+            raise TCError(rc, "tc_profile_read")
+        return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(PHASES)}
+
+    def stats(self) -> dict:
+        out = np.zeros(4, np.uint64)
+        rc = _lib.load().tc_stats(self._h, out.ctypes.data_as(C.c_void_p), 4)
+        if rc < 0:
+            raise TCError(rc, "tc_stats")
+        return {"fresh": int(out[0]), "r2_replaced_retained": int(out[1]), "vertices": int(out[2]),
+                "batches": int(out[3])}
+
+    def last_launches(self) -> int:
+        out = C.c_uint32()
+        self._ck(_lib.load().tc_last_launches(self._h, C.byref(out)), "tc_last_launches")
+        return int(out.value)
+
+    @staticmethod
+    def _ck(rc, where):
+        if rc != 0:
+            raise TCError(rc, where)

@@ -1,0 +1,79 @@
+"""ctypes declarations of include/tc.h.  Argument marshalling only: every step of the batch update
+runs inside libtc_b200.so on the GPU.  There is no CPU fallback: if the library is missing this
+module raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libtc_b200.so")
+
+TC_OK = 0
+TC_EINVAL = -1
+TC_ENOMEM = -2
+TC_ESELFLOOP = -3
+TC_EDUP = -4
+TC_EOVERFLOW = -5
+TC_ECUDA = -6
+TC_ESTATE = -8
+TC_NPHASES = 5
+PHASES = ("stage", "segment", "scatter", "sort", "update")
+
+EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_destroy", "tc_closed_sum",
+           "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_sync",
+           "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_strerror", "tc_last_error"]
+
+_lib = None
+
+
+class TCError(RuntimeError):
+    def __init__(self, code, where=""):
+        self.code = code
+        super().__init__(f"{where}: {strerror(code)} ({code})" if where else f"{strerror(code)} ({code})")
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library (raises OSError / ImportError when it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the product path has no CPU fallback)")
+    L = C.CDLL(path)
+    u64, u32, vp, i32 = C.c_uint64, C.c_uint32, C.c_void_p, C.c_int
+    sig = {
+        "tc_create": (vp, [u64, u64]),
+        "tc_create_shard": (vp, [u64, u64, u64, u64, i32, u64]),
+        "tc_push_batch": (i32, [vp, vp, u64]),
+        "tc_estimate": (i32, [vp, C.POINTER(C.c_double)]),
+        "tc_destroy": (None, [vp]),
+        "tc_closed_sum": (i32, [vp, C.POINTER(u64)]),
+        "tc_estimate_mom": (i32, [vp, u32, C.POINTER(C.c_double)]),
+        "tc_group_sums": (i32, [vp, u32, vp]),
+        "tc_get_state": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, vp]),
+        "tc_counters": (i32, [vp, C.POINTER(u64), C.POINTER(u32)]),
+        "tc_set_async": (i32, [vp, i32]),
+        "tc_sync": (i32, [vp]),
+        "tc_stream": (vp, [vp]),
+        "tc_profile": (i32, [vp, i32]),
+        "tc_profile_read": (i32, [vp, vp, vp, i32]),
+        "tc_stats": (i32, [vp, vp, i32]),
+        "tc_last_launches": (i32, [vp, C.POINTER(u32)]),
+        "tc_strerror": (C.c_char_p, [i32]),
+        "tc_last_error": (i32, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def strerror(code: int) -> str:
+    try:
+        return load().tc_strerror(code).decode()
+    except Exception:  # library missing: still produce a message
+        return f"error {code}"

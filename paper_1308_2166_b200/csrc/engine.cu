@@ -1,0 +1,467 @@
+// engine.cu -- host side of the C ABI declared in include/tc.h: handle, device memory, the per-batch
+// launch sequence, error handling and readback.  No PyTorch types; plain pointers and sizes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "../../include/tc.h"
+#include "kernels.h"
+
+using namespace tcb;
+
+namespace {
+thread_local int g_last_error = TC_OK;
+
+uint64_t next_pow2(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+}  // namespace
+
+struct tc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t r = 0, seed = 0, first = 0, count = 0;
+    uint64_t m = 0;
+    uint32_t b = 0;
+    uint32_t epoch = 0;
+    int async_errors = 0;
+    int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
+    int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
+    uint32_t last_launches = 0;
+    StateBufs st;
+    IndexBufs ix;
+    uint32_t *h_err = nullptr;  // pinned
+    cudaEvent_t copy_done = nullptr;
+    // profiling
+    int prof = 0;
+    cudaEvent_t ev[TC_NPHASES + 1] = {};
+    double prof_ms[TC_NPHASES] = {};
+    uint64_t prof_launch[TC_NPHASES] = {};
+    int prof_pending = 0;
+};
+
+static int fail_cuda(tc_ctx *c) {
+    cudaGetLastError();
+    if (c) c->poisoned = TC_ECUDA;
+    return TC_ECUDA;
+}
+
+#define CK(call)                                   \
+    do {                                           \
+        if ((call) != cudaSuccess) return fail_cuda(ctx); \
+    } while (0)
+
+static void free_index(IndexBufs &ix) {
+    cudaFree(ix.E);
+    cudaFree(ix.arcrec);
+    cudaFree(ix.segU);
+    cudaFree(ix.segS);
+    cudaFree(ix.einfo);
+    cudaFree(ix.vt);
+    cudaFree(ix.pt);
+    cudaFree(ix.vlist);
+    cudaFree(ix.chunks);
+    cudaFree(ix.ctr);
+    cudaFree(ix.stage);
+    ix = IndexBufs();
+}
+
+// (Re)allocate the per-batch index for batches of up to w edges.
+static int grow_index(tc_ctx *ctx, uint64_t w) {
+    if (w <= ctx->ix.wcap) return TC_OK;
+    CK(cudaStreamSynchronize(ctx->stream));
+    free_index(ctx->ix);
+    IndexBufs &ix = ctx->ix;
+    const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
+    const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w arcs' vertices: load <= 50%
+    const uint64_t pslots = next_pow2(2 * cap);  // w pairs: load <= 50%
+    ix.chunk_cap = 2 * cap / (kSmallSeg + 1) + 2 * cap / kChunk + 64;
+    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.arcrec, 16 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.segU, 8 * cap) == cudaSuccess && cudaMalloc(&ix.segS, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.vlist, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.chunks, 16 * ix.chunk_cap) == cudaSuccess &&
+              cudaMalloc(&ix.ctr, 64) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        free_index(ix);
+        return TC_ENOMEM;
+    }
+    ix.vmask = (uint32_t)(vslots - 1);
+    ix.pmask = (uint32_t)(pslots - 1);
+    ix.wcap = cap;
+    // epoch 0 marks every slot empty; live epochs start at 1
+    CK(cudaMemsetAsync(ix.vt, 0, 16 * vslots, ctx->stream));
+    CK(cudaMemsetAsync(ix.pt, 0, 16 * pslots, ctx->stream));
+    CK(cudaMemsetAsync(ix.ctr, 0, 64, ctx->stream));
+    ctx->epoch = 0;
+    return TC_OK;
+}
+
+static void destroy_ctx(tc_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    free_index(ctx->ix);
+    cudaFree(ctx->st.r1);
+    cudaFree(ctx->st.r2);
+    cudaFree(ctx->st.cf);
+    cudaFree(ctx->st.p1);
+    cudaFree(ctx->st.p2);
+    cudaFree(ctx->st.S);
+    cudaFree(ctx->st.stats);
+    if (ctx->h_err) cudaFreeHost(ctx->h_err);
+    if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    for (auto &e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+extern "C" {
+
+tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t count, int device, uint64_t w_max_hint) {
+    g_last_error = TC_OK;
+    if (r == 0 || first > r || count > r - first || w_max_hint > 0x7FFFFFFFull) {
+        g_last_error = TC_EINVAL;
+        return nullptr;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        g_last_error = TC_ECUDA;
+        return nullptr;
+    }
+    if (device < 0) cudaGetDevice(&device);
+    if (device >= ndev || cudaSetDevice(device) != cudaSuccess) {
+        cudaGetLastError();
+        g_last_error = TC_EINVAL;
+        return nullptr;
+    }
+    tc_ctx *ctx = new (std::nothrow) tc_ctx();
+    if (!ctx) {
+        g_last_error = TC_ENOMEM;
+        return nullptr;
+    }
+    ctx->device = device;
+    ctx->r = r;
+    ctx->seed = seed;
+    ctx->first = first;
+    ctx->count = count;
+    ctx->st.count = count;
+    const uint64_t n = std::max<uint64_t>(count, 1);
+    bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaMalloc(&ctx->st.r1, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.r2, 8 * n) == cudaSuccess &&
+              cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 8 * n) == cudaSuccess &&
+              cudaMalloc(&ctx->st.p2, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
+              cudaMalloc(&ctx->st.stats, 32) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess;
+    if (ok) {
+        for (auto &e : ctx->ev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
+    }
+    if (ok) {
+        ok = cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream) == cudaSuccess &&
+             cudaMemsetAsync(ctx->st.stats, 0, 32, ctx->stream) == cudaSuccess;
+        launch_init_state(ctx->st, ctx->stream);
+        ok = ok && cudaGetLastError() == cudaSuccess;
+    }
+    if (ok && w_max_hint) ok = grow_index(ctx, w_max_hint) == TC_OK;
+    if (ok) ok = cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        destroy_ctx(ctx);
+        g_last_error = TC_ENOMEM;
+        return nullptr;
+    }
+    return ctx;
+}
+
+tc_ctx *tc_create(uint64_t r, uint64_t seed) { return tc_create_shard(r, seed, 0, r, -1, 0); }
+
+void tc_destroy(tc_ctx *ctx) { destroy_ctx(ctx); }
+
+static int decode_err(uint32_t e) {
+    if (e & kErrInval) return TC_EINVAL;
+    if (e & kErrLoop) return TC_ESELFLOOP;
+    if (e & kErrDup) return TC_EDUP;
+    if (e & kErrOvf) return TC_EOVERFLOW;
+    return TC_OK;
+}
+
+// Wait for queued work and surface a pending asynchronous batch error (poisons the handle).
+static int settle(tc_ctx *ctx) {
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (ctx->async_errors && !ctx->poisoned && ctx->ix.ctr) {
+        CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr + 3, 4, cudaMemcpyDeviceToHost));
+        const int code = decode_err(*ctx->h_err);
+        if (code != TC_OK) {
+            ctx->poisoned = code;
+            return code;
+        }
+    }
+    if (ctx->prof_pending) {
+        for (int p = 0; p < TC_NPHASES; ++p) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->ev[p], ctx->ev[p + 1]) == cudaSuccess) ctx->prof_ms[p] += ms;
+        }
+        cudaGetLastError();
+        ctx->prof_pending = 0;
+    }
+    return ctx->poisoned ? (ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE) : TC_OK;
+}
+
+int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
+    if (!ctx) return TC_EINVAL;
+    if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
+    if (w == 0) return TC_OK;
+    if (!edges || w > 0x7FFFFFFFull) return TC_EINVAL;
+    CK(cudaSetDevice(ctx->device));
+    const bool ovf = ctx->m + w > 0x7FFFFFFFull;  // chi <= m must fit 31 bits (reading R13)
+    if (ovf && ctx->async_errors) return TC_EOVERFLOW;  // async mode: reported first, state untouched
+    if (ctx->prof_pending) {
+        int rc = settle(ctx);
+        if (rc != TC_OK) return rc;
+    }
+    int rc = grow_index(ctx, w);
+    if (rc != TC_OK) return rc;
+    // where are the edges?
+    const uint2 *in = nullptr;
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, edges) != cudaSuccess) {
+        cudaGetLastError();
+        attr.type = cudaMemoryTypeUnregistered;
+    }
+    const bool on_device = (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
+                           attr.device == ctx->device;
+    if (attr.type == cudaMemoryTypeDevice && attr.device != ctx->device) return TC_EINVAL;
+    IndexBufs &ix = ctx->ix;
+    if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    if (on_device) {
+        in = reinterpret_cast<const uint2 *>(edges);
+    } else {
+        CK(cudaMemcpyAsync(ix.stage, edges, 8 * w, cudaMemcpyHostToDevice, ctx->stream));
+        if (attr.type == cudaMemoryTypeHost) {  // pinned: wait so the caller may reuse the buffer
+            CK(cudaEventRecord(ctx->copy_done, ctx->stream));
+            CK(cudaEventSynchronize(ctx->copy_done));
+        }
+        in = ix.stage;
+    }
+    if (++ctx->epoch == 0xFFFFFFFFu) {  // never reuse a live epoch: clear the tables
+        CK(cudaMemsetAsync(ix.vt, 0, 16ull * (ix.vmask + 1ull), ctx->stream));
+        CK(cudaMemsetAsync(ix.pt, 0, 16ull * (ix.pmask + 1ull), ctx->stream));
+        ctx->epoch = 1;
+    }
+    const int slot = (int)((ctx->b + 1) & 1u);
+    if (ctx->async_errors) {
+        CK(cudaMemsetAsync(ix.ctr, 0, 12, ctx->stream));  // keep the sticky error word
+    } else {
+        const uint32_t init[4] = {0, 0, 0, ovf ? kErrOvf : 0u};
+        CK(cudaMemcpyAsync(ix.ctr, init, 16, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
+    BatchArgs a;
+    a.in = in;
+    a.w = (uint32_t)w;
+    a.epoch = ctx->epoch;
+    a.m_prev = ctx->m;
+    a.batch = ctx->b;
+    a.first = ctx->first;
+    a.seed = ctx->seed;
+    a.S_slot = slot;
+    uint32_t launches = 0;
+    int n;
+    n = launch_stage(ix, a, ctx->stream);
+    launches += n;
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[1], ctx->stream)); ctx->prof_launch[0] += n; }
+    n = launch_segment(ix, a, ctx->stream);
+    launches += n;
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[2], ctx->stream)); ctx->prof_launch[1] += n; }
+    n = launch_scatter(ix, a, ctx->stream);
+    launches += n;
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[3], ctx->stream)); ctx->prof_launch[2] += n; }
+    n = launch_sort(ix, a, ctx->stream);
+    launches += n;
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[4], ctx->stream)); ctx->prof_launch[3] += n; }
+    n = launch_update(ix, ctx->st, a, ctx->stream);
+    launches += n;
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[5], ctx->stream)); ctx->prof_launch[4] += n; ctx->prof_pending = 1; }
+    CK(cudaGetLastError());
+    if (!ctx->async_errors) {
+        CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + 3, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const int code = decode_err(*ctx->h_err);
+        if (code != TC_OK) return code;  // nothing was mutated: k_update bailed out
+    }
+    ctx->m += w;
+    ctx->b += 1;
+    ctx->S_slot = slot;
+    ctx->last_launches = launches;
+    return TC_OK;
+}
+
+int tc_sync(tc_ctx *ctx) {
+    if (!ctx) return TC_EINVAL;
+    return settle(ctx);
+}
+
+int tc_closed_sum(tc_ctx *ctx, uint64_t *S) {
+    if (!ctx || !S) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    *S = 0;
+    if (ctx->S_slot >= 0) {
+        unsigned long long v = 0;
+        CK(cudaMemcpy(&v, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToHost));
+        *S = v;
+    }
+    return TC_OK;
+}
+
+int tc_estimate(tc_ctx *ctx, double *out) {
+    if (!out) return TC_EINVAL;
+    uint64_t S = 0;
+    int rc = tc_closed_sum(ctx, &S);
+    if (rc != TC_OK) return rc;
+    *out = (double)ctx->m * (double)S / (double)ctx->r;  // reading R9: one fixed fp64 expression
+    return TC_OK;
+}
+
+int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g) {
+    if (!ctx || !S_g || groups == 0 || groups > ctx->count) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    unsigned long long *d = nullptr;
+    CK(cudaMalloc(&d, 8ull * groups));
+    if (cudaMemsetAsync(d, 0, 8ull * groups, ctx->stream) != cudaSuccess) {
+        cudaFree(d);
+        return fail_cuda(ctx);
+    }
+    launch_group_sums(ctx->st, groups, d, ctx->stream);
+    const bool ok = cudaGetLastError() == cudaSuccess &&
+                    cudaMemcpyAsync(S_g, d, 8ull * groups, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess &&
+                    cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+    cudaFree(d);
+    return ok ? TC_OK : fail_cuda(ctx);
+}
+
+int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out) {
+    if (!ctx || !out || groups == 0 || groups > ctx->count) return TC_EINVAL;
+    std::vector<uint64_t> S(groups);
+    int rc = tc_group_sums(ctx, groups, S.data());
+    if (rc != TC_OK) return rc;
+    std::vector<double> means(groups);
+    const uint64_t n = ctx->count;
+    for (uint32_t g = 0; g < groups; ++g) {
+        const uint64_t lo = (uint64_t)g * n / groups, hi = (uint64_t)(g + 1) * n / groups;
+        // group mean of X_i = chi_i * m: m * S_g / |g|, same expression order as the oracle
+        means[g] = (double)(ctx->m * S[g]) / (double)(hi - lo);
+    }
+    std::sort(means.begin(), means.end());
+    *out = means[(groups - 1) / 2];
+    return TC_OK;
+}
+
+int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint64_t *p1, uint32_t *r2,
+                 uint64_t *p2, uint32_t *c, uint8_t *closed) {
+    if (!ctx || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK && rc != TC_ESTATE) return rc;
+    if (count == 0) return TC_OK;
+    if (r1) CK(cudaMemcpy(r1, ctx->st.r1 + first, 8 * count, cudaMemcpyDeviceToHost));
+    if (r2) CK(cudaMemcpy(r2, ctx->st.r2 + first, 8 * count, cudaMemcpyDeviceToHost));
+    if (p1) CK(cudaMemcpy(p1, ctx->st.p1 + first, 8 * count, cudaMemcpyDeviceToHost));
+    if (p2) CK(cudaMemcpy(p2, ctx->st.p2 + first, 8 * count, cudaMemcpyDeviceToHost));
+    if (c || closed) {
+        std::vector<uint32_t> cf(count);
+        CK(cudaMemcpy(cf.data(), ctx->st.cf + first, 4 * count, cudaMemcpyDeviceToHost));
+        for (uint64_t i = 0; i < count; ++i) {
+            if (c) c[i] = cf[i] & kCMask;
+            if (closed) closed[i] = (cf[i] & kClosedBit) ? 1 : 0;
+        }
+    }
+    return TC_OK;
+}
+
+int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches) {
+    if (!ctx) return TC_EINVAL;
+    if (m) *m = ctx->m;
+    if (batches) *batches = ctx->b;
+    return TC_OK;
+}
+
+int tc_set_async(tc_ctx *ctx, int async_errors) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    ctx->async_errors = async_errors ? 1 : 0;
+    return TC_OK;
+}
+
+void *tc_stream(tc_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+
+int tc_profile(tc_ctx *ctx, int enable) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    ctx->prof = enable ? 1 : 0;
+    CK(cudaMemsetAsync(ctx->st.stats, 0, 32, ctx->stream));
+    for (int p = 0; p < TC_NPHASES; ++p) {
+        ctx->prof_ms[p] = 0;
+        ctx->prof_launch[p] = 0;
+    }
+    return TC_OK;
+}
+
+int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    for (int p = 0; p < n && p < TC_NPHASES; ++p) {
+        if (ms) ms[p] = ctx->prof_ms[p];
+        if (launches) launches[p] = ctx->prof_launch[p];
+    }
+    return TC_NPHASES;
+}
+
+int tc_stats(tc_ctx *ctx, uint64_t *out, int n) {
+    if (!ctx || !out) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    unsigned long long v[4];
+    CK(cudaMemcpy(v, ctx->st.stats, 32, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
+    return 4;
+}
+
+int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {
+    if (!ctx || !launches) return TC_EINVAL;
+    *launches = ctx->last_launches;
+    return TC_OK;
+}
+
+const char *tc_strerror(int code) {
+    switch (code) {
+        case TC_OK: return "ok";
+        case TC_EINVAL: return "invalid argument or reserved vertex id 0xFFFFFFFF";
+        case TC_ENOMEM: return "out of memory";
+        case TC_ESELFLOOP: return "self-loop in batch";
+        case TC_EDUP: return "duplicate edge in batch";
+        case TC_EOVERFLOW: return "stream longer than 2^31-1 edges (chi field overflow)";
+        case TC_ECUDA: return "CUDA error";
+        case TC_ESTATE: return "handle poisoned by an earlier asynchronous error";
+        default: return "unknown error";
+    }
+}
+
+int tc_last_error(void) { return g_last_error; }
+
+}  // extern "C"

@@ -174,11 +174,14 @@ def test_error_paths_all_or_nothing(kind):
 
 
 def test_mom_and_sizing():
-    X = [5, 1, 9, 3, 7, 2]
-    assert nbsi.median_of_means(X, 1) == sum(X) / 6
-    assert nbsi.median_of_means(X, 6) == 3  # lower median of the values
-    assert nbsi.median_of_means(X, 3) == 4.5  # group means 3, 6, 4.5 -> median 4.5
-    assert nbsi.median_of_means(X, 2) == 4.0  # group means 5, 4 -> lower median 4
+    # closed estimators with c = (5, 1, 9, 3, 7, 2), m = 1 -> X = c
+    st = dict(c=np.array([5, 1, 9, 3, 7, 2]), closed=np.ones(6, np.uint8))
+    assert nbsi.median_of_means(st, 1, 1) == 27 / 6
+    assert nbsi.median_of_means(st, 1, 6) == 3  # lower median of the values
+    assert nbsi.median_of_means(st, 1, 3) == 4.5  # group means 3, 6, 4.5 -> median 4.5
+    assert nbsi.median_of_means(st, 1, 2) == 4.0  # group means 5, 4 -> lower median 4
+    st2 = dict(c=np.array([5, 1, 9, 3]), closed=np.array([1, 0, 0, 1], np.uint8))
+    assert nbsi.median_of_means(st2, 10, 2) == 15.0  # group means 50/2, 30/2 -> lower median 15
     # Theorem mdelta-suffices: 96/eps^2 * m*Delta/tau * ln(1/delta)
     import math
     assert nbsi.required_estimators(0.5, math.exp(-1), 10, 4, 20) == math.ceil(96 / 0.25 * 2.0)
