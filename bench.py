@@ -129,6 +129,7 @@ def algorithmic_bytes(phase, w, R, D, fresh, r2old):
              index probes are L2 traffic at C2 and not counted.
     stage  : read 8 B/edge; write E 8 + arc record 16 + pair slot 16 B/edge; 16 B per vertex slot.
     segment: 24 B per distinct vertex.   scatter: 16 + 8 B/edge.   sort: 8 + 8 + 16 B/edge.
+    clear  : 16 B per distinct vertex (list + key + info) and 12 B/edge (list + pair key).
     """
     if phase == "update":
         return 24 * (R - fresh) + 36 * fresh + 16 * r2old
@@ -140,6 +141,8 @@ def algorithmic_bytes(phase, w, R, D, fresh, r2old):
         return 24 * w
     if phase == "sort":
         return 32 * w
+    if phase == "clear":
+        return 16 * D + 12 * w
     raise KeyError(phase)
 
 
@@ -267,8 +270,8 @@ def run_b200(args):
         "segment": algorithmic_bytes("segment", 0, 0, D, 0, 0),
         "scatter": algorithmic_bytes("scatter", edges_done, 0, 0, 0, 0),
         "sort": algorithmic_bytes("sort", edges_done, 0, 0, 0, 0),
+        "clear": algorithmic_bytes("clear", edges_done, 0, D, 0, 0),
     }
-    kernels_in = {"stage": 1, "segment": 1, "scatter": 1, "sort": 3, "update": 1}
     dom_secs = prof[dom][0] / 1e3
     achieved = total_alg[dom] / dom_secs / 1e9 if dom_secs > 0 else None
     upd_secs = prof["update"][0] / 1e3

@@ -128,7 +128,8 @@ enum {
     TC_PHASE_SCATTER = 2, /* a2: arc placement                                                  */
     TC_PHASE_SORT = 3,    /* a2: in-segment arrival order (small + big segments)                */
     TC_PHASE_UPDATE = 4,  /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)       */
-    TC_NPHASES = 5
+    TC_PHASE_CLEAR = 5,   /* freeing the table slots the batch used                             */
+    TC_NPHASES = 6
 };
 int tc_profile(tc_ctx *ctx, int enable);
 int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n);

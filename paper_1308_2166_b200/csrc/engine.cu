@@ -30,7 +30,6 @@ struct tc_ctx {
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
-    uint32_t epoch = 0;
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -61,12 +60,16 @@ static int fail_cuda(tc_ctx *c) {
 static void free_index(IndexBufs &ix) {
     cudaFree(ix.E);
     cudaFree(ix.arcrec);
+    cudaFree(ix.pslot);
     cudaFree(ix.segU);
     cudaFree(ix.segS);
     cudaFree(ix.einfo);
-    cudaFree(ix.vt);
-    cudaFree(ix.pt);
+    cudaFree(ix.vkey);
+    cudaFree(ix.vinfo);
+    cudaFree(ix.pkey);
+    cudaFree(ix.ppos);
     cudaFree(ix.vlist);
+    cudaFree(ix.midlist);
     cudaFree(ix.chunks);
     cudaFree(ix.ctr);
     cudaFree(ix.stage);
@@ -80,13 +83,17 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     free_index(ctx->ix);
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
-    const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w arcs' vertices: load <= 50%
-    const uint64_t pslots = next_pow2(2 * cap);  // w pairs: load <= 50%
-    ix.chunk_cap = 2 * cap / (kSmallSeg + 1) + 2 * cap / kChunk + 64;
+    const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
+    const uint64_t pslots = next_pow2(4 * cap);  // w pairs: load <= 25%
+    ix.chunk_cap = 2 * cap / (kMidSeg + 1) + 2 * cap / kChunk + 64;
+    const uint64_t mid_cap = 2 * cap / (kTinySeg + 1) + 64;
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.arcrec, 16 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.pslot, 4 * cap) == cudaSuccess &&
               cudaMalloc(&ix.segU, 8 * cap) == cudaSuccess && cudaMalloc(&ix.segS, 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
-              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.vlist, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vkey, 4 * vslots) == cudaSuccess &&
+              cudaMalloc(&ix.vinfo, 8 * vslots) == cudaSuccess && cudaMalloc(&ix.pkey, 8 * pslots) == cudaSuccess &&
+              cudaMalloc(&ix.ppos, 4 * pslots) == cudaSuccess && cudaMalloc(&ix.vlist, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.midlist, 4 * mid_cap) == cudaSuccess &&
               cudaMalloc(&ix.chunks, 16 * ix.chunk_cap) == cudaSuccess &&
               cudaMalloc(&ix.ctr, 64) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
@@ -97,11 +104,9 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     ix.vmask = (uint32_t)(vslots - 1);
     ix.pmask = (uint32_t)(pslots - 1);
     ix.wcap = cap;
-    // epoch 0 marks every slot empty; live epochs start at 1
-    CK(cudaMemsetAsync(ix.vt, 0, 16 * vslots, ctx->stream));
-    CK(cudaMemsetAsync(ix.pt, 0, 16 * pslots, ctx->stream));
+    launch_init_tables(ix, ctx->stream);  // all slots free; afterwards each batch frees its own slots
+    CK(cudaGetLastError());
     CK(cudaMemsetAsync(ix.ctr, 0, 64, ctx->stream));
-    ctx->epoch = 0;
     return TC_OK;
 }
 
@@ -255,23 +260,18 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         }
         in = ix.stage;
     }
-    if (++ctx->epoch == 0xFFFFFFFFu) {  // never reuse a live epoch: clear the tables
-        CK(cudaMemsetAsync(ix.vt, 0, 16ull * (ix.vmask + 1ull), ctx->stream));
-        CK(cudaMemsetAsync(ix.pt, 0, 16ull * (ix.pmask + 1ull), ctx->stream));
-        ctx->epoch = 1;
-    }
     const int slot = (int)((ctx->b + 1) & 1u);
     if (ctx->async_errors) {
-        CK(cudaMemsetAsync(ix.ctr, 0, 12, ctx->stream));  // keep the sticky error word
+        CK(cudaMemsetAsync(ix.ctr, 0, 12, ctx->stream));  // keep the sticky error word ctr[3]
+        CK(cudaMemsetAsync(ix.ctr + 4, 0, 4, ctx->stream));
     } else {
-        const uint32_t init[4] = {0, 0, 0, ovf ? kErrOvf : 0u};
-        CK(cudaMemcpyAsync(ix.ctr, init, 16, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(ix.ctr, 0, 32, ctx->stream));
+        if (ovf) CK(cudaMemsetAsync(ix.ctr + 3, (int)kErrOvf, 1, ctx->stream));
     }
     CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
     BatchArgs a;
     a.in = in;
     a.w = (uint32_t)w;
-    a.epoch = ctx->epoch;
     a.m_prev = ctx->m;
     a.batch = ctx->b;
     a.first = ctx->first;
@@ -293,7 +293,10 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     if (ctx->prof) { CK(cudaEventRecord(ctx->ev[4], ctx->stream)); ctx->prof_launch[3] += n; }
     n = launch_update(ix, ctx->st, a, ctx->stream);
     launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[5], ctx->stream)); ctx->prof_launch[4] += n; ctx->prof_pending = 1; }
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[5], ctx->stream)); ctx->prof_launch[4] += n; }
+    n = launch_clear(ix, a, ctx->stream);
+    launches += n;
+    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[6], ctx->stream)); ctx->prof_launch[5] += n; ctx->prof_pending = 1; }
     CK(cudaGetLastError());
     if (!ctx->async_errors) {
         CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + 3, 4, cudaMemcpyDeviceToHost, ctx->stream));
