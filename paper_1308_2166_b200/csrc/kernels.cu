@@ -108,7 +108,6 @@ struct StageCtx {
     unsigned long long *pkey;
     uint32_t *ppos;
     uint32_t pmask;
-    uint32_t *vlist;
     uint32_t *ctr;
 };
 
@@ -132,8 +131,6 @@ __device__ __forceinline__ uint32_t stage_one(const StageCtx &c, uint2 e, uint32
     // arrival tickets: deg_W counters (two independent atomics)
     const uint32_t ta = atomicAdd(&c.vinfo[a.slot].x, 1u);
     const uint32_t tb = atomicAdd(&c.vinfo[b.slot].x, 1u);
-    if (a.claimed) c.vlist[atomicAdd(&c.ctr[0], 1u)] = a.slot;
-    if (b.claimed) c.vlist[atomicAdd(&c.ctr[0], 1u)] = b.slot;
     c.arcrec[k] = make_uint4(a.slot, ta, b.slot, tb);
     c.pslot[k] = q.slot;
     if (!q.dup) c.ppos[q.slot] = k;
@@ -163,53 +160,87 @@ __global__ void __launch_bounds__(256) k_stage(const uint2 *__restrict__ in, uin
 // ------------------------------------------------------------------------------------------------
 // a2: segments
 
-// Segment start of every vertex of W (the order of segments is irrelevant, only their contents);
-// bins segments by length for the ordering kernels.
-__global__ void __launch_bounds__(256) k_segment(uint2 *vinfo, const uint32_t *__restrict__ vlist,
-                                                 uint32_t *__restrict__ midlist, uint4 *__restrict__ chunks,
-                                                 uint32_t *ctr) {
-    if (ctr[3]) return;
-    const uint32_t D = ctr[0];
-    __shared__ uint32_t wsum[8];
-    __shared__ uint32_t base_sh;
+// Block-wide exclusive scan of a 64-bit value (256 threads); returns the exclusive prefix and sets total.
+__device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long v, unsigned long long &total,
+                                                             unsigned long long *wsum /* [9] */) {
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    for (uint32_t b0 = blockIdx.x * 256u; b0 < D; b0 += gridDim.x * 256u) {
-        const uint32_t d = b0 + threadIdx.x;
-        uint32_t slot = 0, deg = 0;
-        if (d < D) {
-            slot = vlist[d];
-            deg = vinfo[slot].x;
-        }
-        uint32_t incl = deg;
+    unsigned long long incl = v;
 #pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-            if (lane >= (uint32_t)off) incl += y;
-        }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        if (threadIdx.x < 8) {
-            const uint32_t v = wsum[threadIdx.x];
-            uint32_t x = v;
+    for (int off = 1; off < 32; off <<= 1) {
+        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= (uint32_t)off) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (threadIdx.x < 8) {
+        const unsigned long long wv = wsum[threadIdx.x];
+        unsigned long long x = wv;
 #pragma unroll
-            for (int off = 1; off < 8; off <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffu, x, off);
-                if (threadIdx.x >= (uint32_t)off) x += y;
-            }
-            wsum[threadIdx.x] = x - v;
-            if (threadIdx.x == 7) base_sh = atomicAdd(&ctr[1], x);
+        for (int off = 1; off < 8; off <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffu, x, off);
+            if (threadIdx.x >= (uint32_t)off) x += y;
+        }
+        wsum[threadIdx.x] = x - wv;
+        if (threadIdx.x == 7) wsum[8] = x;
+    }
+    __syncthreads();
+    total = wsum[8];
+    const unsigned long long ex = wsum[warp] + incl - v;
+    __syncthreads();
+    return ex;
+}
+
+// Segment start of every vertex of W (the order of segments is irrelevant, only their contents).
+// Walks the vertex table in tiles of 256 x 8 slots: the compact vertex list, the segment starts and
+// the length bins (mid list, big-segment chunks) are appended with ONE atomic per tile and counter.
+__global__ void __launch_bounds__(256) k_segment(const uint32_t *__restrict__ vkey, uint2 *vinfo, uint32_t nslots,
+                                                 uint32_t *__restrict__ vlist, uint32_t *__restrict__ midlist,
+                                                 uint4 *__restrict__ chunks, uint32_t *ctr) {
+    if (ctr[3]) return;
+    __shared__ unsigned long long wsum[9];
+    __shared__ uint32_t base[4];
+    const uint32_t tile_slots = 256u * kVBucket;
+    for (uint32_t t0 = blockIdx.x * tile_slots; t0 < nslots; t0 += gridDim.x * tile_slots) {
+        const uint32_t s0 = t0 + threadIdx.x * kVBucket;
+        const uint4 *p = reinterpret_cast<const uint4 *>(vkey + s0);
+        const uint4 k0 = p[0], k1 = p[1];
+        const uint32_t keys[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+        uint32_t deg[8];
+        uint32_t nocc = 0, nmid = 0, degsum = 0, nch = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            deg[i] = keys[i] != kEmptyV ? vinfo[s0 + i].x : 0u;
+            nocc += keys[i] != kEmptyV;
+            degsum += deg[i];
+            nmid += (deg[i] > kTinySeg && deg[i] <= kMidSeg);
+            nch += deg[i] > kMidSeg ? (deg[i] + kChunk - 1) / kChunk : 0u;
+        }
+        unsigned long long tot_a, tot_b;
+        const unsigned long long ex_a =
+            block_scan_u64(((unsigned long long)degsum << 32) | nocc, tot_a, wsum);  // degsum fits: <= 2w
+        const unsigned long long ex_b = block_scan_u64(((unsigned long long)nch << 32) | nmid, tot_b, wsum);
+        if (threadIdx.x == 0) {
+            base[0] = (uint32_t)tot_a ? atomicAdd(&ctr[0], (uint32_t)tot_a) : 0u;
+            base[1] = (uint32_t)(tot_a >> 32) ? atomicAdd(&ctr[1], (uint32_t)(tot_a >> 32)) : 0u;
+            base[2] = (uint32_t)tot_b ? atomicAdd(&ctr[4], (uint32_t)tot_b) : 0u;
+            base[3] = (uint32_t)(tot_b >> 32) ? atomicAdd(&ctr[2], (uint32_t)(tot_b >> 32)) : 0u;
         }
         __syncthreads();
-        if (d < D) {
-            const uint32_t start = base_sh + wsum[warp] + incl - deg;
-            vinfo[slot].y = start;
-            if (deg > kMidSeg) {
-                const uint32_t nch = (deg + kChunk - 1) / kChunk;
-                const uint32_t c0 = atomicAdd(&ctr[2], nch);
-                for (uint32_t c = 0; c < nch; ++c) chunks[c0 + c] = make_uint4(start, deg, c, 0u);
-            } else if (deg > kTinySeg) {
-                midlist[atomicAdd(&ctr[4], 1u)] = slot;
+        uint32_t li = base[0] + (uint32_t)ex_a, st = base[1] + (uint32_t)(ex_a >> 32);
+        uint32_t mi = base[2] + (uint32_t)ex_b, ci = base[3] + (uint32_t)(ex_b >> 32);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            if (keys[i] == kEmptyV) continue;
+            const uint32_t s = s0 + i;
+            vinfo[s].y = st;
+            vlist[li++] = s;
+            if (deg[i] > kMidSeg) {
+                const uint32_t n = (deg[i] + kChunk - 1) / kChunk;
+                for (uint32_t c = 0; c < n; ++c) chunks[ci++] = make_uint4(st, deg[i], c, 0u);
+            } else if (deg[i] > kTinySeg) {
+                midlist[mi++] = s;
             }
+            st += deg[i];
         }
         __syncthreads();
     }
@@ -628,13 +659,15 @@ static inline uint32_t grid_for(uint64_t items, uint32_t threads, uint32_t per_s
 }
 
 int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    StageCtx c{ix.E, ix.arcrec, ix.pslot, ix.vkey, ix.vinfo, ix.vmask, ix.pkey, ix.ppos, ix.pmask, ix.vlist, ix.ctr};
+    StageCtx c{ix.E, ix.arcrec, ix.pslot, ix.vkey, ix.vinfo, ix.vmask, ix.pkey, ix.ppos, ix.pmask, ix.ctr};
     k_stage<<<grid_for((a.w + 1) / 2, 256, 8), 256, 0, s>>>(a.in, a.w, c);
     return 1;
 }
 
 int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    k_segment<<<grid_for(2ull * a.w, 256, 8), 256, 0, s>>>(ix.vinfo, ix.vlist, ix.midlist, ix.chunks, ix.ctr);
+    const uint64_t nslots = (uint64_t)ix.vmask + 1;
+    k_segment<<<grid_for(nslots / kVBucket, 256, 4), 256, 0, s>>>(ix.vkey, ix.vinfo, (uint32_t)nslots, ix.vlist,
+                                                                  ix.midlist, ix.chunks, ix.ctr);
     return 1;
 }
 
