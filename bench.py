@@ -127,22 +127,21 @@ def algorithmic_bytes(phase, w, R, D, fresh, r2old):
     update : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
              (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
              index probes are L2 traffic at C2 and not counted.
-    stage  : read 8 B/edge; write E 8 + arc record 16 + pair slot 16 B/edge; 16 B per vertex slot.
-    segment: 24 B per distinct vertex.   scatter: 16 + 8 B/edge.   sort: 8 + 8 + 16 B/edge.
-    clear  : 16 B per distinct vertex (list + key + info) and 12 B/edge (list + pair key).
+    stage  : read 8 B/edge; write E 8 + arcs 16 + pair slot 16 + pair-slot list 4 B/edge.
+    sort   : the 2 arcs of an edge read and written once (32 B/edge); extra radix passes are overhead.
+    segment: read sorted arcs 16 + write rank/end 16 B/edge; 16 B per vertex-table entry.
+    clear  : 20 B per distinct vertex (list + slot) and 12 B/edge (list + pair key).
     """
     if phase == "update":
         return 24 * (R - fresh) + 36 * fresh + 16 * r2old
     if phase == "stage":
-        return 48 * w + 16 * D
-    if phase == "segment":
-        return 24 * D
-    if phase == "scatter":
-        return 24 * w
+        return 52 * w
     if phase == "sort":
         return 32 * w
+    if phase == "segment":
+        return 32 * w + 16 * D
     if phase == "clear":
-        return 16 * D + 12 * w
+        return 20 * D + 12 * w
     raise KeyError(phase)
 
 
@@ -267,9 +266,8 @@ def run_b200(args):
     total_alg = {
         "update": algorithmic_bytes("update", 0, count * nsteps, 0, fresh, r2old),
         "stage": algorithmic_bytes("stage", edges_done, 0, D, 0, 0),
-        "segment": algorithmic_bytes("segment", 0, 0, D, 0, 0),
-        "scatter": algorithmic_bytes("scatter", edges_done, 0, 0, 0, 0),
         "sort": algorithmic_bytes("sort", edges_done, 0, 0, 0, 0),
+        "segment": algorithmic_bytes("segment", edges_done, 0, D, 0, 0),
         "clear": algorithmic_bytes("clear", edges_done, 0, D, 0, 0),
     }
     dom_secs = prof[dom][0] / 1e3

@@ -123,13 +123,12 @@ void *tc_stream(tc_ctx *ctx);
  * tc_profile_read fills, for phase p < n (TC_PHASE_*): total milliseconds and launch count since
  * the last reset, and returns the number of phases.  Synchronises. */
 enum {
-    TC_PHASE_STAGE = 0,   /* a1+a3: staging, validation, vertex table, edge-pair hash           */
-    TC_PHASE_SEGMENT = 1, /* a2: segment starts                                                 */
-    TC_PHASE_SCATTER = 2, /* a2: arc placement                                                  */
-    TC_PHASE_SORT = 3,    /* a2: in-segment arrival order (small + big segments)                */
-    TC_PHASE_UPDATE = 4,  /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)       */
-    TC_PHASE_CLEAR = 5,   /* freeing the table slots the batch used                             */
-    TC_NPHASES = 6
+    TC_PHASE_STAGE = 0,   /* a1+a3: staging, validation, arcs + digit histograms, edge-pair hash  */
+    TC_PHASE_SORT = 1,    /* a2: stable radix sort of the arcs by vertex (arrival order kept)    */
+    TC_PHASE_SEGMENT = 2, /* a2: vertex table {deg_W, start}, per-arc rank / segment end         */
+    TC_PHASE_UPDATE = 3,  /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)       */
+    TC_PHASE_CLEAR = 4,   /* freeing the table slots the batch used                             */
+    TC_NPHASES = 5
 };
 int tc_profile(tc_ctx *ctx, int enable);
 int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n);

@@ -30,6 +30,7 @@ struct tc_ctx {
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
+    uint32_t seq = 1;  // look-back sequence numbers of the radix passes (kPasses per push)
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -59,18 +60,17 @@ static int fail_cuda(tc_ctx *c) {
 
 static void free_index(IndexBufs &ix) {
     cudaFree(ix.E);
-    cudaFree(ix.arcrec);
-    cudaFree(ix.pslot);
-    cudaFree(ix.segU);
-    cudaFree(ix.segS);
+    cudaFree(ix.keyA);
+    cudaFree(ix.valA);
+    cudaFree(ix.keyB);
+    cudaFree(ix.valB);
+    cudaFree(ix.hist);
+    cudaFree(ix.look);
     cudaFree(ix.einfo);
-    cudaFree(ix.vkey);
-    cudaFree(ix.vinfo);
-    cudaFree(ix.pkey);
-    cudaFree(ix.ppos);
+    cudaFree(ix.vt);
+    cudaFree(ix.pt);
+    cudaFree(ix.pslot);
     cudaFree(ix.vlist);
-    cudaFree(ix.midlist);
-    cudaFree(ix.chunks);
     cudaFree(ix.ctr);
     cudaFree(ix.stage);
     ix = IndexBufs();
@@ -85,17 +85,16 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
     const uint64_t pslots = next_pow2(4 * cap);  // w pairs: load <= 25%
-    ix.chunk_cap = 2 * cap / (kMidSeg + 1) + 2 * cap / kChunk + 64;
-    const uint64_t mid_cap = 2 * cap / (kTinySeg + 1) + 64;
-    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.arcrec, 16 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.pslot, 4 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.segU, 8 * cap) == cudaSuccess && cudaMalloc(&ix.segS, 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vkey, 4 * vslots) == cudaSuccess &&
-              cudaMalloc(&ix.vinfo, 8 * vslots) == cudaSuccess && cudaMalloc(&ix.pkey, 8 * pslots) == cudaSuccess &&
-              cudaMalloc(&ix.ppos, 4 * pslots) == cudaSuccess && cudaMalloc(&ix.vlist, 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.midlist, 4 * mid_cap) == cudaSuccess &&
-              cudaMalloc(&ix.chunks, 16 * ix.chunk_cap) == cudaSuccess &&
-              cudaMalloc(&ix.ctr, 64) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
+    ix.look_tiles = (2 * cap + kTile - 1) / kTile;
+    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyA, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.valA, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyB, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.valB, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.hist, 4 * kPasses * kRadix) == cudaSuccess &&
+              cudaMalloc(&ix.look, 8 * kRadix * ix.look_tiles) == cudaSuccess &&
+              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.pslot, 4 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.vlist, 8 * cap) == cudaSuccess && cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess &&
+              cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);
@@ -106,7 +105,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     ix.wcap = cap;
     launch_init_tables(ix, ctx->stream);  // all slots free; afterwards each batch frees its own slots
     CK(cudaGetLastError());
-    CK(cudaMemsetAsync(ix.ctr, 0, 64, ctx->stream));
+    CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+    CK(cudaMemsetAsync(ix.look, 0, 8 * kRadix * ix.look_tiles, ctx->stream));  // sequence 0 = never written
     return TC_OK;
 }
 
@@ -206,7 +206,7 @@ static int settle(tc_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
     if (ctx->async_errors && !ctx->poisoned && ctx->ix.ctr) {
-        CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr + 3, 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost));
         const int code = decode_err(*ctx->h_err);
         if (code != TC_OK) {
             ctx->poisoned = code;
@@ -262,12 +262,13 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     }
     const int slot = (int)((ctx->b + 1) & 1u);
     if (ctx->async_errors) {
-        CK(cudaMemsetAsync(ix.ctr, 0, 12, ctx->stream));  // keep the sticky error word ctr[3]
-        CK(cudaMemsetAsync(ix.ctr + 4, 0, 4, ctx->stream));
+        CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ctx->stream));  // keep the sticky error word
+        CK(cudaMemsetAsync(ix.ctr + kCtrErr + 1, 0, 4 * (kCtrWords - kCtrErr - 1), ctx->stream));
     } else {
-        CK(cudaMemsetAsync(ix.ctr, 0, 32, ctx->stream));
-        if (ovf) CK(cudaMemsetAsync(ix.ctr + 3, (int)kErrOvf, 1, ctx->stream));
+        CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+        if (ovf) CK(cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ctx->stream));
     }
+    CK(cudaMemsetAsync(ix.hist, 0, 4 * kPasses * kRadix, ctx->stream));
     CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
     BatchArgs a;
     a.in = in;
@@ -277,29 +278,29 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.first = ctx->first;
     a.seed = ctx->seed;
     a.S_slot = slot;
+    a.seq = ctx->seq;
+    ctx->seq += kPasses;
+    if (ctx->seq >= (1u << 29)) {  // look-back tags are 30 bits: restart them on a zeroed array
+        CK(cudaMemsetAsync(ix.look, 0, 8 * kRadix * ix.look_tiles, ctx->stream));
+        a.seq = 1;
+        ctx->seq = 1 + kPasses;
+    }
     uint32_t launches = 0;
     int n;
-    n = launch_stage(ix, a, ctx->stream);
-    launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[1], ctx->stream)); ctx->prof_launch[0] += n; }
-    n = launch_segment(ix, a, ctx->stream);
-    launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[2], ctx->stream)); ctx->prof_launch[1] += n; }
-    n = launch_scatter(ix, a, ctx->stream);
-    launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[3], ctx->stream)); ctx->prof_launch[2] += n; }
-    n = launch_sort(ix, a, ctx->stream);
-    launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[4], ctx->stream)); ctx->prof_launch[3] += n; }
-    n = launch_update(ix, ctx->st, a, ctx->stream);
-    launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[5], ctx->stream)); ctx->prof_launch[4] += n; }
-    n = launch_clear(ix, a, ctx->stream);
-    launches += n;
-    if (ctx->prof) { CK(cudaEventRecord(ctx->ev[6], ctx->stream)); ctx->prof_launch[5] += n; ctx->prof_pending = 1; }
+    int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {
+        launch_stage, launch_sort, launch_segment, nullptr, launch_clear};
+    for (int p = 0; p < TC_NPHASES; ++p) {
+        n = phase_fn[p] ? phase_fn[p](ix, a, ctx->stream) : launch_update(ix, ctx->st, a, ctx->stream);
+        launches += n;
+        if (ctx->prof) {
+            CK(cudaEventRecord(ctx->ev[p + 1], ctx->stream));
+            ctx->prof_launch[p] += n;
+        }
+    }
+    if (ctx->prof) ctx->prof_pending = 1;
     CK(cudaGetLastError());
     if (!ctx->async_errors) {
-        CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + 3, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         const int code = decode_err(*ctx->h_err);
         if (code != TC_OK) return code;  // nothing was mutated: k_update bailed out

@@ -2,16 +2,16 @@
 //
 // Per batch W = <w_0 .. w_{s-1}> the GPU builds, in HBM:
 //   E[k]      uint2  normalized edge (lo < hi)                        (the F array's edges)
-//   vertex table (open addressing, 8-key buckets = one 32-byte sector):
-//             vkey[slot] u32 vertex id (kEmptyV = free), vinfo[slot] = {deg_W(x), start of x's segment}
-//   segS      uint32 per arc (k<<1 | side), grouped by vertex, ascending k inside a group: the rankAll
-//             order of Fig. 4 read backwards (src asc, pos desc <=> rank asc), so
-//             rank(x->y) of the arc at sorted slot s is segEnd(x) - 1 - s (Definition Rank)
+//   sorted arcs: the 2|W| arcs (vertex, k<<1|side) stably radix-sorted by vertex.  Because arcs enter in
+//             arrival order, each vertex's run holds its arcs in increasing k: the rankAll order of
+//             Fig. 4 read backwards inside each src group (src asc, pos desc <=> rank asc,
+//             PAPER.md:730-734), so rank(x->y) of the arc at sorted slot s is segEnd(x) - 1 - s
+//             (Definition Rank).  segS = the sorted value array.
+//   vertex table (open addressing, 16 B slots, 2 per 32 B sector): {x, deg_W(x), segment start, -}
 //   einfo[k]  uint4 {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
-//   edge-pair hash (4-key buckets = one 32-byte sector): pkey[slot] u64 = lo<<32 | hi, ppos[slot] = k:
-//             Step 3's (src,dst)-sorted "edges" array with its multisearch replaced by
-//             one O(1) probe
-// Tables are emptied after every batch by clearing exactly the slots the batch used (no full memset).
+//   edge-pair hash (16 B slots, 2 per sector): {lo<<32 | hi, k}: Step 3's (src,dst)-sorted "edges"
+//             array with its multisearch replaced by one O(1) probe
+// Both tables are emptied after every batch by clearing exactly the slots the batch used.
 #pragma once
 #include <cstdint>
 
@@ -29,13 +29,27 @@ constexpr uint32_t kErrLoop = 2u;
 constexpr uint32_t kErrDup = 4u;
 constexpr uint32_t kErrOvf = 8u;
 
-// in-segment ordering classes (by deg_W)
-constexpr uint32_t kTinySeg = 16;   // thread per segment, register sorting network
-constexpr uint32_t kMidSeg = 256;   // warp per segment, shared-memory bitonic network
-constexpr uint32_t kChunk = 2048;   // block per chunk of <= kChunk arcs; chunks merged by rank
+// radix sort of arcs by vertex id
+constexpr uint32_t kRadixBits = 8;
+constexpr uint32_t kRadix = 1u << kRadixBits;
+constexpr uint32_t kPasses = 32 / kRadixBits;
+constexpr uint32_t kSortThreads = 256;
+constexpr uint32_t kSortItems = 8;
+constexpr uint32_t kTile = kSortThreads * kSortItems;  // arcs per tile
 
-constexpr uint32_t kVBucket = 8;  // vertex keys per probe (32 B)
-constexpr uint32_t kPBucket = 4;  // pair keys per probe (32 B)
+// device counters (ctr[])
+constexpr int kCtrD = 0;       // vertices of W (claimed vertex-table slots)
+constexpr int kCtrErr = 3;     // error bits
+constexpr int kCtrTile = 4;    // [4 .. 4+kPasses) dynamic tile ids of the radix passes
+constexpr int kCtrWords = 16;
+
+struct __align__(16) VSlot {
+    uint32_t key, deg, start, pad;
+};
+struct __align__(16) PSlot {
+    unsigned long long key;
+    uint32_t pos, pad;
+};
 
 __device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
     x ^= x >> 16;
@@ -60,41 +74,30 @@ __device__ __forceinline__ unsigned long long pair_key(uint32_t lo, uint32_t hi)
     return ((unsigned long long)lo << 32) | hi;
 }
 
-// index of the first lane of a uint4 equal to v (0..3), or -1
-__device__ __forceinline__ int match4(uint4 k, uint32_t v) {
-    return k.x == v ? 0 : k.y == v ? 1 : k.z == v ? 2 : k.w == v ? 3 : -1;
-}
-
 // Probe the complete (read-only) vertex table: {deg_W(v), segment start}, or {0, 0} when v is not in W.
-__device__ __forceinline__ uint2 vt_find(const uint32_t *__restrict__ vkey, const uint2 *__restrict__ vinfo,
-                                         uint32_t mask, uint32_t v) {
-    uint32_t b = hash_vertex(v) & mask & ~(kVBucket - 1);
+// One probe = one 32-byte sector holding two slots.
+__device__ __forceinline__ uint2 vt_find(const VSlot *__restrict__ vt, uint32_t mask, uint32_t v) {
+    uint32_t b = hash_vertex(v) & mask & ~1u;
     while (true) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(vkey + b);
-        const uint4 k0 = __ldg(p), k1 = __ldg(p + 1);
-        int j = match4(k0, v);
-        if (j < 0) {
-            j = match4(k1, v);
-            if (j >= 0) j += 4;
-        }
-        if (j >= 0) return __ldg(vinfo + b + j);
-        if (match4(k0, kEmptyV) >= 0 || match4(k1, kEmptyV) >= 0) return make_uint2(0u, 0u);
-        b = (b + kVBucket) & mask;
+        const uint4 *p = reinterpret_cast<const uint4 *>(vt + b);
+        const uint4 s0 = __ldg(p), s1 = __ldg(p + 1);
+        if (s0.x == v) return make_uint2(s0.y, s0.z);
+        if (s1.x == v) return make_uint2(s1.y, s1.z);
+        if (s0.x == kEmptyV || s1.x == kEmptyV) return make_uint2(0u, 0u);
+        b = (b + 2) & mask;
     }
 }
 
 // Probe the complete (read-only) edge-pair hash: batch position of (lo, hi) or -1.
-__device__ __forceinline__ int64_t pt_find(const unsigned long long *__restrict__ pkey,
-                                           const uint32_t *__restrict__ ppos, uint32_t mask,
-                                           unsigned long long key) {
-    uint32_t b = hash_pair(key) & mask & ~(kPBucket - 1);
+__device__ __forceinline__ int64_t pt_find(const PSlot *__restrict__ pt, uint32_t mask, unsigned long long key) {
+    uint32_t b = hash_pair(key) & mask & ~1u;
     while (true) {
-        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(pkey + b);
-        const ulonglong2 a = __ldg(p), c = __ldg(p + 1);
-        const int j = a.x == key ? 0 : a.y == key ? 1 : c.x == key ? 2 : c.y == key ? 3 : -1;
-        if (j >= 0) return (int64_t)__ldg(ppos + b + j);
-        if (a.x == kEmptyP || a.y == kEmptyP || c.x == kEmptyP || c.y == kEmptyP) return -1;
-        b = (b + kPBucket) & mask;
+        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(pt + b);
+        const ulonglong2 s0 = __ldg(p), s1 = __ldg(p + 1);
+        if (s0.x == key) return (int64_t)(uint32_t)s0.y;
+        if (s1.x == key) return (int64_t)(uint32_t)s1.y;
+        if (s0.x == kEmptyP || s1.x == kEmptyP) return -1;
+        b = (b + 2) & mask;
     }
 }
 

@@ -1,23 +1,22 @@
 // kernels.cu -- the per-batch hot path of bulkUpdateAll on sm_100a.
 //
 // Pipeline for one batch W:
-//   k_stage        a1 + a3 : load W (coalesced 16-byte loads = 2 edges), validate, normalize to (lo, hi),
-//                            insert both endpoints into the vertex table and the edge into the edge-pair
-//                            hash -- one CAS round trip per probe, all three inserts in flight together --
-//                            then take an arrival ticket per arc (atomicAdd on deg_W)
-//   k_segment      a2      : one contiguous segment per vertex (block scan + one atomic per block); bins
-//                            segments by length
-//   k_scatter      a2      : every arc to segment start + ticket (unordered inside a segment)
-//   k_order_tiny   a2      : segments of <= 16 arcs: one thread, register sorting network
-//   k_order_mid    a2      : 17..256 arcs: one warp, shared-memory bitonic network
-//   k_sort_chunks  a2      : longer: one block per <= 2048-arc chunk, shared-memory bitonic network
-//   k_merge_chunks a2      : segments of > 2048 arcs: final slot = sum of ranks across sorted chunks
-//   k_update       a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2
-//                            (chi^+ from ranks / degrees, level-2 pick by segment arithmetic), Step 3
-//                            (closing-edge probe), block partial sums of chi over closed estimators
-//   k_clear                : empties exactly the table slots this batch used
-// After a2 the segment of vertex x holds x's arcs in increasing arrival position, i.e. Fig. 4's
-// rankAll order (src asc, pos desc) reversed inside each src group: rank(x->y) = segEnd - 1 - slot.
+//   k_stage      a1 + a3 : load W (16-byte loads = 2 edges), validate, normalize to (lo, hi); emit the 2|W|
+//                          arcs (vertex, k<<1|side) in arrival order -- the F array of rankAll's proof
+//                           -- and their 8-bit digit histograms; insert the edge into
+//                          the edge-pair hash (one CAS round trip per probe; a repeat is TC_EDUP)
+//   k_radix_pass a2      : stable LSD radix pass over the arcs by vertex id (one kernel per 8-bit digit,
+//                          single sweep with decoupled look-back; passes whose digit is zero for every
+//                          arc are skipped on the device).  Stability keeps arrival order inside a vertex:
+//                          this replaces rankAll's sort by (src, -pos).
+//   k_runs       a2      : runs of equal vertex inside each tile -> vertex table {deg_W, segment start};
+//                          ranks/segment ends of the arcs of tile-internal segments
+//   k_fix        a2      : ranks/segment ends of the arcs of segments that cross tile boundaries
+//   k_update     a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2 (chi^+
+//                          from ranks / degrees, level-2 pick by segment arithmetic), Step 3 (closing-edge
+//                          probe), block partial sums of chi over closed estimators
+//   k_clear              : empties exactly the table slots this batch used
+// rank(x->y) of the arc at sorted slot s = segEnd(x) - 1 - s (Definition Rank).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,115 +29,69 @@
 namespace tcb {
 
 // ------------------------------------------------------------------------------------------------
-// a1 + a3: staging and table inserts
-
-struct VIns {  // an in-flight vertex insert
-    uint32_t v, b, slot;
-    bool done, claimed;
-};
-
-// One probe step of a vertex insert: reads the 8-key bucket, CASes the first free key if v is absent.
-__device__ __forceinline__ void vins_step(uint32_t *vkey, uint32_t mask, VIns &s) {
-    const uint4 *p = reinterpret_cast<const uint4 *>(vkey + s.b);
-    const uint4 k0 = __ldcg(p), k1 = __ldcg(p + 1);
-    int j = match4(k0, s.v);
-    if (j < 0) {
-        j = match4(k1, s.v);
-        if (j >= 0) j += 4;
-    }
-    if (j >= 0) {
-        s.slot = s.b + j;
-        s.done = true;
-        return;
-    }
-    int e = match4(k0, kEmptyV);
-    if (e < 0) {
-        e = match4(k1, kEmptyV);
-        if (e >= 0) e += 4;
-    }
-    if (e < 0) {
-        s.b = (s.b + kVBucket) & mask;  // bucket full without v: next bucket
-        return;
-    }
-    const uint32_t old = atomicCAS(vkey + s.b + e, kEmptyV, s.v);
-    if (old == kEmptyV || old == s.v) {
-        s.slot = s.b + e;
-        s.done = true;
-        s.claimed = (old == kEmptyV);
-    }
-    // else: another vertex took that key slot; re-read the same bucket
-}
-
-struct PIns {
-    unsigned long long key;
-    uint32_t b, slot;
-    bool done, dup;
-};
-
-__device__ __forceinline__ void pins_step(unsigned long long *pkey, uint32_t mask, PIns &s) {
-    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(pkey + s.b);
-    const ulonglong2 a = __ldcg(p), c = __ldcg(p + 1);
-    if (a.x == s.key || a.y == s.key || c.x == s.key || c.y == s.key) {
-        s.done = true;
-        s.dup = true;
-        return;
-    }
-    const int e = a.x == kEmptyP ? 0 : a.y == kEmptyP ? 1 : c.x == kEmptyP ? 2 : c.y == kEmptyP ? 3 : -1;
-    if (e < 0) {
-        s.b = (s.b + kPBucket) & mask;
-        return;
-    }
-    const unsigned long long old = atomicCAS(pkey + s.b + e, kEmptyP, s.key);
-    if (old == kEmptyP) {
-        s.slot = s.b + e;
-        s.done = true;
-    } else if (old == s.key) {
-        s.done = true;
-        s.dup = true;
-    }
-}
+// a1 + a3: staging, arcs, digit histograms, edge-pair hash
 
 struct StageCtx {
     uint2 *E;
-    uint4 *arcrec;
-    uint32_t *pslot;
-    uint32_t *vkey;
-    uint2 *vinfo;
-    uint32_t vmask;
-    unsigned long long *pkey;
-    uint32_t *ppos;
+    uint32_t *key, *val;  // arcs out (radix buffer A)
+    uint32_t *hist;       // [kPasses][kRadix]
+    PSlot *pt;
     uint32_t pmask;
+    uint32_t *pslot;
     uint32_t *ctr;
 };
 
-__device__ __forceinline__ uint32_t stage_one(const StageCtx &c, uint2 e, uint32_t k) {
+// Insert (lo, hi) -> k; false if the pair is already present (an in-batch duplicate).
+__device__ __forceinline__ bool pair_insert(const StageCtx &c, unsigned long long key, uint32_t k) {
+    uint32_t b = hash_pair(key) & c.pmask & ~1u;
+    while (true) {
+        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + b);
+        const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
+        if (s0.x == key || s1.x == key) {
+            c.pslot[k] = kNoSlot;
+            return false;
+        }
+        const uint32_t e = s0.x == kEmptyP ? 0u : s1.x == kEmptyP ? 1u : 2u;
+        if (e == 2u) {
+            b = (b + 2) & c.pmask;
+            continue;
+        }
+        const unsigned long long old = atomicCAS(&c.pt[b + e].key, kEmptyP, key);
+        if (old == kEmptyP) {
+            c.pt[b + e].pos = k;
+            c.pslot[k] = b + e;
+            return true;
+        }
+        if (old == key) {
+            c.pslot[k] = kNoSlot;
+            return false;
+        }
+        // another pair took the slot: re-read the bucket
+    }
+}
+
+__device__ __forceinline__ uint32_t stage_one(const StageCtx &c, uint2 e, uint32_t k, uint32_t (*sh)[kRadix]) {
     if (e.x == kEmptyV || e.y == kEmptyV || e.x == e.y) {
         c.pslot[k] = kNoSlot;
         return (e.x == kEmptyV || e.y == kEmptyV) ? kErrInval : kErrLoop;
     }
     const uint32_t lo = min(e.x, e.y), hi = max(e.x, e.y);
     c.E[k] = make_uint2(lo, hi);
-    VIns a{lo, hash_vertex(lo) & c.vmask & ~(kVBucket - 1), 0, false, false};
-    VIns b{hi, hash_vertex(hi) & c.vmask & ~(kVBucket - 1), 0, false, false};
-    const unsigned long long key = pair_key(lo, hi);
-    PIns q{key, hash_pair(key) & c.pmask & ~(kPBucket - 1), kNoSlot, false, false};
-    // the three inserts are independent: step them together so their round trips overlap
-    while (!(a.done && b.done && q.done)) {
-        if (!a.done) vins_step(c.vkey, c.vmask, a);
-        if (!b.done) vins_step(c.vkey, c.vmask, b);
-        if (!q.done) pins_step(c.pkey, c.pmask, q);
+    reinterpret_cast<uint2 *>(c.key)[k] = make_uint2(lo, hi);
+    reinterpret_cast<uint2 *>(c.val)[k] = make_uint2(k << 1, (k << 1) | 1u);
+#pragma unroll
+    for (uint32_t p = 0; p < kPasses; ++p) {
+        atomicAdd(&sh[p][(lo >> (p * kRadixBits)) & (kRadix - 1)], 1u);
+        atomicAdd(&sh[p][(hi >> (p * kRadixBits)) & (kRadix - 1)], 1u);
     }
-    // arrival tickets: deg_W counters (two independent atomics)
-    const uint32_t ta = atomicAdd(&c.vinfo[a.slot].x, 1u);
-    const uint32_t tb = atomicAdd(&c.vinfo[b.slot].x, 1u);
-    c.arcrec[k] = make_uint4(a.slot, ta, b.slot, tb);
-    c.pslot[k] = q.slot;
-    if (!q.dup) c.ppos[q.slot] = k;
-    return q.dup ? kErrDup : 0u;
+    return pair_insert(c, pair_key(lo, hi), k) ? 0u : kErrDup;
 }
 
 __global__ void __launch_bounds__(256) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
-    if (c.ctr[3] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    __shared__ uint32_t sh[kPasses][kRadix];
+    for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
+    __syncthreads();
     uint32_t bad = 0;
     const uint32_t stride = gridDim.x * blockDim.x;
     if ((reinterpret_cast<uintptr_t>(in) & 15u) == 0) {
@@ -146,306 +99,301 @@ __global__ void __launch_bounds__(256) k_stage(const uint2 *__restrict__ in, uin
         const uint4 *in4 = reinterpret_cast<const uint4 *>(in);
         for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
             const uint4 two = __ldcs(in4 + q);
-            bad |= stage_one(c, make_uint2(two.x, two.y), 2 * q);
-            bad |= stage_one(c, make_uint2(two.z, two.w), 2 * q + 1);
+            bad |= stage_one(c, make_uint2(two.x, two.y), 2 * q, sh);
+            bad |= stage_one(c, make_uint2(two.z, two.w), 2 * q + 1, sh);
         }
-        if ((w & 1u) && blockIdx.x * blockDim.x + threadIdx.x == 0) bad |= stage_one(c, in[w - 1], w - 1);
+        if ((w & 1u) && blockIdx.x * blockDim.x + threadIdx.x == 0) bad |= stage_one(c, in[w - 1], w - 1, sh);
     } else {
-        for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < w; k += stride) bad |= stage_one(c, in[k], k);
+        for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < w; k += stride) bad |= stage_one(c, in[k], k, sh);
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&c.ctr[3], bad);
+    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&c.ctr[kCtrErr], bad);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += blockDim.x) {
+        const uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(c.hist + i, v);
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
-// a2: segments
+// a2: stable LSD radix sort of the arcs by vertex id
 
-// Block-wide exclusive scan of a 64-bit value (256 threads); returns the exclusive prefix and sets total.
-__device__ __forceinline__ unsigned long long block_scan_u64(unsigned long long v, unsigned long long &total,
-                                                             unsigned long long *wsum /* [9] */) {
+// A pass is trivial (identity) when every arc has digit 0; the ping-pong parity counts executed passes.
+__device__ __forceinline__ bool pass_trivial(const uint32_t *hist, uint32_t p, uint32_t n) {
+    return hist[p * kRadix] == n;
+}
+__device__ __forceinline__ uint32_t passes_executed(const uint32_t *hist, uint32_t upto, uint32_t n) {
+    uint32_t e = 0;
+    for (uint32_t p = 0; p < upto; ++p) e += pass_trivial(hist, p, n) ? 0u : 1u;
+    return e;
+}
+
+struct RadixBufs {
+    uint32_t *keyA, *valA, *keyB, *valB;
+    const uint32_t *hist;
+    unsigned long long *look;
+    uint32_t *ctr;
+};
+
+constexpr unsigned long long kFlagAgg = 1ull, kFlagPrefix = 2ull;
+
+__global__ void __launch_bounds__(kSortThreads) k_radix_pass(RadixBufs rb, uint32_t n, uint32_t pass, uint32_t seq) {
+    if (rb.ctr[kCtrErr]) return;
+    if (pass_trivial(rb.hist, pass, n)) return;
+    const bool odd = passes_executed(rb.hist, pass, n) & 1u;
+    const uint32_t *__restrict__ kin = odd ? rb.keyB : rb.keyA;
+    const uint32_t *__restrict__ vin = odd ? rb.valB : rb.valA;
+    uint32_t *__restrict__ kout = odd ? rb.keyA : rb.keyB;
+    uint32_t *__restrict__ vout = odd ? rb.valA : rb.valB;
+    const uint32_t shift = pass * kRadixBits;
+
+    __shared__ uint32_t whist[kSortThreads / 32][kRadix];  // per-warp digit counts -> warp offsets
+    __shared__ uint32_t gofs[kRadix];                      // global start of each digit for this tile
+    __shared__ uint32_t ws[kSortThreads / 32];
+    __shared__ uint32_t tile_sh;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    unsigned long long incl = v;
+    for (uint32_t i = threadIdx.x; i < (kSortThreads / 32) * kRadix; i += kSortThreads) (&whist[0][0])[i] = 0;
+    if (threadIdx.x == 0) tile_sh = atomicAdd(&rb.ctr[kCtrTile + pass], 1u);  // dynamic tile order
+    __syncthreads();
+    const uint32_t tile = tile_sh;
+    const uint32_t wbase = tile * kTile + warp * (32 * kSortItems);
+
+    // stable in-tile ranks: warp w owns a contiguous 256-arc range, processed in 8 rounds of 32
+    uint32_t keys[kSortItems], vals[kSortItems], rnk[kSortItems];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = wbase + j * 32 + lane;
+        const bool valid = idx < n;
+        keys[j] = valid ? __ldcs(kin + idx) : 0u;
+        vals[j] = valid ? __ldcs(vin + idx) : 0u;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const bool valid = wbase + j * 32 + lane < n;
+        const uint32_t d = valid ? (keys[j] >> shift) & (kRadix - 1) : kRadix;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t before = __popc(peers & lt);
+        uint32_t b = 0;
+        if (valid) b = whist[warp][d];
+        __syncwarp();
+        if (valid && before == 0) whist[warp][d] = b + __popc(peers);
+        __syncwarp();
+        rnk[j] = b + before;
+    }
+    __syncthreads();
+    // per digit: exclusive prefix over warps (warp order == arc order), tile total
+    const uint32_t dgt = threadIdx.x;  // kSortThreads == kRadix
+    uint32_t total = 0;
+#pragma unroll
+    for (uint32_t x = 0; x < kSortThreads / 32; ++x) {
+        const uint32_t cnt = whist[x][dgt];
+        whist[x][dgt] = total;
+        total += cnt;
+    }
+    // decoupled look-back over earlier tiles for this digit
+    unsigned long long *lk = rb.look + (size_t)tile * kRadix + dgt;
+    const unsigned long long tag = (unsigned long long)seq << 2;
+    uint32_t excl = 0;
+    if (tile == 0) {
+        atomicExch(lk, ((tag | kFlagPrefix) << 32) | total);
+    } else {
+        atomicExch(lk, ((tag | kFlagAgg) << 32) | total);
+        for (int32_t t = (int32_t)tile - 1; t >= 0; --t) {
+            const volatile unsigned long long *q = rb.look + (size_t)t * kRadix + dgt;
+            unsigned long long v;
+            do {
+                v = *q;
+            } while ((v >> 34) != seq || ((v >> 32) & 3ull) == 0ull);
+            excl += (uint32_t)v;
+            if (((v >> 32) & 3ull) == kFlagPrefix) break;
+        }
+        atomicExch(lk, ((tag | kFlagPrefix) << 32) | (excl + total));
+    }
+    // global digit offset: exclusive scan of this pass's histogram (digit order)
+    const uint32_t h = rb.hist[pass * kRadix + dgt];
+    uint32_t incl = h;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        const unsigned long long y = __shfl_up_sync(0xffffffffu, incl, off);
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= (uint32_t)off) incl += y;
+    }
+    if (lane == 31) ws[warp] = incl;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (uint32_t x = 0; x < warp; ++x) wpre += ws[x];
+    gofs[dgt] = wpre + incl - h + excl;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = wbase + j * 32 + lane;
+        if (idx < n) {
+            const uint32_t d = (keys[j] >> shift) & (kRadix - 1);
+            const uint32_t pos = gofs[d] + whist[warp][d] + rnk[j];
+            kout[pos] = keys[j];
+            vout[pos] = vals[j];
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// a2: segments of the sorted arcs -> vertex table, ranks / segment ends
+
+struct SegBufs {
+    uint32_t *keyA, *valA, *keyB, *valB;
+    const uint32_t *hist;
+    VSlot *vt;
+    uint32_t vmask;
+    uint2 *einfo2;  // [2 wcap]: einfo2[k<<1|side] = {sorted slot, segment end}
+    uint32_t *vlist;
+    uint32_t *ctr;
+};
+
+__device__ __forceinline__ void sorted_bufs(const SegBufs &sb, uint32_t n, const uint32_t *&keys,
+                                            const uint32_t *&vals) {
+    const bool odd = passes_executed(sb.hist, kPasses, n) & 1u;
+    keys = odd ? sb.keyB : sb.keyA;
+    vals = odd ? sb.valB : sb.valA;
+}
+
+// Insert-or-find v; returns the slot, sets claimed when this call created it.
+__device__ __forceinline__ uint32_t vt_insert(VSlot *vt, uint32_t mask, uint32_t v, bool &claimed) {
+    uint32_t b = hash_vertex(v) & mask & ~1u;
+    claimed = false;
+    while (true) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(vt + b);
+        const uint4 s0 = __ldcg(p), s1 = __ldcg(p + 1);
+        if (s0.x == v) return b;
+        if (s1.x == v) return b + 1;
+        const uint32_t e = s0.x == kEmptyV ? 0u : s1.x == kEmptyV ? 1u : 2u;
+        if (e == 2u) {
+            b = (b + 2) & mask;
+            continue;
+        }
+        const uint32_t old = atomicCAS(&vt[b + e].key, kEmptyV, v);
+        if (old == kEmptyV) {
+            claimed = true;
+            return b + e;
+        }
+        if (old == v) return b + e;
+    }
+}
+
+// One block per tile of kTile sorted arcs (8 consecutive per thread).
+__global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
+    if (sb.ctr[kCtrErr]) return;
+    const uint32_t *keys, *vals;
+    sorted_bufs(sb, n, keys, vals);
+    __shared__ uint32_t skey[kTile + 2];
+    __shared__ uint32_t run_start[kTile], run_end[kTile];
+    __shared__ uint32_t wsum[kSortThreads / 32];
+    __shared__ uint32_t nclaim_sh, claim_base;
+    const uint32_t t0 = blockIdx.x * kTile;
+    const uint32_t tn = min(kTile, n - t0);
+    for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads) skey[i + 1] = keys[t0 + i];
+    if (threadIdx.x == 0) {
+        skey[0] = t0 > 0 ? keys[t0 - 1] : ~keys[t0];                       // halo: previous arc's key
+        skey[tn + 1] = t0 + tn < n ? keys[t0 + tn] : ~keys[t0 + tn - 1];  // halo: next arc's key
+        nclaim_sh = 0;
+    }
+    __syncthreads();
+    // local run heads (inside the tile) -> run ids by a block scan
+    const uint32_t i0 = threadIdx.x * kSortItems;
+    uint32_t heads = 0;
+#pragma unroll
+    for (uint32_t e = 0; e < kSortItems; ++e) {
+        const uint32_t i = i0 + e;
+        if (i < tn && (i == 0 || skey[i + 1] != skey[i])) ++heads;
+    }
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t incl = heads;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
         if (lane >= (uint32_t)off) incl += y;
     }
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
-    if (threadIdx.x < 8) {
-        const unsigned long long wv = wsum[threadIdx.x];
-        unsigned long long x = wv;
+    uint32_t wpre = 0, nruns = 0;
+    for (uint32_t x = 0; x < kSortThreads / 32; ++x) {
+        if (x < warp) wpre += wsum[x];
+        nruns += wsum[x];
+    }
+    uint32_t rid[kSortItems];
+    {
+        uint32_t r = wpre + incl - heads;  // runs started before this thread's first arc
 #pragma unroll
-        for (int off = 1; off < 8; off <<= 1) {
-            const unsigned long long y = __shfl_up_sync(0xffu, x, off);
-            if (threadIdx.x >= (uint32_t)off) x += y;
+        for (uint32_t e = 0; e < kSortItems; ++e) {
+            const uint32_t i = i0 + e;
+            if (i < tn && (i == 0 || skey[i + 1] != skey[i])) {
+                run_start[r] = i;
+                ++r;
+            }
+            rid[e] = r - 1;
+            if (i < tn && (i + 1 == tn || skey[i + 2] != skey[i + 1])) run_end[r - 1] = i + 1;
         }
-        wsum[threadIdx.x] = x - wv;
-        if (threadIdx.x == 7) wsum[8] = x;
     }
     __syncthreads();
-    total = wsum[8];
-    const unsigned long long ex = wsum[warp] + incl - v;
-    __syncthreads();
-    return ex;
-}
-
-// Segment start of every vertex of W (the order of segments is irrelevant, only their contents).
-// Walks the vertex table in tiles of 256 x 8 slots: the compact vertex list, the segment starts and
-// the length bins (mid list, big-segment chunks) are appended with ONE atomic per tile and counter.
-__global__ void __launch_bounds__(256) k_segment(const uint32_t *__restrict__ vkey, uint2 *vinfo, uint32_t nslots,
-                                                 uint32_t *__restrict__ vlist, uint32_t *__restrict__ midlist,
-                                                 uint4 *__restrict__ chunks, uint32_t *ctr) {
-    if (ctr[3]) return;
-    __shared__ unsigned long long wsum[9];
-    __shared__ uint32_t base[4];
-    const uint32_t tile_slots = 256u * kVBucket;
-    for (uint32_t t0 = blockIdx.x * tile_slots; t0 < nslots; t0 += gridDim.x * tile_slots) {
-        const uint32_t s0 = t0 + threadIdx.x * kVBucket;
-        const uint4 *p = reinterpret_cast<const uint4 *>(vkey + s0);
-        const uint4 k0 = p[0], k1 = p[1];
-        const uint32_t keys[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
-        uint32_t deg[8];
-        uint32_t nocc = 0, nmid = 0, degsum = 0, nch = 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            deg[i] = keys[i] != kEmptyV ? vinfo[s0 + i].x : 0u;
-            nocc += keys[i] != kEmptyV;
-            degsum += deg[i];
-            nmid += (deg[i] > kTinySeg && deg[i] <= kMidSeg);
-            nch += deg[i] > kMidSeg ? (deg[i] + kChunk - 1) / kChunk : 0u;
-        }
-        unsigned long long tot_a, tot_b;
-        const unsigned long long ex_a =
-            block_scan_u64(((unsigned long long)degsum << 32) | nocc, tot_a, wsum);  // degsum fits: <= 2w
-        const unsigned long long ex_b = block_scan_u64(((unsigned long long)nch << 32) | nmid, tot_b, wsum);
-        if (threadIdx.x == 0) {
-            base[0] = (uint32_t)tot_a ? atomicAdd(&ctr[0], (uint32_t)tot_a) : 0u;
-            base[1] = (uint32_t)(tot_a >> 32) ? atomicAdd(&ctr[1], (uint32_t)(tot_a >> 32)) : 0u;
-            base[2] = (uint32_t)tot_b ? atomicAdd(&ctr[4], (uint32_t)tot_b) : 0u;
-            base[3] = (uint32_t)(tot_b >> 32) ? atomicAdd(&ctr[2], (uint32_t)(tot_b >> 32)) : 0u;
-        }
-        __syncthreads();
-        uint32_t li = base[0] + (uint32_t)ex_a, st = base[1] + (uint32_t)(ex_a >> 32);
-        uint32_t mi = base[2] + (uint32_t)ex_b, ci = base[3] + (uint32_t)(ex_b >> 32);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (keys[i] == kEmptyV) continue;
-            const uint32_t s = s0 + i;
-            vinfo[s].y = st;
-            vlist[li++] = s;
-            if (deg[i] > kMidSeg) {
-                const uint32_t n = (deg[i] + kChunk - 1) / kChunk;
-                for (uint32_t c = 0; c < n; ++c) chunks[ci++] = make_uint4(st, deg[i], c, 0u);
-            } else if (deg[i] > kTinySeg) {
-                midlist[mi++] = s;
-            }
-            st += deg[i];
-        }
-        __syncthreads();
-    }
-}
-
-// every arc to segment start + ticket
-__global__ void __launch_bounds__(256) k_scatter(const uint4 *__restrict__ arcrec, const uint2 *__restrict__ vinfo,
-                                                 uint32_t *__restrict__ segU, uint32_t w, const uint32_t *ctr) {
-    if (ctr[3]) return;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < w; k += gridDim.x * blockDim.x) {
-        const uint4 a = arcrec[k];
-        const uint32_t s0 = vinfo[a.x].y, s1 = vinfo[a.z].y;
-        segU[s0 + a.y] = k << 1;
-        segU[s1 + a.w] = (k << 1) | 1u;
-    }
-}
-
-__device__ __forceinline__ void cswap(uint32_t &a, uint32_t &b) {
-    const uint32_t x = min(a, b), y = max(a, b);
-    a = x;
-    b = y;
-}
-
-// Register bitonic sorter of N (power of two) keys, fully unrolled.
-template <int N>
-__device__ __forceinline__ void bitonic_regs(uint32_t (&x)[N]) {
-#pragma unroll
-    for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                const int j = i ^ stride;
-                if (j > i) {
-                    if ((i & size) == 0) cswap(x[i], x[j]);
-                    else cswap(x[j], x[i]);
-                }
-            }
-        }
-    }
-}
-
-template <int N>
-__device__ __forceinline__ void order_small(const uint32_t *__restrict__ segU, uint32_t *__restrict__ segS,
-                                            uint2 *__restrict__ einfo2, uint32_t start, uint32_t deg) {
-    uint32_t x[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) x[i] = (uint32_t)i < deg ? segU[start + i] : 0xFFFFFFFFu;
-    bitonic_regs<N>(x);
-    const uint32_t end = start + deg;
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        if ((uint32_t)i < deg) {
-            segS[start + i] = x[i];
-            einfo2[x[i]] = make_uint2(start + i, end);
-        }
-    }
-}
-
-// segments of <= kTinySeg arcs: one thread each
-__global__ void __launch_bounds__(256) k_order_tiny(const uint32_t *__restrict__ vlist, const uint2 *__restrict__ vinfo,
-                                                    const uint32_t *__restrict__ segU, uint32_t *__restrict__ segS,
-                                                    uint2 *__restrict__ einfo2, const uint32_t *ctr) {
-    if (ctr[3]) return;
-    const uint32_t D = ctr[0];
-    for (uint32_t d = blockIdx.x * blockDim.x + threadIdx.x; d < D; d += gridDim.x * blockDim.x) {
-        const uint2 inf = vinfo[vlist[d]];
-        const uint32_t deg = inf.x, start = inf.y;
-        if (deg == 1) {
-            const uint32_t v = segU[start];
-            segS[start] = v;
-            einfo2[v] = make_uint2(start, start + 1);
-        } else if (deg == 2) {
-            uint32_t a = segU[start], b = segU[start + 1];
-            cswap(a, b);
-            segS[start] = a;
-            segS[start + 1] = b;
-            einfo2[a] = make_uint2(start, start + 2);
-            einfo2[b] = make_uint2(start + 1, start + 2);
-        } else if (deg <= 4) {
-            order_small<4>(segU, segS, einfo2, start, deg);
-        } else if (deg <= 8) {
-            order_small<8>(segU, segS, einfo2, start, deg);
-        } else if (deg <= kTinySeg) {
-            order_small<16>(segU, segS, einfo2, start, deg);
-        }
-    }
-}
-
-// segments of kTinySeg+1 .. kMidSeg arcs: one warp each, bitonic network in shared memory
-__global__ void __launch_bounds__(256) k_order_mid(const uint32_t *__restrict__ midlist, const uint2 *__restrict__ vinfo,
-                                                   const uint32_t *__restrict__ segU, uint32_t *__restrict__ segS,
-                                                   uint2 *__restrict__ einfo2, const uint32_t *ctr) {
-    if (ctr[3]) return;
-    __shared__ uint32_t sm[8][kMidSeg];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint32_t *s = sm[warp];
-    const uint32_t n_mid = ctr[4];
-    for (uint32_t q = blockIdx.x * 8u + warp; q < n_mid; q += gridDim.x * 8u) {
-        const uint2 inf = vinfo[midlist[q]];
-        const uint32_t deg = inf.x, start = inf.y;
-        uint32_t P = 32;
-        while (P < deg) P <<= 1;
-        for (uint32_t i = lane; i < P; i += 32) s[i] = i < deg ? segU[start + i] : 0xFFFFFFFFu;
-        __syncwarp();
-        for (uint32_t size = 2; size <= P; size <<= 1) {
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = lane; i < (P >> 1); i += 32) {
-                    const uint32_t lo = 2 * i - (i & (stride - 1));
-                    const uint32_t hi = lo + stride;
-                    const uint32_t x = s[lo], y = s[hi];
-                    if ((x > y) == ((lo & size) == 0)) {
-                        s[lo] = y;
-                        s[hi] = x;
-                    }
-                }
-                __syncwarp();
-            }
-        }
-        const uint32_t end = start + deg;
-        for (uint32_t i = lane; i < deg; i += 32) {
-            const uint32_t v = s[i];
-            segS[start + i] = v;
-            einfo2[v] = make_uint2(start + i, end);
-        }
-        __syncwarp();
-    }
-}
-
-// longer segments: sort each chunk of <= kChunk arcs in shared memory (bitonic network)
-__global__ void __launch_bounds__(512) k_sort_chunks(const uint4 *__restrict__ chunks, uint32_t *segU,
-                                                     uint32_t *__restrict__ segS, uint2 *__restrict__ einfo2,
-                                                     const uint32_t *ctr) {
-    if (ctr[3]) return;
-    __shared__ uint32_t sm[kChunk];
-    const uint32_t nch = ctr[2];
-    for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-        const uint4 d = chunks[c];
-        const uint32_t start = d.x, deg = d.y, ci = d.z;
-        const uint32_t base = start + ci * kChunk;
-        const uint32_t n = min(kChunk, deg - ci * kChunk);
-        uint32_t P = 2;
-        while (P < n) P <<= 1;
-        for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) sm[i] = i < n ? segU[base + i] : 0xFFFFFFFFu;
-        __syncthreads();
-        for (uint32_t size = 2; size <= P; size <<= 1) {
-            for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-                for (uint32_t i = threadIdx.x; i < (P >> 1); i += blockDim.x) {
-                    const uint32_t lo = 2 * i - (i & (stride - 1));
-                    const uint32_t hi = lo + stride;
-                    const uint32_t x = sm[lo], y = sm[hi];
-                    if ((x > y) == ((lo & size) == 0)) {
-                        sm[lo] = y;
-                        sm[hi] = x;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        if (deg <= kChunk) {
-            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-                const uint32_t v = sm[i];
-                segS[start + i] = v;
-                einfo2[v] = make_uint2(start + i, start + deg);
-            }
+    // one thread per run: vertex table (complete segments by plain stores, split ones by atomics)
+    for (uint32_t r = threadIdx.x; r < nruns; r += kSortThreads) {
+        const uint32_t s = run_start[r], e = run_end[r];
+        const uint32_t v = skey[s + 1];
+        const bool ghead = skey[s] != v;      // the segment starts in this tile
+        const bool gtail = skey[e + 1] != v;  // ... and ends in it
+        bool claimed;
+        const uint32_t slot = vt_insert(sb.vt, sb.vmask, v, claimed);
+        if (ghead && gtail) {
+            sb.vt[slot].deg = e - s;
+            sb.vt[slot].start = t0 + s;
         } else {
-            for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) segU[base + i] = sm[i];
+            atomicAdd(&sb.vt[slot].deg, e - s);
+            atomicMin(&sb.vt[slot].start, t0 + s);
+            run_end[r] = 0;  // the segment crosses the tile: k_fix writes its arcs' einfo
         }
-        __syncthreads();
+        run_start[r] = claimed ? (slot | 0x80000000u) : 0u;
+        if (claimed) atomicAdd(&nclaim_sh, 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        claim_base = nclaim_sh ? atomicAdd(&sb.ctr[kCtrD], nclaim_sh) : 0u;
+        nclaim_sh = 0;
+    }
+    __syncthreads();
+    // compact the claimed slots into vlist (order inside a tile is irrelevant)
+    for (uint32_t r = threadIdx.x; r < nruns; r += kSortThreads) {
+        if (run_start[r] & 0x80000000u) sb.vlist[claim_base + atomicAdd(&nclaim_sh, 1u)] = run_start[r] & 0x7FFFFFFFu;
+    }
+    // arcs of tile-internal segments: einfo = {sorted slot, segment end}
+#pragma unroll
+    for (uint32_t e = 0; e < kSortItems; ++e) {
+        const uint32_t i = i0 + e;
+        if (i < tn) {
+            const uint32_t end = run_end[rid[e]];
+            if (end) sb.einfo2[vals[t0 + i]] = make_uint2(t0 + i, t0 + end);
+        }
     }
 }
 
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *a, uint32_t n, uint32_t v) {
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) < v) lo = mid + 1;
-        else hi = mid;
+// Arcs of segments that cross tile boundaries (at most the first and the last segment of a tile).
+__global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
+    if (sb.ctr[kCtrErr]) return;
+    const uint32_t *keys, *vals;
+    sorted_bufs(sb, n, keys, vals);
+    __shared__ uint2 seg[2];
+    const uint32_t t0 = blockIdx.x * kTile;
+    const uint32_t t1 = min(t0 + kTile, n);
+    if (threadIdx.x < 2) {
+        const uint32_t v = keys[threadIdx.x == 0 ? t0 : t1 - 1];
+        const uint2 inf = vt_find(sb.vt, sb.vmask, v);  // {deg, start}
+        seg[threadIdx.x] = make_uint2(inf.y, inf.y + inf.x);
     }
-    return lo;
-}
-
-// segments of > kChunk arcs: merge the sorted chunks by rank (values are distinct)
-__global__ void __launch_bounds__(256) k_merge_chunks(const uint4 *__restrict__ chunks, const uint32_t *__restrict__ segU,
-                                                      uint32_t *__restrict__ segS, uint2 *__restrict__ einfo2,
-                                                      const uint32_t *ctr) {
-    if (ctr[3]) return;
-    const uint32_t nch = ctr[2];
-    for (uint32_t c = blockIdx.x; c < nch; c += gridDim.x) {
-        const uint4 d = chunks[c];
-        const uint32_t start = d.x, deg = d.y, ci = d.z;
-        if (deg <= kChunk) continue;
-        const uint32_t nchunks = (deg + kChunk - 1) / kChunk;
-        const uint32_t base = start + ci * kChunk;
-        const uint32_t n = min(kChunk, deg - ci * kChunk);
-        for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-            const uint32_t v = segU[base + i];
-            uint32_t pos = i;
-            for (uint32_t cj = 0; cj < nchunks; ++cj) {
-                if (cj == ci) continue;
-                pos += lower_bound_u32(segU + start + cj * kChunk, min(kChunk, deg - cj * kChunk), v);
-            }
-            segS[start + pos] = v;
-            einfo2[v] = make_uint2(start + pos, start + deg);
-        }
+    __syncthreads();
+    for (uint32_t q = 0; q < 2; ++q) {
+        const uint2 sgm = seg[q];
+        if (sgm.x >= t0 && sgm.y <= t1) continue;   // tile-internal: done by k_runs
+        if (q == 1 && seg[0].x == sgm.x) continue;  // same segment as q == 0
+        const uint32_t lo = max(sgm.x, t0), hi = min(sgm.y, t1);
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += kSortThreads) sb.einfo2[vals[i]] = make_uint2(i, sgm.y);
     }
 }
 
@@ -455,12 +403,11 @@ __global__ void __launch_bounds__(256) k_merge_chunks(const uint4 *__restrict__ 
 struct UpdateIdx {
     const uint2 *E;
     const uint4 *einfo;
-    const uint32_t *vkey;
-    const uint2 *vinfo;
+    const VSlot *vt;
     uint32_t vmask;
-    const uint32_t *segS;
-    const unsigned long long *pkey;
-    const uint32_t *ppos;
+    const uint32_t *valA, *valB;  // the sorted arc values (segS) live in one of them
+    const uint32_t *hist;
+    const PSlot *pt;
     uint32_t pmask;
     const uint32_t *ctr;
 };
@@ -470,7 +417,8 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
                                                 uint64_t *__restrict__ p2s, uint64_t count, uint64_t first,
                                                 uint64_t seed, uint32_t batch, uint64_t m_prev, uint32_t w,
                                                 UpdateIdx ix, unsigned long long *S, unsigned long long *stats) {
-    if (ix.ctr[3]) return;
+    if (ix.ctr[kCtrErr]) return;
+    const uint32_t *__restrict__ segS = (passes_executed(ix.hist, kPasses, 2 * w) & 1u) ? ix.valB : ix.valA;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long contrib = 0;
     uint32_t n_fresh = 0, n_r2old = 0;
@@ -505,8 +453,8 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
             c = cf_old & kCMask;
             closed = (cf_old & kClosedBit) != 0;
             // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
-            const uint2 iu = vt_find(ix.vkey, ix.vinfo, ix.vmask, r1.x);
-            const uint2 iv = vt_find(ix.vkey, ix.vinfo, ix.vmask, r1.y);
+            const uint2 iu = vt_find(ix.vt, ix.vmask, r1.x);
+            const uint2 iv = vt_find(ix.vt, ix.vmask, r1.y);
             ld = iu.x;
             rd = iv.x;
             endU = iu.y + iu.x;
@@ -524,7 +472,7 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
                 const uint32_t phi = (uint32_t)(d2 - c);
                 const uint32_t end = phi < ld ? endU : endV;
                 const uint32_t a = phi < ld ? phi : phi - ld;
-                const uint32_t val = __ldg(ix.segS + (end - 1u - a));
+                const uint32_t val = __ldg(segS + (end - 1u - a));
                 k2 = val >> 1;
                 r2 = __ldg(ix.E + k2);
                 r2new = true;
@@ -537,7 +485,7 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
             if (!r2new) r2 = __ldcs(r2s + t);
             const uint32_t x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;  // f1's endpoint not on f2
             const uint32_t z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;  // f2's endpoint not on f1
-            const int64_t kk = pt_find(ix.pkey, ix.ppos, ix.pmask, pair_key(min(x, z), max(x, z)));
+            const int64_t kk = pt_find(ix.pt, ix.pmask, pair_key(min(x, z), max(x, z)));
             if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
         }
         const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
@@ -584,7 +532,7 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
             if (f) atomicAdd(stats + 0, (unsigned long long)f);
             if (q) atomicAdd(stats + 1, (unsigned long long)q);
             if (blockIdx.x == 0) {
-                atomicAdd(stats + 2, (unsigned long long)ix.ctr[0]);
+                atomicAdd(stats + 2, (unsigned long long)ix.ctr[kCtrD]);
                 atomicAdd(stats + 3, 1ull);
             }
         }
@@ -592,31 +540,29 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
 }
 
 // Empty exactly the table slots this batch used (runs even when the batch was rejected).
-__global__ void __launch_bounds__(256) k_clear(uint32_t *__restrict__ vkey, uint2 *__restrict__ vinfo,
-                                               const uint32_t *__restrict__ vlist, unsigned long long *__restrict__ pkey,
-                                               const uint32_t *__restrict__ pslot, uint32_t w, const uint32_t *ctr) {
-    const uint32_t D = ctr[0];
+__global__ void __launch_bounds__(256) k_clear(VSlot *__restrict__ vt, const uint32_t *__restrict__ vlist,
+                                               PSlot *__restrict__ pt, const uint32_t *__restrict__ pslot, uint32_t w,
+                                               const uint32_t *ctr) {
+    const uint32_t D = ctr[kCtrD];
     const uint32_t n = max(D, w);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (i < D) {
-            const uint32_t s = vlist[i];
-            vkey[s] = kEmptyV;
-            vinfo[s] = make_uint2(0u, 0u);
-        }
+        if (i < D) reinterpret_cast<uint4 *>(vt)[vlist[i]] = make_uint4(kEmptyV, 0u, 0xFFFFFFFFu, 0u);
         if (i < w) {
             const uint32_t s = pslot[i];
-            if (s != kNoSlot) pkey[s] = kEmptyP;
+            if (s != kNoSlot) pt[s].key = kEmptyP;
         }
     }
 }
 
-__global__ void k_init_tables(uint32_t *vkey, uint2 *vinfo, uint64_t vn, unsigned long long *pkey, uint64_t pn) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < max(vn, pn); i += (uint64_t)gridDim.x * blockDim.x) {
-        if (i < vn) {
-            vkey[i] = kEmptyV;
-            vinfo[i] = make_uint2(0u, 0u);
+__global__ void k_init_tables(VSlot *vt, uint64_t vn, PSlot *pt, uint64_t pn) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < max(vn, pn);
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        if (i < vn) reinterpret_cast<uint4 *>(vt)[i] = make_uint4(kEmptyV, 0u, 0xFFFFFFFFu, 0u);
+        if (i < pn) {
+            pt[i].key = kEmptyP;
+            pt[i].pos = 0;
+            pt[i].pad = 0;
         }
-        if (i < pn) pkey[i] = kEmptyP;
     }
 }
 
@@ -659,53 +605,46 @@ static inline uint32_t grid_for(uint64_t items, uint32_t threads, uint32_t per_s
 }
 
 int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    StageCtx c{ix.E, ix.arcrec, ix.pslot, ix.vkey, ix.vinfo, ix.vmask, ix.pkey, ix.ppos, ix.pmask, ix.ctr};
+    StageCtx c{ix.E, ix.keyA, ix.valA, ix.hist, ix.pt, ix.pmask, ix.pslot, ix.ctr};
     k_stage<<<grid_for((a.w + 1) / 2, 256, 8), 256, 0, s>>>(a.in, a.w, c);
     return 1;
 }
 
-int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint64_t nslots = (uint64_t)ix.vmask + 1;
-    k_segment<<<grid_for(nslots / kVBucket, 256, 4), 256, 0, s>>>(ix.vkey, ix.vinfo, (uint32_t)nslots, ix.vlist,
-                                                                  ix.midlist, ix.chunks, ix.ctr);
-    return 1;
-}
-
-int launch_scatter(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    k_scatter<<<grid_for(a.w, 256, 8), 256, 0, s>>>(ix.arcrec, ix.vinfo, ix.segU, a.w, ix.ctr);
-    return 1;
-}
-
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    uint2 *einfo2 = reinterpret_cast<uint2 *>(ix.einfo);
-    k_order_tiny<<<grid_for(2ull * a.w, 256, 8), 256, 0, s>>>(ix.vlist, ix.vinfo, ix.segU, ix.segS, einfo2, ix.ctr);
-    const uint32_t mid_bound = (uint32_t)(2ull * a.w / (kTinySeg + 1) + 1);
-    k_order_mid<<<grid_for(mid_bound, 8, 8), 256, 0, s>>>(ix.midlist, ix.vinfo, ix.segU, ix.segS, einfo2, ix.ctr);
-    const uint32_t chunk_bound =
-        (uint32_t)std::min<uint64_t>(ix.chunk_cap, 2ull * a.w / (kMidSeg + 1) + 2ull * a.w / kChunk + 1);
-    const uint32_t g = std::max<uint32_t>(1, std::min<uint32_t>(chunk_bound, sm_count() * 4));
-    k_sort_chunks<<<g, 512, 0, s>>>(ix.chunks, ix.segU, ix.segS, einfo2, ix.ctr);
-    k_merge_chunks<<<g, 256, 0, s>>>(ix.chunks, ix.segU, ix.segS, einfo2, ix.ctr);
-    return 4;
+    const uint32_t n = 2 * a.w;
+    const uint32_t tiles = (n + kTile - 1) / kTile;
+    RadixBufs rb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.look, ix.ctr};
+    for (uint32_t p = 0; p < kPasses; ++p) k_radix_pass<<<tiles, kSortThreads, 0, s>>>(rb, n, p, a.seq + p);
+    return (int)kPasses;
+}
+
+int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    const uint32_t n = 2 * a.w;
+    const uint32_t tiles = (n + kTile - 1) / kTile;
+    SegBufs sb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.vt, ix.vmask,
+               reinterpret_cast<uint2 *>(ix.einfo), ix.vlist, ix.ctr};
+    k_runs<<<tiles, kSortThreads, 0, s>>>(sb, n);
+    k_fix<<<tiles, kSortThreads, 0, s>>>(sb, n);
+    return 2;
 }
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
     if (st.count == 0) return 0;
     const uint64_t blocks = (st.count + 255) / 256;
-    UpdateIdx u{ix.E, ix.einfo, ix.vkey, ix.vinfo, ix.vmask, ix.segS, ix.pkey, ix.ppos, ix.pmask, ix.ctr};
+    UpdateIdx u{ix.E, ix.einfo, ix.vt, ix.vmask, ix.valA, ix.valB, ix.hist, ix.pt, ix.pmask, ix.ctr};
     k_update<<<(uint32_t)blocks, 256, 0, s>>>(st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch,
                                               a.m_prev, a.w, u, st.S + a.S_slot, st.stats);
     return 1;
 }
 
 int launch_clear(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    k_clear<<<grid_for(2ull * a.w, 256, 8), 256, 0, s>>>(ix.vkey, ix.vinfo, ix.vlist, ix.pkey, ix.pslot, a.w, ix.ctr);
+    k_clear<<<grid_for(2ull * a.w, 256, 8), 256, 0, s>>>(ix.vt, ix.vlist, ix.pt, ix.pslot, a.w, ix.ctr);
     return 1;
 }
 
 int launch_init_tables(const IndexBufs &ix, cudaStream_t s) {
     const uint64_t vn = (uint64_t)ix.vmask + 1, pn = (uint64_t)ix.pmask + 1;
-    k_init_tables<<<grid_for(std::max(vn, pn), 256, 16), 256, 0, s>>>(ix.vkey, ix.vinfo, vn, ix.pkey, pn);
+    k_init_tables<<<grid_for(std::max(vn, pn), 256, 16), 256, 0, s>>>(ix.vt, vn, ix.pt, pn);
     return 1;
 }
 

@@ -11,23 +11,20 @@ namespace tcb {
 struct IndexBufs {
     uint64_t wcap = 0;         // edges the buffers hold
     uint2 *E = nullptr;        // [wcap] normalized edges
-    uint4 *arcrec = nullptr;   // [wcap] {vslot_lo, ticket_lo, vslot_hi, ticket_hi}
-    uint32_t *pslot = nullptr; // [wcap] pair-table slot of edge k (kNoSlot if not inserted)
-    uint32_t *segU = nullptr;  // [2 wcap] arcs grouped by vertex, arbitrary order inside a group
-    uint32_t *segS = nullptr;  // [2 wcap] arcs grouped by vertex, ascending k inside a group
+    uint32_t *keyA = nullptr, *valA = nullptr;  // [2 wcap] radix ping-pong buffers: arc vertex / arc value
+    uint32_t *keyB = nullptr, *valB = nullptr;
+    uint32_t *hist = nullptr;  // [kPasses * kRadix] digit histograms of the arc keys
+    unsigned long long *look = nullptr;  // [tiles * kRadix] decoupled look-back words
+    uint64_t look_tiles = 0;
     uint4 *einfo = nullptr;    // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
-    uint32_t *vkey = nullptr;  // [vmask+1] vertex ids (kEmptyV = free)
-    uint2 *vinfo = nullptr;    // [vmask+1] {deg_W, segment start}
+    VSlot *vt = nullptr;       // [vmask+1]
     uint32_t vmask = 0;
-    unsigned long long *pkey = nullptr;  // [pmask+1] lo<<32|hi (kEmptyP = free)
-    uint32_t *ppos = nullptr;            // [pmask+1] batch position k
+    PSlot *pt = nullptr;       // [pmask+1]
     uint32_t pmask = 0;
-    uint32_t *vlist = nullptr;  // [2 wcap] occupied vertex slots, compact (D of them)
-    uint32_t *midlist = nullptr;  // [2 wcap / (kTinySeg+1)] vertex slots with kTinySeg < deg <= kMidSeg
-    uint4 *chunks = nullptr;    // big-segment chunk descriptors {start, deg, chunk, 0}
-    uint64_t chunk_cap = 0;
-    uint32_t *ctr = nullptr;    // device counters: [0] D, [1] arc cursor, [2] chunks, [3] err, [4] mid
-    uint2 *stage = nullptr;     // [wcap] H2D staging for host batches
+    uint32_t *pslot = nullptr; // [wcap] pair-table slot of edge k (kNoSlot if not inserted)
+    uint32_t *vlist = nullptr; // [2 wcap] claimed vertex-table slots (D of them)
+    uint32_t *ctr = nullptr;   // device counters (index.cuh kCtr*)
+    uint2 *stage = nullptr;    // [wcap] H2D staging for host batches
 };
 
 struct StateBufs {
@@ -44,6 +41,7 @@ struct BatchArgs {
     uint32_t w;
     uint64_t m_prev;
     uint32_t batch;  // index b of this (non-empty) batch
+    uint32_t seq;    // look-back sequence base (kPasses values per batch, never reused)
     uint64_t first;  // global id of local estimator 0
     uint64_t seed;
     int S_slot;
@@ -51,9 +49,8 @@ struct BatchArgs {
 
 // Each returns the number of kernel launches issued.
 int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
-int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
-int launch_scatter(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
+int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s);
 int launch_clear(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_init_tables(const IndexBufs &ix, cudaStream_t s);
