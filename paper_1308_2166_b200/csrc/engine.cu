@@ -85,7 +85,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
     const uint64_t pslots = next_pow2(4 * cap);  // w pairs: load <= 25%
-    ix.look_tiles = (2 * cap + kTile - 1) / kTile;
+    ix.look_tiles = (2 * cap + kRadixTile - 1) / kRadixTile;
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyA, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valA, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyB, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valB, 8 * cap) == cudaSuccess &&

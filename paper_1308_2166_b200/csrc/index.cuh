@@ -34,8 +34,10 @@ constexpr uint32_t kRadixBits = 8;
 constexpr uint32_t kRadix = 1u << kRadixBits;
 constexpr uint32_t kPasses = 32 / kRadixBits;
 constexpr uint32_t kSortThreads = 256;
-constexpr uint32_t kSortItems = 8;
-constexpr uint32_t kTile = kSortThreads * kSortItems;  // arcs per tile
+constexpr uint32_t kSortItems = 16;
+constexpr uint32_t kRadixTile = kSortThreads * kSortItems;  // arcs per radix tile
+constexpr uint32_t kRunItems = 8;
+constexpr uint32_t kTile = kSortThreads * kRunItems;  // arcs per segment tile (k_runs / k_fix)
 
 // device counters (ctr[])
 constexpr int kCtrD = 0;       // vertices of W (claimed vertex-table slots)

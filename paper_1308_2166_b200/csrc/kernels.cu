@@ -41,36 +41,43 @@ struct StageCtx {
     uint32_t *ctr;
 };
 
-// Insert (lo, hi) -> k; false if the pair is already present (an in-batch duplicate).
-__device__ __forceinline__ bool pair_insert(const StageCtx &c, unsigned long long key, uint32_t k) {
-    uint32_t b = hash_pair(key) & c.pmask & ~1u;
-    while (true) {
-        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + b);
-        const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
-        if (s0.x == key || s1.x == key) {
-            c.pslot[k] = kNoSlot;
-            return false;
-        }
-        const uint32_t e = s0.x == kEmptyP ? 0u : s1.x == kEmptyP ? 1u : 2u;
-        if (e == 2u) {
-            b = (b + 2) & c.pmask;
-            continue;
-        }
-        const unsigned long long old = atomicCAS(&c.pt[b + e].key, kEmptyP, key);
-        if (old == kEmptyP) {
-            c.pt[b + e].pos = k;
-            c.pslot[k] = b + e;
-            return true;
-        }
-        if (old == key) {
-            c.pslot[k] = kNoSlot;
-            return false;
-        }
-        // another pair took the slot: re-read the bucket
+// An in-flight edge-pair insert (lo, hi) -> k.
+struct PIns {
+    unsigned long long key;
+    uint32_t b, k;
+    bool armed, done, dup;
+};
+
+// One probe step: read the 2-slot bucket (one sector), CAS the first free key if the pair is absent.
+__device__ __forceinline__ void pins_step(const StageCtx &c, PIns &s) {
+    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + s.b);
+    const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
+    if (s0.x == s.key || s1.x == s.key) {
+        s.done = s.dup = true;
+        return;
     }
+    const uint32_t e = s0.x == kEmptyP ? 0u : s1.x == kEmptyP ? 1u : 2u;
+    if (e == 2u) {
+        s.b = (s.b + 2) & c.pmask;
+        return;
+    }
+    const unsigned long long old = atomicCAS(&c.pt[s.b + e].key, kEmptyP, s.key);
+    if (old == kEmptyP) {
+        s.b += e;
+        s.done = true;
+    } else if (old == s.key) {
+        s.done = s.dup = true;
+    }
+    // else: another pair took the slot; re-read the bucket
 }
 
-__device__ __forceinline__ uint32_t stage_one(const StageCtx &c, uint2 e, uint32_t k, uint32_t (*sh)[kRadix]) {
+// Validate + normalize one edge, emit its arcs and digit counts, arm its pair insert; returns error bits.
+__device__ __forceinline__ uint32_t stage_edge(const StageCtx &c, uint2 e, uint32_t k, uint32_t (*sh)[kRadix],
+                                               PIns &q) {
+    q.k = k;
+    q.armed = false;
+    q.done = true;
+    q.dup = false;
     if (e.x == kEmptyV || e.y == kEmptyV || e.x == e.y) {
         c.pslot[k] = kNoSlot;
         return (e.x == kEmptyV || e.y == kEmptyV) ? kErrInval : kErrLoop;
@@ -84,7 +91,22 @@ __device__ __forceinline__ uint32_t stage_one(const StageCtx &c, uint2 e, uint32
         atomicAdd(&sh[p][(lo >> (p * kRadixBits)) & (kRadix - 1)], 1u);
         atomicAdd(&sh[p][(hi >> (p * kRadixBits)) & (kRadix - 1)], 1u);
     }
-    return pair_insert(c, pair_key(lo, hi), k) ? 0u : kErrDup;
+    q.key = pair_key(lo, hi);
+    q.b = hash_pair(q.key) & c.pmask & ~1u;
+    q.armed = true;
+    q.done = false;
+    return 0u;
+}
+
+__device__ __forceinline__ uint32_t pins_finish(const StageCtx &c, const PIns &q) {
+    if (!q.armed) return 0u;
+    if (q.dup) {
+        c.pslot[q.k] = kNoSlot;
+        return kErrDup;
+    }
+    c.pt[q.b].pos = q.k;
+    c.pslot[q.k] = q.b;
+    return 0u;
 }
 
 __global__ void __launch_bounds__(256) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
@@ -94,17 +116,32 @@ __global__ void __launch_bounds__(256) k_stage(const uint2 *__restrict__ in, uin
     __syncthreads();
     uint32_t bad = 0;
     const uint32_t stride = gridDim.x * blockDim.x;
-    if ((reinterpret_cast<uintptr_t>(in) & 15u) == 0) {
-        const uint32_t npairs = w >> 1;
-        const uint4 *in4 = reinterpret_cast<const uint4 *>(in);
-        for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < npairs; q += stride) {
+    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15u) == 0;
+    const uint4 *in4 = reinterpret_cast<const uint4 *>(in);
+    // two edges per thread per iteration; their hash inserts are stepped together (2 round trips in flight)
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; 2 * q < w; q += stride) {
+        const bool has1 = 2 * q + 1 < w;
+        uint2 e0, e1 = make_uint2(0u, 0u);
+        if (vec && has1) {
             const uint4 two = __ldcs(in4 + q);
-            bad |= stage_one(c, make_uint2(two.x, two.y), 2 * q, sh);
-            bad |= stage_one(c, make_uint2(two.z, two.w), 2 * q + 1, sh);
+            e0 = make_uint2(two.x, two.y);
+            e1 = make_uint2(two.z, two.w);
+        } else {
+            e0 = in[2 * q];
+            if (has1) e1 = in[2 * q + 1];
         }
-        if ((w & 1u) && blockIdx.x * blockDim.x + threadIdx.x == 0) bad |= stage_one(c, in[w - 1], w - 1, sh);
-    } else {
-        for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < w; k += stride) bad |= stage_one(c, in[k], k, sh);
+        PIns a, b;
+        bad |= stage_edge(c, e0, 2 * q, sh, a);
+        b.armed = false;
+        b.done = true;
+        b.dup = false;
+        if (has1) bad |= stage_edge(c, e1, 2 * q + 1, sh, b);
+        while (!(a.done && b.done)) {
+            if (!a.done) pins_step(c, a);
+            if (!b.done) pins_step(c, b);
+        }
+        bad |= pins_finish(c, a);
+        bad |= pins_finish(c, b);
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && (threadIdx.x & 31u) == 0) atomicOr(&c.ctr[kCtrErr], bad);
@@ -156,7 +193,7 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_pass(RadixBufs rb, uint3
     if (threadIdx.x == 0) tile_sh = atomicAdd(&rb.ctr[kCtrTile + pass], 1u);  // dynamic tile order
     __syncthreads();
     const uint32_t tile = tile_sh;
-    const uint32_t wbase = tile * kTile + warp * (32 * kSortItems);
+    const uint32_t wbase = tile * kRadixTile + warp * (32 * kSortItems);
 
     // stable in-tile ranks: warp w owns a contiguous 256-arc range, processed in 8 rounds of 32
     uint32_t keys[kSortItems], vals[kSortItems], rnk[kSortItems];
@@ -199,14 +236,21 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_pass(RadixBufs rb, uint3
         atomicExch(lk, ((tag | kFlagPrefix) << 32) | total);
     } else {
         atomicExch(lk, ((tag | kFlagAgg) << 32) | total);
-        for (int32_t t = (int32_t)tile - 1; t >= 0; --t) {
-            const volatile unsigned long long *q = rb.look + (size_t)t * kRadix + dgt;
-            unsigned long long v;
-            do {
-                v = *q;
-            } while ((v >> 34) != seq || ((v >> 32) & 3ull) == 0ull);
-            excl += (uint32_t)v;
-            if (((v >> 32) & 3ull) == kFlagPrefix) break;
+        // walk back in windows of 8 predecessors (8 independent loads in flight)
+        bool found = false;
+        for (int32_t t = (int32_t)tile - 1; t >= 0 && !found; t -= 8) {
+            unsigned long long v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                v[u] = t - u >= 0 ? *(const volatile unsigned long long *)(rb.look + (size_t)(t - u) * kRadix + dgt) : 0ull;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (found || t - u < 0) break;
+                while ((v[u] >> 34) != seq || ((v[u] >> 32) & 3ull) == 0ull)
+                    v[u] = *(const volatile unsigned long long *)(rb.look + (size_t)(t - u) * kRadix + dgt);
+                excl += (uint32_t)v[u];
+                found = ((v[u] >> 32) & 3ull) == kFlagPrefix;
+            }
         }
         atomicExch(lk, ((tag | kFlagPrefix) << 32) | (excl + total));
     }
@@ -298,10 +342,10 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     }
     __syncthreads();
     // local run heads (inside the tile) -> run ids by a block scan
-    const uint32_t i0 = threadIdx.x * kSortItems;
+    const uint32_t i0 = threadIdx.x * kRunItems;
     uint32_t heads = 0;
 #pragma unroll
-    for (uint32_t e = 0; e < kSortItems; ++e) {
+    for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
         if (i < tn && (i == 0 || skey[i + 1] != skey[i])) ++heads;
     }
@@ -319,11 +363,11 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
         if (x < warp) wpre += wsum[x];
         nruns += wsum[x];
     }
-    uint32_t rid[kSortItems];
+    uint32_t rid[kRunItems];
     {
         uint32_t r = wpre + incl - heads;  // runs started before this thread's first arc
 #pragma unroll
-        for (uint32_t e = 0; e < kSortItems; ++e) {
+        for (uint32_t e = 0; e < kRunItems; ++e) {
             const uint32_t i = i0 + e;
             if (i < tn && (i == 0 || skey[i + 1] != skey[i])) {
                 run_start[r] = i;
@@ -365,7 +409,7 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     }
     // arcs of tile-internal segments: einfo = {sorted slot, segment end}
 #pragma unroll
-    for (uint32_t e = 0; e < kSortItems; ++e) {
+    for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
         if (i < tn) {
             const uint32_t end = run_end[rid[e]];
@@ -412,7 +456,7 @@ struct UpdateIdx {
     const uint32_t *ctr;
 };
 
-__global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *__restrict__ r2s,
+__global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint2 *__restrict__ r2s,
                                                 uint32_t *__restrict__ cfs, uint64_t *__restrict__ p1s,
                                                 uint64_t *__restrict__ p2s, uint64_t count, uint64_t first,
                                                 uint64_t seed, uint32_t batch, uint64_t m_prev, uint32_t w,
@@ -432,7 +476,7 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
         // ---- Step 1: level-1 reservoir ----
         const uint64_t d1 = bounded(m_prev + w, xlo, dc, 0x10000u);
         const bool fresh = d1 >= m_prev;
-        uint2 r1;
+        uint2 r1, r2 = make_uint2(kEmptyV, kEmptyV);
         uint32_t c, cf_old = 0;
         bool closed;
         uint32_t ld, rd, endU, endV;
@@ -450,6 +494,7 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
         } else {
             r1 = __ldcs(r1s + t);
             cf_old = __ldcs(cfs + t);
+            r2 = __ldcs(r2s + t);  // issued early: needed by Step 3 when f2 is kept
             c = cf_old & kCMask;
             closed = (cf_old & kClosedBit) != 0;
             // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
@@ -462,7 +507,6 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
         }
         const uint32_t chi_p = ld + rd;  // |Gamma_W(f1)| = rank(u->v) + rank(v->u)
         bool r2new = false;
-        uint2 r2 = make_uint2(kEmptyV, kEmptyV);
         uint32_t k2 = 0;
         const bool had_r2 = !fresh && c > 0;  // NBSI: chi == 0 <=> f2 empty
         if (chi_p) {
@@ -482,7 +526,6 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
         }
         // ---- Step 3: closing edge after f2 ----
         if ((r2new || had_r2) && !closed) {
-            if (!r2new) r2 = __ldcs(r2s + t);
             const uint32_t x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;  // f1's endpoint not on f2
             const uint32_t z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;  // f2's endpoint not on f1
             const int64_t kk = pt_find(ix.pt, ix.pmask, pair_key(min(x, z), max(x, z)));
@@ -539,18 +582,28 @@ __global__ void __launch_bounds__(256) k_update(uint2 *__restrict__ r1s, uint2 *
     }
 }
 
-// Empty exactly the table slots this batch used (runs even when the batch was rejected).
+// Empty exactly the table slots this batch used (runs even when the batch was rejected).  Four
+// independent index loads per thread before the scattered stores.
 __global__ void __launch_bounds__(256) k_clear(VSlot *__restrict__ vt, const uint32_t *__restrict__ vlist,
                                                PSlot *__restrict__ pt, const uint32_t *__restrict__ pslot, uint32_t w,
                                                const uint32_t *ctr) {
     const uint32_t D = ctr[kCtrD];
-    const uint32_t n = max(D, w);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        if (i < D) reinterpret_cast<uint4 *>(vt)[vlist[i]] = make_uint4(kEmptyV, 0u, 0xFFFFFFFFu, 0u);
-        if (i < w) {
-            const uint32_t s = pslot[i];
-            if (s != kNoSlot) pt[s].key = kEmptyP;
-        }
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += 4 * stride) {
+        uint32_t s[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = i + u * stride < D ? __ldcs(vlist + i + u * stride) : kNoSlot;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (s[u] != kNoSlot) reinterpret_cast<uint4 *>(vt)[s[u]] = make_uint4(kEmptyV, 0u, 0xFFFFFFFFu, 0u);
+    }
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < w; i += 4 * stride) {
+        uint32_t s[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[u] = i + u * stride < w ? __ldcs(pslot + i + u * stride) : kNoSlot;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (s[u] != kNoSlot) pt[s[u]].key = kEmptyP;
     }
 }
 
@@ -612,7 +665,7 @@ int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const uint32_t n = 2 * a.w;
-    const uint32_t tiles = (n + kTile - 1) / kTile;
+    const uint32_t tiles = (n + kRadixTile - 1) / kRadixTile;
     RadixBufs rb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.look, ix.ctr};
     for (uint32_t p = 0; p < kPasses; ++p) k_radix_pass<<<tiles, kSortThreads, 0, s>>>(rb, n, p, a.seq + p);
     return (int)kPasses;
