@@ -127,21 +127,18 @@ def algorithmic_bytes(phase, w, R, D, fresh, r2old):
     update : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
              (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
              index probes are L2 traffic at C2 and not counted.
-    stage  : read 8 B/edge; write E 8 + arcs 16 + pair slot 16 + pair-slot list 4 B/edge.
+    stage  : read 8 B/edge (twice: histogram + stage); write E 8 + arcs 16 + pair slot 16 B/edge.
     sort   : the 2 arcs of an edge read and written once (32 B/edge); extra radix passes are overhead.
     segment: read sorted arcs 16 + write rank/end 16 B/edge; 16 B per vertex-table entry.
-    clear  : 20 B per distinct vertex (list + slot) and 12 B/edge (list + pair key).
     """
     if phase == "update":
         return 24 * (R - fresh) + 36 * fresh + 16 * r2old
     if phase == "stage":
-        return 52 * w
+        return 56 * w
     if phase == "sort":
         return 32 * w
     if phase == "segment":
         return 32 * w + 16 * D
-    if phase == "clear":
-        return 20 * D + 12 * w
     raise KeyError(phase)
 
 
@@ -269,7 +266,6 @@ def run_b200(args):
         "stage": algorithmic_bytes("stage", edges_done, 0, D, 0, 0),
         "sort": algorithmic_bytes("sort", edges_done, 0, 0, 0, 0),
         "segment": algorithmic_bytes("segment", edges_done, 0, D, 0, 0),
-        "clear": algorithmic_bytes("clear", edges_done, 0, D, 0, 0),
     }
     dom_secs = prof[dom][0] / 1e3
     achieved = total_alg[dom] / dom_secs / 1e9 if dom_secs > 0 else None

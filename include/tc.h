@@ -123,12 +123,12 @@ void *tc_stream(tc_ctx *ctx);
  * tc_profile_read fills, for phase p < n (TC_PHASE_*): total milliseconds and launch count since
  * the last reset, and returns the number of phases.  Synchronises. */
 enum {
-    TC_PHASE_STAGE = 0,   /* a1+a3: staging, validation, arcs + digit histograms, edge-pair hash  */
-    TC_PHASE_SORT = 1,    /* a2: stable radix sort of the arcs by vertex (arrival order kept)    */
+    TC_PHASE_STAGE = 0,   /* a1+a3: digit histograms, staging, validation, edge-pair hash, arcs
+                             ranked by radix digit 0                                            */
+    TC_PHASE_SORT = 1,    /* a2: remaining stable radix passes of the arcs by vertex             */
     TC_PHASE_SEGMENT = 2, /* a2: vertex table {deg_W, start}, per-arc rank / segment end         */
     TC_PHASE_UPDATE = 3,  /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)       */
-    TC_PHASE_CLEAR = 4,   /* freeing the table slots the batch used                             */
-    TC_NPHASES = 5
+    TC_NPHASES = 4
 };
 int tc_profile(tc_ctx *ctx, int enable);
 int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n);

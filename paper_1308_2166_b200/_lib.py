@@ -17,8 +17,8 @@ TC_EDUP = -4
 TC_EOVERFLOW = -5
 TC_ECUDA = -6
 TC_ESTATE = -8
-TC_NPHASES = 5
-PHASES = ("stage", "sort", "segment", "update", "clear")
+TC_NPHASES = 4
+PHASES = ("stage", "sort", "segment", "update")
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_sync",

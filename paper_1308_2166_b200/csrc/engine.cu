@@ -30,7 +30,7 @@ struct tc_ctx {
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
-    uint32_t seq = 1;  // look-back sequence numbers of the radix passes (kPasses per push)
+    uint32_t tag = 0;  // table tag of the last push (live slots carry the current push's tag)
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -65,12 +65,10 @@ static void free_index(IndexBufs &ix) {
     cudaFree(ix.keyB);
     cudaFree(ix.valB);
     cudaFree(ix.hist);
-    cudaFree(ix.look);
+    cudaFree(ix.cnt);
     cudaFree(ix.einfo);
     cudaFree(ix.vt);
     cudaFree(ix.pt);
-    cudaFree(ix.pslot);
-    cudaFree(ix.vlist);
     cudaFree(ix.ctr);
     cudaFree(ix.stage);
     ix = IndexBufs();
@@ -85,15 +83,14 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
     const uint64_t pslots = next_pow2(4 * cap);  // w pairs: load <= 25%
-    ix.look_tiles = (2 * cap + kRadixTile - 1) / kRadixTile;
+    ix.tiles_cap = (2 * cap + kRadixTile - 1) / kRadixTile;
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyA, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valA, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyB, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valB, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.hist, 4 * kPasses * kRadix) == cudaSuccess &&
-              cudaMalloc(&ix.look, 8 * kRadix * ix.look_tiles) == cudaSuccess &&
+              cudaMalloc(&ix.cnt, 4 * kRadix * ix.tiles_cap) == cudaSuccess &&
               cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
-              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.pslot, 4 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.vlist, 8 * cap) == cudaSuccess && cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess &&
               cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -103,10 +100,10 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     ix.vmask = (uint32_t)(vslots - 1);
     ix.pmask = (uint32_t)(pslots - 1);
     ix.wcap = cap;
-    launch_init_tables(ix, ctx->stream);  // all slots free; afterwards each batch frees its own slots
+    launch_init_tables(ix, ctx->stream);  // tag 0 everywhere: every slot free
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
-    CK(cudaMemsetAsync(ix.look, 0, 8 * kRadix * ix.look_tiles, ctx->stream));  // sequence 0 = never written
+    ctx->tag = 0;
     return TC_OK;
 }
 
@@ -278,17 +275,15 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.first = ctx->first;
     a.seed = ctx->seed;
     a.S_slot = slot;
-    a.seq = ctx->seq;
-    ctx->seq += kPasses;
-    if (ctx->seq >= (1u << 29)) {  // look-back tags are 30 bits: restart them on a zeroed array
-        CK(cudaMemsetAsync(ix.look, 0, 8 * kRadix * ix.look_tiles, ctx->stream));
-        a.seq = 1;
-        ctx->seq = 1 + kPasses;
+    if (++ctx->tag == 0xFFFFFFFFu) {  // never reuse a tag a slot may still carry: free every slot
+        launch_init_tables(ix, ctx->stream);
+        ctx->tag = 1;
     }
+    a.tag = ctx->tag;
     uint32_t launches = 0;
     int n;
     int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {
-        launch_stage, launch_sort, launch_segment, nullptr, launch_clear};
+        launch_stage, launch_sort, launch_segment, nullptr};
     for (int p = 0; p < TC_NPHASES; ++p) {
         n = phase_fn[p] ? phase_fn[p](ix, a, ctx->stream) : launch_update(ix, ctx->st, a, ctx->stream);
         launches += n;

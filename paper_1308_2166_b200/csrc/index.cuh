@@ -7,19 +7,18 @@
 //             Fig. 4 read backwards inside each src group (src asc, pos desc <=> rank asc,
 //             PAPER.md:730-734), so rank(x->y) of the arc at sorted slot s is segEnd(x) - 1 - s
 //             (Definition Rank).  segS = the sorted value array.
-//   vertex table (open addressing, 16 B slots, 2 per 32 B sector): {x, deg_W(x), segment start, -}
+//   vertex table (open addressing, 16 B slots, 2 per 32 B sector): {x, deg_W(x), segment start, tag}
 //   einfo[k]  uint4 {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
-//   edge-pair hash (16 B slots, 2 per sector): {lo<<32 | hi, k}: Step 3's (src,dst)-sorted "edges"
+//   edge-pair hash (16 B slots, 2 per sector): {lo<<32 | hi, k, tag}: Step 3's (src,dst)-sorted "edges"
 //             array with its multisearch replaced by one O(1) probe
-// Both tables are emptied after every batch by clearing exactly the slots the batch used.
+// A slot is live only when its tag equals the batch's tag, so the tables are never cleared; a slot is
+// claimed with one 128-bit CAS that installs key, payload and tag together.
 #pragma once
 #include <cstdint>
 
 namespace tcb {
 
 constexpr uint32_t kEmptyV = 0xFFFFFFFFu;
-constexpr unsigned long long kEmptyP = ~0ull;
-constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
 constexpr uint32_t kClosedBit = 0x80000000u;
 constexpr uint32_t kCMask = 0x7FFFFFFFu;
 
@@ -35,22 +34,21 @@ constexpr uint32_t kRadix = 1u << kRadixBits;
 constexpr uint32_t kPasses = 32 / kRadixBits;
 constexpr uint32_t kSortThreads = 256;
 constexpr uint32_t kSortItems = 16;
-constexpr uint32_t kRadixTile = kSortThreads * kSortItems;  // arcs per radix tile
+constexpr uint32_t kRadixTile = kSortThreads * kSortItems;  // arcs per radix tile (= 2048 edges)
 constexpr uint32_t kRunItems = 8;
 constexpr uint32_t kTile = kSortThreads * kRunItems;  // arcs per segment tile (k_runs / k_fix)
 
 // device counters (ctr[])
-constexpr int kCtrD = 0;       // vertices of W (claimed vertex-table slots)
-constexpr int kCtrErr = 3;     // error bits
-constexpr int kCtrTile = 4;    // [4 .. 4+kPasses) dynamic tile ids of the radix passes
+constexpr int kCtrD = 0;    // vertices of W (claimed vertex-table slots)
+constexpr int kCtrErr = 3;  // error bits
 constexpr int kCtrWords = 16;
 
 struct __align__(16) VSlot {
-    uint32_t key, deg, start, pad;
+    uint32_t key, deg, start, tag;
 };
 struct __align__(16) PSlot {
     unsigned long long key;
-    uint32_t pos, pad;
+    uint32_t pos, tag;
 };
 
 __device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
@@ -78,27 +76,30 @@ __device__ __forceinline__ unsigned long long pair_key(uint32_t lo, uint32_t hi)
 
 // Probe the complete (read-only) vertex table: {deg_W(v), segment start}, or {0, 0} when v is not in W.
 // One probe = one 32-byte sector holding two slots.
-__device__ __forceinline__ uint2 vt_find(const VSlot *__restrict__ vt, uint32_t mask, uint32_t v) {
+__device__ __forceinline__ uint2 vt_find(const VSlot *__restrict__ vt, uint32_t mask, uint32_t tag, uint32_t v) {
     uint32_t b = hash_vertex(v) & mask & ~1u;
     while (true) {
         const uint4 *p = reinterpret_cast<const uint4 *>(vt + b);
         const uint4 s0 = __ldg(p), s1 = __ldg(p + 1);
-        if (s0.x == v) return make_uint2(s0.y, s0.z);
-        if (s1.x == v) return make_uint2(s1.y, s1.z);
-        if (s0.x == kEmptyV || s1.x == kEmptyV) return make_uint2(0u, 0u);
+        const bool l0 = s0.w == tag, l1 = s1.w == tag;
+        if (l0 && s0.x == v) return make_uint2(s0.y, s0.z);
+        if (l1 && s1.x == v) return make_uint2(s1.y, s1.z);
+        if (!l0 || !l1) return make_uint2(0u, 0u);
         b = (b + 2) & mask;
     }
 }
 
 // Probe the complete (read-only) edge-pair hash: batch position of (lo, hi) or -1.
-__device__ __forceinline__ int64_t pt_find(const PSlot *__restrict__ pt, uint32_t mask, unsigned long long key) {
+__device__ __forceinline__ int64_t pt_find(const PSlot *__restrict__ pt, uint32_t mask, uint32_t tag,
+                                           unsigned long long key) {
     uint32_t b = hash_pair(key) & mask & ~1u;
     while (true) {
         const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(pt + b);
         const ulonglong2 s0 = __ldg(p), s1 = __ldg(p + 1);
-        if (s0.x == key) return (int64_t)(uint32_t)s0.y;
-        if (s1.x == key) return (int64_t)(uint32_t)s1.y;
-        if (s0.x == kEmptyP || s1.x == kEmptyP) return -1;
+        const bool l0 = (uint32_t)(s0.y >> 32) == tag, l1 = (uint32_t)(s1.y >> 32) == tag;
+        if (l0 && s0.x == key) return (int64_t)(uint32_t)s0.y;
+        if (l1 && s1.x == key) return (int64_t)(uint32_t)s1.y;
+        if (!l0 || !l1) return -1;
         b = (b + 2) & mask;
     }
 }

@@ -1,21 +1,22 @@
 // kernels.cu -- the per-batch hot path of bulkUpdateAll on sm_100a.
 //
-// Pipeline for one batch W:
-//   k_stage      a1 + a3 : load W (16-byte loads = 2 edges), validate, normalize to (lo, hi); emit the 2|W|
-//                          arcs (vertex, k<<1|side) in arrival order -- the F array of rankAll's proof
-//                           -- and their 8-bit digit histograms; insert the edge into
-//                          the edge-pair hash (one CAS round trip per probe; a repeat is TC_EDUP)
-//   k_radix_pass a2      : stable LSD radix pass over the arcs by vertex id (one kernel per 8-bit digit,
-//                          single sweep with decoupled look-back; passes whose digit is zero for every
-//                          arc are skipped on the device).  Stability keeps arrival order inside a vertex:
-//                          this replaces rankAll's sort by (src, -pos).
+// Pipeline for one batch W; tiles are 2048 edges = 4096 arcs:
+//   k_hist       a1      : per-tile counts of digit 0 of the arc keys, global histograms of all digits
+//   k_scan               : per digit, exclusive scan over tiles + digit base = each tile's output offsets
+//   k_stage      a1 + a3 : load W (coalesced), validate, normalize to (lo, hi); insert every edge into the
+//                          edge-pair hash (one 128-bit CAS per claim, 8 inserts in flight per thread);
+//                          rank the tile's arcs (vertex, k<<1|side) stably by digit 0 and scatter them --
+//                          the F array of rankAll's proof, already radix pass 0
+//   k_upsweep / k_scan / k_downsweep  a2 : the remaining stable LSD radix passes over the arcs by vertex id
+//                          (passes whose digit is 0 for every arc are skipped on the device).  Stability
+//                          keeps arrival order inside a vertex: this replaces rankAll's sort by (src, -pos)
+//                          (PAPER.md:680-684).
 //   k_runs       a2      : runs of equal vertex inside each tile -> vertex table {deg_W, segment start};
-//                          ranks/segment ends of the arcs of tile-internal segments
-//   k_fix        a2      : ranks/segment ends of the arcs of segments that cross tile boundaries
+//                          rank / segment end of the arcs of tile-internal segments
+//   k_fix        a2      : rank / segment end of the arcs of segments that cross tile boundaries
 //   k_update     a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2 (chi^+
 //                          from ranks / degrees, level-2 pick by segment arithmetic), Step 3 (closing-edge
 //                          probe), block partial sums of chi over closed estimators
-//   k_clear              : empties exactly the table slots this batch used
 // rank(x->y) of the arc at sorted slot s = segEnd(x) - 1 - s (Definition Rank).
 #include <cuda_runtime.h>
 
@@ -28,235 +29,117 @@
 
 namespace tcb {
 
-// ------------------------------------------------------------------------------------------------
-// a1 + a3: staging, arcs, digit histograms, edge-pair hash
+typedef unsigned __int128 u128;
 
-struct StageCtx {
-    uint2 *E;
-    uint32_t *key, *val;  // arcs out (radix buffer A)
-    uint32_t *hist;       // [kPasses][kRadix]
-    PSlot *pt;
-    uint32_t pmask;
-    uint32_t *pslot;
-    uint32_t *ctr;
-};
-
-// An in-flight edge-pair insert (lo, hi) -> k.
-struct PIns {
-    unsigned long long key;
-    uint32_t b, k;
-    bool armed, done, dup;
-};
-
-// One probe step: read the 2-slot bucket (one sector), CAS the first free key if the pair is absent.
-__device__ __forceinline__ void pins_step(const StageCtx &c, PIns &s) {
-    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + s.b);
-    const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
-    if (s0.x == s.key || s1.x == s.key) {
-        s.done = s.dup = true;
-        return;
-    }
-    const uint32_t e = s0.x == kEmptyP ? 0u : s1.x == kEmptyP ? 1u : 2u;
-    if (e == 2u) {
-        s.b = (s.b + 2) & c.pmask;
-        return;
-    }
-    const unsigned long long old = atomicCAS(&c.pt[s.b + e].key, kEmptyP, s.key);
-    if (old == kEmptyP) {
-        s.b += e;
-        s.done = true;
-    } else if (old == s.key) {
-        s.done = s.dup = true;
-    }
-    // else: another pair took the slot; re-read the bucket
+__device__ __forceinline__ u128 pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    return (u128)a | ((u128)b << 32) | ((u128)c << 64) | ((u128)d << 96);
+}
+__device__ __forceinline__ u128 pack2(unsigned long long a, unsigned long long b) {
+    return (u128)a | ((u128)b << 64);
 }
 
-// Validate + normalize one edge, emit its arcs and digit counts, arm its pair insert; returns error bits.
-__device__ __forceinline__ uint32_t stage_edge(const StageCtx &c, uint2 e, uint32_t k, uint32_t (*sh)[kRadix],
-                                               PIns &q) {
-    q.k = k;
-    q.armed = false;
-    q.done = true;
-    q.dup = false;
-    if (e.x == kEmptyV || e.y == kEmptyV || e.x == e.y) {
-        c.pslot[k] = kNoSlot;
-        return (e.x == kEmptyV || e.y == kEmptyV) ? kErrInval : kErrLoop;
-    }
-    const uint32_t lo = min(e.x, e.y), hi = max(e.x, e.y);
-    c.E[k] = make_uint2(lo, hi);
-    reinterpret_cast<uint2 *>(c.key)[k] = make_uint2(lo, hi);
-    reinterpret_cast<uint2 *>(c.val)[k] = make_uint2(k << 1, (k << 1) | 1u);
-#pragma unroll
-    for (uint32_t p = 0; p < kPasses; ++p) {
-        atomicAdd(&sh[p][(lo >> (p * kRadixBits)) & (kRadix - 1)], 1u);
-        atomicAdd(&sh[p][(hi >> (p * kRadixBits)) & (kRadix - 1)], 1u);
-    }
-    q.key = pair_key(lo, hi);
-    q.b = hash_pair(q.key) & c.pmask & ~1u;
-    q.armed = true;
-    q.done = false;
-    return 0u;
+constexpr uint32_t kTileEdges = kRadixTile / 2;
+constexpr uint32_t kWarps = kSortThreads / 32;
+
+// Arc keys are vertex ids; pass p sorts by digit (key >> 8p) & 255.
+__device__ __forceinline__ uint32_t digit_of(uint32_t key, uint32_t pass) {
+    return (key >> (pass * kRadixBits)) & (kRadix - 1);
 }
 
-__device__ __forceinline__ uint32_t pins_finish(const StageCtx &c, const PIns &q) {
-    if (!q.armed) return 0u;
-    if (q.dup) {
-        c.pslot[q.k] = kNoSlot;
-        return kErrDup;
-    }
-    c.pt[q.b].pos = q.k;
-    c.pslot[q.k] = q.b;
-    return 0u;
-}
-
-__global__ void __launch_bounds__(256) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
-    if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
-    __shared__ uint32_t sh[kPasses][kRadix];
-    for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += blockDim.x) (&sh[0][0])[i] = 0;
-    __syncthreads();
-    uint32_t bad = 0;
-    const uint32_t stride = gridDim.x * blockDim.x;
-    const bool vec = (reinterpret_cast<uintptr_t>(in) & 15u) == 0;
-    const uint4 *in4 = reinterpret_cast<const uint4 *>(in);
-    // two edges per thread per iteration; their hash inserts are stepped together (2 round trips in flight)
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; 2 * q < w; q += stride) {
-        const bool has1 = 2 * q + 1 < w;
-        uint2 e0, e1 = make_uint2(0u, 0u);
-        if (vec && has1) {
-            const uint4 two = __ldcs(in4 + q);
-            e0 = make_uint2(two.x, two.y);
-            e1 = make_uint2(two.z, two.w);
-        } else {
-            e0 = in[2 * q];
-            if (has1) e1 = in[2 * q + 1];
-        }
-        PIns a, b;
-        bad |= stage_edge(c, e0, 2 * q, sh, a);
-        b.armed = false;
-        b.done = true;
-        b.dup = false;
-        if (has1) bad |= stage_edge(c, e1, 2 * q + 1, sh, b);
-        while (!(a.done && b.done)) {
-            if (!a.done) pins_step(c, a);
-            if (!b.done) pins_step(c, b);
-        }
-        bad |= pins_finish(c, a);
-        bad |= pins_finish(c, b);
-    }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&c.ctr[kCtrErr], bad);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += blockDim.x) {
-        const uint32_t v = (&sh[0][0])[i];
-        if (v) atomicAdd(c.hist + i, v);
-    }
-}
-
-// ------------------------------------------------------------------------------------------------
-// a2: stable LSD radix sort of the arcs by vertex id
-
-// A pass is trivial (identity) when every arc has digit 0; the ping-pong parity counts executed passes.
+// A pass is trivial (identity) when every arc has digit 0 there.
 __device__ __forceinline__ bool pass_trivial(const uint32_t *hist, uint32_t p, uint32_t n) {
     return hist[p * kRadix] == n;
 }
-__device__ __forceinline__ uint32_t passes_executed(const uint32_t *hist, uint32_t upto, uint32_t n) {
+// k_stage always writes pass 0's output to buffer B; each executed later pass flips A/B.
+__device__ __forceinline__ bool in_buffer_B(const uint32_t *hist, uint32_t upto, uint32_t n) {
     uint32_t e = 0;
-    for (uint32_t p = 0; p < upto; ++p) e += pass_trivial(hist, p, n) ? 0u : 1u;
-    return e;
+    for (uint32_t p = 1; p < upto; ++p) e += pass_trivial(hist, p, n) ? 0u : 1u;
+    return (e & 1u) == 0;
 }
 
-struct RadixBufs {
-    uint32_t *keyA, *valA, *keyB, *valB;
-    const uint32_t *hist;
-    unsigned long long *look;
-    uint32_t *ctr;
-};
+// Edge-tile loads: thread i takes edges i, i+256, ... of the tile (coalesced 8-byte loads).
+__device__ __forceinline__ uint2 norm_edge(uint2 e) { return make_uint2(min(e.x, e.y), max(e.x, e.y)); }
 
-constexpr unsigned long long kFlagAgg = 1ull, kFlagPrefix = 2ull;
+// ------------------------------------------------------------------------------------------------
+// a1: digit histograms
 
-__global__ void __launch_bounds__(kSortThreads) k_radix_pass(RadixBufs rb, uint32_t n, uint32_t pass, uint32_t seq) {
-    if (rb.ctr[kCtrErr]) return;
-    if (pass_trivial(rb.hist, pass, n)) return;
-    const bool odd = passes_executed(rb.hist, pass, n) & 1u;
-    const uint32_t *__restrict__ kin = odd ? rb.keyB : rb.keyA;
-    const uint32_t *__restrict__ vin = odd ? rb.valB : rb.valA;
-    uint32_t *__restrict__ kout = odd ? rb.keyA : rb.keyB;
-    uint32_t *__restrict__ vout = odd ? rb.valA : rb.valB;
-    const uint32_t shift = pass * kRadixBits;
-
-    __shared__ uint32_t whist[kSortThreads / 32][kRadix];  // per-warp digit counts -> warp offsets
-    __shared__ uint32_t gofs[kRadix];                      // global start of each digit for this tile
-    __shared__ uint32_t ws[kSortThreads / 32];
-    __shared__ uint32_t tile_sh;
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i < (kSortThreads / 32) * kRadix; i += kSortThreads) (&whist[0][0])[i] = 0;
-    if (threadIdx.x == 0) tile_sh = atomicAdd(&rb.ctr[kCtrTile + pass], 1u);  // dynamic tile order
+__global__ void __launch_bounds__(kSortThreads) k_hist(const uint2 *__restrict__ in, uint32_t w, uint32_t *hist,
+                                                        uint32_t *cnt, uint32_t ntiles, const uint32_t *ctr) {
+    if (ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    __shared__ uint32_t sh[kPasses][kRadix];
+    for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += kSortThreads) (&sh[0][0])[i] = 0;
     __syncthreads();
-    const uint32_t tile = tile_sh;
-    const uint32_t wbase = tile * kRadixTile + warp * (32 * kSortItems);
-
-    // stable in-tile ranks: warp w owns a contiguous 256-arc range, processed in 8 rounds of 32
-    uint32_t keys[kSortItems], vals[kSortItems], rnk[kSortItems];
-    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t e0 = blockIdx.x * kTileEdges;
+#pragma unroll 4
+    for (uint32_t i = threadIdx.x; i < kTileEdges; i += kSortThreads) {
+        if (e0 + i >= w) break;
+        const uint2 e = norm_edge(__ldg(in + e0 + i));
 #pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t idx = wbase + j * 32 + lane;
-        const bool valid = idx < n;
-        keys[j] = valid ? __ldcs(kin + idx) : 0u;
-        vals[j] = valid ? __ldcs(vin + idx) : 0u;
-    }
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const bool valid = wbase + j * 32 + lane < n;
-        const uint32_t d = valid ? (keys[j] >> shift) & (kRadix - 1) : kRadix;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const uint32_t before = __popc(peers & lt);
-        uint32_t b = 0;
-        if (valid) b = whist[warp][d];
-        __syncwarp();
-        if (valid && before == 0) whist[warp][d] = b + __popc(peers);
-        __syncwarp();
-        rnk[j] = b + before;
-    }
-    __syncthreads();
-    // per digit: exclusive prefix over warps (warp order == arc order), tile total
-    const uint32_t dgt = threadIdx.x;  // kSortThreads == kRadix
-    uint32_t total = 0;
-#pragma unroll
-    for (uint32_t x = 0; x < kSortThreads / 32; ++x) {
-        const uint32_t cnt = whist[x][dgt];
-        whist[x][dgt] = total;
-        total += cnt;
-    }
-    // decoupled look-back over earlier tiles for this digit
-    unsigned long long *lk = rb.look + (size_t)tile * kRadix + dgt;
-    const unsigned long long tag = (unsigned long long)seq << 2;
-    uint32_t excl = 0;
-    if (tile == 0) {
-        atomicExch(lk, ((tag | kFlagPrefix) << 32) | total);
-    } else {
-        atomicExch(lk, ((tag | kFlagAgg) << 32) | total);
-        // walk back in windows of 8 predecessors (8 independent loads in flight)
-        bool found = false;
-        for (int32_t t = (int32_t)tile - 1; t >= 0 && !found; t -= 8) {
-            unsigned long long v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                v[u] = t - u >= 0 ? *(const volatile unsigned long long *)(rb.look + (size_t)(t - u) * kRadix + dgt) : 0ull;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                if (found || t - u < 0) break;
-                while ((v[u] >> 34) != seq || ((v[u] >> 32) & 3ull) == 0ull)
-                    v[u] = *(const volatile unsigned long long *)(rb.look + (size_t)(t - u) * kRadix + dgt);
-                excl += (uint32_t)v[u];
-                found = ((v[u] >> 32) & 3ull) == kFlagPrefix;
-            }
+        for (uint32_t p = 0; p < kPasses; ++p) {
+            atomicAdd(&sh[p][digit_of(e.x, p)], 1u);
+            atomicAdd(&sh[p][digit_of(e.y, p)], 1u);
         }
-        atomicExch(lk, ((tag | kFlagPrefix) << 32) | (excl + total));
     }
-    // global digit offset: exclusive scan of this pass's histogram (digit order)
-    const uint32_t h = rb.hist[pass * kRadix + dgt];
-    uint32_t incl = h;
+    __syncthreads();
+    const uint32_t d = threadIdx.x;  // kSortThreads == kRadix
+    cnt[d * ntiles + blockIdx.x] = sh[0][d];
+#pragma unroll
+    for (uint32_t p = 0; p < kPasses; ++p)
+        if (sh[p][d]) atomicAdd(hist + p * kRadix + d, sh[p][d]);
+}
+
+// Per-tile digit counts of pass p >= 1 (the keys as left by the previous executed pass).
+__global__ void __launch_bounds__(kSortThreads) k_upsweep(const uint32_t *keyA, const uint32_t *keyB, uint32_t n,
+                                                          const uint32_t *hist, uint32_t pass, uint32_t *cnt,
+                                                          uint32_t ntiles, const uint32_t *ctr) {
+    if (ctr[kCtrErr] || pass_trivial(hist, pass, n)) return;
+    const uint32_t *__restrict__ kin = in_buffer_B(hist, pass, n) ? keyB : keyA;
+    __shared__ uint32_t sh[kRadix];
+    sh[threadIdx.x] = 0;
+    __syncthreads();
+    const uint32_t t0 = blockIdx.x * kRadixTile;
+    const uint4 *k4 = reinterpret_cast<const uint4 *>(kin + t0);
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems / 4; ++j) {
+        const uint32_t q = threadIdx.x + j * kSortThreads;
+        if (t0 + 4 * q + 3 < n) {
+            const uint4 v = __ldcs(k4 + q);
+            atomicAdd(&sh[digit_of(v.x, pass)], 1u);
+            atomicAdd(&sh[digit_of(v.y, pass)], 1u);
+            atomicAdd(&sh[digit_of(v.z, pass)], 1u);
+            atomicAdd(&sh[digit_of(v.w, pass)], 1u);
+        } else {
+            for (uint32_t u = 0; u < 4; ++u)
+                if (t0 + 4 * q + u < n) atomicAdd(&sh[digit_of(kin[t0 + 4 * q + u], pass)], 1u);
+        }
+    }
+    __syncthreads();
+    cnt[threadIdx.x * ntiles + blockIdx.x] = sh[threadIdx.x];
+}
+
+// One block per digit: offsets[d][t] = sum_{d' < d} hist[d'] + sum_{t' < t} cnt[d][t'].
+__global__ void __launch_bounds__(kSortThreads) k_scan(uint32_t *cnt, uint32_t ntiles, const uint32_t *hist,
+                                                       uint32_t pass, uint32_t n, const uint32_t *ctr) {
+    if (ctr[kCtrErr]) return;
+    if (pass > 0 && pass_trivial(hist, pass, n)) return;
+    __shared__ uint32_t ws[kWarps];
+    const uint32_t d = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    // digit base
+    uint32_t hv = threadIdx.x < d ? hist[pass * kRadix + threadIdx.x] : 0u;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
+    if (lane == 0) ws[warp] = hv;
+    __syncthreads();
+    uint32_t base = 0;
+    for (uint32_t x = 0; x < kWarps; ++x) base += ws[x];
+    __syncthreads();
+    // exclusive scan of the digit's row, chunk per thread
+    uint32_t *row = cnt + (size_t)d * ntiles;
+    const uint32_t per = (ntiles + kSortThreads - 1) / kSortThreads;
+    const uint32_t c0 = threadIdx.x * per, c1 = min(ntiles, c0 + per);
+    uint32_t local = 0;
+    for (uint32_t i = c0; i < c1; ++i) local += row[i];
+    uint32_t incl = local;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -264,19 +147,178 @@ __global__ void __launch_bounds__(kSortThreads) k_radix_pass(RadixBufs rb, uint3
     }
     if (lane == 31) ws[warp] = incl;
     __syncthreads();
-    uint32_t wpre = 0;
-    for (uint32_t x = 0; x < warp; ++x) wpre += ws[x];
-    gofs[dgt] = wpre + incl - h + excl;
+    uint32_t run = base + incl - local;
+    for (uint32_t x = 0; x < warp; ++x) run += ws[x];
+    for (uint32_t i = c0; i < c1; ++i) {
+        const uint32_t c = row[i];
+        row[i] = run;
+        run += c;
+    }
+}
+
+// Stable in-tile ranks by digit: warp w owns arcs [512w, 512w+512) of the tile in 16 rounds of 32.
+// On return whist[w][d] = arcs of digit d in warps < w, and rnk[j] = rank among digit-d arcs of warp w.
+__device__ __forceinline__ void rank_tile(const uint32_t (&dg)[kSortItems], uint32_t (&rnk)[kSortItems],
+                                          uint32_t (*whist)[kRadix]) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    for (uint32_t i = threadIdx.x; i < kWarps * kRadix; i += kSortThreads) (&whist[0][0])[i] = 0;
     __syncthreads();
 #pragma unroll
     for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t idx = wbase + j * 32 + lane;
-        if (idx < n) {
-            const uint32_t d = (keys[j] >> shift) & (kRadix - 1);
-            const uint32_t pos = gofs[d] + whist[warp][d] + rnk[j];
-            kout[pos] = keys[j];
-            vout[pos] = vals[j];
+        const uint32_t d = dg[j];  // kRadix marks "no arc"
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t before = __popc(peers & lt);
+        uint32_t b = 0;
+        if (d < kRadix) b = whist[warp][d];
+        __syncwarp();
+        if (d < kRadix && before == 0) whist[warp][d] = b + __popc(peers);
+        __syncwarp();
+        rnk[j] = b + before;
+    }
+    __syncthreads();
+    const uint32_t dd = threadIdx.x;  // per digit: exclusive prefix over warps (warp order == arc order)
+    uint32_t tot = 0;
+#pragma unroll
+    for (uint32_t x = 0; x < kWarps; ++x) {
+        const uint32_t c = whist[x][dd];
+        whist[x][dd] = tot;
+        tot += c;
+    }
+    __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------------
+// a1 + a3 (+ radix pass 0): staging, validation, edge-pair hash, arcs
+
+struct StageCtx {
+    uint2 *E;
+    uint32_t *keyB, *valB;  // pass-0 output
+    const uint32_t *off;    // scanned per-tile digit-0 offsets
+    const uint32_t *hist;
+    uint32_t ntiles;
+    PSlot *pt;
+    uint32_t pmask;
+    uint32_t tag;
+    uint32_t *ctr;
+};
+
+// Claim (lo, hi) -> k in the edge-pair hash: 1 = inserted, 0 = duplicate, 2 = keep probing (b advanced).
+__device__ __forceinline__ uint32_t pair_step(const StageCtx &c, unsigned long long key, uint32_t k, uint32_t &b) {
+    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + b);
+    const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
+    const bool l0 = (uint32_t)(s0.y >> 32) == c.tag, l1 = (uint32_t)(s1.y >> 32) == c.tag;
+    if ((l0 && s0.x == key) || (l1 && s1.x == key)) return 0u;
+    if (l0 && l1) {
+        b = (b + 2) & c.pmask;
+        return 2u;
+    }
+    const uint32_t e = l0 ? 1u : 0u;
+    const ulonglong2 s = e ? s1 : s0;
+    const u128 want = pack2(key, ((unsigned long long)c.tag << 32) | k);
+    const u128 old = atomicCAS(reinterpret_cast<u128 *>(c.pt + b + e), pack2(s.x, s.y), want);
+    if (old == pack2(s.x, s.y)) return 1u;
+    return 2u;  // raced with another claim of that slot: re-read the bucket
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+    if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    __shared__ uint2 sedge[kTileEdges];
+    __shared__ uint32_t whist[kWarps][kRadix];
+    __shared__ uint32_t soff[kRadix];
+    const uint32_t e0 = blockIdx.x * kTileEdges;
+    const uint32_t ne = min(kTileEdges, w - e0);
+    const bool trivial0 = pass_trivial(c.hist, 0, 2 * w);
+    soff[threadIdx.x] = c.off[threadIdx.x * c.ntiles + blockIdx.x];
+    // per edge: validate, normalize, E, pair insert (8 edges per thread, inserts stepped together)
+    constexpr uint32_t kPer = kTileEdges / kSortThreads;
+    unsigned long long key[kPer];
+    uint32_t bkt[kPer];
+    uint32_t live = 0, bad = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) {
+        const uint32_t i = threadIdx.x + j * kSortThreads;
+        uint2 e = make_uint2(0u, 0u);
+        if (i < ne) e = __ldcs(in + e0 + i);
+        const uint2 n = norm_edge(e);
+        sedge[i] = n;
+        if (i < ne) {
+            if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
+            else if (e.x == e.y) bad |= kErrLoop;
+            else {
+                c.E[e0 + i] = n;
+                key[j] = pair_key(n.x, n.y);
+                bkt[j] = hash_pair(key[j]) & c.pmask & ~1u;
+                live |= 1u << j;
+            }
         }
+    }
+    while (live) {
+#pragma unroll
+        for (uint32_t j = 0; j < kPer; ++j) {
+            if (!(live & (1u << j))) continue;
+            const uint32_t r = pair_step(c, key[j], e0 + threadIdx.x + j * kSortThreads, bkt[j]);
+            if (r != 2u) live &= ~(1u << j);
+            if (r == 0u) bad |= kErrDup;
+        }
+    }
+    // radix pass 0 over the tile's arcs (arc a = 2k + side, in arrival order)
+    uint32_t dg[kSortItems], rnk[kSortItems], kv[kSortItems];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t a = warp * 512u + j * 32u + lane;  // arc index inside the tile
+        const uint2 n = sedge[a >> 1];
+        kv[j] = (a & 1u) ? n.y : n.x;
+        dg[j] = (a >> 1) < ne ? digit_of(kv[j], 0) : kRadix;
+    }
+    if (!trivial0) rank_tile(dg, rnk, whist);
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t a = warp * 512u + j * 32u + lane;
+        if ((a >> 1) >= ne) continue;
+        const uint32_t ga = 2 * e0 + a;
+        const uint32_t pos = trivial0 ? ga : soff[dg[j]] + whist[warp][dg[j]] + rnk[j];
+        c.keyB[pos] = kv[j];
+        c.valB[pos] = ga;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && lane == 0) atomicOr(&c.ctr[kCtrErr], bad);
+}
+
+// Radix pass p >= 1: stable rank inside the tile, scatter to the scanned offsets.
+__global__ void __launch_bounds__(kSortThreads) k_downsweep(uint32_t *keyA, uint32_t *valA, uint32_t *keyB,
+                                                            uint32_t *valB, uint32_t n, const uint32_t *hist,
+                                                            uint32_t pass, const uint32_t *off, uint32_t ntiles,
+                                                            const uint32_t *ctr) {
+    if (ctr[kCtrErr] || pass_trivial(hist, pass, n)) return;
+    const bool fromB = in_buffer_B(hist, pass, n);
+    const uint32_t *__restrict__ kin = fromB ? keyB : keyA;
+    const uint32_t *__restrict__ vin = fromB ? valB : valA;
+    uint32_t *__restrict__ kout = fromB ? keyA : keyB;
+    uint32_t *__restrict__ vout = fromB ? valA : valB;
+    __shared__ uint32_t whist[kWarps][kRadix];
+    __shared__ uint32_t soff[kRadix];
+    soff[threadIdx.x] = off[threadIdx.x * ntiles + blockIdx.x];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t wbase = blockIdx.x * kRadixTile + warp * 512u;
+    uint32_t keys[kSortItems], vals[kSortItems], dg[kSortItems], rnk[kSortItems];
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t idx = wbase + j * 32u + lane;
+        const bool valid = idx < n;
+        keys[j] = valid ? __ldcs(kin + idx) : 0u;
+        vals[j] = valid ? __ldcs(vin + idx) : 0u;
+        dg[j] = valid ? digit_of(keys[j], pass) : kRadix;
+    }
+    rank_tile(dg, rnk, whist);
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        if (dg[j] == kRadix) continue;
+        const uint32_t pos = soff[dg[j]] + whist[warp][dg[j]] + rnk[j];
+        kout[pos] = keys[j];
+        vout[pos] = vals[j];
     }
 }
 
@@ -288,38 +330,40 @@ struct SegBufs {
     const uint32_t *hist;
     VSlot *vt;
     uint32_t vmask;
+    uint32_t tag;
     uint2 *einfo2;  // [2 wcap]: einfo2[k<<1|side] = {sorted slot, segment end}
-    uint32_t *vlist;
     uint32_t *ctr;
 };
 
 __device__ __forceinline__ void sorted_bufs(const SegBufs &sb, uint32_t n, const uint32_t *&keys,
                                             const uint32_t *&vals) {
-    const bool odd = passes_executed(sb.hist, kPasses, n) & 1u;
-    keys = odd ? sb.keyB : sb.keyA;
-    vals = odd ? sb.valB : sb.valA;
+    const bool B = in_buffer_B(sb.hist, kPasses, n);
+    keys = B ? sb.keyB : sb.keyA;
+    vals = B ? sb.valB : sb.valA;
 }
 
-// Insert-or-find v; returns the slot, sets claimed when this call created it.
-__device__ __forceinline__ uint32_t vt_insert(VSlot *vt, uint32_t mask, uint32_t v, bool &claimed) {
+// Insert-or-find v with payload {deg, start}; returns the slot; claimed = this call created the entry.
+__device__ __forceinline__ uint32_t vt_insert(VSlot *vt, uint32_t mask, uint32_t tag, uint32_t v, uint32_t deg,
+                                              uint32_t start, bool &claimed) {
     uint32_t b = hash_vertex(v) & mask & ~1u;
     claimed = false;
     while (true) {
         const uint4 *p = reinterpret_cast<const uint4 *>(vt + b);
         const uint4 s0 = __ldcg(p), s1 = __ldcg(p + 1);
-        if (s0.x == v) return b;
-        if (s1.x == v) return b + 1;
-        const uint32_t e = s0.x == kEmptyV ? 0u : s1.x == kEmptyV ? 1u : 2u;
-        if (e == 2u) {
+        const bool l0 = s0.w == tag, l1 = s1.w == tag;
+        if (l0 && s0.x == v) return b;
+        if (l1 && s1.x == v) return b + 1;
+        if (l0 && l1) {
             b = (b + 2) & mask;
             continue;
         }
-        const uint32_t old = atomicCAS(&vt[b + e].key, kEmptyV, v);
-        if (old == kEmptyV) {
+        const uint32_t e = l0 ? 1u : 0u;
+        const uint4 s = e ? s1 : s0;
+        const u128 exp = pack4(s.x, s.y, s.z, s.w);
+        if (atomicCAS(reinterpret_cast<u128 *>(vt + b + e), exp, pack4(v, deg, start, tag)) == exp) {
             claimed = true;
             return b + e;
         }
-        if (old == v) return b + e;
     }
 }
 
@@ -330,11 +374,20 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     sorted_bufs(sb, n, keys, vals);
     __shared__ uint32_t skey[kTile + 2];
     __shared__ uint32_t run_start[kTile], run_end[kTile];
-    __shared__ uint32_t wsum[kSortThreads / 32];
-    __shared__ uint32_t nclaim_sh, claim_base;
+    __shared__ uint32_t wsum[kWarps];
+    __shared__ uint32_t nclaim_sh;
     const uint32_t t0 = blockIdx.x * kTile;
     const uint32_t tn = min(kTile, n - t0);
-    for (uint32_t i = threadIdx.x; i < tn; i += kSortThreads) skey[i + 1] = keys[t0 + i];
+    const uint32_t i0 = threadIdx.x * kRunItems;
+    uint32_t myval[kRunItems];
+#pragma unroll
+    for (uint32_t e = 0; e < kRunItems; ++e) {
+        const uint32_t i = i0 + e;
+        if (i < tn) {
+            skey[i + 1] = keys[t0 + i];
+            myval[e] = vals[t0 + i];
+        }
+    }
     if (threadIdx.x == 0) {
         skey[0] = t0 > 0 ? keys[t0 - 1] : ~keys[t0];                       // halo: previous arc's key
         skey[tn + 1] = t0 + tn < n ? keys[t0 + tn] : ~keys[t0 + tn - 1];  // halo: next arc's key
@@ -342,7 +395,6 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     }
     __syncthreads();
     // local run heads (inside the tile) -> run ids by a block scan
-    const uint32_t i0 = threadIdx.x * kRunItems;
     uint32_t heads = 0;
 #pragma unroll
     for (uint32_t e = 0; e < kRunItems; ++e) {
@@ -359,7 +411,7 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     uint32_t wpre = 0, nruns = 0;
-    for (uint32_t x = 0; x < kSortThreads / 32; ++x) {
+    for (uint32_t x = 0; x < kWarps; ++x) {
         if (x < warp) wpre += wsum[x];
         nruns += wsum[x];
     }
@@ -378,42 +430,32 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
         }
     }
     __syncthreads();
-    // one thread per run: vertex table (complete segments by plain stores, split ones by atomics)
+    // one thread per run: vertex table entry (whole segment in one CAS; split segments by atomics)
+    uint32_t claims = 0;
     for (uint32_t r = threadIdx.x; r < nruns; r += kSortThreads) {
         const uint32_t s = run_start[r], e = run_end[r];
         const uint32_t v = skey[s + 1];
-        const bool ghead = skey[s] != v;      // the segment starts in this tile
-        const bool gtail = skey[e + 1] != v;  // ... and ends in it
+        const bool whole = skey[s] != v && skey[e + 1] != v;  // the segment starts and ends in this tile
         bool claimed;
-        const uint32_t slot = vt_insert(sb.vt, sb.vmask, v, claimed);
-        if (ghead && gtail) {
-            sb.vt[slot].deg = e - s;
-            sb.vt[slot].start = t0 + s;
-        } else {
+        const uint32_t slot =
+            vt_insert(sb.vt, sb.vmask, sb.tag, v, whole ? e - s : 0u, whole ? t0 + s : 0xFFFFFFFFu, claimed);
+        if (!whole) {
             atomicAdd(&sb.vt[slot].deg, e - s);
             atomicMin(&sb.vt[slot].start, t0 + s);
             run_end[r] = 0;  // the segment crosses the tile: k_fix writes its arcs' einfo
         }
-        run_start[r] = claimed ? (slot | 0x80000000u) : 0u;
-        if (claimed) atomicAdd(&nclaim_sh, 1u);
+        claims += claimed ? 1u : 0u;
     }
+    if (claims) atomicAdd(&nclaim_sh, claims);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        claim_base = nclaim_sh ? atomicAdd(&sb.ctr[kCtrD], nclaim_sh) : 0u;
-        nclaim_sh = 0;
-    }
-    __syncthreads();
-    // compact the claimed slots into vlist (order inside a tile is irrelevant)
-    for (uint32_t r = threadIdx.x; r < nruns; r += kSortThreads) {
-        if (run_start[r] & 0x80000000u) sb.vlist[claim_base + atomicAdd(&nclaim_sh, 1u)] = run_start[r] & 0x7FFFFFFFu;
-    }
+    if (threadIdx.x == 0 && nclaim_sh) atomicAdd(&sb.ctr[kCtrD], nclaim_sh);
     // arcs of tile-internal segments: einfo = {sorted slot, segment end}
 #pragma unroll
     for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
         if (i < tn) {
             const uint32_t end = run_end[rid[e]];
-            if (end) sb.einfo2[vals[t0 + i]] = make_uint2(t0 + i, t0 + end);
+            if (end) sb.einfo2[myval[e]] = make_uint2(t0 + i, t0 + end);
         }
     }
 }
@@ -428,7 +470,7 @@ __global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
     const uint32_t t1 = min(t0 + kTile, n);
     if (threadIdx.x < 2) {
         const uint32_t v = keys[threadIdx.x == 0 ? t0 : t1 - 1];
-        const uint2 inf = vt_find(sb.vt, sb.vmask, v);  // {deg, start}
+        const uint2 inf = vt_find(sb.vt, sb.vmask, sb.tag, v);  // {deg, start}
         seg[threadIdx.x] = make_uint2(inf.y, inf.y + inf.x);
     }
     __syncthreads();
@@ -453,16 +495,17 @@ struct UpdateIdx {
     const uint32_t *hist;
     const PSlot *pt;
     uint32_t pmask;
+    uint32_t tag;
     const uint32_t *ctr;
 };
 
 __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint2 *__restrict__ r2s,
-                                                uint32_t *__restrict__ cfs, uint64_t *__restrict__ p1s,
-                                                uint64_t *__restrict__ p2s, uint64_t count, uint64_t first,
-                                                uint64_t seed, uint32_t batch, uint64_t m_prev, uint32_t w,
-                                                UpdateIdx ix, unsigned long long *S, unsigned long long *stats) {
+                                                   uint32_t *__restrict__ cfs, uint64_t *__restrict__ p1s,
+                                                   uint64_t *__restrict__ p2s, uint64_t count, uint64_t first,
+                                                   uint64_t seed, uint32_t batch, uint64_t m_prev, uint32_t w,
+                                                   UpdateIdx ix, unsigned long long *S, unsigned long long *stats) {
     if (ix.ctr[kCtrErr]) return;
-    const uint32_t *__restrict__ segS = (passes_executed(ix.hist, kPasses, 2 * w) & 1u) ? ix.valB : ix.valA;
+    const uint32_t *__restrict__ segS = in_buffer_B(ix.hist, kPasses, 2 * w) ? ix.valB : ix.valA;
     const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long contrib = 0;
     uint32_t n_fresh = 0, n_r2old = 0;
@@ -498,8 +541,8 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
             c = cf_old & kCMask;
             closed = (cf_old & kClosedBit) != 0;
             // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
-            const uint2 iu = vt_find(ix.vt, ix.vmask, r1.x);
-            const uint2 iv = vt_find(ix.vt, ix.vmask, r1.y);
+            const uint2 iu = vt_find(ix.vt, ix.vmask, ix.tag, r1.x);
+            const uint2 iv = vt_find(ix.vt, ix.vmask, ix.tag, r1.y);
             ld = iu.x;
             rd = iv.x;
             endU = iu.y + iu.x;
@@ -528,7 +571,7 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
         if ((r2new || had_r2) && !closed) {
             const uint32_t x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;  // f1's endpoint not on f2
             const uint32_t z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;  // f2's endpoint not on f1
-            const int64_t kk = pt_find(ix.pt, ix.pmask, pair_key(min(x, z), max(x, z)));
+            const int64_t kk = pt_find(ix.pt, ix.pmask, ix.tag, pair_key(min(x, z), max(x, z)));
             if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
         }
         const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
@@ -582,43 +625,6 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
     }
 }
 
-// Empty exactly the table slots this batch used (runs even when the batch was rejected).  Four
-// independent index loads per thread before the scattered stores.
-__global__ void __launch_bounds__(256) k_clear(VSlot *__restrict__ vt, const uint32_t *__restrict__ vlist,
-                                               PSlot *__restrict__ pt, const uint32_t *__restrict__ pslot, uint32_t w,
-                                               const uint32_t *ctr) {
-    const uint32_t D = ctr[kCtrD];
-    const uint32_t stride = gridDim.x * blockDim.x;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < D; i += 4 * stride) {
-        uint32_t s[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s[u] = i + u * stride < D ? __ldcs(vlist + i + u * stride) : kNoSlot;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (s[u] != kNoSlot) reinterpret_cast<uint4 *>(vt)[s[u]] = make_uint4(kEmptyV, 0u, 0xFFFFFFFFu, 0u);
-    }
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < w; i += 4 * stride) {
-        uint32_t s[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) s[u] = i + u * stride < w ? __ldcs(pslot + i + u * stride) : kNoSlot;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (s[u] != kNoSlot) pt[s[u]].key = kEmptyP;
-    }
-}
-
-__global__ void k_init_tables(VSlot *vt, uint64_t vn, PSlot *pt, uint64_t pn) {
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < max(vn, pn);
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        if (i < vn) reinterpret_cast<uint4 *>(vt)[i] = make_uint4(kEmptyV, 0u, 0xFFFFFFFFu, 0u);
-        if (i < pn) {
-            pt[i].key = kEmptyP;
-            pt[i].pos = 0;
-            pt[i].pad = 0;
-        }
-    }
-}
-
 __global__ void k_init_state(uint2 *r1, uint2 *r2, uint32_t *cf, uint64_t *p1, uint64_t *p2, uint64_t count) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
         r1[t] = make_uint2(kEmptyV, kEmptyV);
@@ -657,25 +663,32 @@ static inline uint32_t grid_for(uint64_t items, uint32_t threads, uint32_t per_s
     return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
 }
 
+static inline uint32_t radix_tiles(uint32_t w) { return (2 * w + kRadixTile - 1) / kRadixTile; }
+
 int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    StageCtx c{ix.E, ix.keyA, ix.valA, ix.hist, ix.pt, ix.pmask, ix.pslot, ix.ctr};
-    k_stage<<<grid_for((a.w + 1) / 2, 256, 8), 256, 0, s>>>(a.in, a.w, c);
-    return 1;
+    const uint32_t nt = radix_tiles(a.w);
+    k_hist<<<nt, kSortThreads, 0, s>>>(a.in, a.w, ix.hist, ix.cnt, nt, ix.ctr);
+    k_scan<<<kRadix, kSortThreads, 0, s>>>(ix.cnt, nt, ix.hist, 0, 2 * a.w, ix.ctr);
+    StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
+    k_stage<<<nt, kSortThreads, 0, s>>>(a.in, a.w, c);
+    return 3;
 }
 
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint32_t n = 2 * a.w;
-    const uint32_t tiles = (n + kRadixTile - 1) / kRadixTile;
-    RadixBufs rb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.look, ix.ctr};
-    for (uint32_t p = 0; p < kPasses; ++p) k_radix_pass<<<tiles, kSortThreads, 0, s>>>(rb, n, p, a.seq + p);
-    return (int)kPasses;
+    const uint32_t n = 2 * a.w, nt = radix_tiles(a.w);
+    for (uint32_t p = 1; p < kPasses; ++p) {
+        k_upsweep<<<nt, kSortThreads, 0, s>>>(ix.keyA, ix.keyB, n, ix.hist, p, ix.cnt, nt, ix.ctr);
+        k_scan<<<kRadix, kSortThreads, 0, s>>>(ix.cnt, nt, ix.hist, p, n, ix.ctr);
+        k_downsweep<<<nt, kSortThreads, 0, s>>>(ix.keyA, ix.valA, ix.keyB, ix.valB, n, ix.hist, p, ix.cnt, nt, ix.ctr);
+    }
+    return 3 * (int)(kPasses - 1);
 }
 
 int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const uint32_t n = 2 * a.w;
     const uint32_t tiles = (n + kTile - 1) / kTile;
-    SegBufs sb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.vt, ix.vmask,
-               reinterpret_cast<uint2 *>(ix.einfo), ix.vlist, ix.ctr};
+    SegBufs sb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.vt, ix.vmask, a.tag,
+               reinterpret_cast<uint2 *>(ix.einfo), ix.ctr};
     k_runs<<<tiles, kSortThreads, 0, s>>>(sb, n);
     k_fix<<<tiles, kSortThreads, 0, s>>>(sb, n);
     return 2;
@@ -684,21 +697,17 @@ int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
     if (st.count == 0) return 0;
     const uint64_t blocks = (st.count + 255) / 256;
-    UpdateIdx u{ix.E, ix.einfo, ix.vt, ix.vmask, ix.valA, ix.valB, ix.hist, ix.pt, ix.pmask, ix.ctr};
+    UpdateIdx u{ix.E, ix.einfo, ix.vt, ix.vmask, ix.valA, ix.valB, ix.hist, ix.pt, ix.pmask, a.tag, ix.ctr};
     k_update<<<(uint32_t)blocks, 256, 0, s>>>(st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch,
                                               a.m_prev, a.w, u, st.S + a.S_slot, st.stats);
     return 1;
 }
 
-int launch_clear(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    k_clear<<<grid_for(2ull * a.w, 256, 8), 256, 0, s>>>(ix.vt, ix.vlist, ix.pt, ix.pslot, a.w, ix.ctr);
-    return 1;
-}
-
 int launch_init_tables(const IndexBufs &ix, cudaStream_t s) {
-    const uint64_t vn = (uint64_t)ix.vmask + 1, pn = (uint64_t)ix.pmask + 1;
-    k_init_tables<<<grid_for(std::max(vn, pn), 256, 16), 256, 0, s>>>(ix.vt, vn, ix.pt, pn);
-    return 1;
+    // tag 0 marks every slot free (live tags start at 1)
+    cudaMemsetAsync(ix.vt, 0, 16ull * ((uint64_t)ix.vmask + 1), s);
+    cudaMemsetAsync(ix.pt, 0, 16ull * ((uint64_t)ix.pmask + 1), s);
+    return 0;
 }
 
 int launch_init_state(const StateBufs &st, cudaStream_t s) {

@@ -14,15 +14,13 @@ struct IndexBufs {
     uint32_t *keyA = nullptr, *valA = nullptr;  // [2 wcap] radix ping-pong buffers: arc vertex / arc value
     uint32_t *keyB = nullptr, *valB = nullptr;
     uint32_t *hist = nullptr;  // [kPasses * kRadix] digit histograms of the arc keys
-    unsigned long long *look = nullptr;  // [tiles * kRadix] decoupled look-back words
-    uint64_t look_tiles = 0;
+    uint32_t *cnt = nullptr;   // [kRadix * tiles] per-tile digit counts -> offsets (current pass)
+    uint64_t tiles_cap = 0;
     uint4 *einfo = nullptr;    // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
     VSlot *vt = nullptr;       // [vmask+1]
     uint32_t vmask = 0;
     PSlot *pt = nullptr;       // [pmask+1]
     uint32_t pmask = 0;
-    uint32_t *pslot = nullptr; // [wcap] pair-table slot of edge k (kNoSlot if not inserted)
-    uint32_t *vlist = nullptr; // [2 wcap] claimed vertex-table slots (D of them)
     uint32_t *ctr = nullptr;   // device counters (index.cuh kCtr*)
     uint2 *stage = nullptr;    // [wcap] H2D staging for host batches
 };
@@ -41,7 +39,7 @@ struct BatchArgs {
     uint32_t w;
     uint64_t m_prev;
     uint32_t batch;  // index b of this (non-empty) batch
-    uint32_t seq;    // look-back sequence base (kPasses values per batch, never reused)
+    uint32_t tag;    // table tag of this push (never reused while a table slot may carry it)
     uint64_t first;  // global id of local estimator 0
     uint64_t seed;
     int S_slot;
@@ -52,7 +50,6 @@ int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s);
-int launch_clear(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_init_tables(const IndexBufs &ix, cudaStream_t s);
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
