@@ -156,6 +156,19 @@ __global__ void __launch_bounds__(kSortThreads) k_scan(uint32_t *cnt, uint32_t n
     }
 }
 
+// Lanes of the warp whose 8-bit digit equals d (d == kRadix: no arc), from 9 ballots instead of
+// __match_any_sync (a slow MIO op on this part).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
+    uint32_t m = __ballot_sync(0xffffffffu, d < kRadix);
+    if (d >= kRadix) m = ~m;
+#pragma unroll
+    for (uint32_t b = 0; b < kRadixBits; ++b) {
+        const uint32_t v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? v : ~v;
+    }
+    return m;
+}
+
 // Stable in-tile ranks by digit: warp w owns arcs [512w, 512w+512) of the tile in 16 rounds of 32.
 // On return whist[w][d] = arcs of digit d in warps < w, and rnk[j] = rank among digit-d arcs of warp w.
 __device__ __forceinline__ void rank_tile(const uint32_t (&dg)[kSortItems], uint32_t (&rnk)[kSortItems],
@@ -167,7 +180,7 @@ __device__ __forceinline__ void rank_tile(const uint32_t (&dg)[kSortItems], uint
 #pragma unroll
     for (uint32_t j = 0; j < kSortItems; ++j) {
         const uint32_t d = dg[j];  // kRadix marks "no arc"
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = digit_peers(d);
         const uint32_t before = __popc(peers & lt);
         uint32_t b = 0;
         if (d < kRadix) b = whist[warp][d];
@@ -221,7 +234,7 @@ __device__ __forceinline__ uint32_t pair_step(const StageCtx &c, unsigned long l
     return 2u;  // raced with another claim of that slot: re-read the bucket
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+__global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
     if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
     __shared__ uint2 sedge[kTileEdges];
     __shared__ uint32_t whist[kWarps][kRadix];
@@ -288,7 +301,7 @@ __global__ void __launch_bounds__(kSortThreads) k_stage(const uint2 *__restrict_
 }
 
 // Radix pass p >= 1: stable rank inside the tile, scatter to the scanned offsets.
-__global__ void __launch_bounds__(kSortThreads) k_downsweep(uint32_t *keyA, uint32_t *valA, uint32_t *keyB,
+__global__ void __launch_bounds__(kSortThreads, 3) k_downsweep(uint32_t *keyA, uint32_t *valA, uint32_t *keyB,
                                                             uint32_t *valB, uint32_t n, const uint32_t *hist,
                                                             uint32_t pass, const uint32_t *off, uint32_t ntiles,
                                                             const uint32_t *ctr) {
@@ -372,7 +385,9 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     if (sb.ctr[kCtrErr]) return;
     const uint32_t *keys, *vals;
     sorted_bufs(sb, n, keys, vals);
-    __shared__ uint32_t skey[kTile + 2];
+    __shared__ uint32_t skey_[kTile + 2 + (kTile + 2) / 32 + 1];
+    // skewed index (one pad word per 32) so the per-thread contiguous reads below are conflict-free
+#define SKEY(i) skey_[(i) + ((i) >> 5)]
     __shared__ uint32_t run_start[kTile], run_end[kTile];
     __shared__ uint32_t wsum[kWarps];
     __shared__ uint32_t nclaim_sh;
@@ -384,13 +399,13 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
         if (i < tn) {
-            skey[i + 1] = keys[t0 + i];
+            SKEY(i + 1) = keys[t0 + i];
             myval[e] = vals[t0 + i];
         }
     }
     if (threadIdx.x == 0) {
-        skey[0] = t0 > 0 ? keys[t0 - 1] : ~keys[t0];                       // halo: previous arc's key
-        skey[tn + 1] = t0 + tn < n ? keys[t0 + tn] : ~keys[t0 + tn - 1];  // halo: next arc's key
+        SKEY(0) = t0 > 0 ? keys[t0 - 1] : ~keys[t0];                       // halo: previous arc's key
+        SKEY(tn + 1) = t0 + tn < n ? keys[t0 + tn] : ~keys[t0 + tn - 1];  // halo: next arc's key
         nclaim_sh = 0;
     }
     __syncthreads();
@@ -399,7 +414,7 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
 #pragma unroll
     for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
-        if (i < tn && (i == 0 || skey[i + 1] != skey[i])) ++heads;
+        if (i < tn && (i == 0 || SKEY(i + 1) != SKEY(i))) ++heads;
     }
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     uint32_t incl = heads;
@@ -421,12 +436,12 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
 #pragma unroll
         for (uint32_t e = 0; e < kRunItems; ++e) {
             const uint32_t i = i0 + e;
-            if (i < tn && (i == 0 || skey[i + 1] != skey[i])) {
+            if (i < tn && (i == 0 || SKEY(i + 1) != SKEY(i))) {
                 run_start[r] = i;
                 ++r;
             }
             rid[e] = r - 1;
-            if (i < tn && (i + 1 == tn || skey[i + 2] != skey[i + 1])) run_end[r - 1] = i + 1;
+            if (i < tn && (i + 1 == tn || SKEY(i + 2) != SKEY(i + 1))) run_end[r - 1] = i + 1;
         }
     }
     __syncthreads();
@@ -434,8 +449,8 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     uint32_t claims = 0;
     for (uint32_t r = threadIdx.x; r < nruns; r += kSortThreads) {
         const uint32_t s = run_start[r], e = run_end[r];
-        const uint32_t v = skey[s + 1];
-        const bool whole = skey[s] != v && skey[e + 1] != v;  // the segment starts and ends in this tile
+        const uint32_t v = SKEY(s + 1);
+        const bool whole = SKEY(s) != v && SKEY(e + 1) != v;  // the segment starts and ends in this tile
         bool claimed;
         const uint32_t slot =
             vt_insert(sb.vt, sb.vmask, sb.tag, v, whole ? e - s : 0u, whole ? t0 + s : 0xFFFFFFFFu, claimed);
@@ -459,6 +474,7 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
         }
     }
 }
+#undef SKEY
 
 // Arcs of segments that cross tile boundaries (at most the first and the last segment of a tile).
 __global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
