@@ -89,6 +89,24 @@ __device__ __forceinline__ uint2 vt_find(const VSlot *__restrict__ vt, uint32_t 
     }
 }
 
+// Two independent vertex probes whose first sectors are requested together.
+__device__ __forceinline__ void vt_find2(const VSlot *__restrict__ vt, uint32_t mask, uint32_t tag, uint32_t u,
+                                         uint32_t v, uint2 &iu, uint2 &iv) {
+    const uint32_t bu = hash_vertex(u) & mask & ~1u, bv = hash_vertex(v) & mask & ~1u;
+    const uint4 *pu = reinterpret_cast<const uint4 *>(vt + bu);
+    const uint4 *pv = reinterpret_cast<const uint4 *>(vt + bv);
+    const uint4 u0 = __ldg(pu), u1 = __ldg(pu + 1), v0 = __ldg(pv), v1 = __ldg(pv + 1);
+    const bool lu0 = u0.w == tag, lu1 = u1.w == tag, lv0 = v0.w == tag, lv1 = v1.w == tag;
+    if (lu0 && u0.x == u) iu = make_uint2(u0.y, u0.z);
+    else if (lu1 && u1.x == u) iu = make_uint2(u1.y, u1.z);
+    else if (!lu0 || !lu1) iu = make_uint2(0u, 0u);
+    else iu = vt_find(vt, mask, tag, u);  // rare: first bucket full without u
+    if (lv0 && v0.x == v) iv = make_uint2(v0.y, v0.z);
+    else if (lv1 && v1.x == v) iv = make_uint2(v1.y, v1.z);
+    else if (!lv0 || !lv1) iv = make_uint2(0u, 0u);
+    else iv = vt_find(vt, mask, tag, v);
+}
+
 // Probe the complete (read-only) edge-pair hash: batch position of (lo, hi) or -1.
 __device__ __forceinline__ int64_t pt_find(const PSlot *__restrict__ pt, uint32_t mask, uint32_t tag,
                                            unsigned long long key) {

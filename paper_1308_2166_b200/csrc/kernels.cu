@@ -216,25 +216,7 @@ struct StageCtx {
     uint32_t *ctr;
 };
 
-// Claim (lo, hi) -> k in the edge-pair hash: 1 = inserted, 0 = duplicate, 2 = keep probing (b advanced).
-__device__ __forceinline__ uint32_t pair_step(const StageCtx &c, unsigned long long key, uint32_t k, uint32_t &b) {
-    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + b);
-    const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
-    const bool l0 = (uint32_t)(s0.y >> 32) == c.tag, l1 = (uint32_t)(s1.y >> 32) == c.tag;
-    if ((l0 && s0.x == key) || (l1 && s1.x == key)) return 0u;
-    if (l0 && l1) {
-        b = (b + 2) & c.pmask;
-        return 2u;
-    }
-    const uint32_t e = l0 ? 1u : 0u;
-    const ulonglong2 s = e ? s1 : s0;
-    const u128 want = pack2(key, ((unsigned long long)c.tag << 32) | k);
-    const u128 old = atomicCAS(reinterpret_cast<u128 *>(c.pt + b + e), pack2(s.x, s.y), want);
-    if (old == pack2(s.x, s.y)) return 1u;
-    return 2u;  // raced with another claim of that slot: re-read the bucket
-}
-
-__global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+__global__ void __launch_bounds__(kSortThreads, 2) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
     if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
     __shared__ uint2 sedge[kTileEdges];
     __shared__ uint32_t whist[kWarps][kRadix];
@@ -266,13 +248,54 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restri
             }
         }
     }
-    while (live) {
+    // Probe rounds in three phases so the inserts' round trips overlap (two groups of 4 to bound
+    // registers): read every live bucket, then issue every claim (128-bit CAS), then resolve.
 #pragma unroll
-        for (uint32_t j = 0; j < kPer; ++j) {
-            if (!(live & (1u << j))) continue;
-            const uint32_t r = pair_step(c, key[j], e0 + threadIdx.x + j * kSortThreads, bkt[j]);
-            if (r != 2u) live &= ~(1u << j);
-            if (r == 0u) bad |= kErrDup;
+    for (uint32_t g = 0; g < kPer; g += 4) {
+        while (live & (0xFu << g)) {
+            ulonglong2 s[4][2];
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t j = g + q;
+                if (!(live & (1u << j))) continue;
+                const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + bkt[j]);
+                s[q][0] = __ldcg(p);
+                s[q][1] = __ldcg(p + 1);
+            }
+            u128 expv[4], got[4];
+            uint32_t claim = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t j = g + q;
+                if (!(live & (1u << j))) continue;
+                const bool l0 = (uint32_t)(s[q][0].y >> 32) == c.tag, l1 = (uint32_t)(s[q][1].y >> 32) == c.tag;
+                if ((l0 && s[q][0].x == key[j]) || (l1 && s[q][1].x == key[j])) {  // in-batch duplicate
+                    bad |= kErrDup;
+                    live &= ~(1u << j);
+                } else if (l0 && l1) {
+                    bkt[j] = (bkt[j] + 2) & c.pmask;  // bucket full: next bucket
+                } else {
+                    const uint32_t e = l0 ? 1u : 0u;
+                    bkt[j] += e;
+                    expv[q] = pack2(s[q][e].x, s[q][e].y);
+                    claim |= 1u << q;
+                }
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                if (!(claim & (1u << q))) continue;
+                const uint32_t j = g + q;
+                const uint32_t k = e0 + threadIdx.x + j * kSortThreads;
+                got[q] = atomicCAS(reinterpret_cast<u128 *>(c.pt + bkt[j]), expv[q],
+                                   pack2(key[j], ((unsigned long long)c.tag << 32) | k));
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                if (!(claim & (1u << q))) continue;
+                const uint32_t j = g + q;
+                if (got[q] == expv[q]) live &= ~(1u << j);  // claimed
+                else bkt[j] &= ~1u;                         // raced: re-read the bucket
+            }
         }
     }
     // radix pass 0 over the tile's arcs (arc a = 2k + side, in arrival order)
@@ -557,8 +580,8 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
             c = cf_old & kCMask;
             closed = (cf_old & kClosedBit) != 0;
             // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
-            const uint2 iu = vt_find(ix.vt, ix.vmask, ix.tag, r1.x);
-            const uint2 iv = vt_find(ix.vt, ix.vmask, ix.tag, r1.y);
+            uint2 iu, iv;
+            vt_find2(ix.vt, ix.vmask, ix.tag, r1.x, r1.y, iu, iv);
             ld = iu.x;
             rd = iv.x;
             endU = iu.y + iu.x;
