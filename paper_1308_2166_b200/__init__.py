@@ -122,6 +122,9 @@ class TriangleCounter:
     def set_async(self, on: bool = True):
         self._ck(_lib.load().tc_set_async(self._h, 1 if on else 0), "tc_set_async")
 
+    def set_graphs(self, on: bool = True):
+        self._ck(_lib.load().tc_set_graphs(self._h, 1 if on else 0), "tc_set_graphs")
+
     def sync(self) -> int:
         return _lib.load().tc_sync(self._h)
 

@@ -21,7 +21,7 @@ TC_NPHASES = 4
 PHASES = ("stage", "sort", "segment", "update")
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_destroy", "tc_closed_sum",
-           "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_sync",
+           "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_sync",
            "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_strerror", "tc_last_error"]
 
 _lib = None
@@ -55,6 +55,7 @@ def load(path: str = LIB_PATH):
         "tc_get_state": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, vp]),
         "tc_counters": (i32, [vp, C.POINTER(u64), C.POINTER(u32)]),
         "tc_set_async": (i32, [vp, i32]),
+        "tc_set_graphs": (i32, [vp, i32]),
         "tc_sync": (i32, [vp]),
         "tc_stream": (vp, [vp]),
         "tc_profile": (i32, [vp, i32]),

@@ -45,6 +45,9 @@ struct tc_ctx {
     double prof_ms[TC_NPHASES] = {};
     uint64_t prof_launch[TC_NPHASES] = {};
     int prof_pending = 0;
+    // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
+    int use_graph = 1;
+    cudaGraphExec_t gexec = nullptr;
 };
 
 static int fail_cuda(tc_ctx *c) {
@@ -123,6 +126,7 @@ static void destroy_ctx(tc_ctx *ctx) {
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -187,6 +191,7 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
 }
 
 tc_ctx *tc_create(uint64_t r, uint64_t seed) { return tc_create_shard(r, seed, 0, r, -1, 0); }
+
 
 void tc_destroy(tc_ctx *ctx) { destroy_ctx(ctx); }
 
@@ -258,15 +263,6 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         in = ix.stage;
     }
     const int slot = (int)((ctx->b + 1) & 1u);
-    if (ctx->async_errors) {
-        CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ctx->stream));  // keep the sticky error word
-        CK(cudaMemsetAsync(ix.ctr + kCtrErr + 1, 0, 4 * (kCtrWords - kCtrErr - 1), ctx->stream));
-    } else {
-        CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
-        if (ovf) CK(cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ctx->stream));
-    }
-    CK(cudaMemsetAsync(ix.hist, 0, 4 * kPasses * kRadix, ctx->stream));
-    CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
     BatchArgs a;
     a.in = in;
     a.w = (uint32_t)w;
@@ -275,21 +271,57 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.first = ctx->first;
     a.seed = ctx->seed;
     a.S_slot = slot;
-    if (++ctx->tag == 0xFFFFFFFFu) {  // never reuse a tag a slot may still carry: free every slot
-        launch_init_tables(ix, ctx->stream);
-        ctx->tag = 1;
-    }
+    const bool wrap = ++ctx->tag == 0xFFFFFFFFu;  // never reuse a tag a slot may still carry
+    if (wrap) ctx->tag = 1;
     a.tag = ctx->tag;
+    // The batch's whole device sequence (counter resets + kernels) is captured as one CUDA graph and the
+    // previous graph executable is updated in place, so the ~17 launches run without host gaps.
+    const bool graph = ctx->use_graph != 0;
+    if (graph) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     uint32_t launches = 0;
-    int n;
-    int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {
-        launch_stage, launch_sort, launch_segment, nullptr};
-    for (int p = 0; p < TC_NPHASES; ++p) {
-        n = phase_fn[p] ? phase_fn[p](ix, a, ctx->stream) : launch_update(ix, ctx->st, a, ctx->stream);
-        launches += n;
-        if (ctx->prof) {
-            CK(cudaEventRecord(ctx->ev[p + 1], ctx->stream));
-            ctx->prof_launch[p] += n;
+    {
+        bool ok = true;
+        if (ctx->async_errors) {
+            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ctx->stream) == cudaSuccess;  // keep the sticky error
+            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr + 1, 0, 4 * (kCtrWords - kCtrErr - 1), ctx->stream) == cudaSuccess;
+        } else {
+            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream) == cudaSuccess;
+            if (ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ctx->stream) == cudaSuccess;
+        }
+        ok = ok && cudaMemsetAsync(ix.hist, 0, 4 * kPasses * kRadix, ctx->stream) == cudaSuccess;
+        ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream) == cudaSuccess;
+        if (wrap) launch_init_tables(ix, ctx->stream);
+        int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {
+            launch_stage, launch_sort, launch_segment, nullptr};
+        for (int p = 0; p < TC_NPHASES; ++p) {
+            const int n = phase_fn[p] ? phase_fn[p](ix, a, ctx->stream) : launch_update(ix, ctx->st, a, ctx->stream);
+            launches += n;
+            if (ctx->prof) {
+                ok = ok && cudaEventRecord(ctx->ev[p + 1], ctx->stream) == cudaSuccess;
+                ctx->prof_launch[p] += n;
+            }
+        }
+        if (graph) {
+            cudaGraph_t g = nullptr;
+            const bool cap = cudaStreamEndCapture(ctx->stream, &g) == cudaSuccess && g;
+            if (!ok || !cap) {
+                if (g) cudaGraphDestroy(g);
+                return fail_cuda(ctx);
+            }
+            cudaGraphExecUpdateResultInfo info;
+            if (!ctx->gexec || cudaGraphExecUpdate(ctx->gexec, g, &info) != cudaSuccess) {
+                cudaGetLastError();
+                if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+                ctx->gexec = nullptr;
+                if (cudaGraphInstantiate(&ctx->gexec, g, 0) != cudaSuccess) {
+                    cudaGraphDestroy(g);
+                    return fail_cuda(ctx);
+                }
+            }
+            cudaGraphDestroy(g);
+            CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+        } else if (!ok) {
+            return fail_cuda(ctx);
         }
     }
     if (ctx->prof) ctx->prof_pending = 1;
@@ -304,6 +336,14 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     ctx->b += 1;
     ctx->S_slot = slot;
     ctx->last_launches = launches;
+    return TC_OK;
+}
+
+int tc_set_graphs(tc_ctx *ctx, int enable) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    ctx->use_graph = enable ? 1 : 0;
     return TC_OK;
 }
 

@@ -195,3 +195,28 @@ def test_big_batch_hubs_sampled():
     check_properties(s, st, len(s))
     o = oracle_run(s, r, 5, w, r // 2, 1024)
     assert_states_equal({f: st[f][r // 2:r // 2 + 1024] for f in FIELDS}, o.state(), "C5-like shard")
+
+
+def test_graph_and_plain_launches_agree():
+    """The CUDA-graph launch path (default) and plain stream launches give identical states."""
+    from paper_1308_2166_b200 import TriangleCounter
+    s = rmat(13, 16, 9)
+    out = []
+    for graphs in (True, False):
+        tc = TriangleCounter(5000, 77)
+        tc.set_graphs(graphs)
+        tc.set_async(True)
+        k = 0
+        for w in (4096, 4096, 333, 4096, 1, 7000, 4096):
+            tc.push_batch(s[k:k + w])
+            k += w
+        assert tc.sync() == 0
+        out.append(tc.state())
+    assert_states_equal(out[0], out[1], "graph vs plain")
+    from oracle.indexed import IndexedOracle
+    o = IndexedOracle(5000, 77)
+    k = 0
+    for w in (4096, 4096, 333, 4096, 1, 7000, 4096):
+        assert o.push_batch(s[k:k + w]) == 0
+        k += w
+    assert_states_equal(out[0], o.state(), "graph vs oracle")
