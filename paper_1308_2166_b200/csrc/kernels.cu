@@ -313,47 +313,23 @@ struct SegBufs {
     uint32_t *ctr;
 };
 
-// Arcs at sorted slots i (values a = k<<1|side) of segments [start, end): their einfo, and each arc's
-// neighbour in its vertex's region of the neighbour area.  N arcs per call, in three phases so the
-// round trips overlap: the N edge loads, then the N claims (64-bit CAS at the home slot), then linear
-// probing for the rare collisions.  Returns kErrDup when a neighbour is already in the region.
-template <int N>
-__device__ __forceinline__ uint32_t place_arcs(const SegBufs &sb, const uint32_t (&a)[N], const uint32_t (&i)[N],
-                                               const uint32_t (&start)[N], const uint32_t (&end)[N], uint32_t live) {
-    uint2 e[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q)
-        if (live & (1u << q)) e[q] = __ldg(sb.E + (a[q] >> 1));
-    unsigned long long want[N], got[N];
-    uint32_t h[N];
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        if (!(live & (1u << q))) continue;
-        sb.einfo[a[q]] = make_uint4(i[q], start[q], end[q], 0u);
-        const uint32_t y = (a[q] & 1u) ? e[q].x : e[q].y;  // the other endpoint
-        h[q] = region_home(y, 2 * (end[q] - start[q]));
-        want[q] = ((unsigned long long)(a[q] >> 1) << 32) | y;
-        got[q] = atomicCAS(reinterpret_cast<unsigned long long *>(sb.area + 2ull * start[q] + h[q]), kEmptyArea, want[q]);
+// Arc at sorted slot i (value a = k<<1|side) of the segment [start, end): its einfo, and its neighbour in
+// the vertex's region of the neighbour area.  Returns kErrDup when the neighbour is already there.
+__device__ __forceinline__ uint32_t place_arc(const SegBufs &sb, uint32_t a, uint32_t i, uint32_t start,
+                                              uint32_t end) {
+    sb.einfo[a] = make_uint4(i, start, end, 0u);
+    const uint2 e = __ldg(sb.E + (a >> 1));
+    const uint32_t y = (a & 1u) ? e.x : e.y;  // the other endpoint
+    const uint32_t n = 2 * (end - start);
+    uint2 *reg = sb.area + 2ull * start;
+    uint32_t h = region_home(y, n);
+    const unsigned long long want = ((unsigned long long)(a >> 1) << 32) | y;
+    while (true) {
+        const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(reg + h), kEmptyArea, want);
+        if (old == kEmptyArea) return 0u;
+        if ((uint32_t)old == y) return kErrDup;
+        h = h + 1 == n ? 0 : h + 1;
     }
-    uint32_t bad = 0;
-#pragma unroll
-    for (int q = 0; q < N; ++q) {
-        if (!(live & (1u << q))) continue;
-        const uint32_t y = (uint32_t)want[q];
-        const uint32_t n = 2 * (end[q] - start[q]);
-        unsigned long long *reg = reinterpret_cast<unsigned long long *>(sb.area + 2ull * start[q]);
-        unsigned long long old = got[q];
-        uint32_t hh = h[q];
-        while (old != kEmptyArea) {
-            if ((uint32_t)old == y) {
-                bad |= kErrDup;
-                break;
-            }
-            hh = hh + 1 == n ? 0 : hh + 1;
-            old = atomicCAS(reg + hh, kEmptyArea, want[q]);
-        }
-    }
-    return bad;
 }
 
 __device__ __forceinline__ void sorted_bufs(const SegBufs &sb, uint32_t n, const uint32_t *&keys,
@@ -474,17 +450,15 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     __syncthreads();
     if (threadIdx.x == 0 && nclaim_sh) atomicAdd(&sb.ctr[kCtrD], nclaim_sh);
     // arcs of tile-internal segments: einfo + neighbour region (crossing ones: k_fix)
-    uint32_t pi[kRunItems], ps[kRunItems], pe[kRunItems], live = 0;
+    uint32_t bad = 0;
 #pragma unroll
     for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
-        const uint32_t end = i < tn ? run_end[rid[e]] : 0u;
-        pi[e] = t0 + i;
-        ps[e] = end ? t0 + run_lo[rid[e]] : 0u;
-        pe[e] = t0 + end;
-        if (end) live |= 1u << e;
+        if (i < tn) {
+            const uint32_t end = run_end[rid[e]];
+            if (end) bad |= place_arc(sb, myval[e], t0 + i, t0 + run_lo[rid[e]], t0 + end);
+        }
     }
-    uint32_t bad = place_arcs<kRunItems>(sb, myval, pi, ps, pe, live);
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && lane == 0) atomicOr(&sb.ctr[kCtrErr], bad);
 }
@@ -510,18 +484,7 @@ __global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
         if (sgm.x >= t0 && sgm.y <= t1) continue;   // tile-internal: done by k_runs
         if (q == 1 && seg[0].x == sgm.x) continue;  // same segment as q == 0
         const uint32_t lo = max(sgm.x, t0), hi = min(sgm.y, t1);
-        for (uint32_t i0 = lo; i0 < hi; i0 += 4 * kSortThreads) {
-            uint32_t a[4], ii[4], ss[4], ee[4], live = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                ii[q] = i0 + threadIdx.x + q * kSortThreads;
-                ss[q] = sgm.x;
-                ee[q] = sgm.y;
-                a[q] = ii[q] < hi ? vals[ii[q]] : 0u;
-                if (ii[q] < hi) live |= 1u << q;
-            }
-            bad |= place_arcs<4>(sb, a, ii, ss, ee, live);
-        }
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += kSortThreads) bad |= place_arc(sb, vals[i], i, sgm.x, sgm.y);
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
     if (bad && (threadIdx.x & 31u) == 0) atomicOr(&sb.ctr[kCtrErr], bad);
