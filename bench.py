@@ -127,19 +127,18 @@ def algorithmic_bytes(phase, w, R, D, fresh, r2old):
     update : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
              (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
              index probes are L2 traffic at C2 and not counted.
-    stage  : read 8 B/edge (twice: histogram + stage); write E 8 + arcs 16 B/edge.
+    stage  : read 8 B/edge (twice: histogram + stage); write E 8 + arcs 16 + pair slot 16 B/edge.
     sort   : the 2 arcs of an edge read and written once (32 B/edge); extra radix passes are overhead.
-    segment: read sorted arcs 16 + edges 8 + write rank/bounds 32 + neighbour slots 16 B/edge (+ the 32 B/edge
-             area reset); 16 B per vertex-table entry.
+    segment: read sorted arcs 16 + write rank/end 16 B/edge; 16 B per vertex-table entry.
     """
     if phase == "update":
         return 24 * (R - fresh) + 36 * fresh + 16 * r2old
     if phase == "stage":
-        return 40 * w
+        return 56 * w
     if phase == "sort":
         return 32 * w
     if phase == "segment":
-        return 104 * w + 16 * D
+        return 32 * w + 16 * D
     raise KeyError(phase)
 
 

@@ -46,7 +46,7 @@ struct tc_ctx {
     uint64_t prof_launch[TC_NPHASES] = {};
     int prof_pending = 0;
     // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
-    int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
+    int use_graph = 1;
     cudaGraphExec_t gexec = nullptr;
 };
 
@@ -71,7 +71,7 @@ static void free_index(IndexBufs &ix) {
     cudaFree(ix.cnt);
     cudaFree(ix.einfo);
     cudaFree(ix.vt);
-    cudaFree(ix.area);
+    cudaFree(ix.pt);
     cudaFree(ix.ctr);
     cudaFree(ix.stage);
     ix = IndexBufs();
@@ -85,14 +85,15 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
+    const uint64_t pslots = next_pow2(4 * cap);  // w pairs: load <= 25%
     ix.tiles_cap = (2 * cap + kRadixTile - 1) / kRadixTile;
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyA, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valA, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyB, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valB, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.hist, 4 * kPasses * kRadix) == cudaSuccess &&
               cudaMalloc(&ix.cnt, 4 * kRadix * ix.tiles_cap) == cudaSuccess &&
-              cudaMalloc(&ix.einfo, 32 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
-              cudaMalloc(&ix.area, 32 * cap) == cudaSuccess && cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess &&
+              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess &&
               cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -100,6 +101,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
         return TC_ENOMEM;
     }
     ix.vmask = (uint32_t)(vslots - 1);
+    ix.pmask = (uint32_t)(pslots - 1);
     ix.wcap = cap;
     launch_init_tables(ix, ctx->stream);  // tag 0 everywhere: every slot free
     CK(cudaGetLastError());
@@ -287,7 +289,6 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
             if (ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ctx->stream) == cudaSuccess;
         }
         ok = ok && cudaMemsetAsync(ix.hist, 0, 4 * kPasses * kRadix, ctx->stream) == cudaSuccess;
-        ok = ok && cudaMemsetAsync(ix.area, 0xFF, 32 * w, ctx->stream) == cudaSuccess;  // empty neighbour regions
         ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream) == cudaSuccess;
         if (wrap) launch_init_tables(ix, ctx->stream);
         int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {

@@ -8,13 +8,11 @@
 //             PAPER.md:730-734), so rank(x->y) of the arc at sorted slot s is segEnd(x) - 1 - s
 //             (Definition Rank).  segS = the sorted value array.
 //   vertex table (open addressing, 16 B slots, 2 per 32 B sector): {x, deg_W(x), segment start, tag}
-//   einfo[a]  uint4 per arc a = k<<1|side: {sorted slot, segment start, segment end, 0}; the two arcs of
-//             an edge share one 32-byte sector
-//   neighbour area: 2 slots per arc, vertex x's region = [2 start(x), 2 end(x)), an open-addressing
-//             table of x's batch neighbours {y, k}: Step 3's (src,dst)-sorted "edges" array with its
-//             multisearch replaced by one probe inside the region of f1's endpoint
-// A vertex-table slot is live only when its tag equals the batch's tag, so that table is never cleared;
-// a slot is claimed with one 128-bit CAS that installs key, payload and tag together.
+//   einfo[k]  uint4 {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
+//   edge-pair hash (16 B slots, 2 per sector): {lo<<32 | hi, k, tag}: Step 3's (src,dst)-sorted "edges"
+//             array with its multisearch replaced by one O(1) probe
+// A slot is live only when its tag equals the batch's tag, so the tables are never cleared; a slot is
+// claimed with one 128-bit CAS that installs key, payload and tag together.
 #pragma once
 #include <cstdint>
 
@@ -29,9 +27,6 @@ constexpr uint32_t kErrInval = 1u;
 constexpr uint32_t kErrLoop = 2u;
 constexpr uint32_t kErrDup = 4u;
 constexpr uint32_t kErrOvf = 8u;
-// errors found while staging stop the index build; a duplicate (found in k_runs / k_fix) or an overflow
-// (set by the host) only stop the estimator update
-constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 
 // radix sort of arcs by vertex id
 constexpr uint32_t kRadixBits = 8;
@@ -51,7 +46,10 @@ constexpr int kCtrWords = 16;
 struct __align__(16) VSlot {
     uint32_t key, deg, start, tag;
 };
-constexpr unsigned long long kEmptyArea = ~0ull;
+struct __align__(16) PSlot {
+    unsigned long long key;
+    uint32_t pos, tag;
+};
 
 __device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
     x ^= x >> 16;
@@ -60,6 +58,20 @@ __device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
     x *= 0x846ca68bu;
     x ^= x >> 16;
     return x;
+}
+
+__device__ __forceinline__ uint32_t hash_pair(unsigned long long key) {
+    uint64_t x = key;
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return (uint32_t)x;
+}
+
+__device__ __forceinline__ unsigned long long pair_key(uint32_t lo, uint32_t hi) {
+    return ((unsigned long long)lo << 32) | hi;
 }
 
 // Probe the complete (read-only) vertex table: {deg_W(v), segment start}, or {0, 0} when v is not in W.
@@ -95,22 +107,18 @@ __device__ __forceinline__ void vt_find2(const VSlot *__restrict__ vt, uint32_t 
     else iv = vt_find(vt, mask, tag, v);
 }
 
-// Home slot of neighbour y inside a region of n slots (multiply-shift, no modulo).
-__device__ __forceinline__ uint32_t region_home(uint32_t y, uint32_t n) {
-    return (uint32_t)(((unsigned long long)hash_vertex(y ^ 0x9e3779b9u) * n) >> 32);
-}
-
-// Batch position of edge {x, y} from x's neighbour region [2 start, 2 end), or -1.
-__device__ __forceinline__ int64_t area_find(const uint2 *__restrict__ area, uint32_t start, uint32_t end, uint32_t y) {
-    const uint32_t n = 2 * (end - start);
-    if (n == 0) return -1;
-    const uint2 *reg = area + 2ull * start;
-    uint32_t h = region_home(y, n);
+// Probe the complete (read-only) edge-pair hash: batch position of (lo, hi) or -1.
+__device__ __forceinline__ int64_t pt_find(const PSlot *__restrict__ pt, uint32_t mask, uint32_t tag,
+                                           unsigned long long key) {
+    uint32_t b = hash_pair(key) & mask & ~1u;
     while (true) {
-        const uint2 s = __ldg(reg + h);
-        if (s.x == y) return (int64_t)s.y;
-        if (s.x == kEmptyV) return -1;
-        h = h + 1 == n ? 0 : h + 1;
+        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(pt + b);
+        const ulonglong2 s0 = __ldg(p), s1 = __ldg(p + 1);
+        const bool l0 = (uint32_t)(s0.y >> 32) == tag, l1 = (uint32_t)(s1.y >> 32) == tag;
+        if (l0 && s0.x == key) return (int64_t)(uint32_t)s0.y;
+        if (l1 && s1.x == key) return (int64_t)(uint32_t)s1.y;
+        if (!l0 || !l1) return -1;
+        b = (b + 2) & mask;
     }
 }
 

@@ -3,17 +3,17 @@
 // Pipeline for one batch W; tiles are 2048 edges = 4096 arcs:
 //   k_hist       a1      : per-tile counts of digit 0 of the arc keys, global histograms of all digits
 //   k_scan               : per digit, exclusive scan over tiles + digit base = each tile's output offsets
-//   k_stage      a1      : load W (coalesced), validate, normalize to (lo, hi); rank the tile's arcs
-//                          (vertex, k<<1|side) stably by digit 0 and scatter them -- the F array of
-//                          rankAll's proof, already radix pass 0
+//   k_stage      a1 + a3 : load W (coalesced), validate, normalize to (lo, hi); insert every edge into the
+//                          edge-pair hash (one 128-bit CAS per claim, 8 inserts in flight per thread);
+//                          rank the tile's arcs (vertex, k<<1|side) stably by digit 0 and scatter them --
+//                          the F array of rankAll's proof, already radix pass 0
 //   k_upsweep / k_scan / k_downsweep  a2 : the remaining stable LSD radix passes over the arcs by vertex id
 //                          (passes whose digit is 0 for every arc are skipped on the device).  Stability
 //                          keeps arrival order inside a vertex: this replaces rankAll's sort by (src, -pos)
 //                          (PAPER.md:680-684).
-//   k_runs    a2 + a3    : runs of equal vertex inside each tile -> vertex table {deg_W, segment start};
-//                          per arc of a tile-internal segment: rank / segment bounds (einfo) and its
-//                          neighbour in the vertex's region of the neighbour area (a repeat is TC_EDUP)
-//   k_fix     a2 + a3    : the same for the arcs of segments that cross tile boundaries
+//   k_runs       a2      : runs of equal vertex inside each tile -> vertex table {deg_W, segment start};
+//                          rank / segment end of the arcs of tile-internal segments
+//   k_fix        a2      : rank / segment end of the arcs of segments that cross tile boundaries
 //   k_update     a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2 (chi^+
 //                          from ranks / degrees, level-2 pick by segment arithmetic), Step 3 (closing-edge
 //                          probe), block partial sums of chi over closed estimators
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kSortThreads) k_hist(const uint2 *__restrict__
 __global__ void __launch_bounds__(kSortThreads) k_upsweep(const uint32_t *keyA, const uint32_t *keyB, uint32_t n,
                                                           const uint32_t *hist, uint32_t pass, uint32_t *cnt,
                                                           uint32_t ntiles, const uint32_t *ctr) {
-    if ((ctr[kCtrErr] & kErrStage) || pass_trivial(hist, pass, n)) return;
+    if (ctr[kCtrErr] || pass_trivial(hist, pass, n)) return;
     const uint32_t *__restrict__ kin = in_buffer_B(hist, pass, n) ? keyB : keyA;
     __shared__ uint32_t sh[kRadix];
     sh[threadIdx.x] = 0;
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(kSortThreads) k_upsweep(const uint32_t *keyA, 
 // One block per digit: offsets[d][t] = sum_{d' < d} hist[d'] + sum_{t' < t} cnt[d][t'].
 __global__ void __launch_bounds__(kSortThreads) k_scan(uint32_t *cnt, uint32_t ntiles, const uint32_t *hist,
                                                        uint32_t pass, uint32_t n, const uint32_t *ctr) {
-    if (ctr[kCtrErr] & kErrStage) return;
+    if (ctr[kCtrErr]) return;
     if (pass > 0 && pass_trivial(hist, pass, n)) return;
     __shared__ uint32_t ws[kWarps];
     const uint32_t d = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -210,10 +210,13 @@ struct StageCtx {
     const uint32_t *off;    // scanned per-tile digit-0 offsets
     const uint32_t *hist;
     uint32_t ntiles;
+    PSlot *pt;
+    uint32_t pmask;
+    uint32_t tag;
     uint32_t *ctr;
 };
 
-__global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+__global__ void __launch_bounds__(kSortThreads, 2) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
     if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
     __shared__ uint2 sedge[kTileEdges];
     __shared__ uint32_t whist[kWarps][kRadix];
@@ -222,9 +225,11 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restri
     const uint32_t ne = min(kTileEdges, w - e0);
     const bool trivial0 = pass_trivial(c.hist, 0, 2 * w);
     soff[threadIdx.x] = c.off[threadIdx.x * c.ntiles + blockIdx.x];
-    // per edge: validate, normalize, E
+    // per edge: validate, normalize, E, pair insert (8 edges per thread, inserts stepped together)
     constexpr uint32_t kPer = kTileEdges / kSortThreads;
-    uint32_t bad = 0;
+    unsigned long long key[kPer];
+    uint32_t bkt[kPer];
+    uint32_t live = 0, bad = 0;
 #pragma unroll
     for (uint32_t j = 0; j < kPer; ++j) {
         const uint32_t i = threadIdx.x + j * kSortThreads;
@@ -235,7 +240,62 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restri
         if (i < ne) {
             if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
             else if (e.x == e.y) bad |= kErrLoop;
-            else c.E[e0 + i] = n;
+            else {
+                c.E[e0 + i] = n;
+                key[j] = pair_key(n.x, n.y);
+                bkt[j] = hash_pair(key[j]) & c.pmask & ~1u;
+                live |= 1u << j;
+            }
+        }
+    }
+    // Probe rounds in three phases so the inserts' round trips overlap (two groups of 4 to bound
+    // registers): read every live bucket, then issue every claim (128-bit CAS), then resolve.
+#pragma unroll
+    for (uint32_t g = 0; g < kPer; g += 4) {
+        while (live & (0xFu << g)) {
+            ulonglong2 s[4][2];
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t j = g + q;
+                if (!(live & (1u << j))) continue;
+                const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + bkt[j]);
+                s[q][0] = __ldcg(p);
+                s[q][1] = __ldcg(p + 1);
+            }
+            u128 expv[4], got[4];
+            uint32_t claim = 0;
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                const uint32_t j = g + q;
+                if (!(live & (1u << j))) continue;
+                const bool l0 = (uint32_t)(s[q][0].y >> 32) == c.tag, l1 = (uint32_t)(s[q][1].y >> 32) == c.tag;
+                if ((l0 && s[q][0].x == key[j]) || (l1 && s[q][1].x == key[j])) {  // in-batch duplicate
+                    bad |= kErrDup;
+                    live &= ~(1u << j);
+                } else if (l0 && l1) {
+                    bkt[j] = (bkt[j] + 2) & c.pmask;  // bucket full: next bucket
+                } else {
+                    const uint32_t e = l0 ? 1u : 0u;
+                    bkt[j] += e;
+                    expv[q] = pack2(s[q][e].x, s[q][e].y);
+                    claim |= 1u << q;
+                }
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                if (!(claim & (1u << q))) continue;
+                const uint32_t j = g + q;
+                const uint32_t k = e0 + threadIdx.x + j * kSortThreads;
+                got[q] = atomicCAS(reinterpret_cast<u128 *>(c.pt + bkt[j]), expv[q],
+                                   pack2(key[j], ((unsigned long long)c.tag << 32) | k));
+            }
+#pragma unroll
+            for (uint32_t q = 0; q < 4; ++q) {
+                if (!(claim & (1u << q))) continue;
+                const uint32_t j = g + q;
+                if (got[q] == expv[q]) live &= ~(1u << j);  // claimed
+                else bkt[j] &= ~1u;                         // raced: re-read the bucket
+            }
         }
     }
     // radix pass 0 over the tile's arcs (arc a = 2k + side, in arrival order)
@@ -268,7 +328,7 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_downsweep(uint32_t *keyA, u
                                                             uint32_t *valB, uint32_t n, const uint32_t *hist,
                                                             uint32_t pass, const uint32_t *off, uint32_t ntiles,
                                                             const uint32_t *ctr) {
-    if ((ctr[kCtrErr] & kErrStage) || pass_trivial(hist, pass, n)) return;
+    if (ctr[kCtrErr] || pass_trivial(hist, pass, n)) return;
     const bool fromB = in_buffer_B(hist, pass, n);
     const uint32_t *__restrict__ kin = fromB ? keyB : keyA;
     const uint32_t *__restrict__ vin = fromB ? valB : valA;
@@ -307,30 +367,9 @@ struct SegBufs {
     VSlot *vt;
     uint32_t vmask;
     uint32_t tag;
-    uint4 *einfo;  // [2 wcap]: einfo[k<<1|side] = {sorted slot, segment start, segment end, 0}
-    const uint2 *E;
-    uint2 *area;
+    uint2 *einfo2;  // [2 wcap]: einfo2[k<<1|side] = {sorted slot, segment end}
     uint32_t *ctr;
 };
-
-// Arc at sorted slot i (value a = k<<1|side) of the segment [start, end): its einfo, and its neighbour in
-// the vertex's region of the neighbour area.  Returns kErrDup when the neighbour is already there.
-__device__ __forceinline__ uint32_t place_arc(const SegBufs &sb, uint32_t a, uint32_t i, uint32_t start,
-                                              uint32_t end) {
-    sb.einfo[a] = make_uint4(i, start, end, 0u);
-    const uint2 e = __ldg(sb.E + (a >> 1));
-    const uint32_t y = (a & 1u) ? e.x : e.y;  // the other endpoint
-    const uint32_t n = 2 * (end - start);
-    uint2 *reg = sb.area + 2ull * start;
-    uint32_t h = region_home(y, n);
-    const unsigned long long want = ((unsigned long long)(a >> 1) << 32) | y;
-    while (true) {
-        const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long *>(reg + h), kEmptyArea, want);
-        if (old == kEmptyArea) return 0u;
-        if ((uint32_t)old == y) return kErrDup;
-        h = h + 1 == n ? 0 : h + 1;
-    }
-}
 
 __device__ __forceinline__ void sorted_bufs(const SegBufs &sb, uint32_t n, const uint32_t *&keys,
                                             const uint32_t *&vals) {
@@ -366,14 +405,13 @@ __device__ __forceinline__ uint32_t vt_insert(VSlot *vt, uint32_t mask, uint32_t
 
 // One block per tile of kTile sorted arcs (8 consecutive per thread).
 __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
-    if (sb.ctr[kCtrErr] & kErrStage) return;
+    if (sb.ctr[kCtrErr]) return;
     const uint32_t *keys, *vals;
     sorted_bufs(sb, n, keys, vals);
     __shared__ uint32_t skey_[kTile + 2 + (kTile + 2) / 32 + 1];
     // skewed index (one pad word per 32) so the per-thread contiguous reads below are conflict-free
 #define SKEY(i) skey_[(i) + ((i) >> 5)]
     __shared__ uint32_t run_start[kTile], run_end[kTile];
-    uint32_t *const run_lo = run_start;
     __shared__ uint32_t wsum[kWarps];
     __shared__ uint32_t nclaim_sh;
     const uint32_t t0 = blockIdx.x * kTile;
@@ -449,24 +487,21 @@ __global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
     if (claims) atomicAdd(&nclaim_sh, claims);
     __syncthreads();
     if (threadIdx.x == 0 && nclaim_sh) atomicAdd(&sb.ctr[kCtrD], nclaim_sh);
-    // arcs of tile-internal segments: einfo + neighbour region (crossing ones: k_fix)
-    uint32_t bad = 0;
+    // arcs of tile-internal segments: einfo = {sorted slot, segment end}
 #pragma unroll
     for (uint32_t e = 0; e < kRunItems; ++e) {
         const uint32_t i = i0 + e;
         if (i < tn) {
             const uint32_t end = run_end[rid[e]];
-            if (end) bad |= place_arc(sb, myval[e], t0 + i, t0 + run_lo[rid[e]], t0 + end);
+            if (end) sb.einfo2[myval[e]] = make_uint2(t0 + i, t0 + end);
         }
     }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && lane == 0) atomicOr(&sb.ctr[kCtrErr], bad);
 }
 #undef SKEY
 
 // Arcs of segments that cross tile boundaries (at most the first and the last segment of a tile).
 __global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
-    if (sb.ctr[kCtrErr] & kErrStage) return;
+    if (sb.ctr[kCtrErr]) return;
     const uint32_t *keys, *vals;
     sorted_bufs(sb, n, keys, vals);
     __shared__ uint2 seg[2];
@@ -478,16 +513,13 @@ __global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
         seg[threadIdx.x] = make_uint2(inf.y, inf.y + inf.x);
     }
     __syncthreads();
-    uint32_t bad = 0;
     for (uint32_t q = 0; q < 2; ++q) {
         const uint2 sgm = seg[q];
         if (sgm.x >= t0 && sgm.y <= t1) continue;   // tile-internal: done by k_runs
         if (q == 1 && seg[0].x == sgm.x) continue;  // same segment as q == 0
         const uint32_t lo = max(sgm.x, t0), hi = min(sgm.y, t1);
-        for (uint32_t i = lo + threadIdx.x; i < hi; i += kSortThreads) bad |= place_arc(sb, vals[i], i, sgm.x, sgm.y);
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += kSortThreads) sb.einfo2[vals[i]] = make_uint2(i, sgm.y);
     }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&sb.ctr[kCtrErr], bad);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -500,7 +532,8 @@ struct UpdateIdx {
     uint32_t vmask;
     const uint32_t *valA, *valB;  // the sorted arc values (segS) live in one of them
     const uint32_t *hist;
-    const uint2 *area;
+    const PSlot *pt;
+    uint32_t pmask;
     uint32_t tag;
     const uint32_t *ctr;
 };
@@ -528,20 +561,18 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
         uint2 r1, r2 = make_uint2(kEmptyV, kEmptyV);
         uint32_t c, cf_old = 0;
         bool closed;
-        uint32_t ld, rd, startU, endU, startV, endV;
+        uint32_t ld, rd, endU, endV;
         if (fresh) {
             const uint32_t j = (uint32_t)(d1 - m_prev);
             r1 = __ldg(ix.E + j);
             c = 0;
             closed = false;
             // ---- Step 2a for a fresh f1 = w_j: ld = rank(u->v), rd = rank(v->u) ----
-            const uint4 iu = __ldg(ix.einfo + 2 * j), iv = __ldg(ix.einfo + 2 * j + 1);
-            ld = iu.z - 1u - iu.x;
-            rd = iv.z - 1u - iv.x;
-            startU = iu.y;
-            endU = iu.z;
-            startV = iv.y;
-            endV = iv.z;
+            const uint4 inf = __ldg(ix.einfo + j);
+            ld = inf.y - 1u - inf.x;
+            rd = inf.w - 1u - inf.z;
+            endU = inf.y;
+            endV = inf.w;
         } else {
             r1 = __ldcs(r1s + t);
             cf_old = __ldcs(cfs + t);
@@ -553,9 +584,7 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
             vt_find2(ix.vt, ix.vmask, ix.tag, r1.x, r1.y, iu, iv);
             ld = iu.x;
             rd = iv.x;
-            startU = iu.y;
             endU = iu.y + iu.x;
-            startV = iv.y;
             endV = iv.y + iv.x;
         }
         const uint32_t chi_p = ld + rd;  // |Gamma_W(f1)| = rank(u->v) + rank(v->u)
@@ -579,10 +608,9 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
         }
         // ---- Step 3: closing edge after f2 ----
         if ((r2new || had_r2) && !closed) {
-            const bool xu = !(r1.x == r2.x || r1.x == r2.y);                  // f1's endpoint not on f2 is u
+            const uint32_t x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;  // f1's endpoint not on f2
             const uint32_t z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;  // f2's endpoint not on f1
-            // the closing edge {x, z} is in W iff z is in x's neighbour region
-            const int64_t kk = xu ? area_find(ix.area, startU, endU, z) : area_find(ix.area, startV, endV, z);
+            const int64_t kk = pt_find(ix.pt, ix.pmask, ix.tag, pair_key(min(x, z), max(x, z)));
             if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
         }
         const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
@@ -680,7 +708,7 @@ int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const uint32_t nt = radix_tiles(a.w);
     k_hist<<<nt, kSortThreads, 0, s>>>(a.in, a.w, ix.hist, ix.cnt, nt, ix.ctr);
     k_scan<<<kRadix, kSortThreads, 0, s>>>(ix.cnt, nt, ix.hist, 0, 2 * a.w, ix.ctr);
-    StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.ctr};
+    StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
     k_stage<<<nt, kSortThreads, 0, s>>>(a.in, a.w, c);
     return 3;
 }
@@ -698,7 +726,8 @@ int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const uint32_t n = 2 * a.w;
     const uint32_t tiles = (n + kTile - 1) / kTile;
-    SegBufs sb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.vt, ix.vmask, a.tag, ix.einfo, ix.E, ix.area, ix.ctr};
+    SegBufs sb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.vt, ix.vmask, a.tag,
+               reinterpret_cast<uint2 *>(ix.einfo), ix.ctr};
     k_runs<<<tiles, kSortThreads, 0, s>>>(sb, n);
     k_fix<<<tiles, kSortThreads, 0, s>>>(sb, n);
     return 2;
@@ -707,7 +736,7 @@ int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
     if (st.count == 0) return 0;
     const uint64_t blocks = (st.count + 255) / 256;
-    UpdateIdx u{ix.E, ix.einfo, ix.vt, ix.vmask, ix.valA, ix.valB, ix.hist, ix.area, a.tag, ix.ctr};
+    UpdateIdx u{ix.E, ix.einfo, ix.vt, ix.vmask, ix.valA, ix.valB, ix.hist, ix.pt, ix.pmask, a.tag, ix.ctr};
     k_update<<<(uint32_t)blocks, 256, 0, s>>>(st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch,
                                               a.m_prev, a.w, u, st.S + a.S_slot, st.stats);
     return 1;
@@ -716,6 +745,7 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_init_tables(const IndexBufs &ix, cudaStream_t s) {
     // tag 0 marks every slot free (live tags start at 1)
     cudaMemsetAsync(ix.vt, 0, 16ull * ((uint64_t)ix.vmask + 1), s);
+    cudaMemsetAsync(ix.pt, 0, 16ull * ((uint64_t)ix.pmask + 1), s);
     return 0;
 }
 

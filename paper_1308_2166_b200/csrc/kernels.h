@@ -16,10 +16,11 @@ struct IndexBufs {
     uint32_t *hist = nullptr;  // [kPasses * kRadix] digit histograms of the arc keys
     uint32_t *cnt = nullptr;   // [kRadix * tiles] per-tile digit counts -> offsets (current pass)
     uint64_t tiles_cap = 0;
-    uint4 *einfo = nullptr;    // [2 wcap] per arc {sorted slot, segment start, segment end, 0}
+    uint4 *einfo = nullptr;    // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
     VSlot *vt = nullptr;       // [vmask+1]
     uint32_t vmask = 0;
-    uint2 *area = nullptr;     // [4 wcap] neighbour regions {y, k}; emptied (all 0xFF) at the start of a batch
+    PSlot *pt = nullptr;       // [pmask+1]
+    uint32_t pmask = 0;
     uint32_t *ctr = nullptr;   // device counters (index.cuh kCtr*)
     uint2 *stage = nullptr;    // [wcap] H2D staging for host batches
 };
