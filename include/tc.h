@@ -113,8 +113,8 @@ int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches);
  * 1 = asynchronous (sticky error, reported at the next synchronising call). */
 int tc_set_async(tc_ctx *ctx, int async_errors);
 
-/* tc_set_graphs -- 1 (default): each push runs as one CUDA graph (captured, then updated in place);
- * 0: plain stream launches.  Results are identical; only launch overhead differs. */
+/* tc_set_graphs -- 1: each push runs as one CUDA graph (captured, then updated in place);
+ * 0 (default): plain stream launches.  Results are identical; only launch overhead differs. */
 int tc_set_graphs(tc_ctx *ctx, int enable);
 
 /* tc_sync -- wait for all queued work; returns the first asynchronous error, if any. */

@@ -46,7 +46,7 @@ struct tc_ctx {
     uint64_t prof_launch[TC_NPHASES] = {};
     int prof_pending = 0;
     // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
-    int use_graph = 1;
+    int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
     cudaGraphExec_t gexec = nullptr;
 };
 
