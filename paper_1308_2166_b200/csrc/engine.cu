@@ -27,6 +27,8 @@ uint64_t next_pow2(uint64_t x) {
 struct tc_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // second stream: the edge-pair hash is built concurrently with the sort
+    cudaEvent_t fork = nullptr, join = nullptr;
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
@@ -85,7 +87,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
-    const uint64_t pslots = next_pow2(4 * cap);  // w pairs: load <= 25%
+    const uint64_t pslots = next_pow2(2 * cap);  // w pairs: load <= 50% (32 B buckets of 2)
     ix.tiles_cap = (2 * cap + kRadixTile - 1) / kRadixTile;
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyA, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.valA, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyB, 8 * cap) == cudaSuccess &&
@@ -127,6 +129,9 @@ static void destroy_ctx(tc_ctx *ctx) {
     for (auto &e : ctx->ev)
         if (e) cudaEventDestroy(e);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->join) cudaEventDestroy(ctx->join);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -164,6 +169,9 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
     ctx->st.count = count;
     const uint64_t n = std::max<uint64_t>(count, 1);
     bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming) == cudaSuccess &&
               cudaMalloc(&ctx->st.r1, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.r2, 8 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 8 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.p2, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
@@ -291,9 +299,15 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         ok = ok && cudaMemsetAsync(ix.hist, 0, 4 * kPasses * kRadix, ctx->stream) == cudaSuccess;
         ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream) == cudaSuccess;
         if (wrap) launch_init_tables(ix, ctx->stream);
+        // fork: the edge-pair hash (a3) on the side stream, joined before the estimator update
+        ok = ok && cudaEventRecord(ctx->fork, ctx->stream) == cudaSuccess;
+        ok = ok && cudaStreamWaitEvent(ctx->side, ctx->fork, 0) == cudaSuccess;
+        launches += launch_pairs(ix, a, ctx->side);
+        ok = ok && cudaEventRecord(ctx->join, ctx->side) == cudaSuccess;
         int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {
             launch_stage, launch_sort, launch_segment, nullptr};
         for (int p = 0; p < TC_NPHASES; ++p) {
+            if (p == TC_PHASE_UPDATE) ok = ok && cudaStreamWaitEvent(ctx->stream, ctx->join, 0) == cudaSuccess;
             const int n = phase_fn[p] ? phase_fn[p](ix, a, ctx->stream) : launch_update(ix, ctx->st, a, ctx->stream);
             launches += n;
             if (ctx->prof) {

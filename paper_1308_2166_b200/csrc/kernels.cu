@@ -216,7 +216,7 @@ struct StageCtx {
     uint32_t *ctr;
 };
 
-__global__ void __launch_bounds__(kSortThreads, 2) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+__global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
     if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
     __shared__ uint2 sedge[kTileEdges];
     __shared__ uint32_t whist[kWarps][kRadix];
@@ -225,11 +225,9 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_stage(const uint2 *__restri
     const uint32_t ne = min(kTileEdges, w - e0);
     const bool trivial0 = pass_trivial(c.hist, 0, 2 * w);
     soff[threadIdx.x] = c.off[threadIdx.x * c.ntiles + blockIdx.x];
-    // per edge: validate, normalize, E, pair insert (8 edges per thread, inserts stepped together)
+    // per edge: validate, normalize, E (the edge-pair hash is filled concurrently by k_pairs)
     constexpr uint32_t kPer = kTileEdges / kSortThreads;
-    unsigned long long key[kPer];
-    uint32_t bkt[kPer];
-    uint32_t live = 0, bad = 0;
+    uint32_t bad = 0;
 #pragma unroll
     for (uint32_t j = 0; j < kPer; ++j) {
         const uint32_t i = threadIdx.x + j * kSortThreads;
@@ -240,8 +238,53 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_stage(const uint2 *__restri
         if (i < ne) {
             if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
             else if (e.x == e.y) bad |= kErrLoop;
-            else {
-                c.E[e0 + i] = n;
+            else c.E[e0 + i] = n;
+        }
+    }
+    // radix pass 0 over the tile's arcs (arc a = 2k + side, in arrival order)
+    uint32_t dg[kSortItems], rnk[kSortItems], kv[kSortItems];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t a = warp * 512u + j * 32u + lane;  // arc index inside the tile
+        const uint2 n = sedge[a >> 1];
+        kv[j] = (a & 1u) ? n.y : n.x;
+        dg[j] = (a >> 1) < ne ? digit_of(kv[j], 0) : kRadix;
+    }
+    if (!trivial0) rank_tile(dg, rnk, whist);
+#pragma unroll
+    for (uint32_t j = 0; j < kSortItems; ++j) {
+        const uint32_t a = warp * 512u + j * 32u + lane;
+        if ((a >> 1) >= ne) continue;
+        const uint32_t ga = 2 * e0 + a;
+        const uint32_t pos = trivial0 ? ga : soff[dg[j]] + whist[warp][dg[j]] + rnk[j];
+        c.keyB[pos] = kv[j];
+        c.valB[pos] = ga;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (bad && lane == 0) atomicOr(&c.ctr[kCtrErr], bad);
+}
+
+// a3: the edge-pair hash {lo<<32|hi -> k} (Step 3's closing-edge index), built on a second stream
+// concurrently with the radix sort.  8 edges per thread, inserts stepped together in three phases
+// (bucket loads, 128-bit CAS claims, resolution); a repeat of a pair is TC_EDUP.
+__global__ void __launch_bounds__(kSortThreads, 2) k_pairs(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+    if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    const uint32_t e0 = blockIdx.x * kTileEdges;
+    const uint32_t ne = min(kTileEdges, w - e0);
+    constexpr uint32_t kPer = kTileEdges / kSortThreads;
+    unsigned long long key[kPer];
+    uint32_t bkt[kPer];
+    uint32_t live = 0, bad = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kPer; ++j) {
+        const uint32_t i = threadIdx.x + j * kSortThreads;
+        uint2 e = make_uint2(0u, 0u);
+        if (i < ne) e = __ldcs(in + e0 + i);
+        const uint2 n = norm_edge(e);
+        if (i < ne && e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // invalid edges: k_stage reports them
+            {
                 key[j] = pair_key(n.x, n.y);
                 bkt[j] = hash_pair(key[j]) & c.pmask & ~1u;
                 live |= 1u << j;
@@ -298,29 +341,8 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_stage(const uint2 *__restri
             }
         }
     }
-    // radix pass 0 over the tile's arcs (arc a = 2k + side, in arrival order)
-    uint32_t dg[kSortItems], rnk[kSortItems], kv[kSortItems];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    __syncthreads();
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t a = warp * 512u + j * 32u + lane;  // arc index inside the tile
-        const uint2 n = sedge[a >> 1];
-        kv[j] = (a & 1u) ? n.y : n.x;
-        dg[j] = (a >> 1) < ne ? digit_of(kv[j], 0) : kRadix;
-    }
-    if (!trivial0) rank_tile(dg, rnk, whist);
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t a = warp * 512u + j * 32u + lane;
-        if ((a >> 1) >= ne) continue;
-        const uint32_t ga = 2 * e0 + a;
-        const uint32_t pos = trivial0 ? ga : soff[dg[j]] + whist[warp][dg[j]] + rnk[j];
-        c.keyB[pos] = kv[j];
-        c.valB[pos] = ga;
-    }
     bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && lane == 0) atomicOr(&c.ctr[kCtrErr], bad);
+    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&c.ctr[kCtrErr], bad);
 }
 
 // Radix pass p >= 1: stable rank inside the tile, scatter to the scanned offsets.
@@ -711,6 +733,13 @@ int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
     k_stage<<<nt, kSortThreads, 0, s>>>(a.in, a.w, c);
     return 3;
+}
+
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    const uint32_t nt = radix_tiles(a.w);
+    StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
+    k_pairs<<<nt, kSortThreads, 0, s>>>(a.in, a.w, c);
+    return 1;
 }
 
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {

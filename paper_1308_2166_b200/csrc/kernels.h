@@ -47,6 +47,7 @@ struct BatchArgs {
 
 // Each returns the number of kernel launches issued.
 int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s);
