@@ -65,7 +65,8 @@ __device__ __forceinline__ uint2 norm_edge(uint2 e) { return make_uint2(min(e.x,
 
 __global__ void __launch_bounds__(kSortThreads) k_hist(const uint2 *__restrict__ in, uint32_t w, uint32_t *hist,
                                                         uint32_t *cnt, uint32_t ntiles, const uint32_t *ctr) {
-    if (ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    // (a duplicate found by k_pairs of this very batch must not stop staging: only stage errors here)
+    if (ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     __shared__ uint32_t sh[kPasses][kRadix];
     for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += kSortThreads) (&sh[0][0])[i] = 0;
     __syncthreads();
@@ -217,7 +218,7 @@ struct StageCtx {
 };
 
 __global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
-    if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+    if (c.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     __shared__ uint2 sedge[kTileEdges];
     __shared__ uint32_t whist[kWarps][kRadix];
     __shared__ uint32_t soff[kRadix];
@@ -267,77 +268,36 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restri
 }
 
 // a3: the edge-pair hash {lo<<32|hi -> k} (Step 3's closing-edge index), built on a second stream
-// concurrently with the radix sort.  8 edges per thread, inserts stepped together in three phases
-// (bucket loads, 128-bit CAS claims, resolution); a repeat of a pair is TC_EDUP.
-__global__ void __launch_bounds__(kSortThreads, 2) k_pairs(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
+// concurrently with the radix sort.  One edge per thread (many threads in flight hide the probe round
+// trips); a claim is one 128-bit CAS of {key, k, tag}; a repeat of a pair is TC_EDUP.
+__global__ void __launch_bounds__(256) k_pairs(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
     if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
-    const uint32_t e0 = blockIdx.x * kTileEdges;
-    const uint32_t ne = min(kTileEdges, w - e0);
-    constexpr uint32_t kPer = kTileEdges / kSortThreads;
-    unsigned long long key[kPer];
-    uint32_t bkt[kPer];
-    uint32_t live = 0, bad = 0;
-#pragma unroll
-    for (uint32_t j = 0; j < kPer; ++j) {
-        const uint32_t i = threadIdx.x + j * kSortThreads;
-        uint2 e = make_uint2(0u, 0u);
-        if (i < ne) e = __ldcs(in + e0 + i);
-        const uint2 n = norm_edge(e);
-        if (i < ne && e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // invalid edges: k_stage reports them
-            {
-                key[j] = pair_key(n.x, n.y);
-                bkt[j] = hash_pair(key[j]) & c.pmask & ~1u;
-                live |= 1u << j;
-            }
-        }
-    }
-    // Probe rounds in three phases so the inserts' round trips overlap (two groups of 4 to bound
-    // registers): read every live bucket, then issue every claim (128-bit CAS), then resolve.
-#pragma unroll
-    for (uint32_t g = 0; g < kPer; g += 4) {
-        while (live & (0xFu << g)) {
-            ulonglong2 s[4][2];
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
-                const uint32_t j = g + q;
-                if (!(live & (1u << j))) continue;
-                const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + bkt[j]);
-                s[q][0] = __ldcg(p);
-                s[q][1] = __ldcg(p + 1);
-            }
-            u128 expv[4], got[4];
-            uint32_t claim = 0;
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
-                const uint32_t j = g + q;
-                if (!(live & (1u << j))) continue;
-                const bool l0 = (uint32_t)(s[q][0].y >> 32) == c.tag, l1 = (uint32_t)(s[q][1].y >> 32) == c.tag;
-                if ((l0 && s[q][0].x == key[j]) || (l1 && s[q][1].x == key[j])) {  // in-batch duplicate
-                    bad |= kErrDup;
-                    live &= ~(1u << j);
-                } else if (l0 && l1) {
-                    bkt[j] = (bkt[j] + 2) & c.pmask;  // bucket full: next bucket
-                } else {
-                    const uint32_t e = l0 ? 1u : 0u;
-                    bkt[j] += e;
-                    expv[q] = pack2(s[q][e].x, s[q][e].y);
-                    claim |= 1u << q;
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t bad = 0;
+    if (k < w) {
+        const uint2 e = __ldcs(in + k);
+        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // invalid edges: k_stage reports them
+            const uint2 n = norm_edge(e);
+            const unsigned long long key = pair_key(n.x, n.y);
+            uint32_t b = hash_pair(key) & c.pmask & ~1u;
+            while (true) {
+                const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + b);
+                const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
+                const bool l0 = (uint32_t)(s0.y >> 32) == c.tag, l1 = (uint32_t)(s1.y >> 32) == c.tag;
+                if ((l0 && s0.x == key) || (l1 && s1.x == key)) {
+                    bad = kErrDup;
+                    break;
                 }
-            }
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
-                if (!(claim & (1u << q))) continue;
-                const uint32_t j = g + q;
-                const uint32_t k = e0 + threadIdx.x + j * kSortThreads;
-                got[q] = atomicCAS(reinterpret_cast<u128 *>(c.pt + bkt[j]), expv[q],
-                                   pack2(key[j], ((unsigned long long)c.tag << 32) | k));
-            }
-#pragma unroll
-            for (uint32_t q = 0; q < 4; ++q) {
-                if (!(claim & (1u << q))) continue;
-                const uint32_t j = g + q;
-                if (got[q] == expv[q]) live &= ~(1u << j);  // claimed
-                else bkt[j] &= ~1u;                         // raced: re-read the bucket
+                if (l0 && l1) {
+                    b = (b + 2) & c.pmask;
+                    continue;
+                }
+                const uint32_t s = l0 ? 1u : 0u;
+                const ulonglong2 o = s ? s1 : s0;
+                const u128 exp = pack2(o.x, o.y);
+                if (atomicCAS(reinterpret_cast<u128 *>(c.pt + b + s), exp,
+                              pack2(key, ((unsigned long long)c.tag << 32) | k)) == exp)
+                    break;
             }
         }
     }
@@ -738,7 +698,7 @@ int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const uint32_t nt = radix_tiles(a.w);
     StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
-    k_pairs<<<nt, kSortThreads, 0, s>>>(a.in, a.w, c);
+    k_pairs<<<(a.w + 255) / 256, 256, 0, s>>>(a.in, a.w, c);
     return 1;
 }
 
