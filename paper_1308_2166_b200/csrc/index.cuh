@@ -27,6 +27,9 @@ constexpr uint32_t kErrInval = 1u;
 constexpr uint32_t kErrLoop = 2u;
 constexpr uint32_t kErrDup = 4u;
 constexpr uint32_t kErrOvf = 8u;
+// errors found while staging (they stop the index build); a duplicate (found by k_pairs concurrently) or
+// an overflow (set by the host) only stop the estimator update
+constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 
 // radix sort of arcs by vertex id
 constexpr uint32_t kRadixBits = 8;
