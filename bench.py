@@ -37,7 +37,7 @@ L2_FLUSH_BYTES = 256 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=15)
+    ap.add_argument("--steps", type=int, default=150)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
@@ -57,49 +57,78 @@ def dist_env():
 
 # --------------------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock and throttle reasons sampled every 5 ms DURING the timed region (NVML, the library
+    nvidia-smi reads; falls back to `nvidia-smi -lms 200`)."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
     def __init__(self, index: int):
         self.index = index
         self.rows = []
+        self.max_mhz = None
+        self._stop = threading.Event()
         self.proc = None
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+
+            reasons_fn = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = reasons_fn(h)
+                        self.rows.append((float(sm), int(rs)))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+
+            self.t = threading.Thread(target=loop, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:
+            try:
+                q = "clocks.sm,clocks.max.sm,clocks_event_reasons.active"
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                              "--format=csv,noheader,nounits", "-lms", "200"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+
+                def rd():
+                    for line in self.proc.stdout:
+                        f = [x.strip() for x in line.split(",")]
+                        try:
+                            self.max_mhz = float(f[1])
+                            self.rows.append((float(f[0]), int(f[2], 16)))
+                        except (ValueError, IndexError):
+                            pass
+
+                self.t = threading.Thread(target=rd, daemon=True)
+                self.t.start()
+            except OSError:
+                pass
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *exc):
+        self._stop.set()
         if self.proc:
             time.sleep(0.25)
             self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
 
     def summary(self):
         if not self.rows:
             return None
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({name for _, rs in self.rows for name, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.rows), "source": "nvml" if self.proc is None else "nvidia-smi"}
 
 
 def measured_peaks():
@@ -112,11 +141,14 @@ def measured_peaks():
 
 
 def committed_traffic(config):
-    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the committed
+    `ncu --set full` capture (profiles/traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get(config)
+            d = json.load(f).get(config)
+        if d:
+            return d.get("traffic_bytes_per_launch")
     return None
 
 
@@ -168,8 +200,8 @@ def run_b200(args):
     # stream resident in HBM before timing ("excluding I/O"); rank 0 owns it
     dstream = torch.from_numpy(stream.view(np.int32)).to(dev) if rank == 0 else None
     bbuf = torch.empty((w, 2), dtype=torch.int32, device=dev)
-    flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
+    flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
 
     def batch(k, ext=None):
         lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
@@ -199,33 +231,45 @@ def run_b200(args):
     tc = make()
     for k in range(args.warmup):
         if k and k % nb == 0:
-            tc = make()
+            assert tc.sync() == 0
+            tc.reset()
         ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
         tc.push_batch(batch(k, ext))
     assert tc.sync() == 0
-    del tc
 
-    # ---- timed: K steps, each bracketed by CUDA events on the library's stream; L2 flushed between ----
-    tc = make()
+    # ---- timed: K steps = K consecutive batches of the stream (a new pass over the stream starts from a
+    # reset estimator set, untimed); CUDA events on the library's stream around each step; L2 flushed
+    # (read of a 256 MiB buffer) before every step, outside the events ----
+    tc.reset()
     tc.profile(True)
     ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
     evs = []
     launches = 0
     edges_done = 0
-    counters_for_bytes = []
+    prof = {}
+    stats = {"fresh": 0, "r2_replaced_retained": 0, "vertices": 0}
+
+    def harvest():
+        for p, (pms, n) in tc.profile_read().items():
+            a = prof.setdefault(p, [0.0, 0])
+            a[0] += pms
+            a[1] += n
+        for kk, v in tc.stats().items():
+            if kk in stats:
+                stats[kk] += v
+
     barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev.index) as clocks:
         t_wall = time.perf_counter()
         for k in range(args.steps):
-            if k and k % nb == 0:  # stream exhausted: a fresh estimator set (creation untimed)
+            if k and k % nb == 0:  # stream exhausted: a fresh estimator set (untimed)
                 assert tc.sync() == 0
-                counters_for_bytes.append(tc)
-                tc = make()
+                harvest()
+                tc.reset()
                 tc.profile(True)
-                ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
             with torch.cuda.stream(ext):
-                flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache, no dirty lines
+                flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(ext)
             b = batch(k, ext)
@@ -239,7 +283,7 @@ def run_b200(args):
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall
     barrier()
-    counters_for_bytes.append(tc)
+    harvest()
     ms = sum(a.elapsed_time(b) for a, b in evs)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -247,39 +291,26 @@ def run_b200(args):
     ms = float(t.item())
     secs = ms / 1e3
 
-    # per-phase device time (library events) and the dominant kernel's roofline
-    prof = {}
-    for c in counters_for_bytes:
-        for p, (pms, n) in c.profile_read().items():
-            a = prof.setdefault(p, [0.0, 0])
-            a[0] += pms
-            a[1] += n
-    stats = [c.stats() for c in counters_for_bytes]
-    fresh = sum(s["fresh"] for s in stats)
-    r2old = sum(s["r2_replaced_retained"] for s in stats)
-    D = sum(s["vertices"] for s in stats)
-    dom = max(prof, key=lambda p: prof[p][0])
+    # dominant kernel = k_update (the largest single kernel in the committed ncu launch list,
+    # profiles/launches_r01_summary.txt); its events bracket exactly that one launch per step
     peak, peak_src = measured_peaks()
     nsteps = args.steps
-    total_alg = {
-        "update": algorithmic_bytes("update", 0, count * nsteps, 0, fresh, r2old),
-        "stage": algorithmic_bytes("stage", edges_done, 0, D, 0, 0),
+    alg = {
+        "update": algorithmic_bytes("update", 0, count * nsteps, 0, stats["fresh"], stats["r2_replaced_retained"]),
+        "stage": algorithmic_bytes("stage", edges_done, 0, stats["vertices"], 0, 0),
         "sort": algorithmic_bytes("sort", edges_done, 0, 0, 0, 0),
-        "segment": algorithmic_bytes("segment", edges_done, 0, D, 0, 0),
+        "segment": algorithmic_bytes("segment", edges_done, 0, stats["vertices"], 0, 0),
     }
-    dom_secs = prof[dom][0] / 1e3
-    achieved = total_alg[dom] / dom_secs / 1e9 if dom_secs > 0 else None
-    upd_secs = prof["update"][0] / 1e3
-    upd_ach = total_alg["update"] / upd_secs / 1e9 if upd_secs > 0 else None
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak if achieved else None,
+    ach = {p: alg[p] / (prof[p][0] / 1e3) / 1e9 for p in alg if prof.get(p) and prof[p][0] > 0}
+    roofline = {"bound": "hbm", "kernel": "k_update (fused Steps 1-3 + partial sums)",
+                "achieved": ach.get("update"), "peak": peak, "unit": "GB/s",
+                "frac": ach["update"] / peak if ach.get("update") else None,
                 "traffic": committed_traffic(args.config), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": total_alg[dom] / max(1, nsteps),
-                "launch_ms": prof[dom][0] / max(1, nsteps),
-                "update_kernel": {"achieved": upd_ach, "frac": upd_ach / peak if upd_ach else None,
-                                  "launch_ms": prof["update"][0] / max(1, nsteps)},
-                "phase_ms_per_step": {p: prof[p][0] / max(1, nsteps) for p in prof},
-                "phase_share": {p: prof[p][0] / max(1e-12, sum(v[0] for v in prof.values())) for p in prof}}
+                "algorithmic_bytes_per_launch": alg["update"] / max(1, nsteps),
+                "launch_ms": prof["update"][0] / max(1, nsteps),
+                "phases": {p: {"ms_per_step": prof[p][0] / max(1, nsteps), "launches_per_step": prof[p][1] / max(1, nsteps),
+                               "algorithmic_GBps": ach.get(p), "frac": (ach[p] / peak) if ach.get(p) else None}
+                           for p in prof}}
 
     value = edges_done / secs
     out = {
@@ -297,8 +328,7 @@ def run_b200(args):
         "roofline": roofline,
         "wall_s_timed_region": t_wall,
     }
-    clk = clocks.summary()
-    out["clocks"] = clk
+    out["clocks"] = clocks.summary()
 
     # ---- e2e: the public API with HOST (pinned) buffers, H2D + result D2H inside every step ----
     if not args.no_e2e and world == 1:
@@ -307,14 +337,11 @@ def run_b200(args):
         ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
         for k in range(min(args.warmup, nb)):
             tc2.push_batch(host[k * w:(k + 1) * w])
-        del tc2
-        tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
-        ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
-        e_ms, e_edges, h2d = 0.0, 0, 0
+        tc2.reset()
+        e_ms, e_edges, h2d, est = 0.0, 0, 0, 0.0
         for k in range(args.steps):
             if k and k % nb == 0:
-                tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
-                ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
+                tc2.reset()
             lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
             with torch.cuda.stream(ext2):
                 flush_sink.add_(flush.sum())

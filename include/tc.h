@@ -81,6 +81,10 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w);
  * Synchronises.  0.0 before any edge. */
 int tc_estimate(tc_ctx *ctx, double *out);
 
+/* tc_reset -- back to the state right after creation (all estimators empty, m = 0, no batch), keeping
+ * the allocations; clears a poisoned handle.  Synchronises. */
+int tc_reset(tc_ctx *ctx);
+
 /* tc_destroy -- frees the handle and its device memory; NULL-safe. */
 void tc_destroy(tc_ctx *ctx);
 

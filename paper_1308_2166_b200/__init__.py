@@ -119,6 +119,10 @@ class TriangleCounter:
         self._ck(_lib.load().tc_counters(self._h, C.byref(m), C.byref(b)), "tc_counters")
         return int(m.value), int(b.value)
 
+    def reset(self):
+        """Back to the freshly created state (tc_reset); allocations are kept."""
+        self._ck(_lib.load().tc_reset(self._h), "tc_reset")
+
     def set_async(self, on: bool = True):
         self._ck(_lib.load().tc_set_async(self._h, 1 if on else 0), "tc_set_async")
 

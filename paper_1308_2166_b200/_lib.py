@@ -20,7 +20,7 @@ TC_ESTATE = -8
 TC_NPHASES = 4
 PHASES = ("stage", "sort", "segment", "update")
 
-EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_destroy", "tc_closed_sum",
+EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_sync",
            "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_strerror", "tc_last_error"]
 
@@ -48,6 +48,7 @@ def load(path: str = LIB_PATH):
         "tc_create_shard": (vp, [u64, u64, u64, u64, i32, u64]),
         "tc_push_batch": (i32, [vp, vp, u64]),
         "tc_estimate": (i32, [vp, C.POINTER(C.c_double)]),
+        "tc_reset": (i32, [vp]),
         "tc_destroy": (None, [vp]),
         "tc_closed_sum": (i32, [vp, C.POINTER(u64)]),
         "tc_estimate_mom": (i32, [vp, u32, C.POINTER(C.c_double)]),

@@ -361,6 +361,22 @@ int tc_set_graphs(tc_ctx *ctx, int enable) {
     return TC_OK;
 }
 
+int tc_reset(tc_ctx *ctx) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK && rc != TC_ESTATE) return rc;
+    launch_init_state(ctx->st, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream));
+    if (ctx->ix.ctr) CK(cudaMemsetAsync(ctx->ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->m = 0;
+    ctx->b = 0;
+    ctx->S_slot = -1;
+    ctx->poisoned = 0;
+    return TC_OK;
+}
+
 int tc_sync(tc_ctx *ctx) {
     if (!ctx) return TC_EINVAL;
     return settle(ctx);
