@@ -154,23 +154,23 @@ def committed_traffic(config):
 
 # --------------------------------------------------------------------------------------------------
 def algorithmic_bytes(phase, w, R, D, fresh, r2old):
-    """Algorithmic bytes per launch (DESIGN.md "Roofline"): what each phase must move at minimum.
+    """Algorithmic bytes per launch (DESIGN.md §6): what each phase must move at minimum.
 
-    update : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
-             (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
-             index probes are L2 traffic at C2 and not counted.
-    stage  : read 8 B/edge (twice: histogram + stage); write E 8 + arcs 16 + pair slot 16 B/edge.
-    sort   : the 2 arcs of an edge read and written once (32 B/edge); extra radix passes are overhead.
-    segment: read sorted arcs 16 + write rank/end 16 B/edge; 16 B per vertex-table entry.
+    update    : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
+                (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
+                index probes are L2 traffic at C2 and not counted.
+    partition : read the batch once 8 B/edge; write E 8, the two bucketed arcs 16, the bucketed edge 16 B/edge.
+    pairs     : read the bucketed edge 16 B, write its 2 table slots 16 B.
+    vertices  : read the two bucketed arcs 16 B, write segS 8 + einfo 16 B per edge; 32 B (2 slots) per vertex.
     """
     if phase == "update":
         return 24 * (R - fresh) + 36 * fresh + 16 * r2old
-    if phase == "stage":
-        return 56 * w
-    if phase == "sort":
+    if phase == "partition":
+        return 48 * w
+    if phase == "pairs":
         return 32 * w
-    if phase == "segment":
-        return 32 * w + 16 * D
+    if phase == "vertices":
+        return 40 * w + 32 * D
     raise KeyError(phase)
 
 
@@ -297,9 +297,9 @@ def run_b200(args):
     nsteps = args.steps
     alg = {
         "update": algorithmic_bytes("update", 0, count * nsteps, 0, stats["fresh"], stats["r2_replaced_retained"]),
-        "stage": algorithmic_bytes("stage", edges_done, 0, stats["vertices"], 0, 0),
-        "sort": algorithmic_bytes("sort", edges_done, 0, 0, 0, 0),
-        "segment": algorithmic_bytes("segment", edges_done, 0, stats["vertices"], 0, 0),
+        "partition": algorithmic_bytes("partition", edges_done, 0, 0, 0, 0),
+        "pairs": algorithmic_bytes("pairs", edges_done, 0, 0, 0, 0),
+        "vertices": algorithmic_bytes("vertices", edges_done, 0, stats["vertices"], 0, 0),
     }
     ach = {p: alg[p] / (prof[p][0] / 1e3) / 1e9 for p in alg if prof.get(p) and prof[p][0] > 0}
     roofline = {"bound": "hbm", "kernel": "k_update (fused Steps 1-3 + partial sums)",

@@ -64,7 +64,7 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
  *         handle's device.  Host buffers are copied before the call returns; a device buffer must
  *         stay valid and unmodified until the next synchronising call (tc_sync, tc_estimate*,
  *         tc_get_state) when asynchronous errors are enabled, else until this call returns.
- *  w == 0: no-op (the batch index does not advance).
+ *  w == 0: no-op (the batch index does not advance); w > 2^28 -> TC_EINVAL.
  *  Rejects the whole batch (state and counters unchanged) with, in this priority order:
  *  TC_EINVAL (an id 0xFFFFFFFF), TC_ESELFLOOP, TC_EDUP, TC_EOVERFLOW.  Edges that repeat an edge of
  *  an EARLIER batch are not detected (each edge arrives once).
@@ -121,21 +121,32 @@ int tc_set_async(tc_ctx *ctx, int async_errors);
  * 0 (default): plain stream launches.  Results are identical; only launch overhead differs. */
 int tc_set_graphs(tc_ctx *ctx, int enable);
 
+/* tc_tune -- index-geometry knobs (tests / tuning).  Results never depend on them; only speed does.
+ *  TC_TUNE_VBUCKET_ARCS  target arcs per vertex bucket (default 1024; the bucket count is a power of two
+ *                        <= 4096 chosen from 2w / target)
+ *  TC_TUNE_VBUCKET_CAP   vertex buckets with more arcs than this (1..4096, default 4096) leave the common
+ *                        shared-memory hash path for the large-bucket kernel (radix sort on the vertex hash)
+ *  TC_TUNE_VBUCKET_SORT_CAP  large-bucket kernel: buckets with more arcs than this (1..6144, default 6144)
+ *                        are sorted in chunks through global memory instead of in shared memory
+ * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
+enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4 };
+int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
+
 /* tc_sync -- wait for all queued work; returns the first asynchronous error, if any. */
 int tc_sync(tc_ctx *ctx);
 
 /* tc_stream -- the handle's cudaStream_t (as void*), for events recorded by the caller. */
 void *tc_stream(tc_ctx *ctx);
 
-/* Profiling: when enabled, CUDA events bracket each kernel phase of every push.
- * tc_profile_read fills, for phase p < n (TC_PHASE_*): total milliseconds and launch count since
- * the last reset, and returns the number of phases.  Synchronises. */
+/* Profiling: when enabled, CUDA events bracket each kernel phase of every push (the pair phase on the
+ * handle's second stream, where it overlaps the vertex phase).  tc_profile_read fills, for phase p < n
+ * (TC_PHASE_*): total milliseconds and launch count since the last reset, and returns the number of
+ * phases.  Synchronises. */
 enum {
-    TC_PHASE_STAGE = 0,   /* a1+a3: digit histograms, staging, validation, edge-pair hash, arcs
-                             ranked by radix digit 0                                            */
-    TC_PHASE_SORT = 1,    /* a2: remaining stable radix passes of the arcs by vertex             */
-    TC_PHASE_SEGMENT = 2, /* a2: vertex table {deg_W, start}, per-arc rank / segment end         */
-    TC_PHASE_UPDATE = 3,  /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)       */
+    TC_PHASE_PARTITION = 0, /* a1: validation, bucket histograms, scans, stable scatter of arcs / edges  */
+    TC_PHASE_PAIRS = 1,     /* a3: edge-pair table (duplicates -> TC_EDUP), on the second stream         */
+    TC_PHASE_VERTICES = 2,  /* a2: per-bucket grouping of arcs by vertex, ranks / segment ends, vertex table */
+    TC_PHASE_UPDATE = 3,    /* a4-a8: the fused estimator update (Steps 1-3 + partial sums)              */
     TC_NPHASES = 4
 };
 int tc_profile(tc_ctx *ctx, int enable);

@@ -129,6 +129,11 @@ class TriangleCounter:
     def set_graphs(self, on: bool = True):
         self._ck(_lib.load().tc_set_graphs(self._h, 1 if on else 0), "tc_set_graphs")
 
+    def tune(self, **knobs):
+        """Index-geometry knobs (tc_tune): vbucket_arcs, vbucket_cap, vbucket_sort_cap."""
+        for k, v in knobs.items():
+            self._ck(_lib.load().tc_tune(self._h, _lib.TUNE[k], int(v)), f"tc_tune({k})")
+
     def sync(self) -> int:
         return _lib.load().tc_sync(self._h)
 

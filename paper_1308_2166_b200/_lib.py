@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libtc_b200.so")
+LIB_PATH = os.environ.get("TC_LIB_PATH") or os.path.join(PKG, "libtc_b200.so")  # override: A/B experiments
 
 TC_OK = 0
 TC_EINVAL = -1
@@ -18,10 +18,11 @@ TC_EOVERFLOW = -5
 TC_ECUDA = -6
 TC_ESTATE = -8
 TC_NPHASES = 4
-PHASES = ("stage", "sort", "segment", "update")
+PHASES = ("partition", "pairs", "vertices", "update")
+TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4}
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
-           "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_sync",
+           "tc_estimate_mom", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
            "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_strerror", "tc_last_error"]
 
 _lib = None
@@ -57,6 +58,7 @@ def load(path: str = LIB_PATH):
         "tc_counters": (i32, [vp, C.POINTER(u64), C.POINTER(u32)]),
         "tc_set_async": (i32, [vp, i32]),
         "tc_set_graphs": (i32, [vp, i32]),
+        "tc_tune": (i32, [vp, i32, u64]),
         "tc_sync": (i32, [vp]),
         "tc_stream": (vp, [vp]),
         "tc_profile": (i32, [vp, i32]),

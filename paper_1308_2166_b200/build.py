@@ -29,20 +29,23 @@ def stale() -> bool:
     return any(os.path.getmtime(os.path.join(CSRC, f)) > t for f in SOURCES + HEADERS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str = LIB, defines=()) -> str:
+    """Build the library (out: another path for an experimental variant, e.g. with -D defines)."""
+    if out == LIB and not force and not stale():
         return LIB
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc()] + NVCC_FLAGS + ["-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
+    out = os.path.abspath(out)
+    tmp = out + ".tmp%d" % os.getpid()
+    cmd = [nvcc()] + NVCC_FLAGS + [f"-D{d}" for d in defines] + ["-o", tmp] + [os.path.join(CSRC, f) for f in SOURCES]
     res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stderr)
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
-        f.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    if out == LIB:
+        with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
+            f.write(res.stderr)
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":

@@ -27,12 +27,12 @@ uint64_t next_pow2(uint64_t x) {
 struct tc_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;  // second stream: the edge-pair hash is built concurrently with the sort
-    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t side = nullptr;   // second stream: the edge-pair table, concurrently with the vertex buckets
+    cudaStream_t side2 = nullptr;  // third stream: the large vertex buckets
+    cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr;
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
-    uint32_t tag = 0;  // table tag of the last push (live slots carry the current push's tag)
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -43,13 +43,14 @@ struct tc_ctx {
     cudaEvent_t copy_done = nullptr;
     // profiling
     int prof = 0;
-    cudaEvent_t ev[TC_NPHASES + 1] = {};
+    cudaEvent_t ev[2 * TC_NPHASES] = {};  // begin / end of each phase (the pair phase on the side stream)
     double prof_ms[TC_NPHASES] = {};
     uint64_t prof_launch[TC_NPHASES] = {};
     int prof_pending = 0;
     // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
     int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
     cudaGraphExec_t gexec = nullptr;
+    Tuning tune;
 };
 
 static int fail_cuda(tc_ctx *c) {
@@ -64,51 +65,44 @@ static int fail_cuda(tc_ctx *c) {
     } while (0)
 
 static void free_index(IndexBufs &ix) {
-    cudaFree(ix.E);
-    cudaFree(ix.keyA);
-    cudaFree(ix.valA);
-    cudaFree(ix.keyB);
-    cudaFree(ix.valB);
-    cudaFree(ix.hist);
-    cudaFree(ix.cnt);
-    cudaFree(ix.einfo);
-    cudaFree(ix.vt);
-    cudaFree(ix.pt);
-    cudaFree(ix.ctr);
-    cudaFree(ix.stage);
+    void *bufs[] = {ix.E, ix.arcs, ix.scratch, ix.segS, ix.einfo, ix.vt, ix.vslice, ix.vperm, ix.pt,
+                    ix.cntV, ix.arank, ix.vstart, ix.ctr, ix.stage};
+    for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
 }
+
+constexpr uint64_t kMaxBuckets = 1ull << kMaxBucketBits;
+constexpr uint64_t kMaxBatch = 1ull << 28;  // 32-bit table offsets (vertex slices < 8 w slots)
+constexpr uint64_t kStartWords = kMaxBuckets + 8;  // vstart: bucket sizes -> prefixes (+ grand total)
 
 // (Re)allocate the per-batch index for batches of up to w edges.
 static int grow_index(tc_ctx *ctx, uint64_t w) {
     if (w <= ctx->ix.wcap) return TC_OK;
     CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->side));
+    CK(cudaStreamSynchronize(ctx->side2));
     free_index(ctx->ix);
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
-    const uint64_t vslots = next_pow2(4 * cap);  // D <= 2w vertices: load <= 50%
-    const uint64_t pslots = next_pow2(2 * cap);  // w pairs: load <= 50% (32 B buckets of 2)
-    ix.tiles_cap = (2 * cap + kRadixTile - 1) / kRadixTile;
-    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyA, 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.valA, 8 * cap) == cudaSuccess && cudaMalloc(&ix.keyB, 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.valB, 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.hist, 4 * kPasses * kRadix) == cudaSuccess &&
-              cudaMalloc(&ix.cnt, 4 * kRadix * ix.tiles_cap) == cudaSuccess &&
-              cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess && cudaMalloc(&ix.vt, 16 * vslots) == cudaSuccess &&
-              cudaMalloc(&ix.pt, 16 * pslots) == cudaSuccess && cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess &&
-              cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
+    ix.tiles_cap = (cap + kTileEdges - 1) / kTileEdges;
+    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.scratch, 16 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.segS, 16 * cap) == cudaSuccess && cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess &&
+              // vertex-table slices: bucket b owns [4 start_b, 4 start_b + 4 n_b) (next_pow2(2 D_b) < 4 n_b): 8 w slots
+              cudaMalloc(&ix.vt, 16 * 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess &&
+              cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
+              cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
+              cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
+              cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);
         return TC_ENOMEM;
     }
-    ix.vmask = (uint32_t)(vslots - 1);
-    ix.pmask = (uint32_t)(pslots - 1);
     ix.wcap = cap;
-    launch_init_tables(ix, ctx->stream);  // tag 0 everywhere: every slot free
-    CK(cudaGetLastError());
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
-    ctx->tag = 0;
     return TC_OK;
 }
 
@@ -130,6 +124,9 @@ static void destroy_ctx(tc_ctx *ctx) {
         if (e) cudaEventDestroy(e);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->side) cudaStreamDestroy(ctx->side);
+    if (ctx->side2) cudaStreamDestroy(ctx->side2);
+    if (ctx->join2) cudaEventDestroy(ctx->join2);
+    if (ctx->fork2) cudaEventDestroy(ctx->fork2);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
     if (ctx->join) cudaEventDestroy(ctx->join);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -140,7 +137,7 @@ extern "C" {
 
 tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t count, int device, uint64_t w_max_hint) {
     g_last_error = TC_OK;
-    if (r == 0 || first > r || count > r - first || w_max_hint > 0x7FFFFFFFull) {
+    if (r == 0 || first > r || count > r - first || w_max_hint > kMaxBatch) {
         g_last_error = TC_EINVAL;
         return nullptr;
     }
@@ -161,6 +158,16 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
         g_last_error = TC_ENOMEM;
         return nullptr;
     }
+    static uint64_t attrs = 0;  // devices whose kernel attributes (dynamic shared memory) are set
+    if (!(attrs >> (device & 63) & 1)) {
+        if (set_kernel_attributes() != 0) {
+            cudaGetLastError();
+            delete ctx;
+            g_last_error = TC_ECUDA;
+            return nullptr;
+        }
+        attrs |= 1ull << (device & 63);
+    }
     ctx->device = device;
     ctx->r = r;
     ctx->seed = seed;
@@ -170,11 +177,14 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
     const uint64_t n = std::max<uint64_t>(count, 1);
     bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->join2, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->fork2, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming) == cudaSuccess &&
               cudaMalloc(&ctx->st.r1, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.r2, 8 * n) == cudaSuccess &&
-              cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 8 * n) == cudaSuccess &&
-              cudaMalloc(&ctx->st.p2, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
+              cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 4 * n) == cudaSuccess &&
+              cudaMalloc(&ctx->st.p2, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
               cudaMalloc(&ctx->st.stats, 32) == cudaSuccess &&
               cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess;
@@ -215,6 +225,8 @@ static int decode_err(uint32_t e) {
 static int settle(tc_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
     CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaStreamSynchronize(ctx->side));
+    CK(cudaStreamSynchronize(ctx->side2));
     if (ctx->async_errors && !ctx->poisoned && ctx->ix.ctr) {
         CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost));
         const int code = decode_err(*ctx->h_err);
@@ -226,7 +238,7 @@ static int settle(tc_ctx *ctx) {
     if (ctx->prof_pending) {
         for (int p = 0; p < TC_NPHASES; ++p) {
             float ms = 0.f;
-            if (cudaEventElapsedTime(&ms, ctx->ev[p], ctx->ev[p + 1]) == cudaSuccess) ctx->prof_ms[p] += ms;
+            if (cudaEventElapsedTime(&ms, ctx->ev[2 * p], ctx->ev[2 * p + 1]) == cudaSuccess) ctx->prof_ms[p] += ms;
         }
         cudaGetLastError();
         ctx->prof_pending = 0;
@@ -238,7 +250,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     if (!ctx) return TC_EINVAL;
     if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
     if (w == 0) return TC_OK;
-    if (!edges || w > 0x7FFFFFFFull) return TC_EINVAL;
+    if (!edges || w > kMaxBatch) return TC_EINVAL;
     CK(cudaSetDevice(ctx->device));
     const bool ovf = ctx->m + w > 0x7FFFFFFFull;  // chi <= m must fit 31 bits (reading R13)
     if (ovf && ctx->async_errors) return TC_EOVERFLOW;  // async mode: reported first, state untouched
@@ -259,7 +271,6 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
                            attr.device == ctx->device;
     if (attr.type == cudaMemoryTypeDevice && attr.device != ctx->device) return TC_EINVAL;
     IndexBufs &ix = ctx->ix;
-    if (ctx->prof) CK(cudaEventRecord(ctx->ev[0], ctx->stream));
     if (on_device) {
         in = reinterpret_cast<const uint2 *>(edges);
     } else {
@@ -273,48 +284,58 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     const int slot = (int)((ctx->b + 1) & 1u);
     BatchArgs a;
     a.in = in;
-    a.w = (uint32_t)w;
     a.m_prev = ctx->m;
     a.batch = ctx->b;
     a.first = ctx->first;
     a.seed = ctx->seed;
     a.S_slot = slot;
-    const bool wrap = ++ctx->tag == 0xFFFFFFFFu;  // never reuse a tag a slot may still carry
-    if (wrap) ctx->tag = 1;
-    a.tag = ctx->tag;
-    // The batch's whole device sequence (counter resets + kernels) is captured as one CUDA graph and the
-    // previous graph executable is updated in place, so the ~17 launches run without host gaps.
+    a.g = make_geometry((uint32_t)w, ctx->tune);
+    // The batch's whole device sequence (counter resets + kernels) can be captured as one CUDA graph and the
+    // previous graph executable updated in place.
     const bool graph = ctx->use_graph != 0;
     if (graph) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     uint32_t launches = 0;
     {
         bool ok = true;
+        cudaStream_t ms = ctx->stream, ss = ctx->side, s2 = ctx->side2;
+        auto rec = [&](int e, cudaStream_t st) {
+            if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev[e], st) == cudaSuccess;
+        };
         if (ctx->async_errors) {
-            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ctx->stream) == cudaSuccess;  // keep the sticky error
-            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr + 1, 0, 4 * (kCtrWords - kCtrErr - 1), ctx->stream) == cudaSuccess;
+            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ms) == cudaSuccess;  // keep the sticky error
+            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr + 1, 0, 4 * (kCtrWords - kCtrErr - 1), ms) == cudaSuccess;
         } else {
-            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream) == cudaSuccess;
-            if (ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ctx->stream) == cudaSuccess;
+            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ms) == cudaSuccess;
+            if (ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
         }
-        ok = ok && cudaMemsetAsync(ix.hist, 0, 4 * kPasses * kRadix, ctx->stream) == cudaSuccess;
-        ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream) == cudaSuccess;
-        if (wrap) launch_init_tables(ix, ctx->stream);
-        // fork: the edge-pair hash (a3) on the side stream, joined before the estimator update
-        ok = ok && cudaEventRecord(ctx->fork, ctx->stream) == cudaSuccess;
-        ok = ok && cudaStreamWaitEvent(ctx->side, ctx->fork, 0) == cudaSuccess;
-        launches += launch_pairs(ix, a, ctx->side);
-        ok = ok && cudaEventRecord(ctx->join, ctx->side) == cudaSuccess;
-        int (*const phase_fn[TC_NPHASES])(const IndexBufs &, const BatchArgs &, cudaStream_t) = {
-            launch_stage, launch_sort, launch_segment, nullptr};
-        for (int p = 0; p < TC_NPHASES; ++p) {
-            if (p == TC_PHASE_UPDATE) ok = ok && cudaStreamWaitEvent(ctx->stream, ctx->join, 0) == cudaSuccess;
-            const int n = phase_fn[p] ? phase_fn[p](ix, a, ctx->stream) : launch_update(ix, ctx->st, a, ctx->stream);
-            launches += n;
-            if (ctx->prof) {
-                ok = ok && cudaEventRecord(ctx->ev[p + 1], ctx->stream) == cudaSuccess;
-                ctx->prof_launch[p] += n;
-            }
-        }
+        ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ms) == cudaSuccess;
+        // a3 on the second stream, concurrently with a1 and a2 (it reads only the raw batch)
+        ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
+        ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
+        rec(2 * TC_PHASE_PAIRS, ss);
+        launches += launch_pairs(ix, a, ss);
+        rec(2 * TC_PHASE_PAIRS + 1, ss);
+        ok = ok && cudaEventRecord(ctx->join, ss) == cudaSuccess;
+        // a1: count, scans, scatter
+        rec(2 * TC_PHASE_PARTITION, ms);
+        launches += launch_partition(ix, a, ms);
+        rec(2 * TC_PHASE_PARTITION + 1, ms);
+        ok = ok && cudaEventRecord(ctx->fork2, ms) == cudaSuccess;
+        // a2: the large vertex buckets on the third stream, the common ones on the main stream
+        ok = ok && cudaStreamWaitEvent(s2, ctx->fork2, 0) == cudaSuccess;
+        launches += launch_vertices_big(ix, a, s2);
+        ok = ok && cudaEventRecord(ctx->join2, s2) == cudaSuccess;
+        rec(2 * TC_PHASE_VERTICES, ms);
+        launches += launch_vertices(ix, a, ms);
+        ok = ok && cudaStreamWaitEvent(ms, ctx->join2, 0) == cudaSuccess;
+        rec(2 * TC_PHASE_VERTICES + 1, ms);
+        ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
+        rec(2 * TC_PHASE_UPDATE, ms);
+        launches += launch_update(ix, ctx->st, a, ms);
+        rec(2 * TC_PHASE_UPDATE + 1, ms);
+        if (ctx->prof)
+            for (int p = 0; p < TC_NPHASES; ++p)
+                ctx->prof_launch[p] += (p == TC_PHASE_PARTITION ? 4 : p == TC_PHASE_VERTICES ? 2 : 1);
         if (graph) {
             cudaGraph_t g = nullptr;
             const bool cap = cudaStreamEndCapture(ctx->stream, &g) == cudaSuccess && g;
@@ -359,6 +380,28 @@ int tc_set_graphs(tc_ctx *ctx, int enable) {
     if (rc != TC_OK) return rc;
     ctx->use_graph = enable ? 1 : 0;
     return TC_OK;
+}
+
+int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    switch (knob) {
+        case TC_TUNE_VBUCKET_ARCS:
+            if (value < 1 || value > (1u << 30)) return TC_EINVAL;
+            ctx->tune.vbucket_arcs = (uint32_t)value;
+            return TC_OK;
+        case TC_TUNE_VBUCKET_CAP:
+            if (value < 1 || value > 4096) return TC_EINVAL;
+            ctx->tune.vcap = (uint32_t)value;
+            return TC_OK;
+        case TC_TUNE_VBUCKET_SORT_CAP:
+            if (value < 1 || value > kVChunk) return TC_EINVAL;
+            ctx->tune.sortcap = (uint32_t)value;
+            return TC_OK;
+        default:
+            return TC_EINVAL;
+    }
 }
 
 int tc_reset(tc_ctx *ctx) {
@@ -447,8 +490,15 @@ int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint
     if (count == 0) return TC_OK;
     if (r1) CK(cudaMemcpy(r1, ctx->st.r1 + first, 8 * count, cudaMemcpyDeviceToHost));
     if (r2) CK(cudaMemcpy(r2, ctx->st.r2 + first, 8 * count, cudaMemcpyDeviceToHost));
-    if (p1) CK(cudaMemcpy(p1, ctx->st.p1 + first, 8 * count, cudaMemcpyDeviceToHost));
-    if (p2) CK(cudaMemcpy(p2, ctx->st.p2 + first, 8 * count, cudaMemcpyDeviceToHost));
+    if (p1 || p2) {  // stored as u32 (positions < 2^31, reading R13); 0xFFFFFFFF -> UINT64_MAX
+        std::vector<uint32_t> q(count);
+        for (int f = 0; f < 2; ++f) {
+            uint64_t *dst = f ? p2 : p1;
+            if (!dst) continue;
+            CK(cudaMemcpy(q.data(), (f ? ctx->st.p2 : ctx->st.p1) + first, 4 * count, cudaMemcpyDeviceToHost));
+            for (uint64_t i = 0; i < count; ++i) dst[i] = q[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)q[i];
+        }
+    }
     if (c || closed) {
         std::vector<uint32_t> cf(count);
         CK(cudaMemcpy(cf.data(), ctx->st.cf + first, 4 * count, cudaMemcpyDeviceToHost));

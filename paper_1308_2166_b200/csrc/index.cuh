@@ -1,18 +1,20 @@
-// index.cuh -- device data structures of the per-batch incidence index.
+// index.cuh -- device data structures of the per-batch incidence index (DESIGN.md §5 "HBM layout").
 //
 // Per batch W = <w_0 .. w_{s-1}> the GPU builds, in HBM:
-//   E[k]      uint2  normalized edge (lo < hi)                        (the F array's edges)
-//   sorted arcs: the 2|W| arcs (vertex, k<<1|side) stably radix-sorted by vertex.  Because arcs enter in
-//             arrival order, each vertex's run holds its arcs in increasing k: the rankAll order of
-//             Fig. 4 read backwards inside each src group (src asc, pos desc <=> rank asc,
-//             PAPER.md:730-734), so rank(x->y) of the arc at sorted slot s is segEnd(x) - 1 - s
-//             (Definition Rank).  segS = the sorted value array.
-//   vertex table (open addressing, 16 B slots, 2 per 32 B sector): {x, deg_W(x), segment start, tag}
-//   einfo[k]  uint4 {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
-//   edge-pair hash (16 B slots, 2 per sector): {lo<<32 | hi, k, tag}: Step 3's (src,dst)-sorted "edges"
-//             array with its multisearch replaced by one O(1) probe
-// A slot is live only when its tag equals the batch's tag, so the tables are never cleared; a slot is
-// claimed with one 128-bit CAS that installs key, payload and tag together.
+//   E[k]      uint2  normalised edge (lo < hi)                       (the F array's edges)
+//   segS[]    u32    the 2|W| arcs (k<<1 | side) grouped by vertex, arrival order inside a vertex: rankAll's
+//             (src asc, pos desc) order read backwards inside each src group, so
+//             rank(x->y) of the arc at slot s = segEnd(x) - 1 - s (Definition Rank).
+//             Vertices are grouped by BUCKET (the top bv bits of hash_vertex), each bucket owns the slot
+//             range of its arcs; inside a bucket vertices appear in hash order.
+//   einfo[k]  uint4  {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
+//   vertex table: one open-addressing slice per vertex bucket, sized next_pow2(2 D_b) for the bucket's
+//             D_b distinct vertices, 16 B slots {x, deg_W(x), segment start, 0}, at offset 4 * (the bucket's
+//             first arc slot) -- slices never overlap and need no prefix sum; vslice[b] = {offset, size}.
+//             Slices are written whole every batch (empty slots included), so the table needs no tags.
+//   edge-pair table: ceil(w / 2) groups of four 8-byte slots {k, fp} (one 32-byte sector per group, load
+//             <= 1/2), linear probing group by group; Step 3's (src,dst)-sorted "edges" array with its
+//             multisearch becomes one sector read (a fingerprint hit is verified against E[k]).
 #pragma once
 #include <cstdint>
 
@@ -27,34 +29,31 @@ constexpr uint32_t kErrInval = 1u;
 constexpr uint32_t kErrLoop = 2u;
 constexpr uint32_t kErrDup = 4u;
 constexpr uint32_t kErrOvf = 8u;
-// errors found while staging (they stop the index build); a duplicate (found by k_pairs concurrently) or
-// an overflow (set by the host) only stop the estimator update
+// errors found while counting (they stop the index build); a duplicate (found by the pair-bucket kernel,
+// concurrently with the vertex buckets) or an overflow (set by the host) only stop the estimator update
 constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 
-// radix sort of arcs by vertex id
-constexpr uint32_t kRadixBits = 8;
-constexpr uint32_t kRadix = 1u << kRadixBits;
-constexpr uint32_t kPasses = 32 / kRadixBits;
-constexpr uint32_t kSortThreads = 256;
-constexpr uint32_t kSortItems = 16;
-constexpr uint32_t kRadixTile = kSortThreads * kSortItems;  // arcs per radix tile (= 2048 edges)
-constexpr uint32_t kRunItems = 8;
-constexpr uint32_t kTile = kSortThreads * kRunItems;  // arcs per segment tile (k_runs / k_fix)
+// partitioning
+constexpr uint32_t kTileEdges = 2048;     // edges per count/scatter tile
+constexpr uint32_t kTileThreads = 512;
+constexpr uint32_t kMaxBucketBits = 12;   // at most 4096 vertex buckets
+constexpr uint32_t kVBucketThreads = 256; // vertex-bucket CTA
+constexpr uint32_t kVItems = 24;          // arcs per thread held in registers by the vertex-bucket sort
+constexpr uint32_t kVChunk = kVBucketThreads * kVItems;  // 6144 arcs: larger buckets take the chunked path
 
 // device counters (ctr[])
-constexpr int kCtrD = 0;    // vertices of W (claimed vertex-table slots)
-constexpr int kCtrErr = 3;  // error bits
+constexpr int kCtrD = 0;       // distinct vertices of W
+constexpr int kCtrTicket = 1;  // k_vbig's bucket ticket
+constexpr int kCtrBig = 2;     // vertex buckets handled by k_vbig
+constexpr int kCtrErr = 3;     // error bits
 constexpr int kCtrWords = 16;
 
 struct __align__(16) VSlot {
-    uint32_t key, deg, start, tag;
-};
-struct __align__(16) PSlot {
-    unsigned long long key;
-    uint32_t pos, tag;
+    uint32_t key, deg, start, pad;
 };
 
-__device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
+// lowbias32 (a bijection on 32 bits) and its inverse.
+__host__ __device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
     x ^= x >> 16;
     x *= 0x7feb352du;
     x ^= x >> 15;
@@ -62,67 +61,153 @@ __device__ __forceinline__ uint32_t hash_vertex(uint32_t x) {
     x ^= x >> 16;
     return x;
 }
+__host__ __device__ __forceinline__ uint32_t unhash_vertex(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x43021123u;
+    x ^= (x >> 15) ^ (x >> 30);
+    x *= 0x1d69e2a5u;
+    x ^= x >> 16;
+    return x;
+}
 
-__device__ __forceinline__ uint32_t hash_pair(unsigned long long key) {
-    uint64_t x = key;
+__host__ __device__ __forceinline__ uint64_t hash_pair64(uint64_t x) {
     x ^= x >> 33;
     x *= 0xff51afd7ed558ccdull;
     x ^= x >> 33;
     x *= 0xc4ceb9fe1a85ec53ull;
     x ^= x >> 33;
-    return (uint32_t)x;
+    return x;
 }
 
-__device__ __forceinline__ unsigned long long pair_key(uint32_t lo, uint32_t hi) {
-    return ((unsigned long long)lo << 32) | hi;
+__host__ __device__ __forceinline__ uint64_t pair_key(uint32_t lo, uint32_t hi) {
+    return ((uint64_t)lo << 32) | hi;
 }
 
-// Probe the complete (read-only) vertex table: {deg_W(v), segment start}, or {0, 0} when v is not in W.
-// One probe = one 32-byte sector holding two slots.
-__device__ __forceinline__ uint2 vt_find(const VSlot *__restrict__ vt, uint32_t mask, uint32_t tag, uint32_t v) {
-    uint32_t b = hash_vertex(v) & mask & ~1u;
+__host__ __device__ __forceinline__ uint32_t vbucket_of(uint32_t h, uint32_t bv) { return bv ? h >> (32 - bv) : 0u; }
+// slot position word (bits 20..51) and fingerprint (bits 0..31) of a pair hash
+__host__ __device__ __forceinline__ uint32_t pslot_word(uint64_t h) { return (uint32_t)(h >> 20); }
+__host__ __device__ __forceinline__ uint32_t pfinger(uint64_t h) { return (uint32_t)h; }
+__host__ __device__ __forceinline__ uint32_t pgroup_start(uint64_t h, uint32_t groups) {
+    return (uint32_t)(((uint64_t)pslot_word(h) * groups) >> 32);
+}
+
+struct Lookup {
+    const uint2 *E;
+    const VSlot *vt;
+    const uint2 *vslice;   // [BV] {offset, size}
+    uint32_t bv;
+    const uint2 *pt;       // pair slots {k, fp}, groups of 4
+    uint32_t G;            // pair-table groups
+};
+
+__host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) { return (w + 1) / 2; }
+
+// Continue a vertex probe at slot pair b of slice sl (after the first pair missed without an empty slot).
+static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uint32_t b, uint32_t v) {
+    const uint32_t mask = sl.y - 1u;
     while (true) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(vt + b);
+        b = (b + 2) & mask;
+        const uint4 *p = reinterpret_cast<const uint4 *>(L.vt + sl.x + b);
         const uint4 s0 = __ldg(p), s1 = __ldg(p + 1);
-        const bool l0 = s0.w == tag, l1 = s1.w == tag;
-        if (l0 && s0.x == v) return make_uint2(s0.y, s0.z);
-        if (l1 && s1.x == v) return make_uint2(s1.y, s1.z);
-        if (!l0 || !l1) return make_uint2(0u, 0u);
-        b = (b + 2) & mask;
+        if (s0.x == v) return make_uint2(s0.y, s0.z);
+        if (s1.x == v) return make_uint2(s1.y, s1.z);
+        if (s0.x == kEmptyV || s1.x == kEmptyV) return make_uint2(0u, 0u);
     }
 }
 
-// Two independent vertex probes whose first sectors are requested together.
-__device__ __forceinline__ void vt_find2(const VSlot *__restrict__ vt, uint32_t mask, uint32_t tag, uint32_t u,
-                                         uint32_t v, uint2 &iu, uint2 &iv) {
-    const uint32_t bu = hash_vertex(u) & mask & ~1u, bv = hash_vertex(v) & mask & ~1u;
-    const uint4 *pu = reinterpret_cast<const uint4 *>(vt + bu);
-    const uint4 *pv = reinterpret_cast<const uint4 *>(vt + bv);
-    const uint4 u0 = __ldg(pu), u1 = __ldg(pu + 1), v0 = __ldg(pv), v1 = __ldg(pv + 1);
-    const bool lu0 = u0.w == tag, lu1 = u1.w == tag, lv0 = v0.w == tag, lv1 = v1.w == tag;
-    if (lu0 && u0.x == u) iu = make_uint2(u0.y, u0.z);
-    else if (lu1 && u1.x == u) iu = make_uint2(u1.y, u1.z);
-    else if (!lu0 || !lu1) iu = make_uint2(0u, 0u);
-    else iu = vt_find(vt, mask, tag, u);  // rare: first bucket full without u
-    if (lv0 && v0.x == v) iv = make_uint2(v0.y, v0.z);
-    else if (lv1 && v1.x == v) iv = make_uint2(v1.y, v1.z);
-    else if (!lv0 || !lv1) iv = make_uint2(0u, 0u);
-    else iv = vt_find(vt, mask, tag, v);
+// Pair probe split in two so that its loads can be issued together with other probes:
+// pt_issue() reads the bucket's group range and the home group (one 32-byte sector); pt_resolve() scans
+// it and walks on group by group.  Inside a group the filled slots form a prefix, so the first empty slot
+// ends the search.  Result: batch position of {lo, hi} (lo < hi), or -1.
+struct PairProbe {
+    uint32_t lo, hi, fp, g, ng;
+    const uint2 *sl;
+    uint4 q0, q1;
+};
+
+__device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t hi, bool active, PairProbe &P) {
+    const uint64_t h = hash_pair64(pair_key(lo, hi));
+    const uint32_t ng = active ? L.G : 0u;
+    P.lo = lo;
+    P.hi = hi;
+    P.fp = pfinger(h);
+    P.ng = ng;
+    P.sl = L.pt;  // 32-byte aligned
+    P.g = ng ? pgroup_start(h, ng) : 0u;
+    P.q0 = P.q1 = make_uint4(kEmptyV, 0u, kEmptyV, 0u);
+    if (ng) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * P.g);
+        P.q0 = __ldg(q);
+        P.q1 = __ldg(q + 1);
+    }
 }
 
-// Probe the complete (read-only) edge-pair hash: batch position of (lo, hi) or -1.
-__device__ __forceinline__ int64_t pt_find(const PSlot *__restrict__ pt, uint32_t mask, uint32_t tag,
-                                           unsigned long long key) {
-    uint32_t b = hash_pair(key) & mask & ~1u;
+// 0: not in the group and the group has room (absent); 1: found (*k set); 2: group full, go on.
+__device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uint4 q0, uint4 q1, uint32_t *k) {
+    const uint32_t ks[4] = {q0.x, q0.z, q1.x, q1.z}, fs[4] = {q0.y, q0.w, q1.y, q1.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (ks[i] == kEmptyV) return 0;
+        if (fs[i] == P.fp) {
+            const uint2 e = __ldg(L.E + ks[i]);
+            if (e.x == P.lo && e.y == P.hi) {
+                *k = ks[i];
+                return 1;
+            }
+        }
+    }
+    return 2;
+}
+
+static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
+    uint32_t g = P.g;
     while (true) {
-        const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(pt + b);
-        const ulonglong2 s0 = __ldg(p), s1 = __ldg(p + 1);
-        const bool l0 = (uint32_t)(s0.y >> 32) == tag, l1 = (uint32_t)(s1.y >> 32) == tag;
-        if (l0 && s0.x == key) return (int64_t)(uint32_t)s0.y;
-        if (l1 && s1.x == key) return (int64_t)(uint32_t)s1.y;
-        if (!l0 || !l1) return -1;
-        b = (b + 2) & mask;
+        g = (g + 1 == P.ng) ? 0u : g + 1;
+        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * g);
+        uint32_t k;
+        const int r = pt_group(L, P, __ldg(q), __ldg(q + 1), &k);
+        if (r == 0) return -1;
+        if (r == 1) return (int64_t)k;
     }
+}
+
+__device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &P) {
+    if (P.ng == 0) return -1;
+    uint32_t k;
+    const int r = pt_group(L, P, P.q0, P.q1, &k);
+    if (r == 0) return -1;
+    if (r == 1) return (int64_t)k;
+    return pt_walk(L, P);
+}
+
+__device__ __forceinline__ int64_t pt_find(const Lookup &L, uint32_t lo, uint32_t hi) {
+    PairProbe P;
+    pt_issue(L, lo, hi, true, P);
+    return pt_resolve(L, P);
+}
+
+// Vertex probe split likewise: first sector (two 16-byte slots) of each of u and v.
+struct VertProbe {
+    uint2 sl;
+    uint32_t b;
+    uint4 s0, s1;
+};
+
+__device__ __forceinline__ void vt_issue(const Lookup &L, uint32_t v, VertProbe &P) {
+    const uint32_t h = hash_vertex(v);
+    P.sl = __ldg(L.vslice + vbucket_of(h, L.bv));
+    P.b = h & (P.sl.y - 1u) & ~1u;
+    const uint4 *p = reinterpret_cast<const uint4 *>(L.vt + (P.sl.y ? P.sl.x + P.b : 0u));
+    P.s0 = __ldg(p);
+    P.s1 = __ldg(p + 1);
+}
+
+__device__ __forceinline__ uint2 vt_resolve(const Lookup &L, const VertProbe &P, uint32_t v) {
+    if (P.sl.y == 0) return make_uint2(0u, 0u);
+    if (P.s0.x == v) return make_uint2(P.s0.y, P.s0.z);
+    if (P.s1.x == v) return make_uint2(P.s1.y, P.s1.z);
+    if (P.s0.x == kEmptyV || P.s1.x == kEmptyV) return make_uint2(0u, 0u);
+    return vt_find_from(L, P.sl, P.b, v);
 }
 
 }  // namespace tcb

@@ -1,23 +1,27 @@
 // kernels.cu -- the per-batch hot path of bulkUpdateAll on sm_100a.
 //
-// Pipeline for one batch W; tiles are 2048 edges = 4096 arcs:
-//   k_hist       a1      : per-tile counts of digit 0 of the arc keys, global histograms of all digits
-//   k_scan               : per digit, exclusive scan over tiles + digit base = each tile's output offsets
-//   k_stage      a1 + a3 : load W (coalesced), validate, normalize to (lo, hi); insert every edge into the
-//                          edge-pair hash (one 128-bit CAS per claim, 8 inserts in flight per thread);
-//                          rank the tile's arcs (vertex, k<<1|side) stably by digit 0 and scatter them --
-//                          the F array of rankAll's proof, already radix pass 0
-//   k_upsweep / k_scan / k_downsweep  a2 : the remaining stable LSD radix passes over the arcs by vertex id
-//                          (passes whose digit is 0 for every arc are skipped on the device).  Stability
-//                          keeps arrival order inside a vertex: this replaces rankAll's sort by (src, -pos)
-//                          (PAPER.md:680-684).
-//   k_runs       a2      : runs of equal vertex inside each tile -> vertex table {deg_W, segment start};
-//                          rank / segment end of the arcs of tile-internal segments
-//   k_fix        a2      : rank / segment end of the arcs of segments that cross tile boundaries
-//   k_update     a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2 (chi^+
-//                          from ranks / degrees, level-2 pick by segment arithmetic), Step 3 (closing-edge
-//                          probe), block partial sums of chi over closed estimators
-// rank(x->y) of the arc at sorted slot s = segEnd(x) - 1 - s (Definition Rank).
+// Pipeline for one batch W.  Every index structure is PARTITIONED first and then built
+// bucket by bucket in shared memory, so the global tables are written whole, coalesced, and stay small
+// enough to live in L2 while the estimator pass probes them:
+//   k_count      a1      : load W (coalesced), validate, per-tile histograms of vertex buckets (top bv bits of
+//                          hash_vertex, 2 arcs per edge) and pair buckets (top bp bits of hash_pair64)
+//   k_scan_rows / k_scan_tot : per-(bucket, tile) offsets inside the bucket and bucket sizes, then bucket
+//                          starts (exclusive scans)
+//   k_scatter    a1      : normalise, write E; scatter the arcs (vertex, k<<1|side) to their vertex bucket,
+//                          STABLY (ballot ranks inside the tile), so each bucket holds its arcs in arrival
+//                          order -- the F array of rankAll's proof, partitioned; scatter
+//                          the edges {lo, hi, k} to their pair bucket
+//   k_pbuckets   a3      : (second stream) one CTA per pair bucket: open-addressing slice built in shared
+//                          memory, written out whole; a repeated pair is TC_EDUP
+//   k_vbuckets   a2      : one CTA per vertex bucket: stable radix sort of the bucket's arcs by vertex hash in
+//                          shared memory (replaces rankAll's sort by (src, -pos)), segment
+//                          runs -> segS, per-arc {slot, segEnd} (rank = segEnd - 1 - slot, Def. Rank
+//                          PAPER.md:589-600), vertex-table slice {deg_W, start} whose offset comes from a
+//                          decoupled look-back over the buckets; oversized buckets (hubs) take a chunked
+//                          global-memory path in the same kernel
+//   k_update     a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2 (chi^+ from
+//                          ranks / degrees, level-2 pick by segment arithmetic), Step 3 (closing-edge probe),
+//                          block partial sums of chi over closed estimators
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,593 +34,982 @@
 namespace tcb {
 
 typedef unsigned __int128 u128;
+constexpr uint32_t kFull = 0xffffffffu;
 
-__device__ __forceinline__ u128 pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-    return (u128)a | ((u128)b << 32) | ((u128)c << 64) | ((u128)d << 96);
-}
-__device__ __forceinline__ u128 pack2(unsigned long long a, unsigned long long b) {
-    return (u128)a | ((u128)b << 64);
-}
-
-constexpr uint32_t kTileEdges = kRadixTile / 2;
-constexpr uint32_t kWarps = kSortThreads / 32;
-
-// Arc keys are vertex ids; pass p sorts by digit (key >> 8p) & 255.
-__device__ __forceinline__ uint32_t digit_of(uint32_t key, uint32_t pass) {
-    return (key >> (pass * kRadixBits)) & (kRadix - 1);
-}
-
-// A pass is trivial (identity) when every arc has digit 0 there.
-__device__ __forceinline__ bool pass_trivial(const uint32_t *hist, uint32_t p, uint32_t n) {
-    return hist[p * kRadix] == n;
-}
-// k_stage always writes pass 0's output to buffer B; each executed later pass flips A/B.
-__device__ __forceinline__ bool in_buffer_B(const uint32_t *hist, uint32_t upto, uint32_t n) {
-    uint32_t e = 0;
-    for (uint32_t p = 1; p < upto; ++p) e += pass_trivial(hist, p, n) ? 0u : 1u;
-    return (e & 1u) == 0;
-}
-
-// Edge-tile loads: thread i takes edges i, i+256, ... of the tile (coalesced 8-byte loads).
 __device__ __forceinline__ uint2 norm_edge(uint2 e) { return make_uint2(min(e.x, e.y), max(e.x, e.y)); }
 
-// ------------------------------------------------------------------------------------------------
-// a1: digit histograms
-
-__global__ void __launch_bounds__(kSortThreads) k_hist(const uint2 *__restrict__ in, uint32_t w, uint32_t *hist,
-                                                        uint32_t *cnt, uint32_t ntiles, const uint32_t *ctr) {
-    // (a duplicate found by k_pairs of this very batch must not stop staging: only stage errors here)
-    if (ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
-    __shared__ uint32_t sh[kPasses][kRadix];
-    for (uint32_t i = threadIdx.x; i < kPasses * kRadix; i += kSortThreads) (&sh[0][0])[i] = 0;
-    __syncthreads();
-    const uint32_t e0 = blockIdx.x * kTileEdges;
-#pragma unroll 4
-    for (uint32_t i = threadIdx.x; i < kTileEdges; i += kSortThreads) {
-        if (e0 + i >= w) break;
-        const uint2 e = norm_edge(__ldg(in + e0 + i));
+// Lanes of the warp holding the same nbits-bit digit d (invalid lanes group together).  nbits is
+// warp-uniform.  One ballot per digit bit.
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid, uint32_t nbits) {
+    uint32_t m = __ballot_sync(kFull, valid);
+    if (!valid) m = ~m;
 #pragma unroll
-        for (uint32_t p = 0; p < kPasses; ++p) {
-            atomicAdd(&sh[p][digit_of(e.x, p)], 1u);
-            atomicAdd(&sh[p][digit_of(e.y, p)], 1u);
+    for (uint32_t b = 0; b < kMaxBucketBits; ++b) {
+        if (b < nbits) {
+            const uint32_t bit = (d >> b) & 1u;
+            m &= __ballot_sync(kFull, bit) ^ (bit - 1u);  // lanes whose bit b equals mine
         }
     }
-    __syncthreads();
-    const uint32_t d = threadIdx.x;  // kSortThreads == kRadix
-    cnt[d * ntiles + blockIdx.x] = sh[0][d];
-#pragma unroll
-    for (uint32_t p = 0; p < kPasses; ++p)
-        if (sh[p][d]) atomicAdd(hist + p * kRadix + d, sh[p][d]);
+    return m;
 }
 
-// Per-tile digit counts of pass p >= 1 (the keys as left by the previous executed pass).
-__global__ void __launch_bounds__(kSortThreads) k_upsweep(const uint32_t *keyA, const uint32_t *keyB, uint32_t n,
-                                                          const uint32_t *hist, uint32_t pass, uint32_t *cnt,
-                                                          uint32_t ntiles, const uint32_t *ctr) {
-    if (ctr[kCtrErr] || pass_trivial(hist, pass, n)) return;
-    const uint32_t *__restrict__ kin = in_buffer_B(hist, pass, n) ? keyB : keyA;
-    __shared__ uint32_t sh[kRadix];
-    sh[threadIdx.x] = 0;
-    __syncthreads();
-    const uint32_t t0 = blockIdx.x * kRadixTile;
-    const uint4 *k4 = reinterpret_cast<const uint4 *>(kin + t0);
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems / 4; ++j) {
-        const uint32_t q = threadIdx.x + j * kSortThreads;
-        if (t0 + 4 * q + 3 < n) {
-            const uint4 v = __ldcs(k4 + q);
-            atomicAdd(&sh[digit_of(v.x, pass)], 1u);
-            atomicAdd(&sh[digit_of(v.y, pass)], 1u);
-            atomicAdd(&sh[digit_of(v.z, pass)], 1u);
-            atomicAdd(&sh[digit_of(v.w, pass)], 1u);
-        } else {
-            for (uint32_t u = 0; u < 4; ++u)
-                if (t0 + 4 * q + u < n) atomicAdd(&sh[digit_of(kin[t0 + 4 * q + u], pass)], 1u);
-        }
-    }
-    __syncthreads();
-    cnt[threadIdx.x * ntiles + blockIdx.x] = sh[threadIdx.x];
+// The same with one __match_any_sync (cheaper than ballots for wide digits).
+__device__ __forceinline__ uint32_t match_peers(uint32_t d, bool valid) {
+    return __match_any_sync(kFull, valid ? d : 0xFFFFFFFFu);
 }
 
-// One block per digit: offsets[d][t] = sum_{d' < d} hist[d'] + sum_{t' < t} cnt[d][t'].
-__global__ void __launch_bounds__(kSortThreads) k_scan(uint32_t *cnt, uint32_t ntiles, const uint32_t *hist,
-                                                       uint32_t pass, uint32_t n, const uint32_t *ctr) {
-    if (ctr[kCtrErr]) return;
-    if (pass > 0 && pass_trivial(hist, pass, n)) return;
-    __shared__ uint32_t ws[kWarps];
-    const uint32_t d = blockIdx.x, lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    // digit base
-    uint32_t hv = threadIdx.x < d ? hist[pass * kRadix + threadIdx.x] : 0u;
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) hv += __shfl_xor_sync(0xffffffffu, hv, off);
-    if (lane == 0) ws[warp] = hv;
-    __syncthreads();
-    uint32_t base = 0;
-    for (uint32_t x = 0; x < kWarps; ++x) base += ws[x];
-    __syncthreads();
-    // exclusive scan of the digit's row, chunk per thread
-    uint32_t *row = cnt + (size_t)d * ntiles;
-    const uint32_t per = (ntiles + kSortThreads - 1) / kSortThreads;
-    const uint32_t c0 = threadIdx.x * per, c1 = min(ntiles, c0 + per);
-    uint32_t local = 0;
-    for (uint32_t i = c0; i < c1; ++i) local += row[i];
-    uint32_t incl = local;
+// Block-wide exclusive scan of one value per thread (NT threads); returns the prefix, *total the sum.
+template <int NT>
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *sh_warp, uint32_t *total) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t incl = x;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        const uint32_t y = __shfl_up_sync(kFull, incl, off);
         if (lane >= (uint32_t)off) incl += y;
     }
-    if (lane == 31) ws[warp] = incl;
+    if (lane == 31) sh_warp[warp] = incl;
     __syncthreads();
-    uint32_t run = base + incl - local;
-    for (uint32_t x = 0; x < warp; ++x) run += ws[x];
+    if (warp == 0) {
+        uint32_t v = lane < NT / 32 ? sh_warp[lane] : 0u;
+        uint32_t iv = v;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, iv, off);
+            if (lane >= (uint32_t)off) iv += y;
+        }
+        if (lane < NT / 32) sh_warp[lane] = iv - v;
+        if (lane == NT / 32 - 1) sh_warp[NT / 32] = iv;
+    }
+    __syncthreads();
+    const uint32_t r = sh_warp[warp] + incl - x;
+    *total = sh_warp[NT / 32];
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------------------------------------------------------
+// a1: bucket histograms
+
+struct PartArgs {
+    const uint2 *in;
+    Geometry g;
+    uint2 *E;
+    uint4 *arcs;  // {vertex, k<<1|side, neighbour, 0}
+    uint32_t *cntV;    // [nV * tiles]
+    uint16_t *arank;   // [2 w] in-tile ranks
+    uint32_t *vstart;  // bucket sizes (k_scan_rows) -> exclusive prefixes (k_scan_tot)
+    uint32_t *ctr;
+};
+
+// Tile ranking: validate and normalise W, write E, and rank every arc (by vertex bucket) and every edge (by
+// pair bucket) inside its tile, stably in arrival order.  Arc a of the tile (a = 2 e + side) is owned by
+// warp a / kArcsPerWarp, round (a % kArcsPerWarp) / 32, lane a % 32; edges likewise.  Ranks come from
+// ballots and per-warp counters (no shared-memory atomics: they cost 2 cycles per lane on this part).
+constexpr uint32_t kTileWarps = kTileThreads / 32;
+constexpr uint32_t kArcRounds = 2 * kTileEdges / kTileThreads;   // 16
+constexpr uint32_t kEdgeRounds = kTileEdges / kTileThreads;      // 8
+constexpr uint32_t kArcsPerWarp = kArcRounds * 32, kEdgesPerWarp = kEdgeRounds * 32;
+
+__global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
+    if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
+    extern __shared__ uint32_t dsh[];
+    const uint32_t nV = 1u << a.g.bv;
+    uint16_t *wv = reinterpret_cast<uint16_t *>(dsh);  // [kTileWarps][nV]
+    for (uint32_t i = threadIdx.x; i < kTileWarps * nV / 2; i += kTileThreads) dsh[i] = 0;
+    __syncthreads();
+    const uint32_t t = blockIdx.x, e0 = t * kTileEdges;
+    const uint32_t ne = min(kTileEdges, a.g.w - e0);
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    // edges: validate, normalise, E
+    uint32_t bad = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kEdgeRounds; ++j) {
+        const uint32_t i = warp * kEdgesPerWarp + j * 32u + lane;
+        if (i < ne) {
+            const uint2 e = __ldg(a.in + e0 + i);
+            if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
+            else if (e.x == e.y) bad |= kErrLoop;
+            a.E[e0 + i] = norm_edge(e);
+        }
+    }
+    bad = __reduce_or_sync(kFull, bad);
+    if (bad && lane == 0) atomicOr(&a.ctr[kCtrErr], bad);
+    // arcs: stable rank by vertex bucket (this warp's edges, re-read through L1)
+    uint32_t pa[kArcRounds];
+#pragma unroll
+    for (uint32_t j = 0; j < kArcRounds; ++j) {
+        const uint32_t ai = warp * kArcsPerWarp + j * 32u + lane;
+        const bool valid = (ai >> 1) < ne;
+        uint32_t d = 0;
+        if (valid) {
+            const uint2 n = norm_edge(__ldg(a.in + e0 + (ai >> 1)));
+            d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bv);
+        }
+        const uint32_t peers = digit_peers(d, valid, a.g.bv);
+        const uint32_t before = __popc(peers & lt);
+        uint32_t c = 0;
+        if (valid) c = wv[warp * nV + d];
+        __syncwarp();
+        if (valid && before == 0) wv[warp * nV + d] = (uint16_t)(c + __popc(peers));
+        __syncwarp();
+        pa[j] = valid ? (d << 16) | (c + before) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    // per bucket: exclusive prefix over warps, tile count
+    for (uint32_t d = threadIdx.x; d < nV; d += kTileThreads) {
+        uint32_t run = 0;
+#pragma unroll
+        for (uint32_t x = 0; x < kTileWarps; ++x) {
+            const uint32_t c = wv[x * nV + d];
+            wv[x * nV + d] = (uint16_t)run;
+            run += c;
+        }
+        a.cntV[d * a.g.tiles + t] = run;
+    }
+    __syncthreads();
+    // in-tile ranks (coalesced u16 stores)
+#pragma unroll
+    for (uint32_t j = 0; j < kArcRounds; ++j) {
+        if (pa[j] == 0xFFFFFFFFu) continue;
+        const uint32_t ai = warp * kArcsPerWarp + j * 32u + lane;
+        const uint32_t d = pa[j] >> 16;
+        a.arank[2 * e0 + ai] = (uint16_t)(wv[warp * nV + d] + (pa[j] & 0xFFFFu));
+    }
+}
+
+// One block: vertex-bucket sizes -> exclusive prefixes (entry nV = 2w); vperm = the vertex buckets with more
+// than vcap arcs (processed by k_vbig, concurrently with k_vhash), then the others; ctr[kCtrBig] = how many
+// are large.
+__global__ void __launch_bounds__(1024) k_scan_tot(uint32_t *vstart, uint32_t nV, uint32_t vcap, uint32_t *vperm,
+                                                   uint32_t *ctr) {
+    if (ctr[kCtrErr] & kErrStage) return;
+    __shared__ uint32_t ws[33];
+    const uint32_t i0 = threadIdx.x * 4;  // nV <= 4096: 4 per thread
+    uint32_t v[4], s = 0, big = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        v[q] = i0 + q < nV ? vstart[i0 + q] : 0u;
+        s += v[q];
+        big += (i0 + q < nV && v[q] > vcap) ? 1u : 0u;
+    }
+    uint32_t nbig;
+    uint32_t pb = block_exclusive_scan<1024>(big, ws, &nbig);
+    uint32_t ps = nbig + min(i0, nV) - pb;  // small buckets before mine go after all the large ones
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<1024>(s, ws, &tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (i0 + q < nV) {
+            vstart[i0 + q] = run;
+            if (v[q] > vcap) vperm[pb++] = i0 + q;
+            else vperm[ps++] = i0 + q;
+        }
+        run += v[q];
+    }
+    if (threadIdx.x == 0) {
+        vstart[nV] = tot;
+        ctr[kCtrBig] = nbig;
+    }
+}
+
+// One block per vertex-bucket row: cnt[b][t] -> sum_{t' < t} cnt[b][t'] (the tile's offset inside the
+// bucket); the row total (the bucket size) goes to vstart[b].
+__global__ void __launch_bounds__(256) k_scan_rows(uint32_t *cntV, uint32_t *vstart, uint32_t tiles, const uint32_t *ctr) {
+    if (ctr[kCtrErr] & kErrStage) return;
+    __shared__ uint32_t ws[9];
+    const uint32_t b = blockIdx.x;
+    uint32_t *row = cntV + (size_t)b * tiles;
+    const uint32_t per = (tiles + 255) / 256;
+    const uint32_t c0 = threadIdx.x * per, c1 = min(tiles, c0 + per);
+    uint32_t local = 0;
+    for (uint32_t i = c0; i < c1; ++i) local += row[i];
+    uint32_t tot;
+    uint32_t run = block_exclusive_scan<256>(local, ws, &tot);
     for (uint32_t i = c0; i < c1; ++i) {
         const uint32_t c = row[i];
         row[i] = run;
         run += c;
     }
+    if (threadIdx.x == 0) vstart[b] = tot;
 }
 
-// Lanes of the warp whose 8-bit digit equals d (d == kRadix: no arc), from 9 ballots instead of
-// __match_any_sync (a slow MIO op on this part).
-__device__ __forceinline__ uint32_t digit_peers(uint32_t d) {
-    uint32_t m = __ballot_sync(0xffffffffu, d < kRadix);
-    if (d >= kRadix) m = ~m;
-#pragma unroll
-    for (uint32_t b = 0; b < kRadixBits; ++b) {
-        const uint32_t v = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-        m &= ((d >> b) & 1u) ? v : ~v;
-    }
-    return m;
-}
-
-// Stable in-tile ranks by digit: warp w owns arcs [512w, 512w+512) of the tile in 16 rounds of 32.
-// On return whist[w][d] = arcs of digit d in warps < w, and rnk[j] = rank among digit-d arcs of warp w.
-__device__ __forceinline__ void rank_tile(const uint32_t (&dg)[kSortItems], uint32_t (&rnk)[kSortItems],
-                                          uint32_t (*whist)[kRadix]) {
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t lt = (1u << lane) - 1u;
-    for (uint32_t i = threadIdx.x; i < kWarps * kRadix; i += kSortThreads) (&whist[0][0])[i] = 0;
+// Tile scatter: arc {vertex, k<<1|side, neighbour} -> arcs[start(bucket) + offset(bucket, tile) + rank in
+// tile].  Pure streaming: the ranks come from k_count.
+__global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
+    if (a.ctr[kCtrErr] & kErrStage) return;
+    extern __shared__ uint32_t dsh[];
+    const uint32_t nV = 1u << a.g.bv;
+    uint32_t *soff = dsh;
+    const uint32_t t = blockIdx.x, e0 = t * kTileEdges;
+    const uint32_t ne = min(kTileEdges, a.g.w - e0);
+    for (uint32_t d = threadIdx.x; d < nV; d += kTileThreads) soff[d] = a.vstart[d] + a.cntV[d * a.g.tiles + t];
     __syncthreads();
+    constexpr uint32_t kPer = 2 * kTileEdges / kTileThreads;
+    uint2 n[kPer];
+    uint32_t r[kPer];
 #pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t d = dg[j];  // kRadix marks "no arc"
-        const uint32_t peers = digit_peers(d);
-        const uint32_t before = __popc(peers & lt);
-        uint32_t b = 0;
-        if (d < kRadix) b = whist[warp][d];
-        __syncwarp();
-        if (d < kRadix && before == 0) whist[warp][d] = b + __popc(peers);
-        __syncwarp();
-        rnk[j] = b + before;
+    for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t ai = threadIdx.x + q * kTileThreads;
+        if (ai < 2 * ne) {
+            n[q] = a.E[e0 + (ai >> 1)];
+            r[q] = a.arank[2 * e0 + ai];
+        }
     }
-    __syncthreads();
-    const uint32_t dd = threadIdx.x;  // per digit: exclusive prefix over warps (warp order == arc order)
-    uint32_t tot = 0;
 #pragma unroll
-    for (uint32_t x = 0; x < kWarps; ++x) {
-        const uint32_t c = whist[x][dd];
-        whist[x][dd] = tot;
-        tot += c;
+    for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t ai = threadIdx.x + q * kTileThreads;
+        if (ai < 2 * ne) {
+            const uint32_t v = (ai & 1u) ? n[q].y : n[q].x;
+            const uint32_t nb = (ai & 1u) ? n[q].x : n[q].y;
+            __stcs(a.arcs + soff[vbucket_of(hash_vertex(v), a.g.bv)] + r[q], make_uint4(v, 2u * e0 + ai, nb, 0u));
+        }
     }
-    __syncthreads();
 }
 
 // ------------------------------------------------------------------------------------------------
-// a1 + a3 (+ radix pass 0): staging, validation, edge-pair hash, arcs
+// a3: pair-table slices
 
-struct StageCtx {
-    uint2 *E;
-    uint32_t *keyB, *valB;  // pass-0 output
-    const uint32_t *off;    // scanned per-tile digit-0 offsets
-    const uint32_t *hist;
-    uint32_t ntiles;
-    PSlot *pt;
-    uint32_t pmask;
-    uint32_t tag;
-    uint32_t *ctr;
-};
-
-__global__ void __launch_bounds__(kSortThreads, 3) k_stage(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
-    if (c.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
-    __shared__ uint2 sedge[kTileEdges];
-    __shared__ uint32_t whist[kWarps][kRadix];
-    __shared__ uint32_t soff[kRadix];
-    const uint32_t e0 = blockIdx.x * kTileEdges;
-    const uint32_t ne = min(kTileEdges, w - e0);
-    const bool trivial0 = pass_trivial(c.hist, 0, 2 * w);
-    soff[threadIdx.x] = c.off[threadIdx.x * c.ntiles + blockIdx.x];
-    // per edge: validate, normalize, E (the edge-pair hash is filled concurrently by k_pairs)
-    constexpr uint32_t kPer = kTileEdges / kSortThreads;
-    uint32_t bad = 0;
-#pragma unroll
-    for (uint32_t j = 0; j < kPer; ++j) {
-        const uint32_t i = threadIdx.x + j * kSortThreads;
-        uint2 e = make_uint2(0u, 0u);
-        if (i < ne) e = __ldcs(in + e0 + i);
-        const uint2 n = norm_edge(e);
-        sedge[i] = n;
-        if (i < ne) {
-            if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
-            else if (e.x == e.y) bad |= kErrLoop;
-            else c.E[e0 + i] = n;
-        }
-    }
-    // radix pass 0 over the tile's arcs (arc a = 2k + side, in arrival order)
-    uint32_t dg[kSortItems], rnk[kSortItems], kv[kSortItems];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    __syncthreads();
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t a = warp * 512u + j * 32u + lane;  // arc index inside the tile
-        const uint2 n = sedge[a >> 1];
-        kv[j] = (a & 1u) ? n.y : n.x;
-        dg[j] = (a >> 1) < ne ? digit_of(kv[j], 0) : kRadix;
-    }
-    if (!trivial0) rank_tile(dg, rnk, whist);
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t a = warp * 512u + j * 32u + lane;
-        if ((a >> 1) >= ne) continue;
-        const uint32_t ga = 2 * e0 + a;
-        const uint32_t pos = trivial0 ? ga : soff[dg[j]] + whist[warp][dg[j]] + rnk[j];
-        c.keyB[pos] = kv[j];
-        c.valB[pos] = ga;
-    }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && lane == 0) atomicOr(&c.ctr[kCtrErr], bad);
+// The edge-pair table is built directly from the raw batch on the second stream (concurrently with the
+// vertex partition): ceil(w/2) groups of four 8-byte slots {k, fp}, cleared to all-ones by a memset; an
+// edge takes the first free slot of the first group with room from its home group on (64-bit CAS), so the
+// filled slots of a group form a prefix.  Meeting the same pair (checked against the raw batch) is TC_EDUP;
+// invalid edges are skipped here (k_count reports them).
+__device__ __forceinline__ unsigned long long pslot_pack(uint32_t k, uint32_t fp) {
+    return (unsigned long long)k | ((unsigned long long)fp << 32);
 }
+constexpr unsigned long long kEmptyPSlot = 0xFFFFFFFFFFFFFFFFull;
 
-// a3: the edge-pair hash {lo<<32|hi -> k} (Step 3's closing-edge index), built on a second stream
-// concurrently with the radix sort.  One edge per thread (many threads in flight hide the probe round
-// trips); a claim is one 128-bit CAS of {key, k, tag}; a repeat of a pair is TC_EDUP.
-__global__ void __launch_bounds__(256) k_pairs(const uint2 *__restrict__ in, uint32_t w, StageCtx c) {
-    if (c.ctr[kCtrErr] & (kErrInval | kErrLoop | kErrDup)) return;  // sticky error of an earlier async batch
+__global__ void __launch_bounds__(256) k_pairs(const uint2 *__restrict__ in, uint32_t w, uint2 *pt, uint32_t G,
+                                               uint32_t *ctr) {
+    if (ctr[kCtrErr] & (kErrStage | kErrDup)) return;  // sticky error of an earlier async batch
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t bad = 0;
+    bool dup = false;
     if (k < w) {
-        const uint2 e = __ldcs(in + k);
-        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // invalid edges: k_stage reports them
+        const uint2 e = __ldg(in + k);
+        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {
             const uint2 n = norm_edge(e);
-            const unsigned long long key = pair_key(n.x, n.y);
-            uint32_t b = hash_pair(key) & c.pmask & ~1u;
-            while (true) {
-                const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(c.pt + b);
-                const ulonglong2 s0 = __ldcg(p), s1 = __ldcg(p + 1);
-                const bool l0 = (uint32_t)(s0.y >> 32) == c.tag, l1 = (uint32_t)(s1.y >> 32) == c.tag;
-                if ((l0 && s0.x == key) || (l1 && s1.x == key)) {
-                    bad = kErrDup;
-                    break;
+            const uint64_t h = hash_pair64(pair_key(n.x, n.y));
+            const uint32_t fp = pfinger(h);
+            const unsigned long long mine = pslot_pack(k, fp);
+            unsigned long long *t64 = reinterpret_cast<unsigned long long *>(pt);
+            uint32_t g = pgroup_start(h, G);
+            bool placed = false;
+            while (!placed && !dup) {
+                const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
+                const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
+                const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
+#pragma unroll
+                for (uint32_t i = 0; i < 4; ++i) {
+                    unsigned long long cur = cur4[i];
+                    if (cur == kEmptyPSlot) {
+                        cur = atomicCAS(t64 + 4ull * g + i, kEmptyPSlot, mine);
+                        if (cur == kEmptyPSlot) {
+                            placed = true;
+                            break;
+                        }
+                    }
+                    if ((uint32_t)(cur >> 32) == fp) {
+                        const uint2 o = norm_edge(__ldg(in + (uint32_t)cur));
+                        if (o.x == n.x && o.y == n.y) {
+                            dup = true;
+                            break;
+                        }
+                    }
                 }
-                if (l0 && l1) {
-                    b = (b + 2) & c.pmask;
-                    continue;
-                }
-                const uint32_t s = l0 ? 1u : 0u;
-                const ulonglong2 o = s ? s1 : s0;
-                const u128 exp = pack2(o.x, o.y);
-                if (atomicCAS(reinterpret_cast<u128 *>(c.pt + b + s), exp,
-                              pack2(key, ((unsigned long long)c.tag << 32) | k)) == exp)
-                    break;
+                g = (g + 1 == G) ? 0u : g + 1;
             }
         }
     }
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&c.ctr[kCtrErr], bad);
-}
-
-// Radix pass p >= 1: stable rank inside the tile, scatter to the scanned offsets.
-__global__ void __launch_bounds__(kSortThreads, 3) k_downsweep(uint32_t *keyA, uint32_t *valA, uint32_t *keyB,
-                                                            uint32_t *valB, uint32_t n, const uint32_t *hist,
-                                                            uint32_t pass, const uint32_t *off, uint32_t ntiles,
-                                                            const uint32_t *ctr) {
-    if (ctr[kCtrErr] || pass_trivial(hist, pass, n)) return;
-    const bool fromB = in_buffer_B(hist, pass, n);
-    const uint32_t *__restrict__ kin = fromB ? keyB : keyA;
-    const uint32_t *__restrict__ vin = fromB ? valB : valA;
-    uint32_t *__restrict__ kout = fromB ? keyA : keyB;
-    uint32_t *__restrict__ vout = fromB ? valA : valB;
-    __shared__ uint32_t whist[kWarps][kRadix];
-    __shared__ uint32_t soff[kRadix];
-    soff[threadIdx.x] = off[threadIdx.x * ntiles + blockIdx.x];
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    const uint32_t wbase = blockIdx.x * kRadixTile + warp * 512u;
-    uint32_t keys[kSortItems], vals[kSortItems], dg[kSortItems], rnk[kSortItems];
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        const uint32_t idx = wbase + j * 32u + lane;
-        const bool valid = idx < n;
-        keys[j] = valid ? __ldcs(kin + idx) : 0u;
-        vals[j] = valid ? __ldcs(vin + idx) : 0u;
-        dg[j] = valid ? digit_of(keys[j], pass) : kRadix;
-    }
-    rank_tile(dg, rnk, whist);
-#pragma unroll
-    for (uint32_t j = 0; j < kSortItems; ++j) {
-        if (dg[j] == kRadix) continue;
-        const uint32_t pos = soff[dg[j]] + whist[warp][dg[j]] + rnk[j];
-        kout[pos] = keys[j];
-        vout[pos] = vals[j];
-    }
+    dup = __any_sync(kFull, dup);
+    if (dup && (threadIdx.x & 31u) == 0) atomicOr(&ctr[kCtrErr], kErrDup);
 }
 
 // ------------------------------------------------------------------------------------------------
-// a2: segments of the sorted arcs -> vertex table, ranks / segment ends
+// a2: vertex buckets
 
-struct SegBufs {
-    uint32_t *keyA, *valA, *keyB, *valB;
-    const uint32_t *hist;
+struct VertArgs {
+    uint4 *arcs;        // bucketed arcs {vertex, val, neighbour, 0} (overwritten by the chunked path)
+    uint2 *scratch;
+    const uint2 *E;
+    const uint32_t *vstart;
+    uint2 *segS;        // [2 w] {k<<1|side, neighbour} grouped by vertex
+    uint2 *einfo2;      // [2 w]: einfo2[k<<1|side] = {sorted slot, segment end}
     VSlot *vt;
-    uint32_t vmask;
-    uint32_t tag;
-    uint2 *einfo2;  // [2 wcap]: einfo2[k<<1|side] = {sorted slot, segment end}
+    uint2 *vslice;
+    const uint32_t *vperm;
+    uint32_t bv;
+    uint32_t vcap;      // buckets with more arcs go to k_vbig
+    uint32_t sortcap;   // k_vbig: buckets with more arcs take the chunked global-memory path
     uint32_t *ctr;
 };
 
-__device__ __forceinline__ void sorted_bufs(const SegBufs &sb, uint32_t n, const uint32_t *&keys,
-                                            const uint32_t *&vals) {
-    const bool B = in_buffer_B(sb.hist, kPasses, n);
-    keys = B ? sb.keyB : sb.keyA;
-    vals = B ? sb.valB : sb.valA;
-}
+constexpr uint32_t kVWarps = kVBucketThreads / 32;
+constexpr uint32_t kVAux = kVChunk > kVWarps * 256 + 256 ? kVChunk : kVWarps * 256 + 256;
+constexpr uint32_t kVSmemBytes = kVChunk * 8 + kVAux * 4 + kVChunk * 2;  // sbuf | aux | run_start
+static_assert(kVChunk * 8 >= 2 * 4 * kVChunk, "the u16 slice table (<= 4 D slots) must fit in sbuf");
 
-// Insert-or-find v with payload {deg, start}; returns the slot; claimed = this call created the entry.
-__device__ __forceinline__ uint32_t vt_insert(VSlot *vt, uint32_t mask, uint32_t tag, uint32_t v, uint32_t deg,
-                                              uint32_t start, bool &claimed) {
-    uint32_t b = hash_vertex(v) & mask & ~1u;
-    claimed = false;
-    while (true) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(vt + b);
-        const uint4 s0 = __ldcg(p), s1 = __ldcg(p + 1);
-        const bool l0 = s0.w == tag, l1 = s1.w == tag;
-        if (l0 && s0.x == v) return b;
-        if (l1 && s1.x == v) return b + 1;
-        if (l0 && l1) {
-            b = (b + 2) & mask;
-            continue;
+// smallest power of two >= x (x >= 1)
+__device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) { return x <= 1 ? 1u : 1u << (32 - __clz(x - 1)); }
+__device__ __forceinline__ uint32_t log2_ceil(uint32_t x) { return x <= 1 ? 0u : 32 - __clz(x - 1); }
+
+__device__ __forceinline__ uint32_t slice_size(uint32_t D) { return D ? pow2_ceil(2 * D) : 0u; }
+
+// One LSD pass over the items held in registers (warp-blocked layout, R rounds): stable rank by the digit
+// (key >> shift) & ((1 << bits) - 1); returns the destination index of every item in `dst`.
+__device__ __forceinline__ void rank_pass(const uint32_t (&key)[kVItems], uint32_t R, uint32_t nvalid_base,
+                                          uint32_t n, uint32_t shift, uint32_t bits, uint32_t *whist,
+                                          uint32_t *dtot, uint32_t (&dst)[kVItems]) {
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    const uint32_t mask = (1u << bits) - 1u;
+    for (uint32_t i = threadIdx.x; i < kVWarps * 256; i += kVBucketThreads) whist[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kVItems; ++j) {
+        if (j < R) {
+            const uint32_t i = nvalid_base + warp * 32u * R + j * 32u + lane;
+            const bool valid = i < n;
+            const uint32_t d = (key[j] >> shift) & mask;
+            const uint32_t peers = digit_peers(d, valid, bits);
+            const uint32_t before = __popc(peers & lt);
+            uint32_t b = 0;
+            if (valid) b = whist[warp * 256 + d];
+            __syncwarp();
+            if (valid && before == 0) whist[warp * 256 + d] = b + __popc(peers);
+            __syncwarp();
+            dst[j] = valid ? (d << 16) | (b + before) : 0xFFFFFFFFu;
         }
-        const uint32_t e = l0 ? 1u : 0u;
-        const uint4 s = e ? s1 : s0;
-        const u128 exp = pack4(s.x, s.y, s.z, s.w);
-        if (atomicCAS(reinterpret_cast<u128 *>(vt + b + e), exp, pack4(v, deg, start, tag)) == exp) {
-            claimed = true;
-            return b + e;
+    }
+    __syncthreads();
+    if (threadIdx.x < 256) {  // per digit: exclusive prefix over warps; digit totals
+        uint32_t run = 0;
+#pragma unroll
+        for (uint32_t x = 0; x < kVWarps; ++x) {
+            const uint32_t c = whist[x * 256 + threadIdx.x];
+            whist[x * 256 + threadIdx.x] = run;
+            run += c;
+        }
+        dtot[threadIdx.x] = run;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {  // exclusive scan of the 256 digit totals (8 per lane)
+        uint32_t v[8], s = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            v[q] = dtot[threadIdx.x * 8 + q];
+            s += v[q];
+        }
+        uint32_t incl = s;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint32_t y = __shfl_up_sync(kFull, incl, off);
+            if (lane >= (uint32_t)off) incl += y;
+        }
+        uint32_t run = incl - s;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            dtot[256 + threadIdx.x * 8 + q] = run;  // digit base
+            run += v[q];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (uint32_t j = 0; j < kVItems; ++j) {
+        if (j < R && dst[j] != 0xFFFFFFFFu) {
+            const uint32_t d = dst[j] >> 16;
+            dst[j] = dtot[256 + d] + whist[warp * 256 + d] + (dst[j] & 0xFFFFu);
         }
     }
 }
 
-// One block per tile of kTile sorted arcs (8 consecutive per thread).
-__global__ void __launch_bounds__(kSortThreads) k_runs(SegBufs sb, uint32_t n) {
-    if (sb.ctr[kCtrErr]) return;
-    const uint32_t *keys, *vals;
-    sorted_bufs(sb, n, keys, vals);
-    __shared__ uint32_t skey_[kTile + 2 + (kTile + 2) / 32 + 1];
-    // skewed index (one pad word per 32) so the per-thread contiguous reads below are conflict-free
-#define SKEY(i) skey_[(i) + ((i) >> 5)]
-    __shared__ uint32_t run_start[kTile], run_end[kTile];
-    __shared__ uint32_t wsum[kWarps];
-    __shared__ uint32_t nclaim_sh;
-    const uint32_t t0 = blockIdx.x * kTile;
-    const uint32_t tn = min(kTile, n - t0);
-    const uint32_t i0 = threadIdx.x * kRunItems;
-    uint32_t myval[kRunItems];
+// Table insert of run r (vertex hash h) into a power-of-two table of u16 run indices, 2-slot aligned
+// linear probing (the probe order vt_find assumes).
+__device__ __forceinline__ void stable_insert16(uint16_t *table, uint32_t mask, uint32_t h, uint32_t r) {
+    uint32_t s = h & mask & ~1u;
+    while (true) {
+        if (table[s] == 0xFFFFu && atomicCAS(&table[s], (unsigned short)0xFFFFu, (unsigned short)r) == 0xFFFFu) return;
+        s = (s + 1) & mask;
+    }
+}
+
+// The other endpoint of the edge of arc val = k<<1 | side (side 0 = the lo endpoint).
+__device__ __forceinline__ uint32_t arc_neighbour(const uint2 *E, uint32_t val) {
+    const uint2 e = E[val >> 1];
+    return (val & 1u) ? e.x : e.y;
+}
+
+// One large vertex bucket by LSD radix sort on the vertex hash: in shared memory when it holds at most
+// sortcap arcs, else chunked through global memory.  Called by the whole CTA.
+__device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsigned char *vsm, uint32_t *dtot,
+                                          uint32_t *ws) {
+    uint2 *sbuf = reinterpret_cast<uint2 *>(vsm);                    // [kVChunk] {key, val}; later the table
+    uint32_t *aux = reinterpret_cast<uint32_t *>(vsm + kVChunk * 8);  // [kVAux]: sort histograms | run keys
+    uint16_t *run_start = reinterpret_cast<uint16_t *>(vsm + kVChunk * 8 + kVAux * 4);  // [kVChunk]
+    const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
+    // the bucket's vertex-table slice: next_pow2(2 D) <= 4 n slots at offset 4 * base (disjoint slices)
+    const uint64_t off = 4ull * base;
+    const uint32_t keybits = 32 - a.bv;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    uint32_t D = 0;
+
+    if (n <= a.sortcap) {
+        // ---------------- the whole bucket in registers + shared memory ----------------
+        const uint32_t R = (n + kVBucketThreads - 1) / kVBucketThreads;  // rounds (<= kVItems)
+        uint32_t key[kVItems], val[kVItems], dst[kVItems];
 #pragma unroll
-    for (uint32_t e = 0; e < kRunItems; ++e) {
-        const uint32_t i = i0 + e;
-        if (i < tn) {
-            SKEY(i + 1) = keys[t0 + i];
-            myval[e] = vals[t0 + i];
+        for (uint32_t j = 0; j < kVItems; ++j) {
+            if (j < R) {
+                const uint32_t i = warp * 32u * R + j * 32u + lane;
+                if (i < n) {
+                    const uint4 x = a.arcs[base + i];
+                    key[j] = hash_vertex(x.x);
+                    val[j] = x.y;
+                } else {
+                    key[j] = 0;
+                    val[j] = 0;
+                }
+            }
         }
+        for (uint32_t shift = 0; shift < keybits; shift += 8) {
+            rank_pass(key, R, 0, n, shift, min(8u, keybits - shift), aux, dtot, dst);
+#pragma unroll
+            for (uint32_t j = 0; j < kVItems; ++j)
+                if (j < R && dst[j] != 0xFFFFFFFFu) sbuf[dst[j]] = make_uint2(key[j], val[j]);
+            __syncthreads();
+            if (shift + 8 < keybits) {
+#pragma unroll
+                for (uint32_t j = 0; j < kVItems; ++j) {
+                    if (j < R) {
+                        const uint32_t i = warp * 32u * R + j * 32u + lane;
+                        if (i < n) {
+                            const uint2 x = sbuf[i];
+                            key[j] = x.x;
+                            val[j] = x.y;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        // runs of equal key (= equal vertex: hash_vertex is a bijection); blocked items per thread
+        uint32_t *run_key = aux;  // [D] key of each run (the sort's histograms are dead now)
+        const uint32_t i0 = threadIdx.x * R, i1 = min(n, i0 + R);
+        uint32_t heads = 0;
+        for (uint32_t i = i0; i < i1; ++i) heads += (i == 0 || sbuf[i].x != sbuf[i - 1].x) ? 1u : 0u;
+        const uint32_t rid0 = block_exclusive_scan<kVBucketThreads>(heads, ws, &D);  // runs started before i0
+        {
+            uint32_t q = rid0;
+            for (uint32_t i = i0; i < i1; ++i) {
+                const uint32_t k = sbuf[i].x;
+                if (i == 0 || k != sbuf[i - 1].x) {
+                    run_start[q] = (uint16_t)i;
+                    run_key[q] = k;
+                    ++q;
+                }
+            }
+        }
+        __syncthreads();
+        // per arc: segS and {slot, segment end}
+        uint32_t r = rid0;
+        for (uint32_t i = i0; i < i1; ++i) {
+            const uint2 x = sbuf[i];
+            if (i == 0 || x.x != sbuf[i - 1].x) ++r;
+            const uint32_t end = r < D ? run_start[r] : n;  // run r-1 ends where run r starts
+            a.segS[base + i] = make_uint2(x.y, arc_neighbour(a.E, x.y));
+            a.einfo2[x.y] = make_uint2(base + i, base + end);
+        }
+        // the slice, built in shared memory and written whole
+        if (threadIdx.x == 0) {
+            a.vslice[b] = make_uint2((uint32_t)off, slice_size(D));
+            if (D) atomicAdd(&a.ctr[kCtrD], D);
+        }
+        __syncthreads();  // sbuf is dead: it holds the table now
+        const uint32_t S = slice_size(D);
+        uint16_t *table = reinterpret_cast<uint16_t *>(sbuf);
+        for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) table[s] = 0xFFFFu;
+        __syncthreads();
+        for (uint32_t q = threadIdx.x; q < D; q += kVBucketThreads) stable_insert16(table, S - 1, run_key[q], q);
+        __syncthreads();
+        for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) {
+            const uint32_t q = table[s];
+            uint4 o = make_uint4(kEmptyV, 0u, 0u, 0u);
+            if (q != 0xFFFFu) {
+                const uint32_t st = run_start[q], en = q + 1 < D ? run_start[q + 1] : n;
+                o = make_uint4(unhash_vertex(run_key[q]), en - st, base + st, 0u);
+            }
+            reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
+        }
+        return;
+    }
+
+    // ---------------- chunked path (a bucket larger than vcap, e.g. a hub): global-memory buffers ----------------
+    // pass 0 reads the uint4 arcs; then {key, val} ping-pongs between scratch and the bucket's own arc memory
+    uint2 *src = reinterpret_cast<uint2 *>(a.arcs) + 2ull * base, *dstb = a.scratch + base;
+    const uint4 *arcs4 = a.arcs + base;
+    const uint32_t R = kVItems, C = kVChunk;
+    uint32_t key[kVItems], val[kVItems], dst[kVItems];
+    for (uint32_t shift = 0; shift < keybits; shift += 8) {
+        const uint32_t bits = min(8u, keybits - shift), mask = (1u << bits) - 1u;
+        const bool first = shift == 0;
+        // digit histogram over the whole bucket
+        uint32_t *ghist = dtot;  // [256] running digit offsets
+        for (uint32_t i = threadIdx.x; i < 256; i += kVBucketThreads) aux[i] = 0;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += kVBucketThreads) {
+            const uint32_t k = first ? hash_vertex(arcs4[i].x) : src[i].x;
+            atomicAdd(&aux[(k >> shift) & mask], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            uint32_t v[8], s = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                v[q] = aux[threadIdx.x * 8 + q];
+                s += v[q];
+            }
+            uint32_t incl = s;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, incl, off);
+                if (lane >= (uint32_t)off) incl += y;
+            }
+            uint32_t run = incl - s;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                sbuf[threadIdx.x * 8 + q].x = run;  // running offsets live in sbuf[0..256).x
+                run += v[q];
+            }
+        }
+        __syncthreads();
+        for (uint32_t c0 = 0; c0 < n; c0 += C) {
+            const uint32_t cn = min(C, n - c0);
+#pragma unroll
+            for (uint32_t j = 0; j < kVItems; ++j) {
+                const uint32_t i = warp * 32u * R + j * 32u + lane;
+                if (i < cn) {
+                    if (first) {
+                        const uint4 x = arcs4[c0 + i];
+                        key[j] = hash_vertex(x.x);
+                        val[j] = x.y;
+                    } else {
+                        const uint2 x = src[c0 + i];
+                        key[j] = x.x;
+                        val[j] = x.y;
+                    }
+                } else {
+                    key[j] = 0;
+                    val[j] = 0;
+                }
+            }
+            rank_pass(key, R, 0, cn, shift, bits, aux + 256, ghist, dst);  // dst = in-chunk digit position
+            // in-chunk position = digit base (in chunk) + ...; global = running offset[d] + (pos - chunk base[d])
+#pragma unroll
+            for (uint32_t j = 0; j < kVItems; ++j) {
+                if (dst[j] != 0xFFFFFFFFu) {
+                    const uint32_t d = (key[j] >> shift) & mask;
+                    const uint32_t p = sbuf[d].x + (dst[j] - ghist[256 + d]);
+                    dstb[p] = make_uint2(key[j], val[j]);
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < 256) sbuf[threadIdx.x].x += ghist[threadIdx.x];  // chunk's digit totals
+            __syncthreads();
+        }
+        uint2 *t = src;
+        src = dstb;
+        dstb = t;
+        __syncthreads();
+    }
+    // sorted {key, val} in src; runs -> run starts in dstb (as u32)
+    uint32_t *gruns = reinterpret_cast<uint32_t *>(dstb);
+    uint32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += C) {
+        const uint32_t cn = min(C, n - c0);
+        const uint32_t i0 = c0 + threadIdx.x * R, i1 = min(c0 + cn, i0 + R);
+        uint32_t heads = 0;
+        for (uint32_t i = i0; i < i1; ++i) heads += (i == 0 || src[i].x != src[i - 1].x) ? 1u : 0u;
+        uint32_t tot;
+        uint32_t rid = carry + block_exclusive_scan<kVBucketThreads>(heads, ws, &tot);
+        for (uint32_t i = i0; i < i1; ++i)
+            if (i == 0 || src[i].x != src[i - 1].x) gruns[rid++] = i;
+        carry += tot;
+    }
+    D = carry;
+    __syncthreads();
+    carry = 0;
+    for (uint32_t c0 = 0; c0 < n; c0 += C) {
+        const uint32_t cn = min(C, n - c0);
+        const uint32_t i0 = c0 + threadIdx.x * R, i1 = min(c0 + cn, i0 + R);
+        uint32_t heads = 0;
+        for (uint32_t i = i0; i < i1; ++i) heads += (i == 0 || src[i].x != src[i - 1].x) ? 1u : 0u;
+        uint32_t tot;
+        uint32_t r = carry + block_exclusive_scan<kVBucketThreads>(heads, ws, &tot);  // runs started before i0
+        for (uint32_t i = i0; i < i1; ++i) {
+            const uint2 x = src[i];
+            if (i == 0 || x.x != src[i - 1].x) ++r;
+            const uint32_t run = r - 1;
+            const uint32_t end = run + 1 < D ? gruns[run + 1] : n;
+            a.segS[base + i] = make_uint2(x.y, arc_neighbour(a.E, x.y));
+            a.einfo2[x.y] = make_uint2(base + i, base + end);
+        }
+        carry += tot;
     }
     if (threadIdx.x == 0) {
-        SKEY(0) = t0 > 0 ? keys[t0 - 1] : ~keys[t0];                       // halo: previous arc's key
-        SKEY(tn + 1) = t0 + tn < n ? keys[t0 + tn] : ~keys[t0 + tn - 1];  // halo: next arc's key
-        nclaim_sh = 0;
+        a.vslice[b] = make_uint2((uint32_t)off, slice_size(D));
+        if (D) atomicAdd(&a.ctr[kCtrD], D);
     }
+    const uint32_t S = slice_size(D);
+    VSlot *sl = a.vt + off;
+    for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads)
+        reinterpret_cast<uint4 *>(sl)[s] = make_uint4(kEmptyV, 0u, 0u, 0u);
+    __threadfence();
     __syncthreads();
-    // local run heads (inside the tile) -> run ids by a block scan
-    uint32_t heads = 0;
-#pragma unroll
-    for (uint32_t e = 0; e < kRunItems; ++e) {
-        const uint32_t i = i0 + e;
-        if (i < tn && (i == 0 || SKEY(i + 1) != SKEY(i))) ++heads;
-    }
-    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-    uint32_t incl = heads;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= (uint32_t)off) incl += y;
-    }
-    if (lane == 31) wsum[warp] = incl;
-    __syncthreads();
-    uint32_t wpre = 0, nruns = 0;
-    for (uint32_t x = 0; x < kWarps; ++x) {
-        if (x < warp) wpre += wsum[x];
-        nruns += wsum[x];
-    }
-    uint32_t rid[kRunItems];
-    {
-        uint32_t r = wpre + incl - heads;  // runs started before this thread's first arc
-#pragma unroll
-        for (uint32_t e = 0; e < kRunItems; ++e) {
-            const uint32_t i = i0 + e;
-            if (i < tn && (i == 0 || SKEY(i + 1) != SKEY(i))) {
-                run_start[r] = i;
-                ++r;
-            }
-            rid[e] = r - 1;
-            if (i < tn && (i + 1 == tn || SKEY(i + 2) != SKEY(i + 1))) run_end[r - 1] = i + 1;
-        }
-    }
-    __syncthreads();
-    // one thread per run: vertex table entry (whole segment in one CAS; split segments by atomics)
-    uint32_t claims = 0;
-    for (uint32_t r = threadIdx.x; r < nruns; r += kSortThreads) {
-        const uint32_t s = run_start[r], e = run_end[r];
-        const uint32_t v = SKEY(s + 1);
-        const bool whole = SKEY(s) != v && SKEY(e + 1) != v;  // the segment starts and ends in this tile
-        bool claimed;
-        const uint32_t slot =
-            vt_insert(sb.vt, sb.vmask, sb.tag, v, whole ? e - s : 0u, whole ? t0 + s : 0xFFFFFFFFu, claimed);
-        if (!whole) {
-            atomicAdd(&sb.vt[slot].deg, e - s);
-            atomicMin(&sb.vt[slot].start, t0 + s);
-            run_end[r] = 0;  // the segment crosses the tile: k_fix writes its arcs' einfo
-        }
-        claims += claimed ? 1u : 0u;
-    }
-    if (claims) atomicAdd(&nclaim_sh, claims);
-    __syncthreads();
-    if (threadIdx.x == 0 && nclaim_sh) atomicAdd(&sb.ctr[kCtrD], nclaim_sh);
-    // arcs of tile-internal segments: einfo = {sorted slot, segment end}
-#pragma unroll
-    for (uint32_t e = 0; e < kRunItems; ++e) {
-        const uint32_t i = i0 + e;
-        if (i < tn) {
-            const uint32_t end = run_end[rid[e]];
-            if (end) sb.einfo2[myval[e]] = make_uint2(t0 + i, t0 + end);
-        }
+    const u128 empty = (u128)kEmptyV;
+    for (uint32_t q = threadIdx.x; q < D; q += kVBucketThreads) {
+        const uint32_t st = gruns[q], en = q + 1 < D ? gruns[q + 1] : n;
+        const uint32_t h = src[st].x;
+        const u128 v = (u128)unhash_vertex(h) | ((u128)(en - st) << 32) | ((u128)(base + st) << 64);
+        uint32_t s = h & (S - 1) & ~1u;
+        while (atomicCAS(reinterpret_cast<u128 *>(sl + s), empty, v) != empty) s = (s + 1) & (S - 1);
     }
 }
-#undef SKEY
 
-// Arcs of segments that cross tile boundaries (at most the first and the last segment of a tile).
-__global__ void __launch_bounds__(kSortThreads) k_fix(SegBufs sb, uint32_t n) {
-    if (sb.ctr[kCtrErr]) return;
-    const uint32_t *keys, *vals;
-    sorted_bufs(sb, n, keys, vals);
-    __shared__ uint2 seg[2];
-    const uint32_t t0 = blockIdx.x * kTile;
-    const uint32_t t1 = min(t0 + kTile, n);
-    if (threadIdx.x < 2) {
-        const uint32_t v = keys[threadIdx.x == 0 ? t0 : t1 - 1];
-        const uint2 inf = vt_find(sb.vt, sb.vmask, sb.tag, v);  // {deg, start}
-        seg[threadIdx.x] = make_uint2(inf.y, inf.y + inf.x);
+// Persistent CTAs over the large buckets (vperm[0 .. ctr[kCtrBig])), on their own stream.
+__global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
+    if (a.ctr[kCtrErr] & kErrStage) return;
+    extern __shared__ __align__(16) unsigned char vsm[];
+    __shared__ uint32_t dtot[512];
+    __shared__ uint32_t ws[33];
+    __shared__ uint32_t s_b;
+    const uint32_t nbig = a.ctr[kCtrBig];
+    while (true) {
+        if (threadIdx.x == 0) {
+            const uint32_t t = atomicAdd(&a.ctr[kCtrTicket], 1u);
+            s_b = t < nbig ? a.vperm[t] : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        const uint32_t b = s_b;
+        __syncthreads();
+        if (b == 0xFFFFFFFFu) return;
+        vbucket_sort(a, b, vsm, dtot, ws);
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// a2, common case: a vertex bucket of at most vcap (<= kHCap) arcs.  Vertices get bucket-local ids from a
+// shared-memory hash table (claim order), then ONE stable ballot ranking pass by local id -- instead of
+// three radix passes on the vertex hash -- gives every arc its rank inside its vertex.
+
+constexpr uint32_t kHThreads = 256, kHWarps = kHThreads / 32;
+constexpr uint32_t kHCap = 4096;           // arcs
+constexpr uint32_t kHTable = 2 * kHCap;    // hash slots (power of two >= 2 n)
+constexpr uint32_t kHSweep = 2048;         // local ids ranked per sweep
+// shared memory: R1 = {hkey u32[kHTable], lid u16[kHTable]} while hashing; then {whist u16[8][kHSweep],
+// segst u32[kHCap + 1]}; the slice table (u32, <= 2 kHCap slots) reuses whist.  vkey u32[kHCap] apart.
+constexpr uint32_t kHR1 = kHTable * 6 + 64;
+constexpr uint32_t kHSmemBytes = kHR1 + kHCap * 4;
+static_assert(kHWarps * kHSweep * 2 + (kHCap + 1) * 4 <= kHR1, "phase-3 arrays must fit R1");
+static_assert(2 * kHCap * 4 <= kHWarps * kHSweep * 2 + 4, "the slice table must fit over whist");
+
+template <int R>
+__device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint32_t base, uint32_t n,
+                                             unsigned char *sm, uint32_t *ws, uint32_t *sD) {
+    uint32_t *hkey = reinterpret_cast<uint32_t *>(sm);
+    uint16_t *lid = reinterpret_cast<uint16_t *>(sm + kHTable * 4);
+    uint16_t *whist = reinterpret_cast<uint16_t *>(sm);
+    uint32_t *segst = reinterpret_cast<uint32_t *>(sm + kHWarps * kHSweep * 2);
+    uint32_t *table = reinterpret_cast<uint32_t *>(sm);
+    uint32_t *vkey = reinterpret_cast<uint32_t *>(sm + kHR1);
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    const uint32_t Tb = pow2_ceil(2 * n);
+    for (uint32_t s = threadIdx.x; s < Tb; s += kHThreads) hkey[s] = kEmptyV;
+    if (threadIdx.x == 0) *sD = 0;
+    __syncthreads();
+    // phase 1: local ids (claim order) through the shared hash table; warp w owns items [w 32 R, (w+1) 32 R)
+    uint32_t val[R], pk[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const uint32_t i = warp * 32u * R + j * 32u + lane;
+        pk[j] = 0xFFFFFFFFu;
+        if (i < n) {
+            const uint4 x = a.arcs[base + i];
+            val[j] = x.y;
+            uint32_t s = hash_vertex(x.x) & (Tb - 1);
+            while (true) {
+                uint32_t k = hkey[s];
+                if (k == kEmptyV) {
+                    k = atomicCAS(&hkey[s], kEmptyV, x.x);
+                    if (k == kEmptyV) {
+                        const uint32_t l = atomicAdd(sD, 1u);
+                        lid[s] = (uint16_t)l;
+                        vkey[l] = x.x;
+                        break;
+                    }
+                }
+                if (k == x.x) break;
+                s = (s + 1) & (Tb - 1);
+            }
+            pk[j] = s;
+        }
     }
     __syncthreads();
-    for (uint32_t q = 0; q < 2; ++q) {
-        const uint2 sgm = seg[q];
-        if (sgm.x >= t0 && sgm.y <= t1) continue;   // tile-internal: done by k_runs
-        if (q == 1 && seg[0].x == sgm.x) continue;  // same segment as q == 0
-        const uint32_t lo = max(sgm.x, t0), hi = min(sgm.y, t1);
-        for (uint32_t i = lo + threadIdx.x; i < hi; i += kSortThreads) sb.einfo2[vals[i]] = make_uint2(i, sgm.y);
+    const uint32_t D = *sD;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+        if (pk[j] != 0xFFFFFFFFu) pk[j] = (uint32_t)lid[pk[j]] << 16;  // local id << 16 | rank (below)
+    __syncthreads();  // R1 becomes whist + segst
+    // phase 2: stable rank of each arc inside its vertex, local ids in sweeps of kHSweep
+    for (uint32_t l0 = 0; l0 < D; l0 += kHSweep) {
+        const uint32_t nd = min(kHSweep, D - l0);
+        const uint32_t bits = log2_ceil(nd);
+        for (uint32_t i = threadIdx.x; i < kHWarps * nd; i += kHThreads) whist[i] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t d = (pk[j] >> 16) - l0;
+            const bool in = pk[j] != 0xFFFFFFFFu && d < nd;
+#ifdef TC_VHASH_BALLOT
+            const uint32_t peers = digit_peers(d, in, bits);
+#else
+            const uint32_t peers = match_peers(d, in);
+#endif
+            const uint32_t before = __popc(peers & lt);
+            uint32_t c = 0;
+            if (in) c = whist[warp * nd + d];
+            __syncwarp();
+            if (in && before == 0) whist[warp * nd + d] = (uint16_t)(c + __popc(peers));
+            __syncwarp();
+            if (in) pk[j] += c + before;
+        }
+        __syncthreads();
+        for (uint32_t d = threadIdx.x; d < nd; d += kHThreads) {  // exclusive prefix over warps; degree
+            uint32_t run = 0;
+#pragma unroll
+            for (uint32_t x = 0; x < kHWarps; ++x) {
+                const uint32_t c = whist[x * nd + d];
+                whist[x * nd + d] = (uint16_t)run;
+                run += c;
+            }
+            segst[l0 + d] = run;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const uint32_t d = (pk[j] >> 16) - l0;
+            if (pk[j] != 0xFFFFFFFFu && d < nd) pk[j] += whist[warp * nd + d];
+        }
+        __syncthreads();
     }
+    // phase 3: segment starts = exclusive scan of the degrees over local ids
+    {
+        const uint32_t per = (D + kHThreads - 1) / kHThreads;
+        const uint32_t q0 = min(D, threadIdx.x * per), q1 = min(D, q0 + per);
+        uint32_t sum = 0;
+        for (uint32_t q = q0; q < q1; ++q) sum += segst[q];
+        uint32_t tot;
+        uint32_t run = block_exclusive_scan<kHThreads>(sum, ws, &tot);
+        for (uint32_t q = q0; q < q1; ++q) {
+            const uint32_t c = segst[q];
+            segst[q] = run;
+            run += c;
+        }
+        if (threadIdx.x == 0) segst[D] = n;
+        __syncthreads();
+    }
+    // phase 4: per arc, segS and {slot, segment end}
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        if (pk[j] == 0xFFFFFFFFu) continue;
+        const uint32_t l = pk[j] >> 16;
+        const uint32_t pos = segst[l] + (pk[j] & 0xFFFFu);
+        const uint32_t i = warp * 32u * R + j * 32u + lane;
+        a.segS[base + pos] = make_uint2(val[j], __ldcs(a.arcs + base + i).z);
+        a.einfo2[val[j]] = make_uint2(base + pos, base + segst[l + 1]);
+    }
+    // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole
+    const uint32_t S = slice_size(D);
+    const uint64_t off = 4ull * base;
+    if (threadIdx.x == 0) {
+        a.vslice[b] = make_uint2((uint32_t)off, S);
+        if (D) atomicAdd(&a.ctr[kCtrD], D);
+    }
+    for (uint32_t s = threadIdx.x; s < S; s += kHThreads) table[s] = kEmptyV;
+    __syncthreads();
+    for (uint32_t l = threadIdx.x; l < D; l += kHThreads) {
+        uint32_t s = hash_vertex(vkey[l]) & (S - 1) & ~1u;
+        while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV) s = (s + 1) & (S - 1);
+    }
+    __syncthreads();
+    for (uint32_t s = threadIdx.x; s < S; s += kHThreads) {
+        const uint32_t l = table[s];
+        uint4 o = make_uint4(kEmptyV, 0u, 0u, 0u);
+        if (l != kEmptyV) o = make_uint4(vkey[l], segst[l + 1] - segst[l], base + segst[l], 0u);
+        reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
+    }
+}
+
+__global__ void __launch_bounds__(kHThreads, 3) k_vhash(VertArgs a) {
+    if (a.ctr[kCtrErr] & kErrStage) return;
+    extern __shared__ __align__(16) unsigned char hsm[];
+    __shared__ uint32_t ws[9];
+    __shared__ uint32_t sD;
+    const uint32_t b = blockIdx.x;
+    const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
+    if (n > a.vcap) return;  // k_vbig's
+    if (n <= 256) vbucket_hash<1>(a, b, base, n, hsm, ws, &sD);
+    else if (n <= 512) vbucket_hash<2>(a, b, base, n, hsm, ws, &sD);
+    else if (n <= 1024) vbucket_hash<4>(a, b, base, n, hsm, ws, &sD);
+    else if (n <= 2048) vbucket_hash<8>(a, b, base, n, hsm, ws, &sD);
+    else vbucket_hash<16>(a, b, base, n, hsm, ws, &sD);
 }
 
 // ------------------------------------------------------------------------------------------------
 // a4..a8: the fused estimator update, one thread per estimator.
 
 struct UpdateIdx {
-    const uint2 *E;
+    Lookup L;
     const uint4 *einfo;
-    const VSlot *vt;
-    uint32_t vmask;
-    const uint32_t *valA, *valB;  // the sorted arc values (segS) live in one of them
-    const uint32_t *hist;
-    const PSlot *pt;
-    uint32_t pmask;
-    uint32_t tag;
+    const uint2 *segS;
     const uint32_t *ctr;
 };
 
-__global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint2 *__restrict__ r2s,
-                                                   uint32_t *__restrict__ cfs, uint64_t *__restrict__ p1s,
-                                                   uint64_t *__restrict__ p2s, uint64_t count, uint64_t first,
-                                                   uint64_t seed, uint32_t batch, uint64_t m_prev, uint32_t w,
-                                                   UpdateIdx ix, unsigned long long *S, unsigned long long *stats) {
+struct EstState {
+    uint2 r1, r2;
+    uint32_t cf, p1, p2;
+};
+
+struct UpdateArgs {
+    uint2 *r1s, *r2s;
+    uint32_t *cfs, *p1s, *p2s;
+    uint64_t count, first, seed;
+    uint32_t batch, w;
+    uint64_t m_prev;
+};
+
+__device__ __forceinline__ EstState load_state(const UpdateArgs &u, uint64_t t) {
+    EstState e;
+    e.r1 = __ldcs(u.r1s + t);
+    e.cf = __ldcs(u.cfs + t);
+    e.r2 = __ldcs(u.r2s + t);
+    e.p1 = __ldcs(u.p1s + t);
+    e.p2 = __ldcs(u.p2s + t);
+    return e;
+}
+
+// Steps 1-3 for estimator t (local index) whose state was read into `old`.  Returns chi if it ends closed.
+__device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const UpdateIdx &ix, uint64_t t, const EstState &old,
+                                               uint32_t &n_fresh, uint32_t &n_r2old) {
+    const uint64_t gid = u.first + t;
+    const DrawCtx dc{gid, u.batch, PhiloxKey{(uint32_t)u.seed, (uint32_t)(u.seed >> 32)}};
+    const uint4 o = philox4x32_10(make_uint4((uint32_t)gid, (uint32_t)(gid >> 32), u.batch, 0u), dc.key);
+    const uint64_t xlo = (uint64_t)o.x | ((uint64_t)o.y << 32);
+    const uint64_t xhi = (uint64_t)o.z | ((uint64_t)o.w << 32);
+    const uint64_t m_prev = u.m_prev;
+
+    // ---- Step 1: level-1 reservoir ----
+    const uint64_t d1 = bounded(m_prev + u.w, xlo, dc, 0x10000u);
+    const bool fresh = d1 >= m_prev;
+    uint2 r1, r2;
+    uint32_t c, ld, rd, endU, endV;
+    bool closed, had_r2 = false;
+    if (fresh) {
+        const uint32_t j = (uint32_t)(d1 - m_prev);
+        r1 = __ldg(ix.L.E + j);
+        r2 = make_uint2(kEmptyV, kEmptyV);
+        c = 0;
+        closed = false;
+        // ---- Step 2a for a fresh f1 = w_j: ld = rank(u->v), rd = rank(v->u) ----
+        const uint4 inf = __ldg(ix.einfo + j);
+        ld = inf.y - 1u - inf.x;
+        rd = inf.w - 1u - inf.z;
+        endU = inf.y;
+        endV = inf.w;
+    } else {
+        r1 = old.r1;
+        r2 = old.r2;
+        c = old.cf & kCMask;
+        closed = (old.cf & kClosedBit) != 0;
+        had_r2 = c > 0;  // NBSI: chi == 0 <=> f2 empty
+        // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
+        VertProbe pu, pv;
+        vt_issue(ix.L, r1.x, pu);
+        vt_issue(ix.L, r1.y, pv);
+        const uint2 iu = vt_resolve(ix.L, pu, r1.x), iv = vt_resolve(ix.L, pv, r1.y);
+        ld = iu.x;
+        rd = iv.x;
+        endU = iu.y + iu.x;
+        endV = iv.y + iv.x;
+    }
+    const uint32_t chi_p = ld + rd;  // |Gamma_W(f1)| = rank(u->v) + rank(v->u)
+    bool r2new = false;
+    uint32_t k2 = 0, x = 0, z = 0;
+    if (chi_p) {
+        // ---- Step 2b: keep f2 w.p. chi^-/(chi^-+chi^+), else phi names an edge ----
+        const uint64_t d2 = bounded((uint64_t)c + chi_p, xhi, dc, 0x20000u);
+        if (d2 >= c) {
+            const uint32_t phi = (uint32_t)(d2 - c);
+            const bool atU = phi < ld;  // (src = u, rank = phi) or (src = v, rank = phi - ld)
+            const uint32_t end = atU ? endU : endV;
+            const uint32_t a = atU ? phi : phi - ld;
+            const uint2 arc = __ldg(ix.segS + (end - 1u - a));  // {k<<1|side, neighbour}
+            const uint32_t src = atU ? r1.x : r1.y;
+            k2 = arc.x >> 1;
+            r2 = make_uint2(min(src, arc.y), max(src, arc.y));
+            x = atU ? r1.y : r1.x;  // f1's endpoint not on f2
+            z = arc.y;              // f2's endpoint not on f1
+            r2new = true;
+            closed = false;
+        }
+        c += chi_p;
+    }
+    // ---- Step 3: closing edge after f2; an old f2 precedes every batch edge ----
+    if ((r2new || had_r2) && !closed) {
+        if (!r2new) {
+            x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;
+            z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;
+        }
+        const int64_t kk = pt_find(ix.L, min(x, z), max(x, z));
+        if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
+    }
+    const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
+    // every field rewritten: coalesced full sectors, no partial-sector read-modify-write
+    __stcs(u.cfs + t, cf_new);
+    __stcs(u.r1s + t, r1);
+    __stcs(u.r2s + t, r2);
+    __stcs(u.p1s + t, fresh ? (uint32_t)d1 : old.p1);
+    __stcs(u.p2s + t, r2new ? (uint32_t)(m_prev + k2) : fresh ? kEmptyV : old.p2);
+    n_fresh += fresh ? 1u : 0u;
+    n_r2old += (r2new && !fresh) ? 1u : 0u;
+    return closed ? c : 0u;
+}
+
+// One pass over the estimator SoA: a grid of a few CTAs per SM loops over the estimators, reading the next
+// estimator's state while it works on the current one.
+__global__ void __launch_bounds__(256, 3) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
+                                                   unsigned long long *stats) {
     if (ix.ctr[kCtrErr]) return;
-    const uint32_t *__restrict__ segS = in_buffer_B(ix.hist, kPasses, 2 * w) ? ix.valB : ix.valA;
-    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long contrib = 0;
     uint32_t n_fresh = 0, n_r2old = 0;
-    if (t < count) {
-        const uint64_t gid = first + t;
-        const DrawCtx dc{gid, batch, PhiloxKey{(uint32_t)seed, (uint32_t)(seed >> 32)}};
-        const uint4 o = philox4x32_10(make_uint4((uint32_t)gid, (uint32_t)(gid >> 32), batch, 0u), dc.key);
-        const uint64_t xlo = (uint64_t)o.x | ((uint64_t)o.y << 32);
-        const uint64_t xhi = (uint64_t)o.z | ((uint64_t)o.w << 32);
-
-        // ---- Step 1: level-1 reservoir ----
-        const uint64_t d1 = bounded(m_prev + w, xlo, dc, 0x10000u);
-        const bool fresh = d1 >= m_prev;
-        uint2 r1, r2 = make_uint2(kEmptyV, kEmptyV);
-        uint32_t c, cf_old = 0;
-        bool closed;
-        uint32_t ld, rd, endU, endV;
-        if (fresh) {
-            const uint32_t j = (uint32_t)(d1 - m_prev);
-            r1 = __ldg(ix.E + j);
-            c = 0;
-            closed = false;
-            // ---- Step 2a for a fresh f1 = w_j: ld = rank(u->v), rd = rank(v->u) ----
-            const uint4 inf = __ldg(ix.einfo + j);
-            ld = inf.y - 1u - inf.x;
-            rd = inf.w - 1u - inf.z;
-            endU = inf.y;
-            endV = inf.w;
-        } else {
-            r1 = __ldcs(r1s + t);
-            cf_old = __ldcs(cfs + t);
-            r2 = __ldcs(r2s + t);  // issued early: needed by Step 3 when f2 is kept
-            c = cf_old & kCMask;
-            closed = (cf_old & kClosedBit) != 0;
-            // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
-            uint2 iu, iv;
-            vt_find2(ix.vt, ix.vmask, ix.tag, r1.x, r1.y, iu, iv);
-            ld = iu.x;
-            rd = iv.x;
-            endU = iu.y + iu.x;
-            endV = iv.y + iv.x;
-        }
-        const uint32_t chi_p = ld + rd;  // |Gamma_W(f1)| = rank(u->v) + rank(v->u)
-        bool r2new = false;
-        uint32_t k2 = 0;
-        const bool had_r2 = !fresh && c > 0;  // NBSI: chi == 0 <=> f2 empty
-        if (chi_p) {
-            // ---- Step 2b: keep f2 w.p. chi^-/(chi^-+chi^+), else phi names an edge ----
-            const uint64_t d2 = bounded((uint64_t)c + chi_p, xhi, dc, 0x20000u);
-            if (d2 >= c) {
-                const uint32_t phi = (uint32_t)(d2 - c);
-                const uint32_t end = phi < ld ? endU : endV;
-                const uint32_t a = phi < ld ? phi : phi - ld;
-                const uint32_t val = __ldg(segS + (end - 1u - a));
-                k2 = val >> 1;
-                r2 = __ldg(ix.E + k2);
-                r2new = true;
-                closed = false;
-            }
-            c += chi_p;
-        }
-        // ---- Step 3: closing edge after f2 ----
-        if ((r2new || had_r2) && !closed) {
-            const uint32_t x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;  // f1's endpoint not on f2
-            const uint32_t z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;  // f2's endpoint not on f1
-            const int64_t kk = pt_find(ix.pt, ix.pmask, ix.tag, pair_key(min(x, z), max(x, z)));
-            if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
-        }
-        const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
-        if (fresh || cf_new != cf_old) __stcs(cfs + t, cf_new);
-        if (fresh) {
-            __stcs(r1s + t, r1);
-            __stcs(p1s + t, d1);
-        }
-        if (r2new) {
-            __stcs(r2s + t, r2);
-            __stcs(p2s + t, m_prev + k2);
-        } else if (fresh) {
-            __stcs(r2s + t, make_uint2(kEmptyV, kEmptyV));
-            __stcs(p2s + t, ~0ull);
-        }
-        if (closed) contrib = c;
-        n_fresh = fresh ? 1u : 0u;
-        n_r2old = (r2new && !fresh) ? 1u : 0u;
+    EstState cur;
+    if (t < u.count) cur = load_state(u, t);
+    while (t < u.count) {
+        const uint64_t tn = t + stride;
+        EstState nxt;
+        if (tn < u.count) nxt = load_state(u, tn);
+        contrib += update_one(u, ix, t, cur, n_fresh, n_r2old);
+        cur = nxt;
+        t = tn;
     }
     // ---- a8: partial sum of chi over closed estimators (+ event counts for the byte model) ----
-    n_fresh = __popc(__ballot_sync(0xffffffffu, n_fresh != 0));
-    n_r2old = __popc(__ballot_sync(0xffffffffu, n_r2old != 0));
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        contrib += __shfl_xor_sync(kFull, contrib, off);
+        n_fresh += __shfl_xor_sync(kFull, n_fresh, off);
+        n_r2old += __shfl_xor_sync(kFull, n_r2old, off);
+    }
     __shared__ unsigned long long ws[8];
     __shared__ uint32_t wf[8], wr[8];
     if ((threadIdx.x & 31u) == 0) {
@@ -646,13 +1039,13 @@ __global__ void __launch_bounds__(256, 4) k_update(uint2 *__restrict__ r1s, uint
     }
 }
 
-__global__ void k_init_state(uint2 *r1, uint2 *r2, uint32_t *cf, uint64_t *p1, uint64_t *p2, uint64_t count) {
+__global__ void k_init_state(uint2 *r1, uint2 *r2, uint32_t *cf, uint32_t *p1, uint32_t *p2, uint64_t count) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
         r1[t] = make_uint2(kEmptyV, kEmptyV);
         r2[t] = make_uint2(kEmptyV, kEmptyV);
         cf[t] = 0;
-        p1[t] = ~0ull;
-        p2[t] = ~0ull;
+        p1[t] = kEmptyV;
+        p2[t] = kEmptyV;
     }
 }
 
@@ -678,64 +1071,73 @@ int sm_count() {
     return g_sms;
 }
 
+constexpr uint32_t kUpdateCTAsPerSM = 3, kUpdateWaves = 2;  // k_update grid: estimators per thread >= 1
+
 static inline uint32_t grid_for(uint64_t items, uint32_t threads, uint32_t per_sm) {
     const uint64_t want = (items + threads - 1) / threads;
     const uint64_t cap = (uint64_t)sm_count() * per_sm;
     return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
 }
 
-static inline uint32_t radix_tiles(uint32_t w) { return (2 * w + kRadixTile - 1) / kRadixTile; }
+static inline uint32_t ceil_log2(uint64_t x) {
+    uint32_t b = 0;
+    while ((1ull << b) < x) ++b;
+    return b;
+}
 
-int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint32_t nt = radix_tiles(a.w);
-    k_hist<<<nt, kSortThreads, 0, s>>>(a.in, a.w, ix.hist, ix.cnt, nt, ix.ctr);
-    k_scan<<<kRadix, kSortThreads, 0, s>>>(ix.cnt, nt, ix.hist, 0, 2 * a.w, ix.ctr);
-    StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
-    k_stage<<<nt, kSortThreads, 0, s>>>(a.in, a.w, c);
-    return 3;
+Geometry make_geometry(uint32_t w, const Tuning &t) {
+    Geometry g;
+    g.w = w;
+    g.tiles = (w + kTileEdges - 1) / kTileEdges;
+    g.bv = std::min(kMaxBucketBits, ceil_log2((2ull * w + t.vbucket_arcs - 1) / t.vbucket_arcs));
+    g.vcap = std::min(t.vcap, kHCap);
+    g.sortcap = std::min(t.sortcap, kVChunk);
+    return g;
+}
+
+static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
+    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.arank, ix.vstart, ix.ctr};
+}
+
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    const Geometry &g = a.g;
+    const uint32_t nV = 1u << g.bv;
+    const PartArgs p = part_args(ix, a);
+    k_count<<<g.tiles, kTileThreads, 2 * kTileWarps * nV, s>>>(p);
+    k_scan_rows<<<nV, 256, 0, s>>>(ix.cntV, ix.vstart, g.tiles, ix.ctr);
+    k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.vcap, ix.vperm, ix.ctr);
+    k_scatter<<<g.tiles, kTileThreads, 4 * nV, s>>>(p);
+    return 4;
 }
 
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint32_t nt = radix_tiles(a.w);
-    StageCtx c{ix.E, ix.keyB, ix.valB, ix.cnt, ix.hist, nt, ix.pt, ix.pmask, a.tag, ix.ctr};
-    k_pairs<<<(a.w + 255) / 256, 256, 0, s>>>(a.in, a.w, c);
+    const uint32_t G = pair_groups(a.g.w);
+    cudaMemsetAsync(ix.pt, 0xFF, 32ull * G, s);
+    k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(a.in, a.g.w, ix.pt, G, ix.ctr);
     return 1;
 }
 
-int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint32_t n = 2 * a.w, nt = radix_tiles(a.w);
-    for (uint32_t p = 1; p < kPasses; ++p) {
-        k_upsweep<<<nt, kSortThreads, 0, s>>>(ix.keyA, ix.keyB, n, ix.hist, p, ix.cnt, nt, ix.ctr);
-        k_scan<<<kRadix, kSortThreads, 0, s>>>(ix.cnt, nt, ix.hist, p, n, ix.ctr);
-        k_downsweep<<<nt, kSortThreads, 0, s>>>(ix.keyA, ix.valA, ix.keyB, ix.valB, n, ix.hist, p, ix.cnt, nt, ix.ctr);
-    }
-    return 3 * (int)(kPasses - 1);
+static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
+    return VertArgs{ix.arcs, ix.scratch, ix.E, ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
+                    ix.vperm, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 
-int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint32_t n = 2 * a.w;
-    const uint32_t tiles = (n + kTile - 1) / kTile;
-    SegBufs sb{ix.keyA, ix.valA, ix.keyB, ix.valB, ix.hist, ix.vt, ix.vmask, a.tag,
-               reinterpret_cast<uint2 *>(ix.einfo), ix.ctr};
-    k_runs<<<tiles, kSortThreads, 0, s>>>(sb, n);
-    k_fix<<<tiles, kSortThreads, 0, s>>>(sb, n);
-    return 2;
+int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    k_vhash<<<1u << a.g.bv, kHThreads, kHSmemBytes, s>>>(vert_args(ix, a));
+    return 1;
+}
+
+int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    k_vbig<<<kBigCTAs, kVBucketThreads, kVSmemBytes, s>>>(vert_args(ix, a));
+    return 1;
 }
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
     if (st.count == 0) return 0;
-    const uint64_t blocks = (st.count + 255) / 256;
-    UpdateIdx u{ix.E, ix.einfo, ix.vt, ix.vmask, ix.valA, ix.valB, ix.hist, ix.pt, ix.pmask, a.tag, ix.ctr};
-    k_update<<<(uint32_t)blocks, 256, 0, s>>>(st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch,
-                                              a.m_prev, a.w, u, st.S + a.S_slot, st.stats);
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w)}, ix.einfo, ix.segS, ix.ctr};
+    UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
+    k_update<<<grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves), 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats);
     return 1;
-}
-
-int launch_init_tables(const IndexBufs &ix, cudaStream_t s) {
-    // tag 0 marks every slot free (live tags start at 1)
-    cudaMemsetAsync(ix.vt, 0, 16ull * ((uint64_t)ix.vmask + 1), s);
-    cudaMemsetAsync(ix.pt, 0, 16ull * ((uint64_t)ix.pmask + 1), s);
-    return 0;
 }
 
 int launch_init_state(const StateBufs &st, cudaStream_t s) {
@@ -748,6 +1150,13 @@ int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *
     if (!st.count) return 0;
     k_group_sums<<<grid_for(st.count, 256, 16), 256, 0, s>>>(st.cf, st.count, groups, out);
     return 1;
+}
+
+int set_kernel_attributes() {
+    cudaError_t e1 = cudaFuncSetAttribute(k_vbig, cudaFuncAttributeMaxDynamicSharedMemorySize, kVSmemBytes);
+    if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kHSmemBytes);
+    cudaError_t e2 = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * 4096);
+    return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;
 }
 
 }  // namespace tcb

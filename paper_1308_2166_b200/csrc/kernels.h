@@ -9,55 +9,73 @@
 namespace tcb {
 
 struct IndexBufs {
-    uint64_t wcap = 0;         // edges the buffers hold
-    uint2 *E = nullptr;        // [wcap] normalized edges
-    uint32_t *keyA = nullptr, *valA = nullptr;  // [2 wcap] radix ping-pong buffers: arc vertex / arc value
-    uint32_t *keyB = nullptr, *valB = nullptr;
-    uint32_t *hist = nullptr;  // [kPasses * kRadix] digit histograms of the arc keys
-    uint32_t *cnt = nullptr;   // [kRadix * tiles] per-tile digit counts -> offsets (current pass)
-    uint64_t tiles_cap = 0;
-    uint4 *einfo = nullptr;    // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
-    VSlot *vt = nullptr;       // [vmask+1]
-    uint32_t vmask = 0;
-    PSlot *pt = nullptr;       // [pmask+1]
-    uint32_t pmask = 0;
-    uint32_t *ctr = nullptr;   // device counters (index.cuh kCtr*)
-    uint2 *stage = nullptr;    // [wcap] H2D staging for host batches
+    uint64_t wcap = 0;             // edges the buffers hold
+    uint64_t tiles_cap = 0;        // count/scatter tiles
+    uint2 *E = nullptr;            // [wcap] normalised edges
+    uint4 *arcs = nullptr;         // [2 wcap] vertex-bucketed arcs {vertex, k<<1|side, neighbour, 0}, arrival
+                                   // order per bucket
+    uint2 *scratch = nullptr;      // [2 wcap] sort scratch of oversized vertex buckets
+    uint2 *segS = nullptr;         // [2 wcap] arcs {k<<1|side, neighbour} grouped by vertex
+    uint4 *einfo = nullptr;        // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
+    VSlot *vt = nullptr;           // [8 wcap] vertex-table slices (bucket b at 4 * start_b)
+    uint2 *vslice = nullptr;       // [4096] {offset, size}
+    uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
+    uint2 *pt = nullptr;           // [4 ceil(wcap / 2)] pair slots {k, fp}, groups of 4
+    uint32_t *cntV = nullptr;      // [4096 * tiles] per-tile vertex-bucket counts -> scatter offsets
+    uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
+    uint32_t *vstart = nullptr;    // [4097] vertex-bucket totals -> exclusive prefix
+    uint32_t *ctr = nullptr;       // device counters (index.cuh kCtr*)
+    uint2 *stage = nullptr;        // [wcap] H2D staging for host batches
 };
 
 struct StateBufs {
     uint64_t count = 0;
     uint2 *r1 = nullptr, *r2 = nullptr;
     uint32_t *cf = nullptr;  // chi in bits 0..30, closed flag in bit 31
-    uint64_t *p1 = nullptr, *p2 = nullptr;
-    unsigned long long *S = nullptr;  // [2] closed-sum accumulators (double-buffered by batch parity)
+    uint32_t *p1 = nullptr, *p2 = nullptr;  // 0-based global positions (< 2^31, reading R13); 0xFFFFFFFF = empty
+    unsigned long long *S = nullptr;      // [2] closed-sum accumulators (double-buffered by batch parity)
     unsigned long long *stats = nullptr;  // [4] fresh f1, replaced f2 of retained f1, sum of D, batches
+};
+
+// Bucket geometry of one batch (host-computed from w and the tuning knobs).
+struct Geometry {
+    uint32_t w;
+    uint32_t tiles;    // ceil(w / kTileEdges)
+    uint32_t bv;       // vertex bucket bits
+    uint32_t vcap;     // vertex buckets larger than this go to k_vbig (<= 4096)
+    uint32_t sortcap;  // k_vbig: buckets larger than this take the chunked global-memory path (<= kVChunk)
 };
 
 struct BatchArgs {
     const uint2 *in;  // w raw edges (device)
-    uint32_t w;
     uint64_t m_prev;
-    uint32_t batch;  // index b of this (non-empty) batch
-    uint32_t tag;    // table tag of this push (never reused while a table slot may carry it)
-    uint64_t first;  // global id of local estimator 0
+    uint32_t batch;   // index b of this (non-empty) batch
+    uint64_t first;   // global id of local estimator 0
     uint64_t seed;
     int S_slot;
+    Geometry g;
 };
 
+struct Tuning {
+    uint32_t vbucket_arcs = 1024;  // target arcs per vertex bucket
+    uint32_t vcap = 4096;
+    uint32_t sortcap = kVChunk;
+};
+
+Geometry make_geometry(uint32_t w, const Tuning &t);
+
 // Each returns the number of kernel launches issued.
-int launch_stage(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
-int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
-int launch_sort(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
-int launch_segment(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a1: count, scans, scatter
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);      // a3: edge-pair table
+int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);   // a2: grouping, ranks, vertex table
+int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a2: the buckets > vcap
+constexpr uint32_t kBigCTAs = 32;
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s);
-int launch_init_tables(const IndexBufs &ix, cudaStream_t s);
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
 int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *out, cudaStream_t s);
-int launch_unpack_state(const StateBufs &st, uint64_t first, uint64_t count, uint32_t *c, uint8_t *closed,
-                        cudaStream_t s);
 
 int sm_count();
+int set_kernel_attributes();  // dynamic shared memory limits on the current device
 
 }  // namespace tcb

@@ -73,8 +73,8 @@ def test_C1_per_batch_states():
         assert_states_equal(g.state(), o.state(), f"after batch {k // 2048}")
 
 
-def test_hub_segments_multi_chunk():
-    """A star with 5000 leaves plus noise: segments > 32 (bitonic chunks) and > 2048 (chunk merge)."""
+def _hub_stream():
+    """A star with 5000 leaves plus ER noise, deduplicated, random order and orientation."""
     rng = np.random.default_rng(5)
     leaves = rng.permutation(np.arange(1, 9000, dtype=np.uint32))[:5000]
     star = np.stack([np.zeros(5000, np.uint32), leaves], 1)
@@ -86,9 +86,36 @@ def test_hub_segments_multi_chunk():
     s[flip] = s[flip][:, ::-1]
     keys = np.sort(s, 1)
     _, uniq = np.unique(keys[:, 0].astype(np.uint64) << np.uint64(32) | keys[:, 1], return_index=True)
-    s = np.ascontiguousarray(s[np.sort(uniq)])
+    return np.ascontiguousarray(s[np.sort(uniq)])
+
+
+def test_hub_segments_multi_chunk():
+    """The hub's vertex bucket (> 4096 arcs at the largest w) takes the chunked global-memory path."""
+    s = _hub_stream()
     for w in (len(s), 4099, 700):
         _compare(s, 3000, 99 + w, w)
+
+
+@pytest.mark.parametrize("knobs", [
+    dict(vbucket_cap=1, vbucket_sort_cap=1),       # every non-trivial bucket through the chunked global path
+    dict(vbucket_cap=1),                           # every vertex bucket through the radix-sort kernel
+    dict(vbucket_cap=37, vbucket_sort_cap=200),    # a mix of all paths
+    dict(vbucket_arcs=16),                         # many buckets (bucket bits capped at 12)
+    dict(vbucket_arcs=1 << 30),                    # one vertex bucket
+])
+def test_index_geometry_knobs(knobs):
+    """Results never depend on the index geometry (tc_tune): bit-exact against the oracle."""
+    from paper_1308_2166_b200 import TriangleCounter
+    s = _hub_stream()
+    for w in (len(s), 2500, 1):
+        ww = w if w > 1 else 1
+        tc = TriangleCounter(1500, 5 + w)
+        tc.tune(**knobs)
+        n = len(s) if w > 1 else 300
+        for k in range(0, n, ww):
+            tc.push_batch(s[k:min(n, k + ww)])
+        o = oracle_run(s[:n], 1500, 5 + w, ww)
+        assert_states_equal(tc.state(), o.state(), f"{knobs} w={w}")
 
 
 def test_device_pinned_pageable_inputs_agree():
