@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <array>
 #include <vector>
 
 #include "../../include/tc.h"
@@ -43,10 +44,11 @@ struct tc_ctx {
     cudaEvent_t copy_done = nullptr;
     // profiling
     int prof = 0;
-    cudaEvent_t ev[2 * TC_NPHASES] = {};  // begin / end of each phase (the pair phase on the side stream)
+    // begin / end events of each phase, one set per profiled push (read and recycled at the next sync)
+    std::vector<std::array<cudaEvent_t, 2 * TC_NPHASES>> ev_pool;
+    size_t ev_used = 0;
     double prof_ms[TC_NPHASES] = {};
     uint64_t prof_launch[TC_NPHASES] = {};
-    int prof_pending = 0;
     // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
     int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
     cudaGraphExec_t gexec = nullptr;
@@ -65,7 +67,7 @@ static int fail_cuda(tc_ctx *c) {
     } while (0)
 
 static void free_index(IndexBufs &ix) {
-    void *bufs[] = {ix.E, ix.arcs, ix.scratch, ix.segS, ix.einfo, ix.vt, ix.vslice, ix.vperm, ix.pt,
+    void *bufs[] = {ix.E, ix.arcs, ix.scratch, ix.segS, ix.einfo, ix.vt, ix.vslice, ix.vperm, ix.vdefer, ix.pt,
                     ix.cntV, ix.arank, ix.vstart, ix.ctr, ix.stage};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
@@ -91,7 +93,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
               // vertex-table slices: bucket b owns [4 start_b, 4 start_b + 4 n_b) (next_pow2(2 D_b) < 4 n_b): 8 w slots
               cudaMalloc(&ix.vt, 16 * 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess &&
-              cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
+              cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.vdefer, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
               cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
               cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess &&
               cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
@@ -120,8 +122,9 @@ static void destroy_ctx(tc_ctx *ctx) {
     cudaFree(ctx->st.stats);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
-    for (auto &e : ctx->ev)
-        if (e) cudaEventDestroy(e);
+    for (auto &set : ctx->ev_pool)
+        for (auto &e : set)
+            if (e) cudaEventDestroy(e);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->side2) cudaStreamDestroy(ctx->side2);
@@ -189,9 +192,6 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
               cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess;
     if (ok) {
-        for (auto &e : ctx->ev) ok = ok && cudaEventCreate(&e) == cudaSuccess;
-    }
-    if (ok) {
         ok = cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream) == cudaSuccess &&
              cudaMemsetAsync(ctx->st.stats, 0, 32, ctx->stream) == cudaSuccess;
         launch_init_state(ctx->st, ctx->stream);
@@ -235,14 +235,15 @@ static int settle(tc_ctx *ctx) {
             return code;
         }
     }
-    if (ctx->prof_pending) {
+    for (size_t i = 0; i < ctx->ev_used; ++i) {  // completed profiled pushes
         for (int p = 0; p < TC_NPHASES; ++p) {
             float ms = 0.f;
-            if (cudaEventElapsedTime(&ms, ctx->ev[2 * p], ctx->ev[2 * p + 1]) == cudaSuccess) ctx->prof_ms[p] += ms;
+            if (cudaEventElapsedTime(&ms, ctx->ev_pool[i][2 * p], ctx->ev_pool[i][2 * p + 1]) == cudaSuccess)
+                ctx->prof_ms[p] += ms;
         }
-        cudaGetLastError();
-        ctx->prof_pending = 0;
     }
+    cudaGetLastError();
+    ctx->ev_used = 0;
     return ctx->poisoned ? (ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE) : TC_OK;
 }
 
@@ -254,9 +255,11 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     CK(cudaSetDevice(ctx->device));
     const bool ovf = ctx->m + w > 0x7FFFFFFFull;  // chi <= m must fit 31 bits (reading R13)
     if (ovf && ctx->async_errors) return TC_EOVERFLOW;  // async mode: reported first, state untouched
-    if (ctx->prof_pending) {
-        int rc = settle(ctx);
-        if (rc != TC_OK) return rc;
+    if (ctx->prof && ctx->ev_used == ctx->ev_pool.size()) {  // a new event set for this push
+        std::array<cudaEvent_t, 2 * TC_NPHASES> set{};
+        for (auto &e : set)
+            if (cudaEventCreate(&e) != cudaSuccess) return fail_cuda(ctx);
+        ctx->ev_pool.push_back(set);
     }
     int rc = grow_index(ctx, w);
     if (rc != TC_OK) return rc;
@@ -299,7 +302,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         bool ok = true;
         cudaStream_t ms = ctx->stream, ss = ctx->side, s2 = ctx->side2;
         auto rec = [&](int e, cudaStream_t st) {
-            if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev[e], st) == cudaSuccess;
+            if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev_pool[ctx->ev_used][e], st) == cudaSuccess;
         };
         if (ctx->async_errors) {
             ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ms) == cudaSuccess;  // keep the sticky error
@@ -335,7 +338,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         rec(2 * TC_PHASE_UPDATE + 1, ms);
         if (ctx->prof)
             for (int p = 0; p < TC_NPHASES; ++p)
-                ctx->prof_launch[p] += (p == TC_PHASE_PARTITION ? 4 : p == TC_PHASE_VERTICES ? 2 : 1);
+                ctx->prof_launch[p] += (p == TC_PHASE_PARTITION ? 4 : p == TC_PHASE_VERTICES ? 3 : 1);
         if (graph) {
             cudaGraph_t g = nullptr;
             const bool cap = cudaStreamEndCapture(ctx->stream, &g) == cudaSuccess && g;
@@ -359,7 +362,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
             return fail_cuda(ctx);
         }
     }
-    if (ctx->prof) ctx->prof_pending = 1;
+    if (ctx->prof) ++ctx->ev_used;
     CK(cudaGetLastError());
     if (!ctx->async_errors) {
         CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost, ctx->stream));

@@ -43,9 +43,11 @@ constexpr uint32_t kVChunk = kVBucketThreads * kVItems;  // 6144 arcs: larger bu
 
 // device counters (ctr[])
 constexpr int kCtrD = 0;       // distinct vertices of W
-constexpr int kCtrTicket = 1;  // k_vbig's bucket ticket
-constexpr int kCtrBig = 2;     // vertex buckets handled by k_vbig
+constexpr int kCtrTicket = 1;  // k_vhub's bucket ticket
+constexpr int kCtrBig = 2;     // vertex buckets larger than vcap (k_vhub's)
 constexpr int kCtrErr = 3;     // error bits
+constexpr int kCtrDefer = 4;   // buckets k_vhub deferred to k_vbig
+constexpr int kCtrTicket2 = 5; // k_vbig's bucket ticket
 constexpr int kCtrWords = 16;
 
 struct __align__(16) VSlot {

@@ -26,6 +26,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "index.cuh"
 #include "kernels.h"
@@ -338,6 +339,7 @@ struct VertArgs {
     VSlot *vt;
     uint2 *vslice;
     const uint32_t *vperm;
+    uint32_t *vdefer;
     uint32_t bv;
     uint32_t vcap;      // buckets with more arcs go to k_vbig
     uint32_t sortcap;   // k_vbig: buckets with more arcs take the chunked global-memory path
@@ -674,18 +676,18 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
     }
 }
 
-// Persistent CTAs over the large buckets (vperm[0 .. ctr[kCtrBig])), on their own stream.
+// Persistent CTAs over the buckets k_vhub deferred (vdefer[0 .. ctr[kCtrDefer])), after it on its stream.
 __global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ __align__(16) unsigned char vsm[];
     __shared__ uint32_t dtot[512];
     __shared__ uint32_t ws[33];
     __shared__ uint32_t s_b;
-    const uint32_t nbig = a.ctr[kCtrBig];
+    const uint32_t ndef = a.ctr[kCtrDefer];
     while (true) {
         if (threadIdx.x == 0) {
-            const uint32_t t = atomicAdd(&a.ctr[kCtrTicket], 1u);
-            s_b = t < nbig ? a.vperm[t] : 0xFFFFFFFFu;
+            const uint32_t t = atomicAdd(&a.ctr[kCtrTicket2], 1u);
+            s_b = t < ndef ? a.vdefer[t] : 0xFFFFFFFFu;
         }
         __syncthreads();
         const uint32_t b = s_b;
@@ -712,9 +714,28 @@ constexpr uint32_t kHSmemBytes = kHR1 + kHCap * 4;
 static_assert(kHWarps * kHSweep * 2 + (kHCap + 1) * 4 <= kHR1, "phase-3 arrays must fit R1");
 static_assert(2 * kHCap * 4 <= kHWarps * kHSweep * 2 + 4, "the slice table must fit over whist");
 
+// Arcs of a bucket as the hash path reads them: straight from the bucketed arcs, or (after a hub vertex
+// was peeled off) from a shared-memory list of the remaining arcs.
+struct ArcSrc {
+    const uint4 *g;                    // global {vertex, val, neighbour, 0} (g != nullptr), else:
+    const uint32_t *sv, *sval, *snb;   // shared-memory lists
+    __device__ __forceinline__ uint32_t v(uint32_t i) const { return g ? g[i].x : sv[i]; }
+    __device__ __forceinline__ uint2 vv(uint32_t i) const {
+        if (g) {
+            const uint4 x = g[i];
+            return make_uint2(x.x, x.y);
+        }
+        return make_uint2(sv[i], sval[i]);
+    }
+    __device__ __forceinline__ uint32_t nb(uint32_t i) const { return g ? __ldcs(g + i).z : snb[i]; }
+};
+
+// Hash-path grouping of n arcs (src) of bucket b whose segments start at slot base + off0; `hub` (if
+// hubn > 0) is an extra vertex whose segment [base, base + hubn) was already written.
 template <int R>
-__device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint32_t base, uint32_t n,
-                                             unsigned char *sm, uint32_t *ws, uint32_t *sD) {
+__device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint32_t base, const ArcSrc &src, uint32_t n,
+                                             uint32_t off0, uint32_t hub, uint32_t hubn, unsigned char *sm,
+                                             uint32_t *ws, uint32_t *sD) {
     uint32_t *hkey = reinterpret_cast<uint32_t *>(sm);
     uint16_t *lid = reinterpret_cast<uint16_t *>(sm + kHTable * 4);
     uint16_t *whist = reinterpret_cast<uint16_t *>(sm);
@@ -722,7 +743,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     uint32_t *table = reinterpret_cast<uint32_t *>(sm);
     uint32_t *vkey = reinterpret_cast<uint32_t *>(sm + kHR1);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
-    const uint32_t Tb = pow2_ceil(2 * n);
+    const uint32_t Tb = pow2_ceil(2 * max(n, 1u));
     for (uint32_t s = threadIdx.x; s < Tb; s += kHThreads) hkey[s] = kEmptyV;
     if (threadIdx.x == 0) *sD = 0;
     __syncthreads();
@@ -733,7 +754,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         const uint32_t i = warp * 32u * R + j * 32u + lane;
         pk[j] = 0xFFFFFFFFu;
         if (i < n) {
-            const uint4 x = a.arcs[base + i];
+            const uint2 x = src.vv(i);
             val[j] = x.y;
             uint32_t s = hash_vertex(x.x) & (Tb - 1);
             while (true) {
@@ -818,35 +839,48 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         __syncthreads();
     }
     // phase 4: per arc, segS and {slot, segment end}
+    const uint32_t b0 = base + off0;
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         if (pk[j] == 0xFFFFFFFFu) continue;
         const uint32_t l = pk[j] >> 16;
         const uint32_t pos = segst[l] + (pk[j] & 0xFFFFu);
         const uint32_t i = warp * 32u * R + j * 32u + lane;
-        a.segS[base + pos] = make_uint2(val[j], __ldcs(a.arcs + base + i).z);
-        a.einfo2[val[j]] = make_uint2(base + pos, base + segst[l + 1]);
+        a.segS[b0 + pos] = make_uint2(val[j], src.nb(i));
+        a.einfo2[val[j]] = make_uint2(b0 + pos, b0 + segst[l + 1]);
     }
-    // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole
-    const uint32_t S = slice_size(D);
+    // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole; the hub (if
+    // any) is entry D
+    const uint32_t Dt = D + (hubn ? 1u : 0u);
+    const uint32_t S = slice_size(Dt);
     const uint64_t off = 4ull * base;
     if (threadIdx.x == 0) {
         a.vslice[b] = make_uint2((uint32_t)off, S);
-        if (D) atomicAdd(&a.ctr[kCtrD], D);
+        if (Dt) atomicAdd(&a.ctr[kCtrD], Dt);
     }
     for (uint32_t s = threadIdx.x; s < S; s += kHThreads) table[s] = kEmptyV;
     __syncthreads();
-    for (uint32_t l = threadIdx.x; l < D; l += kHThreads) {
-        uint32_t s = hash_vertex(vkey[l]) & (S - 1) & ~1u;
+    for (uint32_t l = threadIdx.x; l < Dt; l += kHThreads) {
+        uint32_t s = hash_vertex(l < D ? vkey[l] : hub) & (S - 1) & ~1u;
         while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV) s = (s + 1) & (S - 1);
     }
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < S; s += kHThreads) {
         const uint32_t l = table[s];
         uint4 o = make_uint4(kEmptyV, 0u, 0u, 0u);
-        if (l != kEmptyV) o = make_uint4(vkey[l], segst[l + 1] - segst[l], base + segst[l], 0u);
+        if (l < D) o = make_uint4(vkey[l], segst[l + 1] - segst[l], b0 + segst[l], 0u);
+        else if (l == D) o = make_uint4(hub, hubn, base, 0u);
         reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
     }
+}
+
+template <typename F>
+__device__ __forceinline__ void hash_dispatch(uint32_t n, F f) {
+    if (n <= 256) f(std::integral_constant<int, 1>());
+    else if (n <= 512) f(std::integral_constant<int, 2>());
+    else if (n <= 1024) f(std::integral_constant<int, 4>());
+    else if (n <= 2048) f(std::integral_constant<int, 8>());
+    else f(std::integral_constant<int, 16>());
 }
 
 __global__ void __launch_bounds__(kHThreads, 3) k_vhash(VertArgs a) {
@@ -856,12 +890,135 @@ __global__ void __launch_bounds__(kHThreads, 3) k_vhash(VertArgs a) {
     __shared__ uint32_t sD;
     const uint32_t b = blockIdx.x;
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
-    if (n > a.vcap) return;  // k_vbig's
-    if (n <= 256) vbucket_hash<1>(a, b, base, n, hsm, ws, &sD);
-    else if (n <= 512) vbucket_hash<2>(a, b, base, n, hsm, ws, &sD);
-    else if (n <= 1024) vbucket_hash<4>(a, b, base, n, hsm, ws, &sD);
-    else if (n <= 2048) vbucket_hash<8>(a, b, base, n, hsm, ws, &sD);
-    else vbucket_hash<16>(a, b, base, n, hsm, ws, &sD);
+    if (n > a.vcap) return;  // k_vhub's
+    const ArcSrc src{a.arcs + base, nullptr, nullptr, nullptr};
+    hash_dispatch(n, [&](auto r) { vbucket_hash<decltype(r)::value>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD); });
+}
+
+// Large buckets (more than vcap arcs): almost always one hub vertex plus about a normal bucket's worth of
+// others.  The most frequent vertex of a sample is peeled off (its arcs are one segment, already in arrival
+// order: a 1-bit stable partition), the rest goes through the hash path from shared memory.  Buckets whose
+// rest is still too large are deferred to k_vbig.  Persistent CTAs over vperm[0 .. ctr[kCtrBig]).
+constexpr uint32_t kHubSample = 256;
+constexpr uint32_t kVHubSmemBytes = kHSmemBytes + 3 * kHCap * 4;
+
+__global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
+    if (a.ctr[kCtrErr] & kErrStage) return;
+    extern __shared__ __align__(16) unsigned char hsm[];
+    uint32_t *rv = reinterpret_cast<uint32_t *>(hsm + kHSmemBytes);
+    uint32_t *rval = rv + kHCap, *rnb = rval + kHCap;
+    __shared__ uint32_t ws[9];
+    __shared__ uint32_t sD, s_b, s_h, s_cnt;
+    __shared__ uint32_t skey[2 * kHubSample], scnt[2 * kHubSample];
+    __shared__ uint32_t wtot[2][kHWarps];
+    __shared__ unsigned long long wbest[kHWarps];
+    const uint32_t nbig = a.ctr[kCtrBig];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    while (true) {
+        if (threadIdx.x == 0) {
+            const uint32_t t = atomicAdd(&a.ctr[kCtrTicket], 1u);
+            s_b = t < nbig ? a.vperm[t] : 0xFFFFFFFFu;
+        }
+        __syncthreads();
+        const uint32_t b = s_b;
+        if (b == 0xFFFFFFFFu) return;
+        const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
+        const uint4 *arcs = a.arcs + base;
+        // 1. candidate hub = the most frequent vertex of kHubSample evenly spaced arcs
+        for (uint32_t s = threadIdx.x; s < 2 * kHubSample; s += kHThreads) {
+            skey[s] = kEmptyV;
+            scnt[s] = 0;
+        }
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        {
+            const uint32_t v = arcs[(uint32_t)(((uint64_t)threadIdx.x * n) / kHubSample)].x;
+            uint32_t s = hash_vertex(v) & (2 * kHubSample - 1);
+            while (true) {
+                const uint32_t k = atomicCAS(&skey[s], kEmptyV, v);
+                if (k == kEmptyV || k == v) break;
+                s = (s + 1) & (2 * kHubSample - 1);
+            }
+            atomicAdd(&scnt[s], 1u);
+        }
+        __syncthreads();
+        {
+            uint32_t best = 0, bs = 0;
+            for (uint32_t t2 = threadIdx.x; t2 < 2 * kHubSample; t2 += kHThreads)
+                if (scnt[t2] > best) {
+                    best = scnt[t2];
+                    bs = t2;
+                }
+            unsigned long long pkd = ((unsigned long long)best << 32) | bs;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long y = __shfl_xor_sync(kFull, pkd, o);
+                pkd = y > pkd ? y : pkd;
+            }
+            if (lane == 0) wbest[warp] = pkd;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long m = wbest[0];
+                for (uint32_t x = 1; x < kHWarps; ++x) m = wbest[x] > m ? wbest[x] : m;
+                s_h = skey[(uint32_t)m];
+            }
+            __syncthreads();
+        }
+        const uint32_t h = s_h;
+        // 2. hub arcs H; the rest must fit the hash path
+        uint32_t mine = 0;
+        for (uint32_t i = threadIdx.x; i < n; i += kHThreads) mine += arcs[i].x == h ? 1u : 0u;
+        mine = __reduce_add_sync(kFull, mine);
+        if (lane == 0) atomicAdd(&s_cnt, mine);
+        __syncthreads();
+        const uint32_t H = s_cnt;
+        if (n - H > kHCap) {  // not one hub: the radix-sort kernel takes it
+            if (threadIdx.x == 0) a.vdefer[atomicAdd(&a.ctr[kCtrDefer], 1u)] = b;
+            __syncthreads();
+            continue;
+        }
+        // 3. stable 1-bit partition: hub arcs -> segment [base, base + H); the rest -> shared lists
+        uint32_t hubrun = 0, restrun = 0;
+        for (uint32_t q0 = 0; q0 < n; q0 += kHThreads) {
+            const uint32_t i = q0 + threadIdx.x;
+            uint4 x = make_uint4(0u, 0u, 0u, 0u);
+            if (i < n) x = arcs[i];
+            const bool valid = i < n, isH = valid && x.x == h;
+            const uint32_t bh = __ballot_sync(kFull, isH), br = __ballot_sync(kFull, valid && !isH);
+            if (lane == 0) {
+                wtot[0][warp] = __popc(bh);
+                wtot[1][warp] = __popc(br);
+            }
+            __syncthreads();
+            uint32_t ph = hubrun, pr = restrun, th = 0, tr = 0;
+#pragma unroll
+            for (uint32_t w2 = 0; w2 < kHWarps; ++w2) {
+                if (w2 < warp) {
+                    ph += wtot[0][w2];
+                    pr += wtot[1][w2];
+                }
+                th += wtot[0][w2];
+                tr += wtot[1][w2];
+            }
+            if (isH) {
+                const uint32_t pos = ph + __popc(bh & lt);
+                a.segS[base + pos] = make_uint2(x.y, x.z);
+                a.einfo2[x.y] = make_uint2(base + pos, base + H);
+            } else if (valid) {
+                const uint32_t r = pr + __popc(br & lt);
+                rv[r] = x.x;
+                rval[r] = x.y;
+                rnb[r] = x.z;
+            }
+            hubrun += th;
+            restrun += tr;
+            __syncthreads();
+        }
+        // 4. the rest through the hash path (segments after the hub's), the hub as an extra vertex
+        const ArcSrc src{nullptr, rv, rval, rnb};
+        hash_dispatch(n - H, [&](auto r) { vbucket_hash<decltype(r)::value>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD); });
+        __syncthreads();
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -898,6 +1055,8 @@ __device__ __forceinline__ EstState load_state(const UpdateArgs &u, uint64_t t) 
 }
 
 // Steps 1-3 for estimator t (local index) whose state was read into `old`.  Returns chi if it ends closed.
+// Written straight-line: the loads of the fresh-f1 and retained-f1 paths are predicated, not branched, so
+// a warp with both kinds of lanes waits for one round trip, not two.
 __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const UpdateIdx &ix, uint64_t t, const EstState &old,
                                                uint32_t &n_fresh, uint32_t &n_r2old) {
     const uint64_t gid = u.first + t;
@@ -910,65 +1069,80 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
     // ---- Step 1: level-1 reservoir ----
     const uint64_t d1 = bounded(m_prev + u.w, xlo, dc, 0x10000u);
     const bool fresh = d1 >= m_prev;
-    uint2 r1, r2;
-    uint32_t c, ld, rd, endU, endV;
-    bool closed, had_r2 = false;
+    const uint32_t j = fresh ? (uint32_t)(d1 - m_prev) : 0u;
+    // ---- Step 2a: chi^+ = rank(u->v) + rank(v->u) ----
+    // fresh f1 = w_j: its ranks from einfo[j]; retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821)
+    uint2 r1 = old.r1;
+    uint4 inf = make_uint4(0u, 0u, 0u, 0u);
+    uint2 su = make_uint2(0u, 0u), sv = make_uint2(0u, 0u);
+    const uint32_t hu = hash_vertex(r1.x), hv = hash_vertex(r1.y);
     if (fresh) {
-        const uint32_t j = (uint32_t)(d1 - m_prev);
         r1 = __ldg(ix.L.E + j);
-        r2 = make_uint2(kEmptyV, kEmptyV);
-        c = 0;
-        closed = false;
-        // ---- Step 2a for a fresh f1 = w_j: ld = rank(u->v), rd = rank(v->u) ----
-        const uint4 inf = __ldg(ix.einfo + j);
+        inf = __ldg(ix.einfo + j);
+    } else {
+        su = __ldg(ix.L.vslice + vbucket_of(hu, ix.L.bv));
+        sv = __ldg(ix.L.vslice + vbucket_of(hv, ix.L.bv));
+    }
+    const uint32_t bu = hu & (su.y - 1u) & ~1u, bw = hv & (sv.y - 1u) & ~1u;
+    uint4 u0 = make_uint4(kEmptyV, 0u, 0u, 0u), u1 = u0, v0 = u0, v1 = u0;
+    if (su.y) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(ix.L.vt + su.x + bu);
+        u0 = __ldg(p);
+        u1 = __ldg(p + 1);
+    }
+    if (sv.y) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(ix.L.vt + sv.x + bw);
+        v0 = __ldg(p);
+        v1 = __ldg(p + 1);
+    }
+    uint32_t ld, rd, endU, endV;
+    if (fresh) {
         ld = inf.y - 1u - inf.x;
         rd = inf.w - 1u - inf.z;
         endU = inf.y;
         endV = inf.w;
     } else {
-        r1 = old.r1;
-        r2 = old.r2;
-        c = old.cf & kCMask;
-        closed = (old.cf & kClosedBit) != 0;
-        had_r2 = c > 0;  // NBSI: chi == 0 <=> f2 empty
-        // ---- Step 2a for a retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821) ----
-        VertProbe pu, pv;
-        vt_issue(ix.L, r1.x, pu);
-        vt_issue(ix.L, r1.y, pv);
-        const uint2 iu = vt_resolve(ix.L, pu, r1.x), iv = vt_resolve(ix.L, pv, r1.y);
+        uint2 iu = u0.x == r1.x ? make_uint2(u0.y, u0.z) : u1.x == r1.x ? make_uint2(u1.y, u1.z) : make_uint2(0u, 0u);
+        uint2 iv = v0.x == r1.y ? make_uint2(v0.y, v0.z) : v1.x == r1.y ? make_uint2(v1.y, v1.z) : make_uint2(0u, 0u);
+        if (su.y && u0.x != r1.x && u1.x != r1.x && u0.x != kEmptyV && u1.x != kEmptyV)
+            iu = vt_find_from(ix.L, su, bu, r1.x);  // rare: the first sector is full without u
+        if (sv.y && v0.x != r1.y && v1.x != r1.y && v0.x != kEmptyV && v1.x != kEmptyV)
+            iv = vt_find_from(ix.L, sv, bw, r1.y);
         ld = iu.x;
         rd = iv.x;
         endU = iu.y + iu.x;
         endV = iv.y + iv.x;
     }
-    const uint32_t chi_p = ld + rd;  // |Gamma_W(f1)| = rank(u->v) + rank(v->u)
+    uint2 r2 = fresh ? make_uint2(kEmptyV, kEmptyV) : old.r2;
+    uint32_t c = fresh ? 0u : (old.cf & kCMask);
+    bool closed = !fresh && (old.cf & kClosedBit) != 0;
+    const bool had_r2 = c > 0;  // NBSI: chi == 0 <=> f2 empty (always false for a fresh f1)
+    const uint32_t chi_p = ld + rd;  // |Gamma_W(f1)|
+    // ---- Step 2b: keep f2 w.p. chi^-/(chi^-+chi^+), else phi names an edge ----
     bool r2new = false;
     uint32_t k2 = 0, x = 0, z = 0;
     if (chi_p) {
-        // ---- Step 2b: keep f2 w.p. chi^-/(chi^-+chi^+), else phi names an edge ----
         const uint64_t d2 = bounded((uint64_t)c + chi_p, xhi, dc, 0x20000u);
-        if (d2 >= c) {
-            const uint32_t phi = (uint32_t)(d2 - c);
-            const bool atU = phi < ld;  // (src = u, rank = phi) or (src = v, rank = phi - ld)
-            const uint32_t end = atU ? endU : endV;
-            const uint32_t a = atU ? phi : phi - ld;
-            const uint2 arc = __ldg(ix.segS + (end - 1u - a));  // {k<<1|side, neighbour}
+        r2new = d2 >= c;
+        c += chi_p;
+        const uint32_t phi = (uint32_t)(d2 - (c - chi_p));
+        const bool atU = phi < ld;  // (src = u, rank = phi) or (src = v, rank = phi - ld)
+        if (r2new) {
+            const uint2 arc = __ldg(ix.segS + ((atU ? endU : endV) - 1u - (atU ? phi : phi - ld)));
             const uint32_t src = atU ? r1.x : r1.y;
             k2 = arc.x >> 1;
             r2 = make_uint2(min(src, arc.y), max(src, arc.y));
             x = atU ? r1.y : r1.x;  // f1's endpoint not on f2
             z = arc.y;              // f2's endpoint not on f1
-            r2new = true;
             closed = false;
         }
-        c += chi_p;
     }
     // ---- Step 3: closing edge after f2; an old f2 precedes every batch edge ----
+    if (!r2new) {
+        x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;
+        z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;
+    }
     if ((r2new || had_r2) && !closed) {
-        if (!r2new) {
-            x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;
-            z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;
-        }
         const int64_t kk = pt_find(ix.L, min(x, z), max(x, z));
         if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
     }
@@ -986,7 +1160,10 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
 
 // One pass over the estimator SoA: a grid of a few CTAs per SM loops over the estimators, reading the next
 // estimator's state while it works on the current one.
-__global__ void __launch_bounds__(256, 3) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
+#ifndef TC_UPD_MINB
+#define TC_UPD_MINB 4
+#endif
+__global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
                                                    unsigned long long *stats) {
     if (ix.ctr[kCtrErr]) return;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1071,7 +1248,10 @@ int sm_count() {
     return g_sms;
 }
 
-constexpr uint32_t kUpdateCTAsPerSM = 3, kUpdateWaves = 2;  // k_update grid: estimators per thread >= 1
+#ifndef TC_UPD_WAVES
+#define TC_UPD_WAVES 1
+#endif
+constexpr uint32_t kUpdateCTAsPerSM = 4, kUpdateWaves = TC_UPD_WAVES;  // k_update grid
 
 static inline uint32_t grid_for(uint64_t items, uint32_t threads, uint32_t per_sm) {
     const uint64_t want = (items + threads - 1) / threads;
@@ -1119,7 +1299,7 @@ int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
     return VertArgs{ix.arcs, ix.scratch, ix.E, ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
-                    ix.vperm, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
+                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
@@ -1128,8 +1308,9 @@ int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    k_vhub<<<kBigCTAs, kHThreads, kVHubSmemBytes, s>>>(vert_args(ix, a));
     k_vbig<<<kBigCTAs, kVBucketThreads, kVSmemBytes, s>>>(vert_args(ix, a));
-    return 1;
+    return 2;
 }
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
@@ -1155,6 +1336,7 @@ int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *
 int set_kernel_attributes() {
     cudaError_t e1 = cudaFuncSetAttribute(k_vbig, cudaFuncAttributeMaxDynamicSharedMemorySize, kVSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kHSmemBytes);
+    if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
     cudaError_t e2 = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * 4096);
     return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;
 }

@@ -20,6 +20,7 @@ struct IndexBufs {
     VSlot *vt = nullptr;           // [8 wcap] vertex-table slices (bucket b at 4 * start_b)
     uint2 *vslice = nullptr;       // [4096] {offset, size}
     uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
+    uint32_t *vdefer = nullptr;    // [4096] large buckets k_vhub hands to k_vbig
     uint2 *pt = nullptr;           // [4 ceil(wcap / 2)] pair slots {k, fp}, groups of 4
     uint32_t *cntV = nullptr;      // [4096 * tiles] per-tile vertex-bucket counts -> scatter offsets
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket

@@ -97,8 +97,9 @@ def test_hub_segments_multi_chunk():
 
 
 @pytest.mark.parametrize("knobs", [
-    dict(vbucket_cap=1, vbucket_sort_cap=1),       # every non-trivial bucket through the chunked global path
-    dict(vbucket_cap=1),                           # every vertex bucket through the radix-sort kernel
+    dict(vbucket_cap=1, vbucket_sort_cap=1),       # every bucket through the hub-peel kernel; deferred ones chunked
+    dict(vbucket_cap=1),                           # every vertex bucket through the hub-peel kernel
+    dict(vbucket_arcs=8192, vbucket_cap=1),        # hub-less buckets > 4096 arcs: radix sort in shared memory
     dict(vbucket_cap=37, vbucket_sort_cap=200),    # a mix of all paths
     dict(vbucket_arcs=16),                         # many buckets (bucket bits capped at 12)
     dict(vbucket_arcs=1 << 30),                    # one vertex bucket
