@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--w", type=int, default=0, help="override the batch size (C5 sweep)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], help="index-geometry knob key=value (tc_tune)")
     return ap.parse_args()
 
 
@@ -186,6 +187,7 @@ def run_b200(args):
     dev = torch.device("cuda", torch.cuda.current_device())
 
     from paper_1308_2166_b200 import TriangleCounter, build as libbuild
+    from paper_1308_2166_b200.dist import ShardedCounter
     libbuild.build()
 
     cfg = dict(CONFIGS[args.config])
@@ -199,42 +201,42 @@ def run_b200(args):
 
     # stream resident in HBM before timing ("excluding I/O"); rank 0 owns it
     dstream = torch.from_numpy(stream.view(np.int32)).to(dev) if rank == 0 else None
-    bbuf = torch.empty((w, 2), dtype=torch.int32, device=dev)
     flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
 
-    def batch(k, ext=None):
+    knobs = {k: int(v) for k, v in (kv.split("=") for kv in args.tune)}
+
+    def engine(r_, seed_, first_, count_):
+        tc_ = TriangleCounter(r_, seed_, first=first_, count=count_, device=dev.index, w_max_hint=w)
+        tc_.set_async(True)
+        if knobs:
+            tc_.tune(**knobs)
+        return tc_
+
+    # one shard of the estimators per rank; rank 0 broadcasts each batch on the library's stream (NCCL over
+    # NVLink: the per-batch exchange, inside the timed step)
+    sc = ShardedCounter(r, args.seed, w, device=dev, engine_factory=engine)
+    assert (sc.first, sc.count) == (first, count)
+    tc = sc.engine
+
+    def push(k):
         lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
         if world == 1:
-            return dstream[lo:hi]
-        n = hi - lo
-        cur = torch.cuda.current_stream()
-        if ext is not None:
-            cur.wait_stream(ext)  # the previous batch's kernels are done reading bbuf
-        if rank == 0:
-            bbuf[:n].copy_(dstream[lo:hi])
-        torch.distributed.broadcast(bbuf[:n], src=0)  # NCCL over NVLink: the per-batch exchange
-        if ext is not None:
-            ext.wait_stream(cur)  # the library stream sees the broadcast batch
-        return bbuf[:n]
-
-    def make():
-        tc = TriangleCounter(r, args.seed, first=first, count=count, device=dev.index, w_max_hint=w)
-        tc.set_async(True)
-        return tc
+            tc.push_batch(dstream[lo:hi])
+        else:
+            sc.push_batch(dstream[lo:hi] if rank == 0 else None, w=hi - lo)
+        return hi - lo
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
     # ---- warm-up (untimed) ----
-    tc = make()
     for k in range(args.warmup):
         if k and k % nb == 0:
             assert tc.sync() == 0
             tc.reset()
-        ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
-        tc.push_batch(batch(k, ext))
+        push(k)
     assert tc.sync() == 0
 
     # ---- timed: K steps = K consecutive batches of the stream (a new pass over the stream starts from a
@@ -272,13 +274,12 @@ def run_b200(args):
                 flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(ext)
-            b = batch(k, ext)
-            tc.push_batch(b)
+            n = push(k)
             with torch.cuda.stream(ext):
                 e1.record(ext)
             evs.append((e0, e1))
             launches += tc.last_launches()
-            edges_done += b.shape[0]
+            edges_done += n
         assert tc.sync() == 0
         torch.cuda.synchronize()
         t_wall = time.perf_counter() - t_wall

@@ -122,7 +122,7 @@ int tc_set_async(tc_ctx *ctx, int async_errors);
 int tc_set_graphs(tc_ctx *ctx, int enable);
 
 /* tc_tune -- index-geometry knobs (tests / tuning).  Results never depend on them; only speed does.
- *  TC_TUNE_VBUCKET_ARCS  target arcs per vertex bucket (default 1024; the bucket count is a power of two
+ *  TC_TUNE_VBUCKET_ARCS  target arcs per vertex bucket (default 2048; the bucket count is a power of two
  *                        <= 4096 chosen from 2w / target)
  *  TC_TUNE_VBUCKET_CAP   vertex buckets with more arcs than this (1..4096, default 4096) leave the common
  *                        shared-memory hash path for the large-bucket kernel (radix sort on the vertex hash)

@@ -34,6 +34,7 @@ struct tc_ctx {
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
+    uint32_t ptag = 0;  // edge-pair table tag of the last push
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -105,6 +106,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     }
     ix.wcap = cap;
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+    CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)cap), ctx->stream));  // tag 0: free
+    ctx->ptag = 0;
     return TC_OK;
 }
 
@@ -293,6 +296,11 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.seed = ctx->seed;
     a.S_slot = slot;
     a.g = make_geometry((uint32_t)w, ctx->tune);
+    if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
+        CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
+        ctx->ptag = 1;
+    }
+    a.ptag = ctx->ptag;
     // The batch's whole device sequence (counter resets + kernels) can be captured as one CUDA graph and the
     // previous graph executable updated in place.
     const bool graph = ctx->use_graph != 0;

@@ -12,8 +12,8 @@
 //             D_b distinct vertices, 16 B slots {x, deg_W(x), segment start, 0}, at offset 4 * (the bucket's
 //             first arc slot) -- slices never overlap and need no prefix sum; vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
-//   edge-pair table: ceil(w / 2) groups of four 8-byte slots {k, fp} (one 32-byte sector per group, load
-//             <= 1/2), linear probing group by group; Step 3's (src,dst)-sorted "edges" array with its
+//   edge-pair table: ceil(w / 2) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
+//             <= 1/2), linear probing group by group, filled while the batch is staged; Step 3's (src,dst)-sorted "edges" array with its
 //             multisearch becomes one sector read (a fingerprint hit is verified against E[k]).
 #pragma once
 #include <cstdint>
@@ -86,9 +86,11 @@ __host__ __device__ __forceinline__ uint64_t pair_key(uint32_t lo, uint32_t hi) 
 }
 
 __host__ __device__ __forceinline__ uint32_t vbucket_of(uint32_t h, uint32_t bv) { return bv ? h >> (32 - bv) : 0u; }
-// slot position word (bits 20..51) and fingerprint (bits 0..31) of a pair hash
+// slot position word (bits 20..51) and 24-bit fingerprint (bits 0..23) of a pair hash; a slot is
+// {k, tag << 24 | fingerprint} and is live only when its tag is the batch's (1..254), so the table is
+// cleared once per 254 batches, not per batch
 __host__ __device__ __forceinline__ uint32_t pslot_word(uint64_t h) { return (uint32_t)(h >> 20); }
-__host__ __device__ __forceinline__ uint32_t pfinger(uint64_t h) { return (uint32_t)h; }
+__host__ __device__ __forceinline__ uint32_t pfinger(uint64_t h) { return (uint32_t)h & 0xFFFFFFu; }
 __host__ __device__ __forceinline__ uint32_t pgroup_start(uint64_t h, uint32_t groups) {
     return (uint32_t)(((uint64_t)pslot_word(h) * groups) >> 32);
 }
@@ -98,8 +100,9 @@ struct Lookup {
     const VSlot *vt;
     const uint2 *vslice;   // [BV] {offset, size}
     uint32_t bv;
-    const uint2 *pt;       // pair slots {k, fp}, groups of 4
+    const uint2 *pt;       // pair slots {k, tag << 24 | fp}, groups of 4
     uint32_t G;            // pair-table groups
+    uint32_t ptag;         // this batch's slot tag
 };
 
 __host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) { return (w + 1) / 2; }
@@ -132,11 +135,11 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
     const uint32_t ng = active ? L.G : 0u;
     P.lo = lo;
     P.hi = hi;
-    P.fp = pfinger(h);
+    P.fp = (L.ptag << 24) | pfinger(h);
     P.ng = ng;
     P.sl = L.pt;  // 32-byte aligned
     P.g = ng ? pgroup_start(h, ng) : 0u;
-    P.q0 = P.q1 = make_uint4(kEmptyV, 0u, kEmptyV, 0u);
+    P.q0 = P.q1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
     if (ng) {
         const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * P.g);
         P.q0 = __ldg(q);
@@ -149,7 +152,7 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
     const uint32_t ks[4] = {q0.x, q0.z, q1.x, q1.z}, fs[4] = {q0.y, q0.w, q1.y, q1.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        if (ks[i] == kEmptyV) return 0;
+        if ((fs[i] >> 24) != L.ptag) return 0;  // free slot (stale tag)
         if (fs[i] == P.fp) {
             const uint2 e = __ldg(L.E + ks[i]);
             if (e.x == P.lo && e.y == P.hi) {

@@ -3,8 +3,10 @@
 // Pipeline for one batch W.  Every index structure is PARTITIONED first and then built
 // bucket by bucket in shared memory, so the global tables are written whole, coalesced, and stay small
 // enough to live in L2 while the estimator pass probes them:
-//   k_count      a1      : load W (coalesced), validate, per-tile histograms of vertex buckets (top bv bits of
-//                          hash_vertex, 2 arcs per edge) and pair buckets (top bp bits of hash_pair64)
+//   k_pairs      a3      : (second stream, concurrently with the partition) insert every edge of the raw batch
+//                          into the edge-pair table (64-bit CAS; a repeat is TC_EDUP)
+//   k_count      a1      : load W (coalesced), validate, normalise into E, stable in-tile ranks of the arcs
+//                          by vertex bucket (top bv bits of hash_vertex) and per-tile bucket counts
 //   k_scan_rows / k_scan_tot : per-(bucket, tile) offsets inside the bucket and bucket sizes, then bucket
 //                          starts (exclusive scans)
 //   k_scatter    a1      : normalise, write E; scatter the arcs (vertex, k<<1|side) to their vertex bucket,
@@ -100,8 +102,51 @@ struct PartArgs {
     uint32_t *cntV;    // [nV * tiles]
     uint16_t *arank;   // [2 w] in-tile ranks
     uint32_t *vstart;  // bucket sizes (k_scan_rows) -> exclusive prefixes (k_scan_tot)
+    uint2 *pt;         // edge-pair table (G groups of 4 slots)
+    uint32_t G, ptag;
     uint32_t *ctr;
 };
+
+// a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
+// with room from its home group on, by 64-bit CAS, so the live slots of a group form a prefix.  Meeting the
+// same pair (confirmed against the raw batch, which is stable while E is being written) returns true.
+__device__ __forceinline__ bool pt_insert(const PartArgs &a, uint2 n, uint32_t k) {
+    const uint64_t h = hash_pair64(pair_key(n.x, n.y));
+    const uint32_t tf = (a.ptag << 24) | pfinger(h);
+    const unsigned long long mine = (unsigned long long)k | ((unsigned long long)tf << 32);
+    unsigned long long *t64 = reinterpret_cast<unsigned long long *>(a.pt);
+    uint32_t g = pgroup_start(h, a.G);
+    while (true) {
+        const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
+        const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
+        const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+            unsigned long long cur = cur4[i];
+            if ((uint32_t)(cur >> 56) != a.ptag) {
+                const unsigned long long old = atomicCAS(t64 + 4ull * g + i, cur, mine);
+                if (old == cur) return false;
+                cur = old;  // taken meanwhile (by this batch)
+            }
+            if ((uint32_t)(cur >> 32) == tf) {
+                const uint2 o = norm_edge(__ldg(a.in + (uint32_t)cur));
+                if (o.x == n.x && o.y == n.y) return true;
+            }
+        }
+        g = (g + 1 == a.G) ? 0u : g + 1;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pairs(PartArgs a) {
+    if (a.ctr[kCtrErr] & (kErrStage | kErrDup)) return;  // sticky error of an earlier async batch
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    bool dup = false;
+    if (k < a.g.w) {
+        const uint2 e = __ldg(a.in + k);
+        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) dup = pt_insert(a, norm_edge(e), k);  // k_count reports the rest
+    }
+    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+}
 
 // Tile ranking: validate and normalise W, write E, and rank every arc (by vertex bucket) and every edge (by
 // pair bucket) inside its tile, stably in arrival order.  Arc a of the tile (a = 2 e + side) is owned by
@@ -129,9 +174,9 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
         const uint32_t i = warp * kEdgesPerWarp + j * 32u + lane;
         if (i < ne) {
             const uint2 e = __ldg(a.in + e0 + i);
+            a.E[e0 + i] = norm_edge(e);
             if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
             else if (e.x == e.y) bad |= kErrLoop;
-            a.E[e0 + i] = norm_edge(e);
         }
     }
     bad = __reduce_or_sync(kFull, bad);
@@ -270,61 +315,6 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
 
 // ------------------------------------------------------------------------------------------------
 // a3: pair-table slices
-
-// The edge-pair table is built directly from the raw batch on the second stream (concurrently with the
-// vertex partition): ceil(w/2) groups of four 8-byte slots {k, fp}, cleared to all-ones by a memset; an
-// edge takes the first free slot of the first group with room from its home group on (64-bit CAS), so the
-// filled slots of a group form a prefix.  Meeting the same pair (checked against the raw batch) is TC_EDUP;
-// invalid edges are skipped here (k_count reports them).
-__device__ __forceinline__ unsigned long long pslot_pack(uint32_t k, uint32_t fp) {
-    return (unsigned long long)k | ((unsigned long long)fp << 32);
-}
-constexpr unsigned long long kEmptyPSlot = 0xFFFFFFFFFFFFFFFFull;
-
-__global__ void __launch_bounds__(256) k_pairs(const uint2 *__restrict__ in, uint32_t w, uint2 *pt, uint32_t G,
-                                               uint32_t *ctr) {
-    if (ctr[kCtrErr] & (kErrStage | kErrDup)) return;  // sticky error of an earlier async batch
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    bool dup = false;
-    if (k < w) {
-        const uint2 e = __ldg(in + k);
-        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {
-            const uint2 n = norm_edge(e);
-            const uint64_t h = hash_pair64(pair_key(n.x, n.y));
-            const uint32_t fp = pfinger(h);
-            const unsigned long long mine = pslot_pack(k, fp);
-            unsigned long long *t64 = reinterpret_cast<unsigned long long *>(pt);
-            uint32_t g = pgroup_start(h, G);
-            bool placed = false;
-            while (!placed && !dup) {
-                const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
-                const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
-                const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
-#pragma unroll
-                for (uint32_t i = 0; i < 4; ++i) {
-                    unsigned long long cur = cur4[i];
-                    if (cur == kEmptyPSlot) {
-                        cur = atomicCAS(t64 + 4ull * g + i, kEmptyPSlot, mine);
-                        if (cur == kEmptyPSlot) {
-                            placed = true;
-                            break;
-                        }
-                    }
-                    if ((uint32_t)(cur >> 32) == fp) {
-                        const uint2 o = norm_edge(__ldg(in + (uint32_t)cur));
-                        if (o.x == n.x && o.y == n.y) {
-                            dup = true;
-                            break;
-                        }
-                    }
-                }
-                g = (g + 1 == G) ? 0u : g + 1;
-            }
-        }
-    }
-    dup = __any_sync(kFull, dup);
-    if (dup && (threadIdx.x & 31u) == 0) atomicOr(&ctr[kCtrErr], kErrDup);
-}
 
 // ------------------------------------------------------------------------------------------------
 // a2: vertex buckets
@@ -1276,7 +1266,7 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.arank, ix.vstart, ix.ctr};
+    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
@@ -1291,9 +1281,7 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    const uint32_t G = pair_groups(a.g.w);
-    cudaMemsetAsync(ix.pt, 0xFF, 32ull * G, s);
-    k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(a.in, a.g.w, ix.pt, G, ix.ctr);
+    k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
     return 1;
 }
 
@@ -1315,7 +1303,7 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s)
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w)}, ix.einfo, ix.segS, ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), a.ptag}, ix.einfo, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
     k_update<<<grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves), 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats);
     return 1;

@@ -54,11 +54,12 @@ struct BatchArgs {
     uint64_t first;   // global id of local estimator 0
     uint64_t seed;
     int S_slot;
+    uint32_t ptag;    // edge-pair table tag of this push (1..254)
     Geometry g;
 };
 
 struct Tuning {
-    uint32_t vbucket_arcs = 1024;  // target arcs per vertex bucket
+    uint32_t vbucket_arcs = 2048;  // target arcs per vertex bucket
     uint32_t vcap = 4096;
     uint32_t sortcap = kVChunk;
 };
