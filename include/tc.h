@@ -122,10 +122,11 @@ int tc_set_async(tc_ctx *ctx, int async_errors);
 int tc_set_graphs(tc_ctx *ctx, int enable);
 
 /* tc_tune -- index-geometry knobs (tests / tuning).  Results never depend on them; only speed does.
- *  TC_TUNE_VBUCKET_ARCS  target arcs per vertex bucket (default 2048; the bucket count is a power of two
+ *  TC_TUNE_VBUCKET_ARCS  target arcs per vertex bucket (default 1024; the bucket count is a power of two
  *                        <= 4096 chosen from 2w / target)
- *  TC_TUNE_VBUCKET_CAP   vertex buckets with more arcs than this (1..4096, default 4096) leave the common
- *                        shared-memory hash path for the large-bucket kernel (radix sort on the vertex hash)
+ *  TC_TUNE_VBUCKET_CAP   vertex buckets with more arcs than this (1..2048, default 2048) leave the common
+ *                        shared-memory hash path for the large-bucket kernel (hub peeling, then the hash
+ *                        path for up to 4095 remaining arcs, else a radix sort on the vertex hash)
  *  TC_TUNE_VBUCKET_SORT_CAP  large-bucket kernel: buckets with more arcs than this (1..6144, default 6144)
  *                        are sorted in chunks through global memory instead of in shared memory
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */

@@ -403,7 +403,7 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
             ctx->tune.vbucket_arcs = (uint32_t)value;
             return TC_OK;
         case TC_TUNE_VBUCKET_CAP:
-            if (value < 1 || value > 4096) return TC_EINVAL;
+            if (value < 1 || value > 2048) return TC_EINVAL;
             ctx->tune.vcap = (uint32_t)value;
             return TC_OK;
         case TC_TUNE_VBUCKET_SORT_CAP:

@@ -13,7 +13,8 @@
 //             first arc slot) -- slices never overlap and need no prefix sum; vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
 //   edge-pair table: ceil(w / 2) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
-//             <= 1/2), linear probing group by group, filled while the batch is staged; Step 3's (src,dst)-sorted "edges" array with its
+//             <= 1/2); a pair probes its home group A, then an independent group B (both read together),
+//             then A+1, A+2, ...; Step 3's (src,dst)-sorted "edges" array with its
 //             multisearch becomes one sector read (a fingerprint hit is verified against E[k]).
 #pragma once
 #include <cstdint>
@@ -34,7 +35,10 @@ constexpr uint32_t kErrOvf = 8u;
 constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 
 // partitioning
-constexpr uint32_t kTileEdges = 2048;     // edges per count/scatter tile
+#ifndef TC_TILE_EDGES
+#define TC_TILE_EDGES 4096
+#endif
+constexpr uint32_t kTileEdges = TC_TILE_EDGES;  // edges per count/scatter tile
 constexpr uint32_t kTileThreads = 512;
 constexpr uint32_t kMaxBucketBits = 12;   // at most 4096 vertex buckets
 constexpr uint32_t kVBucketThreads = 256; // vertex-bucket CTA
@@ -94,6 +98,18 @@ __host__ __device__ __forceinline__ uint32_t pfinger(uint64_t h) { return (uint3
 __host__ __device__ __forceinline__ uint32_t pgroup_start(uint64_t h, uint32_t groups) {
     return (uint32_t)(((uint64_t)pslot_word(h) * groups) >> 32);
 }
+// Probe sequence of a pair over the G groups: its home group A, a second independent group B, then
+// A+1, A+2, ... (a key sits in the first group of its sequence that had room when it was inserted).
+__host__ __device__ __forceinline__ uint32_t pgroup_second(uint64_t h, uint32_t groups, uint32_t A) {
+    const uint32_t B = (uint32_t)(((uint64_t)hash_vertex((uint32_t)(h >> 32) ^ 0x9E3779B9u) * groups) >> 32);
+    return (B != A || groups == 1) ? B : (A + 1 == groups ? 0u : A + 1);
+}
+__host__ __device__ __forceinline__ uint32_t pgroup_at(uint32_t A, uint32_t B, uint32_t i, uint32_t groups) {
+    if (i == 0) return A;
+    if (i == 1) return B;
+    const uint64_t g = (uint64_t)A + i - 1;
+    return (uint32_t)(g % groups);
+}
 
 struct Lookup {
     const uint2 *E;
@@ -125,9 +141,9 @@ static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uin
 // it and walks on group by group.  Inside a group the filled slots form a prefix, so the first empty slot
 // ends the search.  Result: batch position of {lo, hi} (lo < hi), or -1.
 struct PairProbe {
-    uint32_t lo, hi, fp, g, ng;
+    uint32_t lo, hi, fp, A, B, ng;
     const uint2 *sl;
-    uint4 q0, q1;
+    uint4 a0, a1, b0, b1;  // groups A and B, read together
 };
 
 __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t hi, bool active, PairProbe &P) {
@@ -138,12 +154,16 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
     P.fp = (L.ptag << 24) | pfinger(h);
     P.ng = ng;
     P.sl = L.pt;  // 32-byte aligned
-    P.g = ng ? pgroup_start(h, ng) : 0u;
-    P.q0 = P.q1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
+    P.A = ng ? pgroup_start(h, ng) : 0u;
+    P.B = ng ? pgroup_second(h, ng, P.A) : 0u;
+    P.a0 = P.a1 = P.b0 = P.b1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
     if (ng) {
-        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * P.g);
-        P.q0 = __ldg(q);
-        P.q1 = __ldg(q + 1);
+        const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
+        const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
+        P.a0 = __ldg(qa);
+        P.a1 = __ldg(qa + 1);
+        P.b0 = __ldg(qb);
+        P.b1 = __ldg(qb + 1);
     }
 }
 
@@ -165,10 +185,8 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
 }
 
 static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
-    uint32_t g = P.g;
-    while (true) {
-        g = (g + 1 == P.ng) ? 0u : g + 1;
-        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * g);
+    for (uint32_t i = 2;; ++i) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * pgroup_at(P.A, P.B, i, P.ng));
         uint32_t k;
         const int r = pt_group(L, P, __ldg(q), __ldg(q + 1), &k);
         if (r == 0) return -1;
@@ -179,7 +197,8 @@ static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
 __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &P) {
     if (P.ng == 0) return -1;
     uint32_t k;
-    const int r = pt_group(L, P, P.q0, P.q1, &k);
+    int r = pt_group(L, P, P.a0, P.a1, &k);
+    if (r == 2) r = pt_group(L, P, P.b0, P.b1, &k);
     if (r == 0) return -1;
     if (r == 1) return (int64_t)k;
     return pt_walk(L, P);

@@ -108,15 +108,17 @@ struct PartArgs {
 };
 
 // a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
-// with room from its home group on, by 64-bit CAS, so the live slots of a group form a prefix.  Meeting the
+// with room along its probe sequence (A, B, A+1, ...), by 64-bit CAS, so the live slots of a group form a
+// prefix.  Meeting the
 // same pair (confirmed against the raw batch, which is stable while E is being written) returns true.
 __device__ __forceinline__ bool pt_insert(const PartArgs &a, uint2 n, uint32_t k) {
     const uint64_t h = hash_pair64(pair_key(n.x, n.y));
     const uint32_t tf = (a.ptag << 24) | pfinger(h);
     const unsigned long long mine = (unsigned long long)k | ((unsigned long long)tf << 32);
     unsigned long long *t64 = reinterpret_cast<unsigned long long *>(a.pt);
-    uint32_t g = pgroup_start(h, a.G);
-    while (true) {
+    const uint32_t A = pgroup_start(h, a.G), B = pgroup_second(h, a.G, A);
+    for (uint32_t step = 0;; ++step) {
+        const uint32_t g = pgroup_at(A, B, step, a.G);
         const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
         const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
         const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
@@ -133,7 +135,6 @@ __device__ __forceinline__ bool pt_insert(const PartArgs &a, uint2 n, uint32_t k
                 if (o.x == n.x && o.y == n.y) return true;
             }
         }
-        g = (g + 1 == a.G) ? 0u : g + 1;
     }
 }
 
@@ -694,15 +695,22 @@ __global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
 // three radix passes on the vertex hash -- gives every arc its rank inside its vertex.
 
 constexpr uint32_t kHThreads = 256, kHWarps = kHThreads / 32;
-constexpr uint32_t kHCap = 4096;           // arcs
-constexpr uint32_t kHTable = 2 * kHCap;    // hash slots (power of two >= 2 n)
-constexpr uint32_t kHSweep = 2048;         // local ids ranked per sweep
-// shared memory: R1 = {hkey u32[kHTable], lid u16[kHTable]} while hashing; then {whist u16[8][kHSweep],
-// segst u32[kHCap + 1]}; the slice table (u32, <= 2 kHCap slots) reuses whist.  vkey u32[kHCap] apart.
-constexpr uint32_t kHR1 = kHTable * 6 + 64;
-constexpr uint32_t kHSmemBytes = kHR1 + kHCap * 4;
-static_assert(kHWarps * kHSweep * 2 + (kHCap + 1) * 4 <= kHR1, "phase-3 arrays must fit R1");
-static_assert(2 * kHCap * 4 <= kHWarps * kHSweep * 2 + 4, "the slice table must fit over whist");
+constexpr uint32_t kHCap = 4096;  // arcs: the largest bucket (or rest after a hub) the hash path takes
+
+// Shared-memory layout of the hash path for buckets of at most CAP arcs: R1 = {hkey u32[2 CAP], lid
+// u16[2 CAP]} while hashing; then {whist u16[8][SW], segst u32[CAP + 1]}; the slice table (u32,
+// <= 2 CAP slots) reuses whist; vkey u32[CAP] apart.
+template <uint32_t CAP>
+struct HL {
+    static constexpr uint32_t T = 2 * CAP;
+    static constexpr uint32_t SW = CAP < 2048 ? CAP : 2048;
+    static constexpr uint32_t WH = kHWarps * SW * 2;
+    static constexpr uint32_t TBL = 4 * 2 * CAP;
+    static constexpr uint32_t SEGOFF = WH > TBL ? WH : TBL;
+    static constexpr uint32_t R1A = T * 6, R1B = SEGOFF + (CAP + 1) * 4;
+    static constexpr uint32_t R1 = (R1A > R1B ? R1A : R1B) + 64;
+    static constexpr uint32_t BYTES = R1 + CAP * 4;
+};
 
 // Arcs of a bucket as the hash path reads them: straight from the bucketed arcs, or (after a hub vertex
 // was peeled off) from a shared-memory list of the remaining arcs.
@@ -717,35 +725,44 @@ struct ArcSrc {
         }
         return make_uint2(sv[i], sval[i]);
     }
-    __device__ __forceinline__ uint32_t nb(uint32_t i) const { return g ? __ldcs(g + i).z : snb[i]; }
+    __device__ __forceinline__ uint3 vvn(uint32_t i) const {
+        if (g) {
+            const uint4 x = g[i];
+            return make_uint3(x.x, x.y, x.z);
+        }
+        return make_uint3(sv[i], sval[i], snb[i]);
+    }
 };
 
 // Hash-path grouping of n arcs (src) of bucket b whose segments start at slot base + off0; `hub` (if
 // hubn > 0) is an extra vertex whose segment [base, base + hubn) was already written.
-template <int R>
+template <int R, uint32_t CAP>
 __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint32_t base, const ArcSrc &src, uint32_t n,
                                              uint32_t off0, uint32_t hub, uint32_t hubn, unsigned char *sm,
                                              uint32_t *ws, uint32_t *sD) {
+    using L = HL<CAP>;
+    static_assert((uint32_t)R * kHThreads <= CAP, "items per thread exceed the layout");
     uint32_t *hkey = reinterpret_cast<uint32_t *>(sm);
-    uint16_t *lid = reinterpret_cast<uint16_t *>(sm + kHTable * 4);
+    uint16_t *lid = reinterpret_cast<uint16_t *>(sm + L::T * 4);
     uint16_t *whist = reinterpret_cast<uint16_t *>(sm);
-    uint32_t *segst = reinterpret_cast<uint32_t *>(sm + kHWarps * kHSweep * 2);
+    uint32_t *segst = reinterpret_cast<uint32_t *>(sm + L::SEGOFF);
     uint32_t *table = reinterpret_cast<uint32_t *>(sm);
-    uint32_t *vkey = reinterpret_cast<uint32_t *>(sm + kHR1);
+    uint32_t *vkey = reinterpret_cast<uint32_t *>(sm + L::R1);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
     const uint32_t Tb = pow2_ceil(2 * max(n, 1u));
     for (uint32_t s = threadIdx.x; s < Tb; s += kHThreads) hkey[s] = kEmptyV;
     if (threadIdx.x == 0) *sD = 0;
     __syncthreads();
     // phase 1: local ids (claim order) through the shared hash table; warp w owns items [w 32 R, (w+1) 32 R)
-    uint32_t val[R], pk[R];
+    uint32_t val[R], pk[R], nbv[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const uint32_t i = warp * 32u * R + j * 32u + lane;
         pk[j] = 0xFFFFFFFFu;
         if (i < n) {
-            const uint2 x = src.vv(i);
+            const uint3 x = src.vvn(i);
             val[j] = x.y;
+            nbv[j] = x.z;
             uint32_t s = hash_vertex(x.x) & (Tb - 1);
             while (true) {
                 uint32_t k = hkey[s];
@@ -771,8 +788,8 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         if (pk[j] != 0xFFFFFFFFu) pk[j] = (uint32_t)lid[pk[j]] << 16;  // local id << 16 | rank (below)
     __syncthreads();  // R1 becomes whist + segst
     // phase 2: stable rank of each arc inside its vertex, local ids in sweeps of kHSweep
-    for (uint32_t l0 = 0; l0 < D; l0 += kHSweep) {
-        const uint32_t nd = min(kHSweep, D - l0);
+    for (uint32_t l0 = 0; l0 < D; l0 += L::SW) {
+        const uint32_t nd = min(L::SW, D - l0);
         const uint32_t bits = log2_ceil(nd);
         for (uint32_t i = threadIdx.x; i < kHWarps * nd; i += kHThreads) whist[i] = 0;
         __syncthreads();
@@ -835,8 +852,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         if (pk[j] == 0xFFFFFFFFu) continue;
         const uint32_t l = pk[j] >> 16;
         const uint32_t pos = segst[l] + (pk[j] & 0xFFFFu);
-        const uint32_t i = warp * 32u * R + j * 32u + lane;
-        a.segS[b0 + pos] = make_uint2(val[j], src.nb(i));
+        a.segS[b0 + pos] = make_uint2(val[j], nbv[j]);
         a.einfo2[val[j]] = make_uint2(b0 + pos, b0 + segst[l + 1]);
     }
     // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole; the hub (if
@@ -864,16 +880,20 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     }
 }
 
-template <typename F>
+template <uint32_t CAP, typename F>
 __device__ __forceinline__ void hash_dispatch(uint32_t n, F f) {
     if (n <= 256) f(std::integral_constant<int, 1>());
     else if (n <= 512) f(std::integral_constant<int, 2>());
     else if (n <= 1024) f(std::integral_constant<int, 4>());
-    else if (n <= 2048) f(std::integral_constant<int, 8>());
-    else f(std::integral_constant<int, 16>());
+    else if (CAP <= 2048 || n <= 2048) f(std::integral_constant<int, (CAP >= 2048 ? 8 : 4)>());
+    else f(std::integral_constant<int, (CAP >= 4096 ? 16 : 8)>());
 }
 
-__global__ void __launch_bounds__(kHThreads, 3) k_vhash(VertArgs a) {
+// Common buckets (<= vcap <= kHCapSmall arcs): 4 CTAs per SM.
+constexpr uint32_t kHCapSmall = 2048;
+constexpr uint32_t kVHashSmemBytes = HL<kHCapSmall>::BYTES;
+
+__global__ void __launch_bounds__(kHThreads, 4) k_vhash(VertArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ __align__(16) unsigned char hsm[];
     __shared__ uint32_t ws[9];
@@ -882,7 +902,9 @@ __global__ void __launch_bounds__(kHThreads, 3) k_vhash(VertArgs a) {
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
     if (n > a.vcap) return;  // k_vhub's
     const ArcSrc src{a.arcs + base, nullptr, nullptr, nullptr};
-    hash_dispatch(n, [&](auto r) { vbucket_hash<decltype(r)::value>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD); });
+    hash_dispatch<kHCapSmall>(n, [&](auto r) {
+        vbucket_hash<decltype(r)::value, kHCapSmall>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
+    });
 }
 
 // Large buckets (more than vcap arcs): almost always one hub vertex plus about a normal bucket's worth of
@@ -890,12 +912,12 @@ __global__ void __launch_bounds__(kHThreads, 3) k_vhash(VertArgs a) {
 // order: a 1-bit stable partition), the rest goes through the hash path from shared memory.  Buckets whose
 // rest is still too large are deferred to k_vbig.  Persistent CTAs over vperm[0 .. ctr[kCtrBig]).
 constexpr uint32_t kHubSample = 256;
-constexpr uint32_t kVHubSmemBytes = kHSmemBytes + 3 * kHCap * 4;
+constexpr uint32_t kVHubSmemBytes = HL<kHCap>::BYTES + 3 * kHCap * 4;
 
 __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ __align__(16) unsigned char hsm[];
-    uint32_t *rv = reinterpret_cast<uint32_t *>(hsm + kHSmemBytes);
+    uint32_t *rv = reinterpret_cast<uint32_t *>(hsm + HL<kHCap>::BYTES);
     uint32_t *rval = rv + kHCap, *rnb = rval + kHCap;
     __shared__ uint32_t ws[9];
     __shared__ uint32_t sD, s_b, s_h, s_cnt;
@@ -962,7 +984,7 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
         if (lane == 0) atomicAdd(&s_cnt, mine);
         __syncthreads();
         const uint32_t H = s_cnt;
-        if (n - H > kHCap) {  // not one hub: the radix-sort kernel takes it
+        if (n - H > kHCap - 1) {  // not one hub: the radix-sort kernel takes it (D + hub must fit 2 kHCap slots)
             if (threadIdx.x == 0) a.vdefer[atomicAdd(&a.ctr[kCtrDefer], 1u)] = b;
             __syncthreads();
             continue;
@@ -1006,7 +1028,9 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
         }
         // 4. the rest through the hash path (segments after the hub's), the hub as an extra vertex
         const ArcSrc src{nullptr, rv, rval, rnb};
-        hash_dispatch(n - H, [&](auto r) { vbucket_hash<decltype(r)::value>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD); });
+        hash_dispatch<kHCap>(n - H, [&](auto r) {
+            vbucket_hash<decltype(r)::value, kHCap>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD);
+        });
         __syncthreads();
     }
 }
@@ -1260,7 +1284,7 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
     g.w = w;
     g.tiles = (w + kTileEdges - 1) / kTileEdges;
     g.bv = std::min(kMaxBucketBits, ceil_log2((2ull * w + t.vbucket_arcs - 1) / t.vbucket_arcs));
-    g.vcap = std::min(t.vcap, kHCap);
+    g.vcap = std::min(t.vcap, kHCapSmall);
     g.sortcap = std::min(t.sortcap, kVChunk);
     return g;
 }
@@ -1291,7 +1315,7 @@ static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
 }
 
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    k_vhash<<<1u << a.g.bv, kHThreads, kHSmemBytes, s>>>(vert_args(ix, a));
+    k_vhash<<<1u << a.g.bv, kHThreads, kVHashSmemBytes, s>>>(vert_args(ix, a));
     return 1;
 }
 
@@ -1323,7 +1347,7 @@ int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *
 
 int set_kernel_attributes() {
     cudaError_t e1 = cudaFuncSetAttribute(k_vbig, cudaFuncAttributeMaxDynamicSharedMemorySize, kVSmemBytes);
-    if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kHSmemBytes);
+    if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
     cudaError_t e2 = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * 4096);
     return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;

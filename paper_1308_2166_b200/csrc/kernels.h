@@ -43,7 +43,7 @@ struct Geometry {
     uint32_t w;
     uint32_t tiles;    // ceil(w / kTileEdges)
     uint32_t bv;       // vertex bucket bits
-    uint32_t vcap;     // vertex buckets larger than this go to k_vbig (<= 4096)
+    uint32_t vcap;     // vertex buckets larger than this go to k_vhub (<= 2048)
     uint32_t sortcap;  // k_vbig: buckets larger than this take the chunked global-memory path (<= kVChunk)
 };
 
@@ -59,8 +59,8 @@ struct BatchArgs {
 };
 
 struct Tuning {
-    uint32_t vbucket_arcs = 2048;  // target arcs per vertex bucket
-    uint32_t vcap = 4096;
+    uint32_t vbucket_arcs = 1024;  // target arcs per vertex bucket
+    uint32_t vcap = 2048;
     uint32_t sortcap = kVChunk;
 };
 
@@ -71,7 +71,10 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);      // a3: edge-pair table
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);   // a2: grouping, ranks, vertex table
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a2: the buckets > vcap
-constexpr uint32_t kBigCTAs = 32;
+#ifndef TC_BIG_CTAS
+#define TC_BIG_CTAS 64
+#endif
+constexpr uint32_t kBigCTAs = TC_BIG_CTAS;
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s);
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
