@@ -68,7 +68,7 @@ static int fail_cuda(tc_ctx *c) {
     } while (0)
 
 static void free_index(IndexBufs &ix) {
-    void *bufs[] = {ix.E, ix.arcs, ix.scratch, ix.segS, ix.einfo, ix.vt, ix.vslice, ix.vperm, ix.vdefer, ix.pt,
+    void *bufs[] = {ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
                     ix.cntV, ix.arank, ix.vstart, ix.ctr, ix.stage};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
@@ -88,17 +88,16 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     ix.tiles_cap = (cap + kTileEdges - 1) / kTileEdges;
-    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.scratch, 16 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.segS, 16 * cap) == cudaSuccess && cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess &&
-              // vertex-table slices: bucket b owns [4 start_b, 4 start_b + 4 n_b) (next_pow2(2 D_b) < 4 n_b): 8 w slots
-              cudaMalloc(&ix.vt, 16 * 8 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess &&
-              cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.vdefer, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
-              cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
-              cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
-              cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
+    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.segS, 16 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
+              cudaMalloc(&ix.vt, 16 * 4 * cap) == cudaSuccess &&  // slices at 2 * (bucket start), <= 2 n_b slots
+              cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess;
+    ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.scratch, 16 * cap) == cudaSuccess &&
+         cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.vdefer, 4 * kMaxBuckets) == cudaSuccess &&
+         cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
+         cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
+         cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);

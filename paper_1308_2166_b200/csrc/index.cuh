@@ -8,9 +8,10 @@
 //             Vertices are grouped by BUCKET (the top bv bits of hash_vertex), each bucket owns the slot
 //             range of its arcs; inside a bucket vertices appear in hash order.
 //   einfo[k]  uint4  {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
-//   vertex table: one open-addressing slice per vertex bucket, sized next_pow2(2 D_b) for the bucket's
-//             D_b distinct vertices, 16 B slots {x, deg_W(x), segment start, 0}, at offset 4 * (the bucket's
-//             first arc slot) -- slices never overlap and need no prefix sum; vslice[b] = {offset, size}.
+//   vertex table: one open-addressing slice per vertex bucket, min(next_pow2(2 D_b), 2 n_b) slots for the
+//             bucket's D_b distinct vertices (n_b arcs), 16 B slots {x, deg_W(x), segment start, 0}, at offset
+//             2 * (the bucket's first arc slot) -- slices never overlap and need no prefix sum;
+//             vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
 //   edge-pair table: ceil(w / 2) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
 //             <= 1/2); a pair probes its home group A, then an independent group B (both read together),
@@ -111,6 +112,15 @@ __host__ __device__ __forceinline__ uint32_t pgroup_at(uint32_t A, uint32_t B, u
     return (uint32_t)(g % groups);
 }
 
+// Vertex-table slices: bucket b (n_b arcs, D_b distinct vertices) owns the S_b = min(next_pow2(2 D_b), 2 n_b)
+// slots at offset 2 * (its first arc slot) (load <= 1/2, slices disjoint).  A vertex with hash h probes the
+// slot pairs from vslot_start(h, S) on, wrapping at S (S is even).
+__host__ __device__ __forceinline__ uint32_t vslot_start(uint32_t h, uint32_t S) {
+    // the bucket is the top bits of h: remix so that the low bits choose the slot
+    return (uint32_t)(((uint64_t)(h * 0x9E3779B9u) * S) >> 32) & ~1u;
+}
+__host__ __device__ __forceinline__ uint32_t vslot_next(uint32_t s, uint32_t S) { return s + 2 >= S ? 0u : s + 2; }
+
 struct Lookup {
     const uint2 *E;
     const VSlot *vt;
@@ -125,9 +135,8 @@ __host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) { return (w
 
 // Continue a vertex probe at slot pair b of slice sl (after the first pair missed without an empty slot).
 static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uint32_t b, uint32_t v) {
-    const uint32_t mask = sl.y - 1u;
     while (true) {
-        b = (b + 2) & mask;
+        b = vslot_next(b, sl.y);
         const uint4 *p = reinterpret_cast<const uint4 *>(L.vt + sl.x + b);
         const uint4 s0 = __ldg(p), s1 = __ldg(p + 1);
         if (s0.x == v) return make_uint2(s0.y, s0.z);
@@ -220,7 +229,7 @@ struct VertProbe {
 __device__ __forceinline__ void vt_issue(const Lookup &L, uint32_t v, VertProbe &P) {
     const uint32_t h = hash_vertex(v);
     P.sl = __ldg(L.vslice + vbucket_of(h, L.bv));
-    P.b = h & (P.sl.y - 1u) & ~1u;
+    P.b = vslot_start(h, P.sl.y);
     const uint4 *p = reinterpret_cast<const uint4 *>(L.vt + (P.sl.y ? P.sl.x + P.b : 0u));
     P.s0 = __ldg(p);
     P.s1 = __ldg(p + 1);

@@ -346,7 +346,8 @@ static_assert(kVChunk * 8 >= 2 * 4 * kVChunk, "the u16 slice table (<= 4 D slots
 __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) { return x <= 1 ? 1u : 1u << (32 - __clz(x - 1)); }
 __device__ __forceinline__ uint32_t log2_ceil(uint32_t x) { return x <= 1 ? 0u : 32 - __clz(x - 1); }
 
-__device__ __forceinline__ uint32_t slice_size(uint32_t D) { return D ? pow2_ceil(2 * D) : 0u; }
+// vertex-table slice of D vertices in a bucket of n arcs (D <= n): load <= 1/2, at most 2 n slots
+__device__ __forceinline__ uint32_t slice_size(uint32_t D, uint32_t n) { return D ? min(pow2_ceil(2 * D), 2 * n) : 0u; }
 
 // One LSD pass over the items held in registers (warp-blocked layout, R rounds): stable rank by the digit
 // (key >> shift) & ((1 << bits) - 1); returns the destination index of every item in `dst`.
@@ -417,11 +418,11 @@ __device__ __forceinline__ void rank_pass(const uint32_t (&key)[kVItems], uint32
 
 // Table insert of run r (vertex hash h) into a power-of-two table of u16 run indices, 2-slot aligned
 // linear probing (the probe order vt_find assumes).
-__device__ __forceinline__ void stable_insert16(uint16_t *table, uint32_t mask, uint32_t h, uint32_t r) {
-    uint32_t s = h & mask & ~1u;
+__device__ __forceinline__ void stable_insert16(uint16_t *table, uint32_t S, uint32_t h, uint32_t r) {
+    uint32_t s = vslot_start(h, S);
     while (true) {
         if (table[s] == 0xFFFFu && atomicCAS(&table[s], (unsigned short)0xFFFFu, (unsigned short)r) == 0xFFFFu) return;
-        s = (s + 1) & mask;
+        if (++s == S) s = 0;
     }
 }
 
@@ -439,8 +440,8 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
     uint32_t *aux = reinterpret_cast<uint32_t *>(vsm + kVChunk * 8);  // [kVAux]: sort histograms | run keys
     uint16_t *run_start = reinterpret_cast<uint16_t *>(vsm + kVChunk * 8 + kVAux * 4);  // [kVChunk]
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
-    // the bucket's vertex-table slice: next_pow2(2 D) <= 4 n slots at offset 4 * base (disjoint slices)
-    const uint64_t off = 4ull * base;
+    // the bucket's vertex-table slice: min(next_pow2(2 D), 2 n) slots at offset 2 * base (disjoint slices)
+    const uint64_t off = 2ull * base;
     const uint32_t keybits = 32 - a.bv;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     uint32_t D = 0;
@@ -513,15 +514,15 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         }
         // the slice, built in shared memory and written whole
         if (threadIdx.x == 0) {
-            a.vslice[b] = make_uint2((uint32_t)off, slice_size(D));
+            a.vslice[b] = make_uint2((uint32_t)off, slice_size(D, n));
             if (D) atomicAdd(&a.ctr[kCtrD], D);
         }
         __syncthreads();  // sbuf is dead: it holds the table now
-        const uint32_t S = slice_size(D);
+        const uint32_t S = slice_size(D, n);
         uint16_t *table = reinterpret_cast<uint16_t *>(sbuf);
         for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) table[s] = 0xFFFFu;
         __syncthreads();
-        for (uint32_t q = threadIdx.x; q < D; q += kVBucketThreads) stable_insert16(table, S - 1, run_key[q], q);
+        for (uint32_t q = threadIdx.x; q < D; q += kVBucketThreads) stable_insert16(table, S, run_key[q], q);
         __syncthreads();
         for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) {
             const uint32_t q = table[s];
@@ -648,10 +649,10 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         carry += tot;
     }
     if (threadIdx.x == 0) {
-        a.vslice[b] = make_uint2((uint32_t)off, slice_size(D));
+        a.vslice[b] = make_uint2((uint32_t)off, slice_size(D, n));
         if (D) atomicAdd(&a.ctr[kCtrD], D);
     }
-    const uint32_t S = slice_size(D);
+    const uint32_t S = slice_size(D, n);
     VSlot *sl = a.vt + off;
     for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads)
         reinterpret_cast<uint4 *>(sl)[s] = make_uint4(kEmptyV, 0u, 0u, 0u);
@@ -662,8 +663,9 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         const uint32_t st = gruns[q], en = q + 1 < D ? gruns[q + 1] : n;
         const uint32_t h = src[st].x;
         const u128 v = (u128)unhash_vertex(h) | ((u128)(en - st) << 32) | ((u128)(base + st) << 64);
-        uint32_t s = h & (S - 1) & ~1u;
-        while (atomicCAS(reinterpret_cast<u128 *>(sl + s), empty, v) != empty) s = (s + 1) & (S - 1);
+        uint32_t s = vslot_start(h, S);
+        while (atomicCAS(reinterpret_cast<u128 *>(sl + s), empty, v) != empty)
+            if (++s == S) s = 0;
     }
 }
 
@@ -858,8 +860,8 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole; the hub (if
     // any) is entry D
     const uint32_t Dt = D + (hubn ? 1u : 0u);
-    const uint32_t S = slice_size(Dt);
-    const uint64_t off = 4ull * base;
+    const uint32_t S = slice_size(Dt, off0 + n);
+    const uint64_t off = 2ull * base;
     if (threadIdx.x == 0) {
         a.vslice[b] = make_uint2((uint32_t)off, S);
         if (Dt) atomicAdd(&a.ctr[kCtrD], Dt);
@@ -867,8 +869,9 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     for (uint32_t s = threadIdx.x; s < S; s += kHThreads) table[s] = kEmptyV;
     __syncthreads();
     for (uint32_t l = threadIdx.x; l < Dt; l += kHThreads) {
-        uint32_t s = hash_vertex(l < D ? vkey[l] : hub) & (S - 1) & ~1u;
-        while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV) s = (s + 1) & (S - 1);
+        uint32_t s = vslot_start(hash_vertex(l < D ? vkey[l] : hub), S);
+        while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV)
+            if (++s == S) s = 0;
     }
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < S; s += kHThreads) {
@@ -1097,7 +1100,7 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
         su = __ldg(ix.L.vslice + vbucket_of(hu, ix.L.bv));
         sv = __ldg(ix.L.vslice + vbucket_of(hv, ix.L.bv));
     }
-    const uint32_t bu = hu & (su.y - 1u) & ~1u, bw = hv & (sv.y - 1u) & ~1u;
+    const uint32_t bu = vslot_start(hu, su.y), bw = vslot_start(hv, sv.y);
     uint4 u0 = make_uint4(kEmptyV, 0u, 0u, 0u), u1 = u0, v0 = u0, v1 = u0;
     if (su.y) {
         const uint4 *p = reinterpret_cast<const uint4 *>(ix.L.vt + su.x + bu);

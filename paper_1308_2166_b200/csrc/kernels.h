@@ -17,7 +17,7 @@ struct IndexBufs {
     uint2 *scratch = nullptr;      // [2 wcap] sort scratch of oversized vertex buckets
     uint2 *segS = nullptr;         // [2 wcap] arcs {k<<1|side, neighbour} grouped by vertex
     uint4 *einfo = nullptr;        // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
-    VSlot *vt = nullptr;           // [8 wcap] vertex-table slices (bucket b at 4 * start_b)
+    VSlot *vt = nullptr;           // [4 wcap] vertex-table slices (bucket b at 2 * start_b)
     uint2 *vslice = nullptr;       // [4096] {offset, size}
     uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
     uint32_t *vdefer = nullptr;    // [4096] large buckets k_vhub hands to k_vbig
