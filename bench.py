@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tune", action="append", default=[], help="index-geometry knob key=value (tc_tune)")
+    ap.add_argument("--no-graphs", action="store_true", help="plain stream launches instead of one CUDA graph per push")
     return ap.parse_args()
 
 
@@ -157,15 +158,15 @@ def committed_traffic(config):
 def algorithmic_bytes(phase, w, R, D, fresh, r2old):
     """Algorithmic bytes per launch: what each phase must move at minimum.
 
-    update    : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 36 B per fresh one
-                (write cf, r1, p1, r2, p2), +16 B per retained estimator whose f2 is replaced (r2, p2);
-                index probes are L2 traffic at C2 and not counted.
+    update    : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 28 B per fresh one
+                (write cf 4, r1 8, p1 4, r2 8, p2 4), +12 B per retained estimator whose f2 is replaced
+                (r2, p2); the index probes are not counted (the byte model of SURVEY §8d).
     partition : read the batch once 8 B/edge; write E 8, the two bucketed arcs 16, the bucketed edge 16 B/edge.
     pairs     : read the bucketed edge 16 B, write its 2 table slots 16 B.
     vertices  : read the two bucketed arcs 16 B, write segS 8 + einfo 16 B per edge; 32 B (2 slots) per vertex.
     """
     if phase == "update":
-        return 24 * (R - fresh) + 36 * fresh + 16 * r2old
+        return 24 * (R - fresh) + 28 * fresh + 12 * r2old
     if phase == "partition":
         return 48 * w
     if phase == "pairs":
@@ -242,65 +243,74 @@ def run_b200(args):
     # ---- timed: K steps = K consecutive batches of the stream (a new pass over the stream starts from a
     # reset estimator set, untimed); CUDA events on the library's stream around each step; L2 flushed
     # (read of a 256 MiB buffer) before every step, outside the events ----
-    tc.reset()
-    tc.profile(True)
     ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
-    evs = []
-    launches = 0
-    edges_done = 0
-    prof = {}
-    stats = {"fresh": 0, "r2_replaced_retained": 0, "vertices": 0}
 
-    def harvest():
-        for p, (pms, n) in tc.profile_read().items():
-            a = prof.setdefault(p, [0.0, 0])
-            a[0] += pms
-            a[1] += n
-        for kk, v in tc.stats().items():
-            if kk in stats:
-                stats[kk] += v
+    def timed_pass(nsteps, profile, graphs):
+        tc.set_graphs(graphs)
+        tc.reset()
+        tc.profile(profile)
+        evs, launches, edges = [], 0, 0
+        prof = {}
+        stats = {"fresh": 0, "r2_replaced_retained": 0, "vertices": 0}
 
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(dev.index) as clocks:
-        t_wall = time.perf_counter()
-        for k in range(args.steps):
-            if k and k % nb == 0:  # stream exhausted: a fresh estimator set (untimed)
-                assert tc.sync() == 0
-                harvest()
-                tc.reset()
-                tc.profile(True)
-            with torch.cuda.stream(ext):
-                flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(ext)
-            n = push(k)
-            with torch.cuda.stream(ext):
-                e1.record(ext)
-            evs.append((e0, e1))
-            launches += tc.last_launches()
-            edges_done += n
-        assert tc.sync() == 0
+        def harvest():
+            if profile:
+                for p, (pms, n) in tc.profile_read().items():
+                    acc = prof.setdefault(p, [0.0, 0])
+                    acc[0] += pms
+                    acc[1] += n
+            for kk, v in tc.stats().items():
+                if kk in stats:
+                    stats[kk] += v
+
+        barrier()
         torch.cuda.synchronize()
-        t_wall = time.perf_counter() - t_wall
-    barrier()
-    harvest()
-    ms = sum(a.elapsed_time(b) for a, b in evs)
+        with ClockSampler(dev.index) as clocks:
+            t0 = time.perf_counter()
+            for k in range(nsteps):
+                if k and k % nb == 0:  # stream exhausted: a fresh estimator set (untimed)
+                    assert tc.sync() == 0
+                    harvest()
+                    tc.reset()
+                    tc.profile(profile)
+                with torch.cuda.stream(ext):
+                    flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(ext)
+                n = push(k)
+                with torch.cuda.stream(ext):
+                    e1.record(ext)
+                evs.append((e0, e1))
+                launches += tc.last_launches()
+                edges += n
+            assert tc.sync() == 0
+            torch.cuda.synchronize()
+            wall = time.perf_counter() - t0
+        barrier()
+        harvest()
+        ms_ = sum(x.elapsed_time(y) for x, y in evs)
+        return ms_, launches, edges, prof, stats, clocks, wall
+
+    # headline: every push as one CUDA graph (--no-graphs: plain stream launches), no profiling events
+    ms, launches, edges_done, _, _, clocks, t_wall = timed_pass(args.steps, False, not args.no_graphs)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
     ms = float(t.item())
     secs = ms / 1e3
+    # per-phase times (and the dominant kernel's launch time): one more pass over the stream with CUDA events
+    # bracketing each phase (plain launches: the events are stream operations between the kernels)
+    _, _, prof_edges, prof, stats, _, _ = timed_pass(nb, True, False)
 
     # dominant kernel = k_update (the largest single kernel in the committed ncu launch list,
     # profiles/launches_r01_summary.txt); its events bracket exactly that one launch per step
     peak, peak_src = measured_peaks()
-    nsteps = args.steps
+    nsteps = nb
     alg = {
         "update": algorithmic_bytes("update", 0, count * nsteps, 0, stats["fresh"], stats["r2_replaced_retained"]),
-        "partition": algorithmic_bytes("partition", edges_done, 0, 0, 0, 0),
-        "pairs": algorithmic_bytes("pairs", edges_done, 0, 0, 0, 0),
-        "vertices": algorithmic_bytes("vertices", edges_done, 0, stats["vertices"], 0, 0),
+        "partition": algorithmic_bytes("partition", prof_edges, 0, 0, 0, 0),
+        "pairs": algorithmic_bytes("pairs", prof_edges, 0, 0, 0, 0),
+        "vertices": algorithmic_bytes("vertices", prof_edges, 0, stats["vertices"], 0, 0),
     }
     ach = {p: alg[p] / (prof[p][0] / 1e3) / 1e9 for p in alg if prof.get(p) and prof[p][0] > 0}
     roofline = {"bound": "hbm", "kernel": "k_update (fused Steps 1-3 + partial sums)",
@@ -322,9 +332,11 @@ def run_b200(args):
         "config": {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w, "stream_edges": m_total,
                    "batches_per_stream": nb, "estimators_per_gpu": count, "parallelism": f"estimator-shard x{world}",
                    "l2": "flushed before every step (256 MiB read, outside the step events)",
+                   "launch": "one CUDA graph per push" if not args.no_graphs else "plain stream launches",
+                   "phases_from": "a second pass over the stream with per-phase CUDA events (plain launches)",
                    "timing": "CUDA events on the library stream around each tc_push_batch, summed; max over ranks"},
         "estimator_updates_per_s": edges_done * r / secs,
-        "batch_estimator_updates_per_s": nsteps * r / secs,
+        "batch_estimator_updates_per_s": args.steps * r / secs,
         "gpu_launches": launches,
         "roofline": roofline,
         "wall_s_timed_region": t_wall,
@@ -335,6 +347,7 @@ def run_b200(args):
     if not args.no_e2e and world == 1:
         host = torch.from_numpy(stream.view(np.int32)).pin_memory()
         tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+        tc2.set_graphs(not args.no_graphs)
         ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
         for k in range(min(args.warmup, nb)):
             tc2.push_batch(host[k * w:(k + 1) * w])
