@@ -69,7 +69,7 @@ static int fail_cuda(tc_ctx *c) {
 
 static void free_index(IndexBufs &ix) {
     void *bufs[] = {ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
-                    ix.cntV, ix.arank, ix.vstart, ix.ctr, ix.stage};
+                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
 }
@@ -96,6 +96,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.scratch, 16 * cap) == cudaSuccess &&
          cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.vdefer, 4 * kMaxBuckets) == cudaSuccess &&
          cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
+         cudaMalloc(&ix.offV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
          cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {

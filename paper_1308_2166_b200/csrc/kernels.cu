@@ -99,7 +99,8 @@ struct PartArgs {
     Geometry g;
     uint2 *E;
     uint4 *arcs;  // {vertex, k<<1|side, neighbour, 0}
-    uint32_t *cntV;    // [nV * tiles]
+    uint32_t *cntV;    // [nV * tiles] per-(bucket, tile) arc counts
+    uint32_t *offV;    // [nV * tiles] the tile's offset inside the bucket
     uint16_t *arank;   // [2 w] in-tile ranks
     uint32_t *vstart;  // bucket sizes (k_scan_rows) -> exclusive prefixes (k_scan_tot)
     uint2 *pt;         // edge-pair table (G groups of 4 slots)
@@ -262,11 +263,13 @@ __global__ void __launch_bounds__(1024) k_scan_tot(uint32_t *vstart, uint32_t nV
 
 // One block per vertex-bucket row: cnt[b][t] -> sum_{t' < t} cnt[b][t'] (the tile's offset inside the
 // bucket); the row total (the bucket size) goes to vstart[b].
-__global__ void __launch_bounds__(256) k_scan_rows(uint32_t *cntV, uint32_t *vstart, uint32_t tiles, const uint32_t *ctr) {
+__global__ void __launch_bounds__(256) k_scan_rows(const uint32_t *cntV, uint32_t *offV, uint32_t *vstart, uint32_t tiles,
+                                                  const uint32_t *ctr) {
     if (ctr[kCtrErr] & kErrStage) return;
     __shared__ uint32_t ws[9];
     const uint32_t b = blockIdx.x;
-    uint32_t *row = cntV + (size_t)b * tiles;
+    const uint32_t *row = cntV + (size_t)b * tiles;
+    uint32_t *orow = offV + (size_t)b * tiles;
     const uint32_t per = (tiles + 255) / 256;
     const uint32_t c0 = threadIdx.x * per, c1 = min(tiles, c0 + per);
     uint32_t local = 0;
@@ -274,9 +277,8 @@ __global__ void __launch_bounds__(256) k_scan_rows(uint32_t *cntV, uint32_t *vst
     uint32_t tot;
     uint32_t run = block_exclusive_scan<256>(local, ws, &tot);
     for (uint32_t i = c0; i < c1; ++i) {
-        const uint32_t c = row[i];
-        row[i] = run;
-        run += c;
+        orow[i] = run;
+        run += row[i];
     }
     if (threadIdx.x == 0) vstart[b] = tot;
 }
@@ -286,31 +288,46 @@ __global__ void __launch_bounds__(256) k_scan_rows(uint32_t *cntV, uint32_t *vst
 __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ uint32_t dsh[];
+    __shared__ uint32_t ws[kTileThreads / 32 + 1];
     const uint32_t nV = 1u << a.g.bv;
-    uint32_t *soff = dsh;
+    uint32_t *soff = dsh, *toff = dsh + nV;                            // [nV] each
+    uint2 *sE = reinterpret_cast<uint2 *>(dsh + 2 * nV);               // [kTileEdges] the tile's edges
+    uint16_t *idx = reinterpret_cast<uint16_t *>(sE + kTileEdges);    // [2 kTileEdges] arcs in bucket order
     const uint32_t t = blockIdx.x, e0 = t * kTileEdges;
     const uint32_t ne = min(kTileEdges, a.g.w - e0);
-    for (uint32_t d = threadIdx.x; d < nV; d += kTileThreads) soff[d] = a.vstart[d] + a.cntV[d * a.g.tiles + t];
+    for (uint32_t d = threadIdx.x; d < nV; d += kTileThreads) {
+        soff[d] = a.vstart[d] + a.offV[d * a.g.tiles + t];
+        toff[d] = a.cntV[d * a.g.tiles + t];
+    }
+    for (uint32_t i = threadIdx.x; i < ne; i += kTileThreads) sE[i] = a.E[e0 + i];
     __syncthreads();
-    constexpr uint32_t kPer = 2 * kTileEdges / kTileThreads;
-    uint2 n[kPer];
-    uint32_t r[kPer];
-#pragma unroll
-    for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t ai = threadIdx.x + q * kTileThreads;
-        if (ai < 2 * ne) {
-            n[q] = a.E[e0 + (ai >> 1)];
-            r[q] = a.arank[2 * e0 + ai];
+    {  // where each bucket's run starts in the tile's bucket order
+        const uint32_t per = (nV + kTileThreads - 1) / kTileThreads;
+        const uint32_t q0 = min(nV, threadIdx.x * per), q1 = min(nV, q0 + per);
+        uint32_t sum = 0;
+        for (uint32_t q = q0; q < q1; ++q) sum += toff[q];
+        uint32_t tot;
+        uint32_t run = block_exclusive_scan<kTileThreads>(sum, ws, &tot);
+        for (uint32_t q = q0; q < q1; ++q) {
+            const uint32_t c = toff[q];
+            toff[q] = run;
+            run += c;
         }
     }
-#pragma unroll
-    for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t ai = threadIdx.x + q * kTileThreads;
-        if (ai < 2 * ne) {
-            const uint32_t v = (ai & 1u) ? n[q].y : n[q].x;
-            const uint32_t nb = (ai & 1u) ? n[q].x : n[q].y;
-            __stcs(a.arcs + soff[vbucket_of(hash_vertex(v), a.g.bv)] + r[q], make_uint4(v, 2u * e0 + ai, nb, 0u));
-        }
+    __syncthreads();
+    for (uint32_t ai = threadIdx.x; ai < 2 * ne; ai += kTileThreads) {
+        const uint2 n = sE[ai >> 1];
+        const uint32_t d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bv);
+        idx[toff[d] + a.arank[2 * e0 + ai]] = (uint16_t)ai;
+    }
+    __syncthreads();
+    // consecutive threads write consecutive positions of the tile's bucket order: a bucket's run coalesces
+    for (uint32_t pos = threadIdx.x; pos < 2 * ne; pos += kTileThreads) {
+        const uint32_t ai = idx[pos];
+        const uint2 n = sE[ai >> 1];
+        const uint32_t v = (ai & 1u) ? n.y : n.x, nb = (ai & 1u) ? n.x : n.y;
+        const uint32_t d = vbucket_of(hash_vertex(v), a.g.bv);
+        __stcs(a.arcs + soff[d] + (pos - toff[d]), make_uint4(v, 2u * e0 + ai, nb, 0u));
     }
 }
 
@@ -1293,7 +1310,7 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr};
+    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
@@ -1301,9 +1318,9 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const uint32_t nV = 1u << g.bv;
     const PartArgs p = part_args(ix, a);
     k_count<<<g.tiles, kTileThreads, 2 * kTileWarps * nV, s>>>(p);
-    k_scan_rows<<<nV, 256, 0, s>>>(ix.cntV, ix.vstart, g.tiles, ix.ctr);
+    k_scan_rows<<<nV, 256, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, ix.ctr);
     k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.vcap, ix.vperm, ix.ctr);
-    k_scatter<<<g.tiles, kTileThreads, 4 * nV, s>>>(p);
+    k_scatter<<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
     return 4;
 }
 
@@ -1353,6 +1370,8 @@ int set_kernel_attributes() {
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
     cudaError_t e2 = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * 4096);
+    if (e2 == cudaSuccess)
+        e2 = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 + 12 * kTileEdges);
     return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;
 }
 

@@ -22,7 +22,8 @@ struct IndexBufs {
     uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
     uint32_t *vdefer = nullptr;    // [4096] large buckets k_vhub hands to k_vbig
     uint2 *pt = nullptr;           // [4 ceil(wcap / 2)] pair slots {k, fp}, groups of 4
-    uint32_t *cntV = nullptr;      // [4096 * tiles] per-tile vertex-bucket counts -> scatter offsets
+    uint32_t *cntV = nullptr;      // [4096 * tiles] per-(bucket, tile) arc counts
+    uint32_t *offV = nullptr;      // [4096 * tiles] the tile's offset inside the bucket
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
     uint32_t *vstart = nullptr;    // [4097] vertex-bucket totals -> exclusive prefix
     uint32_t *ctr = nullptr;       // device counters (index.cuh kCtr*)
