@@ -13,8 +13,8 @@
 //             2 * (the bucket's first arc slot) -- slices never overlap and need no prefix sum;
 //             vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
-//   edge-pair table: ceil(w / 2) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
-//             <= 1/2); a pair probes its home group A, then an independent group B (both read together),
+//   edge-pair table: ceil(3w / 4) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
+//             <= 1/3); a pair probes its home group A, then an independent group B (both read together),
 //             then A+1, A+2, ...; Step 3's (src,dst)-sorted "edges" array with its
 //             multisearch becomes one sector read (a fingerprint hit is verified against E[k]).
 #pragma once
@@ -102,6 +102,9 @@ __host__ __device__ __forceinline__ uint32_t pgroup_start(uint64_t h, uint32_t g
 // Probe sequence of a pair over the G groups: its home group A, a second independent group B, then
 // A+1, A+2, ... (a key sits in the first group of its sequence that had room when it was inserted).
 __host__ __device__ __forceinline__ uint32_t pgroup_second(uint64_t h, uint32_t groups, uint32_t A) {
+#ifdef TC_PT_SINGLE
+    return A + 1 == groups ? 0u : A + 1;  // plain linear probing over groups
+#endif
     const uint32_t B = (uint32_t)(((uint64_t)hash_vertex((uint32_t)(h >> 32) ^ 0x9E3779B9u) * groups) >> 32);
     return (B != A || groups == 1) ? B : (A + 1 == groups ? 0u : A + 1);
 }
@@ -131,7 +134,12 @@ struct Lookup {
     uint32_t ptag;         // this batch's slot tag
 };
 
-__host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) { return (w + 1) / 2; }
+#ifndef TC_PT_GROUPS_PER_8
+#define TC_PT_GROUPS_PER_8 6  // groups of 4 slots per 8 edges: 6 -> load 1/3
+#endif
+__host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) {
+    return (uint32_t)(((uint64_t)w * TC_PT_GROUPS_PER_8 + 7) / 8);
+}
 
 // Continue a vertex probe at slot pair b of slice sl (after the first pair missed without an empty slot).
 static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uint32_t b, uint32_t v) {
@@ -168,11 +176,13 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
     P.a0 = P.a1 = P.b0 = P.b1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
     if (ng) {
         const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
-        const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
         P.a0 = __ldg(qa);
         P.a1 = __ldg(qa + 1);
+#ifndef TC_PT_SINGLE
+        const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
         P.b0 = __ldg(qb);
         P.b1 = __ldg(qb + 1);
+#endif
     }
 }
 
@@ -207,6 +217,9 @@ __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &
     if (P.ng == 0) return -1;
     uint32_t k;
     int r = pt_group(L, P, P.a0, P.a1, &k);
+#ifdef TC_PT_SINGLE
+    if (r == 2) return pt_walk(L, P);  // walks from the second group of the sequence
+#endif
     if (r == 2) r = pt_group(L, P, P.b0, P.b1, &k);
     if (r == 0) return -1;
     if (r == 1) return (int64_t)k;
