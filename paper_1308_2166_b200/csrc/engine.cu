@@ -93,7 +93,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
               cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
               cudaMalloc(&ix.vt, 16 * 4 * cap) == cudaSuccess &&  // slices at 2 * (bucket start), <= 2 n_b slots
               cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess;
-    ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.scratch, 16 * cap) == cudaSuccess &&
+    ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.scratch, 32 * cap) == cudaSuccess &&
          cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.vdefer, 4 * kMaxBuckets) == cudaSuccess &&
          cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.offV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&

@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
 struct VertArgs {
     uint4 *arcs;        // bucketed arcs {vertex, val, neighbour, 0} (overwritten by the chunked path)
     uint2 *scratch;
+    uint4 *scratch4;    // the same memory, as uint4 (k_vhub's rest arcs)
     const uint2 *E;
     const uint32_t *vstart;
     uint2 *segS;        // [2 w] {k<<1|side, neighbour} grouped by vertex
@@ -719,11 +720,11 @@ constexpr uint32_t kHCap = 4096;  // arcs: the largest bucket (or rest after a h
 // Shared-memory layout of the hash path for buckets of at most CAP arcs: R1 = {hkey u32[2 CAP], lid
 // u16[2 CAP]} while hashing; then {whist u16[8][SW], segst u32[CAP + 1]}; the slice table (u32,
 // <= 2 CAP slots) reuses whist; vkey u32[CAP] apart.
-template <uint32_t CAP>
+template <uint32_t CAP, int NT = kHThreads>
 struct HL {
     static constexpr uint32_t T = 2 * CAP;
     static constexpr uint32_t SW = CAP < 2048 ? CAP : 2048;
-    static constexpr uint32_t WH = kHWarps * SW * 2;
+    static constexpr uint32_t WH = (NT / 32) * SW * 2;
     static constexpr uint32_t TBL = 4 * 2 * CAP;
     static constexpr uint32_t SEGOFF = WH > TBL ? WH : TBL;
     static constexpr uint32_t R1A = T * 6, R1B = SEGOFF + (CAP + 1) * 4;
@@ -755,12 +756,13 @@ struct ArcSrc {
 
 // Hash-path grouping of n arcs (src) of bucket b whose segments start at slot base + off0; `hub` (if
 // hubn > 0) is an extra vertex whose segment [base, base + hubn) was already written.
-template <int R, uint32_t CAP>
+template <int R, uint32_t CAP, int NT = kHThreads>
 __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint32_t base, const ArcSrc &src, uint32_t n,
                                              uint32_t off0, uint32_t hub, uint32_t hubn, unsigned char *sm,
                                              uint32_t *ws, uint32_t *sD) {
-    using L = HL<CAP>;
-    static_assert((uint32_t)R * kHThreads <= CAP, "items per thread exceed the layout");
+    using L = HL<CAP, NT>;
+    constexpr uint32_t NW = NT / 32;
+    static_assert((uint32_t)R * NT <= CAP, "items per thread exceed the layout");
     uint32_t *hkey = reinterpret_cast<uint32_t *>(sm);
     uint16_t *lid = reinterpret_cast<uint16_t *>(sm + L::T * 4);
     uint16_t *whist = reinterpret_cast<uint16_t *>(sm);
@@ -769,7 +771,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     uint32_t *vkey = reinterpret_cast<uint32_t *>(sm + L::R1);
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
     const uint32_t Tb = pow2_ceil(2 * max(n, 1u));
-    for (uint32_t s = threadIdx.x; s < Tb; s += kHThreads) hkey[s] = kEmptyV;
+    for (uint32_t s = threadIdx.x; s < Tb; s += NT) hkey[s] = kEmptyV;
     if (threadIdx.x == 0) *sD = 0;
     __syncthreads();
     // phase 1: local ids (claim order) through the shared hash table; warp w owns items [w 32 R, (w+1) 32 R)
@@ -810,7 +812,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     for (uint32_t l0 = 0; l0 < D; l0 += L::SW) {
         const uint32_t nd = min(L::SW, D - l0);
         const uint32_t bits = log2_ceil(nd);
-        for (uint32_t i = threadIdx.x; i < kHWarps * nd; i += kHThreads) whist[i] = 0;
+        for (uint32_t i = threadIdx.x; i < NW * nd; i += NT) whist[i] = 0;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < R; ++j) {
@@ -830,10 +832,10 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
             if (in) pk[j] += c + before;
         }
         __syncthreads();
-        for (uint32_t d = threadIdx.x; d < nd; d += kHThreads) {  // exclusive prefix over warps; degree
+        for (uint32_t d = threadIdx.x; d < nd; d += NT) {  // exclusive prefix over warps; degree
             uint32_t run = 0;
 #pragma unroll
-            for (uint32_t x = 0; x < kHWarps; ++x) {
+            for (uint32_t x = 0; x < NW; ++x) {
                 const uint32_t c = whist[x * nd + d];
                 whist[x * nd + d] = (uint16_t)run;
                 run += c;
@@ -850,12 +852,12 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     }
     // phase 3: segment starts = exclusive scan of the degrees over local ids
     {
-        const uint32_t per = (D + kHThreads - 1) / kHThreads;
+        const uint32_t per = (D + NT - 1) / NT;
         const uint32_t q0 = min(D, threadIdx.x * per), q1 = min(D, q0 + per);
         uint32_t sum = 0;
         for (uint32_t q = q0; q < q1; ++q) sum += segst[q];
         uint32_t tot;
-        uint32_t run = block_exclusive_scan<kHThreads>(sum, ws, &tot);
+        uint32_t run = block_exclusive_scan<NT>(sum, ws, &tot);
         for (uint32_t q = q0; q < q1; ++q) {
             const uint32_t c = segst[q];
             segst[q] = run;
@@ -883,15 +885,15 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         a.vslice[b] = make_uint2((uint32_t)off, S);
         if (Dt) atomicAdd(&a.ctr[kCtrD], Dt);
     }
-    for (uint32_t s = threadIdx.x; s < S; s += kHThreads) table[s] = kEmptyV;
+    for (uint32_t s = threadIdx.x; s < S; s += NT) table[s] = kEmptyV;
     __syncthreads();
-    for (uint32_t l = threadIdx.x; l < Dt; l += kHThreads) {
+    for (uint32_t l = threadIdx.x; l < Dt; l += NT) {
         uint32_t s = vslot_start(hash_vertex(l < D ? vkey[l] : hub), S);
         while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV)
             if (++s == S) s = 0;
     }
     __syncthreads();
-    for (uint32_t s = threadIdx.x; s < S; s += kHThreads) {
+    for (uint32_t s = threadIdx.x; s < S; s += NT) {
         const uint32_t l = table[s];
         uint4 o = make_uint4(kEmptyV, 0u, 0u, 0u);
         if (l < D) o = make_uint4(vkey[l], segst[l + 1] - segst[l], b0 + segst[l], 0u);
@@ -900,13 +902,14 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     }
 }
 
-template <uint32_t CAP, typename F>
+template <uint32_t CAP, int NT, typename F>
 __device__ __forceinline__ void hash_dispatch(uint32_t n, F f) {
-    if (n <= 256) f(std::integral_constant<int, 1>());
-    else if (n <= 512) f(std::integral_constant<int, 2>());
-    else if (n <= 1024) f(std::integral_constant<int, 4>());
-    else if (CAP <= 2048 || n <= 2048) f(std::integral_constant<int, (CAP >= 2048 ? 8 : 4)>());
-    else f(std::integral_constant<int, (CAP >= 4096 ? 16 : 8)>());
+    constexpr int RMAX = (int)(CAP / NT);  // 8 or 16
+    if (n <= 1u * NT) f(std::integral_constant<int, 1>());
+    else if (n <= 2u * NT) f(std::integral_constant<int, 2>());
+    else if (n <= 4u * NT) f(std::integral_constant<int, 4>());
+    else if (RMAX <= 8 || n <= 8u * NT) f(std::integral_constant<int, (RMAX >= 8 ? 8 : 4)>());
+    else f(std::integral_constant<int, (RMAX >= 16 ? 16 : 8)>());
 }
 
 // Common buckets (<= vcap <= kHCapSmall arcs): 4 CTAs per SM.
@@ -922,28 +925,31 @@ __global__ void __launch_bounds__(kHThreads, 4) k_vhash(VertArgs a) {
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
     if (n > a.vcap) return;  // k_vhub's
     const ArcSrc src{a.arcs + base, nullptr, nullptr, nullptr};
-    hash_dispatch<kHCapSmall>(n, [&](auto r) {
-        vbucket_hash<decltype(r)::value, kHCapSmall>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
+    hash_dispatch<kHCapSmall, kHThreads>(n, [&](auto r) {
+        vbucket_hash<decltype(r)::value, kHCapSmall, kHThreads>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
     });
 }
 
-// Large buckets (more than vcap arcs): almost always one hub vertex plus about a normal bucket's worth of
-// others.  The most frequent vertex of a sample is peeled off (its arcs are one segment, already in arrival
-// order: a 1-bit stable partition), the rest goes through the hash path from shared memory.  Buckets whose
-// rest is still too large are deferred to k_vbig.  Persistent CTAs over vperm[0 .. ctr[kCtrBig]).
-constexpr uint32_t kHubSample = 256;
-constexpr uint32_t kVHubSmemBytes = HL<kHCap>::BYTES + 3 * kHCap * 4;
+// Large buckets (more than vcap arcs; at batch sizes of 2^22 and beyond, most buckets): 512-thread CTAs with
+// the hash path for up to kHubCap arcs.  A bucket larger than that is almost always one hub vertex plus
+// about a normal bucket's worth of others: the most frequent vertex of a sample is peeled off (its arcs are
+// one segment, already in arrival order: a 1-bit stable partition) and the rest, copied to the scratch
+// buffer, goes through the hash path.  Buckets whose rest is still too large are deferred to k_vbig.
+// Persistent CTAs (one per SM) over vperm[0 .. ctr[kCtrBig]).
+constexpr int kHubThreads = 1024;
+constexpr uint32_t kHubWarps = kHubThreads / 32;
+constexpr uint32_t kHubCap = 8192;
+constexpr uint32_t kHubSample = kHubThreads;
+constexpr uint32_t kVHubSmemBytes = HL<kHubCap, kHubThreads>::BYTES;
 
-__global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
+__global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ __align__(16) unsigned char hsm[];
-    uint32_t *rv = reinterpret_cast<uint32_t *>(hsm + HL<kHCap>::BYTES);
-    uint32_t *rval = rv + kHCap, *rnb = rval + kHCap;
-    __shared__ uint32_t ws[9];
+    __shared__ uint32_t ws[kHubWarps + 1];
     __shared__ uint32_t sD, s_b, s_h, s_cnt;
     __shared__ uint32_t skey[2 * kHubSample], scnt[2 * kHubSample];
-    __shared__ uint32_t wtot[2][kHWarps];
-    __shared__ unsigned long long wbest[kHWarps];
+    __shared__ uint32_t wtot[2][kHubWarps];
+    __shared__ unsigned long long wbest[kHubWarps];
     const uint32_t nbig = a.ctr[kCtrBig];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
     while (true) {
@@ -956,8 +962,16 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
         if (b == 0xFFFFFFFFu) return;
         const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
         const uint4 *arcs = a.arcs + base;
+        if (n <= kHubCap) {  // no peeling needed
+            const ArcSrc src{arcs, nullptr, nullptr, nullptr};
+            hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
+                vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
+            });
+            __syncthreads();
+            continue;
+        }
         // 1. candidate hub = the most frequent vertex of kHubSample evenly spaced arcs
-        for (uint32_t s = threadIdx.x; s < 2 * kHubSample; s += kHThreads) {
+        for (uint32_t s = threadIdx.x; s < 2 * kHubSample; s += kHubThreads) {
             skey[s] = kEmptyV;
             scnt[s] = 0;
         }
@@ -976,7 +990,7 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
         __syncthreads();
         {
             uint32_t best = 0, bs = 0;
-            for (uint32_t t2 = threadIdx.x; t2 < 2 * kHubSample; t2 += kHThreads)
+            for (uint32_t t2 = threadIdx.x; t2 < 2 * kHubSample; t2 += kHubThreads)
                 if (scnt[t2] > best) {
                     best = scnt[t2];
                     bs = t2;
@@ -991,27 +1005,28 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
             __syncthreads();
             if (threadIdx.x == 0) {
                 unsigned long long m = wbest[0];
-                for (uint32_t x = 1; x < kHWarps; ++x) m = wbest[x] > m ? wbest[x] : m;
+                for (uint32_t x = 1; x < kHubWarps; ++x) m = wbest[x] > m ? wbest[x] : m;
                 s_h = skey[(uint32_t)m];
             }
             __syncthreads();
         }
         const uint32_t h = s_h;
-        // 2. hub arcs H; the rest must fit the hash path
+        // 2. hub arcs H; the rest must fit the hash path (with the hub, D + 1 <= kHubCap vertices)
         uint32_t mine = 0;
-        for (uint32_t i = threadIdx.x; i < n; i += kHThreads) mine += arcs[i].x == h ? 1u : 0u;
+        for (uint32_t i = threadIdx.x; i < n; i += kHubThreads) mine += arcs[i].x == h ? 1u : 0u;
         mine = __reduce_add_sync(kFull, mine);
         if (lane == 0) atomicAdd(&s_cnt, mine);
         __syncthreads();
         const uint32_t H = s_cnt;
-        if (n - H > kHCap - 1) {  // not one hub: the radix-sort kernel takes it (D + hub must fit 2 kHCap slots)
+        if (n - H > kHubCap - 1) {  // not one hub: the radix-sort kernel takes it
             if (threadIdx.x == 0) a.vdefer[atomicAdd(&a.ctr[kCtrDefer], 1u)] = b;
             __syncthreads();
             continue;
         }
-        // 3. stable 1-bit partition: hub arcs -> segment [base, base + H); the rest -> shared lists
+        // 3. stable 1-bit partition: hub arcs -> segment [base, base + H); the rest -> scratch[base ..)
+        uint4 *rest = a.scratch4 + base;
         uint32_t hubrun = 0, restrun = 0;
-        for (uint32_t q0 = 0; q0 < n; q0 += kHThreads) {
+        for (uint32_t q0 = 0; q0 < n; q0 += kHubThreads) {
             const uint32_t i = q0 + threadIdx.x;
             uint4 x = make_uint4(0u, 0u, 0u, 0u);
             if (i < n) x = arcs[i];
@@ -1024,7 +1039,7 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
             __syncthreads();
             uint32_t ph = hubrun, pr = restrun, th = 0, tr = 0;
 #pragma unroll
-            for (uint32_t w2 = 0; w2 < kHWarps; ++w2) {
+            for (uint32_t w2 = 0; w2 < kHubWarps; ++w2) {
                 if (w2 < warp) {
                     ph += wtot[0][w2];
                     pr += wtot[1][w2];
@@ -1037,19 +1052,18 @@ __global__ void __launch_bounds__(kHThreads, 1) k_vhub(VertArgs a) {
                 a.segS[base + pos] = make_uint2(x.y, x.z);
                 a.einfo2[x.y] = make_uint2(base + pos, base + H);
             } else if (valid) {
-                const uint32_t r = pr + __popc(br & lt);
-                rv[r] = x.x;
-                rval[r] = x.y;
-                rnb[r] = x.z;
+                rest[pr + __popc(br & lt)] = x;
             }
             hubrun += th;
             restrun += tr;
             __syncthreads();
         }
+        __threadfence_block();
+        __syncthreads();
         // 4. the rest through the hash path (segments after the hub's), the hub as an extra vertex
-        const ArcSrc src{nullptr, rv, rval, rnb};
-        hash_dispatch<kHCap>(n - H, [&](auto r) {
-            vbucket_hash<decltype(r)::value, kHCap>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD);
+        const ArcSrc src{rest, nullptr, nullptr, nullptr};
+        hash_dispatch<kHubCap, kHubThreads>(n - H, [&](auto r) {
+            vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD);
         });
         __syncthreads();
     }
@@ -1330,7 +1344,7 @@ int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
-    return VertArgs{ix.arcs, ix.scratch, ix.E, ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
+    return VertArgs{ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E, ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
                     ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 
@@ -1340,7 +1354,7 @@ int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    k_vhub<<<kBigCTAs, kHThreads, kVHubSmemBytes, s>>>(vert_args(ix, a));
+    k_vhub<<<sm_count(), kHubThreads, kVHubSmemBytes, s>>>(vert_args(ix, a));
     k_vbig<<<kBigCTAs, kVBucketThreads, kVSmemBytes, s>>>(vert_args(ix, a));
     return 2;
 }
