@@ -99,6 +99,13 @@ int tc_closed_sum(tc_ctx *ctx, uint64_t *S);
  * 887-888 (reading R9).  1 <= groups <= count.  Synchronises. */
 int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out);
 
+/* tc_required_estimators -- the number of estimators that suffices for an (eps, delta)-approximation
+ * (Theorem mdelta-suffices): r = ceil(96 / eps^2 * (m * Delta / tau) * ln(1 / delta)),
+ * natural log (reading R10), evaluated in fp64.  m: stream edges, Delta: maximum degree, tau: a
+ * lower bound on the triangle count.  Host-only (no device work).  TC_EINVAL unless 0 < eps, 0 < delta < 1,
+ * tau > 0 and m * Delta < 2^64; TC_EOVERFLOW if r does not fit 64 bits. */
+int tc_required_estimators(double eps, double delta, uint64_t m, uint64_t Delta, uint64_t tau, uint64_t *r);
+
 /* tc_group_sums -- S_g for the same contiguous groups (exact uint64, host array of `groups`). */
 int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g);
 

@@ -13,11 +13,20 @@ import numpy as np
 from . import _lib
 from ._lib import PHASES, TCError
 
-__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library"]
+__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators"]
 
 
 def load_library():
     return _lib.load()
+
+
+def required_estimators(eps: float, delta: float, m: int, Delta: int, tau: int) -> int:
+    """tc_required_estimators: r = ceil(96/eps^2 * m*Delta/tau * ln(1/delta)) (PAPER.md:377-383)."""
+    out = C.c_uint64()
+    rc = _lib.load().tc_required_estimators(float(eps), float(delta), int(m), int(Delta), int(tau), C.byref(out))
+    if rc != 0:
+        raise TCError(rc, "tc_required_estimators")
+    return int(out.value)
 
 
 def _edges_ptr(edges):

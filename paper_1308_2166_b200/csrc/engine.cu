@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -486,6 +487,16 @@ int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g) {
                     cudaStreamSynchronize(ctx->stream) == cudaSuccess;
     cudaFree(d);
     return ok ? TC_OK : fail_cuda(ctx);
+}
+
+int tc_required_estimators(double eps, double delta, uint64_t m, uint64_t Delta, uint64_t tau, uint64_t *r) {
+    if (!r || !(eps > 0.0) || !(delta > 0.0 && delta < 1.0) || tau == 0) return TC_EINVAL;
+    if (Delta && m > UINT64_MAX / Delta) return TC_EINVAL;
+    const double x = 96.0 / (eps * eps) * ((double)(m * Delta) / (double)tau) * std::log(1.0 / delta);
+    const double c = std::ceil(x);
+    if (!(c < 18446744073709551616.0)) return TC_EOVERFLOW;
+    *r = (uint64_t)c;
+    return TC_OK;
 }
 
 int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out) {

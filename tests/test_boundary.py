@@ -54,3 +54,21 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle|#include\s*[<\"].*oracle|liboracle", txt, re.M), f
+
+
+def test_required_estimators_matches_oracle():
+    """tc_required_estimators (host-only, no device needed) against the oracle's sizing helper (Theorem
+    mdelta-suffices) and its closed form at ln(1/delta) = 1."""
+    import math
+
+    from oracle import nbsi
+    from paper_1308_2166_b200 import TCError, required_estimators
+    from paper_1308_2166_b200 import build as b
+    b.build()
+    assert required_estimators(0.5, math.exp(-1), 10, 4, 20) == math.ceil(96 / 0.25 * 2.0)
+    for eps, delta, m, D, tau in [(0.1, 0.05, 117_185_083, 33_313, 627_584_181), (0.2, 0.01, 1_000, 59, 10_615),
+                                  (0.05, 0.1, 1_806_067_135, 5_214, 4_173_724_142)]:
+        assert required_estimators(eps, delta, m, D, tau) == nbsi.required_estimators(eps, delta, m, D, tau)
+    for bad in [(0.0, 0.5, 1, 1, 1), (0.1, 1.0, 1, 1, 1), (0.1, 0.5, 1, 1, 0)]:
+        with pytest.raises(TCError):
+            required_estimators(*bad)
