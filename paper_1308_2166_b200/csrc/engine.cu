@@ -69,7 +69,7 @@ static int fail_cuda(tc_ctx *c) {
     } while (0)
 
 static void free_index(IndexBufs &ix) {
-    void *bufs[] = {ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
+    void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
                     ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
@@ -94,10 +94,11 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
               cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
               cudaMalloc(&ix.vt, 16 * 4 * cap) == cudaSuccess &&  // slices at 2 * (bucket start), <= 2 n_b slots
               cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess;
-    ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.scratch, 32 * cap) == cudaSuccess &&
+    ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.vstart2, 4 * kStartWords) == cudaSuccess &&
+         cudaMalloc(&ix.arcs2, 32 * cap) == cudaSuccess && cudaMalloc(&ix.scratch, 32 * cap) == cudaSuccess &&
          cudaMalloc(&ix.vperm, 4 * kMaxBuckets) == cudaSuccess && cudaMalloc(&ix.vdefer, 4 * kMaxBuckets) == cudaSuccess &&
-         cudaMalloc(&ix.cntV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
-         cudaMalloc(&ix.offV, 4 * kMaxBuckets * ix.tiles_cap) == cudaSuccess &&
+         cudaMalloc(&ix.cntV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
+         cudaMalloc(&ix.offV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
          cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
     if (!ok) {
@@ -359,7 +360,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         rec(2 * TC_PHASE_UPDATE + 1, ms);
         if (ctx->prof)
             for (int p = 0; p < TC_NPHASES; ++p)
-                ctx->prof_launch[p] += (p == TC_PHASE_PARTITION ? 4 : p == TC_PHASE_VERTICES ? 3 : 1);
+                ctx->prof_launch[p] += (p == TC_PHASE_PARTITION ? 4 + (a.g.bs ? 1 : 0) : p == TC_PHASE_VERTICES ? 3 : 1);
         if (graph) {
             cudaGraph_t g = nullptr;
             const bool cap = cudaStreamEndCapture(ctx->stream, &g) == cudaSuccess && g;

@@ -41,7 +41,9 @@ constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 #endif
 constexpr uint32_t kTileEdges = TC_TILE_EDGES;  // edges per count/scatter tile
 constexpr uint32_t kTileThreads = 512;
-constexpr uint32_t kMaxBucketBits = 12;   // at most 4096 vertex buckets
+constexpr uint32_t kMaxPartBits = 12;     // the partition kernels: at most 4096 vertex buckets
+constexpr uint32_t kMaxSplitBits = 3;     // k_split: each of them into at most 8 sub-buckets
+constexpr uint32_t kMaxBucketBits = kMaxPartBits + kMaxSplitBits;
 constexpr uint32_t kVBucketThreads = 256; // vertex-bucket CTA
 constexpr uint32_t kVItems = 24;          // arcs per thread held in registers by the vertex-bucket sort
 constexpr uint32_t kVChunk = kVBucketThreads * kVItems;  // 6144 arcs: larger buckets take the chunked path

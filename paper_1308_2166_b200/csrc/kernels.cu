@@ -47,7 +47,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid, uint32_t
     uint32_t m = __ballot_sync(kFull, valid);
     if (!valid) m = ~m;
 #pragma unroll
-    for (uint32_t b = 0; b < kMaxBucketBits; ++b) {
+    for (uint32_t b = 0; b < kMaxPartBits; ++b) {
         if (b < nbits) {
             const uint32_t bit = (d >> b) & 1u;
             m &= __ballot_sync(kFull, bit) ^ (bit - 1u);  // lanes whose bit b equals mine
@@ -162,7 +162,7 @@ constexpr uint32_t kArcsPerWarp = kArcRounds * 32, kEdgesPerWarp = kEdgeRounds *
 __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     extern __shared__ uint32_t dsh[];
-    const uint32_t nV = 1u << a.g.bv;
+    const uint32_t nV = 1u << a.g.bp1;
     uint16_t *wv = reinterpret_cast<uint16_t *>(dsh);  // [kTileWarps][nV]
     for (uint32_t i = threadIdx.x; i < kTileWarps * nV / 2; i += kTileThreads) dsh[i] = 0;
     __syncthreads();
@@ -192,9 +192,9 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
         uint32_t d = 0;
         if (valid) {
             const uint2 n = norm_edge(__ldg(a.in + e0 + (ai >> 1)));
-            d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bv);
+            d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bp1);
         }
-        const uint32_t peers = digit_peers(d, valid, a.g.bv);
+        const uint32_t peers = digit_peers(d, valid, a.g.bp1);
         const uint32_t before = __popc(peers & lt);
         uint32_t c = 0;
         if (valid) c = wv[warp * nV + d];
@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ uint32_t dsh[];
     __shared__ uint32_t ws[kTileThreads / 32 + 1];
-    const uint32_t nV = 1u << a.g.bv;
+    const uint32_t nV = 1u << a.g.bp1;
     uint32_t *soff = dsh, *toff = dsh + nV;                            // [nV] each
     uint2 *sE = reinterpret_cast<uint2 *>(dsh + 2 * nV);               // [kTileEdges] the tile's edges
     uint16_t *idx = reinterpret_cast<uint16_t *>(sE + kTileEdges);    // [2 kTileEdges] arcs in bucket order
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
     __syncthreads();
     for (uint32_t ai = threadIdx.x; ai < 2 * ne; ai += kTileThreads) {
         const uint2 n = sE[ai >> 1];
-        const uint32_t d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bv);
+        const uint32_t d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bp1);
         idx[toff[d] + a.arank[2 * e0 + ai]] = (uint16_t)ai;
     }
     __syncthreads();
@@ -326,13 +326,98 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
         const uint32_t ai = idx[pos];
         const uint2 n = sE[ai >> 1];
         const uint32_t v = (ai & 1u) ? n.y : n.x, nb = (ai & 1u) ? n.x : n.y;
-        const uint32_t d = vbucket_of(hash_vertex(v), a.g.bv);
+        const uint32_t d = vbucket_of(hash_vertex(v), a.g.bp1);
         __stcs(a.arcs + soff[d] + (pos - toff[d]), make_uint4(v, 2u * e0 + ai, nb, 0u));
     }
 }
 
 // ------------------------------------------------------------------------------------------------
 // a3: pair-table slices
+
+// ------------------------------------------------------------------------------------------------
+// a2 at large batches: the partition makes at most 4096 buckets (its per-tile counters and offsets grow
+// with buckets x tiles), so for 2w > 4096 x 1024 arcs each bucket is split again, stably, by the next bs
+// bits of the vertex hash into 2^bs sub-buckets (one 1024-thread CTA per bucket; ballots per sub-bucket
+// value).  The sub-buckets are the vertex buckets of the rest of the batch (bucket id = top bp1 + bs bits).
+
+struct SplitArgs {
+    const uint4 *arcs;
+    uint4 *arcs2;
+    const uint32_t *vstart;  // partition-bucket starts
+    uint32_t *vstart2;       // sub-bucket starts
+    uint32_t bp1, bs, vcap;
+    uint32_t *vperm;         // sub-buckets larger than vcap (k_vhub's list)
+    uint32_t *ctr;
+};
+
+constexpr int kSplitThreads = 1024;
+
+__global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
+    if (a.ctr[kCtrErr] & kErrStage) return;
+    constexpr uint32_t NW = kSplitThreads / 32;
+    __shared__ uint32_t wc[NW][1u << kMaxSplitBits];
+    __shared__ uint32_t tot[1u << kMaxSplitBits], soff[1u << kMaxSplitBits], run[1u << kMaxSplitBits];
+    const uint32_t b = blockIdx.x, S = 1u << a.bs;
+    const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
+    const uint32_t sh = 32 - a.bp1 - a.bs, smask = S - 1u;
+    if (threadIdx.x < S) {
+        tot[threadIdx.x] = 0;
+        run[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    // pass A: sub-bucket sizes
+    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
+        const uint32_t i = q0 + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t sb = valid ? (hash_vertex(a.arcs[base + i].x) >> sh) & smask : 0u;
+        for (uint32_t x = 0; x < S; ++x) {
+            const uint32_t c = __popc(__ballot_sync(kFull, valid && sb == x));
+            if (lane == 0 && c) atomicAdd(&tot[x], c);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (uint32_t x = 0; x < S; ++x) {
+            soff[x] = r;
+            a.vstart2[(b << a.bs) + x] = base + r;
+            if (tot[x] > a.vcap) a.vperm[atomicAdd(&a.ctr[kCtrBig], 1u)] = (b << a.bs) + x;
+            r += tot[x];
+        }
+        if (b == gridDim.x - 1) a.vstart2[gridDim.x << a.bs] = base + n;
+    }
+    __syncthreads();
+    // pass B: stable ranks chunk by chunk (chunk order, then warp order, then lane order = arrival order)
+    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
+        const uint32_t i = q0 + threadIdx.x;
+        const bool valid = i < n;
+        uint4 x4 = make_uint4(0u, 0u, 0u, 0u);
+        if (valid) x4 = a.arcs[base + i];
+        const uint32_t sb = valid ? (hash_vertex(x4.x) >> sh) & smask : 0u;
+        uint32_t mine = 0;
+        for (uint32_t x = 0; x < S; ++x) {
+            const uint32_t m = __ballot_sync(kFull, valid && sb == x);
+            if (lane == 0) wc[warp][x] = __popc(m);
+            if (sb == x) mine = __popc(m & lt);
+        }
+        __syncthreads();
+        if (threadIdx.x < S) {  // per sub-bucket: exclusive prefix over warps
+            uint32_t r = 0;
+            for (uint32_t w2 = 0; w2 < NW; ++w2) {
+                const uint32_t c = wc[w2][threadIdx.x];
+                wc[w2][threadIdx.x] = r;
+                r += c;
+            }
+            tot[threadIdx.x] = r;  // this chunk's count
+        }
+        __syncthreads();
+        if (valid) a.arcs2[base + soff[sb] + run[sb] + wc[warp][sb] + mine] = x4;
+        __syncthreads();
+        if (threadIdx.x < S) run[threadIdx.x] += tot[threadIdx.x];
+        __syncthreads();
+    }
+}
 
 // ------------------------------------------------------------------------------------------------
 // a2: vertex buckets
@@ -1318,6 +1403,8 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
     g.w = w;
     g.tiles = (w + kTileEdges - 1) / kTileEdges;
     g.bv = std::min(kMaxBucketBits, ceil_log2((2ull * w + t.vbucket_arcs - 1) / t.vbucket_arcs));
+    g.bp1 = std::min(g.bv, kMaxPartBits);
+    g.bs = g.bv - g.bp1;
     g.vcap = std::min(t.vcap, kHCapSmall);
     g.sortcap = std::min(t.sortcap, kVChunk);
     return g;
@@ -1329,13 +1416,17 @@ static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const Geometry &g = a.g;
-    const uint32_t nV = 1u << g.bv;
+    const uint32_t nV = 1u << g.bp1;
     const PartArgs p = part_args(ix, a);
     k_count<<<g.tiles, kTileThreads, 2 * kTileWarps * nV, s>>>(p);
     k_scan_rows<<<nV, 256, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, ix.ctr);
-    k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.vcap, ix.vperm, ix.ctr);
+    // with a split, the large-bucket list is built by k_split over the sub-buckets
+    k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.bs ? 0xFFFFFFFFu : g.vcap, ix.vperm, ix.ctr);
     k_scatter<<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
-    return 4;
+    if (!g.bs) return 4;
+    SplitArgs sa{ix.arcs, ix.arcs2, ix.vstart, ix.vstart2, g.bp1, g.bs, g.vcap, ix.vperm, ix.ctr};
+    k_split<<<nV, kSplitThreads, 0, s>>>(sa);
+    return 5;
 }
 
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
@@ -1344,7 +1435,8 @@ int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
-    return VertArgs{ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E, ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
+    return VertArgs{a.g.bs ? ix.arcs2 : ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E,
+                    a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
                     ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 

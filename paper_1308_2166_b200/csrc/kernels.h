@@ -14,6 +14,8 @@ struct IndexBufs {
     uint2 *E = nullptr;            // [wcap] normalised edges
     uint4 *arcs = nullptr;         // [2 wcap] vertex-bucketed arcs {vertex, k<<1|side, neighbour, 0}, arrival
                                    // order per bucket
+    uint4 *arcs2 = nullptr;        // [2 wcap] arcs of the split sub-buckets (when Geometry::bs > 0)
+    uint32_t *vstart2 = nullptr;   // [2^15 + 1] sub-bucket starts
     uint2 *scratch = nullptr;      // [2 wcap] sort scratch of oversized vertex buckets
     uint2 *segS = nullptr;         // [2 wcap] arcs {k<<1|side, neighbour} grouped by vertex
     uint4 *einfo = nullptr;        // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
@@ -43,7 +45,9 @@ struct StateBufs {
 struct Geometry {
     uint32_t w;
     uint32_t tiles;    // ceil(w / kTileEdges)
-    uint32_t bv;       // vertex bucket bits
+    uint32_t bv;       // vertex bucket bits (= bp1 + bs)
+    uint32_t bp1;      // partition bits (<= 12): the buckets of k_count / k_scatter
+    uint32_t bs;       // split bits (k_split: each partition bucket into 2^bs sub-buckets; 0 = no split)
     uint32_t vcap;     // vertex buckets larger than this go to k_vhub (<= 2048)
     uint32_t sortcap;  // k_vbig: buckets larger than this take the chunked global-memory path (<= kVChunk)
 };
@@ -68,7 +72,7 @@ struct Tuning {
 Geometry make_geometry(uint32_t w, const Tuning &t);
 
 // Each returns the number of kernel launches issued.
-int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a1: count, scans, scatter
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a1: count, scans, scatter, split
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);      // a3: edge-pair table
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);   // a2: grouping, ranks, vertex table
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a2: the buckets > vcap

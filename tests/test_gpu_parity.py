@@ -101,7 +101,9 @@ def test_hub_segments_multi_chunk():
     dict(vbucket_cap=1),                           # every vertex bucket through the hub-peel kernel
     dict(vbucket_arcs=8192, vbucket_cap=1),        # hub-less buckets > 4096 arcs: radix sort in shared memory
     dict(vbucket_cap=37, vbucket_sort_cap=200),    # a mix of all paths
-    dict(vbucket_arcs=16),                         # many buckets (bucket bits capped at 12)
+    dict(vbucket_arcs=16),                         # many buckets
+    dict(vbucket_arcs=1),                          # 2^15 buckets: 4096 partition buckets split 8 ways (k_split)
+    dict(vbucket_arcs=2, vbucket_cap=3),           # split + most sub-buckets through the large-bucket kernels
     dict(vbucket_arcs=1 << 30),                    # one vertex bucket
 ])
 def test_index_geometry_knobs(knobs):
