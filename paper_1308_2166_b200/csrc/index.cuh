@@ -14,8 +14,8 @@
 //             vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
 //   edge-pair table: ceil(3w / 4) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
-//             <= 1/3); a pair probes its home group A, then an independent group B (both read together),
-//             then A+1, A+2, ...; Step 3's (src,dst)-sorted "edges" array with its
+//             <= 1/3); a pair probes its home group A, then (if A is full) an independent group B, then
+//             A+1, A+2, ...; Step 3's (src,dst)-sorted "edges" array with its
 //             multisearch becomes one sector read (a fingerprint hit is verified against E[k]).
 #pragma once
 #include <cstdint>
@@ -180,7 +180,7 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
         const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
         P.a0 = __ldg(qa);
         P.a1 = __ldg(qa + 1);
-#ifndef TC_PT_SINGLE
+#if !defined(TC_PT_SINGLE) && defined(TC_PT_EAGER_B)
         const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
         P.b0 = __ldg(qb);
         P.b1 = __ldg(qb + 1);
@@ -219,8 +219,16 @@ __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &
     if (P.ng == 0) return -1;
     uint32_t k;
     int r = pt_group(L, P, P.a0, P.a1, &k);
-#ifdef TC_PT_SINGLE
+#if defined(TC_PT_SINGLE)
     if (r == 2) return pt_walk(L, P);  // walks from the second group of the sequence
+#elif !defined(TC_PT_EAGER_B)
+    if (r == 2) {  // group A full (rare at load 1/3): read B now
+        const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
+        r = pt_group(L, P, __ldg(qb), __ldg(qb + 1), &k);
+        if (r == 0) return -1;
+        if (r == 1) return (int64_t)k;
+        return pt_walk(L, P);
+    }
 #endif
     if (r == 2) r = pt_group(L, P, P.b0, P.b1, &k);
     if (r == 0) return -1;
