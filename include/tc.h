@@ -168,6 +168,21 @@ int tc_stats(tc_ctx *ctx, uint64_t *out, int n);
 /* Number of kernel launches issued by the last successful push (for the bench's gpu_launches). */
 int tc_last_launches(tc_ctx *ctx, uint32_t *launches);
 
+/* ------------------------------------------------------------------------------------------- */
+/* Ground truth for the accuracy study (MD% methodology PAPER.md:993-1003).   */
+
+/* tc_exact_triangles -- tau = |T(G)|, the exact number of triangles of the simple undirected graph
+ * whose m edges are `edges` (§2: T(G) the triangles, tau = |T(G)|), computed on the
+ * current CUDA device by degree-ordered wedge closing (exact.cu).  edges: host or device memory, any
+ * orientation, m < 2^31; read only, owned by the caller.  Independent of every estimator handle (it
+ * allocates and frees its own device scratch, about 80 bytes per edge, on its own stream).
+ * *tau receives the count; device_ms (may be NULL) the device time of the computation from the first
+ * kernel to the last (CUDA events; the host->device copy of host edges is excluded).
+ * Errors: TC_EINVAL (tau NULL, edges NULL with m > 0, m >= 2^31, or a vertex id 0xFFFFFFFF),
+ * TC_ESELFLOOP (u == v), TC_EDUP (the same undirected pair twice), TC_ENOMEM, TC_ECUDA.  On error *tau
+ * is 0.  Synchronises. */
+int tc_exact_triangles(const tc_edge *edges, uint64_t m, uint64_t *tau, double *device_ms);
+
 const char *tc_strerror(int code);
 int tc_last_error(void); /* thread-local code of the last failed tc_create* */
 

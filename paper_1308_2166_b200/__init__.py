@@ -13,7 +13,7 @@ import numpy as np
 from . import _lib
 from ._lib import PHASES, TCError
 
-__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators"]
+__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators", "exact_triangles"]
 
 
 def load_library():
@@ -27,6 +27,19 @@ def required_estimators(eps: float, delta: float, m: int, Delta: int, tau: int) 
     if rc != 0:
         raise TCError(rc, "tc_required_estimators")
     return int(out.value)
+
+
+def exact_triangles(edges, timing: bool = False):
+    """tc_exact_triangles: tau = |T(G)| of the simple graph with these edges, on the
+    current CUDA device.  edges: (m, 2) uint32 numpy array or uint32/int32 torch tensor (host or cuda).
+    Returns tau, or (tau, device_ms) with timing=True."""
+    ptr, m, keep = _edges_ptr(edges)
+    tau, ms = C.c_uint64(), C.c_double()
+    rc = _lib.load().tc_exact_triangles(ptr, int(m), C.byref(tau), C.byref(ms))
+    del keep
+    if rc != 0:
+        raise TCError(rc, "tc_exact_triangles")
+    return (int(tau.value), float(ms.value)) if timing else int(tau.value)
 
 
 def _edges_ptr(edges):

@@ -23,7 +23,8 @@ TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4}
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
-           "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_strerror", "tc_last_error"]
+           "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_strerror",
+           "tc_last_error"]
 
 _lib = None
 
@@ -66,6 +67,7 @@ def load(path: str = LIB_PATH):
         "tc_profile_read": (i32, [vp, vp, vp, i32]),
         "tc_stats": (i32, [vp, vp, i32]),
         "tc_last_launches": (i32, [vp, C.POINTER(u32)]),
+        "tc_exact_triangles": (i32, [vp, u64, C.POINTER(u64), C.POINTER(C.c_double)]),
         "tc_strerror": (C.c_char_p, [i32]),
         "tc_last_error": (i32, []),
     }
