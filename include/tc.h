@@ -45,7 +45,9 @@ enum {
     TC_EDUP = -4,        /* the same undirected pair twice in one batch  */
     TC_EOVERFLOW = -5,   /* m would exceed 2^31-1: chi <= m must fit 31 bits (reading R13)  */
     TC_ECUDA = -6,       /* a CUDA call failed; the handle is poisoned                      */
-    TC_ESTATE = -8       /* handle poisoned by an earlier asynchronous error               */
+    TC_ESTATE = -8,      /* handle poisoned by an earlier asynchronous error               */
+    TC_EPARSE = -9,      /* malformed edge-list line (tc_parse_edges / tc_ingest_file)      */
+    TC_EIO = -10         /* the edge-list file cannot be opened or read                     */
 };
 
 /* tc_create -- r estimators (ids 0..r-1) on the current CUDA device, all "empty" (f1 = f2 = f3 =
@@ -182,6 +184,46 @@ int tc_last_launches(tc_ctx *ctx, uint32_t *launches);
  * TC_ESELFLOOP (u == v), TC_EDUP (the same undirected pair twice), TC_ENOMEM, TC_ECUDA.  On error *tau
  * is 0.  Synchronises. */
 int tc_exact_triangles(const tc_edge *edges, uint64_t m, uint64_t *tau, double *device_ms);
+
+/* ------------------------------------------------------------------------------------------- */
+/* Ingestion in front of the path: SNAP-format text edge lists, the format of
+ * the paper's datasets ("a list of edges in plain text", Table 1; streamed "as they are read from
+ * disk"; I/O timed apart from processing).                  */
+
+/* Line format: blank lines and lines whose first non-blank character is '#' or '%' are skipped; an
+ * edge line is  <u> <whitespace> <v>  with u, v decimal ids <= 0xFFFFFFFE (spaces / tabs, '\r' allowed),
+ * optionally followed by whitespace and further columns, which are ignored.  u == v is TC_ESELFLOOP
+ * unless TC_INGEST_SKIP_LOOPS is set (then the line is skipped).  Duplicate pairs are NOT removed: the
+ * file must list a simple graph, each edge once (a repeat inside one batch fails the push with TC_EDUP). */
+enum { TC_INGEST_SKIP_LOOPS = 1 };
+
+/* tc_parse_edges -- parse text[0, len) (host memory) into out[0, cap) (host).  Complete lines only,
+ * unless final != 0 (then a last line without '\n' counts too); stops early when out is full (the
+ * line that did not fit is not consumed).  *n_edges = edges written, *consumed = bytes consumed (a
+ * prefix of whole lines), *lines = lines consumed.  On TC_EPARSE / TC_ESELFLOOP, *consumed stops before
+ * the bad line and *lines counts it (so the caller's running count + *lines is its 1-based number).
+ * Host-only (no device work). */
+int tc_parse_edges(const char *text, uint64_t len, int final, int flags, tc_edge *out, uint64_t cap,
+                   uint64_t *n_edges, uint64_t *consumed, uint64_t *lines);
+
+typedef struct {
+    uint64_t edges;       /* edges pushed (accepted)                                             */
+    uint64_t batches;     /* tc_push_batch calls that succeeded                                  */
+    uint64_t lines;       /* lines read                                                          */
+    uint64_t error_line;  /* 1-based line of a parse error / self-loop, else 0                    */
+    double io_s;          /* reader thread busy time: file reads + parsing (the paper's "I/O")   */
+    double push_s;        /* time inside tc_push_batch (staging copy + update; strict mode: sync) */
+    double wait_s;        /* time the pushing thread waited for a parsed batch (I/O-bound part)  */
+    double wall_s;        /* whole call                                                          */
+} tc_ingest_stats;
+
+/* tc_ingest_file -- stream the SNAP-format edge list at `path` through tc_push_batch in batches of w
+ * edges (the last one may be short), in file order.  A reader thread reads and parses into one of two
+ * pinned host batch buffers while the calling thread pushes the other, so file I/O and parsing overlap
+ * the GPU update.  Returns the first error: TC_EIO, TC_EPARSE / TC_ESELFLOOP (stats->error_line says
+ * where; batches before it may already have been pushed -- stats->edges of them), or any tc_push_batch
+ * code.  Synchronises at the end (tc_sync).  stats may be NULL. */
+int tc_ingest_file(tc_ctx *ctx, const char *path, uint64_t w, int flags, tc_ingest_stats *stats);
 
 const char *tc_strerror(int code);
 int tc_last_error(void); /* thread-local code of the last failed tc_create* */

@@ -7,13 +7,14 @@ library's CUDA kernels.  PyTorch, when used, only supplies device memory and str
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
 from . import _lib
 from ._lib import PHASES, TCError
 
-__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators", "exact_triangles"]
+__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators", "exact_triangles", "parse_edges"]
 
 
 def load_library():
@@ -40,6 +41,21 @@ def exact_triangles(edges, timing: bool = False):
     if rc != 0:
         raise TCError(rc, "tc_exact_triangles")
     return (int(tau.value), float(ms.value)) if timing else int(tau.value)
+
+
+def parse_edges(text: bytes, final: bool = True, skip_loops: bool = False, cap: int | None = None):
+    """tc_parse_edges on a bytes chunk: returns (edges (n, 2) uint32, bytes consumed, lines consumed)."""
+    buf = bytes(text)
+    cap = len(buf) // 4 + 1 if cap is None else int(cap)  # an edge line takes >= 4 bytes ("1 2\n")
+    out = np.empty((cap, 2), dtype=np.uint32)
+    n, used, lines = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    rc = _lib.load().tc_parse_edges(buf, len(buf), int(final), _lib.TC_INGEST_SKIP_LOOPS if skip_loops else 0,
+                                    out.ctypes.data_as(C.c_void_p), cap, C.byref(n), C.byref(used), C.byref(lines))
+    if rc != 0:
+        err = TCError(rc, f"tc_parse_edges (line {lines.value})")
+        err.line = int(lines.value)
+        raise err
+    return out[:n.value].copy(), int(used.value), int(lines.value)
 
 
 def _edges_ptr(edges):
@@ -102,6 +118,19 @@ class TriangleCounter:
     def push_batch_ptr(self, ptr: int, w: int) -> int:
         """Raw pointer form (device or host address of w tc_edge); returns the status code."""
         return _lib.load().tc_push_batch(self._h, C.c_void_p(ptr), int(w))
+
+    def ingest_file(self, path: str, w: int, skip_loops: bool = False) -> dict:
+        """tc_ingest_file: stream a SNAP-format edge list through push_batch in batches of w (a reader
+        thread parses ahead into two pinned buffers).  Returns the tc_ingest_stats fields as a dict."""
+        st = _lib.IngestStats()
+        rc = _lib.load().tc_ingest_file(self._h, os.fsencode(path), int(w),
+                                        _lib.TC_INGEST_SKIP_LOOPS if skip_loops else 0, C.byref(st))
+        out = {f: getattr(st, f) for f, _ in st._fields_}
+        if rc != 0:
+            err = TCError(rc, "tc_ingest_file" + (f" (line {st.error_line})" if st.error_line else ""))
+            err.stats = out
+            raise err
+        return out
 
     def estimate(self) -> float:
         out = C.c_double()

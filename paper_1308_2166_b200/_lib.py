@@ -17,16 +17,25 @@ TC_EDUP = -4
 TC_EOVERFLOW = -5
 TC_ECUDA = -6
 TC_ESTATE = -8
+TC_EPARSE = -9
+TC_EIO = -10
+TC_INGEST_SKIP_LOOPS = 1
 TC_NPHASES = 4
 PHASES = ("partition", "pairs", "vertices", "update")
 TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4}
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
-           "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_strerror",
+           "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_parse_edges", "tc_ingest_file", "tc_strerror",
            "tc_last_error"]
 
 _lib = None
+
+
+class IngestStats(C.Structure):
+    """tc_ingest_stats (include/tc.h)."""
+    _fields_ = [("edges", C.c_uint64), ("batches", C.c_uint64), ("lines", C.c_uint64), ("error_line", C.c_uint64),
+                ("io_s", C.c_double), ("push_s", C.c_double), ("wait_s", C.c_double), ("wall_s", C.c_double)]
 
 
 class TCError(RuntimeError):
@@ -68,6 +77,8 @@ def load(path: str = LIB_PATH):
         "tc_stats": (i32, [vp, vp, i32]),
         "tc_last_launches": (i32, [vp, C.POINTER(u32)]),
         "tc_exact_triangles": (i32, [vp, u64, C.POINTER(u64), C.POINTER(C.c_double)]),
+        "tc_parse_edges": (i32, [vp, u64, i32, i32, vp, u64, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
+        "tc_ingest_file": (i32, [vp, C.c_char_p, u64, i32, C.POINTER(IngestStats)]),
         "tc_strerror": (C.c_char_p, [i32]),
         "tc_last_error": (i32, []),
     }

@@ -612,6 +612,8 @@ const char *tc_strerror(int code) {
         case TC_EOVERFLOW: return "stream longer than 2^31-1 edges (chi field overflow)";
         case TC_ECUDA: return "CUDA error";
         case TC_ESTATE: return "handle poisoned by an earlier asynchronous error";
+        case TC_EPARSE: return "malformed edge-list line";
+        case TC_EIO: return "cannot open or read the edge-list file";
         default: return "unknown error";
     }
 }
