@@ -63,7 +63,9 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
 
 /* tc_push_batch -- bulkUpdateAll on the next w edges of the stream.
  *  edges: w tc_edge in arrival order.  Host memory (pageable or pinned) or device memory on the
- *         handle's device.  Host buffers are copied before the call returns; a device buffer must
+ *         handle's device.  Host buffers are copied before the call returns (uploaded on a copy stream
+ *         into one of two staging buffers, so the upload overlaps the previous batch's kernels when
+ *         asynchronous errors are enabled); a device buffer must
  *         stay valid and unmodified until the next synchronising call (tc_sync, tc_estimate*,
  *         tc_get_state) when asynchronous errors are enabled, else until this call returns.
  *  w == 0: no-op (the batch index does not advance); w > 2^28 -> TC_EINVAL.
@@ -107,6 +109,14 @@ int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out);
  * lower bound on the triangle count.  Host-only (no device work).  TC_EINVAL unless 0 < eps, 0 < delta < 1,
  * tau > 0 and m * Delta < 2^64; TC_EOVERFLOW if r does not fit 64 bits. */
 int tc_required_estimators(double eps, double delta, uint64_t m, uint64_t Delta, uint64_t tau, uint64_t *r);
+
+/* tc_closed_sum_async -- enqueue, on the handle's stream after the last pushed batch, the copy of that
+ * batch's S (exact uint64) to *S (host memory; pinned keeps the call asynchronous).  Returns without
+ * waiting: *S is valid once the stream has passed that point (tc_sync, or any synchronising call), and
+ * only if that call reports TC_OK (in asynchronous mode a rejected batch leaves garbage there).  The
+ * estimate is then m * S / r with m after that batch (tc_estimate's expression).  Lets a pipeline read
+ * every batch's result without a host synchronisation per batch. */
+int tc_closed_sum_async(tc_ctx *ctx, uint64_t *S);
 
 /* tc_group_sums -- S_g for the same contiguous groups (exact uint64, host array of `groups`). */
 int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g);

@@ -142,6 +142,19 @@ class TriangleCounter:
         self._ck(_lib.load().tc_closed_sum(self._h, C.byref(out)), "tc_closed_sum")
         return int(out.value)
 
+    def closed_sum_async(self, buf, index: int = 0):
+        """tc_closed_sum_async: enqueue the copy of the last batch's S into buf[index] (a pinned host torch
+        int64 tensor, or a numpy uint64/int64 array); valid after the next successful sync."""
+        if type(buf).__module__.startswith("torch"):
+            if buf.device.type != "cpu" or buf.element_size() != 8:
+                raise TypeError("buf must be a host 8-byte tensor")
+            ptr = buf.data_ptr() + 8 * int(index)
+        else:
+            if buf.dtype.itemsize != 8:
+                raise TypeError("buf must hold 8-byte integers")
+            ptr = buf.ctypes.data + 8 * int(index)
+        self._ck(_lib.load().tc_closed_sum_async(self._h, C.c_void_p(ptr)), "tc_closed_sum_async")
+
     def estimate_mom(self, groups: int) -> float:
         out = C.c_double()
         self._ck(_lib.load().tc_estimate_mom(self._h, int(groups), C.byref(out)), "tc_estimate_mom")

@@ -31,6 +31,9 @@ struct tc_ctx {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;   // second stream: the edge-pair table, concurrently with the vertex buckets
     cudaStream_t side2 = nullptr;  // third stream: the large vertex buckets
+    cudaStream_t copy = nullptr;   // host-batch uploads, so batch b+1's H2D overlaps batch b's kernels
+    cudaEvent_t copied[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+    int stage_next = 0;            // staging buffer of the next host batch
     cudaEvent_t fork = nullptr, join = nullptr, fork2 = nullptr, join2 = nullptr;
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
@@ -70,7 +73,7 @@ static int fail_cuda(tc_ctx *c) {
 
 static void free_index(IndexBufs &ix) {
     void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
-                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage};
+                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
 }
@@ -85,6 +88,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     CK(cudaStreamSynchronize(ctx->stream));
     CK(cudaStreamSynchronize(ctx->side));
     CK(cudaStreamSynchronize(ctx->side2));
+    CK(cudaStreamSynchronize(ctx->copy));
     free_index(ctx->ix);
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
@@ -100,7 +104,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
          cudaMalloc(&ix.cntV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.offV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
-         cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess;
+         cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess &&
+         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);
@@ -133,6 +138,11 @@ static void destroy_ctx(tc_ctx *ctx) {
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->side2) cudaStreamDestroy(ctx->side2);
+    if (ctx->copy) cudaStreamDestroy(ctx->copy);
+    for (int i = 0; i < 2; ++i) {
+        if (ctx->copied[i]) cudaEventDestroy(ctx->copied[i]);
+        if (ctx->stage_free[i]) cudaEventDestroy(ctx->stage_free[i]);
+    }
     if (ctx->join2) cudaEventDestroy(ctx->join2);
     if (ctx->fork2) cudaEventDestroy(ctx->fork2);
     if (ctx->fork) cudaEventDestroy(ctx->fork);
@@ -186,6 +196,11 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
     bool ok = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) == cudaSuccess &&
               cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->copied[0], cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->copied[1], cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->stage_free[0], cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->stage_free[1], cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->join2, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->fork2, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming) == cudaSuccess &&
@@ -279,15 +294,20 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
                            attr.device == ctx->device;
     if (attr.type == cudaMemoryTypeDevice && attr.device != ctx->device) return TC_EINVAL;
     IndexBufs &ix = ctx->ix;
+    int sb = -1;  // staging buffer used by this push (host input)
     if (on_device) {
         in = reinterpret_cast<const uint2 *>(edges);
     } else {
-        CK(cudaMemcpyAsync(ix.stage, edges, 8 * w, cudaMemcpyHostToDevice, ctx->stream));
-        if (attr.type == cudaMemoryTypeHost) {  // pinned: wait so the caller may reuse the buffer
-            CK(cudaEventRecord(ctx->copy_done, ctx->stream));
-            CK(cudaEventSynchronize(ctx->copy_done));
-        }
-        in = ix.stage;
+        // upload on the copy stream into the staging buffer the push before last used (its kernels are done
+        // with it: stage_free), so the copy overlaps the previous batch's kernels; the main stream waits
+        sb = ctx->stage_next;
+        uint2 *dst = sb ? ix.stage2 : ix.stage;
+        CK(cudaStreamWaitEvent(ctx->copy, ctx->stage_free[sb], 0));
+        CK(cudaMemcpyAsync(dst, edges, 8 * w, cudaMemcpyHostToDevice, ctx->copy));
+        CK(cudaEventRecord(ctx->copied[sb], ctx->copy));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->copied[sb], 0));
+        if (attr.type == cudaMemoryTypeHost) CK(cudaEventSynchronize(ctx->copied[sb]));  // pinned: the caller may reuse it
+        in = dst;
     }
     const int slot = (int)((ctx->b + 1) & 1u);
     BatchArgs a;
@@ -386,6 +406,10 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     }
     if (ctx->prof) ++ctx->ev_used;
     CK(cudaGetLastError());
+    if (sb >= 0) {
+        CK(cudaEventRecord(ctx->stage_free[sb], ctx->stream));
+        ctx->stage_next = sb ^ 1;
+    }
     if (!ctx->async_errors) {
         CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -469,6 +493,18 @@ int tc_estimate(tc_ctx *ctx, double *out) {
     int rc = tc_closed_sum(ctx, &S);
     if (rc != TC_OK) return rc;
     *out = (double)ctx->m * (double)S / (double)ctx->r;  // reading R9: one fixed fp64 expression
+    return TC_OK;
+}
+
+int tc_closed_sum_async(tc_ctx *ctx, uint64_t *S) {
+    if (!ctx || !S) return TC_EINVAL;
+    if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->S_slot < 0) {
+        *S = 0;
+        return TC_OK;
+    }
+    CK(cudaMemcpyAsync(S, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToHost, ctx->stream));
     return TC_OK;
 }
 

@@ -29,7 +29,8 @@ struct IndexBufs {
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
     uint32_t *vstart = nullptr;    // [4097] vertex-bucket totals -> exclusive prefix
     uint32_t *ctr = nullptr;       // device counters (index.cuh kCtr*)
-    uint2 *stage = nullptr;        // [wcap] H2D staging for host batches
+    uint2 *stage = nullptr;        // [wcap] H2D staging for host batches (two buffers, alternating)
+    uint2 *stage2 = nullptr;
 };
 
 struct StateBufs {

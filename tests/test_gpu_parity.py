@@ -250,3 +250,36 @@ def test_graph_and_plain_launches_agree():
         assert o.push_batch(s[k:k + w]) == 0
         k += w
     assert_states_equal(out[0], o.state(), "graph vs oracle")
+
+
+def test_async_host_uploads_and_closed_sum_async():
+    """Host batches in asynchronous mode go through the two alternating staging buffers on the copy stream
+    (the upload of batch b+1 overlaps batch b's kernels); mixing pinned, pageable and device batches, with
+    and without graphs, must leave the oracle's state, and tc_closed_sum_async must return every batch's S."""
+    from paper_1308_2166_b200 import TriangleCounter
+    from oracle.indexed import IndexedOracle
+    s = rmat(13, 16, 5)
+    ws = [3000, 5000, 1, 4096, 2500, 6000, 4096, 4096, 777]
+    pinned = torch.from_numpy(s.view(np.int32)).pin_memory()
+    dev = torch.from_numpy(s.view(np.int32)).cuda()
+    o = IndexedOracle(3000, 21)
+    ref_S = []
+    k = 0
+    for w in ws:
+        assert o.push_batch(s[k:k + w]) == 0
+        ref_S.append(o.closed_sum())
+        k += w
+    for graphs in (True, False):
+        tc = TriangleCounter(3000, 21)
+        tc.set_async(True)
+        tc.set_graphs(graphs)
+        Sbuf = torch.zeros(len(ws), dtype=torch.int64).pin_memory()
+        k = 0
+        for i, w in enumerate(ws):
+            src = (pinned, s, pinned, dev)[i % 4]
+            tc.push_batch(src[k:k + w])
+            tc.closed_sum_async(Sbuf, i)
+            k += w
+        assert tc.sync() == 0
+        assert Sbuf.tolist() == ref_S
+        assert_states_equal(tc.state(), o.state(), f"async uploads graphs={graphs}")
