@@ -155,18 +155,19 @@ def committed_traffic(config):
 
 
 # --------------------------------------------------------------------------------------------------
-def algorithmic_bytes(phase, w, R, D, fresh, r2old):
+def algorithmic_bytes(phase, w, R, D, fresh, r2old, skipped=0):
     """Algorithmic bytes per launch: what each phase must move at minimum.
 
     update    : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 28 B per fresh one
                 (write cf 4, r1 8, p1 4, r2 8, p2 4), +12 B per retained estimator whose f2 is replaced
-                (r2, p2); the index probes are not counted (the byte model of SURVEY §8d).
+                (r2, p2); 20 B (no write) per estimator the small-batch pass skips as untouched; the index
+                probes are not counted (the byte model of SURVEY §8d).
     partition : read the batch once 8 B/edge; write E 8, the two bucketed arcs 16, the bucketed edge 16 B/edge.
     pairs     : read the bucketed edge 16 B, write its 2 table slots 16 B.
     vertices  : read the two bucketed arcs 16 B, write segS 8 + einfo 16 B per edge; 32 B (2 slots) per vertex.
     """
     if phase == "update":
-        return 24 * (R - fresh) + 28 * fresh + 12 * r2old
+        return 24 * (R - fresh) + 28 * fresh + 12 * r2old - 4 * skipped
     if phase == "partition":
         return 48 * w
     if phase == "pairs":
@@ -251,7 +252,7 @@ def run_b200(args):
         tc.profile(profile)
         evs, launches, edges = [], 0, 0
         prof = {}
-        stats = {"fresh": 0, "r2_replaced_retained": 0, "vertices": 0}
+        stats = {"fresh": 0, "r2_replaced_retained": 0, "vertices": 0, "skipped": 0}
 
         def harvest():
             if profile:
@@ -307,7 +308,8 @@ def run_b200(args):
     peak, peak_src = measured_peaks()
     nsteps = nb
     alg = {
-        "update": algorithmic_bytes("update", 0, count * nsteps, 0, stats["fresh"], stats["r2_replaced_retained"]),
+        "update": algorithmic_bytes("update", 0, count * nsteps, 0, stats["fresh"], stats["r2_replaced_retained"],
+                                    stats["skipped"]),
         "partition": algorithmic_bytes("partition", prof_edges, 0, 0, 0, 0),
         "pairs": algorithmic_bytes("pairs", prof_edges, 0, 0, 0, 0),
         "vertices": algorithmic_bytes("vertices", prof_edges, 0, stats["vertices"], 0, 0),
@@ -319,6 +321,7 @@ def run_b200(args):
                 "traffic": committed_traffic(args.config), "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": alg["update"] / max(1, nsteps),
                 "launch_ms": prof["update"][0] / max(1, nsteps),
+                "small_batch_skipped_frac": stats["skipped"] / max(1, count * nsteps),
                 "phases": {p: {"ms_per_step": prof[p][0] / max(1, nsteps), "launches_per_step": prof[p][1] / max(1, nsteps),
                                "algorithmic_GBps": ach.get(p), "frac": (ach[p] / peak) if ach.get(p) else None}
                            for p in prof}}

@@ -148,8 +148,13 @@ int tc_set_graphs(tc_ctx *ctx, int enable);
  *                        path for up to 4095 remaining arcs, else a radix sort on the vertex hash)
  *  TC_TUNE_VBUCKET_SORT_CAP  large-bucket kernel: buckets with more arcs than this (1..6144, default 6144)
  *                        are sorted in chunks through global memory instead of in shared memory
+ *  TC_TUNE_SMALL_BATCH   the estimator pass for small batches: 0 = auto (default; batches
+ *                        of at most 16384 edges), 1 = never, 2 = always.  It reads r1, r2, chi of every
+ *                        estimator, tests them against two bit filters of the batch (its vertices, its edge
+ *                        pairs; no false negatives) and runs Steps 1-3 only for estimators whose f1 is
+ *                        replaced or that the batch can touch, writing only the fields that change.
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
-enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4 };
+enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6 };
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
 
 /* tc_sync -- wait for all queued work; returns the first asynchronous error, if any. */
@@ -174,7 +179,8 @@ int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n);
 
 /* tc_stats -- event counts since the last tc_profile() call (for the bench's byte model):
  * out[0] estimators whose f1 was replaced, out[1] retained-f1 estimators whose f2 was replaced,
- * out[2] sum over batches of the number of distinct vertices in W, out[3] batches.  Returns 4. */
+ * out[2] sum over batches of the number of distinct vertices in W, out[3] batches, out[4] estimators the
+ * small-batch pass skipped as untouched (TC_TUNE_SMALL_BATCH).  Returns 5. */
 int tc_stats(tc_ctx *ctx, uint64_t *out, int n);
 
 /* Number of kernel launches issued by the last successful push (for the bench's gpu_launches). */

@@ -218,12 +218,12 @@ class TriangleCounter:
         return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(PHASES)}
 
     def stats(self) -> dict:
-        out = np.zeros(4, np.uint64)
-        rc = _lib.load().tc_stats(self._h, out.ctypes.data_as(C.c_void_p), 4)
+        out = np.zeros(5, np.uint64)
+        rc = _lib.load().tc_stats(self._h, out.ctypes.data_as(C.c_void_p), 5)
         if rc < 0:
             raise TCError(rc, "tc_stats")
         return {"fresh": int(out[0]), "r2_replaced_retained": int(out[1]), "vertices": int(out[2]),
-                "batches": int(out[3])}
+                "batches": int(out[3]), "skipped": int(out[4])}
 
     def last_launches(self) -> int:
         out = C.c_uint32()

@@ -73,7 +73,7 @@ static int fail_cuda(tc_ctx *c) {
 
 static void free_index(IndexBufs &ix) {
     void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
-                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2};
+                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2, ix.filt};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
 }
@@ -105,7 +105,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
          cudaMalloc(&ix.offV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
          cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess &&
-         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess;
+         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess && cudaMalloc(&ix.filt, 8ull * kFilterWords) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);
@@ -208,12 +208,12 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
               cudaMalloc(&ctx->st.r1, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.r2, 8 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 4 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.p2, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
-              cudaMalloc(&ctx->st.stats, 32) == cudaSuccess &&
+              cudaMalloc(&ctx->st.stats, 40) == cudaSuccess &&
               cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess;
     if (ok) {
         ok = cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream) == cudaSuccess &&
-             cudaMemsetAsync(ctx->st.stats, 0, 32, ctx->stream) == cudaSuccess;
+             cudaMemsetAsync(ctx->st.stats, 0, 40, ctx->stream) == cudaSuccess;
         launch_init_state(ctx->st, ctx->stream);
         ok = ok && cudaGetLastError() == cudaSuccess;
     }
@@ -318,6 +318,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.seed = ctx->seed;
     a.S_slot = slot;
     a.g = make_geometry((uint32_t)w, ctx->tune);
+    a.small = ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax);
     if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
         CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
         ctx->ptag = 1;
@@ -443,6 +444,10 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
         case TC_TUNE_VBUCKET_CAP:
             if (value < 1 || value > 2048) return TC_EINVAL;
             ctx->tune.vcap = (uint32_t)value;
+            return TC_OK;
+        case TC_TUNE_SMALL_BATCH:
+            if (value > 2) return TC_EINVAL;
+            ctx->tune.small = (uint32_t)value;
             return TC_OK;
         case TC_TUNE_VBUCKET_SORT_CAP:
             if (value < 1 || value > kVChunk) return TC_EINVAL;
@@ -603,7 +608,7 @@ int tc_profile(tc_ctx *ctx, int enable) {
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     ctx->prof = enable ? 1 : 0;
-    CK(cudaMemsetAsync(ctx->st.stats, 0, 32, ctx->stream));
+    CK(cudaMemsetAsync(ctx->st.stats, 0, 40, ctx->stream));
     for (int p = 0; p < TC_NPHASES; ++p) {
         ctx->prof_ms[p] = 0;
         ctx->prof_launch[p] = 0;
@@ -626,10 +631,10 @@ int tc_stats(tc_ctx *ctx, uint64_t *out, int n) {
     if (!ctx || !out) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
-    unsigned long long v[4];
-    CK(cudaMemcpy(v, ctx->st.stats, 32, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < n && i < 4; ++i) out[i] = v[i];
-    return 4;
+    unsigned long long v[5];
+    CK(cudaMemcpy(v, ctx->st.stats, 40, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
+    return 5;
 }
 
 int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {

@@ -106,6 +106,7 @@ struct PartArgs {
     uint2 *pt;         // edge-pair table (G groups of 4 slots)
     uint32_t G, ptag;
     uint32_t *ctr;
+    uint32_t *filt;    // small batches: vertex and pair filters to fill (else null)
 };
 
 // a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
@@ -145,7 +146,17 @@ __global__ void __launch_bounds__(256) k_pairs(PartArgs a) {
     bool dup = false;
     if (k < a.g.w) {
         const uint2 e = __ldg(a.in + k);
-        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) dup = pt_insert(a, norm_edge(e), k);  // k_count reports the rest
+        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // k_count reports the rest
+            const uint2 n = norm_edge(e);
+            dup = pt_insert(a, n, k);
+            if (a.filt) {
+                const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
+                const uint32_t b2 = pfilter_bit(hash_pair64(pair_key(n.x, n.y)));
+                atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
+                atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
+                atomicOr(a.filt + kFilterWords + (b2 >> 5), 1u << (b2 & 31u));
+            }
+        }
     }
     if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
 }
@@ -1177,21 +1188,29 @@ struct UpdateArgs {
     uint64_t m_prev;
 };
 
+template <bool kSmall>
 __device__ __forceinline__ EstState load_state(const UpdateArgs &u, uint64_t t) {
     EstState e;
     e.r1 = __ldcs(u.r1s + t);
     e.cf = __ldcs(u.cfs + t);
     e.r2 = __ldcs(u.r2s + t);
-    e.p1 = __ldcs(u.p1s + t);
-    e.p2 = __ldcs(u.p2s + t);
+    if (!kSmall) {  // the small-batch pass writes p1 / p2 only when it replaces them: it never reads them
+        e.p1 = __ldcs(u.p1s + t);
+        e.p2 = __ldcs(u.p2s + t);
+    } else {
+        e.p1 = e.p2 = 0u;
+    }
     return e;
 }
+
+__device__ __forceinline__ bool filter_has(const uint32_t *f, uint32_t bit) { return (f[bit >> 5] >> (bit & 31u)) & 1u; }
 
 // Steps 1-3 for estimator t (local index) whose state was read into `old`.  Returns chi if it ends closed.
 // Written straight-line: the loads of the fresh-f1 and retained-f1 paths are predicated, not branched, so
 // a warp with both kinds of lanes waits for one round trip, not two.
+template <bool kSmall>
 __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const UpdateIdx &ix, uint64_t t, const EstState &old,
-                                               uint32_t &n_fresh, uint32_t &n_r2old) {
+                                               uint32_t &n_fresh, uint32_t &n_r2old, uint32_t &n_skip, const uint32_t *sf) {
     const uint64_t gid = u.first + t;
     const DrawCtx dc{gid, u.batch, PhiloxKey{(uint32_t)u.seed, (uint32_t)(u.seed >> 32)}};
     const uint4 o = philox4x32_10(make_uint4((uint32_t)gid, (uint32_t)(gid >> 32), u.batch, 0u), dc.key);
@@ -1203,6 +1222,22 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
     const uint64_t d1 = bounded(m_prev + u.w, xlo, dc, 0x10000u);
     const bool fresh = d1 >= m_prev;
     const uint32_t j = fresh ? (uint32_t)(d1 - m_prev) : 0u;
+    if (kSmall && !fresh) {
+        // a retained f1 changes only if the batch has an arc at one of its endpoints (chi^+ > 0) or the closing
+        // edge of an open wedge (Step 3); with neither, the state is untouched and nothing is written
+        const uint32_t c0 = old.cf & kCMask;
+        const bool cl0 = (old.cf & kClosedBit) != 0;
+        bool touched = filter_has(sf, vfilter_bit(hash_vertex(old.r1.x))) || filter_has(sf, vfilter_bit(hash_vertex(old.r1.y)));
+        if (!touched && c0 > 0 && !cl0) {
+            const uint2 a = old.r1, b = old.r2;
+            const uint32_t x = (a.x == b.x || a.x == b.y) ? a.y : a.x, z = (b.x == a.x || b.x == a.y) ? b.y : b.x;
+            touched = filter_has(sf + kFilterWords, pfilter_bit(hash_pair64(pair_key(min(x, z), max(x, z)))));
+        }
+        if (!touched) {
+            ++n_skip;
+            return cl0 ? c0 : 0u;
+        }
+    }
     // ---- Step 2a: chi^+ = rank(u->v) + rank(v->u) ----
     // fresh f1 = w_j: its ranks from einfo[j]; retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821)
     uint2 r1 = old.r1;
@@ -1280,12 +1315,24 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
         if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
     }
     const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
-    // every field rewritten: coalesced full sectors, no partial-sector read-modify-write
-    __stcs(u.cfs + t, cf_new);
-    __stcs(u.r1s + t, r1);
-    __stcs(u.r2s + t, r2);
-    __stcs(u.p1s + t, fresh ? (uint32_t)d1 : old.p1);
-    __stcs(u.p2s + t, r2new ? (uint32_t)(m_prev + k2) : fresh ? kEmptyV : old.p2);
+    if (kSmall) {  // only what changed (few estimators per batch)
+        __stcs(u.cfs + t, cf_new);
+        if (fresh) {
+            __stcs(u.r1s + t, r1);
+            __stcs(u.p1s + t, (uint32_t)d1);
+        }
+        if (fresh || r2new) {
+            __stcs(u.r2s + t, r2);
+            __stcs(u.p2s + t, r2new ? (uint32_t)(m_prev + k2) : kEmptyV);
+        }
+    } else {
+        // every field rewritten: coalesced full sectors, no partial-sector read-modify-write
+        __stcs(u.cfs + t, cf_new);
+        __stcs(u.r1s + t, r1);
+        __stcs(u.r2s + t, r2);
+        __stcs(u.p1s + t, fresh ? (uint32_t)d1 : old.p1);
+        __stcs(u.p2s + t, r2new ? (uint32_t)(m_prev + k2) : fresh ? kEmptyV : old.p2);
+    }
     n_fresh += fresh ? 1u : 0u;
     n_r2old += (r2new && !fresh) ? 1u : 0u;
     return closed ? c : 0u;
@@ -1296,20 +1343,27 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
 #ifndef TC_UPD_MINB
 #define TC_UPD_MINB 4
 #endif
+template <bool kSmall>
 __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
-                                                   unsigned long long *stats) {
+                                                   unsigned long long *stats, const uint32_t *filt) {
     if (ix.ctr[kCtrErr]) return;
+    __shared__ uint32_t sf[kSmall ? 2 * kFilterWords : 1];
+    if (kSmall) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(filt);
+        for (uint32_t i = threadIdx.x; i < 2 * kFilterWords / 4; i += blockDim.x) reinterpret_cast<uint4 *>(sf)[i] = __ldg(src + i);
+        __syncthreads();
+    }
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     unsigned long long contrib = 0;
-    uint32_t n_fresh = 0, n_r2old = 0;
+    uint32_t n_fresh = 0, n_r2old = 0, n_skip = 0;
     EstState cur;
-    if (t < u.count) cur = load_state(u, t);
+    if (t < u.count) cur = load_state<kSmall>(u, t);
     while (t < u.count) {
         const uint64_t tn = t + stride;
         EstState nxt;
-        if (tn < u.count) nxt = load_state(u, tn);
-        contrib += update_one(u, ix, t, cur, n_fresh, n_r2old);
+        if (tn < u.count) nxt = load_state<kSmall>(u, tn);
+        contrib += update_one<kSmall>(u, ix, t, cur, n_fresh, n_r2old, n_skip, sf);
         cur = nxt;
         t = tn;
     }
@@ -1319,28 +1373,32 @@ __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, Updat
         contrib += __shfl_xor_sync(kFull, contrib, off);
         n_fresh += __shfl_xor_sync(kFull, n_fresh, off);
         n_r2old += __shfl_xor_sync(kFull, n_r2old, off);
+        if (kSmall) n_skip += __shfl_xor_sync(kFull, n_skip, off);
     }
     __shared__ unsigned long long ws[8];
-    __shared__ uint32_t wf[8], wr[8];
+    __shared__ uint32_t wf[8], wr[8], wk[8];
     if ((threadIdx.x & 31u) == 0) {
         ws[threadIdx.x >> 5] = contrib;
         wf[threadIdx.x >> 5] = n_fresh;
         wr[threadIdx.x >> 5] = n_r2old;
+        wk[threadIdx.x >> 5] = n_skip;
     }
     __syncthreads();
     if (threadIdx.x < 8) {
         unsigned long long v = ws[threadIdx.x];
-        uint32_t f = wf[threadIdx.x], q = wr[threadIdx.x];
+        uint32_t f = wf[threadIdx.x], q = wr[threadIdx.x], sk = wk[threadIdx.x];
 #pragma unroll
         for (int off = 4; off > 0; off >>= 1) {
             v += __shfl_xor_sync(0xffu, v, off);
             f += __shfl_xor_sync(0xffu, f, off);
             q += __shfl_xor_sync(0xffu, q, off);
+            if (kSmall) sk += __shfl_xor_sync(0xffu, sk, off);
         }
         if (threadIdx.x == 0) {
             if (v) atomicAdd(S, v);
             if (f) atomicAdd(stats + 0, (unsigned long long)f);
             if (q) atomicAdd(stats + 1, (unsigned long long)q);
+            if (kSmall && sk) atomicAdd(stats + 4, (unsigned long long)sk);
             if (blockIdx.x == 0) {
                 atomicAdd(stats + 2, (unsigned long long)ix.ctr[kCtrD]);
                 atomicAdd(stats + 3, 1ull);
@@ -1411,7 +1469,8 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr};
+    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr,
+                    a.small ? ix.filt : nullptr};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
@@ -1430,6 +1489,7 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+    if (a.small && cudaMemsetAsync(ix.filt, 0, 8ull * kFilterWords, s) != cudaSuccess) return 0;
     k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
     return 1;
 }
@@ -1455,7 +1515,11 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
     if (st.count == 0) return 0;
     UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), a.ptag}, ix.einfo, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
-    k_update<<<grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves), 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats);
+    const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
+    if (a.small)
+        k_update<true><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, ix.filt);
+    else
+        k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, nullptr);
     return 1;
 }
 

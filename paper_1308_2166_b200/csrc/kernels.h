@@ -29,6 +29,7 @@ struct IndexBufs {
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
     uint32_t *vstart = nullptr;    // [4097] vertex-bucket totals -> exclusive prefix
     uint32_t *ctr = nullptr;       // device counters (index.cuh kCtr*)
+    uint32_t *filt = nullptr;      // [2 kFilterWords] small-batch filters: vertices, then edge pairs
     uint2 *stage = nullptr;        // [wcap] H2D staging for host batches (two buffers, alternating)
     uint2 *stage2 = nullptr;
 };
@@ -39,7 +40,8 @@ struct StateBufs {
     uint32_t *cf = nullptr;  // chi in bits 0..30, closed flag in bit 31
     uint32_t *p1 = nullptr, *p2 = nullptr;  // 0-based global positions (< 2^31, reading R13); 0xFFFFFFFF = empty
     unsigned long long *S = nullptr;      // [2] closed-sum accumulators (double-buffered by batch parity)
-    unsigned long long *stats = nullptr;  // [4] fresh f1, replaced f2 of retained f1, sum of D, batches
+    unsigned long long *stats = nullptr;  // [5] fresh f1, replaced f2 of retained f1, sum of D, batches,
+                                          // estimators the small-batch pass skipped
 };
 
 // Bucket geometry of one batch (host-computed from w and the tuning knobs).
@@ -61,10 +63,15 @@ struct BatchArgs {
     uint64_t seed;
     int S_slot;
     uint32_t ptag;    // edge-pair table tag of this push (1..254)
+    bool small;       // small-batch estimator pass (filters built by k_pairs, k_update skips untouched estimators)
     Geometry g;
 };
 
+// Batches of at most this many edges take the filtered small-batch estimator pass (filter load <= 1/4)
+constexpr uint32_t kSmallBatchMax = kFilterBits / 8;
+
 struct Tuning {
+    uint32_t small = 0;            // 0 auto (w <= kSmallBatchMax), 1 never, 2 always
     uint32_t vbucket_arcs = 1024;  // target arcs per vertex bucket
     uint32_t vcap = 2048;
     uint32_t sortcap = kVChunk;

@@ -105,6 +105,8 @@ def test_hub_segments_multi_chunk():
     dict(vbucket_arcs=1),                          # 2^15 buckets: 4096 partition buckets split 8 ways (k_split)
     dict(vbucket_arcs=2, vbucket_cap=3),           # split + most sub-buckets through the large-bucket kernels
     dict(vbucket_arcs=1 << 30),                    # one vertex bucket
+    dict(small_batch=1),                           # the full estimator pass even for small batches
+    dict(small_batch=2),                           # the filtered small-batch pass even for large batches
 ])
 def test_index_geometry_knobs(knobs):
     """Results never depend on the index geometry (tc_tune): bit-exact against the oracle."""
@@ -283,3 +285,29 @@ def test_async_host_uploads_and_closed_sum_async():
         assert tc.sync() == 0
         assert Sbuf.tolist() == ref_S
         assert_states_equal(tc.state(), o.state(), f"async uploads graphs={graphs}")
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_small_batch_pass_long_stream(mode):
+    """Many small batches through many estimators (the regime of the filtered pass): the
+    filtered pass (mode 2, also the default at these sizes) and the full pass (mode 1) both equal the
+    oracle bit for bit, including the closed sums after every batch."""
+    from paper_1308_2166_b200 import TriangleCounter
+    s = rmat(12, 16, 8)[:30000]
+    r, w = 20000, 512
+    tc = TriangleCounter(r, 3)
+    tc.tune(small_batch=mode)
+    tc.set_async(True)
+    Sbuf = torch.zeros(len(range(0, len(s), w)), dtype=torch.int64).pin_memory()
+    for i, k in enumerate(range(0, len(s), w)):
+        tc.push_batch(s[k:k + w])
+        tc.closed_sum_async(Sbuf, i)
+    assert tc.sync() == 0
+    from oracle.indexed import IndexedOracle
+    o = IndexedOracle(r, 3)
+    ref = []
+    for k in range(0, len(s), w):
+        assert o.push_batch(s[k:k + w]) == 0
+        ref.append(o.closed_sum())
+    assert Sbuf.tolist() == ref
+    assert_states_equal(tc.state(), o.state(), f"small-batch mode {mode}")
