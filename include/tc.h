@@ -149,7 +149,7 @@ int tc_set_graphs(tc_ctx *ctx, int enable);
  *  TC_TUNE_VBUCKET_SORT_CAP  large-bucket kernel: buckets with more arcs than this (1..6144, default 6144)
  *                        are sorted in chunks through global memory instead of in shared memory
  *  TC_TUNE_SMALL_BATCH   the estimator pass for small batches: 0 = auto (default; batches
- *                        of at most 16384 edges), 1 = never, 2 = always.  It reads r1, r2, chi of every
+ *                        of at most 8192 edges), 1 = never, 2 = always.  It reads r1, r2, chi of every
  *                        estimator, tests them against two bit filters of the batch (its vertices, its edge
  *                        pairs; no false negatives) and runs Steps 1-3 only for estimators whose f1 is
  *                        replaced or that the batch can touch, writing only the fields that change.

@@ -67,8 +67,8 @@ struct BatchArgs {
     Geometry g;
 };
 
-// Batches of at most this many edges take the filtered small-batch estimator pass (filter load <= 1/4)
-constexpr uint32_t kSmallBatchMax = kFilterBits / 8;
+// Batches of at most this many edges take the filtered small-batch estimator pass (filter load <= 1/8)
+constexpr uint32_t kSmallBatchMax = kFilterBits / 16;  // 8192: measured break-even ~16384 on C5
 
 struct Tuning {
     uint32_t small = 0;            // 0 auto (w <= kSmallBatchMax), 1 never, 2 always
