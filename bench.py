@@ -154,6 +154,31 @@ def committed_traffic(config):
     return None
 
 
+def committed_limiters(kernel="k_update"):
+    """What bounds the dominant kernel besides HBM, from the committed `ncu --set full` summary
+    (profiles/ncu_full_r01.json): L2 throughput, issue activity, occupancy and the top stall reason."""
+    p = os.path.join(ROOT, "profiles", "ncu_full_r01.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        rows = [x for x in json.load(f) if x.get("kernel") == kernel]
+    if not rows:
+        return None
+    x = rows[-1]
+
+    def num(k):
+        try:
+            return float(str(x.get(k, "")).split()[0])
+        except (ValueError, IndexError):
+            return None
+    return {"kernel": kernel, "lts_throughput_pct": num("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
+            "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+            "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+            "warp_instructions_per_launch": num("smsp__inst_executed.sum"),
+            "top_stall": (x.get("top_stalls") or [[None]])[0][0],
+            "source": "profiles/ncu_full_r01.json (cold-L2 replay)"}
+
+
 # --------------------------------------------------------------------------------------------------
 def algorithmic_bytes(phase, w, R, D, fresh, r2old, skipped=0):
     """Algorithmic bytes per launch: what each phase must move at minimum.
@@ -322,6 +347,7 @@ def run_b200(args):
                 "algorithmic_bytes_per_launch": alg["update"] / max(1, nsteps),
                 "launch_ms": prof["update"][0] / max(1, nsteps),
                 "small_batch_skipped_frac": stats["skipped"] / max(1, count * nsteps),
+                "limiters": committed_limiters("k_update"),
                 "phases": {p: {"ms_per_step": prof[p][0] / max(1, nsteps), "launches_per_step": prof[p][1] / max(1, nsteps),
                                "algorithmic_GBps": ach.get(p), "frac": (ach[p] / peak) if ach.get(p) else None}
                            for p in prof}}
