@@ -343,28 +343,17 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
             if (ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
         }
         ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ms) == cudaSuccess;
-#ifndef TC_PAIRS_MODE
-#define TC_PAIRS_MODE 2
-#endif
-        // a3 (it reads only the raw batch): mode 0 on the second stream from the start of the batch, mode 1
-        // on the main stream after the partition, mode 2 on the second stream alongside the vertex phase
-        auto pairs_on = [&](cudaStream_t st, bool fork_from_main) {
-            if (fork_from_main) {
-                ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
-                ok = ok && cudaStreamWaitEvent(st, ctx->fork, 0) == cudaSuccess;
-            }
-            rec(2 * TC_PHASE_PAIRS, st);
-            launches += launch_pairs(ix, a, st);
-            rec(2 * TC_PHASE_PAIRS + 1, st);
-            if (st != ms) ok = ok && cudaEventRecord(ctx->join, st) == cudaSuccess;
-        };
-        if (TC_PAIRS_MODE == 0) pairs_on(ss, true);
         // a1: count, scans, scatter
         rec(2 * TC_PHASE_PARTITION, ms);
         launches += launch_partition(ix, a, ms);
         rec(2 * TC_PHASE_PARTITION + 1, ms);
-        if (TC_PAIRS_MODE == 1) pairs_on(ms, false);
-        if (TC_PAIRS_MODE == 2) pairs_on(ss, true);
+        // a3 (it reads only the raw batch) on the second stream, alongside the vertex phase
+        ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
+        ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
+        rec(2 * TC_PHASE_PAIRS, ss);
+        launches += launch_pairs(ix, a, ss);
+        rec(2 * TC_PHASE_PAIRS + 1, ss);
+        ok = ok && cudaEventRecord(ctx->join, ss) == cudaSuccess;
         ok = ok && cudaEventRecord(ctx->fork2, ms) == cudaSuccess;
         // a2: the large vertex buckets on the third stream, the common ones on the main stream
         ok = ok && cudaStreamWaitEvent(s2, ctx->fork2, 0) == cudaSuccess;
@@ -374,7 +363,6 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         launches += launch_vertices(ix, a, ms);
         ok = ok && cudaStreamWaitEvent(ms, ctx->join2, 0) == cudaSuccess;
         rec(2 * TC_PHASE_VERTICES + 1, ms);
-        if (TC_PAIRS_MODE != 1)
         ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
         rec(2 * TC_PHASE_UPDATE, ms);
         launches += launch_update(ix, ctx->st, a, ms);

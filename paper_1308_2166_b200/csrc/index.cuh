@@ -104,9 +104,6 @@ __host__ __device__ __forceinline__ uint32_t pgroup_start(uint64_t h, uint32_t g
 // Probe sequence of a pair over the G groups: its home group A, a second independent group B, then
 // A+1, A+2, ... (a key sits in the first group of its sequence that had room when it was inserted).
 __host__ __device__ __forceinline__ uint32_t pgroup_second(uint64_t h, uint32_t groups, uint32_t A) {
-#ifdef TC_PT_SINGLE
-    return A + 1 == groups ? 0u : A + 1;  // plain linear probing over groups
-#endif
     const uint32_t B = (uint32_t)(((uint64_t)hash_vertex((uint32_t)(h >> 32) ^ 0x9E3779B9u) * groups) >> 32);
     return (B != A || groups == 1) ? B : (A + 1 == groups ? 0u : A + 1);
 }
@@ -163,14 +160,14 @@ static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uin
     }
 }
 
-// Pair probe split in two so that its loads can be issued together with other probes:
-// pt_issue() reads the bucket's group range and the home group (one 32-byte sector); pt_resolve() scans
-// it and walks on group by group.  Inside a group the filled slots form a prefix, so the first empty slot
+// Pair probe split in two so that its load can be issued together with other probes: pt_issue() reads
+// the home group A (one 32-byte sector); pt_resolve() scans it and, only when A is full (rare at load
+// 1/3), goes on to B, A+1, ...  Inside a group the filled slots form a prefix, so the first empty slot
 // ends the search.  Result: batch position of {lo, hi} (lo < hi), or -1.
 struct PairProbe {
     uint32_t lo, hi, fp, A, B, ng;
     const uint2 *sl;
-    uint4 a0, a1, b0, b1;  // groups A and B, read together
+    uint4 a0, a1;  // group A
 };
 
 __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t hi, bool active, PairProbe &P) {
@@ -183,16 +180,11 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
     P.sl = L.pt;  // 32-byte aligned
     P.A = ng ? pgroup_start(h, ng) : 0u;
     P.B = ng ? pgroup_second(h, ng, P.A) : 0u;
-    P.a0 = P.a1 = P.b0 = P.b1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
+    P.a0 = P.a1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
     if (ng) {
         const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
         P.a0 = __ldg(qa);
         P.a1 = __ldg(qa + 1);
-#if !defined(TC_PT_SINGLE) && defined(TC_PT_EAGER_B)
-        const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
-        P.b0 = __ldg(qb);
-        P.b1 = __ldg(qb + 1);
-#endif
     }
 }
 
@@ -227,21 +219,13 @@ __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &
     if (P.ng == 0) return -1;
     uint32_t k;
     int r = pt_group(L, P, P.a0, P.a1, &k);
-#if defined(TC_PT_SINGLE)
-    if (r == 2) return pt_walk(L, P);  // walks from the second group of the sequence
-#elif !defined(TC_PT_EAGER_B)
     if (r == 2) {  // group A full (rare at load 1/3): read B now
         const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
         r = pt_group(L, P, __ldg(qb), __ldg(qb + 1), &k);
-        if (r == 0) return -1;
-        if (r == 1) return (int64_t)k;
-        return pt_walk(L, P);
+        if (r == 2) return pt_walk(L, P);
     }
-#endif
-    if (r == 2) r = pt_group(L, P, P.b0, P.b1, &k);
     if (r == 0) return -1;
-    if (r == 1) return (int64_t)k;
-    return pt_walk(L, P);
+    return (int64_t)k;
 }
 
 __device__ __forceinline__ int64_t pt_find(const Lookup &L, uint32_t lo, uint32_t hi) {

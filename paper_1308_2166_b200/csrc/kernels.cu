@@ -914,11 +914,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         for (int j = 0; j < R; ++j) {
             const uint32_t d = (pk[j] >> 16) - l0;
             const bool in = pk[j] != 0xFFFFFFFFu && d < nd;
-#ifdef TC_VHASH_BALLOT
-            const uint32_t peers = digit_peers(d, in, bits);
-#else
             const uint32_t peers = match_peers(d, in);
-#endif
             const uint32_t before = __popc(peers & lt);
             uint32_t c = 0;
             if (in) c = whist[warp * nd + d];
