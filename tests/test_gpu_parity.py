@@ -202,13 +202,20 @@ def test_C2_full_size_sampled_and_properties():
     """BASELINE.json configs[1] at full size in the bench's launch configuration (r = w = 2^20):
     two estimator shards (the first and last 2048 ids) bit-exact against the oracle; NBSI properties
     on every estimator; aggregate to 1e-12 against a naive fp64 sum."""
+    from paper_1308_2166_b200 import TriangleCounter
     s = rmat(20, 16, 1)
     r = w = 1 << 20
-    g = gpu_run(s, r, 42, w, device_input=True, w_max_hint=w)
+    g = TriangleCounter(r, 42, w_max_hint=w)
+    g.set_graphs(True)  # as bench.py: one CUDA graph per push, asynchronous errors
+    g.set_async(True)
+    dev = torch.from_numpy(s.view(np.int32)).cuda()
+    for k in range(0, len(s), w):
+        g.push_batch(dev[k:k + w])
+    assert g.sync() == 0
     st = g.state()
     m = len(s)
     check_properties(s, st, m)
-    for first in (0, r - 2048):
+    for first in (0, r // 2 + 777, r - 2048):
         o = oracle_run(s, r, 42, w, first, 2048)
         sub = {f: st[f][first:first + 2048] for f in FIELDS}
         assert_states_equal(sub, o.state(), f"C2 shard {first}")
