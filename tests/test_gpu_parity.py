@@ -318,3 +318,33 @@ def test_small_batch_pass_long_stream(mode):
         ref.append(o.closed_sum())
     assert Sbuf.tolist() == ref
     assert_states_equal(tc.state(), o.state(), f"small-batch mode {mode}")
+
+
+def test_reset_limits_and_poison_recovery():
+    """tc_reset restores the just-created state (also clearing a poisoned handle); oversized calls are
+    rejected before touching memory (include/tc.h)."""
+    import ctypes as C
+    from paper_1308_2166_b200 import TriangleCounter, load_library
+    from paper_1308_2166_b200._lib import TC_EINVAL, TC_ESELFLOOP
+    s = rmat(11, 16, 12)
+    tc = TriangleCounter(2500, 8)
+    for k in range(0, len(s) // 2, 3000):
+        tc.push_batch(s[k:k + 3000])
+    tc.reset()
+    assert tc.counters() == (0, 0) and tc.estimate() == 0.0
+    for k in range(0, len(s), 3000):
+        tc.push_batch(s[k:k + 3000])
+    assert_states_equal(tc.state(), oracle_run(s, 2500, 8, 3000).state(), "after reset")
+    # poisoned (asynchronous error) -> reset -> usable again
+    tc.set_async(True)
+    tc.push_batch(np.array([[9, 9]], np.uint32), check=False)
+    assert tc.sync() == TC_ESELFLOOP
+    tc.reset()
+    tc.set_async(False)
+    for k in range(0, len(s), 3000):
+        tc.push_batch(s[k:k + 3000])
+    assert_states_equal(tc.state(), oracle_run(s, 2500, 8, 3000).state(), "after poisoned reset")
+    # w > 2^28 and m >= 2^31 are rejected up front
+    assert tc.push_batch_ptr(s.ctypes.data, (1 << 28) + 1) == TC_EINVAL
+    tau, ms = C.c_uint64(), C.c_double()
+    assert load_library().tc_exact_triangles(C.c_void_p(s.ctypes.data), 1 << 31, C.byref(tau), C.byref(ms)) == TC_EINVAL
