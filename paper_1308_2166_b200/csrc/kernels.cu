@@ -1,26 +1,26 @@
 // kernels.cu -- the per-batch hot path of bulkUpdateAll on sm_100a.
 //
-// Pipeline for one batch W.  Every index structure is PARTITIONED first and then built
-// bucket by bucket in shared memory, so the global tables are written whole, coalesced, and stay small
-// enough to live in L2 while the estimator pass probes them:
-//   k_pairs      a3      : (second stream, concurrently with the partition) insert every edge of the raw batch
-//                          into the edge-pair table (64-bit CAS; a repeat is TC_EDUP)
+// Pipeline for one batch W.  The incidence index is PARTITIONED first (a stable scatter of
+// the arcs into vertex-hash buckets) and then built bucket by bucket in shared memory, so the global
+// tables are written whole and coalesced, and stay small enough to live in L2 while the estimator pass
+// probes them:
 //   k_count      a1      : load W (coalesced), validate, normalise into E, stable in-tile ranks of the arcs
-//                          by vertex bucket (top bv bits of hash_vertex) and per-tile bucket counts
-//   k_scan_rows / k_scan_tot : per-(bucket, tile) offsets inside the bucket and bucket sizes, then bucket
-//                          starts (exclusive scans)
-//   k_scatter    a1      : normalise, write E; scatter the arcs (vertex, k<<1|side) to their vertex bucket,
-//                          STABLY (ballot ranks inside the tile), so each bucket holds its arcs in arrival
-//                          order -- the F array of rankAll's proof, partitioned; scatter
-//                          the edges {lo, hi, k} to their pair bucket
-//   k_pbuckets   a3      : (second stream) one CTA per pair bucket: open-addressing slice built in shared
-//                          memory, written out whole; a repeated pair is TC_EDUP
-//   k_vbuckets   a2      : one CTA per vertex bucket: stable radix sort of the bucket's arcs by vertex hash in
-//                          shared memory (replaces rankAll's sort by (src, -pos)), segment
-//                          runs -> segS, per-arc {slot, segEnd} (rank = segEnd - 1 - slot, Def. Rank
-//                          PAPER.md:589-600), vertex-table slice {deg_W, start} whose offset comes from a
-//                          decoupled look-back over the buckets; oversized buckets (hubs) take a chunked
-//                          global-memory path in the same kernel
+//                          by partition bucket (top bits of hash_vertex; one ballot per bit) and per-(bucket,
+//                          tile) counts
+//   k_scan_rows / k_scan_tot : tile offsets inside each bucket, bucket sizes and starts; the list of
+//                          oversized buckets (k_vhub's)
+//   k_scatter    a1      : arcs {vertex, k<<1|side, neighbour} to their bucket STABLY (staged in shared
+//                          memory, written as coalesced runs), so each bucket holds its arcs in arrival order
+//                          -- the F array of rankAll's proof, partitioned
+//   k_split      a1      : (w > 2^21 only) each bucket stably split again by the next hash bits
+//   k_pairs      a3      : (second stream, alongside the vertex phase) every edge of the raw batch into the
+//                          edge-pair table (64-bit CAS; a repeat is TC_EDUP); small batches also fill the
+//                          vertex / pair filters
+//   k_vhash      a2      : one CTA per vertex bucket: bucket-local vertex ids from a shared-memory hash
+//                          table, one stable ranking pass by local id (replaces rankAll's sort by (src, -pos),
+//                          PAPER.md:680-684), segment starts -> segS, per-arc {slot, segEnd} (rank = segEnd -
+//                          1 - slot, Def. Rank), the bucket's vertex-table slice {deg_W, start}
+//   k_vhub / k_vbig a2   : (third stream) oversized buckets: hub peeling + the same hash path; radix sort
 //   k_update     a4..a8  : ONE pass over the estimator SoA: Step 1 (level-1 reservoir), Step 2 (chi^+ from
 //                          ranks / degrees, level-2 pick by segment arithmetic), Step 3 (closing-edge probe),
 //                          block partial sums of chi over closed estimators
