@@ -166,3 +166,15 @@ def test_ingest_errors(tmp_path):
     with pytest.raises(TCError) as ei:
         tc3.ingest_file(str(p2), 100)
     assert ei.value.code == TC_EDUP and ei.value.stats["edges"] == 0
+
+
+@pytest.mark.gpu
+def test_ingest_empty_and_comment_only(tmp_path):
+    from paper_1308_2166_b200 import TriangleCounter
+    tc = TriangleCounter(100, 1)
+    for name, text in (("empty.txt", b""), ("comments.txt", b"# a\n% b\n\n  \n# c")):
+        p = tmp_path / name
+        p.write_bytes(text)
+        st = tc.ingest_file(str(p), 64)
+        assert st["edges"] == 0 and st["batches"] == 0 and st["error_line"] == 0
+    assert tc.counters() == (0, 0) and tc.estimate() == 0.0
