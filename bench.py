@@ -161,7 +161,7 @@ def committed_limiters(kernel="k_update"):
     if not os.path.exists(p):
         return None
     with open(p) as f:
-        rows = [x for x in json.load(f) if x.get("kernel") == kernel]
+        rows = [x for x in json.load(f) if x.get("kernel", "").split("<")[0] == kernel]
     if not rows:
         return None
     x = rows[-1]

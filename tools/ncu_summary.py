@@ -18,7 +18,8 @@ def main(path, out=None):
     hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
-        d = {"kernel": r[hdr.index("Kernel Name")].split("(")[0]}
+        name = r[hdr.index("Kernel Name")].split("(")[0]
+        d = {"kernel": name[5:] if name.startswith("void ") else name}
         for k in KEYS:
             if k in hdr:
                 d[k] = r[hdr.index(k)] + (" " + units[hdr.index(k)] if units[hdr.index(k)] else "")
