@@ -10,11 +10,13 @@
 //   2. rank(x) = (deg x, x); each edge keeps the one arc that points up in rank (the oriented graph has
 //      out-degrees <= sqrt(2m)), compacted stably, so every out-list stays sorted;
 //   3. each triangle {a, b, c} with rank a < b < c is counted exactly once, by the arc a -> b, as the
-//      element c of N+(a) ∩ N+(b); the intersection walks the shorter list and binary-searches the longer
-//      one (thread per arc; arcs whose shorter list is long go to a warp-per-arc kernel).
+//      element c of N+(a) ∩ N+(b).  Sources with long out-lists go vertex-centric: a CTA puts N+(a) into
+//      a shared-memory hash set and probes it with every N+(b), b in N+(a); the other arcs intersect by
+//      binary search, thread per arc (a warp per arc when both lists are long).
 #include <cuda_runtime.h>
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -26,6 +28,10 @@ namespace {
 constexpr uint32_t kFull = 0xFFFFFFFFu;
 constexpr uint32_t kErrInval = 1u, kErrLoop = 2u, kErrDup = 4u;
 constexpr uint32_t kHeavy = 48;  // shorter-list length above which an arc goes to the warp kernel
+constexpr uint32_t kBigDeg = 32;                       // sources with longer out-lists: vertex-centric kernel
+constexpr uint32_t kSetMax = 1u << 15;                 // largest shared-memory set (slots; 128 KB)
+constexpr uint32_t kSetDegMax = kSetMax / 4 * 3;       // ... holds out-lists up to load 3/4
+constexpr int kVThreads = 512;
 constexpr int kThreads = 256;
 
 inline uint32_t grid_for(uint64_t n, int per_sm_ctas = 8) {
@@ -164,6 +170,7 @@ __global__ void __launch_bounds__(kThreads) kx_count(const uint32_t *__restrict_
         const uint32_t a = src[q], x = adj[q];
         const uint32_t a0 = offp[a], a1 = offp[a + 1], x0 = offp[x], x1 = offp[x + 1];
         const uint32_t na = a1 - a0, nx = x1 - x0;
+        if (na > kBigDeg && na <= kSetDegMax) continue;  // kx_count_vertex's source
         if (min(na, nx) > kHeavy) {
             heavy[atomicAdd(nheavy, 1u)] = (uint32_t)q;
             continue;
@@ -187,6 +194,76 @@ __global__ void __launch_bounds__(kThreads) kx_count_heavy(const uint32_t *__res
         const uint32_t a0 = offp[a], a1 = offp[a + 1], x0 = offp[x], x1 = offp[x + 1];
         const uint32_t na = a1 - a0, nx = x1 - x0;
         c += na <= nx ? count_in(adj + a0, na, adj + x0, nx, lane, 32) : count_in(adj + x0, nx, adj + a0, na, lane, 32);
+    }
+    c = __reduce_add_sync(kFull, c);
+    if (lane == 0 && c) atomicAdd(tau, (unsigned long long)c);
+}
+
+// the sources kx_count_vertex takes (kBigDeg < out-degree <= kSetDegMax), and the largest out-degree
+__global__ void __launch_bounds__(kThreads) kx_bigsrc(const uint32_t *__restrict__ offp, const uint32_t *__restrict__ pD,
+                                                      uint32_t *__restrict__ list, uint32_t *w) {
+    const uint32_t D = *pD;
+    uint32_t mx = 0;
+    for (uint64_t v = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; v < D; v += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t deg = offp[v + 1] - offp[v];
+        mx = max(mx, deg);
+        if (deg > kBigDeg && deg <= kSetDegMax) list[atomicAdd(&w[6], 1u)] = (uint32_t)v;
+    }
+    mx = __reduce_max_sync(kFull, mx);
+    if ((threadIdx.x & 31u) == 0) atomicMax(&w[7], mx);
+}
+
+// CTA per listed source a (taken by ticket): N+(a) into a shared-memory hash set, then warps over x in N+(a)
+// and lanes over N+(x), counting the members (or, when N+(x) is much the longer list, binary-searching
+// N+(a)'s members in it) -- every triangle whose lowest vertex is a, once.
+__global__ void __launch_bounds__(kVThreads) kx_count_vertex(const uint32_t *__restrict__ adj, const uint32_t *__restrict__ offp,
+                                                             const uint32_t *__restrict__ list, uint32_t *w, uint32_t S,
+                                                             unsigned long long *tau) {
+    extern __shared__ uint32_t set[];
+    __shared__ uint32_t s_i;
+    constexpr uint32_t NW = kVThreads / 32;
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t nbig = w[6];
+    uint32_t c = 0;
+    while (true) {
+        if (threadIdx.x == 0) s_i = atomicAdd(&w[8], 1u);
+        __syncthreads();
+        const uint32_t i = s_i;
+        __syncthreads();  // s_i is read by all before thread 0 takes the next ticket
+        if (i >= nbig) break;
+        const uint32_t a = list[i], a0 = offp[a], na = offp[a + 1] - a0;
+        uint32_t T = 1;
+        while (T < 2 * na && T < S) T <<= 1;
+        const uint32_t mask = T - 1u, sh = 32u - (31u - __clz(T));
+        for (uint32_t j = threadIdx.x; j < T; j += kVThreads) set[j] = kFull;
+        __syncthreads();
+        for (uint32_t j = threadIdx.x; j < na; j += kVThreads) {
+            const uint32_t y = adj[a0 + j];
+            uint32_t h = T > 1 ? (y * 0x9E3779B1u) >> sh : 0u;
+            while (atomicCAS(&set[h], kFull, y) != kFull) h = (h + 1u) & mask;
+        }
+        __syncthreads();
+        for (uint32_t j = warp; j < na; j += NW) {
+            const uint32_t x = adj[a0 + j], x0 = offp[x], nx = offp[x + 1] - x0;
+            if (nx > na * (32u - __clz(nx))) {  // N+(x) much longer: binary-search N+(a)'s members in it
+                c += count_in(adj + a0, na, adj + x0, nx, lane, 32);
+                continue;
+            }
+            for (uint32_t t = lane; t < nx; t += 32) {
+                const uint32_t y = __ldg(adj + x0 + t);
+                uint32_t h = T > 1 ? (y * 0x9E3779B1u) >> sh : 0u;
+                while (true) {
+                    const uint32_t k = set[h];
+                    if (k == y) {
+                        ++c;
+                        break;
+                    }
+                    if (k == kFull) break;
+                    h = (h + 1u) & mask;
+                }
+            }
+        }
+        __syncthreads();
     }
     c = __reduce_add_sync(kFull, c);
     if (lane == 0 && c) atomicAdd(tau, (unsigned long long)c);
@@ -314,10 +391,27 @@ extern "C" int tc_exact_triangles(const tc_edge *edges, uint64_t m, uint64_t *ta
     uint32_t *adj = reinterpret_cast<uint32_t *>(const_cast<uint64_t *>(sk)), *src = adj + m, *heavy = adj + 2 * m;
     kx_compact<<<grid_for(n), kThreads, 0, s>>>(keep, kpos, dst, vinc, n, adj, src);
     kx_outoff<<<grid_for(n + 1), kThreads, 0, s>>>(off, kpos, vinc + n - 1, m, offp);
-    // 3. wedge closing
+    // 3. wedge closing: sources with long out-lists vertex-centric (a shared-memory set of N+(a)), the rest
+    //    arc by arc (binary search; a warp per arc when both lists are long)
     unsigned long long *dtau = reinterpret_cast<unsigned long long *>(w + 4);
+    uint32_t *big = keep;  // keep | kpos are dead after kx_outoff: the source list
+    kx_bigsrc<<<grid_for(n + 1), kThreads, 0, s>>>(offp, vinc + n - 1, big, w);
     kx_count<<<grid_for(m), kThreads, 0, s>>>(adj, src, offp, m, dtau, heavy, w + 2);
     kx_count_heavy<<<grid_for(32ull * m, 8), kThreads, 0, s>>>(adj, src, offp, heavy, w + 2, dtau);
+    uint32_t hb[2];
+    XK(cudaMemcpyAsync(hb, w + 6, 8, cudaMemcpyDeviceToHost, s));
+    XK(cudaStreamSynchronize(s));
+    if (hb[0]) {
+        uint32_t S = 1;
+        while (S < 2 * std::min(hb[1], kSetDegMax) && S < kSetMax) S <<= 1;
+        XK(cudaFuncSetAttribute(kx_count_vertex, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * S)));
+        int dev2 = 0, sms = 148, per = 1;
+        XK(cudaGetDevice(&dev2));
+        XK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev2));
+        XK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kx_count_vertex, kVThreads, 4 * S));
+        const uint32_t grid = std::min<uint32_t>(hb[0], (uint32_t)(sms * std::max(per, 1)));
+        kx_count_vertex<<<grid, kVThreads, 4 * S, s>>>(adj, offp, big, w, S, dtau);
+    }
     XK(cudaEventRecord(e1, s));
     unsigned long long ht = 0;
     XK(cudaMemcpyAsync(&ht, dtau, 8, cudaMemcpyDeviceToHost, s));
