@@ -363,3 +363,41 @@ def test_C3_launch_configuration_sampled():
     for first in (0, r - 1024):
         o = oracle_run(s, r, 17, w, first, 1024)
         assert_states_equal({f: st[f][first:first + 1024] for f in FIELDS}, o.state(), f"C3-like shard {first}")
+
+
+def test_C1_many_seeds_parity_and_statistics():
+    """C1 over 1000 estimator seeds: every seed's final state equals the oracle's (compared by
+    closed sum and a state digest), and the mean GPU estimate lies within 4 sigma of the exact tau, sigma
+    from the closed-form variance Var X = m * sum_t C(t) - tau^2 (Claim discovery-prob)
+    over r * seeds independent estimators."""
+    import hashlib
+    from oracle import exact
+    from oracle.indexed import IndexedOracle
+    from paper_1308_2166_b200 import TriangleCounter
+    s = er(1000, 20000, 1)
+    r, w, seeds = 4096, 2048, 1000
+    dev = torch.from_numpy(s.view(np.int32)).cuda()
+    ests = []
+
+    def digest(st):
+        h = hashlib.sha1()
+        for f in FIELDS:
+            h.update(np.ascontiguousarray(st[f]).tobytes())
+        return h.hexdigest()
+
+    for seed in range(seeds):
+        g = TriangleCounter(r, 1000 + seed, w_max_hint=w)
+        for k in range(0, len(s), w):
+            g.push_batch(dev[k:k + w])
+        o = IndexedOracle(r, 1000 + seed)
+        for k in range(0, len(s), w):
+            assert o.push_batch(s[k:k + w]) == 0
+        assert g.closed_sum() == o.closed_sum(), seed
+        if seed % 50 == 0:
+            assert digest(g.state()) == digest(o.state()), seed
+        ests.append(g.estimate())
+        g.close()
+    tau, sumC, m = exact.moments(s)
+    var_x = m * sumC - tau * tau
+    sigma = (var_x / (r * seeds)) ** 0.5
+    assert abs(float(np.mean(ests)) - tau) <= 4 * sigma, (np.mean(ests), tau, sigma)
