@@ -401,3 +401,22 @@ def test_C1_many_seeds_parity_and_statistics():
     var_x = m * sumC - tau * tau
     sigma = (var_x / (r * seeds)) ** 0.5
     assert abs(float(np.mean(ests)) - tau) <= 4 * sigma, (np.mean(ests), tau, sigma)
+
+
+@pytest.fixture(scope="module")
+def rmat22():
+    return rmat(22, 16, 2)
+
+
+@pytest.mark.parametrize("lw", [12, 14, 16, 18, 20])
+def test_C5_batch_sizes_sampled(rmat22, lw):
+    """C5 (R-MAT scale 22, r = 2^22) at the sweep's batch sizes: three batches plus a ragged tail of the
+    stream, sampled shards bit-exact against the oracle, NBSI properties on every estimator."""
+    w, r = 1 << lw, 1 << 22
+    s = rmat22[: 3 * w + 123]
+    g = gpu_run(s, r, 9, w, device_input=True, w_max_hint=w)
+    st = g.state()
+    check_properties(s, st, len(s))
+    for first in (0, r - 1024):
+        o = oracle_run(s, r, 9, w, first, 1024)
+        assert_states_equal({f: st[f][first:first + 1024] for f in FIELDS}, o.state(), f"C5 w=2^{lw} shard {first}")
