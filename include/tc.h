@@ -129,6 +129,19 @@ int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g);
 int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint64_t *p1,
                  uint32_t *r2, uint64_t *p2, uint32_t *c, uint8_t *closed);
 
+/* tc_set_state -- checkpoint restore: overwrite local estimators [first, first+count)
+ * from HOST arrays in tc_get_state's layout (all pointers required when count > 0).  Validated first
+ * (TC_EINVAL and nothing written unless every r1 / r2 is empty with position UINT64_MAX or has lo < hi and
+ * a position < 2^31 - 1, c < 2^31 and closed in {0, 1}).  The closed sum S is recomputed.  Together with
+ * tc_set_counters this resumes a stream exactly: the next push draws with the restored batch index.
+ * Synchronises. */
+int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1, const uint64_t *p1,
+                 const uint32_t *r2, const uint64_t *p2, const uint32_t *c, const uint8_t *closed);
+
+/* tc_set_counters -- restore m (< 2^31) and the number of accepted non-empty batches (0 iff m = 0);
+ * recomputes S.  Synchronises. */
+int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches);
+
 /* tc_counters -- m (edges accepted so far) and the number of accepted non-empty batches. */
 int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches);
 

@@ -178,6 +178,20 @@ class TriangleCounter:
                  "tc_get_state")
         return dict(r1=r1, p1=p1, r2=r2, p2=p2, c=c, closed=closed)
 
+    def set_state(self, state: dict, first: int = 0):
+        """tc_set_state: restore estimators [first, first + n) from a dict in state()'s layout."""
+        a = {f: np.ascontiguousarray(state[f], dtype=t) for f, t in
+             (("r1", np.uint32), ("p1", np.uint64), ("r2", np.uint32), ("p2", np.uint64), ("c", np.uint32),
+              ("closed", np.uint8))}
+        n = len(a["c"])
+        P = lambda x: x.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._ck(_lib.load().tc_set_state(self._h, int(first), n, P(a["r1"]), P(a["p1"]), P(a["r2"]), P(a["p2"]),
+                                          P(a["c"]), P(a["closed"])), "tc_set_state")
+
+    def set_counters(self, m: int, batches: int):
+        """tc_set_counters: restore m and the number of accepted batches (resume a checkpointed stream)."""
+        self._ck(_lib.load().tc_set_counters(self._h, int(m), int(batches)), "tc_set_counters")
+
     def counters(self):
         m, b = C.c_uint64(), C.c_uint32()
         self._ck(_lib.load().tc_counters(self._h, C.byref(m), C.byref(b)), "tc_counters")

@@ -25,7 +25,7 @@ PHASES = ("partition", "pairs", "vertices", "update")
 TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4, "small_batch": 6}
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
-           "tc_estimate_mom", "tc_closed_sum_async", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
+           "tc_estimate_mom", "tc_closed_sum_async", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_set_state", "tc_set_counters", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
            "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_parse_edges", "tc_ingest_file", "tc_strerror",
            "tc_last_error"]
 
@@ -67,6 +67,8 @@ def load(path: str = LIB_PATH):
         "tc_required_estimators": (i32, [C.c_double, C.c_double, u64, u64, u64, C.POINTER(u64)]),
         "tc_group_sums": (i32, [vp, u32, vp]),
         "tc_get_state": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, vp]),
+        "tc_set_state": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, vp]),
+        "tc_set_counters": (i32, [vp, u64, u32]),
         "tc_counters": (i32, [vp, C.POINTER(u64), C.POINTER(u32)]),
         "tc_set_async": (i32, [vp, i32]),
         "tc_set_graphs": (i32, [vp, i32]),

@@ -574,6 +574,59 @@ int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint
     return TC_OK;
 }
 
+// S of the restored state, into the accumulator slot the next push does not overwrite
+static int recompute_S(tc_ctx *ctx) {
+    if (ctx->b == 0) {
+        ctx->S_slot = -1;
+        return TC_OK;
+    }
+    const int slot = (int)(ctx->b & 1u);
+    CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
+    launch_group_sums(ctx->st, 1, ctx->st.S + slot, ctx->stream);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->S_slot = slot;
+    return TC_OK;
+}
+
+int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1, const uint64_t *p1,
+                 const uint32_t *r2, const uint64_t *p2, const uint32_t *c, const uint8_t *closed) {
+    if (!ctx || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
+    if (count && (!r1 || !p1 || !r2 || !p2 || !c || !closed)) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    std::vector<uint32_t> q1(count), q2(count), cf(count);
+    for (uint64_t i = 0; i < count; ++i) {  // validate everything before touching the device
+        for (int f = 0; f < 2; ++f) {
+            const uint32_t lo = (f ? r2 : r1)[2 * i], hi = (f ? r2 : r1)[2 * i + 1];
+            const uint64_t p = (f ? p2 : p1)[i];
+            const bool empty = lo == 0xFFFFFFFFu && hi == 0xFFFFFFFFu;
+            if (empty != (p == ~0ull)) return TC_EINVAL;
+            if (!empty && (lo >= hi || p >= 0x7FFFFFFFull)) return TC_EINVAL;
+            (f ? q2 : q1)[i] = empty ? 0xFFFFFFFFu : (uint32_t)p;
+        }
+        if (c[i] > kCMask || closed[i] > 1) return TC_EINVAL;
+        cf[i] = c[i] | (closed[i] ? kClosedBit : 0u);
+    }
+    if (count) {
+        CK(cudaMemcpy(ctx->st.r1 + first, r1, 8 * count, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->st.r2 + first, r2, 8 * count, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->st.p1 + first, q1.data(), 4 * count, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->st.p2 + first, q2.data(), 4 * count, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->st.cf + first, cf.data(), 4 * count, cudaMemcpyHostToDevice));
+    }
+    return recompute_S(ctx);
+}
+
+int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches) {
+    if (!ctx || m > 0x7FFFFFFFull || (batches == 0) != (m == 0)) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    ctx->m = m;
+    ctx->b = batches;
+    return recompute_S(ctx);
+}
+
 int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches) {
     if (!ctx) return TC_EINVAL;
     if (m) *m = ctx->m;

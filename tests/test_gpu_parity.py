@@ -420,3 +420,35 @@ def test_C5_batch_sizes_sampled(rmat22, lw):
     for first in (0, r - 1024):
         o = oracle_run(s, r, 9, w, first, 1024)
         assert_states_equal({f: st[f][first:first + 1024] for f in FIELDS}, o.state(), f"C5 w=2^{lw} shard {first}")
+
+
+def test_checkpoint_resume():
+    """tc_get_state / tc_counters -> tc_set_state / tc_set_counters on a fresh handle resumes the stream
+    bit-exactly (the next push draws with the restored batch index); invalid snapshots are rejected
+    without effect."""
+    from paper_1308_2166_b200 import TCError, TriangleCounter
+    s = rmat(12, 16, 21)
+    r, w = 3000, 2500
+    ref = oracle_run(s, r, 4, w)
+    a = TriangleCounter(r, 4)
+    half = (len(s) // w // 2) * w
+    for k in range(0, half, w):
+        a.push_batch(s[k:k + w])
+    snap, (m, b) = a.state(), a.counters()
+    a.close()
+    c = TriangleCounter(r, 4)
+    c.set_state(snap)
+    c.set_counters(m, b)
+    assert c.closed_sum() == int(snap["c"][snap["closed"] == 1].astype(np.int64).sum())
+    for k in range(half, len(s), w):
+        c.push_batch(s[k:k + w])
+    assert_states_equal(c.state(), ref.state(), "resumed")
+    assert c.estimate() == ref.estimate() and c.counters() == ref.counters()
+    bad = {f: v.copy() for f, v in snap.items()}
+    bad["r1"][5] = bad["r1"][5][::-1]  # lo > hi
+    before = c.state()
+    with pytest.raises(TCError):
+        c.set_state(bad)
+    assert_states_equal(c.state(), before, "rejected snapshot")
+    with pytest.raises(TCError):
+        c.set_counters(0, 3)
