@@ -28,18 +28,22 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, host_feed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle.indexed import IndexedOracle
-        stream = er(300, 5000, 4) if rank == 0 else None
-        sc = ShardedCounter(R, SEED, W, device="cpu",
+        full = er(300, 5000, 4)
+        stream = full if (rank == 0 or host_feed) else None
+        sc = ShardedCounter(R, SEED, W + world, device="cpu",
                             engine_factory=lambda r, s, f, c: IndexedOracle(r, s, f, c))
         nb = (5000 + W - 1) // W
         for k in range(nb):
-            sc.push_batch(stream[k * W:(k + 1) * W] if rank == 0 else None)
+            if host_feed:  # every rank holds the batch, uploads its slice, all-gather
+                sc.push_batch_host(torch.from_numpy(stream[k * W:(k + 1) * W].view("int32")))
+            else:
+                sc.push_batch(stream[k * W:(k + 1) * W] if rank == 0 else None)
         q.put((rank, sc.first, sc.count, sc.engine.state(), sc.closed_sum(), sc.estimate(), sc.m))
     finally:
         dist.destroy_process_group()
@@ -57,12 +61,14 @@ def test_shard_bounds():
         shard(10, 2, 2)
 
 
-def test_two_ranks_gloo_equal_unsharded():
+@pytest.mark.parametrize("host_feed", [False, True])
+def test_two_ranks_gloo_equal_unsharded(host_feed):
+    """Batch broadcast from rank 0 (host_feed False) or per-rank slices + all-gather (True)."""
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(g, world, port, q)) for g in range(world)]
+    procs = [ctx.Process(target=_worker, args=(g, world, port, q, host_feed)) for g in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=240) for _ in range(world))
