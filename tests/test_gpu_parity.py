@@ -452,3 +452,32 @@ def test_checkpoint_resume():
     assert_states_equal(c.state(), before, "rejected snapshot")
     with pytest.raises(TCError):
         c.set_counters(0, 3)
+
+
+def _shuffled(edges, seed):
+    rng = np.random.default_rng(seed)
+    e = np.asarray(edges, dtype=np.uint32)
+    e = e[rng.permutation(len(e))]
+    flip = rng.random(len(e)) < 0.5
+    e[flip] = e[flip][:, ::-1]
+    return np.ascontiguousarray(e)
+
+
+@pytest.mark.parametrize("kind", ["star", "path", "complete", "bipartite", "two_hubs"])
+def test_degenerate_graphs(kind):
+    """Degenerate shapes of the method: a star (one vertex in every edge: a single hub segment, no
+    triangle), a path (no wedge closes), a dense complete graph, a bipartite graph (wedges, no triangle),
+    and two hubs joined to every other vertex (triangles only through the hub edge)."""
+    if kind == "star":
+        g = [(0, i) for i in range(1, 20000)]
+    elif kind == "path":
+        g = [(i, i + 1) for i in range(20000)]
+    elif kind == "complete":
+        g = [(a, b) for a in range(160) for b in range(a + 1, 160)]
+    elif kind == "bipartite":
+        g = [(a, 1000 + b) for a in range(100) for b in range(150)]
+    else:
+        g = [(0, 1)] + [(h, i) for h in (0, 1) for i in range(2, 9000)]
+    s = _shuffled(g, 3)
+    for w in (len(s), 4096, 777):
+        _compare(s, 5000, 31 + w, w)
