@@ -317,6 +317,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.first = ctx->first;
     a.seed = ctx->seed;
     a.S_slot = slot;
+    a.S_reset = ctx->st.S + slot;
     a.g = make_geometry((uint32_t)w, ctx->tune);
     a.small = ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax);
     if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
@@ -335,14 +336,11 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         auto rec = [&](int e, cudaStream_t st) {
             if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev_pool[ctx->ev_used][e], st) == cudaSuccess;
         };
-        if (ctx->async_errors) {
-            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrErr, ms) == cudaSuccess;  // keep the sticky error
-            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr + 1, 0, 4 * (kCtrWords - kCtrErr - 1), ms) == cudaSuccess;
-        } else {
-            ok = ok && cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ms) == cudaSuccess;
-            if (ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
-        }
-        ok = ok && cudaMemsetAsync(ctx->st.S + slot, 0, 8, ms) == cudaSuccess;
+        // k_count zeroes the counters and this batch's S; the error word is sticky in asynchronous mode and
+        // cleared (or set to the overflow error) here in strict mode
+        if (!ctx->async_errors)
+            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, 0, 4, ms) == cudaSuccess;
+        if (!ctx->async_errors && ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
         // a1: count, scans, scatter
         rec(2 * TC_PHASE_PARTITION, ms);
         launches += launch_partition(ix, a, ms);

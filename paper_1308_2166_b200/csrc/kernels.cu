@@ -107,6 +107,7 @@ struct PartArgs {
     uint32_t G, ptag;
     uint32_t *ctr;
     uint32_t *filt;    // small batches: vertex and pair filters to fill (else null)
+    unsigned long long *S_reset;  // k_count zeroes this batch's S accumulator and the counters (not the error word)
 };
 
 // a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
@@ -171,6 +172,10 @@ constexpr uint32_t kEdgeRounds = kTileEdges / kTileThreads;      // 8
 constexpr uint32_t kArcsPerWarp = kArcRounds * 32, kEdgesPerWarp = kEdgeRounds * 32;
 
 __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
+    if (blockIdx.x == 0) {  // per-batch resets (every later kernel of the batch starts after this one)
+        if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr) a.ctr[threadIdx.x] = 0u;
+        if (threadIdx.x == 0) *a.S_reset = 0ull;
+    }
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     extern __shared__ uint32_t dsh[];
     const uint32_t nV = 1u << a.g.bp1;
@@ -1466,7 +1471,7 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
     return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr,
-                    a.small ? ix.filt : nullptr};
+                    a.small ? ix.filt : nullptr, a.S_reset};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {

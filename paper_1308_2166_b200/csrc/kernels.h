@@ -62,6 +62,7 @@ struct BatchArgs {
     uint64_t first;   // global id of local estimator 0
     uint64_t seed;
     int S_slot;
+    unsigned long long *S_reset;  // the S accumulator of this batch (zeroed by k_count)
     uint32_t ptag;    // edge-pair table tag of this push (1..254)
     bool small;       // small-batch estimator pass (filters built by k_pairs, k_update skips untouched estimators)
     Geometry g;
