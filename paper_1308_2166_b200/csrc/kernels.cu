@@ -811,12 +811,12 @@ __global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// a2, common case: a vertex bucket of at most vcap (<= kHCap) arcs.  Vertices get bucket-local ids from a
-// shared-memory hash table (claim order), then ONE stable ballot ranking pass by local id -- instead of
-// three radix passes on the vertex hash -- gives every arc its rank inside its vertex.
+// a2, common case: a vertex bucket of at most vcap (<= kHCapSmall) arcs.  Vertices get bucket-local ids from a
+// shared-memory hash table (claim order), then ONE stable ranking pass by local id (__match_any_sync peers,
+// per-warp counters) -- instead of three radix passes on the vertex hash -- gives every arc its rank inside
+// its vertex.
 
-constexpr uint32_t kHThreads = 256, kHWarps = kHThreads / 32;
-constexpr uint32_t kHCap = 4096;  // arcs: the largest bucket (or rest after a hub) the hash path takes
+constexpr uint32_t kHThreads = 256;
 
 // Shared-memory layout of the hash path for buckets of at most CAP arcs: R1 = {hkey u32[2 CAP], lid
 // u16[2 CAP]} while hashing; then {whist u16[8][SW], segst u32[CAP + 1]}; the slice table (u32,
