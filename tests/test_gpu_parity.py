@@ -481,3 +481,50 @@ def test_degenerate_graphs(kind):
     s = _shuffled(g, 3)
     for w in (len(s), 4096, 777):
         _compare(s, 5000, 31 + w, w)
+
+
+@pytest.mark.parametrize("case", range(64))
+def test_fuzz_configurations(case):
+    """Random graph, r, batch-size sequence, index knobs, launch mode and input placement per case; the
+    CUDA path must equal the oracle bit for bit after every run."""
+    from paper_1308_2166_b200 import TriangleCounter
+    rng = np.random.default_rng(1000 + case)
+    if rng.random() < 0.5:
+        s = rmat(int(rng.integers(8, 13)), int(rng.integers(4, 17)), int(rng.integers(1, 99)))
+    else:
+        n = int(rng.integers(30, 3000))
+        s = er(n, int(rng.integers(1, min(30000, n * (n - 1) // 2))), int(rng.integers(1, 99)))
+    r = int(rng.choice([1, 2, 31, 257, 1000, 4096, 30000]))
+    seed = int(rng.integers(0, 2**63))
+    sizes, k = [], 0
+    while k < len(s):
+        w = int(rng.choice([1, 2, 7, 100, 1000, 4096, 5000, 20000]))
+        sizes.append(min(w, len(s) - k))
+        k += sizes[-1]
+    tc = TriangleCounter(r, seed)
+    knobs = {}
+    if rng.random() < 0.4:
+        knobs["small_batch"] = int(rng.integers(0, 3))
+    if rng.random() < 0.3:
+        knobs["vbucket_arcs"] = int(rng.choice([1, 16, 256, 4096]))
+    if rng.random() < 0.3:
+        knobs["vbucket_cap"] = int(rng.choice([1, 64, 2048]))
+    if knobs:
+        tc.tune(**knobs)
+    tc.set_graphs(bool(rng.random() < 0.5))
+    tc.set_async(bool(rng.random() < 0.5))
+    place = rng.integers(0, 3)
+    src = {0: s, 1: torch.from_numpy(s.view(np.int32)).pin_memory(), 2: torch.from_numpy(s.view(np.int32)).cuda()}[int(place)]
+    k = 0
+    for w in sizes:
+        tc.push_batch(src[k:k + w])
+        k += w
+    assert tc.sync() == 0
+    from oracle.indexed import IndexedOracle
+    o = IndexedOracle(r, seed)
+    k = 0
+    for w in sizes:
+        assert o.push_batch(s[k:k + w]) == 0
+        k += w
+    assert_states_equal(tc.state(), o.state(), f"fuzz case {case} r={r} knobs={knobs} place={place}")
+    assert tc.closed_sum() == o.closed_sum() and tc.counters() == o.counters()
