@@ -179,6 +179,19 @@ def committed_limiters(kernel="k_update"):
             "source": "profiles/ncu_full_r01.json (cold-L2 replay)"}
 
 
+def limiters_with_issue(lim, launch_ms):
+    """Add the issue-rate view: the committed capture's warp instructions per launch over this run's launch
+    time, against 4 warp instructions per SM per cycle at the SM clock the recipe gives for B200
+    (148 SMs x 4 x 1.965 GHz)."""
+    if not lim or not lim.get("warp_instructions_per_launch") or not launch_ms:
+        return lim
+    peak = 148 * 4 * 1.965e9
+    ach = lim["warp_instructions_per_launch"] / (launch_ms * 1e-3)
+    lim = dict(lim)
+    lim["issue"] = {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": peak, "frac": ach / peak}
+    return lim
+
+
 # --------------------------------------------------------------------------------------------------
 def algorithmic_bytes(phase, w, R, D, fresh, r2old, skipped=0):
     """Algorithmic bytes per launch: what each phase must move at minimum.
@@ -347,7 +360,7 @@ def run_b200(args):
                 "algorithmic_bytes_per_launch": alg["update"] / max(1, nsteps),
                 "launch_ms": prof["update"][0] / max(1, nsteps),
                 "small_batch_skipped_frac": stats["skipped"] / max(1, count * nsteps),
-                "limiters": committed_limiters("k_update"),
+                "limiters": limiters_with_issue(committed_limiters("k_update"), prof["update"][0] / max(1, nsteps)),
                 "phases": {p: {"ms_per_step": prof[p][0] / max(1, nsteps), "launches_per_step": prof[p][1] / max(1, nsteps),
                                "algorithmic_GBps": ach.get(p), "frac": (ach[p] / peak) if ach.get(p) else None}
                            for p in prof}}
