@@ -1311,7 +1311,10 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
         x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;
         z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;
     }
-    if ((r2new || had_r2) && !closed) {
+    // the closing edge touches x, so it can only be in W (after f2) if x has a batch arc (after f1 when f1 is
+    // fresh): ld / rd count exactly those arcs, so x without any needs no probe
+    const uint32_t degx = x == r1.x ? ld : rd;
+    if ((r2new || had_r2) && !closed && degx) {
         const int64_t kk = pt_find(ix.L, min(x, z), max(x, z));
         if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
     }
