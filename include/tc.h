@@ -163,9 +163,9 @@ int tc_set_graphs(tc_ctx *ctx, int enable);
  *                        are sorted in chunks through global memory instead of in shared memory
  *  TC_TUNE_SMALL_BATCH   the estimator pass for small batches: 0 = auto (default; batches
  *                        of at most 8192 edges), 1 = never, 2 = always.  It reads r1, r2, chi of every
- *                        estimator, tests them against two bit filters of the batch (its vertices, its edge
- *                        pairs; no false negatives) and runs Steps 1-3 only for estimators whose f1 is
- *                        replaced or that the batch can touch, writing only the fields that change.
+ *                        estimator, tests f1's endpoints against a bit filter of the batch's vertices (no
+ *                        false negatives) and runs Steps 1-3 only for estimators whose f1 is replaced or has
+ *                        an endpoint in the batch, writing only the fields that change.
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
 enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6 };
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value);

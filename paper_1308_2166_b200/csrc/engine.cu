@@ -105,7 +105,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
          cudaMalloc(&ix.offV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
          cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess &&
-         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess && cudaMalloc(&ix.filt, 8ull * kFilterWords) == cudaSuccess;
+         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess && cudaMalloc(&ix.filt, 4ull * kFilterWords) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);

@@ -123,13 +123,13 @@ __host__ __device__ __forceinline__ uint32_t vslot_start(uint32_t h, uint32_t S)
 }
 __host__ __device__ __forceinline__ uint32_t vslot_next(uint32_t s, uint32_t S) { return s + 2 >= S ? 0u : s + 2; }
 
-// Small batches: two bit filters of the batch -- one over its vertices, one over its
-// edge pairs -- let the estimator pass skip every estimator that the batch cannot change.  A filter has
-// no false negatives, so skipping is exact; a false positive only costs the full update.
-constexpr uint32_t kFilterBits = 1u << 17;                 // per filter (16 KB)
+// Small batches: a bit filter over the batch's vertices lets the estimator pass skip
+// every estimator the batch cannot change -- a retained f1 with neither endpoint in W gets no chi^+ and no
+// closing edge (that edge would touch f1's endpoint x).  The filter has no false negatives, so skipping is
+// exact; a false positive only costs the full update.
+constexpr uint32_t kFilterBits = 1u << 18;                 // 32 KB
 constexpr uint32_t kFilterWords = kFilterBits / 32;
 __host__ __device__ __forceinline__ uint32_t vfilter_bit(uint32_t hv) { return hv & (kFilterBits - 1u); }
-__host__ __device__ __forceinline__ uint32_t pfilter_bit(uint64_t hp) { return (uint32_t)(hp >> 40) & (kFilterBits - 1u); }
 
 struct Lookup {
     const uint2 *E;

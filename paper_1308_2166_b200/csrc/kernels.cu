@@ -15,7 +15,7 @@
 //   k_split      a1      : (w > 2^21 only) each bucket stably split again by the next hash bits
 //   k_pairs      a3      : (second stream, alongside the vertex phase) every edge of the raw batch into the
 //                          edge-pair table (64-bit CAS; a repeat is TC_EDUP); small batches also fill the
-//                          vertex / pair filters
+//                          vertex filter
 //   k_vhash      a2      : one CTA per vertex bucket: bucket-local vertex ids from a shared-memory hash
 //                          table, one stable ranking pass by local id (replaces rankAll's sort by (src, -pos),
 //                          PAPER.md:680-684), segment starts -> segS, per-arc {slot, segEnd} (rank = segEnd -
@@ -106,7 +106,7 @@ struct PartArgs {
     uint2 *pt;         // edge-pair table (G groups of 4 slots)
     uint32_t G, ptag;
     uint32_t *ctr;
-    uint32_t *filt;    // small batches: vertex and pair filters to fill (else null)
+    uint32_t *filt;    // small batches: the vertex filter to fill (else null)
     unsigned long long *S_reset;  // k_count zeroes this batch's S accumulator and the counters (not the error word)
 };
 
@@ -152,10 +152,8 @@ __global__ void __launch_bounds__(256) k_pairs(PartArgs a) {
             dup = pt_insert(a, n, k);
             if (a.filt) {
                 const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
-                const uint32_t b2 = pfilter_bit(hash_pair64(pair_key(n.x, n.y)));
                 atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
                 atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
-                atomicOr(a.filt + kFilterWords + (b2 >> 5), 1u << (b2 & 31u));
             }
         }
     }
@@ -1224,16 +1222,12 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
     const bool fresh = d1 >= m_prev;
     const uint32_t j = fresh ? (uint32_t)(d1 - m_prev) : 0u;
     if (kSmall && !fresh) {
-        // a retained f1 changes only if the batch has an arc at one of its endpoints (chi^+ > 0) or the closing
-        // edge of an open wedge (Step 3); with neither, the state is untouched and nothing is written
+        // a retained f1 changes only if the batch has an arc at one of its endpoints: chi^+ > 0, or the closing
+        // edge of an open wedge (it touches f1's endpoint x); with neither, nothing changes or is written
         const uint32_t c0 = old.cf & kCMask;
         const bool cl0 = (old.cf & kClosedBit) != 0;
-        bool touched = filter_has(sf, vfilter_bit(hash_vertex(old.r1.x))) || filter_has(sf, vfilter_bit(hash_vertex(old.r1.y)));
-        if (!touched && c0 > 0 && !cl0) {
-            const uint2 a = old.r1, b = old.r2;
-            const uint32_t x = (a.x == b.x || a.x == b.y) ? a.y : a.x, z = (b.x == a.x || b.x == a.y) ? b.y : b.x;
-            touched = filter_has(sf + kFilterWords, pfilter_bit(hash_pair64(pair_key(min(x, z), max(x, z)))));
-        }
+        const bool touched =
+            filter_has(sf, vfilter_bit(hash_vertex(old.r1.x))) || filter_has(sf, vfilter_bit(hash_vertex(old.r1.y)));
         if (!touched) {
             ++n_skip;
             return cl0 ? c0 : 0u;
@@ -1351,10 +1345,10 @@ template <bool kSmall>
 __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
                                                    unsigned long long *stats, const uint32_t *filt) {
     if (ix.ctr[kCtrErr]) return;
-    __shared__ uint32_t sf[kSmall ? 2 * kFilterWords : 1];
+    __shared__ uint32_t sf[kSmall ? kFilterWords : 1];
     if (kSmall) {
         const uint4 *src = reinterpret_cast<const uint4 *>(filt);
-        for (uint32_t i = threadIdx.x; i < 2 * kFilterWords / 4; i += blockDim.x) reinterpret_cast<uint4 *>(sf)[i] = __ldg(src + i);
+        for (uint32_t i = threadIdx.x; i < kFilterWords / 4; i += blockDim.x) reinterpret_cast<uint4 *>(sf)[i] = __ldg(src + i);
         __syncthreads();
     }
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -1493,7 +1487,7 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 }
 
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
-    if (a.small && cudaMemsetAsync(ix.filt, 0, 8ull * kFilterWords, s) != cudaSuccess) return 0;
+    if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
     k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
     return 1;
 }

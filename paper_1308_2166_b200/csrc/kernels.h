@@ -29,7 +29,7 @@ struct IndexBufs {
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
     uint32_t *vstart = nullptr;    // [4097] vertex-bucket totals -> exclusive prefix
     uint32_t *ctr = nullptr;       // device counters (index.cuh kCtr*)
-    uint32_t *filt = nullptr;      // [2 kFilterWords] small-batch filters: vertices, then edge pairs
+    uint32_t *filt = nullptr;      // [kFilterWords] small-batch filter over the batch's vertices
     uint2 *stage = nullptr;        // [wcap] H2D staging for host batches (two buffers, alternating)
     uint2 *stage2 = nullptr;
 };
@@ -68,8 +68,8 @@ struct BatchArgs {
     Geometry g;
 };
 
-// Batches of at most this many edges take the filtered small-batch estimator pass (filter load <= 1/8)
-constexpr uint32_t kSmallBatchMax = kFilterBits / 16;  // 8192: measured break-even ~16384 on C5
+// Batches of at most this many edges take the filtered small-batch estimator pass (filter load <= 1/16)
+constexpr uint32_t kSmallBatchMax = 8192;  // measured break-even ~16384 on C5
 
 struct Tuning {
     uint32_t small = 0;            // 0 auto (w <= kSmallBatchMax), 1 never, 2 always
