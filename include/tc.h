@@ -254,6 +254,7 @@ typedef struct {
  * code.  Synchronises at the end (tc_sync).  stats may be NULL. */
 int tc_ingest_file(tc_ctx *ctx, const char *path, uint64_t w, int flags, tc_ingest_stats *stats);
 
+/* tc_strerror -- a static, never-NULL description of a TC_* code (owned by the library). */
 const char *tc_strerror(int code);
 int tc_last_error(void); /* thread-local code of the last failed tc_create* */
 
