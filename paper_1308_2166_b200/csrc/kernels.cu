@@ -41,6 +41,19 @@ constexpr uint32_t kFull = 0xffffffffu;
 
 __device__ __forceinline__ uint2 norm_edge(uint2 e) { return make_uint2(min(e.x, e.y), max(e.x, e.y)); }
 
+// Lanes of the warp holding the same NB-bit digit d (invalid lanes group together), NB known at compile time.
+template <int NB>
+__device__ __forceinline__ uint32_t digit_peers_c(uint32_t d, bool valid) {
+    uint32_t m = __ballot_sync(kFull, valid);
+    if (!valid) m = ~m;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const uint32_t bit = (d >> b) & 1u;
+        m &= __ballot_sync(kFull, bit) ^ (bit - 1u);
+    }
+    return m;
+}
+
 // Lanes of the warp holding the same nbits-bit digit d (invalid lanes group together).  nbits is
 // warp-uniform.  One ballot per digit bit.
 __device__ __forceinline__ uint32_t digit_peers(uint32_t d, bool valid, uint32_t nbits) {
@@ -169,6 +182,7 @@ constexpr uint32_t kArcRounds = 2 * kTileEdges / kTileThreads;   // 16
 constexpr uint32_t kEdgeRounds = kTileEdges / kTileThreads;      // 8
 constexpr uint32_t kArcsPerWarp = kArcRounds * 32, kEdgesPerWarp = kEdgeRounds * 32;
 
+template <int NB>  // the partition bits a.g.bp1, as a compile-time constant
 __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
     if (blockIdx.x == 0) {  // per-batch resets (every later kernel of the batch starts after this one)
         if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr) a.ctr[threadIdx.x] = 0u;
@@ -208,7 +222,7 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
             const uint2 n = norm_edge(__ldg(a.in + e0 + (ai >> 1)));
             d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bp1);
         }
-        const uint32_t peers = digit_peers(d, valid, a.g.bp1);
+        const uint32_t peers = digit_peers_c<NB>(d, valid);
         const uint32_t before = __popc(peers & lt);
         uint32_t c = 0;
         if (valid) c = wv[warp * nV + d];
@@ -1475,7 +1489,15 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
     const Geometry &g = a.g;
     const uint32_t nV = 1u << g.bp1;
     const PartArgs p = part_args(ix, a);
-    k_count<<<g.tiles, kTileThreads, 2 * kTileWarps * nV, s>>>(p);
+    switch (g.bp1) {
+#define TC_COUNT_CASE(B) \
+    case B: k_count<B><<<g.tiles, kTileThreads, 2 * kTileWarps * nV, s>>>(p); break;
+        TC_COUNT_CASE(0) TC_COUNT_CASE(1) TC_COUNT_CASE(2) TC_COUNT_CASE(3) TC_COUNT_CASE(4) TC_COUNT_CASE(5)
+        TC_COUNT_CASE(6) TC_COUNT_CASE(7) TC_COUNT_CASE(8) TC_COUNT_CASE(9) TC_COUNT_CASE(10) TC_COUNT_CASE(11)
+        TC_COUNT_CASE(12)
+#undef TC_COUNT_CASE
+        default: return 0;
+    }
     k_scan_rows<<<nV, 256, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, ix.ctr);
     // with a split, the large-bucket list is built by k_split over the sub-buckets
     k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.bs ? 0xFFFFFFFFu : g.vcap, ix.vperm, ix.ctr);
@@ -1537,7 +1559,14 @@ int set_kernel_attributes() {
     cudaError_t e1 = cudaFuncSetAttribute(k_vbig, cudaFuncAttributeMaxDynamicSharedMemorySize, kVSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
-    cudaError_t e2 = cudaFuncSetAttribute(k_count, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * 4096);
+    cudaError_t e2 = cudaSuccess;
+    const void *counts[] = {(const void *)k_count<0>, (const void *)k_count<1>, (const void *)k_count<2>,
+                            (const void *)k_count<3>, (const void *)k_count<4>, (const void *)k_count<5>,
+                            (const void *)k_count<6>, (const void *)k_count<7>, (const void *)k_count<8>,
+                            (const void *)k_count<9>, (const void *)k_count<10>, (const void *)k_count<11>,
+                            (const void *)k_count<12>};
+    for (int b = 0; b <= 12 && e2 == cudaSuccess; ++b)
+        e2 = cudaFuncSetAttribute(counts[b], cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * (1 << b));
     if (e2 == cudaSuccess)
         e2 = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 + 12 * kTileEdges);
     return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;
