@@ -7,7 +7,7 @@
 //   k_count      a1      : load W (coalesced), validate, normalise into E, stable in-tile ranks of the arcs
 //                          by partition bucket (top bits of hash_vertex; one ballot per bit) and per-(bucket,
 //                          tile) counts
-//   k_scan_rows / k_scan_tot : tile offsets inside each bucket, bucket sizes and starts; the list of
+//   k_scan_cols / k_scan_tot : tile offsets inside each bucket, bucket sizes and starts; the list of
 //                          oversized buckets (k_vhub's)
 //   k_scatter    a1      : arcs {vertex, k<<1|side, neighbour} to their bucket STABLY (staged in shared
 //                          memory, written as coalesced runs), so each bucket holds its arcs in arrival order
@@ -112,10 +112,10 @@ struct PartArgs {
     Geometry g;
     uint2 *E;
     uint4 *arcs;  // {vertex, k<<1|side, neighbour, 0}
-    uint32_t *cntV;    // [nV * tiles] per-(bucket, tile) arc counts
-    uint32_t *offV;    // [nV * tiles] the tile's offset inside the bucket
+    uint32_t *cntV;    // [tiles][nV] per-(tile, bucket) arc counts
+    uint32_t *offV;    // [tiles][nV] the tile's offset inside the bucket
     uint16_t *arank;   // [2 w] in-tile ranks
-    uint32_t *vstart;  // bucket sizes (k_scan_rows) -> exclusive prefixes (k_scan_tot)
+    uint32_t *vstart;  // bucket sizes (k_scan_cols) -> exclusive prefixes (k_scan_tot)
     uint2 *pt;         // edge-pair table (G groups of 4 slots)
     uint32_t G, ptag;
     uint32_t *ctr;
@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
             wv[x * nV + d] = (uint16_t)run;
             run += c;
         }
-        a.cntV[d * a.g.tiles + t] = run;
+        a.cntV[(size_t)t * nV + d] = run;  // tile-major: this tile's counts are one contiguous row
     }
     __syncthreads();
     // in-tile ranks (coalesced u16 stores)
@@ -289,26 +289,33 @@ __global__ void __launch_bounds__(1024) k_scan_tot(uint32_t *vstart, uint32_t nV
     }
 }
 
-// One block per vertex-bucket row: cnt[b][t] -> sum_{t' < t} cnt[b][t'] (the tile's offset inside the
-// bucket); the row total (the bucket size) goes to vstart[b].
-__global__ void __launch_bounds__(256) k_scan_rows(const uint32_t *cntV, uint32_t *offV, uint32_t *vstart, uint32_t tiles,
-                                                  const uint32_t *ctr) {
+
+// Tile-major counts cnt[t][b]: one block per 32 buckets (a column strip); warp w sums its slice of tiles for
+// each of the 32 columns (coalesced 128-byte rows), a prefix over the 8 warps, then the exclusive prefix
+// down each column is written to off[t][b] (the tile's offset inside the bucket) and the column total (the
+// bucket size) to vstart[b].
+__global__ void __launch_bounds__(256) k_scan_cols(const uint32_t *cntV, uint32_t *offV, uint32_t *vstart, uint32_t tiles,
+                                                   uint32_t nV, const uint32_t *ctr) {
     if (ctr[kCtrErr] & kErrStage) return;
-    __shared__ uint32_t ws[9];
-    const uint32_t b = blockIdx.x;
-    const uint32_t *row = cntV + (size_t)b * tiles;
-    uint32_t *orow = offV + (size_t)b * tiles;
-    const uint32_t per = (tiles + 255) / 256;
-    const uint32_t c0 = threadIdx.x * per, c1 = min(tiles, c0 + per);
-    uint32_t local = 0;
-    for (uint32_t i = c0; i < c1; ++i) local += row[i];
-    uint32_t tot;
-    uint32_t run = block_exclusive_scan<256>(local, ws, &tot);
-    for (uint32_t i = c0; i < c1; ++i) {
-        orow[i] = run;
-        run += row[i];
+    __shared__ uint32_t part[8][33];
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    const uint32_t b = blockIdx.x * 32u + lane;
+    const bool on = b < nV;
+    const uint32_t per = (tiles + 7) / 8, t0 = min(tiles, warp * per), t1 = min(tiles, t0 + per);
+    uint32_t sum = 0;
+    for (uint32_t t = t0; t < t1; ++t) sum += on ? cntV[(size_t)t * nV + b] : 0u;
+    part[warp][lane] = sum;
+    __syncthreads();
+    uint32_t run = 0;
+    for (uint32_t x = 0; x < warp; ++x) run += part[x][lane];
+    for (uint32_t t = t0; t < t1; ++t) {
+        if (on) {
+            const uint32_t c = cntV[(size_t)t * nV + b];
+            offV[(size_t)t * nV + b] = run;
+            run += c;
+        }
     }
-    if (threadIdx.x == 0) vstart[b] = tot;
+    if (warp == 7 && on) vstart[b] = run;  // the last warp's running sum is the column total
 }
 
 // Tile scatter: arc {vertex, k<<1|side, neighbour} -> arcs[start(bucket) + offset(bucket, tile) + rank in
@@ -324,8 +331,8 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
     const uint32_t t = blockIdx.x, e0 = t * kTileEdges;
     const uint32_t ne = min(kTileEdges, a.g.w - e0);
     for (uint32_t d = threadIdx.x; d < nV; d += kTileThreads) {
-        soff[d] = a.vstart[d] + a.offV[d * a.g.tiles + t];
-        toff[d] = a.cntV[d * a.g.tiles + t];
+        soff[d] = a.vstart[d] + a.offV[(size_t)t * nV + d];
+        toff[d] = a.cntV[(size_t)t * nV + d];
     }
     for (uint32_t i = threadIdx.x; i < ne; i += kTileThreads) sE[i] = a.E[e0 + i];
     __syncthreads();
@@ -1498,7 +1505,7 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 #undef TC_COUNT_CASE
         default: return 0;
     }
-    k_scan_rows<<<nV, 256, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, ix.ctr);
+    k_scan_cols<<<(nV + 31) / 32, 256, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, nV, ix.ctr);
     // with a split, the large-bucket list is built by k_split over the sub-buckets
     k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.bs ? 0xFFFFFFFFu : g.vcap, ix.vperm, ix.ctr);
     k_scatter<<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
