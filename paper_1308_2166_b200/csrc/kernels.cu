@@ -291,17 +291,21 @@ __global__ void __launch_bounds__(1024) k_scan_tot(uint32_t *vstart, uint32_t nV
 
 
 // Tile-major counts cnt[t][b]: one block per 32 buckets (a column strip); warp w sums its slice of tiles for
-// each of the 32 columns (coalesced 128-byte rows), a prefix over the 8 warps, then the exclusive prefix
+// each of the 32 columns (coalesced 128-byte rows), a prefix over the 32 warps, then the exclusive prefix
 // down each column is written to off[t][b] (the tile's offset inside the bucket) and the column total (the
 // bucket size) to vstart[b].
-__global__ void __launch_bounds__(256) k_scan_cols(const uint32_t *cntV, uint32_t *offV, uint32_t *vstart, uint32_t tiles,
-                                                   uint32_t nV, const uint32_t *ctr) {
+#ifndef TC_SCAN_WARPS
+#define TC_SCAN_WARPS 32
+#endif
+constexpr uint32_t kScanWarps = TC_SCAN_WARPS;
+__global__ void __launch_bounds__(kScanWarps * 32) k_scan_cols(const uint32_t *cntV, uint32_t *offV, uint32_t *vstart,
+                                                               uint32_t tiles, uint32_t nV, const uint32_t *ctr) {
     if (ctr[kCtrErr] & kErrStage) return;
-    __shared__ uint32_t part[8][33];
+    __shared__ uint32_t part[kScanWarps][33];
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
     const uint32_t b = blockIdx.x * 32u + lane;
     const bool on = b < nV;
-    const uint32_t per = (tiles + 7) / 8, t0 = min(tiles, warp * per), t1 = min(tiles, t0 + per);
+    const uint32_t per = (tiles + kScanWarps - 1) / kScanWarps, t0 = min(tiles, warp * per), t1 = min(tiles, t0 + per);
     uint32_t sum = 0;
     for (uint32_t t = t0; t < t1; ++t) sum += on ? cntV[(size_t)t * nV + b] : 0u;
     part[warp][lane] = sum;
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(256) k_scan_cols(const uint32_t *cntV, uint32_
             run += c;
         }
     }
-    if (warp == 7 && on) vstart[b] = run;  // the last warp's running sum is the column total
+    if (warp == kScanWarps - 1 && on) vstart[b] = run;  // the last warp's running sum is the column total
 }
 
 // Tile scatter: arc {vertex, k<<1|side, neighbour} -> arcs[start(bucket) + offset(bucket, tile) + rank in
@@ -1505,7 +1509,7 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 #undef TC_COUNT_CASE
         default: return 0;
     }
-    k_scan_cols<<<(nV + 31) / 32, 256, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, nV, ix.ctr);
+    k_scan_cols<<<(nV + 31) / 32, kScanWarps * 32, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, nV, ix.ctr);
     // with a split, the large-bucket list is built by k_split over the sub-buckets
     k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.bs ? 0xFFFFFFFFu : g.vcap, ix.vperm, ix.ctr);
     k_scatter<<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
