@@ -180,8 +180,12 @@ static int64_t find_edge(const edge_rec *S, int64_t n, uint32_t a, uint32_t z) {
     return -1;
 }
 
-/* bulkUpdateAll for one batch; edges = 2*w uint32 (u, v) in arrival order, any orientation. */
-int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
+/* bulkUpdateAll for one batch; edges = 2*w uint32 (u, v) in arrival order, any orientation.
+   forced_d1 / forced_d2 (test wiring, may be NULL): per estimator, the value of Step 1's draw
+   randInt(|W|+|E|) and of Step 2's draw over chi^- + chi^+ instead of the Philox + Lemire draw;
+   an out-of-range forced value rejects the batch with ORC_EINVAL (nothing is mutated). */
+static int push_batch_impl(orc *o, const uint32_t *edges, uint64_t w, const uint64_t *forced_d1,
+                           const uint64_t *forced_d2) {
     if (w == 0) return ORC_OK;
     int err_inval = 0, err_loop = 0, err_dup = 0;
     uint32_t *E = (uint32_t *)malloc(8 * w);           /* normalized W */
@@ -220,20 +224,37 @@ int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
             if (last) sum = 0; else sum += 1;
         }
     }
-    /* overflow guard (reading R13): chi <= m always, and chi must fit 31 bits */
-    if (code == ORC_OK && o->m + w > C_MAX) code = ORC_EOVERFLOW;
     if (code != ORC_OK) { free(E); free(S); free(F); free(idx); return code; }
 
     const uint64_t m_prev = o->m, seed = o->seed, first = o->first;
     const uint32_t b = o->b;
     const int64_t cnt = (int64_t)o->count;
+    /* all-or-nothing: the state is snapshotted and restored if some estimator's chi overflows
+       (reading R13) or a forced draw is out of range */
+    const uint64_t n = o->count ? o->count : 1;
+    uint32_t *s_r1 = (uint32_t *)malloc(8 * n), *s_r2 = (uint32_t *)malloc(8 * n), *s_c = (uint32_t *)malloc(4 * n);
+    uint64_t *s_p1 = (uint64_t *)malloc(8 * n), *s_p2 = (uint64_t *)malloc(8 * n);
+    uint8_t *s_cl = (uint8_t *)malloc(n);
+    if (!s_r1 || !s_r2 || !s_c || !s_p1 || !s_p2 || !s_cl) {
+        free(s_r1); free(s_r2); free(s_c); free(s_p1); free(s_p2); free(s_cl);
+        free(E); free(S); free(F); free(idx);
+        return ORC_ENOMEM;
+    }
+    memcpy(s_r1, o->r1, 8 * o->count); memcpy(s_r2, o->r2, 8 * o->count); memcpy(s_c, o->c, 4 * o->count);
+    memcpy(s_p1, o->p1, 8 * o->count); memcpy(s_p2, o->p2, 8 * o->count); memcpy(s_cl, o->closed, o->count);
+    int ovf = 0, bad_draw = 0;
 
     /* ---- Step 1: idx[i] = randInt(|W|+|E|) - |E| or null ---- */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) reduction(|:bad_draw)
     for (int64_t i = 0; i < cnt; ++i) {
-        uint64_t xlo, xhi;
-        block_words(seed, first + (uint64_t)i, b, 0, &xlo, &xhi);
-        uint64_t d1 = lemire(m_prev + w, xlo, seed, first + (uint64_t)i, b, 0x10000u);
+        uint64_t xlo, xhi, d1;
+        if (forced_d1) {
+            d1 = forced_d1[i];
+            if (d1 >= m_prev + w) { bad_draw = 1; d1 = 0; }
+        } else {
+            block_words(seed, first + (uint64_t)i, b, 0, &xlo, &xhi);
+            d1 = lemire(m_prev + w, xlo, seed, first + (uint64_t)i, b, 0x10000u);
+        }
         idx[i] = d1 >= m_prev ? (int64_t)(d1 - m_prev) : -1;
     }
     /* extract + combine */
@@ -248,7 +269,7 @@ int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
     }
 
     /* ---- Step 2 ---- */
-#pragma omp parallel for schedule(static)
+#pragma omp parallel for schedule(static) reduction(|:ovf, bad_draw)
     for (int64_t i = 0; i < cnt; ++i) {
         uint32_t u = o->r1[2 * i], v = o->r1[2 * i + 1]; /* u = min (reading R1) */
         int64_t p = idx[i] >= 0 ? idx[i] : -1;        /* footnote PAPER.md:818-821 */
@@ -257,9 +278,14 @@ int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
         uint64_t rd = av < 0 ? 0 : (p >= 0 ? F[av].rank : (uint64_t)F[av].rank + 1);
         uint64_t chi_m = o->c[i], chi_p = ld + rd;
         if (chi_p == 0) continue;
-        uint64_t xlo, xhi;
-        block_words(seed, first + (uint64_t)i, b, 0, &xlo, &xhi);
-        uint64_t d2 = lemire(chi_m + chi_p, xhi, seed, first + (uint64_t)i, b, 0x20000u);
+        uint64_t xlo, xhi, d2;
+        if (forced_d2) {
+            d2 = forced_d2[i];
+            if (d2 >= chi_m + chi_p) { bad_draw = 1; d2 = 0; }
+        } else {
+            block_words(seed, first + (uint64_t)i, b, 0, &xlo, &xhi);
+            d2 = lemire(chi_m + chi_p, xhi, seed, first + (uint64_t)i, b, 0x20000u);
+        }
         if (d2 >= chi_m) {
             uint64_t phi = d2 - chi_m;
             uint32_t src = phi < ld ? u : v;
@@ -271,6 +297,9 @@ int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
             o->p2[i] = m_prev + (uint64_t)F[k].pos;
             o->closed[i] = 0;
         }
+        /* overflow guard (reading R13): chi^- + chi^+ in 64 bits; chi must fit 31 bits (bit 31 of the
+           GPU's packed word is the closed flag).  m and positions are uint64 and not limited. */
+        if (chi_m + chi_p > C_MAX) ovf = 1;
         o->c[i] = (uint32_t)(chi_m + chi_p);
     }
 
@@ -287,11 +316,37 @@ int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) {
         if (k >= 0 && m_prev + (uint64_t)S[k].pos > o->p2[i]) o->closed[i] = 1;
     }
 
-    o->m += w;
-    o->b += 1;
+    code = bad_draw ? ORC_EINVAL : ovf ? ORC_EOVERFLOW : ORC_OK;
+    if (code != ORC_OK) {  /* reject the whole batch: restore the snapshot */
+        memcpy(o->r1, s_r1, 8 * o->count); memcpy(o->r2, s_r2, 8 * o->count); memcpy(o->c, s_c, 4 * o->count);
+        memcpy(o->p1, s_p1, 8 * o->count); memcpy(o->p2, s_p2, 8 * o->count); memcpy(o->closed, s_cl, o->count);
+    } else {
+        o->m += w;
+        o->b += 1;
+    }
+    free(s_r1); free(s_r2); free(s_c); free(s_p1); free(s_p2); free(s_cl);
     free(E); free(S); free(F); free(idx);
-    return ORC_OK;
+    return code;
 }
+
+int orc_push_batch(orc *o, const uint32_t *edges, uint64_t w) { return push_batch_impl(o, edges, w, NULL, NULL); }
+
+/* Test wiring: the same batch update with the two draws of every estimator supplied (forced). */
+int orc_push_batch_forced(orc *o, const uint32_t *edges, uint64_t w, const uint64_t *d1, const uint64_t *d2) {
+    if (!d1 || !d2) return ORC_EINVAL;
+    return push_batch_impl(o, edges, w, d1, d2);
+}
+
+/* Test wiring: overwrite estimator i's state / the counters (e.g. a chi near 2^31 or m past 2^32, to
+   exercise the overflow guard without streaming billions of edges).  No validation: tests only. */
+void orc_set_estimator(orc *o, uint64_t i, const uint32_t r1[2], uint64_t p1, const uint32_t r2[2], uint64_t p2,
+                       uint32_t c, uint8_t closed) {
+    o->r1[2 * i] = r1[0]; o->r1[2 * i + 1] = r1[1]; o->p1[i] = p1;
+    o->r2[2 * i] = r2[0]; o->r2[2 * i + 1] = r2[1]; o->p2[i] = p2;
+    o->c[i] = c; o->closed[i] = closed;
+}
+
+void orc_set_counters(orc *o, uint64_t m, uint32_t b) { o->m = m; o->b = b; }
 
 void orc_get_state(const orc *o, uint32_t *r1, uint64_t *p1, uint32_t *r2, uint64_t *p2, uint32_t *c,
                    uint8_t *closed) {

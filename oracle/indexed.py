@@ -47,6 +47,10 @@ def lib():
         L.orc_lemire_words.restype = u64
         L.orc_lemire_words.argtypes = [u64, u64, u64, u64, u32, u32]
         L.orc_threads.restype = C.c_int
+        L.orc_push_batch_forced.restype = C.c_int
+        L.orc_push_batch_forced.argtypes = [vp, vp, u64, vp, vp]
+        L.orc_set_estimator.argtypes = [vp, u64, vp, u64, vp, u64, u32, C.c_uint8]
+        L.orc_set_counters.argtypes = [vp, u64, u32]
         _lib = L
     return _lib
 
@@ -74,6 +78,23 @@ class IndexedOracle:
     def push_batch(self, edges) -> int:
         e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
         return lib().orc_push_batch(self._h, _ptr(e), e.shape[0])
+
+    def push_batch_forced(self, edges, d1, d2) -> int:
+        """Test wiring: the batch update with every estimator's Step 1 draw d1[i] (over |W|+|E|) and
+        Step 2 draw d2[i] (over chi^- + chi^+, used only when chi^+ > 0) supplied."""
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint32).reshape(-1, 2))
+        a = np.ascontiguousarray(np.asarray(d1, dtype=np.uint64).reshape(self.count))
+        b = np.ascontiguousarray(np.asarray(d2, dtype=np.uint64).reshape(self.count))
+        return lib().orc_push_batch_forced(self._h, _ptr(e), e.shape[0], _ptr(a), _ptr(b))
+
+    def set_estimator(self, i, r1, p1, r2, p2, c, closed):
+        """Test wiring: overwrite local estimator i (no validation)."""
+        a = np.asarray(r1, np.uint32)
+        b = np.asarray(r2, np.uint32)
+        lib().orc_set_estimator(self._h, int(i), _ptr(a), int(p1), _ptr(b), int(p2), int(c), int(closed))
+
+    def set_counters(self, m, b):
+        lib().orc_set_counters(self._h, int(m), int(b))
 
     def state(self):
         n = self.count

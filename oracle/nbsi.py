@@ -15,7 +15,7 @@ EMPTY edge = (0xFFFFFFFF, 0xFFFFFFFF), EMPTY position = 2^64-1.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass, field
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
@@ -196,9 +196,6 @@ class BruteOracle:
         E_W = [normalize(u, v) for (u, v) in W]
         E_lo = np.array([e[0] for e in E_W], dtype=np.int64)
         E_hi = np.array([e[1] for e in E_W], dtype=np.int64)
-        # overflow guard (reading R13): chi <= m always, and chi must fit 31 bits
-        if self.m + len(W) > C_MAX:
-            return TC_EOVERFLOW
         m_prev = self.m
         ids = np.arange(self.first, self.first + self.count, dtype=np.uint64)
         if uniform_factory is None:
@@ -207,10 +204,17 @@ class BruteOracle:
                      for i, a, c in zip(ids, xlo, xhi)]
         else:
             hooks = [uniform_factory(int(i), self.b) for i in ids]
-        for est, uniform in zip(self.ests, hooks):
+        new = [replace(e) for e in self.ests]  # all-or-nothing: commit only if no estimator overflows
+        for est, uniform in zip(new, hooks):
             step1_level1(est, E_W, m_prev, uniform)
             step2_level2(est, E_W, E_lo, E_hi, m_prev, uniform)
             step3_closing(est, E_W, m_prev)
+        # overflow guard (reading R13): chi = chi^- + chi^+ is computed exactly; a batch after which some
+        # estimator's chi exceeds 2^31 - 1 (bit 31 of the packed word is the closed flag) is rejected whole.
+        # Positions and m are unbounded (u64 in the state), so no other limit applies.
+        if any(e.c > C_MAX for e in new):
+            return TC_EOVERFLOW
+        self.ests = new
         self.m += len(W)
         self.b += 1
         return TC_OK
