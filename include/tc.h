@@ -43,7 +43,7 @@ enum {
     TC_ENOMEM = -2,      /* device or host allocation failed                                */
     TC_ESELFLOOP = -3,   /* u == v in the batch (the graph is simple)          */
     TC_EDUP = -4,        /* the same undirected pair twice in one batch  */
-    TC_EOVERFLOW = -5,   /* m would exceed 2^31-1: chi <= m must fit 31 bits (reading R13)  */
+    TC_EOVERFLOW = -5,   /* chi overflow (reading R13), or the library limit m <= 2^31-1    */
     TC_ECUDA = -6,       /* a CUDA call failed; the handle is poisoned                      */
     TC_ESTATE = -8,      /* handle poisoned by an earlier asynchronous error               */
     TC_EPARSE = -9,      /* malformed edge-list line (tc_parse_edges / tc_ingest_file)      */
@@ -72,11 +72,21 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
  *  Rejects the whole batch (state and counters unchanged) with, in this priority order:
  *  TC_EINVAL (an id 0xFFFFFFFF), TC_ESELFLOOP, TC_EDUP, TC_EOVERFLOW.  Edges that repeat an edge of
  *  an EARLIER batch are not detected (each edge arrives once).
+ *  LIBRARY LIMIT: stream positions are stored in 32 bits on the device, so a batch that would take m past
+ *  2^31 - 1 edges is rejected with TC_EOVERFLOW (reading R13).  This is a restriction of this
+ *  library, not of the method (the oracle keeps u64 positions); below it chi <= m - 1 cannot overflow its
+ *  31 bits either.  In asynchronous mode this limit is checked before enqueueing and returned at once.
  *  In the default strict mode the call synchronises and returns the batch's status; with
  *  tc_set_async(ctx, 1) it returns TC_OK after enqueueing, a failure is reported by the next
- *  synchronising call, and the handle is then poisoned (TC_ESTATE) -- its state stays that of the
- *  last accepted batch. */
+ *  synchronising call, and the handle is then poisoned (TC_ESTATE) -- its state and counters stay
+ *  those of the last accepted batch (tc_get_state, tc_counters and tc_reset still work on it). */
 int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w);
+
+/* tc_push_batch_after -- tc_push_batch for a DEVICE batch produced by work queued on producer_stream (a
+ * cudaStream_t as void*; NULL = no ordering, i.e. tc_push_batch): the handle's stream first waits for
+ * everything enqueued on producer_stream so far (an event; no host synchronisation), so the batch may still
+ * be being written when the call is made.  Same arguments, semantics and errors as tc_push_batch. */
+int tc_push_batch_after(tc_ctx *ctx, const tc_edge *edges, uint64_t w, void *producer_stream);
 
 /* tc_estimate -- the mean of the coarse estimates X_i = chi_i * m if f3_i != empty else 0
  * (Lemma unbiased-est), over ALL r estimators, computed as
@@ -132,7 +142,9 @@ int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint
 /* tc_set_state -- checkpoint restore: overwrite local estimators [first, first+count)
  * from HOST arrays in tc_get_state's layout (all pointers required when count > 0).  Validated first
  * (TC_EINVAL and nothing written unless every r1 / r2 is empty with position UINT64_MAX or has lo < hi and
- * a position < 2^31 - 1, c < 2^31 and closed in {0, 1}).  The closed sum S is recomputed.  Together with
+ * a position < 2^31 - 1, c < 2^31 and closed in {0, 1}, and the NBSI invariants the estimator pass relies
+ * on hold: an empty f1 has an empty f2, c = 0 and closed = 0; c == 0 iff f2 is empty;
+ * closed implies f2 present; f2 shares exactly one endpoint with f1 and p1 < p2).  The closed sum S is recomputed.  Together with
  * tc_set_counters this resumes a stream exactly: the next push draws with the restored batch index.
  * Synchronises. */
 int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1, const uint64_t *p1,
@@ -142,7 +154,9 @@ int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1
  * recomputes S.  Synchronises. */
 int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches);
 
-/* tc_counters -- m (edges accepted so far) and the number of accepted non-empty batches. */
+/* tc_counters -- m (edges accepted so far) and the number of accepted non-empty batches.  In asynchronous
+ * mode it synchronises first, so that a batch rejected after it was enqueued is not counted (on a handle
+ * poisoned that way it returns the counters of the last accepted batch, matching tc_get_state). */
 int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches);
 
 /* tc_set_async -- 0 = strict (default: each push synchronises and reports its status);
@@ -253,6 +267,21 @@ typedef struct {
  * where; batches before it may already have been pushed -- stats->edges of them), or any tc_push_batch
  * code.  Synchronises at the end (tc_sync).  stats may be NULL. */
 int tc_ingest_file(tc_ctx *ctx, const char *path, uint64_t w, int flags, tc_ingest_stats *stats);
+
+/* ------------------------------------------------------------------------------------------- */
+/* Test hooks (not on the path): the estimator pass's own device functions on chosen inputs, on the
+ * current CUDA device, host arrays in and out, synchronous.                                     */
+
+/* tc_test_draws -- out[i] = the device bounded uniform (Lemire multiply-shift with rejection, DESIGN.md
+ * reading R8) of n[i] (> 0) from the first 64-bit word x[i], retries drawn from Philox4x32-10 with key
+ * seed and counter (id[i].lo32, id[i].hi32, b[i], base[i] + t) (reading R7), exactly as the estimator pass
+ * calls it.  TC_EINVAL on a NULL array or an n[i] = 0. */
+int tc_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b,
+                  const uint32_t *base, uint64_t seed, uint64_t count, uint64_t *out);
+
+/* tc_test_philox -- out[4i..4i+3] = the device Philox4x32-10 block of counter ctr[4i..4i+3] and key
+ * key[2i..2i+1]. */
+int tc_test_philox(const uint32_t *ctr, const uint32_t *key, uint64_t count, uint32_t *out);
 
 /* tc_strerror -- a static, never-NULL description of a TC_* code (owned by the library). */
 const char *tc_strerror(int code);

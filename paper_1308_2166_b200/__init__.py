@@ -14,7 +14,8 @@ import numpy as np
 from . import _lib
 from ._lib import PHASES, TCError
 
-__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators", "exact_triangles", "parse_edges"]
+__all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators", "exact_triangles", "parse_edges",
+           "test_draws", "test_philox"]
 
 
 def load_library():
@@ -56,6 +57,39 @@ def parse_edges(text: bytes, final: bool = True, skip_loops: bool = False, cap: 
         err.line = int(lines.value)
         raise err
     return out[:n.value].copy(), int(used.value), int(lines.value)
+
+
+def test_draws(n, x, ids, b, base, seed):
+    """tc_test_draws: the device bounded uniform on chosen inputs (uint64 arrays n, x, ids; uint32 b, base)."""
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    n, x, ids = (np.ascontiguousarray(v, dtype=np.uint64) for v in (n, x, ids))
+    b, base = (np.ascontiguousarray(v, dtype=np.uint32) for v in (b, base))
+    out = np.empty(len(n), np.uint64)
+    rc = _lib.load().tc_test_draws(P(n), P(x), P(ids), P(b), P(base), int(seed), len(n), P(out))
+    if rc != 0:
+        raise TCError(rc, "tc_test_draws")
+    return out
+
+
+def test_philox(ctr, key):
+    """tc_test_philox: device Philox4x32-10 blocks; ctr (k, 4) and key (k, 2) uint32 -> (k, 4) uint32."""
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    ctr = np.ascontiguousarray(ctr, dtype=np.uint32).reshape(-1, 4)
+    key = np.ascontiguousarray(key, dtype=np.uint32).reshape(-1, 2)
+    out = np.empty_like(ctr)
+    rc = _lib.load().tc_test_philox(P(ctr), P(key), ctr.shape[0], P(out))
+    if rc != 0:
+        raise TCError(rc, "tc_test_philox")
+    return out
+
+
+def _producer_stream(edges):
+    """cudaStream_t (int) of torch's current stream when edges is a CUDA tensor (the stream that produced
+    it, by torch's convention), else None."""
+    if type(edges).__module__.startswith("torch") and edges.is_cuda:
+        import torch
+        return torch.cuda.current_stream(edges.device).cuda_stream
+    return None
 
 
 def _edges_ptr(edges):
@@ -108,8 +142,14 @@ class TriangleCounter:
 
     # -- the path ------------------------------------------------------------------------------
     def push_batch(self, edges, check: bool = True) -> int:
+        """tc_push_batch; a CUDA tensor goes through tc_push_batch_after with torch's current stream as the
+        producer, so the engine's stream waits for the kernels / copies that wrote it."""
         ptr, w, keep = _edges_ptr(edges)
-        rc = _lib.load().tc_push_batch(self._h, ptr, int(w))
+        prod = _producer_stream(edges)
+        if prod is not None:
+            rc = _lib.load().tc_push_batch_after(self._h, ptr, int(w), C.c_void_p(prod))
+        else:
+            rc = _lib.load().tc_push_batch(self._h, ptr, int(w))
         del keep
         if check and rc != 0:
             raise TCError(rc, "tc_push_batch")

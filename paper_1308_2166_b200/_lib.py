@@ -24,7 +24,7 @@ TC_NPHASES = 4
 PHASES = ("partition", "pairs", "vertices", "update")
 TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4, "small_batch": 6}
 
-EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
+EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_push_batch_after", "tc_test_draws", "tc_test_philox", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_closed_sum_async", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_set_state", "tc_set_counters", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
            "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_parse_edges", "tc_ingest_file", "tc_strerror",
            "tc_last_error"]
@@ -58,6 +58,9 @@ def load(path: str = LIB_PATH):
         "tc_create": (vp, [u64, u64]),
         "tc_create_shard": (vp, [u64, u64, u64, u64, i32, u64]),
         "tc_push_batch": (i32, [vp, vp, u64]),
+        "tc_push_batch_after": (i32, [vp, vp, u64, vp]),
+        "tc_test_draws": (i32, [vp, vp, vp, vp, vp, u64, u64, vp]),
+        "tc_test_philox": (i32, [vp, vp, u64, vp]),
         "tc_estimate": (i32, [vp, C.POINTER(C.c_double)]),
         "tc_reset": (i32, [vp]),
         "tc_destroy": (None, [vp]),

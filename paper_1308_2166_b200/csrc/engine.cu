@@ -42,11 +42,16 @@ struct tc_ctx {
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
+    // asynchronous mode: m before each batch enqueued since the last clean settle (batch indices
+    // async_b0, async_b0 + 1, ...), so that a rejected batch found later can be rolled back to
+    std::vector<uint64_t> async_mprev;
+    uint32_t async_b0 = 0;
     uint32_t last_launches = 0;
     StateBufs st;
     IndexBufs ix;
     uint32_t *h_err = nullptr;  // pinned
     cudaEvent_t copy_done = nullptr;
+    cudaEvent_t produced = nullptr;  // tc_push_batch_after: the producer stream's work so far
     // profiling
     int prof = 0;
     // begin / end events of each phase, one set per profiled push (read and recycled at the next sync)
@@ -83,11 +88,15 @@ constexpr uint64_t kMaxBatch = 1ull << 28;  // 32-bit table offsets (vertex slic
 constexpr uint64_t kStartWords = kMaxBuckets + 8;  // vstart: bucket sizes -> prefixes (+ grand total)
 
 // (Re)allocate the per-batch index for batches of up to w edges.
+extern "C" {
+static int settle(tc_ctx *ctx);
+}
+
 static int grow_index(tc_ctx *ctx, uint64_t w) {
     if (w <= ctx->ix.wcap) return TC_OK;
-    CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaStreamSynchronize(ctx->side));
-    CK(cudaStreamSynchronize(ctx->side2));
+    // the counters hold the only copy of the sticky asynchronous error word: surface it first
+    const int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
     CK(cudaStreamSynchronize(ctx->copy));
     free_index(ctx->ix);
     IndexBufs &ix = ctx->ix;
@@ -113,6 +122,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     }
     ix.wcap = cap;
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+    CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
     CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)cap), ctx->stream));  // tag 0: free
     ctx->ptag = 0;
     return TC_OK;
@@ -132,6 +142,7 @@ static void destroy_ctx(tc_ctx *ctx) {
     cudaFree(ctx->st.stats);
     if (ctx->h_err) cudaFreeHost(ctx->h_err);
     if (ctx->copy_done) cudaEventDestroy(ctx->copy_done);
+    if (ctx->produced) cudaEventDestroy(ctx->produced);
     for (auto &set : ctx->ev_pool)
         for (auto &e : set)
             if (e) cudaEventDestroy(e);
@@ -210,7 +221,8 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
               cudaMalloc(&ctx->st.p2, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
               cudaMalloc(&ctx->st.stats, 40) == cudaSuccess &&
               cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
-              cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess;
+              cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess &&
+              cudaEventCreateWithFlags(&ctx->produced, cudaEventDisableTiming) == cudaSuccess;
     if (ok) {
         ok = cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream) == cudaSuccess &&
              cudaMemsetAsync(ctx->st.stats, 0, 40, ctx->stream) == cudaSuccess;
@@ -241,6 +253,8 @@ static int decode_err(uint32_t e) {
     return TC_OK;
 }
 
+static int recompute_S(tc_ctx *ctx);
+
 // Wait for queued work and surface a pending asynchronous batch error (poisons the handle).
 static int settle(tc_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
@@ -248,12 +262,24 @@ static int settle(tc_ctx *ctx) {
     CK(cudaStreamSynchronize(ctx->side));
     CK(cudaStreamSynchronize(ctx->side2));
     if (ctx->async_errors && !ctx->poisoned && ctx->ix.ctr) {
-        CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost));
-        const int code = decode_err(*ctx->h_err);
+        CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr, 4 * kCtrWords, cudaMemcpyDeviceToHost));
+        const int code = decode_err(ctx->h_err[kCtrErr]);
         if (code != TC_OK) {
+            // the first batch whose estimator pass found the sticky error word set is the rejected one:
+            // m and the batch count go back to what they were before it (all later batches were skipped)
+            const uint32_t fb = ctx->h_err[kCtrFailB];
+            if (fb >= ctx->async_b0 && fb - ctx->async_b0 < ctx->async_mprev.size()) {
+                ctx->m = ctx->async_mprev[fb - ctx->async_b0];
+                ctx->b = fb;
+            }
+            ctx->async_mprev.clear();
+            ctx->async_b0 = ctx->b;
             ctx->poisoned = code;
-            return code;
+            const int rs = recompute_S(ctx);  // later skipped batches reset the S slots
+            return rs != TC_OK ? rs : code;
         }
+        ctx->async_mprev.clear();
+        ctx->async_b0 = ctx->b;
     }
     for (size_t i = 0; i < ctx->ev_used; ++i) {  // completed profiled pushes
         for (int p = 0; p < TC_NPHASES; ++p) {
@@ -339,7 +365,8 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         // k_count zeroes the counters and this batch's S; the error word is sticky in asynchronous mode and
         // cleared (or set to the overflow error) here in strict mode
         if (!ctx->async_errors)
-            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, 0, 4, ms) == cudaSuccess;
+            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, 0, 4, ms) == cudaSuccess &&
+                 cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ms) == cudaSuccess;
         if (!ctx->async_errors && ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
         // a1: count, scans, scatter
         rec(2 * TC_PHASE_PARTITION, ms);
@@ -403,11 +430,26 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         const int code = decode_err(*ctx->h_err);
         if (code != TC_OK) return code;  // nothing was mutated: k_update bailed out
     }
+    if (ctx->async_errors) {
+        if (ctx->async_mprev.empty()) ctx->async_b0 = ctx->b;
+        ctx->async_mprev.push_back(ctx->m);
+    }
     ctx->m += w;
     ctx->b += 1;
     ctx->S_slot = slot;
     ctx->last_launches = launches;
     return TC_OK;
+}
+
+int tc_push_batch_after(tc_ctx *ctx, const tc_edge *edges, uint64_t w, void *producer_stream) {
+    if (!ctx) return TC_EINVAL;
+    if (producer_stream && w) {
+        if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaEventRecord(ctx->produced, (cudaStream_t)producer_stream));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->produced, 0));
+    }
+    return tc_push_batch(ctx, edges, w);
 }
 
 int tc_set_graphs(tc_ctx *ctx, int enable) {
@@ -444,19 +486,32 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
     }
 }
 
+// settle() for calls that are allowed on a handle poisoned by a rejected asynchronous batch (its state is
+// that of the last accepted batch): only a CUDA failure is an error for them.
+static int settle_allow_poisoned(tc_ctx *ctx) {
+    const int rc = settle(ctx);
+    if (rc == TC_OK || (ctx->poisoned && ctx->poisoned != TC_ECUDA && rc != TC_ECUDA)) return TC_OK;
+    return rc;
+}
+
 int tc_reset(tc_ctx *ctx) {
     if (!ctx) return TC_EINVAL;
-    int rc = settle(ctx);
-    if (rc != TC_OK && rc != TC_ESTATE) return rc;
+    int rc = settle_allow_poisoned(ctx);
+    if (rc != TC_OK) return rc;
     launch_init_state(ctx->st, ctx->stream);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream));
-    if (ctx->ix.ctr) CK(cudaMemsetAsync(ctx->ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+    if (ctx->ix.ctr) {
+        CK(cudaMemsetAsync(ctx->ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+        CK(cudaMemsetAsync(ctx->ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
+    }
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->m = 0;
     ctx->b = 0;
     ctx->S_slot = -1;
     ctx->poisoned = 0;
+    ctx->async_mprev.clear();
+    ctx->async_b0 = 0;
     return TC_OK;
 }
 
@@ -536,8 +591,9 @@ int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out) {
     const uint64_t n = ctx->count;
     for (uint32_t g = 0; g < groups; ++g) {
         const uint64_t lo = (uint64_t)g * n / groups, hi = (uint64_t)(g + 1) * n / groups;
-        // group mean of X_i = chi_i * m: m * S_g / |g|, same expression order as the oracle
-        means[g] = (double)(ctx->m * S[g]) / (double)(hi - lo);
+        // group mean of X_i = chi_i * m: (double)m * (double)S_g / (double)|g|, the oracle's expression
+        // (nbsi.median_of_means); no 64-bit product m * S_g, which could wrap
+        means[g] = (double)ctx->m * (double)S[g] / (double)(hi - lo);
     }
     std::sort(means.begin(), means.end());
     *out = means[(groups - 1) / 2];
@@ -547,8 +603,8 @@ int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out) {
 int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint64_t *p1, uint32_t *r2,
                  uint64_t *p2, uint32_t *c, uint8_t *closed) {
     if (!ctx || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
-    int rc = settle(ctx);
-    if (rc != TC_OK && rc != TC_ESTATE) return rc;
+    int rc = settle_allow_poisoned(ctx);
+    if (rc != TC_OK) return rc;
     if (count == 0) return TC_OK;
     if (r1) CK(cudaMemcpy(r1, ctx->st.r1 + first, 8 * count, cudaMemcpyDeviceToHost));
     if (r2) CK(cudaMemcpy(r2, ctx->st.r2 + first, 8 * count, cudaMemcpyDeviceToHost));
@@ -604,6 +660,16 @@ int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1
             (f ? q2 : q1)[i] = empty ? 0xFFFFFFFFu : (uint32_t)p;
         }
         if (c[i] > kCMask || closed[i] > 1) return TC_EINVAL;
+        // NBSI as the estimator pass relies on it: an empty f1 has nothing else;
+        // chi == 0 <=> f2 empty; closed => f2 present; f2 after f1 and sharing exactly one endpoint
+        const bool e1 = q1[i] == 0xFFFFFFFFu, e2 = q2[i] == 0xFFFFFFFFu;
+        if (e1 && (!e2 || c[i] || closed[i])) return TC_EINVAL;
+        if ((c[i] == 0) != e2 || (closed[i] && e2)) return TC_EINVAL;
+        if (!e2) {
+            const uint32_t a0 = r1[2 * i], a1 = r1[2 * i + 1], b0 = r2[2 * i], b1 = r2[2 * i + 1];
+            const int shared = (a0 == b0) + (a0 == b1) + (a1 == b0) + (a1 == b1);
+            if (shared != 1 || q2[i] <= q1[i]) return TC_EINVAL;
+        }
         cf[i] = c[i] | (closed[i] ? kClosedBit : 0u);
     }
     if (count) {
@@ -627,6 +693,10 @@ int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches) {
 
 int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches) {
     if (!ctx) return TC_EINVAL;
+    if (ctx->async_errors) {  // enqueued batches count only once they are known to be accepted
+        const int rc = settle_allow_poisoned(ctx);
+        if (rc != TC_OK) return rc;
+    }
     if (m) *m = ctx->m;
     if (batches) *batches = ctx->b;
     return TC_OK;
@@ -680,6 +750,56 @@ int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {
     if (!ctx || !launches) return TC_EINVAL;
     *launches = ctx->last_launches;
     return TC_OK;
+}
+
+// Test hooks: copy host arrays in, run the device function, copy the results out (own stream-less path on
+// the current device; synchronous).
+int tc_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b, const uint32_t *base,
+                  uint64_t seed, uint64_t count, uint64_t *out) {
+    if (!count) return TC_OK;
+    if (!n || !x || !id || !b || !base || !out) return TC_EINVAL;
+    for (uint64_t i = 0; i < count; ++i)
+        if (n[i] == 0) return TC_EINVAL;
+    uint64_t *d = nullptr;
+    const size_t B8 = 8 * count, B4 = 4 * count;
+    if (cudaMalloc(&d, 4 * B8 + 2 * B4) != cudaSuccess) {
+        cudaGetLastError();
+        return TC_ENOMEM;
+    }
+    uint64_t *dn = d, *dx = d + count, *did = d + 2 * count, *dout = d + 3 * count;
+    uint32_t *db = reinterpret_cast<uint32_t *>(d + 4 * count), *dbase = db + count;
+    bool ok = cudaMemcpy(dn, n, B8, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(dx, x, B8, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(did, id, B8, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(db, b, B4, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(dbase, base, B4, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) {
+        launch_test_draws(dn, dx, did, db, dbase, seed, count, dout, 0);
+        ok = cudaGetLastError() == cudaSuccess && cudaMemcpy(out, dout, B8, cudaMemcpyDeviceToHost) == cudaSuccess;
+    }
+    cudaFree(d);
+    if (!ok) cudaGetLastError();
+    return ok ? TC_OK : TC_ECUDA;
+}
+
+int tc_test_philox(const uint32_t *ctr, const uint32_t *key, uint64_t count, uint32_t *out) {
+    if (!count) return TC_OK;
+    if (!ctr || !key || !out) return TC_EINVAL;
+    uint32_t *d = nullptr;
+    if (cudaMalloc(&d, 40 * count) != cudaSuccess) {
+        cudaGetLastError();
+        return TC_ENOMEM;
+    }
+    uint32_t *dc = d, *dk = d + 4 * count, *dout = d + 6 * count;
+    bool ok = cudaMemcpy(dc, ctr, 16 * count, cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(dk, key, 8 * count, cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) {
+        launch_test_philox(dc, dk, count, dout, 0);
+        ok = cudaGetLastError() == cudaSuccess && cudaMemcpy(out, dout, 16 * count, cudaMemcpyDeviceToHost) == cudaSuccess;
+    }
+    cudaFree(d);
+    if (!ok) cudaGetLastError();
+    return ok ? TC_OK : TC_ECUDA;
 }
 
 const char *tc_strerror(int code) {

@@ -55,6 +55,7 @@ constexpr int kCtrBig = 2;     // vertex buckets larger than vcap (k_vhub's)
 constexpr int kCtrErr = 3;     // error bits
 constexpr int kCtrDefer = 4;   // buckets k_vhub deferred to k_vbig
 constexpr int kCtrTicket2 = 5; // k_vbig's bucket ticket
+constexpr int kCtrFailB = 6;   // batch index of the first batch that found the error word set (async mode)
 constexpr int kCtrWords = 16;
 
 struct __align__(16) VSlot {

@@ -185,7 +185,8 @@ constexpr uint32_t kArcsPerWarp = kArcRounds * 32, kEdgesPerWarp = kEdgeRounds *
 template <int NB>  // the partition bits a.g.bp1, as a compile-time constant
 __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
     if (blockIdx.x == 0) {  // per-batch resets (every later kernel of the batch starts after this one)
-        if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr) a.ctr[threadIdx.x] = 0u;
+        if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
+            a.ctr[threadIdx.x] = 0u;
         if (threadIdx.x == 0) *a.S_reset = 0ull;
     }
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
@@ -1196,7 +1197,7 @@ struct UpdateIdx {
     Lookup L;
     const uint4 *einfo;
     const uint2 *segS;
-    const uint32_t *ctr;
+    uint32_t *ctr;
 };
 
 struct EstState {
@@ -1369,7 +1370,13 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
 template <bool kSmall>
 __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
                                                    unsigned long long *stats, const uint32_t *filt) {
-    if (ix.ctr[kCtrErr]) return;
+    if (ix.ctr[kCtrErr]) {  // this batch (or, in asynchronous mode, an earlier one) was rejected: no update
+        // the first batch to see the sticky error word is the one that set it: record its index so that the
+        // host can restore m and the batch count of the last accepted batch
+        if (blockIdx.x == 0 && threadIdx.x == 0 && ix.ctr[kCtrFailB] == 0xFFFFFFFFu)
+            ix.ctr[kCtrFailB] = u.batch;
+        return;
+    }
     __shared__ uint32_t sf[kSmall ? kFilterWords : 1];
     if (kSmall) {
         const uint4 *src = reinterpret_cast<const uint4 *>(filt);
@@ -1448,6 +1455,34 @@ __global__ void k_group_sums(const uint32_t *__restrict__ cf, uint64_t n, uint32
         const uint64_t g = ((t + 1) * G + n - 1) / n - 1;
         atomicAdd(out + g, (unsigned long long)(v & kCMask));
     }
+}
+
+// Test hooks (tc_test_draws / tc_test_philox): the estimator pass's own device functions on chosen inputs.
+__global__ void k_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b,
+                             const uint32_t *base, uint64_t seed, uint64_t count, uint64_t *out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const DrawCtx dc{id[t], b[t], PhiloxKey{(uint32_t)seed, (uint32_t)(seed >> 32)}};
+    out[t] = bounded(n[t], x[t], dc, base[t]);
+}
+
+__global__ void k_test_philox(const uint4 *ctr, const uint2 *key, uint64_t count, uint4 *out) {
+    const uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    out[t] = philox4x32_10(ctr[t], PhiloxKey{key[t].x, key[t].y});
+}
+
+int launch_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b, const uint32_t *base,
+                      uint64_t seed, uint64_t count, uint64_t *out, cudaStream_t s) {
+    k_test_draws<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(n, x, id, b, base, seed, count, out);
+    return 1;
+}
+
+int launch_test_philox(const uint32_t *ctr, const uint32_t *key, uint64_t count, uint32_t *out, cudaStream_t s) {
+    k_test_philox<<<(unsigned)((count + 255) / 256), 256, 0, s>>>(reinterpret_cast<const uint4 *>(ctr),
+                                                                  reinterpret_cast<const uint2 *>(key), count,
+                                                                  reinterpret_cast<uint4 *>(out));
+    return 1;
 }
 
 // ------------------------------------------------------------------------------------------------

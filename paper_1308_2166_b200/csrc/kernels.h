@@ -94,6 +94,10 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
 int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *out, cudaStream_t s);
 
+int launch_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b, const uint32_t *base,
+                      uint64_t seed, uint64_t count, uint64_t *out, cudaStream_t s);
+int launch_test_philox(const uint32_t *ctr, const uint32_t *key, uint64_t count, uint32_t *out, cudaStream_t s);
+
 int sm_count();
 int set_kernel_attributes();  // dynamic shared memory limits on the current device
 

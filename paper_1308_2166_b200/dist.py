@@ -80,6 +80,8 @@ class ShardedCounter:
             fill(buf)
             return buf[:w], None
         self.comm.wait_event(self.consumed[i])
+        # rank 0's source tensor (or a host staging copy) may still be being produced on the caller's stream
+        self.comm.wait_stream(torch.cuda.current_stream(self.device))
         with torch.cuda.stream(self.comm):
             fill(buf)
             ready = torch.cuda.Event()
@@ -146,10 +148,15 @@ class ShardedCounter:
         src = src.view(torch.int32).reshape(w, 2)
         lo, hi = self.rank * per, min(w, (self.rank + 1) * per)
 
+        if getattr(self, "_slice", None) is None or self._slice.shape[0] < per:
+            self._slice = torch.zeros((per, 2), dtype=torch.int32, device=self.device)
+
         def fill(buf):
-            mine = torch.zeros((per, 2), dtype=torch.int32, device=self.device)
+            mine = self._slice[:per]
             if hi > lo:
                 mine[: hi - lo].copy_(src[lo:hi], non_blocking=True)
+            if hi - lo < per:
+                mine[max(0, hi - lo):].zero_()
             dist.all_gather_into_tensor(buf[: per * self.world], mine, group=self.group)
 
         batch, tok = self._exchange(fill, w)
