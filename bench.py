@@ -2,22 +2,24 @@
 """Benchmark of the per-batch update of r neighborhood-sampling estimators (bulkUpdateAll,
 PAPER.md:494-505) on B200.
 
-One step = one tc_push_batch of the next w edges of the synthetic stream (all §8(a) rows: staging,
-incidence index, edge-pair hash, fused Steps 1-3 + partial sums).  Default workload = BASELINE.json
-configs[1] (C2: R-MAT scale 20, ~15.7M edges, r = w = 2^20): the full stream is 15 batches, so the
-default --steps 15 times one whole stream through a fresh estimator set.
+One step = one tc_push_batch of the next w edges of the synthetic stream (all SURVEY 8(a) rows: staging,
+incidence index, edge-pair hash, fused Steps 1-3 + partial sums).  BASELINE.json's metric names no config,
+so the N = 1 workload is the largest single-GPU config, configs[2] = C3 (Chung-Lu gamma 2.1, 3M vertices,
+117M edges, r = 2^22, w = 2^23: 14 batches per stream).  Steps run through the stream in order; when it is
+exhausted a new pass starts from a reset estimator set (the reset is untimed).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
 
-Multi-GPU (torchrun, one process per GPU): estimators are sharded by global id; rank 0 holds the
-stream and broadcasts each batch over NCCL inside the timed region; the estimate all-reduces the
-per-rank exact partial sums.  Prints ONE JSON line on rank 0.
+Multi-GPU (torchrun, one process per GPU): estimators are sharded by global id; rank 0 holds the stream
+and broadcasts each batch over NCCL inside the timed region; the estimate all-reduces the per-rank exact
+partial sums.  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -37,9 +39,9 @@ L2_FLUSH_BYTES = 256 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=150)
+    ap.add_argument("--steps", type=int, default=28)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--w", type=int, default=0, help="override the batch size (C5 sweep)")
@@ -47,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--tune", action="append", default=[], help="index-geometry knob key=value (tc_tune)")
     ap.add_argument("--no-graphs", action="store_true", help="plain stream launches instead of one CUDA graph per push")
+    ap.add_argument("--no-profile-pass", action="store_true", help="skip the per-kernel attribution pass")
+    ap.add_argument("--cpu-batches", type=int, default=0, help="batches in the cpu_baseline sample (0: auto)")
     return ap.parse_args()
 
 
@@ -142,77 +146,54 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def committed_traffic(config):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the committed
-    `ncu --set full` capture (profiles/traffic.json), or None."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
+def committed_ncu(config):
+    """Per-kernel DRAM traffic and L2 hit rates for this config from the committed ncu capture
+    (profiles/ncu_pipeline_<config>.json: application replay with --cache-control none, so each kernel is
+    measured with the L2 contents the pipeline leaves it), or {}."""
+    p = os.path.join(ROOT, "profiles", f"ncu_pipeline_{config}.json")
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f).get(config)
-        if d:
-            return d.get("traffic_bytes_per_launch")
-    return None
+            return json.load(f)
+    return {}
 
 
-def committed_limiters(kernel="k_update"):
-    """What bounds the dominant kernel besides HBM, from the committed `ncu --set full` summary
-    (profiles/ncu_full_r01.json): L2 throughput, issue activity, occupancy and the top stall reason."""
-    p = os.path.join(ROOT, "profiles", "ncu_full_r01.json")
-    if not os.path.exists(p):
-        return None
-    with open(p) as f:
-        rows = [x for x in json.load(f) if x.get("kernel", "").split("<")[0] == kernel]
-    if not rows:
-        return None
-    x = rows[-1]
-
-    def num(k):
-        try:
-            return float(str(x.get(k, "")).split()[0])
-        except (ValueError, IndexError):
-            return None
-    return {"kernel": kernel, "lts_throughput_pct": num("lts__throughput.avg.pct_of_peak_sustained_elapsed"),
-            "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-            "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
-            "warp_instructions_per_launch": num("smsp__inst_executed.sum"),
-            "top_stall": (x.get("top_stalls") or [[None]])[0][0],
-            "source": "profiles/ncu_full_r01.json (cold-L2 replay)"}
-
-
-def limiters_with_issue(lim, launch_ms):
-    """Add the issue-rate view: the committed capture's warp instructions per launch over this run's launch
-    time, against 4 warp instructions per SM per cycle at the SM clock the recipe gives for B200
-    (148 SMs x 4 x 1.965 GHz)."""
-    if not lim or not lim.get("warp_instructions_per_launch") or not launch_ms:
-        return lim
-    peak = 148 * 4 * 1.965e9
-    ach = lim["warp_instructions_per_launch"] / (launch_ms * 1e-3)
-    lim = dict(lim)
-    lim["issue"] = {"achieved_warp_inst_per_s": ach, "peak_warp_inst_per_s": peak, "frac": ach / peak}
-    return lim
+def cpu_info():
+    model = platform.processor() or ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
 
 
 # --------------------------------------------------------------------------------------------------
-def algorithmic_bytes(phase, w, R, D, fresh, r2old, skipped=0):
-    """Algorithmic bytes per launch: what each phase must move at minimum.
-
-    update    : 24 B per retained estimator (read r1 8 + cf 4 + r2 8, write cf 4), 28 B per fresh one
-                (write cf 4, r1 8, p1 4, r2 8, p2 4), +12 B per retained estimator whose f2 is replaced
-                (r2, p2); 20 B (no write) per estimator the small-batch pass skips as untouched; the index
-                probes are not counted (the byte model of SURVEY §8d).
-    partition : read the batch once 8 B/edge; write E 8, the two bucketed arcs 16, the bucketed edge 16 B/edge.
-    pairs     : read the bucketed edge 16 B, write its 2 table slots 16 B.
-    vertices  : read the two bucketed arcs 16 B, write segS 8 + einfo 16 B per edge; 32 B (2 slots) per vertex.
-    """
-    if phase == "update":
-        return 24 * (R - fresh) + 28 * fresh + 12 * r2old - 4 * skipped
-    if phase == "partition":
-        return 48 * w
-    if phase == "pairs":
-        return 32 * w
-    if phase == "vertices":
-        return 40 * w + 32 * D
-    raise KeyError(phase)
+# Algorithmic bytes (SURVEY 8(d) byte model, DESIGN.md section 7): what each kernel MUST move, per launch.
+#   Ke (staging): read the batch 8 B/edge, write E 8 B/edge  -> k_count; write 2 arcs x 8 B -> k_scatter
+#   Ki (index)  : 8 B per arc grouped + 16 B per distinct vertex (16w + 16D)  -> k_vhash, k_vhub (+k_vbig)
+#   Kp (pairs)  : read E 8 B/edge + one 16 B pair slot per edge (24w)        -> k_pairs
+#   Ku (update) : 24 B per estimator (read r1, c, r2 20 B, write c 4 B) + 16 B per replaced r1 (r1, p1)
+#                 + 16 B per replaced r2 (r2, p2): B_est = 24 + 16 (P_r1 + P_r2)
+#   k_scan_*, k_split: 0 (implementation overhead of the grouping; it shows up as a lower fraction)
+# Whole step, the minimal model: w B_edge + R B_est with B_edge = 40 + 16 D/w.
+def kernel_bytes(kernel, w, st, R):
+    arcs = 2 * w
+    if kernel == "k_count":
+        return 16 * w
+    if kernel == "k_scatter":
+        return 16 * w
+    if kernel == "k_pairs":
+        return 24 * w
+    if kernel == "k_vhash":
+        return 8 * (arcs - st["arcs_big"]) + 16 * (st["vertices"] - st["vertices_big"])
+    if kernel == "k_vhub":
+        return 8 * st["arcs_big"] + 16 * st["vertices_big"]
+    if kernel == "k_update":
+        return 24 * R + 32 * st["fresh"] + 16 * st["r2_replaced_retained"] - 4 * st["skipped"]
+    return 0
 
 
 def run_b200(args):
@@ -233,14 +214,18 @@ def run_b200(args):
     cfg = dict(CONFIGS[args.config])
     r = cfg["r"]
     w = args.w or cfg["w"]
+    t_gen = time.perf_counter()
     stream = config_stream(args.config)
+    t_gen = time.perf_counter() - t_gen
     m_total = len(stream)
     nb = (m_total + w - 1) // w
     first = rank * r // world
     count = (rank + 1) * r // world - first
 
-    # stream resident in HBM before timing ("excluding I/O"); rank 0 owns it
-    dstream = torch.from_numpy(stream.view(np.int32)).to(dev) if rank == 0 else None
+    # stream resident in HBM before timing ("excluding I/O"); rank 0 owns it.  C4's ~1B
+    # edges (8 GB) stay in host memory: only the e2e leg (pinned host feed) runs for it
+    resident = args.config != "C4"
+    dstream = torch.from_numpy(stream.view(np.int32)).to(dev) if (rank == 0 and resident) else None
     flush = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     flush_sink = torch.zeros((), dtype=torch.float32, device=dev)
 
@@ -253,11 +238,12 @@ def run_b200(args):
             tc_.tune(**knobs)
         return tc_
 
-    # one shard of the estimators per rank; rank 0 broadcasts each batch on the library's stream (NCCL over
-    # NVLink: the per-batch exchange, inside the timed step)
+    # one shard of the estimators per rank; rank 0 broadcasts each batch (NCCL over NVLink: the per-batch
+    # exchange, inside the timed step)
     sc = ShardedCounter(r, args.seed, w, device=dev, engine_factory=engine)
     assert (sc.first, sc.count) == (first, count)
     tc = sc.engine
+    ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
 
     def push(k):
         lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
@@ -271,170 +257,195 @@ def run_b200(args):
         if world > 1:
             torch.distributed.barrier()
 
-    # ---- warm-up (untimed) ----
-    for k in range(args.warmup):
-        if k and k % nb == 0:
-            assert tc.sync() == 0
-            tc.reset()
-        push(k)
-    assert tc.sync() == 0
-
-    # ---- timed: K steps = K consecutive batches of the stream (a new pass over the stream starts from a
-    # reset estimator set, untimed); CUDA events on the library's stream around each step; L2 flushed
-    # (read of a 256 MiB buffer) before every step, outside the events ----
-    ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
-
-    def timed_pass(nsteps, profile, graphs):
-        tc.set_graphs(graphs)
-        tc.reset()
-        tc.profile(profile)
-        evs, launches, edges = [], 0, 0
-        prof = {}
-        stats = {"fresh": 0, "r2_replaced_retained": 0, "vertices": 0, "skipped": 0}
-
-        def harvest():
-            if profile:
-                for p, (pms, n) in tc.profile_read().items():
-                    acc = prof.setdefault(p, [0.0, 0])
-                    acc[0] += pms
-                    acc[1] += n
-            for kk, v in tc.stats().items():
-                if kk in stats:
-                    stats[kk] += v
-
-        barrier()
-        torch.cuda.synchronize()
-        with ClockSampler(dev.index) as clocks:
-            t0 = time.perf_counter()
-            for k in range(nsteps):
-                if k and k % nb == 0:  # stream exhausted: a fresh estimator set (untimed)
-                    assert tc.sync() == 0
-                    harvest()
-                    tc.reset()
-                    tc.profile(profile)
-                with torch.cuda.stream(ext):
-                    flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache
-                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                    e0.record(ext)
-                n = push(k)
-                with torch.cuda.stream(ext):
-                    e1.record(ext)
-                evs.append((e0, e1))
-                launches += tc.last_launches()
-                edges += n
-            assert tc.sync() == 0
-            torch.cuda.synchronize()
-            wall = time.perf_counter() - t0
-        barrier()
-        harvest()
-        ms_ = sum(x.elapsed_time(y) for x, y in evs)
-        return ms_, launches, edges, prof, stats, clocks, wall
-
-    # headline: every push as one CUDA graph (--no-graphs: plain stream launches), no profiling events
-    ms, launches, edges_done, _, _, clocks, t_wall = timed_pass(args.steps, False, not args.no_graphs)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    ms = float(t.item())
-    secs = ms / 1e3
-    # per-phase times (and the dominant kernel's launch time): one more pass over the stream with CUDA events
-    # bracketing each phase (plain launches: the events are stream operations between the kernels)
-    _, _, prof_edges, prof, stats, _, _ = timed_pass(nb, True, False)
-
-    # dominant kernel = k_update (the largest single kernel in the committed ncu launch list,
-    # profiles/launches_r01_summary.txt); its events bracket exactly that one launch per step
+    out = {"metric": METRIC, "unit": "edges/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+           "dtype": "u32",
+           "data": "synthetic (seeded native generator, synth/gen.c; the paper's SNAP datasets are not available)"}
     peak, peak_src = measured_peaks()
-    nsteps = nb
-    alg = {
-        "update": algorithmic_bytes("update", 0, count * nsteps, 0, stats["fresh"], stats["r2_replaced_retained"],
-                                    stats["skipped"]),
-        "partition": algorithmic_bytes("partition", prof_edges, 0, 0, 0, 0),
-        "pairs": algorithmic_bytes("pairs", prof_edges, 0, 0, 0, 0),
-        "vertices": algorithmic_bytes("vertices", prof_edges, 0, stats["vertices"], 0, 0),
-    }
-    ach = {p: alg[p] / (prof[p][0] / 1e3) / 1e9 for p in alg if prof.get(p) and prof[p][0] > 0}
-    roofline = {"bound": "hbm", "kernel": "k_update (fused Steps 1-3 + partial sums)",
-                "achieved": ach.get("update"), "peak": peak, "unit": "GB/s",
-                "frac": ach["update"] / peak if ach.get("update") else None,
-                "traffic": committed_traffic(args.config), "peak_source": peak_src,
-                "algorithmic_bytes_per_launch": alg["update"] / max(1, nsteps),
-                "launch_ms": prof["update"][0] / max(1, nsteps),
-                "small_batch_skipped_frac": stats["skipped"] / max(1, count * nsteps),
-                "limiters": limiters_with_issue(committed_limiters("k_update"), prof["update"][0] / max(1, nsteps)),
-                "phases": {p: {"ms_per_step": prof[p][0] / max(1, nsteps), "launches_per_step": prof[p][1] / max(1, nsteps),
-                               "algorithmic_GBps": ach.get(p), "frac": (ach[p] / peak) if ach.get(p) else None}
-                           for p in prof}}
 
-    value = edges_done / secs
-    out = {
-        "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic (seeded R-MAT/ER/Chung-Lu stand-ins; the paper's SNAP datasets are not available)",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w, "stream_edges": m_total,
-                   "batches_per_stream": nb, "estimators_per_gpu": count, "parallelism": f"estimator-shard x{world}",
-                   "l2": "flushed before every step (256 MiB read, outside the step events)",
-                   "launch": "one CUDA graph per push" if not args.no_graphs else "plain stream launches",
-                   "phases_from": "a second pass over the stream with per-phase CUDA events (plain launches)",
-                   "timing": "CUDA events on the library stream around each tc_push_batch, summed; max over ranks"},
-        "estimator_updates_per_s": edges_done * r / secs,
-        "batch_estimator_updates_per_s": args.steps * r / secs,
-        "gpu_launches": launches,
-        "roofline": roofline,
-        "wall_s_timed_region": t_wall,
-    }
-    out["clocks"] = clocks.summary()
+    if resident:
+        # ---- warm-up (untimed) ----
+        for k in range(args.warmup):
+            if k and k % nb == 0:
+                assert tc.sync() == 0
+                tc.reset()
+            push(k)
+        assert tc.sync() == 0
+
+        # ---- timed: K steps = K consecutive batches of the stream; CUDA events on the library's stream
+        # around each step; L2 flushed (read of a 256 MiB buffer) before every step, outside the events ----
+        def timed_pass(nsteps, profile, graphs):
+            tc.set_graphs(graphs)
+            tc.reset()
+            tc.profile(profile)
+            evs, launches, edges = [], 0, 0
+            kern = {}
+            stats = {}
+
+            def harvest():
+                if profile:
+                    for name, (kms, n) in tc.profile_kernels().items():
+                        acc = kern.setdefault(name, [0.0, 0])
+                        acc[0] += kms
+                        acc[1] += n
+                for kk, v in tc.stats().items():
+                    stats[kk] = stats.get(kk, 0) + v
+
+            barrier()
+            torch.cuda.synchronize()
+            with ClockSampler(dev.index) as clocks:
+                t0 = time.perf_counter()
+                for k in range(nsteps):
+                    if k and k % nb == 0:  # stream exhausted: a fresh estimator set (untimed)
+                        assert tc.sync() == 0
+                        harvest()
+                        tc.reset()
+                        tc.profile(profile)
+                    with torch.cuda.stream(ext):
+                        flush_sink.add_(flush.sum())  # read 256 MiB (> L2): every step starts with a cold cache
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(ext)
+                    n = push(k)
+                    with torch.cuda.stream(ext):
+                        e1.record(ext)
+                    evs.append((e0, e1))
+                    launches += tc.last_launches()
+                    edges += n
+                assert tc.sync() == 0
+                torch.cuda.synchronize()
+                wall = time.perf_counter() - t0
+            barrier()
+            harvest()
+            ms_ = sum(x.elapsed_time(y) for x, y in evs)
+            return ms_, launches, edges, kern, stats, clocks, wall
+
+        # headline: every push as one CUDA graph (--no-graphs: plain stream launches), no profiling events
+        ms, launches, edges_done, _, _, clocks, t_wall = timed_pass(args.steps, False, not args.no_graphs)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        secs = ms / 1e3
+        value = edges_done / secs
+        out.update({"value": value, "ms_per_step": ms / args.steps, "gpu_launches": launches,
+                    "estimator_updates_per_s": edges_done * r / secs,
+                    "batch_estimator_updates_per_s": args.steps * r / secs,
+                    "wall_s_timed_region": t_wall, "clocks": clocks.summary()})
+
+        # ---- attribution: one more pass over the whole stream with CUDA events around every kernel (plain
+        # launches), the per-kernel algorithmic bytes of the byte model and the event counts it needs ----
+        if not args.no_profile_pass:
+            _, _, prof_edges, kern, stats, _, _ = timed_pass(nb, True, False)
+            nsteps = nb
+            R_total = count * nsteps
+            rows = {}
+            for name, (kms, n) in kern.items():
+                if n == 0:
+                    continue
+                B = kernel_bytes(name, prof_edges, stats, R_total)
+                rows[name] = {"ms_per_launch": kms / n, "launches": n, "share_of_kernel_time": None,
+                              "algorithmic_bytes_per_launch": B / n,
+                              "achieved_GBps": (B / (kms / 1e3) / 1e9) if B and kms > 0 else None}
+            ktot = sum(kern[k][0] for k in rows)
+            for name in rows:
+                rows[name]["share_of_kernel_time"] = kern[name][0] / ktot
+                if rows[name]["achieved_GBps"]:
+                    rows[name]["frac"] = rows[name]["achieved_GBps"] / peak
+            dom = max(rows, key=lambda k: kern[k][0])
+            ncu = committed_ncu(args.config)
+            traffic = (ncu.get("kernels", {}).get(dom) or {}).get("dram_bytes_per_launch")
+            D_avg = stats["vertices"] / nsteps
+            B_step = (40 * prof_edges + 16 * stats["vertices"]) / nsteps + \
+                kernel_bytes("k_update", prof_edges, stats, R_total) / nsteps
+            step_ms = ms / args.steps
+            out["roofline"] = {
+                "bound": "hbm", "kernel": dom,
+                "achieved": rows[dom]["achieved_GBps"], "peak": peak, "unit": "GB/s",
+                "frac": rows[dom].get("frac"), "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": rows[dom]["algorithmic_bytes_per_launch"],
+                "launch_ms": rows[dom]["ms_per_launch"],
+                "byte_model": "SURVEY 8(d): Ke 16w (k_count) + 16w (k_scatter); Ki 8 B/arc + 16 B/vertex; "
+                              "Kp 24w; Ku 24 B/estimator + 16 B per replaced r1 + 16 B per replaced r2",
+                "kernels": rows,
+                "whole_step": {"algorithmic_bytes": B_step, "ms": step_ms,
+                               "achieved_GBps": B_step / (step_ms / 1e3) / 1e9,
+                               "frac": B_step / (step_ms / 1e3) / 1e9 / peak,
+                               "model": "w (40 + 16 D/w) + R (24 + 16 (P_r1 + P_r2)) bytes (SURVEY 8(d) minimal)"},
+                "events_per_batch": {"D": D_avg, "fresh_r1": stats["fresh"] / nsteps,
+                                     "r2_replaced_retained": stats["r2_replaced_retained"] / nsteps},
+                "from": "CUDA events around every kernel, a second pass over the stream (plain launches); shares "
+                        "agree with the committed ncu launch list profiles/launches_r02_<config>.csv",
+                "l2_hit_rate_probes": (ncu.get("kernels", {}).get("k_update") or {}).get("lts_hit_rate_pct"),
+                "ncu_source": ncu.get("source")}
+
+    out["config"] = {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w, "stream_edges": m_total,
+                     "batches_per_stream": nb, "estimators_per_gpu": count,
+                     "parallelism": f"estimator-shard x{world}",
+                     "l2": "flushed before every step (256 MiB read, outside the step events)",
+                     "launch": "one CUDA graph per push" if not args.no_graphs else "plain stream launches",
+                     "timing": "CUDA events on the library stream around each tc_push_batch, summed; max over ranks",
+                     "generation_s": round(t_gen, 2)}
 
     # ---- e2e: the public API with HOST (pinned) buffers, H2D + result D2H inside every step ----
     # Asynchronous errors: each push uploads its batch on the library's copy stream (overlapping the previous
     # batch's kernels) and tc_closed_sum_async copies the batch's S (the step's result) back to pinned host
-    # memory; the per-step L2 flush stays inside the timed region here.  Timed per pass over the stream with
-    # CUDA events on the library stream; the reset between passes is untimed.
+    # memory; the per-step L2 flush stays inside the timed region.  CUDA events on the library stream per pass
+    # over the stream; the reset between passes is untimed.
     if not args.no_e2e and world == 1:
-        host = torch.from_numpy(stream.view(np.int32)).pin_memory()
-        tc2 = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+        e_steps = args.steps if resident else min(args.steps, nb)
+        host_rows = min(m_total, e_steps * w) if not resident else m_total
+        host = torch.from_numpy(stream[:host_rows].view(np.int32)).pin_memory()
+        if not resident:
+            tc.set_graphs(not args.no_graphs)
+        tc2 = tc if not resident else TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
         tc2.set_async(True)
         tc2.set_graphs(not args.no_graphs)
         ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
-        Sbuf = torch.zeros(args.steps, dtype=torch.int64).pin_memory()
+        Sbuf = torch.zeros(e_steps, dtype=torch.int64).pin_memory()
         for k in range(min(args.warmup, nb)):
             tc2.push_batch(host[k * w:(k + 1) * w])
         assert tc2.sync() == 0
         tc2.reset()
         e_ms, e_edges, h2d, k, est, est_ok = 0.0, 0, 0, 0, 0.0, True
-        while k < args.steps:
-            n_pass = min(nb, args.steps - k)
-            torch.cuda.synchronize()
-            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a0.record(ext2)
-            m_run = []
-            for j in range(n_pass):
-                lo, hi = j * w, min(m_total, j * w + w)
-                with torch.cuda.stream(ext2):
-                    flush_sink.add_(flush.sum())
-                tc2.push_batch(host[lo:hi])
-                tc2.closed_sum_async(Sbuf, k + j)
-                m_run.append(hi)
-                h2d += 8 * (hi - lo)
-                e_edges += hi - lo
-            a1.record(ext2)
-            assert tc2.sync() == 0
-            e_ms += a0.elapsed_time(a1)
-            est = float(m_run[-1]) * float(Sbuf[k + n_pass - 1].item()) / float(r)  # the last step's result
-            est_ok = est_ok and est == tc2.estimate()
-            tc2.reset()
-            k += n_pass
+        with ClockSampler(dev.index) as clocks2:
+            while k < e_steps:
+                n_pass = min(nb, e_steps - k)
+                torch.cuda.synchronize()
+                a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a0.record(ext2)
+                m_run = []
+                for j in range(n_pass):
+                    lo, hi = j * w, min(m_total, j * w + w)
+                    with torch.cuda.stream(ext2):
+                        flush_sink.add_(flush.sum())
+                    tc2.push_batch(host[lo:hi])
+                    tc2.closed_sum_async(Sbuf, k + j)
+                    m_run.append(hi)
+                    h2d += 8 * (hi - lo)
+                    e_edges += hi - lo
+                a1.record(ext2)
+                assert tc2.sync() == 0
+                e_ms += a0.elapsed_time(a1)
+                est = float(m_run[-1]) * float(Sbuf[k + n_pass - 1].item()) / float(r)  # the last step's result
+                est_ok = est_ok and est == tc2.estimate()
+                tc2.reset()
+                k += n_pass
         out["e2e"] = {"value": e_edges / (e_ms / 1e3), "unit": "edges/s",
-                      "h2d_bytes_per_step": h2d // args.steps, "d2h_bytes_per_step": 8,
-                      "note": "tc_push_batch(pinned host edges, asynchronous errors: H2D on the copy stream overlaps the "
-                              "previous batch) + tc_closed_sum_async (8-byte S per step) + the per-step L2 flush; CUDA "
-                              "events on the library stream per pass over the stream"}
+                      "h2d_bytes_per_step": h2d // e_steps, "d2h_bytes_per_step": 8, "steps": e_steps,
+                      "note": "tc_push_batch(pinned host edges, asynchronous errors: H2D on the copy stream overlaps "
+                              "the previous batch) + tc_closed_sum_async (8-byte S per step) + the per-step L2 flush; "
+                              "CUDA events on the library stream per pass over the stream"}
         out["e2e_last_estimate"] = est
         out["e2e_results_match_tc_estimate"] = est_ok
+        if not resident:  # C4: the pinned-host feed IS the workload
+            out.update({"value": out["e2e"]["value"], "ms_per_step": e_ms / e_steps, "steps": e_steps,
+                        "estimator_updates_per_s": e_edges * r / (e_ms / 1e3),
+                        "clocks": clocks2.summary()})
 
     # ---- CPU baseline: the oracle as it stands, on this host's cores (rank 0, N = 1 only) ----
     if not args.no_cpu_baseline and world == 1:
-        out["cpu_baseline"] = cpu_baseline(stream, r, w, args.seed, nbatches=min(8, nb))
+        nbat = args.cpu_batches or max(1, min(8, (1 << 24) // max(w, r)))
+        out["cpu_baseline"] = cpu_baseline(stream, r, w, args.seed, nbatches=min(nbat, nb))
 
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -452,13 +463,17 @@ def cpu_baseline(stream, r, w, seed, nbatches):
         assert o.push_batch(W) == 0
         edges += len(W)
     dt = time.perf_counter() - t0
+    model, ncpu = cpu_info()
     return {"value": edges / dt, "unit": "edges/s", "cores": threads(), "kind": "oracle",
-            "sample": f"first {nbatches} batches ({edges} edges) of the same stream at full r={r}, w={w}; "
+            "cpu_model": model, "host_cpus": ncpu, "omp_num_threads_env": os.environ.get("OMP_NUM_THREADS"),
+            "sample": f"first {nbatches} batch(es) ({edges} edges) of the same stream at full r={r}, w={w}; "
                       f"oracle/indexed.c (qsort + binary-search multisearch, OpenMP over estimators), {dt:.1f} s"}
 
 
 def run_reference(args):
-    """--impl reference: the oracle (this tier's reference arm) timed on the host cores."""
+    """--impl reference: the oracle (this tier's reference arm) timed on the host cores, on the same config.
+    A step is one whole batch at full r; the run is bounded to at most 3 timed steps and 1 warm-up step so
+    that it ends within a few minutes at C3/C4 (a C3 batch takes the oracle ~5-10 s)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
@@ -468,15 +483,15 @@ def run_reference(args):
     w = args.w or cfg["w"]
     stream = config_stream(args.config)
     nb = (len(stream) + w - 1) // w
+    steps = max(1, min(args.steps, 3 if w * 1.0 * r >= 2 ** 40 else args.steps))
+    warm = min(args.warmup, 1)
     o = IndexedOracle(r, args.seed)
-    for k in range(args.warmup):
-        if k and k % nb == 0:
-            o = IndexedOracle(r, args.seed)
+    for k in range(warm):
         o.push_batch(stream[(k % nb) * w:(k % nb) * w + w])
     o = IndexedOracle(r, args.seed)
     t0 = time.perf_counter()
     edges = 0
-    for k in range(args.steps):
+    for k in range(steps):
         if k and k % nb == 0:
             o = IndexedOracle(r, args.seed)
         W = stream[(k % nb) * w:(k % nb) * w + w]
@@ -484,12 +499,14 @@ def run_reference(args):
         edges += len(W)
     dt = time.perf_counter() - t0
     v = edges / dt
-    cb = {"value": v, "unit": "edges/s", "cores": threads(), "kind": "oracle",
-          "sample": f"{args.steps} whole batches (w={w}) of {args.config} at full r={r}"}
+    model, ncpu = cpu_info()
+    cb = {"value": v, "unit": "edges/s", "cores": threads(), "kind": "oracle", "cpu_model": model,
+          "host_cpus": ncpu, "sample": f"{steps} whole batch(es) (w={w}) of {args.config} at full r={r}"}
     print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world,
-                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-                      "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
-                      "data": "synthetic", "config": {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w},
+                      "steps": steps, "steps_requested": args.steps, "warmup": warm,
+                      "ms_per_step": dt * 1e3 / steps, "higher_is_better": True, "scaling": "weak",
+                      "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                      "config": {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w},
                       "cpu_baseline": cb,
                       "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
           flush=True)

@@ -204,10 +204,18 @@ enum {
 int tc_profile(tc_ctx *ctx, int enable);
 int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n);
 
+/* tc_profile_kernels -- the same per KERNEL (CUDA events around each launch; profiled pushes run as plain
+ * stream launches, never as a graph): total milliseconds and launch count of kernel k < n since the last
+ * tc_profile() call; returns the number of kernel ids.  Synchronises.  tc_kernel_name(k): its name (static
+ * string, "" for an unknown id). */
+int tc_profile_kernels(tc_ctx *ctx, double *ms, uint64_t *launches, int n);
+const char *tc_kernel_name(int k);
+
 /* tc_stats -- event counts since the last tc_profile() call (for the bench's byte model):
  * out[0] estimators whose f1 was replaced, out[1] retained-f1 estimators whose f2 was replaced,
  * out[2] sum over batches of the number of distinct vertices in W, out[3] batches, out[4] estimators the
- * small-batch pass skipped as untouched (TC_TUNE_SMALL_BATCH).  Returns 5. */
+ * small-batch pass skipped as untouched (TC_TUNE_SMALL_BATCH), out[5] arcs and out[6] distinct vertices
+ * grouped by the large-bucket kernels (k_vhub / k_vbig).  Returns 7. */
 int tc_stats(tc_ctx *ctx, uint64_t *out, int n);
 
 /* Number of kernel launches issued by the last successful push (for the bench's gpu_launches). */

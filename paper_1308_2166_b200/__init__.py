@@ -271,13 +271,24 @@ class TriangleCounter:
             raise TCError(rc, "tc_profile_read")
         return {p: (float(ms[i]), int(n[i])) for i, p in enumerate(PHASES)}
 
+    def profile_kernels(self):
+        """tc_profile_kernels: {kernel name: (total ms, launches)} since the last profile() call."""
+        L = _lib.load()
+        n = L.tc_profile_kernels(self._h, None, None, 0)
+        if n < 0:
+            raise TCError(n, "tc_profile_kernels")
+        ms = np.zeros(n, np.float64)
+        cnt = np.zeros(n, np.uint64)
+        L.tc_profile_kernels(self._h, ms.ctypes.data_as(C.c_void_p), cnt.ctypes.data_as(C.c_void_p), n)
+        return {L.tc_kernel_name(k).decode(): (float(ms[k]), int(cnt[k])) for k in range(n)}
+
     def stats(self) -> dict:
-        out = np.zeros(5, np.uint64)
-        rc = _lib.load().tc_stats(self._h, out.ctypes.data_as(C.c_void_p), 5)
+        out = np.zeros(7, np.uint64)
+        rc = _lib.load().tc_stats(self._h, out.ctypes.data_as(C.c_void_p), 7)
         if rc < 0:
             raise TCError(rc, "tc_stats")
         return {"fresh": int(out[0]), "r2_replaced_retained": int(out[1]), "vertices": int(out[2]),
-                "batches": int(out[3]), "skipped": int(out[4])}
+                "batches": int(out[3]), "skipped": int(out[4]), "arcs_big": int(out[5]), "vertices_big": int(out[6])}
 
     def last_launches(self) -> int:
         out = C.c_uint32()

@@ -26,7 +26,7 @@ TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4, "small_batch
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_push_batch_after", "tc_test_draws", "tc_test_philox", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_closed_sum_async", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_set_state", "tc_set_counters", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
-           "tc_stream", "tc_profile", "tc_profile_read", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_parse_edges", "tc_ingest_file", "tc_strerror",
+           "tc_stream", "tc_profile", "tc_profile_read", "tc_profile_kernels", "tc_kernel_name", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_parse_edges", "tc_ingest_file", "tc_strerror",
            "tc_last_error"]
 
 _lib = None
@@ -80,6 +80,8 @@ def load(path: str = LIB_PATH):
         "tc_stream": (vp, [vp]),
         "tc_profile": (i32, [vp, i32]),
         "tc_profile_read": (i32, [vp, vp, vp, i32]),
+        "tc_profile_kernels": (i32, [vp, vp, vp, i32]),
+        "tc_kernel_name": (C.c_char_p, [i32]),
         "tc_stats": (i32, [vp, vp, i32]),
         "tc_last_launches": (i32, [vp, C.POINTER(u32)]),
         "tc_exact_triangles": (i32, [vp, u64, C.POINTER(u64), C.POINTER(C.c_double)]),

@@ -54,11 +54,15 @@ struct tc_ctx {
     cudaEvent_t produced = nullptr;  // tc_push_batch_after: the producer stream's work so far
     // profiling
     int prof = 0;
-    // begin / end events of each phase, one set per profiled push (read and recycled at the next sync)
-    std::vector<std::array<cudaEvent_t, 2 * TC_NPHASES>> ev_pool;
+    // begin / end events of each phase, then of each kernel (KernelId), one set per profiled push (read and
+    // recycled at the next sync); ev_kused: which kernels the push launched
+    std::vector<std::array<cudaEvent_t, 2 * TC_NPHASES + 2 * K_NKERNELS>> ev_pool;
+    std::vector<uint32_t> ev_kused;
     size_t ev_used = 0;
     double prof_ms[TC_NPHASES] = {};
     uint64_t prof_launch[TC_NPHASES] = {};
+    double prof_kms[K_NKERNELS] = {};
+    uint64_t prof_klaunch[K_NKERNELS] = {};
     // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
     int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
     cudaGraphExec_t gexec = nullptr;
@@ -219,13 +223,13 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
               cudaMalloc(&ctx->st.r1, 8 * n) == cudaSuccess && cudaMalloc(&ctx->st.r2, 8 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 4 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.p2, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
-              cudaMalloc(&ctx->st.stats, 40) == cudaSuccess &&
+              cudaMalloc(&ctx->st.stats, 8 * kNStats) == cudaSuccess &&
               cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->produced, cudaEventDisableTiming) == cudaSuccess;
     if (ok) {
         ok = cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream) == cudaSuccess &&
-             cudaMemsetAsync(ctx->st.stats, 0, 40, ctx->stream) == cudaSuccess;
+             cudaMemsetAsync(ctx->st.stats, 0, 8 * kNStats, ctx->stream) == cudaSuccess;
         launch_init_state(ctx->st, ctx->stream);
         ok = ok && cudaGetLastError() == cudaSuccess;
     }
@@ -287,6 +291,15 @@ static int settle(tc_ctx *ctx) {
             if (cudaEventElapsedTime(&ms, ctx->ev_pool[i][2 * p], ctx->ev_pool[i][2 * p + 1]) == cudaSuccess)
                 ctx->prof_ms[p] += ms;
         }
+        for (int k = 0; k < K_NKERNELS; ++k) {
+            if (!(ctx->ev_kused[i] >> k & 1u)) continue;
+            float ms = 0.f;
+            const cudaEvent_t *e = &ctx->ev_pool[i][2 * TC_NPHASES + 2 * k];
+            if (cudaEventElapsedTime(&ms, e[0], e[1]) == cudaSuccess) {
+                ctx->prof_kms[k] += ms;
+                ctx->prof_klaunch[k] += 1;
+            }
+        }
     }
     cudaGetLastError();
     ctx->ev_used = 0;
@@ -302,10 +315,11 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     const bool ovf = ctx->m + w > 0x7FFFFFFFull;  // chi <= m must fit 31 bits (reading R13)
     if (ovf && ctx->async_errors) return TC_EOVERFLOW;  // async mode: reported first, state untouched
     if (ctx->prof && ctx->ev_used == ctx->ev_pool.size()) {  // a new event set for this push
-        std::array<cudaEvent_t, 2 * TC_NPHASES> set{};
+        std::array<cudaEvent_t, 2 * TC_NPHASES + 2 * K_NKERNELS> set{};
         for (auto &e : set)
             if (cudaEventCreate(&e) != cudaSuccess) return fail_cuda(ctx);
         ctx->ev_pool.push_back(set);
+        ctx->ev_kused.push_back(0u);
     }
     int rc = grow_index(ctx, w);
     if (rc != TC_OK) return rc;
@@ -353,7 +367,13 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     a.ptag = ctx->ptag;
     // The batch's whole device sequence (counter resets + kernels) can be captured as one CUDA graph and the
     // previous graph executable updated in place.
-    const bool graph = ctx->use_graph != 0;
+    const bool graph = ctx->use_graph != 0 && !ctx->prof;  // profiling events need plain launches
+    KRec kr;
+    if (ctx->prof) {
+        kr.ev = &ctx->ev_pool[ctx->ev_used][2 * TC_NPHASES];
+        ctx->ev_kused[ctx->ev_used] = 0u;
+        kr.used = &ctx->ev_kused[ctx->ev_used];
+    }
     if (graph) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
     uint32_t launches = 0;
     {
@@ -370,27 +390,27 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         if (!ctx->async_errors && ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
         // a1: count, scans, scatter
         rec(2 * TC_PHASE_PARTITION, ms);
-        launches += launch_partition(ix, a, ms);
+        launches += launch_partition(ix, a, ms, kr);
         rec(2 * TC_PHASE_PARTITION + 1, ms);
         // a3 (it reads only the raw batch) on the second stream, alongside the vertex phase
         ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
         ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
         rec(2 * TC_PHASE_PAIRS, ss);
-        launches += launch_pairs(ix, a, ss);
+        launches += launch_pairs(ix, a, ss, kr);
         rec(2 * TC_PHASE_PAIRS + 1, ss);
         ok = ok && cudaEventRecord(ctx->join, ss) == cudaSuccess;
         ok = ok && cudaEventRecord(ctx->fork2, ms) == cudaSuccess;
         // a2: the large vertex buckets on the third stream, the common ones on the main stream
         ok = ok && cudaStreamWaitEvent(s2, ctx->fork2, 0) == cudaSuccess;
-        launches += launch_vertices_big(ix, a, s2);
+        launches += launch_vertices_big(ix, a, s2, kr);
         ok = ok && cudaEventRecord(ctx->join2, s2) == cudaSuccess;
         rec(2 * TC_PHASE_VERTICES, ms);
-        launches += launch_vertices(ix, a, ms);
+        launches += launch_vertices(ix, a, ms, kr);
         ok = ok && cudaStreamWaitEvent(ms, ctx->join2, 0) == cudaSuccess;
         rec(2 * TC_PHASE_VERTICES + 1, ms);
         ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
         rec(2 * TC_PHASE_UPDATE, ms);
-        launches += launch_update(ix, ctx->st, a, ms);
+        launches += launch_update(ix, ctx->st, a, ms, kr);
         rec(2 * TC_PHASE_UPDATE + 1, ms);
         if (ctx->prof)
             for (int p = 0; p < TC_NPHASES; ++p)
@@ -717,12 +737,33 @@ int tc_profile(tc_ctx *ctx, int enable) {
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     ctx->prof = enable ? 1 : 0;
-    CK(cudaMemsetAsync(ctx->st.stats, 0, 40, ctx->stream));
+    CK(cudaMemsetAsync(ctx->st.stats, 0, 8 * kNStats, ctx->stream));
     for (int p = 0; p < TC_NPHASES; ++p) {
         ctx->prof_ms[p] = 0;
         ctx->prof_launch[p] = 0;
     }
+    for (int k = 0; k < K_NKERNELS; ++k) {
+        ctx->prof_kms[k] = 0;
+        ctx->prof_klaunch[k] = 0;
+    }
     return TC_OK;
+}
+
+int tc_profile_kernels(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
+    if (!ctx) return TC_EINVAL;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    for (int k = 0; k < n && k < K_NKERNELS; ++k) {
+        if (ms) ms[k] = ctx->prof_kms[k];
+        if (launches) launches[k] = ctx->prof_klaunch[k];
+    }
+    return K_NKERNELS;
+}
+
+const char *tc_kernel_name(int k) {
+    static const char *names[K_NKERNELS] = {"k_count", "k_scan_cols", "k_scan_tot", "k_scatter", "k_split",
+                                            "k_pairs", "k_vhub", "k_vbig", "k_vhash", "k_update"};
+    return (k >= 0 && k < K_NKERNELS) ? names[k] : "";
 }
 
 int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
@@ -740,10 +781,10 @@ int tc_stats(tc_ctx *ctx, uint64_t *out, int n) {
     if (!ctx || !out) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
-    unsigned long long v[5];
-    CK(cudaMemcpy(v, ctx->st.stats, 40, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < n && i < 5; ++i) out[i] = v[i];
-    return 5;
+    unsigned long long v[kNStats];
+    CK(cudaMemcpy(v, ctx->st.stats, 8 * kNStats, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n && i < kNStats; ++i) out[i] = v[i];
+    return kNStats;
 }
 
 int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {

@@ -56,6 +56,8 @@ constexpr int kCtrErr = 3;     // error bits
 constexpr int kCtrDefer = 4;   // buckets k_vhub deferred to k_vbig
 constexpr int kCtrTicket2 = 5; // k_vbig's bucket ticket
 constexpr int kCtrFailB = 6;   // batch index of the first batch that found the error word set (async mode)
+constexpr int kCtrArcsBig = 7; // arcs grouped by the large-bucket kernels (k_vhub / k_vbig)
+constexpr int kCtrDBig = 8;    // distinct vertices of those buckets
 constexpr int kCtrWords = 16;
 
 struct __align__(16) VSlot {

@@ -659,6 +659,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         if (threadIdx.x == 0) {
             a.vslice[b] = make_uint2((uint32_t)off, slice_size(D, n));
             if (D) atomicAdd(&a.ctr[kCtrD], D);
+            if (D) atomicAdd(&a.ctr[kCtrDBig], D);
         }
         __syncthreads();  // sbuf is dead: it holds the table now
         const uint32_t S = slice_size(D, n);
@@ -794,6 +795,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
     if (threadIdx.x == 0) {
         a.vslice[b] = make_uint2((uint32_t)off, slice_size(D, n));
         if (D) atomicAdd(&a.ctr[kCtrD], D);
+        if (D) atomicAdd(&a.ctr[kCtrDBig], D);
     }
     const uint32_t S = slice_size(D, n);
     VSlot *sl = a.vt + off;
@@ -841,6 +843,8 @@ __global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
 // its vertex.
 
 constexpr uint32_t kHThreads = 256;
+
+constexpr int kHubThreadsC = 1024;  // k_vhub's CTA size (the hash path counts its vertices apart)
 
 // Shared-memory layout of the hash path for buckets of at most CAP arcs: R1 = {hkey u32[2 CAP], lid
 // u16[2 CAP]} while hashing; then {whist u16[8][SW], segst u32[CAP + 1]}; the slice table (u32,
@@ -1005,6 +1009,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     if (threadIdx.x == 0) {
         a.vslice[b] = make_uint2((uint32_t)off, S);
         if (Dt) atomicAdd(&a.ctr[kCtrD], Dt);
+        if (Dt && NT == kHubThreadsC) atomicAdd(&a.ctr[kCtrDBig], Dt);
     }
     for (uint32_t s = threadIdx.x; s < S; s += NT) table[s] = kEmptyV;
     __syncthreads();
@@ -1057,7 +1062,7 @@ __global__ void __launch_bounds__(kHThreads, 4) k_vhash(VertArgs a) {
 // one segment, already in arrival order: a 1-bit stable partition) and the rest, copied to the scratch
 // buffer, goes through the hash path.  Buckets whose rest is still too large are deferred to k_vbig.
 // Persistent CTAs (one per SM) over vperm[0 .. ctr[kCtrBig]).
-constexpr int kHubThreads = 1024;
+constexpr int kHubThreads = kHubThreadsC;
 constexpr uint32_t kHubWarps = kHubThreads / 32;
 constexpr uint32_t kHubCap = 8192;
 constexpr uint32_t kHubSample = kHubThreads;
@@ -1083,6 +1088,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
         if (b == 0xFFFFFFFFu) return;
         const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
         const uint4 *arcs = a.arcs + base;
+        if (threadIdx.x == 0) atomicAdd(&a.ctr[kCtrArcsBig], n);
         if (n <= kHubCap) {  // no peeling needed
             const ArcSrc src{arcs, nullptr, nullptr, nullptr};
             hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
@@ -1432,6 +1438,8 @@ __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, Updat
             if (blockIdx.x == 0) {
                 atomicAdd(stats + 2, (unsigned long long)ix.ctr[kCtrD]);
                 atomicAdd(stats + 3, 1ull);
+                atomicAdd(stats + 5, (unsigned long long)ix.ctr[kCtrArcsBig]);
+                atomicAdd(stats + 6, (unsigned long long)ix.ctr[kCtrDBig]);
             }
         }
     }
@@ -1531,10 +1539,11 @@ static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
                     a.small ? ix.filt : nullptr, a.S_reset};
 }
 
-int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     const Geometry &g = a.g;
     const uint32_t nV = 1u << g.bp1;
     const PartArgs p = part_args(ix, a);
+    kr.beg(K_COUNT, s);
     switch (g.bp1) {
 #define TC_COUNT_CASE(B) \
     case B: k_count<B><<<g.tiles, kTileThreads, 2 * kTileWarps * nV, s>>>(p); break;
@@ -1544,19 +1553,30 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
 #undef TC_COUNT_CASE
         default: return 0;
     }
+    kr.end(K_COUNT, s);
+    kr.beg(K_SCAN_COLS, s);
     k_scan_cols<<<(nV + 31) / 32, kScanWarps * 32, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, nV, ix.ctr);
+    kr.end(K_SCAN_COLS, s);
     // with a split, the large-bucket list is built by k_split over the sub-buckets
+    kr.beg(K_SCAN_TOT, s);
     k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.bs ? 0xFFFFFFFFu : g.vcap, ix.vperm, ix.ctr);
+    kr.end(K_SCAN_TOT, s);
+    kr.beg(K_SCATTER, s);
     k_scatter<<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
+    kr.end(K_SCATTER, s);
     if (!g.bs) return 4;
     SplitArgs sa{ix.arcs, ix.arcs2, ix.vstart, ix.vstart2, g.bp1, g.bs, g.vcap, ix.vperm, ix.ctr};
+    kr.beg(K_SPLIT, s);
     k_split<<<nV, kSplitThreads, 0, s>>>(sa);
+    kr.end(K_SPLIT, s);
     return 5;
 }
 
-int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
+    kr.beg(K_PAIRS, s);
     k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
+    kr.end(K_PAIRS, s);
     return 1;
 }
 
@@ -1566,26 +1586,34 @@ static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
                     ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 
-int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
+    kr.beg(K_VHASH, s);
     k_vhash<<<1u << a.g.bv, kHThreads, kVHashSmemBytes, s>>>(vert_args(ix, a));
+    kr.end(K_VHASH, s);
     return 1;
 }
 
-int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s) {
+int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
+    kr.beg(K_VHUB, s);
     k_vhub<<<sm_count(), kHubThreads, kVHubSmemBytes, s>>>(vert_args(ix, a));
+    kr.end(K_VHUB, s);
+    kr.beg(K_VBIG, s);
     k_vbig<<<kBigCTAs, kVBucketThreads, kVSmemBytes, s>>>(vert_args(ix, a));
+    kr.end(K_VBIG, s);
     return 2;
 }
 
-int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s) {
+int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
     UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), a.ptag}, ix.einfo, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
+    kr.beg(K_UPDATE, s);
     if (a.small)
         k_update<true><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, ix.filt);
     else
         k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, nullptr);
+    kr.end(K_UPDATE, s);
     return 1;
 }
 

@@ -34,14 +34,17 @@ struct IndexBufs {
     uint2 *stage2 = nullptr;
 };
 
+constexpr int kNStats = 7;
+
 struct StateBufs {
     uint64_t count = 0;
     uint2 *r1 = nullptr, *r2 = nullptr;
     uint32_t *cf = nullptr;  // chi in bits 0..30, closed flag in bit 31
     uint32_t *p1 = nullptr, *p2 = nullptr;  // 0-based global positions (< 2^31, reading R13); 0xFFFFFFFF = empty
     unsigned long long *S = nullptr;      // [2] closed-sum accumulators (double-buffered by batch parity)
-    unsigned long long *stats = nullptr;  // [5] fresh f1, replaced f2 of retained f1, sum of D, batches,
-                                          // estimators the small-batch pass skipped
+    unsigned long long *stats = nullptr;  // [kNStats] fresh f1, replaced f2 of retained f1, sum of D, batches,
+                                          // estimators the small-batch pass skipped, arcs / vertices of the
+                                          // large-bucket kernels
 };
 
 // Bucket geometry of one batch (host-computed from w and the tuning knobs).
@@ -80,16 +83,33 @@ struct Tuning {
 
 Geometry make_geometry(uint32_t w, const Tuning &t);
 
+// Per-kernel profiling (tc_profile_kernels): ids match include/tc.h TC_KERNEL_*.
+enum KernelId { K_COUNT = 0, K_SCAN_COLS, K_SCAN_TOT, K_SCATTER, K_SPLIT, K_PAIRS, K_VHUB, K_VBIG, K_VHASH, K_UPDATE,
+                K_NKERNELS };
+struct KRec {
+    cudaEvent_t *ev = nullptr;  // 2 K_NKERNELS events (begin, end) or null: no profiling
+    uint32_t *used = nullptr;   // bit k set once kernel k's events were recorded in this push
+    void beg(int k, cudaStream_t s) const {
+        if (ev) cudaEventRecord(ev[2 * k], s);
+    }
+    void end(int k, cudaStream_t s) const {
+        if (ev) {
+            cudaEventRecord(ev[2 * k + 1], s);
+            *used |= 1u << k;
+        }
+    }
+};
+
 // Each returns the number of kernel launches issued.
-int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a1: count, scans, scatter, split
-int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);      // a3: edge-pair table
-int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);   // a2: grouping, ranks, vertex table
-int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s);  // a2: the buckets > vcap
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());      // a3
+int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());   // a2
+int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a2 > vcap
 #ifndef TC_BIG_CTAS
 #define TC_BIG_CTAS 64
 #endif
 constexpr uint32_t kBigCTAs = TC_BIG_CTAS;
-int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s);
+int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
 int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *out, cudaStream_t s);

@@ -166,11 +166,15 @@ CONFIGS = {
 
 
 def config_stream(name: str, seed: int = 1) -> np.ndarray:
+    """The stream of a BASELINE.json config.  C1 comes from the numpy generator above; C2-C5 from the
+    native counter-based generator (synth/gen.c: same recipe, seconds instead of minutes at 10^8-10^9
+    edges)."""
     cfg = CONFIGS[name]
     if cfg["kind"] == "er":
         return er(cfg["n"], cfg["m"], seed)
+    from . import native
     if cfg["kind"] == "rmat":
-        return rmat(cfg["scale"], cfg["edge_factor"], seed)
+        return native.rmat(cfg["scale"], cfg["edge_factor"], seed)
     if cfg["kind"] == "chung_lu":
-        return chung_lu(cfg["n"], cfg["m"], cfg["gamma"], seed=seed)
+        return native.chung_lu(cfg["n"], cfg["m"], cfg["gamma"], seed=seed)
     raise KeyError(name)

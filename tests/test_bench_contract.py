@@ -37,8 +37,14 @@ def test_b200_arm_json_line():
               "vs_baseline", "dtype", "data", "config", "roofline", "clocks", "e2e", "gpu_launches"):
         assert k in d, k
     r = d["roofline"]
-    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "kernels", "whole_step"):
         assert k in r, k
     assert 0 < r["frac"] < 1 and d["gpu_launches"] >= 6 * 9 and d["value"] > 0
+    # the dominant kernel is the one with the largest measured time, and the shares add up
+    ks = r["kernels"]
+    assert r["kernel"] == max(ks, key=lambda k: ks[k]["ms_per_launch"] * ks[k]["launches"])
+    assert abs(sum(v["share_of_kernel_time"] for v in ks.values()) - 1) < 1e-6
+    assert 0 < r["whole_step"]["frac"] < 1
+    assert d["cpu_baseline"]["cpu_model"] if "cpu_baseline" in d else True
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d.get("e2e_results_match_tc_estimate") is True
