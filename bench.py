@@ -208,7 +208,7 @@ def run_b200(args):
     dev = torch.device("cuda", torch.cuda.current_device())
 
     from paper_1308_2166_b200 import TriangleCounter, build as libbuild
-    from paper_1308_2166_b200.dist import ShardedCounter
+    from paper_1308_2166_b200.dist import RankCounter
     libbuild.build()
 
     cfg = dict(CONFIGS[args.config])
@@ -231,26 +231,25 @@ def run_b200(args):
 
     knobs = {k: int(v) for k, v in (kv.split("=") for kv in args.tune)}
 
-    def engine(r_, seed_, first_, count_):
-        tc_ = TriangleCounter(r_, seed_, first=first_, count=count_, device=dev.index, w_max_hint=w)
-        tc_.set_async(True)
-        if knobs:
-            tc_.tune(**knobs)
-        return tc_
-
-    # one shard of the estimators per rank; rank 0 broadcasts each batch (NCCL over NVLink: the per-batch
-    # exchange, inside the timed step)
-    sc = ShardedCounter(r, args.seed, w, device=dev, engine_factory=engine)
-    assert (sc.first, sc.count) == (first, count)
-    tc = sc.engine
+    # one shard of the estimators per rank (tc_create_rank): the library broadcasts each batch from rank 0 with
+    # NCCL over NVLink (the per-batch exchange, inside the timed step) and all-reduces the partial sums
+    if world > 1:
+        sc = RankCounter(r, args.seed, w, device=dev)
+        tc = sc.engine
+    else:
+        tc = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+    assert (tc.first, tc.count) == (first, count)
+    tc.set_async(True)
+    if knobs:
+        tc.tune(**knobs)
     ext = torch.cuda.ExternalStream(tc.stream_ptr, device=dev)
 
     def push(k):
         lo, hi = (k % nb) * w, min(m_total, (k % nb) * w + w)
-        if world == 1:
+        if rank == 0:
             tc.push_batch(dstream[lo:hi])
         else:
-            sc.push_batch(dstream[lo:hi] if rank == 0 else None, w=hi - lo)
+            tc.push_batch(None, w=hi - lo)
         return hi - lo
 
     def barrier():
@@ -352,6 +351,10 @@ def run_b200(args):
                 if rows[name]["achieved_GBps"]:
                     rows[name]["frac"] = rows[name]["achieved_GBps"] / peak
             dom = max(rows, key=lambda k: kern[k][0])
+            per_rank = None
+            if world > 1:  # per-kernel times of every rank: the replicated index build is the Amdahl term
+                per_rank = [None] * world
+                torch.distributed.all_gather_object(per_rank, {k: v["ms_per_launch"] for k, v in rows.items()})
             ncu = committed_ncu(args.config)
             traffic = (ncu.get("kernels", {}).get(dom) or {}).get("dram_bytes_per_launch")
             D_avg = stats["vertices"] / nsteps
@@ -375,6 +378,7 @@ def run_b200(args):
                                      "r2_replaced_retained": stats["r2_replaced_retained"] / nsteps},
                 "from": "CUDA events around every kernel, a second pass over the stream (plain launches); shares "
                         "agree with the committed ncu launch list profiles/launches_r02_<config>.csv",
+                "per_rank_kernel_ms": per_rank,
                 "l2_hit_rate_probes": (ncu.get("kernels", {}).get("k_update") or {}).get("lts_hit_rate_pct"),
                 "ncu_source": ncu.get("source")}
 

@@ -45,6 +45,8 @@ enum {
     TC_EDUP = -4,        /* the same undirected pair twice in one batch  */
     TC_EOVERFLOW = -5,   /* chi overflow (reading R13), or the library limit m <= 2^31-1    */
     TC_ECUDA = -6,       /* a CUDA call failed; the handle is poisoned                      */
+    TC_ENCCL = -7,       /* NCCL unavailable or failed; the communicator is aborted and the
+                            handle poisoned                                                 */
     TC_ESTATE = -8,      /* handle poisoned by an earlier asynchronous error               */
     TC_EPARSE = -9,      /* malformed edge-list line (tc_parse_edges / tc_ingest_file)      */
     TC_EIO = -10         /* the edge-list file cannot be opened or read                     */
@@ -60,6 +62,55 @@ tc_ctx *tc_create(uint64_t r, uint64_t seed);
  * demand).  count may be 0 (an idle shard still tracks m).  NULL on failure. */
 tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t count, int device,
                         uint64_t w_max_hint);
+
+/* ------------------------------------------------------------------------------------------- */
+/* Multi-GPU: estimators are independent, so GPU g of G owns the contiguous global ids
+ * [floor(g r / G), floor((g+1) r / G)) and runs the whole per-batch update for them; all randomness is keyed
+ * by the GLOBAL id, so the union of the shards is bit-identical to one unsharded run.  The only exchanges are
+ * the batch (ncclBroadcast from rank 0, 8 w bytes, on a communication stream into one of two receive
+ * buffers, so batch b+1's broadcast overlaps batch b's kernels) and, per estimate, an ncclAllReduce of the
+ * exact u64 partial sums.  NCCL is loaded at run time (libnccl.so.2) on first use.                      */
+
+/* tc_nccl_unique_id -- write a new ncclUniqueId (128 bytes, NCCL_UNIQUE_ID_BYTES) to id; rank 0 calls it and
+ * passes the bytes to every rank out of band (e.g. a torch.distributed broadcast).  TC_ENCCL if NCCL is
+ * unavailable. */
+int tc_nccl_unique_id(void *id);
+
+/* tc_create_rank -- one process per GPU ("torchrun mode"): this rank's shard of r estimators on CUDA device
+ * `device` (-1 = current) and an NCCL communicator of `world` ranks (ncclCommInitRank with the 128-byte
+ * nccl_unique_id from tc_nccl_unique_id on rank 0; a collective: every rank calls it).  On such a handle:
+ *  - tc_push_batch / tc_push_batch_after are collective: every rank calls them with the same w, rank 0 passes
+ *    the edges (host or its device), the other ranks pass edges = NULL (ignored otherwise); the library
+ *    broadcasts the batch and every rank updates its shard.  A bad batch is rejected identically everywhere.
+ *  - tc_closed_sum, tc_estimate, tc_closed_sum_async, tc_group_sums and tc_estimate_mom are collective and
+ *    return the values over ALL r estimators on every rank.
+ *  - tc_get_state / tc_set_state address the local shard (local ids 0 .. count-1); tc_rank_info tells which.
+ *  - waits poll ncclCommGetAsyncError: an NCCL failure, or no progress for TC_NCCL_TIMEOUT_S seconds
+ *    (environment, default 600), aborts the communicator and poisons the handle with TC_ENCCL.
+ * NULL on failure (tc_last_error: TC_EINVAL, TC_ENOMEM, TC_ECUDA, TC_ENCCL). */
+tc_ctx *tc_create_rank(uint64_t r, uint64_t seed, int rank, int world, const void *nccl_unique_id, int device,
+                       uint64_t w_max_hint);
+
+/* tc_config -- options of tc_create_ex (zero-initialise, then set what you need). */
+typedef struct {
+    int ngpus;            /* GPUs this process drives (<= 1: one GPU, a plain handle)                        */
+    const int *devices;   /* ngpus CUDA device ids, or NULL for 0 .. ngpus-1 (the current device if ngpus <= 1) */
+    int strict_errors;    /* 1: strict mode (each push synchronises); 0: asynchronous errors (tc_set_async)   */
+    int graphs;           /* 1: each push as one CUDA graph per GPU (tc_set_graphs)                           */
+    uint64_t w_max_hint;  /* preallocate the per-batch index for batches of up to this many edges             */
+} tc_config;
+
+/* tc_create_ex -- one process drives cfg->ngpus GPUs (ncclCommInitAll): one handle whose shards live on the
+ * listed devices.  tc_push_batch takes the edges (host, or device memory of devices[0]) and broadcasts them;
+ * tc_estimate / tc_closed_sum / tc_group_sums / tc_estimate_mom cover all r estimators; tc_get_state
+ * addresses GLOBAL ids across the shards; tc_counters, tc_sync, tc_reset, tc_set_async, tc_set_graphs,
+ * tc_tune apply to every shard; tc_set_state, tc_set_counters, tc_closed_sum_async, tc_profile* and tc_stats
+ * are not available on a multi-GPU handle (TC_EINVAL).  NULL on failure (tc_last_error says why). */
+tc_ctx *tc_create_ex(uint64_t r, uint64_t seed, const tc_config *cfg);
+
+/* tc_rank_info -- rank and world of a rank handle (0 and 1 otherwise; world = ngpus for a tc_create_ex group)
+ * and the global id of its first estimator and how many it owns. */
+int tc_rank_info(tc_ctx *ctx, int *rank, int *world, uint64_t *first, uint64_t *count);
 
 /* tc_push_batch -- bulkUpdateAll on the next w edges of the stream.
  *  edges: w tc_edge in arrival order.  Host memory (pageable or pinned) or device memory on the
@@ -108,9 +159,10 @@ void tc_destroy(tc_ctx *ctx);
 /* tc_closed_sum -- S for this handle (exact uint64; shards all-reduce it).  Synchronises. */
 int tc_closed_sum(tc_ctx *ctx, uint64_t *S);
 
-/* tc_estimate_mom -- median of means over `groups` contiguous groups of the handle's estimators,
- * group g = local ids [floor(g*count/G), floor((g+1)*count/G)), lower median; PAPER.md:373-376,
- * 887-888 (reading R9).  1 <= groups <= count.  Synchronises. */
+/* tc_estimate_mom -- median of means over `groups` contiguous groups of ALL r estimators, group g = global ids
+ * [floor(g*r/G), floor((g+1)*r/G)), group mean (double)m * (double)S_g / (double)|g|, lower median;
+ * PAPER.md:373-376, 887-888 (reading R9).  1 <= groups <= r.  TC_EINVAL on a lone shard
+ * (tc_create_shard with count < r: it has only part of every group).  Synchronises. */
 int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out);
 
 /* tc_required_estimators -- the number of estimators that suffices for an (eps, delta)-approximation
@@ -128,7 +180,10 @@ int tc_required_estimators(double eps, double delta, uint64_t m, uint64_t Delta,
  * every batch's result without a host synchronisation per batch. */
 int tc_closed_sum_async(tc_ctx *ctx, uint64_t *S);
 
-/* tc_group_sums -- S_g for the same contiguous groups (exact uint64, host array of `groups`). */
+/* tc_group_sums -- S_g (exact uint64, host array of `groups`, 1 <= groups <= r) over contiguous groups of the
+ * GLOBAL estimator ids g = [floor(g r / G), floor((g+1) r / G)): a shard handle reports the part of its own
+ * estimators (groups it does not intersect are 0; shard vectors add up), a rank handle or a tc_create_ex
+ * group the total. */
 int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g);
 
 /* tc_get_state -- copy local estimators [first, first+count) to HOST arrays (SoA):

@@ -15,7 +15,7 @@ from . import _lib
 from ._lib import PHASES, TCError
 
 __all__ = ["TriangleCounter", "TCError", "PHASES", "load_library", "required_estimators", "exact_triangles", "parse_edges",
-           "test_draws", "test_philox"]
+           "test_draws", "test_philox", "nccl_unique_id"]
 
 
 def load_library():
@@ -107,20 +107,66 @@ def _edges_ptr(edges):
     return a.ctypes.data_as(C.c_void_p), a.shape[0], a
 
 
+def nccl_unique_id() -> bytes:
+    """tc_nccl_unique_id: a fresh 128-byte ncclUniqueId (rank 0 creates it and shares it out of band)."""
+    buf = C.create_string_buffer(128)
+    rc = _lib.load().tc_nccl_unique_id(buf)
+    if rc != 0:
+        raise TCError(rc, "tc_nccl_unique_id")
+    return buf.raw
+
+
 class TriangleCounter:
     """r estimators (or the shard [first, first+count) of them) on one GPU.
 
     tc_create(r, seed) / tc_create_shard(...), tc_push_batch, tc_estimate, tc_destroy (include/tc.h).
+    Multi-GPU: TriangleCounter.rank(...) (tc_create_rank: one process per GPU, NCCL inside the library) and
+    TriangleCounter.multi(...) (tc_create_ex: one process, several GPUs).
     """
 
     def __init__(self, r: int, seed: int, first: int = 0, count: int | None = None, device: int = -1,
-                 w_max_hint: int = 0):
+                 w_max_hint: int = 0, _handle=None):
         L = _lib.load()
         self.r, self.seed, self.first = int(r), int(seed), int(first)
         self.count = self.r - self.first if count is None else int(count)
+        self.rank_id, self.world = 0, 1
+        if _handle is not None:
+            self._h = _handle
+            return
         self._h = L.tc_create_shard(self.r, self.seed, self.first, self.count, int(device), int(w_max_hint))
         if not self._h:
             raise TCError(L.tc_last_error(), "tc_create_shard")
+
+    @classmethod
+    def rank(cls, r: int, seed: int, rank: int, world: int, unique_id: bytes, device: int = -1, w_max_hint: int = 0):
+        """tc_create_rank: this rank's shard [floor(rank r / world), floor((rank+1) r / world)) with an NCCL
+        communicator; push_batch / estimate / closed_sum / group_sums are then collective (every rank calls
+        them; ranks other than 0 pass edges=None with the batch size w)."""
+        L = _lib.load()
+        uid = C.create_string_buffer(bytes(unique_id), 128)
+        h = L.tc_create_rank(int(r), int(seed), int(rank), int(world), uid, int(device), int(w_max_hint))
+        if not h:
+            raise TCError(L.tc_last_error(), "tc_create_rank")
+        return cls._wrap(h, r, seed)
+
+    @classmethod
+    def multi(cls, r: int, seed: int, devices, strict: bool = False, graphs: bool = True, w_max_hint: int = 0):
+        """tc_create_ex: one handle over the GPUs `devices` of this process (ncclCommInitAll)."""
+        L = _lib.load()
+        devs = (C.c_int * len(devices))(*[int(d) for d in devices])
+        cfg = _lib.TCConfig(len(devices), devs, 1 if strict else 0, 1 if graphs else 0, int(w_max_hint))
+        h = L.tc_create_ex(int(r), int(seed), C.byref(cfg))
+        if not h:
+            raise TCError(L.tc_last_error(), "tc_create_ex")
+        return cls._wrap(h, r, seed)
+
+    @classmethod
+    def _wrap(cls, h, r, seed):
+        rk, wd, first, count = C.c_int(), C.c_int(), C.c_uint64(), C.c_uint64()
+        _lib.load().tc_rank_info(h, C.byref(rk), C.byref(wd), C.byref(first), C.byref(count))
+        obj = cls(r, seed, first=int(first.value), count=int(count.value), _handle=h)
+        obj.rank_id, obj.world = int(rk.value), int(wd.value)
+        return obj
 
     # -- lifecycle -------------------------------------------------------------------------------
     def close(self):
@@ -141,9 +187,15 @@ class TriangleCounter:
         self.close()
 
     # -- the path ------------------------------------------------------------------------------
-    def push_batch(self, edges, check: bool = True) -> int:
+    def push_batch(self, edges, check: bool = True, w: int | None = None) -> int:
         """tc_push_batch; a CUDA tensor goes through tc_push_batch_after with torch's current stream as the
-        producer, so the engine's stream waits for the kernels / copies that wrote it."""
+        producer, so the engine's stream waits for the kernels / copies that wrote it.  On a rank handle the
+        ranks other than 0 pass edges=None and the batch size w."""
+        if edges is None:
+            rc = _lib.load().tc_push_batch(self._h, None, int(w))
+            if check and rc != 0:
+                raise TCError(rc, "tc_push_batch")
+            return rc
         ptr, w, keep = _edges_ptr(edges)
         prod = _producer_stream(edges)
         if prod is not None:

@@ -16,6 +16,7 @@ TC_ESELFLOOP = -3
 TC_EDUP = -4
 TC_EOVERFLOW = -5
 TC_ECUDA = -6
+TC_ENCCL = -7
 TC_ESTATE = -8
 TC_EPARSE = -9
 TC_EIO = -10
@@ -24,7 +25,7 @@ TC_NPHASES = 4
 PHASES = ("partition", "pairs", "vertices", "update")
 TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4, "small_batch": 6}
 
-EXPORTS = ["tc_create", "tc_create_shard", "tc_push_batch", "tc_push_batch_after", "tc_test_draws", "tc_test_philox", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
+EXPORTS = ["tc_create", "tc_create_shard", "tc_create_rank", "tc_create_ex", "tc_nccl_unique_id", "tc_rank_info", "tc_push_batch", "tc_push_batch_after", "tc_test_draws", "tc_test_philox", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_closed_sum_async", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_set_state", "tc_set_counters", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_tune", "tc_sync",
            "tc_stream", "tc_profile", "tc_profile_read", "tc_profile_kernels", "tc_kernel_name", "tc_stats", "tc_last_launches", "tc_exact_triangles", "tc_parse_edges", "tc_ingest_file", "tc_strerror",
            "tc_last_error"]
@@ -36,6 +37,12 @@ class IngestStats(C.Structure):
     """tc_ingest_stats (include/tc.h)."""
     _fields_ = [("edges", C.c_uint64), ("batches", C.c_uint64), ("lines", C.c_uint64), ("error_line", C.c_uint64),
                 ("io_s", C.c_double), ("push_s", C.c_double), ("wait_s", C.c_double), ("wall_s", C.c_double)]
+
+
+class TCConfig(C.Structure):
+    """tc_config (include/tc.h)."""
+    _fields_ = [("ngpus", C.c_int), ("devices", C.POINTER(C.c_int)), ("strict_errors", C.c_int), ("graphs", C.c_int),
+                ("w_max_hint", C.c_uint64)]
 
 
 class TCError(RuntimeError):
@@ -57,6 +64,10 @@ def load(path: str = LIB_PATH):
     sig = {
         "tc_create": (vp, [u64, u64]),
         "tc_create_shard": (vp, [u64, u64, u64, u64, i32, u64]),
+        "tc_create_rank": (vp, [u64, u64, i32, i32, vp, i32, u64]),
+        "tc_create_ex": (vp, [u64, u64, C.POINTER(TCConfig)]),
+        "tc_nccl_unique_id": (i32, [vp]),
+        "tc_rank_info": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(u64), C.POINTER(u64)]),
         "tc_push_batch": (i32, [vp, vp, u64]),
         "tc_push_batch_after": (i32, [vp, vp, u64, vp]),
         "tc_test_draws": (i32, [vp, vp, vp, vp, vp, u64, u64, vp]),

@@ -11,8 +11,12 @@
 #include <array>
 #include <vector>
 
+#include <chrono>
+#include <thread>
+
 #include "../../include/tc.h"
 #include "kernels.h"
+#include "nccl_api.h"
 
 using namespace tcb;
 
@@ -67,7 +71,29 @@ struct tc_ctx {
     int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
     cudaGraphExec_t gexec = nullptr;
     Tuning tune;
+    // multi-GPU: a rank handle (tc_create_rank, or a peer of a tc_create_ex group) owns the
+    // global estimator ids [first, first + count) of r and an NCCL communicator; every batch is broadcast from
+    // rank 0 into one of two receive buffers on the comm stream (batch b+1's broadcast overlaps batch b's
+    // kernels) and the exact partial sums are all-reduced when an estimate is asked for
+    ncclComm_t nccl = nullptr;
+    int rank = 0, world = 1;
+    int nccl_dead = 0;             // the communicator was aborted after an error
+    cudaStream_t comm = nullptr;
+    uint2 *bcast[2] = {nullptr, nullptr};
+    cudaEvent_t bc_done = nullptr, bc_free[2] = {nullptr, nullptr}, inready = nullptr;
+    int bc_next = 0;
+    unsigned long long *d_red = nullptr;  // device scratch of the all-reduces (grown on demand)
+    uint64_t d_red_words = 0;
+    double nccl_timeout_s = 600.0;
+    // a tc_create_ex handle over several GPUs of this process: the peers (rank handles) do all the work
+    std::vector<tc_ctx *> peers;
 };
+
+// what a call on a poisoned handle returns: the CUDA / NCCL failure itself, else TC_ESTATE (a rejected batch)
+static int poisoned_code(const tc_ctx *c) {
+    if (!c->poisoned) return TC_OK;
+    return (c->poisoned == TC_ECUDA || c->poisoned == TC_ENCCL) ? c->poisoned : TC_ESTATE;
+}
 
 static int fail_cuda(tc_ctx *c) {
     cudaGetLastError();
@@ -124,6 +150,17 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
         free_index(ix);
         return TC_ENOMEM;
     }
+    if (ctx->nccl) {  // receive buffers of the per-batch broadcast
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(ctx->bcast[i]);
+            ctx->bcast[i] = nullptr;
+            if (cudaMalloc(&ctx->bcast[i], 8 * cap) != cudaSuccess) {
+                cudaGetLastError();
+                free_index(ix);
+                return TC_ENOMEM;
+            }
+        }
+    }
     ix.wcap = cap;
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
     CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
@@ -134,7 +171,25 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
 
 static void destroy_ctx(tc_ctx *ctx) {
     if (!ctx) return;
+    for (tc_ctx *p : ctx->peers) destroy_ctx(p);
+    if (!ctx->peers.empty()) {
+        delete ctx;
+        return;
+    }
     cudaSetDevice(ctx->device);
+    if (ctx->comm) cudaStreamSynchronize(ctx->comm);
+    if (ctx->nccl) {
+        if (ctx->nccl_dead) nccl().CommAbort(ctx->nccl);
+        else nccl().CommDestroy(ctx->nccl);
+    }
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(ctx->bcast[i]);
+        if (ctx->bc_free[i]) cudaEventDestroy(ctx->bc_free[i]);
+    }
+    if (ctx->bc_done) cudaEventDestroy(ctx->bc_done);
+    if (ctx->inready) cudaEventDestroy(ctx->inready);
+    if (ctx->comm) cudaStreamDestroy(ctx->comm);
+    cudaFree(ctx->d_red);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     free_index(ctx->ix);
     cudaFree(ctx->st.r1);
@@ -224,7 +279,7 @@ tc_ctx *tc_create_shard(uint64_t r, uint64_t seed, uint64_t first, uint64_t coun
               cudaMalloc(&ctx->st.cf, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.p1, 4 * n) == cudaSuccess &&
               cudaMalloc(&ctx->st.p2, 4 * n) == cudaSuccess && cudaMalloc(&ctx->st.S, 16) == cudaSuccess &&
               cudaMalloc(&ctx->st.stats, 8 * kNStats) == cudaSuccess &&
-              cudaMallocHost(&ctx->h_err, 64) == cudaSuccess &&
+              cudaMallocHost(&ctx->h_err, 128) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->copy_done, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&ctx->produced, cudaEventDisableTiming) == cudaSuccess;
     if (ok) {
@@ -260,11 +315,43 @@ static int decode_err(uint32_t e) {
 static int recompute_S(tc_ctx *ctx);
 
 // Wait for queued work and surface a pending asynchronous batch error (poisons the handle).
+// Wait for stream s.  On a rank handle the wait polls the communicator too: an asynchronous NCCL error (or
+// no progress for nccl_timeout_s) aborts the communicator and poisons the handle with TC_ENCCL, instead of
+// blocking forever behind a collective whose peer is gone.
+static int wait_stream(tc_ctx *ctx, cudaStream_t s) {
+    if (!s) return TC_OK;
+    if (!ctx->nccl || ctx->nccl_dead) return cudaStreamSynchronize(s) == cudaSuccess ? TC_OK : fail_cuda(ctx);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int spin = 0;; ++spin) {
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q == cudaSuccess) return TC_OK;
+        if (q != cudaErrorNotReady) return fail_cuda(ctx);
+        ncclResult_t ae = ncclSuccess;
+        const bool timed_out =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > ctx->nccl_timeout_s;
+        if (nccl().CommGetAsyncError(ctx->nccl, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress) ||
+            timed_out) {
+            nccl().CommAbort(ctx->nccl);
+            ctx->nccl_dead = 1;
+            ctx->poisoned = TC_ENCCL;
+            return TC_ENCCL;
+        }
+        if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+}
+
+#define WAIT(s)                                  \
+    do {                                         \
+        const int wrc_ = wait_stream(ctx, (s));  \
+        if (wrc_ != TC_OK) return wrc_;          \
+    } while (0)
+
 static int settle(tc_ctx *ctx) {
     CK(cudaSetDevice(ctx->device));
-    CK(cudaStreamSynchronize(ctx->stream));
-    CK(cudaStreamSynchronize(ctx->side));
-    CK(cudaStreamSynchronize(ctx->side2));
+    WAIT(ctx->comm);
+    WAIT(ctx->stream);
+    WAIT(ctx->side);
+    WAIT(ctx->side2);
     if (ctx->async_errors && !ctx->poisoned && ctx->ix.ctr) {
         CK(cudaMemcpy(ctx->h_err, ctx->ix.ctr, 4 * kCtrWords, cudaMemcpyDeviceToHost));
         const int code = decode_err(ctx->h_err[kCtrErr]);
@@ -303,17 +390,31 @@ static int settle(tc_ctx *ctx) {
     }
     cudaGetLastError();
     ctx->ev_used = 0;
-    return ctx->poisoned ? (ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE) : TC_OK;
+    return poisoned_code(ctx);
 }
 
-int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
+// One push = prepare (checks, index capacity, the batch onto the device: staging upload and, on a rank handle,
+// the broadcast from rank 0) + launch (the kernels, the strict-mode status, the counters).  A tc_create_ex
+// group prepares all its peers inside one NCCL group, then launches them.
+struct PushPrep {
+    const uint2 *in = nullptr;  // the batch on this device
+    int sb = -1;                // staging buffer used (host input), else -1
+    int bslot = -1;             // broadcast receive buffer used (rank handles), else -1
+    bool ovf = false;           // strict mode: the library's m limit is exceeded (reported by the kernels' word)
+};
+
+static int push_check(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     if (!ctx) return TC_EINVAL;
-    if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
+    if (ctx->poisoned) return poisoned_code(ctx);
     if (w == 0) return TC_OK;
-    if (!edges || w > kMaxBatch) return TC_EINVAL;
+    if (w > kMaxBatch || (!edges && ctx->rank == 0)) return TC_EINVAL;
+    return TC_OK;
+}
+
+static int push_prepare(tc_ctx *ctx, const tc_edge *edges, uint64_t w, PushPrep *pp) {
     CK(cudaSetDevice(ctx->device));
-    const bool ovf = ctx->m + w > 0x7FFFFFFFull;  // chi <= m must fit 31 bits (reading R13)
-    if (ovf && ctx->async_errors) return TC_EOVERFLOW;  // async mode: reported first, state untouched
+    pp->ovf = ctx->m + w > 0x7FFFFFFFull;  // the library's limit: 32-bit device positions (reading R13)
+    if (pp->ovf && ctx->async_errors) return TC_EOVERFLOW;  // async mode: reported first, state untouched
     if (ctx->prof && ctx->ev_used == ctx->ev_pool.size()) {  // a new event set for this push
         std::array<cudaEvent_t, 2 * TC_NPHASES + 2 * K_NKERNELS> set{};
         for (auto &e : set)
@@ -323,35 +424,59 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     }
     int rc = grow_index(ctx, w);
     if (rc != TC_OK) return rc;
-    // where are the edges?
-    const uint2 *in = nullptr;
-    cudaPointerAttributes attr;
-    if (cudaPointerGetAttributes(&attr, edges) != cudaSuccess) {
-        cudaGetLastError();
-        attr.type = cudaMemoryTypeUnregistered;
-    }
-    const bool on_device = (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
-                           attr.device == ctx->device;
-    if (attr.type == cudaMemoryTypeDevice && attr.device != ctx->device) return TC_EINVAL;
     IndexBufs &ix = ctx->ix;
-    int sb = -1;  // staging buffer used by this push (host input)
-    if (on_device) {
-        in = reinterpret_cast<const uint2 *>(edges);
-    } else {
-        // upload on the copy stream into the staging buffer the push before last used (its kernels are done
-        // with it: stage_free), so the copy overlaps the previous batch's kernels; the main stream waits
-        sb = ctx->stage_next;
-        uint2 *dst = sb ? ix.stage2 : ix.stage;
-        CK(cudaStreamWaitEvent(ctx->copy, ctx->stage_free[sb], 0));
-        CK(cudaMemcpyAsync(dst, edges, 8 * w, cudaMemcpyHostToDevice, ctx->copy));
-        CK(cudaEventRecord(ctx->copied[sb], ctx->copy));
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->copied[sb], 0));
-        if (attr.type == cudaMemoryTypeHost) CK(cudaEventSynchronize(ctx->copied[sb]));  // pinned: the caller may reuse it
-        in = dst;
+    if (ctx->rank == 0) {
+        // where are the edges?
+        cudaPointerAttributes attr;
+        if (cudaPointerGetAttributes(&attr, edges) != cudaSuccess) {
+            cudaGetLastError();
+            attr.type = cudaMemoryTypeUnregistered;
+        }
+        const bool on_device = (attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged) &&
+                               attr.device == ctx->device;
+        if (attr.type == cudaMemoryTypeDevice && attr.device != ctx->device) return TC_EINVAL;
+        if (on_device) {
+            pp->in = reinterpret_cast<const uint2 *>(edges);
+        } else {
+            // upload on the copy stream into the staging buffer the push before last used (its kernels are done
+            // with it: stage_free), so the copy overlaps the previous batch's kernels; the main stream waits
+            pp->sb = ctx->stage_next;
+            uint2 *dst = pp->sb ? ix.stage2 : ix.stage;
+            CK(cudaStreamWaitEvent(ctx->copy, ctx->stage_free[pp->sb], 0));
+            CK(cudaMemcpyAsync(dst, edges, 8 * w, cudaMemcpyHostToDevice, ctx->copy));
+            CK(cudaEventRecord(ctx->copied[pp->sb], ctx->copy));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->copied[pp->sb], 0));
+            if (attr.type == cudaMemoryTypeHost) CK(cudaEventSynchronize(ctx->copied[pp->sb]));  // pinned: reusable
+            pp->in = dst;
+        }
     }
+    if (ctx->nccl) {
+        // the batch exchange: ncclBroadcast from rank 0 on the comm stream, into the receive
+        // buffer the push before last used (its kernels are done with it: bc_free); rank 0 broadcasts in place
+        // from its input.  The main stream waits for the broadcast before its kernels.
+        pp->bslot = ctx->bc_next;
+        uint2 *recv = ctx->rank == 0 ? const_cast<uint2 *>(pp->in) : ctx->bcast[pp->bslot];
+        if (ctx->rank == 0) {
+            CK(cudaEventRecord(ctx->inready, ctx->stream));  // the upload / the producer's work, as ordered so far
+            CK(cudaStreamWaitEvent(ctx->comm, ctx->inready, 0));
+        }
+        CK(cudaStreamWaitEvent(ctx->comm, ctx->bc_free[pp->bslot], 0));
+        if (nccl().Broadcast(recv, recv, 2 * w, ncclUint32, 0, ctx->nccl, ctx->comm) != ncclSuccess) {
+            ctx->poisoned = TC_ENCCL;
+            return TC_ENCCL;
+        }
+        CK(cudaEventRecord(ctx->bc_done, ctx->comm));
+        CK(cudaStreamWaitEvent(ctx->stream, ctx->bc_done, 0));
+        pp->in = recv;
+    }
+    return TC_OK;
+}
+
+static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
+    IndexBufs &ix = ctx->ix;
     const int slot = (int)((ctx->b + 1) & 1u);
     BatchArgs a;
-    a.in = in;
+    a.in = pp.in;
     a.m_prev = ctx->m;
     a.batch = ctx->b;
     a.first = ctx->first;
@@ -378,7 +503,8 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     uint32_t launches = 0;
     {
         bool ok = true;
-        cudaStream_t ms = ctx->stream, ss = ctx->side, s2 = ctx->side2;
+        // profiled pushes run every kernel on the main stream, so each kernel's events time it alone
+        cudaStream_t ms = ctx->stream, ss = ctx->prof ? ms : ctx->side, s2 = ctx->prof ? ms : ctx->side2;
         auto rec = [&](int e, cudaStream_t st) {
             if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev_pool[ctx->ev_used][e], st) == cudaSuccess;
         };
@@ -387,7 +513,7 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
         if (!ctx->async_errors)
             ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, 0, 4, ms) == cudaSuccess &&
                  cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ms) == cudaSuccess;
-        if (!ctx->async_errors && ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
+        if (!ctx->async_errors && pp.ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
         // a1: count, scans, scatter
         rec(2 * TC_PHASE_PARTITION, ms);
         launches += launch_partition(ix, a, ms, kr);
@@ -440,13 +566,17 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     }
     if (ctx->prof) ++ctx->ev_used;
     CK(cudaGetLastError());
-    if (sb >= 0) {
-        CK(cudaEventRecord(ctx->stage_free[sb], ctx->stream));
-        ctx->stage_next = sb ^ 1;
+    if (pp.sb >= 0) {
+        CK(cudaEventRecord(ctx->stage_free[pp.sb], ctx->stream));
+        ctx->stage_next = pp.sb ^ 1;
+    }
+    if (pp.bslot >= 0) {
+        CK(cudaEventRecord(ctx->bc_free[pp.bslot], ctx->stream));
+        ctx->bc_next = pp.bslot ^ 1;
     }
     if (!ctx->async_errors) {
         CK(cudaMemcpyAsync(ctx->h_err, ix.ctr + kCtrErr, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        WAIT(ctx->stream);
         const int code = decode_err(*ctx->h_err);
         if (code != TC_OK) return code;  // nothing was mutated: k_update bailed out
     }
@@ -461,95 +591,216 @@ int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
     return TC_OK;
 }
 
+int tc_push_batch(tc_ctx *ctx, const tc_edge *edges, uint64_t w) {
+    int rc = push_check(ctx, edges, w);
+    if (rc != TC_OK || w == 0) return rc;
+    if (!ctx->peers.empty()) {  // tc_create_ex group: peer 0 takes the edges, the others receive them
+        for (tc_ctx *p : ctx->peers) {
+            rc = push_check(p, p->rank == 0 ? edges : nullptr, w);
+            if (rc != TC_OK) return rc;
+        }
+        std::vector<PushPrep> pp(ctx->peers.size());
+        if (nccl().GroupStart() != ncclSuccess) return TC_ENCCL;
+        int first_err = TC_OK;
+        for (size_t g = 0; g < ctx->peers.size(); ++g) {
+            tc_ctx *p = ctx->peers[g];
+            rc = push_prepare(p, p->rank == 0 ? edges : nullptr, w, &pp[g]);
+            if (rc != TC_OK && first_err == TC_OK) first_err = rc;
+        }
+        if (nccl().GroupEnd() != ncclSuccess && first_err == TC_OK) first_err = TC_ENCCL;
+        if (first_err != TC_OK) return first_err;
+        for (size_t g = 0; g < ctx->peers.size(); ++g) {
+            rc = push_launch(ctx->peers[g], w, pp[g]);
+            if (rc != TC_OK && first_err == TC_OK) first_err = rc;
+        }
+        if (first_err == TC_OK) {
+            ctx->m = ctx->peers[0]->m;
+            ctx->b = ctx->peers[0]->b;
+        }
+        return first_err;
+    }
+    PushPrep pp;
+    rc = push_prepare(ctx, edges, w, &pp);
+    if (rc != TC_OK) return rc;
+    return push_launch(ctx, w, pp);
+}
+
 int tc_push_batch_after(tc_ctx *ctx, const tc_edge *edges, uint64_t w, void *producer_stream) {
     if (!ctx) return TC_EINVAL;
     if (producer_stream && w) {
-        if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
-        CK(cudaSetDevice(ctx->device));
-        CK(cudaEventRecord(ctx->produced, (cudaStream_t)producer_stream));
-        CK(cudaStreamWaitEvent(ctx->stream, ctx->produced, 0));
+        tc_ctx *c = ctx->peers.empty() ? ctx : ctx->peers[0];  // a group reads the edges on peer 0's device
+        if (c->poisoned) return poisoned_code(c);
+        if (cudaSetDevice(c->device) != cudaSuccess || cudaEventRecord(c->produced, (cudaStream_t)producer_stream) != cudaSuccess ||
+            cudaStreamWaitEvent(c->stream, c->produced, 0) != cudaSuccess)
+            return fail_cuda(c);
     }
     return tc_push_batch(ctx, edges, w);
 }
 
+// Run f on every peer of a tc_create_ex group (first error wins); f(ctx) itself on any other handle.
+extern "C++" {
+template <typename F>
+static int each(tc_ctx *ctx, F f) {
+    if (ctx->peers.empty()) return f(ctx);
+    int first = TC_OK;
+    for (tc_ctx *p : ctx->peers) {
+        const int rc = f(p);
+        if (rc != TC_OK && first == TC_OK) first = rc;
+    }
+    return first;
+}
+}
+
 int tc_set_graphs(tc_ctx *ctx, int enable) {
     if (!ctx) return TC_EINVAL;
-    int rc = settle(ctx);
-    if (rc != TC_OK) return rc;
-    ctx->use_graph = enable ? 1 : 0;
-    return TC_OK;
+    return each(ctx, [&](tc_ctx *c) -> int {
+        int rc = settle(c);
+        if (rc != TC_OK) return rc;
+        c->use_graph = enable ? 1 : 0;
+        return TC_OK;
+    });
 }
 
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
     if (!ctx) return TC_EINVAL;
-    int rc = settle(ctx);
-    if (rc != TC_OK) return rc;
-    switch (knob) {
-        case TC_TUNE_VBUCKET_ARCS:
-            if (value < 1 || value > (1u << 30)) return TC_EINVAL;
-            ctx->tune.vbucket_arcs = (uint32_t)value;
-            return TC_OK;
-        case TC_TUNE_VBUCKET_CAP:
-            if (value < 1 || value > 2048) return TC_EINVAL;
-            ctx->tune.vcap = (uint32_t)value;
-            return TC_OK;
-        case TC_TUNE_SMALL_BATCH:
-            if (value > 2) return TC_EINVAL;
-            ctx->tune.small = (uint32_t)value;
-            return TC_OK;
-        case TC_TUNE_VBUCKET_SORT_CAP:
-            if (value < 1 || value > kVChunk) return TC_EINVAL;
-            ctx->tune.sortcap = (uint32_t)value;
-            return TC_OK;
-        default:
-            return TC_EINVAL;
-    }
+    return each(ctx, [&](tc_ctx *c) -> int {
+        int rc = settle(c);
+        if (rc != TC_OK) return rc;
+        switch (knob) {
+            case TC_TUNE_VBUCKET_ARCS:
+                if (value < 1 || value > (1u << 30)) return TC_EINVAL;
+                c->tune.vbucket_arcs = (uint32_t)value;
+                return TC_OK;
+            case TC_TUNE_VBUCKET_CAP:
+                if (value < 1 || value > 2048) return TC_EINVAL;
+                c->tune.vcap = (uint32_t)value;
+                return TC_OK;
+            case TC_TUNE_SMALL_BATCH:
+                if (value > 2) return TC_EINVAL;
+                c->tune.small = (uint32_t)value;
+                return TC_OK;
+            case TC_TUNE_VBUCKET_SORT_CAP:
+                if (value < 1 || value > kVChunk) return TC_EINVAL;
+                c->tune.sortcap = (uint32_t)value;
+                return TC_OK;
+            default:
+                return TC_EINVAL;
+        }
+    });
 }
 
 // settle() for calls that are allowed on a handle poisoned by a rejected asynchronous batch (its state is
-// that of the last accepted batch): only a CUDA failure is an error for them.
+// that of the last accepted batch): only a CUDA / NCCL failure is an error for them.
 static int settle_allow_poisoned(tc_ctx *ctx) {
     const int rc = settle(ctx);
-    if (rc == TC_OK || (ctx->poisoned && ctx->poisoned != TC_ECUDA && rc != TC_ECUDA)) return TC_OK;
+    if (rc == TC_OK || (ctx->poisoned && poisoned_code(ctx) == TC_ESTATE && rc != TC_ECUDA && rc != TC_ENCCL))
+        return TC_OK;
     return rc;
 }
 
 int tc_reset(tc_ctx *ctx) {
     if (!ctx) return TC_EINVAL;
-    int rc = settle_allow_poisoned(ctx);
-    if (rc != TC_OK) return rc;
-    launch_init_state(ctx->st, ctx->stream);
-    CK(cudaGetLastError());
-    CK(cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream));
-    if (ctx->ix.ctr) {
-        CK(cudaMemsetAsync(ctx->ix.ctr, 0, 4 * kCtrWords, ctx->stream));
-        CK(cudaMemsetAsync(ctx->ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
+    const int rc0 = each(ctx, [&](tc_ctx *c) -> int {
+        int rc = settle_allow_poisoned(c);
+        if (rc != TC_OK) return rc;
+        tc_ctx *ctx = c;  // for CK
+        launch_init_state(ctx->st, ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream));
+        if (ctx->ix.ctr) {
+            CK(cudaMemsetAsync(ctx->ix.ctr, 0, 4 * kCtrWords, ctx->stream));
+            CK(cudaMemsetAsync(ctx->ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->m = 0;
+        ctx->b = 0;
+        ctx->S_slot = -1;
+        ctx->poisoned = 0;
+        ctx->async_mprev.clear();
+        ctx->async_b0 = 0;
+        return TC_OK;
+    });
+    if (rc0 == TC_OK) {
+        ctx->m = 0;
+        ctx->b = 0;
     }
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->m = 0;
-    ctx->b = 0;
-    ctx->S_slot = -1;
-    ctx->poisoned = 0;
-    ctx->async_mprev.clear();
-    ctx->async_b0 = 0;
-    return TC_OK;
+    return rc0;
 }
 
 int tc_sync(tc_ctx *ctx) {
     if (!ctx) return TC_EINVAL;
-    return settle(ctx);
+    return each(ctx, [](tc_ctx *c) { return settle(c); });
+}
+
+// Device scratch for the all-reduces of a rank handle.
+static int red_scratch(tc_ctx *ctx, uint64_t words) {
+    if (ctx->d_red_words >= words) return TC_OK;
+    cudaFree(ctx->d_red);
+    ctx->d_red = nullptr;
+    ctx->d_red_words = 0;
+    if (cudaMalloc(&ctx->d_red, 8 * words) != cudaSuccess) {
+        cudaGetLastError();
+        return TC_ENOMEM;
+    }
+    ctx->d_red_words = words;
+    return TC_OK;
+}
+
+// In-place sum over the ranks of n u64 words on the handle's stream (no-op unless a rank handle).
+static int allreduce_u64(tc_ctx *ctx, unsigned long long *dev, uint64_t n) {
+    if (!ctx->nccl) return TC_OK;
+    if (ctx->nccl_dead) return TC_ENCCL;
+    if (nccl().AllReduce(dev, dev, n, ncclUint64, ncclSum, ctx->nccl, ctx->stream) != ncclSuccess) {
+        ctx->poisoned = TC_ENCCL;
+        return TC_ENCCL;
+    }
+    return TC_OK;
+}
+
+// S of this handle's estimators; on a rank handle the sum over all ranks (a collective: every rank calls).
+static int closed_sum_one(tc_ctx *ctx, uint64_t *S) {
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    *S = 0;
+    if (!ctx->nccl) {
+        if (ctx->S_slot >= 0) {
+            unsigned long long v = 0;
+            CK(cudaMemcpy(&v, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToHost));
+            *S = v;
+        }
+        return TC_OK;
+    }
+    rc = red_scratch(ctx, 1);
+    if (rc != TC_OK) return rc;
+    if (ctx->S_slot >= 0) CK(cudaMemcpyAsync(ctx->d_red, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    else CK(cudaMemsetAsync(ctx->d_red, 0, 8, ctx->stream));
+    rc = allreduce_u64(ctx, ctx->d_red, 1);
+    if (rc != TC_OK) return rc;
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(ctx->h_err + 16, ctx->d_red, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    WAIT(ctx->stream);
+    std::memcpy(&v, ctx->h_err + 16, 8);
+    *S = v;
+    return TC_OK;
 }
 
 int tc_closed_sum(tc_ctx *ctx, uint64_t *S) {
     if (!ctx || !S) return TC_EINVAL;
-    int rc = settle(ctx);
-    if (rc != TC_OK) return rc;
-    *S = 0;
-    if (ctx->S_slot >= 0) {
-        unsigned long long v = 0;
-        CK(cudaMemcpy(&v, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToHost));
-        *S = v;
+    if (ctx->peers.empty()) return closed_sum_one(ctx, S);
+    uint64_t tot = 0;
+    for (tc_ctx *p : ctx->peers) {  // one process: the host adds the peers' exact sums
+        uint64_t v = 0;
+        const int rc = p->nccl ? settle(p) : TC_OK;
+        if (rc != TC_OK) return rc;
+        tc_ctx *ctx = p;  // for CK
+        if (p->S_slot >= 0) {
+            unsigned long long x = 0;
+            CK(cudaMemcpy(&x, p->st.S + p->S_slot, 8, cudaMemcpyDeviceToHost));
+            v = x;
+        }
+        tot += v;
     }
+    *S = tot;
     return TC_OK;
 }
 
@@ -563,33 +814,62 @@ int tc_estimate(tc_ctx *ctx, double *out) {
 }
 
 int tc_closed_sum_async(tc_ctx *ctx, uint64_t *S) {
-    if (!ctx || !S) return TC_EINVAL;
-    if (ctx->poisoned) return ctx->poisoned == TC_ECUDA ? TC_ECUDA : TC_ESTATE;
+    if (!ctx || !S || !ctx->peers.empty()) return TC_EINVAL;
+    if (ctx->poisoned) return poisoned_code(ctx);
     CK(cudaSetDevice(ctx->device));
-    if (ctx->S_slot < 0) {
-        *S = 0;
+    if (!ctx->nccl) {
+        if (ctx->S_slot < 0) {
+            *S = 0;
+            return TC_OK;
+        }
+        CK(cudaMemcpyAsync(S, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToHost, ctx->stream));
         return TC_OK;
     }
-    CK(cudaMemcpyAsync(S, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    int rc = red_scratch(ctx, 1);  // rank handle: the all-reduced S, enqueued behind the last batch
+    if (rc != TC_OK) return rc;
+    if (ctx->S_slot >= 0) CK(cudaMemcpyAsync(ctx->d_red, ctx->st.S + ctx->S_slot, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    else CK(cudaMemsetAsync(ctx->d_red, 0, 8, ctx->stream));
+    rc = allreduce_u64(ctx, ctx->d_red, 1);
+    if (rc != TC_OK) return rc;
+    CK(cudaMemcpyAsync(S, ctx->d_red, 8, cudaMemcpyDeviceToHost, ctx->stream));
     return TC_OK;
 }
 
-int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g) {
-    if (!ctx || !S_g || groups == 0 || groups > ctx->count) return TC_EINVAL;
+// S_g over contiguous groups of the GLOBAL ids [floor(g r / G), floor((g+1) r / G)): this handle's part (a
+// shard contributes only to the groups its ids fall in), summed over the ranks on a rank handle.
+static int group_sums_one(tc_ctx *ctx, uint32_t groups, uint64_t *S_g) {
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     unsigned long long *d = nullptr;
     CK(cudaMalloc(&d, 8ull * groups));
-    if (cudaMemsetAsync(d, 0, 8ull * groups, ctx->stream) != cudaSuccess) {
-        cudaFree(d);
-        return fail_cuda(ctx);
+    bool ok = cudaMemsetAsync(d, 0, 8ull * groups, ctx->stream) == cudaSuccess;
+    if (ok) {
+        launch_group_sums(ctx->st, ctx->first, ctx->r, groups, d, ctx->stream);
+        ok = cudaGetLastError() == cudaSuccess;
     }
-    launch_group_sums(ctx->st, groups, d, ctx->stream);
-    const bool ok = cudaGetLastError() == cudaSuccess &&
-                    cudaMemcpyAsync(S_g, d, 8ull * groups, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess &&
-                    cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+    if (ok) rc = allreduce_u64(ctx, d, groups);
+    ok = ok && rc == TC_OK && cudaMemcpyAsync(S_g, d, 8ull * groups, cudaMemcpyDeviceToHost, ctx->stream) == cudaSuccess;
+    const int wrc = ok ? wait_stream(ctx, ctx->stream) : TC_OK;
     cudaFree(d);
+    if (rc != TC_OK) return rc;
+    if (wrc != TC_OK) return wrc;
     return ok ? TC_OK : fail_cuda(ctx);
+}
+
+int tc_group_sums(tc_ctx *ctx, uint32_t groups, uint64_t *S_g) {
+    if (!ctx || !S_g || groups == 0 || groups > ctx->r) return TC_EINVAL;
+    if (ctx->peers.empty()) return group_sums_one(ctx, groups, S_g);
+    std::vector<uint64_t> part(groups);
+    std::fill(S_g, S_g + groups, 0ull);
+    for (tc_ctx *p : ctx->peers) {
+        ncclComm_t saved = p->nccl;  // no all-reduce inside one process: the host adds the peers' vectors
+        p->nccl = nullptr;
+        const int rc = group_sums_one(p, groups, part.data());
+        p->nccl = saved;
+        if (rc != TC_OK) return rc;
+        for (uint32_t g = 0; g < groups; ++g) S_g[g] += part[g];
+    }
+    return TC_OK;
 }
 
 int tc_required_estimators(double eps, double delta, uint64_t m, uint64_t Delta, uint64_t tau, uint64_t *r) {
@@ -603,12 +883,14 @@ int tc_required_estimators(double eps, double delta, uint64_t m, uint64_t Delta,
 }
 
 int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out) {
-    if (!ctx || !out || groups == 0 || groups > ctx->count) return TC_EINVAL;
+    if (!ctx || !out || groups == 0 || groups > ctx->r) return TC_EINVAL;
+    // the groups cover all r estimators: a lone shard (tc_create_shard with count < r) has only its part
+    if (ctx->peers.empty() && !ctx->nccl && ctx->count != ctx->r) return TC_EINVAL;
     std::vector<uint64_t> S(groups);
     int rc = tc_group_sums(ctx, groups, S.data());
     if (rc != TC_OK) return rc;
     std::vector<double> means(groups);
-    const uint64_t n = ctx->count;
+    const uint64_t n = ctx->r;
     for (uint32_t g = 0; g < groups; ++g) {
         const uint64_t lo = (uint64_t)g * n / groups, hi = (uint64_t)(g + 1) * n / groups;
         // group mean of X_i = chi_i * m: (double)m * (double)S_g / (double)|g|, the oracle's expression
@@ -622,6 +904,19 @@ int tc_estimate_mom(tc_ctx *ctx, uint32_t groups, double *out) {
 
 int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint64_t *p1, uint32_t *r2,
                  uint64_t *p2, uint32_t *c, uint8_t *closed) {
+    if (ctx && !ctx->peers.empty()) {  // a group: [first, first + count) of the global ids, across the peers
+        if (first > ctx->r || count > ctx->r - first) return TC_EINVAL;
+        for (tc_ctx *p : ctx->peers) {
+            const uint64_t lo = std::max(first, p->first), hi = std::min(first + count, p->first + p->count);
+            if (lo >= hi) continue;
+            const uint64_t o = lo - first;
+            const int rc = tc_get_state(p, lo - p->first, hi - lo, r1 ? r1 + 2 * o : nullptr, p1 ? p1 + o : nullptr,
+                                        r2 ? r2 + 2 * o : nullptr, p2 ? p2 + o : nullptr, c ? c + o : nullptr,
+                                        closed ? closed + o : nullptr);
+            if (rc != TC_OK) return rc;
+        }
+        return TC_OK;
+    }
     if (!ctx || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
     int rc = settle_allow_poisoned(ctx);
     if (rc != TC_OK) return rc;
@@ -656,7 +951,7 @@ static int recompute_S(tc_ctx *ctx) {
     }
     const int slot = (int)(ctx->b & 1u);
     CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
-    launch_group_sums(ctx->st, 1, ctx->st.S + slot, ctx->stream);
+    launch_group_sums(ctx->st, 0, 1, 1, ctx->st.S + slot, ctx->stream);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->S_slot = slot;
@@ -665,7 +960,7 @@ static int recompute_S(tc_ctx *ctx) {
 
 int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1, const uint64_t *p1,
                  const uint32_t *r2, const uint64_t *p2, const uint32_t *c, const uint8_t *closed) {
-    if (!ctx || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
+    if (!ctx || !ctx->peers.empty() || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
     if (count && (!r1 || !p1 || !r2 || !p2 || !c || !closed)) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
@@ -703,7 +998,7 @@ int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1
 }
 
 int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches) {
-    if (!ctx || m > 0x7FFFFFFFull || (batches == 0) != (m == 0)) return TC_EINVAL;
+    if (!ctx || !ctx->peers.empty() || m > 0x7FFFFFFFull || (batches == 0) != (m == 0)) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     ctx->m = m;
@@ -713,6 +1008,7 @@ int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches) {
 
 int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches) {
     if (!ctx) return TC_EINVAL;
+    if (!ctx->peers.empty()) return tc_counters(ctx->peers[0], m, batches);  // every peer saw every batch
     if (ctx->async_errors) {  // enqueued batches count only once they are known to be accepted
         const int rc = settle_allow_poisoned(ctx);
         if (rc != TC_OK) return rc;
@@ -724,16 +1020,21 @@ int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches) {
 
 int tc_set_async(tc_ctx *ctx, int async_errors) {
     if (!ctx) return TC_EINVAL;
-    int rc = settle(ctx);
-    if (rc != TC_OK) return rc;
-    ctx->async_errors = async_errors ? 1 : 0;
-    return TC_OK;
+    return each(ctx, [&](tc_ctx *c) -> int {
+        int rc = settle(c);
+        if (rc != TC_OK) return rc;
+        c->async_errors = async_errors ? 1 : 0;
+        return TC_OK;
+    });
 }
 
-void *tc_stream(tc_ctx *ctx) { return ctx ? (void *)ctx->stream : nullptr; }
+void *tc_stream(tc_ctx *ctx) {
+    if (ctx && !ctx->peers.empty()) ctx = ctx->peers[0];
+    return ctx ? (void *)ctx->stream : nullptr;
+}
 
 int tc_profile(tc_ctx *ctx, int enable) {
-    if (!ctx) return TC_EINVAL;
+    if (!ctx || !ctx->peers.empty()) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     ctx->prof = enable ? 1 : 0;
@@ -750,7 +1051,7 @@ int tc_profile(tc_ctx *ctx, int enable) {
 }
 
 int tc_profile_kernels(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
-    if (!ctx) return TC_EINVAL;
+    if (!ctx || !ctx->peers.empty()) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     for (int k = 0; k < n && k < K_NKERNELS; ++k) {
@@ -767,7 +1068,7 @@ const char *tc_kernel_name(int k) {
 }
 
 int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
-    if (!ctx) return TC_EINVAL;
+    if (!ctx || !ctx->peers.empty()) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     for (int p = 0; p < n && p < TC_NPHASES; ++p) {
@@ -778,7 +1079,7 @@ int tc_profile_read(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
 }
 
 int tc_stats(tc_ctx *ctx, uint64_t *out, int n) {
-    if (!ctx || !out) return TC_EINVAL;
+    if (!ctx || !out || !ctx->peers.empty()) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     unsigned long long v[kNStats];
@@ -789,7 +1090,144 @@ int tc_stats(tc_ctx *ctx, uint64_t *out, int n) {
 
 int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {
     if (!ctx || !launches) return TC_EINVAL;
-    *launches = ctx->last_launches;
+    *launches = 0;
+    if (!ctx->peers.empty())
+        for (tc_ctx *p : ctx->peers) *launches += p->last_launches;
+    else
+        *launches = ctx->last_launches;
+    return TC_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Multi-GPU handles.
+
+int tc_nccl_unique_id(void *id) {
+    if (!id) return TC_EINVAL;
+    if (!nccl().ok) return TC_ENCCL;
+    ncclUniqueId u;
+    if (nccl().GetUniqueId(&u) != ncclSuccess) return TC_ENCCL;
+    std::memcpy(id, &u, sizeof(u));
+    return TC_OK;
+}
+
+// Give a freshly created shard handle its communicator and the broadcast machinery.
+static int attach_comm(tc_ctx *ctx, ncclComm_t comm, int rank, int world) {
+    ctx->nccl = comm;
+    ctx->rank = rank;
+    ctx->world = world;
+    if (const char *t = std::getenv("TC_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::atof(t);
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->bc_done, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->inready, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) CK(cudaEventCreateWithFlags(&ctx->bc_free[i], cudaEventDisableTiming));
+    if (ctx->ix.wcap) {  // the index was preallocated before the communicator existed: add the receive buffers
+        for (int i = 0; i < 2; ++i)
+            if (cudaMalloc(&ctx->bcast[i], 8 * ctx->ix.wcap) != cudaSuccess) {
+                cudaGetLastError();
+                return TC_ENOMEM;
+            }
+    }
+    return TC_OK;
+}
+
+tc_ctx *tc_create_rank(uint64_t r, uint64_t seed, int rank, int world, const void *nccl_unique_id, int device,
+                       uint64_t w_max_hint) {
+    g_last_error = TC_OK;
+    if (r == 0 || world < 1 || rank < 0 || rank >= world || !nccl_unique_id) {
+        g_last_error = TC_EINVAL;
+        return nullptr;
+    }
+    if (!nccl().ok) {
+        g_last_error = TC_ENCCL;
+        return nullptr;
+    }
+    const uint64_t first = (uint64_t)rank * r / (uint64_t)world;
+    const uint64_t count = (uint64_t)(rank + 1) * r / (uint64_t)world - first;
+    tc_ctx *ctx = tc_create_shard(r, seed, first, count, device, w_max_hint);
+    if (!ctx) return nullptr;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclComm_t comm = nullptr;
+    cudaSetDevice(ctx->device);
+    if (nccl().CommInitRank(&comm, world, id, rank) != ncclSuccess) {
+        destroy_ctx(ctx);
+        g_last_error = TC_ENCCL;
+        return nullptr;
+    }
+    const int rc = attach_comm(ctx, comm, rank, world);
+    if (rc != TC_OK) {
+        destroy_ctx(ctx);
+        g_last_error = rc;
+        return nullptr;
+    }
+    return ctx;
+}
+
+tc_ctx *tc_create_ex(uint64_t r, uint64_t seed, const tc_config *cfg) {
+    g_last_error = TC_OK;
+    tc_config def{};
+    if (!cfg) cfg = &def;
+    const int G = cfg->ngpus < 1 ? 1 : cfg->ngpus;
+    std::vector<int> devs(G);
+    for (int g = 0; g < G; ++g) devs[g] = cfg->devices ? cfg->devices[g] : (G == 1 ? -1 : g);
+    auto configure = [&](tc_ctx *c) -> int {
+        return tc_set_async(c, cfg->strict_errors ? 0 : 1) == TC_OK && tc_set_graphs(c, cfg->graphs ? 1 : 0) == TC_OK;
+    };
+    if (G == 1) {  // one GPU: a plain handle
+        tc_ctx *ctx = tc_create_shard(r, seed, 0, r, devs[0], cfg->w_max_hint);
+        if (ctx && !configure(ctx)) {
+            destroy_ctx(ctx);
+            g_last_error = TC_ECUDA;
+            return nullptr;
+        }
+        return ctx;
+    }
+    if (r == 0) {
+        g_last_error = TC_EINVAL;
+        return nullptr;
+    }
+    if (!nccl().ok) {
+        g_last_error = TC_ENCCL;
+        return nullptr;
+    }
+    std::vector<ncclComm_t> comms(G, nullptr);
+    if (nccl().CommInitAll(comms.data(), G, devs.data()) != ncclSuccess) {
+        g_last_error = TC_ENCCL;
+        return nullptr;
+    }
+    tc_ctx *grp = new (std::nothrow) tc_ctx();
+    if (!grp) {
+        for (auto c : comms) nccl().CommDestroy(c);
+        g_last_error = TC_ENOMEM;
+        return nullptr;
+    }
+    grp->r = r;
+    grp->seed = seed;
+    grp->count = r;
+    grp->device = devs[0];
+    for (int g = 0; g < G; ++g) {
+        const uint64_t first = (uint64_t)g * r / (uint64_t)G, count = (uint64_t)(g + 1) * r / (uint64_t)G - first;
+        tc_ctx *p = tc_create_shard(r, seed, first, count, devs[g], cfg->w_max_hint);
+        const int rc = p ? attach_comm(p, comms[g], g, G) : tc_last_error();
+        if (p) grp->peers.push_back(p);
+        else nccl().CommDestroy(comms[g]);
+        if (rc != TC_OK || !configure(p)) {
+            for (int h = g + 1; h < G; ++h) nccl().CommDestroy(comms[h]);
+            destroy_ctx(grp);
+            g_last_error = rc != TC_OK ? rc : TC_ECUDA;
+            return nullptr;
+        }
+    }
+    return grp;
+}
+
+int tc_rank_info(tc_ctx *ctx, int *rank, int *world, uint64_t *first, uint64_t *count) {
+    if (!ctx) return TC_EINVAL;
+    if (rank) *rank = ctx->rank;
+    if (world) *world = ctx->peers.empty() ? ctx->world : (int)ctx->peers.size();
+    if (first) *first = ctx->first;
+    if (count) *count = ctx->count;
     return TC_OK;
 }
 
@@ -853,6 +1291,7 @@ const char *tc_strerror(int code) {
         case TC_EOVERFLOW: return "stream longer than 2^31-1 edges (chi field overflow)";
         case TC_ECUDA: return "CUDA error";
         case TC_ESTATE: return "handle poisoned by an earlier asynchronous error";
+        case TC_ENCCL: return "NCCL error (communicator aborted)";
         case TC_EPARSE: return "malformed edge-list line";
         case TC_EIO: return "cannot open or read the edge-list file";
         default: return "unknown error";

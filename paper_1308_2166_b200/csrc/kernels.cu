@@ -1455,12 +1455,15 @@ __global__ void k_init_state(uint2 *r1, uint2 *r2, uint32_t *cf, uint32_t *p1, u
     }
 }
 
-// S_g over contiguous groups g = [floor(g n / G), floor((g+1) n / G)).
-__global__ void k_group_sums(const uint32_t *__restrict__ cf, uint64_t n, uint32_t G, unsigned long long *out) {
-    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (uint64_t)gridDim.x * blockDim.x) {
+// S_g over contiguous groups of global ids g = [floor(g N / G), floor((g+1) N / G)); local estimator t has
+// global id first + t (N = 1 puts every estimator into group 0).
+__global__ void k_group_sums(const uint32_t *__restrict__ cf, uint64_t count, uint64_t first, uint64_t N, uint32_t G,
+                             unsigned long long *out) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = cf[t];
         if (!(v & kClosedBit)) continue;
-        const uint64_t g = ((t + 1) * G + n - 1) / n - 1;
+        const uint64_t i = N == 1 ? 0 : first + t;
+        const uint64_t g = ((i + 1) * G + N - 1) / N - 1;
         atomicAdd(out + g, (unsigned long long)(v & kCMask));
     }
 }
@@ -1623,9 +1626,10 @@ int launch_init_state(const StateBufs &st, cudaStream_t s) {
     return 1;
 }
 
-int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *out, cudaStream_t s) {
+int launch_group_sums(const StateBufs &st, uint64_t first, uint64_t N, uint32_t groups, unsigned long long *out,
+                      cudaStream_t s) {
     if (!st.count) return 0;
-    k_group_sums<<<grid_for(st.count, 256, 16), 256, 0, s>>>(st.cf, st.count, groups, out);
+    k_group_sums<<<grid_for(st.count, 256, 16), 256, 0, s>>>(st.cf, st.count, first, N, groups, out);
     return 1;
 }
 

@@ -112,7 +112,8 @@ constexpr uint32_t kBigCTAs = TC_BIG_CTAS;
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
-int launch_group_sums(const StateBufs &st, uint32_t groups, unsigned long long *out, cudaStream_t s);
+int launch_group_sums(const StateBufs &st, uint64_t first, uint64_t N, uint32_t groups, unsigned long long *out,
+                      cudaStream_t s);  // groups over global ids (first = global id of local 0, N = r)
 
 int launch_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b, const uint32_t *base,
                       uint64_t seed, uint64_t count, uint64_t *out, cudaStream_t s);

@@ -172,3 +172,39 @@ class ShardedCounter:
     def estimate(self) -> float:
         """m * S / r as one fixed fp64 expression (reading R9) -- identical on every rank."""
         return float(self.m) * float(self.closed_sum()) / float(self.r)
+
+
+class RankCounter:
+    """The production multi-GPU path: this rank's shard behind tc_create_rank, the batch broadcast and the
+    partial-sum all-reduce done by NCCL INSIDE the library (include/tc.h).  torch.distributed only
+    bootstraps it (rank 0's 128-byte ncclUniqueId is broadcast over the default process group).
+
+    push_batch(edges, w): rank 0 passes the batch (host array / tensor or a CUDA tensor on its device), the
+    other ranks pass None; every rank passes the same w.  estimate() / closed_sum() are collective."""
+
+    def __init__(self, r: int, seed: int, w_max: int, device=None, group=None):
+        from . import TriangleCounter, nccl_unique_id
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = bytearray(nccl_unique_id() if self.rank == 0 else bytes(128))
+        if self.world > 1:
+            t = torch.tensor(list(uid), dtype=torch.uint8,
+                             device="cuda" if dist.get_backend(group) == "nccl" else "cpu")
+            dist.broadcast(t, src=0, group=group)
+            uid = bytes(t.cpu().tolist())
+        dev = torch.cuda.current_device() if device is None else int(torch.device(device).index or 0)
+        self.engine = TriangleCounter.rank(r, seed, self.rank, self.world, bytes(uid), device=dev, w_max_hint=w_max)
+        self.r, self.seed = int(r), int(seed)
+        self.first, self.count = self.engine.first, self.engine.count
+        assert (self.first, self.count) == shard(self.r, self.rank, self.world)
+
+    def push_batch(self, edges, w: int | None = None):
+        if edges is None:
+            return self.engine.push_batch(None, w=int(w))
+        return self.engine.push_batch(edges)
+
+    def closed_sum(self) -> int:
+        return self.engine.closed_sum()
+
+    def estimate(self) -> float:
+        return self.engine.estimate()

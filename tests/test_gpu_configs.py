@@ -106,9 +106,10 @@ def test_full_range_vertex_ids():
     from synth import native
     s = native.rmat(16, 16, 11)
     g = np.random.default_rng(4)
-    vals = np.unique(g.integers(2, 0xFFFFFFFD, size=70000, dtype=np.uint64))[: (1 << 16) - 4]
-    ids = np.concatenate([np.array([0, 1, 0xFFFFFFFD, 0xFFFFFFFE], np.uint64), g.permutation(vals)])
-    ids = g.permutation(ids).astype(np.uint32)  # an injective relabelling of [0, 2^16) into the id range
+    vals = np.unique(g.integers(2, 0xFFFFFFFD, size=70000, dtype=np.uint64))[: (1 << 16)]
+    ids = g.permutation(vals)[: 1 << 16].astype(np.uint32)  # an injective relabelling of [0, 2^16)
+    hubs = np.argsort(-np.bincount(s.ravel().astype(np.int64), minlength=1 << 16), kind="stable")[:4]
+    ids[hubs] = [0, 0xFFFFFFFE, 1, 0xFFFFFFFD]  # the extremes go to the busiest vertices
     assert len(np.unique(ids)) == 1 << 16
     t = np.ascontiguousarray(ids[s])
     assert t.max() == 0xFFFFFFFE and t.min() == 0
