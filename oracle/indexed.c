@@ -92,6 +92,13 @@ typedef struct {
     uint64_t *p1, *p2;
     uint32_t *c;
     uint8_t *closed;
+    /* per-step trace of the last accepted batch (test wiring, orc_set_trace): Step 1's replacement index j
+       (UINT32_MAX = f1 retained), chi^- after Step 1, rank(u->v) and rank(v->u) (chi^+ = ld + rd), Step 2's
+       draw d2 (UINT64_MAX = no draw), the batch position of the new f2 (UINT32_MAX = kept), Step 3's flag */
+    int trace;
+    uint32_t *t_j, *t_chim, *t_ld, *t_rd, *t_k2;
+    uint64_t *t_d2;
+    uint8_t *t_closed;
 } orc;
 
 orc *orc_create(uint64_t r, uint64_t seed, uint64_t first, uint64_t count) {
@@ -114,6 +121,7 @@ orc *orc_create(uint64_t r, uint64_t seed, uint64_t first, uint64_t count) {
 
 void orc_destroy(orc *o) {
     if (!o) return;
+    free(o->t_j); free(o->t_chim); free(o->t_ld); free(o->t_rd); free(o->t_k2); free(o->t_d2); free(o->t_closed);
     free(o->r1); free(o->r2); free(o->p1); free(o->p2); free(o->c); free(o->closed);
     free(o);
 }
@@ -256,6 +264,7 @@ static int push_batch_impl(orc *o, const uint32_t *edges, uint64_t w, const uint
             d1 = lemire(m_prev + w, xlo, seed, first + (uint64_t)i, b, 0x10000u);
         }
         idx[i] = d1 >= m_prev ? (int64_t)(d1 - m_prev) : -1;
+        if (o->trace) o->t_j[i] = idx[i] >= 0 ? (uint32_t)idx[i] : UINT32_MAX;
     }
     /* extract + combine */
 #pragma omp parallel for schedule(static)
@@ -277,6 +286,10 @@ static int push_batch_impl(orc *o, const uint32_t *edges, uint64_t w, const uint
         uint64_t ld = au < 0 ? 0 : (p >= 0 ? F[au].rank : (uint64_t)F[au].rank + 1);
         uint64_t rd = av < 0 ? 0 : (p >= 0 ? F[av].rank : (uint64_t)F[av].rank + 1);
         uint64_t chi_m = o->c[i], chi_p = ld + rd;
+        if (o->trace) {
+            o->t_chim[i] = (uint32_t)chi_m; o->t_ld[i] = (uint32_t)ld; o->t_rd[i] = (uint32_t)rd;
+            o->t_d2[i] = UINT64_MAX; o->t_k2[i] = UINT32_MAX;
+        }
         if (chi_p == 0) continue;
         uint64_t xlo, xhi, d2;
         if (forced_d2) {
@@ -286,6 +299,7 @@ static int push_batch_impl(orc *o, const uint32_t *edges, uint64_t w, const uint
             block_words(seed, first + (uint64_t)i, b, 0, &xlo, &xhi);
             d2 = lemire(chi_m + chi_p, xhi, seed, first + (uint64_t)i, b, 0x20000u);
         }
+        if (o->trace) o->t_d2[i] = d2;
         if (d2 >= chi_m) {
             uint64_t phi = d2 - chi_m;
             uint32_t src = phi < ld ? u : v;
@@ -296,6 +310,7 @@ static int push_batch_impl(orc *o, const uint32_t *edges, uint64_t w, const uint
             o->r2[2 * i] = x < y ? x : y; o->r2[2 * i + 1] = x < y ? y : x;
             o->p2[i] = m_prev + (uint64_t)F[k].pos;
             o->closed[i] = 0;
+            if (o->trace) o->t_k2[i] = (uint32_t)F[k].pos;
         }
         /* overflow guard (reading R13): chi^- + chi^+ in 64 bits; chi must fit 31 bits (bit 31 of the
            GPU's packed word is the closed flag).  m and positions are uint64 and not limited. */
@@ -316,6 +331,7 @@ static int push_batch_impl(orc *o, const uint32_t *edges, uint64_t w, const uint
         if (k >= 0 && m_prev + (uint64_t)S[k].pos > o->p2[i]) o->closed[i] = 1;
     }
 
+    if (o->trace) memcpy(o->t_closed, o->closed, o->count);
     code = bad_draw ? ORC_EINVAL : ovf ? ORC_EOVERFLOW : ORC_OK;
     if (code != ORC_OK) {  /* reject the whole batch: restore the snapshot */
         memcpy(o->r1, s_r1, 8 * o->count); memcpy(o->r2, s_r2, 8 * o->count); memcpy(o->c, s_c, 4 * o->count);
@@ -347,6 +363,26 @@ void orc_set_estimator(orc *o, uint64_t i, const uint32_t r1[2], uint64_t p1, co
 }
 
 void orc_set_counters(orc *o, uint64_t m, uint32_t b) { o->m = m; o->b = b; }
+
+/* Test wiring: record the per-step values of every later batch (see the orc fields); 0 on success. */
+int orc_set_trace(orc *o, int on) {
+    if (on && !o->t_j) {
+        uint64_t n = o->count ? o->count : 1;
+        o->t_j = (uint32_t *)calloc(n, 4); o->t_chim = (uint32_t *)calloc(n, 4); o->t_ld = (uint32_t *)calloc(n, 4);
+        o->t_rd = (uint32_t *)calloc(n, 4); o->t_k2 = (uint32_t *)calloc(n, 4); o->t_d2 = (uint64_t *)calloc(n, 8);
+        o->t_closed = (uint8_t *)calloc(n, 1);
+        if (!o->t_j || !o->t_chim || !o->t_ld || !o->t_rd || !o->t_k2 || !o->t_d2 || !o->t_closed) return ORC_ENOMEM;
+    }
+    o->trace = on;
+    return ORC_OK;
+}
+
+void orc_get_trace(const orc *o, uint32_t *j, uint32_t *chim, uint32_t *ld, uint32_t *rd, uint64_t *d2, uint32_t *k2,
+                   uint8_t *closed) {
+    memcpy(j, o->t_j, 4 * o->count); memcpy(chim, o->t_chim, 4 * o->count); memcpy(ld, o->t_ld, 4 * o->count);
+    memcpy(rd, o->t_rd, 4 * o->count); memcpy(d2, o->t_d2, 8 * o->count); memcpy(k2, o->t_k2, 4 * o->count);
+    memcpy(closed, o->t_closed, o->count);
+}
 
 void orc_get_state(const orc *o, uint32_t *r1, uint64_t *p1, uint32_t *r2, uint64_t *p2, uint32_t *c,
                    uint8_t *closed) {

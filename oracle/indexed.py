@@ -51,6 +51,9 @@ def lib():
         L.orc_push_batch_forced.argtypes = [vp, vp, u64, vp, vp]
         L.orc_set_estimator.argtypes = [vp, u64, vp, u64, vp, u64, u32, C.c_uint8]
         L.orc_set_counters.argtypes = [vp, u64, u32]
+        L.orc_set_trace.restype = C.c_int
+        L.orc_set_trace.argtypes = [vp, C.c_int]
+        L.orc_get_trace.argtypes = [vp] + [vp] * 7
         _lib = L
     return _lib
 
@@ -95,6 +98,22 @@ class IndexedOracle:
 
     def set_counters(self, m, b):
         lib().orc_set_counters(self._h, int(m), int(b))
+
+    def set_trace(self, on: bool = True):
+        """Test wiring: record the per-step values of every later batch (trace())."""
+        if lib().orc_set_trace(self._h, 1 if on else 0) != 0:
+            raise MemoryError("orc_set_trace")
+
+    def trace(self):
+        """Per-step values of the last batch: j (Step 1 replacement index, 2^32-1 = retained), chi_m (chi^-),
+        ld, rd (ranks; chi^+ = ld + rd), d2 (Step 2 draw, 2^64-1 = none), k2 (batch position of the new f2,
+        2^32-1 = kept), closed (after Step 3)."""
+        n = self.count
+        out = dict(j=np.empty(n, np.uint32), chi_m=np.empty(n, np.uint32), ld=np.empty(n, np.uint32),
+                   rd=np.empty(n, np.uint32), d2=np.empty(n, np.uint64), k2=np.empty(n, np.uint32),
+                   closed=np.empty(n, np.uint8))
+        lib().orc_get_trace(self._h, *[_ptr(out[f]) for f in ("j", "chi_m", "ld", "rd", "d2", "k2", "closed")])
+        return out
 
     def state(self):
         n = self.count
