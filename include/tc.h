@@ -235,9 +235,23 @@ int tc_set_graphs(tc_ctx *ctx, int enable);
  *                        estimator, tests f1's endpoints against a bit filter of the batch's vertices (no
  *                        false negatives) and runs Steps 1-3 only for estimators whose f1 is replaced or has
  *                        an endpoint in the batch, writing only the fields that change.
+ *  TC_TUNE_SPLIT_KERNELS 1: the estimator pass runs as one kernel per step of SURVEY.md §8(a) -- k_u1_resample
+ *                        (Step 1, a4), k_u2_count (Step 2a, a5), k_u3_select (Step 2b, a6), k_u4_close (Step 3,
+ *                        a7), k_r_reduce (aggregation, a8) -- instead of the fused k_update, keeping every step's
+ *                        values per estimator (tc_get_steps) for per-step parity and per-step timing; 0 (default):
+ *                        fused.  The states are identical either way.
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
-enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6 };
+enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6,
+       TC_TUNE_SPLIT_KERNELS = 8 };
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
+
+/* tc_get_steps -- with TC_TUNE_SPLIT_KERNELS on: the per-step values of the last batch for local estimators
+ * [first, first+count), HOST arrays (any may be NULL): j = Step 1's replacement index in W (0xFFFFFFFF: f1
+ * retained), chim = chi^- after Step 1, ld / rd = rank(u->v) / rank(v->u) (chi^+ = ld + rd; u = min endpoint,
+ * reading R1), d2 = Step 2's draw over chi^- + chi^+ (UINT64_MAX: no draw), k2 = batch position of the new f2
+ * (0xFFFFFFFF: kept).  TC_EINVAL if the split pass was never enabled.  Synchronises. */
+int tc_get_steps(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *j, uint32_t *chim, uint32_t *ld, uint32_t *rd,
+                 uint64_t *d2, uint32_t *k2);
 
 /* tc_sync -- wait for all queued work; returns the first asynchronous error, if any. */
 int tc_sync(tc_ctx *ctx);

@@ -304,6 +304,17 @@ class TriangleCounter:
         for k, v in knobs.items():
             self._ck(_lib.load().tc_tune(self._h, _lib.TUNE[k], int(v)), f"tc_tune({k})")
 
+    def steps(self, first: int = 0, count: int | None = None) -> dict:
+        """tc_get_steps: the per-step values of the last batch (split estimator pass, tune(split_kernels=1))."""
+        n = self.count - first if count is None else count
+        out = dict(j=np.empty(n, np.uint32), chi_m=np.empty(n, np.uint32), ld=np.empty(n, np.uint32),
+                   rd=np.empty(n, np.uint32), d2=np.empty(n, np.uint64), k2=np.empty(n, np.uint32))
+        P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._ck(_lib.load().tc_get_steps(self._h, int(first), int(n), *[P(out[f]) for f in
+                                                                         ("j", "chi_m", "ld", "rd", "d2", "k2")]),
+                 "tc_get_steps")
+        return out
+
     def sync(self) -> int:
         return _lib.load().tc_sync(self._h)
 

@@ -85,6 +85,7 @@ struct tc_ctx {
     unsigned long long *d_red = nullptr;  // device scratch of the all-reduces (grown on demand)
     uint64_t d_red_words = 0;
     double nccl_timeout_s = 600.0;
+    StepBufs steps;  // split estimator pass (TC_TUNE_SPLIT_KERNELS): per-step values of the last batch
     // a tc_create_ex handle over several GPUs of this process: the peers (rank handles) do all the work
     std::vector<tc_ctx *> peers;
 };
@@ -101,10 +102,36 @@ static int fail_cuda(tc_ctx *c) {
     return TC_ECUDA;
 }
 
+#define CK2(c, call)                                   \
+    do {                                               \
+        if ((call) != cudaSuccess) return fail_cuda(c); \
+    } while (0)
+
 #define CK(call)                                   \
     do {                                           \
         if ((call) != cudaSuccess) return fail_cuda(ctx); \
     } while (0)
+
+static void free_steps(StepBufs &sb) {
+    void *bufs[] = {sb.j, sb.xhi, sb.chim, sb.ld, sb.rd, sb.endU, sb.endV, sb.d2, sb.k2};
+    for (void *p : bufs) cudaFree(p);
+    sb = StepBufs();
+}
+
+static bool alloc_steps(StepBufs &sb, uint64_t count) {
+    const uint64_t n = std::max<uint64_t>(count, 1);
+    sb.count = count;
+    const bool ok = cudaMalloc(&sb.j, 4 * n) == cudaSuccess && cudaMalloc(&sb.xhi, 8 * n) == cudaSuccess &&
+                    cudaMalloc(&sb.chim, 4 * n) == cudaSuccess && cudaMalloc(&sb.ld, 4 * n) == cudaSuccess &&
+                    cudaMalloc(&sb.rd, 4 * n) == cudaSuccess && cudaMalloc(&sb.endU, 4 * n) == cudaSuccess &&
+                    cudaMalloc(&sb.endV, 4 * n) == cudaSuccess && cudaMalloc(&sb.d2, 8 * n) == cudaSuccess &&
+                    cudaMalloc(&sb.k2, 4 * n) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        free_steps(sb);
+    }
+    return ok;
+}
 
 static void free_index(IndexBufs &ix) {
     void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
@@ -190,6 +217,7 @@ static void destroy_ctx(tc_ctx *ctx) {
     if (ctx->inready) cudaEventDestroy(ctx->inready);
     if (ctx->comm) cudaStreamDestroy(ctx->comm);
     cudaFree(ctx->d_red);
+    free_steps(ctx->steps);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     free_index(ctx->ix);
     cudaFree(ctx->st.r1);
@@ -536,7 +564,8 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
         rec(2 * TC_PHASE_VERTICES + 1, ms);
         ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
         rec(2 * TC_PHASE_UPDATE, ms);
-        launches += launch_update(ix, ctx->st, a, ms, kr);
+        if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
+        else launches += launch_update(ix, ctx->st, a, ms, kr);
         rec(2 * TC_PHASE_UPDATE + 1, ms);
         if (ctx->prof)
             for (int p = 0; p < TC_NPHASES; ++p)
@@ -683,6 +712,14 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
                 if (value < 1 || value > kVChunk) return TC_EINVAL;
                 c->tune.sortcap = (uint32_t)value;
                 return TC_OK;
+            case TC_TUNE_SPLIT_KERNELS:
+                if (value > 1) return TC_EINVAL;
+                if (value && !c->steps.j) {
+                    CK2(c, cudaSetDevice(c->device));
+                    if (!alloc_steps(c->steps, c->count)) return TC_ENOMEM;
+                }
+                c->tune.split = (uint32_t)value;
+                return TC_OK;
             default:
                 return TC_EINVAL;
         }
@@ -736,6 +773,7 @@ int tc_sync(tc_ctx *ctx) {
 static int red_scratch(tc_ctx *ctx, uint64_t words) {
     if (ctx->d_red_words >= words) return TC_OK;
     cudaFree(ctx->d_red);
+    free_steps(ctx->steps);
     ctx->d_red = nullptr;
     ctx->d_red_words = 0;
     if (cudaMalloc(&ctx->d_red, 8 * words) != cudaSuccess) {
@@ -1063,7 +1101,8 @@ int tc_profile_kernels(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
 
 const char *tc_kernel_name(int k) {
     static const char *names[K_NKERNELS] = {"k_count", "k_scan_cols", "k_scan_tot", "k_scatter", "k_split",
-                                            "k_pairs", "k_vhub", "k_vbig", "k_vhash", "k_update"};
+                                            "k_pairs", "k_vhub", "k_vbig", "k_vhash", "k_update",
+                                            "k_u1_resample", "k_u2_count", "k_u3_select", "k_u4_close", "k_r_reduce"};
     return (k >= 0 && k < K_NKERNELS) ? names[k] : "";
 }
 
@@ -1095,6 +1134,23 @@ int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {
         for (tc_ctx *p : ctx->peers) *launches += p->last_launches;
     else
         *launches = ctx->last_launches;
+    return TC_OK;
+}
+
+int tc_get_steps(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *j, uint32_t *chim, uint32_t *ld, uint32_t *rd,
+                 uint64_t *d2, uint32_t *k2) {
+    if (!ctx || !ctx->peers.empty() || !ctx->steps.j || first > ctx->count || count > ctx->count - first)
+        return TC_EINVAL;
+    int rc = settle_allow_poisoned(ctx);
+    if (rc != TC_OK) return rc;
+    if (count == 0) return TC_OK;
+    const StepBufs &sb = ctx->steps;
+    if (j) CK(cudaMemcpy(j, sb.j + first, 4 * count, cudaMemcpyDeviceToHost));
+    if (chim) CK(cudaMemcpy(chim, sb.chim + first, 4 * count, cudaMemcpyDeviceToHost));
+    if (ld) CK(cudaMemcpy(ld, sb.ld + first, 4 * count, cudaMemcpyDeviceToHost));
+    if (rd) CK(cudaMemcpy(rd, sb.rd + first, 4 * count, cudaMemcpyDeviceToHost));
+    if (d2) CK(cudaMemcpy(d2, sb.d2 + first, 8 * count, cudaMemcpyDeviceToHost));
+    if (k2) CK(cudaMemcpy(k2, sb.k2 + first, 4 * count, cudaMemcpyDeviceToHost));
     return TC_OK;
 }
 

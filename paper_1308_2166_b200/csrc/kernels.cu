@@ -1445,6 +1445,155 @@ __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, Updat
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// a4..a8 split into one kernel per step (TC_TUNE_SPLIT_KERNELS): the same arithmetic as update_one, with the
+// intermediate values of every estimator kept in StepBufs (per-step parity against the oracle's trace, and
+// per-step timing -- the analogue of the paper's time-breakdown figure).
+
+#define TC_GRID_STRIDE(t, n) for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < (n); \
+                                  t += (uint64_t)gridDim.x * blockDim.x)
+
+// Ku1 -- Step 1, level-1 reservoir: one Philox block per estimator; a replaced f1 resets
+// chi, f2 and the closed flag (readings R2, R3).
+__global__ void __launch_bounds__(256) k_u1_resample(UpdateArgs u, const uint2 *E, StepBufs sb, uint32_t *ctr) {
+    if (ctr[kCtrErr]) {  // as k_update: the first batch to see the sticky error word records its index
+        if (blockIdx.x == 0 && threadIdx.x == 0 && ctr[kCtrFailB] == 0xFFFFFFFFu) ctr[kCtrFailB] = u.batch;
+        return;
+    }
+    TC_GRID_STRIDE(t, u.count) {
+        const uint64_t gid = u.first + t;
+        const DrawCtx dc{gid, u.batch, PhiloxKey{(uint32_t)u.seed, (uint32_t)(u.seed >> 32)}};
+        const uint4 o = philox4x32_10(make_uint4((uint32_t)gid, (uint32_t)(gid >> 32), u.batch, 0u), dc.key);
+        const uint64_t xlo = (uint64_t)o.x | ((uint64_t)o.y << 32);
+        const uint64_t d1 = bounded(u.m_prev + u.w, xlo, dc, 0x10000u);
+        const bool fresh = d1 >= u.m_prev;
+        const uint32_t j = fresh ? (uint32_t)(d1 - u.m_prev) : kEmptyV;
+        if (fresh) {
+            u.r1s[t] = E[j];
+            u.p1s[t] = (uint32_t)d1;
+            u.cfs[t] = 0u;
+            u.r2s[t] = make_uint2(kEmptyV, kEmptyV);
+            u.p2s[t] = kEmptyV;
+        }
+        sb.j[t] = j;
+        sb.xhi[t] = (uint64_t)o.z | ((uint64_t)o.w << 32);
+    }
+}
+
+// Ku2 -- Step 2a, chi^+ = rank(u->v) + rank(v->u): a fresh f1's ranks from einfo, a retained
+// f1's from the vertex table (deg_W, footnote PAPER.md:818-821).
+__global__ void __launch_bounds__(256) k_u2_count(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
+    if (ix.ctr[kCtrErr]) return;
+    TC_GRID_STRIDE(t, u.count) {
+        const uint2 r1 = u.r1s[t];
+        const uint32_t j = sb.j[t];
+        uint32_t ld, rd, endU, endV;
+        if (j != kEmptyV) {
+            const uint4 inf = ix.einfo[j];
+            ld = inf.y - 1u - inf.x;
+            rd = inf.w - 1u - inf.z;
+            endU = inf.y;
+            endV = inf.w;
+        } else {
+            VertProbe pu, pv;
+            vt_issue(ix.L, r1.x, pu);
+            vt_issue(ix.L, r1.y, pv);
+            const uint2 iu = vt_resolve(ix.L, pu, r1.x), iv = vt_resolve(ix.L, pv, r1.y);
+            ld = iu.x;
+            rd = iv.x;
+            endU = iu.y + iu.x;
+            endV = iv.y + iv.x;
+        }
+        sb.chim[t] = u.cfs[t] & kCMask;
+        sb.ld[t] = ld;
+        sb.rd[t] = rd;
+        sb.endU[t] = endU;
+        sb.endV[t] = endV;
+    }
+}
+
+// Ku3 -- Step 2b, level-2 select (naming 761-767): one draw d2 over chi^- + chi^+ (reading
+// R4); phi = d2 - chi^- names the (phi)-th arc at u, else the (phi - ld)-th at v, by segment arithmetic.
+__global__ void __launch_bounds__(256) k_u3_select(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
+    if (ix.ctr[kCtrErr]) return;
+    TC_GRID_STRIDE(t, u.count) {
+        const uint32_t ld = sb.ld[t], rd = sb.rd[t], chim = sb.chim[t], chi_p = ld + rd;
+        uint64_t d2 = ~0ull;
+        uint32_t k2 = kEmptyV;
+        if (chi_p) {
+            const uint64_t gid = u.first + t;
+            const DrawCtx dc{gid, u.batch, PhiloxKey{(uint32_t)u.seed, (uint32_t)(u.seed >> 32)}};
+            d2 = bounded((uint64_t)chim + chi_p, sb.xhi[t], dc, 0x20000u);
+            uint32_t cf = u.cfs[t];
+            if (d2 >= chim) {
+                const uint2 r1 = u.r1s[t];
+                const uint32_t phi = (uint32_t)(d2 - chim);
+                const bool atU = phi < ld;
+                const uint2 arc = ix.segS[(atU ? sb.endU[t] : sb.endV[t]) - 1u - (atU ? phi : phi - ld)];
+                const uint32_t src = atU ? r1.x : r1.y;
+                k2 = arc.x >> 1;
+                u.r2s[t] = make_uint2(min(src, arc.y), max(src, arc.y));
+                u.p2s[t] = (uint32_t)(u.m_prev + k2);
+                cf = 0u;  // a new f2 has no closing edge yet (reading R5)
+            }
+            u.cfs[t] = (cf & kClosedBit) | (chim + chi_p);
+        }
+        sb.d2[t] = d2;
+        sb.k2[t] = k2;
+    }
+}
+
+// Ku4 -- Step 3, closing edge: the wedge's closing pair in the edge-pair hash, after f2
+// (reading R6); skipped exactly when f1's endpoint x has no batch arc (the closing edge would touch x).
+__global__ void __launch_bounds__(256) k_u4_close(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
+    if (ix.ctr[kCtrErr]) return;
+    TC_GRID_STRIDE(t, u.count) {
+        const uint32_t cf = u.cfs[t];
+        const uint2 r2 = u.r2s[t];
+        if (r2.x == kEmptyV || (cf & kClosedBit)) continue;
+        const uint2 r1 = u.r1s[t];
+        const uint32_t x = (r1.x == r2.x || r1.x == r2.y) ? r1.y : r1.x;
+        const uint32_t z = (r2.x == r1.x || r2.x == r1.y) ? r2.y : r2.x;
+        const uint32_t degx = x == r1.x ? sb.ld[t] : sb.rd[t];
+        if (!degx) continue;
+        const uint32_t k2 = sb.k2[t];
+        const int64_t kk = pt_find(ix.L, min(x, z), max(x, z));
+        if (kk >= 0 && (k2 == kEmptyV || (uint32_t)kk > k2)) u.cfs[t] = cf | kClosedBit;
+    }
+}
+
+// Kr -- aggregation: S = sum of chi over closed estimators (exact u64) + the event counts.
+__global__ void __launch_bounds__(256) k_r_reduce(UpdateArgs u, StepBufs sb, unsigned long long *S,
+                                                  unsigned long long *stats, const uint32_t *ctr) {
+    if (ctr[kCtrErr]) return;
+    unsigned long long contrib = 0;
+    uint32_t n_fresh = 0, n_r2old = 0;
+    TC_GRID_STRIDE(t, u.count) {
+        const uint32_t cf = u.cfs[t];
+        if (cf & kClosedBit) contrib += cf & kCMask;
+        const bool fresh = sb.j[t] != kEmptyV;
+        n_fresh += fresh ? 1u : 0u;
+        n_r2old += (!fresh && sb.k2[t] != kEmptyV) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        contrib += __shfl_xor_sync(kFull, contrib, off);
+        n_fresh += __shfl_xor_sync(kFull, n_fresh, off);
+        n_r2old += __shfl_xor_sync(kFull, n_r2old, off);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (contrib) atomicAdd(S, contrib);
+        if (n_fresh) atomicAdd(stats + 0, (unsigned long long)n_fresh);
+        if (n_r2old) atomicAdd(stats + 1, (unsigned long long)n_r2old);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        atomicAdd(stats + 2, (unsigned long long)ctr[kCtrD]);
+        atomicAdd(stats + 3, 1ull);
+        atomicAdd(stats + 5, (unsigned long long)ctr[kCtrArcsBig]);
+        atomicAdd(stats + 6, (unsigned long long)ctr[kCtrDBig]);
+    }
+}
+
 __global__ void k_init_state(uint2 *r1, uint2 *r2, uint32_t *cf, uint32_t *p1, uint32_t *p2, uint64_t count) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
         r1[t] = make_uint2(kEmptyV, kEmptyV);
@@ -1618,6 +1767,30 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
         k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, nullptr);
     kr.end(K_UPDATE, s);
     return 1;
+}
+
+int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
+                        const KRec &kr) {
+    if (st.count == 0) return 0;
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), a.ptag}, ix.einfo, ix.segS, ix.ctr};
+    UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
+    const uint32_t grid = grid_for(st.count, 256, 8);
+    kr.beg(K_U1, s);
+    k_u1_resample<<<grid, 256, 0, s>>>(u, ix.E, sb, ix.ctr);
+    kr.end(K_U1, s);
+    kr.beg(K_U2, s);
+    k_u2_count<<<grid, 256, 0, s>>>(u, ui, sb);
+    kr.end(K_U2, s);
+    kr.beg(K_U3, s);
+    k_u3_select<<<grid, 256, 0, s>>>(u, ui, sb);
+    kr.end(K_U3, s);
+    kr.beg(K_U4, s);
+    k_u4_close<<<grid, 256, 0, s>>>(u, ui, sb);
+    kr.end(K_U4, s);
+    kr.beg(K_R, s);
+    k_r_reduce<<<grid, 256, 0, s>>>(u, sb, st.S + a.S_slot, st.stats, ix.ctr);
+    kr.end(K_R, s);
+    return 5;
 }
 
 int launch_init_state(const StateBufs &st, cudaStream_t s) {

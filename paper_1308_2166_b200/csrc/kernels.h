@@ -36,6 +36,20 @@ struct IndexBufs {
 
 constexpr int kNStats = 7;
 
+// Split estimator pass (tc_tune TC_TUNE_SPLIT_KERNELS): one kernel per step of SURVEY.md §8(a) -- Ku1 level-1
+// resample (a4), Ku2 adjacency count (a5), Ku3 level-2 select (a6), Ku4 closing-edge lookup (a7), Kr aggregation
+// (a8) -- with each step's values kept per estimator for per-step parity and per-step timing.
+struct StepBufs {
+    uint64_t count = 0;
+    uint32_t *j = nullptr;     // Step 1: replacement index in W, 0xFFFFFFFF = f1 retained
+    uint64_t *xhi = nullptr;   // the Philox word of Step 2's draw
+    uint32_t *chim = nullptr;  // chi^- (after Step 1)
+    uint32_t *ld = nullptr, *rd = nullptr;      // rank(u->v), rank(v->u): chi^+ = ld + rd
+    uint32_t *endU = nullptr, *endV = nullptr;  // segment ends of u and v
+    uint64_t *d2 = nullptr;    // Step 2's draw over chi^- + chi^+ (UINT64_MAX: no draw)
+    uint32_t *k2 = nullptr;    // batch position of the new f2 (0xFFFFFFFF: f2 kept)
+};
+
 struct StateBufs {
     uint64_t count = 0;
     uint2 *r1 = nullptr, *r2 = nullptr;
@@ -79,13 +93,14 @@ struct Tuning {
     uint32_t vbucket_arcs = 1024;  // target arcs per vertex bucket
     uint32_t vcap = 2048;
     uint32_t sortcap = kVChunk;
+    uint32_t split = 0;            // 1: the estimator pass as the split per-step kernels
 };
 
 Geometry make_geometry(uint32_t w, const Tuning &t);
 
 // Per-kernel profiling (tc_profile_kernels): ids match include/tc.h TC_KERNEL_*.
 enum KernelId { K_COUNT = 0, K_SCAN_COLS, K_SCAN_TOT, K_SCATTER, K_SPLIT, K_PAIRS, K_VHUB, K_VBIG, K_VHASH, K_UPDATE,
-                K_NKERNELS };
+                K_U1, K_U2, K_U3, K_U4, K_R, K_NKERNELS };
 struct KRec {
     cudaEvent_t *ev = nullptr;  // 2 K_NKERNELS events (begin, end) or null: no profiling
     uint32_t *used = nullptr;   // bit k set once kernel k's events were recorded in this push
@@ -110,6 +125,8 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 #endif
 constexpr uint32_t kBigCTAs = TC_BIG_CTAS;
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());
+int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
+                        const KRec &kr = KRec());
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
 int launch_group_sums(const StateBufs &st, uint64_t first, uint64_t N, uint32_t groups, unsigned long long *out,

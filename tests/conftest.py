@@ -11,3 +11,4 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: longer CPU statistical test")
+    config.addinivalue_line("markers", "sanitizer: compute-sanitizer run (one tool per GPU session; not part of -m gpu)")
