@@ -39,6 +39,8 @@ def test_compute_sanitizer(tool):
     os.makedirs(os.path.dirname(log), exist_ok=True)
     with open(log, "w") as f:
         f.write(out.stdout + "\n---- stderr ----\n" + out.stderr)
+    if "closed on this pool" in out.stdout + out.stderr:  # the GPU pool refuses compute-sanitizer
+        pytest.skip("compute-sanitizer is closed on this GPU pool")
     assert out.returncode == 0, out.stdout[-3000:] + out.stderr[-3000:]
     assert "sanitize workload ok" in out.stdout
     assert "ERROR SUMMARY: 0 errors" in out.stdout + out.stderr
