@@ -218,9 +218,16 @@ int tc_counters(tc_ctx *ctx, uint64_t *m, uint32_t *batches);
  * 1 = asynchronous (sticky error, reported at the next synchronising call). */
 int tc_set_async(tc_ctx *ctx, int async_errors);
 
-/* tc_set_graphs -- 1: each push runs as one CUDA graph (captured, then updated in place);
- * 0 (default): plain stream launches.  Results are identical; only launch overhead differs. */
+/* tc_set_graphs -- 1: each push runs as one CUDA graph: the launch sequence is captured once per batch shape
+ * (w, and the small-batch / split passes) and relaunched for every later batch of that shape with only its
+ * first node's arguments changed (the per-batch descriptor: input pointer, m, batch index, pair tag, S slot),
+ * so a push costs one small host call plus the graph launch; up to 4 shapes are kept (least recently used
+ * evicted; index growth and tc_tune drop them).  0 (default): plain stream launches.  Results are identical;
+ * only launch overhead differs. */
 int tc_set_graphs(tc_ctx *ctx, int enable);
+
+/* tc_graph_captures -- how many graphs the handle has captured so far (a steady stream: one per shape). */
+int tc_graph_captures(tc_ctx *ctx, uint64_t *captures);
 
 /* tc_tune -- index-geometry knobs (tests / tuning).  Results never depend on them; only speed does.
  *  TC_TUNE_VBUCKET_ARCS  target arcs per vertex bucket (default 1024; the bucket count is a power of two

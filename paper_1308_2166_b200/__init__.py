@@ -299,6 +299,11 @@ class TriangleCounter:
     def set_graphs(self, on: bool = True):
         self._ck(_lib.load().tc_set_graphs(self._h, 1 if on else 0), "tc_set_graphs")
 
+    def graph_captures(self) -> int:
+        out = C.c_uint64()
+        self._ck(_lib.load().tc_graph_captures(self._h, C.byref(out)), "tc_graph_captures")
+        return int(out.value)
+
     def tune(self, **knobs):
         """Index-geometry knobs (tc_tune): vbucket_arcs, vbucket_cap, vbucket_sort_cap."""
         for k, v in knobs.items():

@@ -67,9 +67,19 @@ struct tc_ctx {
     uint64_t prof_launch[TC_NPHASES] = {};
     double prof_kms[K_NKERNELS] = {};
     uint64_t prof_klaunch[K_NKERNELS] = {};
-    // CUDA graph of the per-batch launch sequence (re-captured per push, updated in place)
-    int use_graph = 0;  // opt-in (tc_set_graphs): re-capturing per push costs more host time than it saves
-    cudaGraphExec_t gexec = nullptr;
+    // CUDA graphs of the per-batch launch sequence, one per batch shape (w, small-batch pass, split pass):
+    // captured once, then relaunched with only the descriptor node's arguments changed (BatchDesc)
+    int use_graph = 0;  // opt-in (tc_set_graphs)
+    struct GraphEntry {
+        uint64_t key = 0, last_use = 0;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t desc_node = nullptr;
+        uint32_t launches = 0;
+    };
+    std::vector<GraphEntry> graphs;
+    uint64_t graph_clock = 0;
+    uint64_t graph_captures = 0;  // how many captures (tests: a steady stream captures once per shape)
     Tuning tune;
     // multi-GPU: a rank handle (tc_create_rank, or a peer of a tc_create_ex group) owns the
     // global estimator ids [first, first + count) of r and an NCCL communicator; every batch is broadcast from
@@ -135,7 +145,7 @@ static bool alloc_steps(StepBufs &sb, uint64_t count) {
 
 static void free_index(IndexBufs &ix) {
     void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
-                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2, ix.filt};
+                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2, ix.filt, ix.desc};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
 }
@@ -145,6 +155,14 @@ constexpr uint64_t kMaxBatch = 1ull << 28;  // 32-bit table offsets (vertex slic
 constexpr uint64_t kStartWords = kMaxBuckets + 8;  // vstart: bucket sizes -> prefixes (+ grand total)
 
 // (Re)allocate the per-batch index for batches of up to w edges.
+static void drop_graphs(tc_ctx *ctx) {
+    for (auto &g : ctx->graphs) {
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+        if (g.graph) cudaGraphDestroy(g.graph);
+    }
+    ctx->graphs.clear();
+}
+
 extern "C" {
 static int settle(tc_ctx *ctx);
 }
@@ -155,6 +173,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     const int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     CK(cudaStreamSynchronize(ctx->copy));
+    drop_graphs(ctx);  // the captured graphs hold the old buffers' addresses
     free_index(ctx->ix);
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
@@ -171,7 +190,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
          cudaMalloc(&ix.offV, 4ull * (1u << kMaxPartBits) * ix.tiles_cap) == cudaSuccess &&
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
          cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess &&
-         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess && cudaMalloc(&ix.filt, 4ull * kFilterWords) == cudaSuccess;
+         cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess && cudaMalloc(&ix.filt, 4ull * kFilterWords) == cudaSuccess &&
+         cudaMalloc(&ix.desc, sizeof(BatchDesc)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
         free_index(ix);
@@ -233,7 +253,7 @@ static void destroy_ctx(tc_ctx *ctx) {
     for (auto &set : ctx->ev_pool)
         for (auto &e : set)
             if (e) cudaEventDestroy(e);
-    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+    drop_graphs(ctx);
     if (ctx->side) cudaStreamDestroy(ctx->side);
     if (ctx->side2) cudaStreamDestroy(ctx->side2);
     if (ctx->copy) cudaStreamDestroy(ctx->copy);
@@ -500,98 +520,151 @@ static int push_prepare(tc_ctx *ctx, const tc_edge *edges, uint64_t w, PushPrep 
     return TC_OK;
 }
 
+// The kernels of one push (after k_desc), on the handle's streams; returns the number of launches.
+static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr, bool *ok_out) {
+    IndexBufs &ix = ctx->ix;
+    bool ok = true;
+    uint32_t launches = 0;
+    // profiled pushes run every kernel on the main stream, so each kernel's events time it alone
+    cudaStream_t ms = ctx->stream, ss = ctx->prof ? ms : ctx->side, s2 = ctx->prof ? ms : ctx->side2;
+    auto rec = [&](int e, cudaStream_t st) {
+        if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev_pool[ctx->ev_used][e], st) == cudaSuccess;
+    };
+    // a1: count, scans, scatter (k_count zeroes the counters and this batch's S)
+    rec(2 * TC_PHASE_PARTITION, ms);
+    launches += launch_partition(ix, a, ms, kr);
+    rec(2 * TC_PHASE_PARTITION + 1, ms);
+    // a3 (it reads only the raw batch) on the second stream, alongside the vertex phase
+    ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
+    ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
+    rec(2 * TC_PHASE_PAIRS, ss);
+    launches += launch_pairs(ix, a, ss, kr);
+    rec(2 * TC_PHASE_PAIRS + 1, ss);
+    ok = ok && cudaEventRecord(ctx->join, ss) == cudaSuccess;
+    ok = ok && cudaEventRecord(ctx->fork2, ms) == cudaSuccess;
+    // a2: the large vertex buckets on the third stream, the common ones on the main stream
+    ok = ok && cudaStreamWaitEvent(s2, ctx->fork2, 0) == cudaSuccess;
+    launches += launch_vertices_big(ix, a, s2, kr);
+    ok = ok && cudaEventRecord(ctx->join2, s2) == cudaSuccess;
+    rec(2 * TC_PHASE_VERTICES, ms);
+    launches += launch_vertices(ix, a, ms, kr);
+    ok = ok && cudaStreamWaitEvent(ms, ctx->join2, 0) == cudaSuccess;
+    rec(2 * TC_PHASE_VERTICES + 1, ms);
+    ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
+    rec(2 * TC_PHASE_UPDATE, ms);
+    if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
+    else launches += launch_update(ix, ctx->st, a, ms, kr);
+    rec(2 * TC_PHASE_UPDATE + 1, ms);
+    *ok_out = ok;
+    return launches;
+}
+
+// The graph of a batch shape: found in the cache, or captured (k_desc + the kernels) and instantiated.
+static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx::GraphEntry **out) {
+    const uint64_t key = (uint64_t)a.g.w | ((uint64_t)a.small << 32) | ((uint64_t)ctx->tune.split << 33);
+    for (auto &g : ctx->graphs)
+        if (g.key == key) {
+            g.last_use = ++ctx->graph_clock;
+            *out = &g;
+            return TC_OK;
+        }
+    if (ctx->graphs.size() >= 4) {  // evict the least recently used shape
+        auto lru = std::min_element(ctx->graphs.begin(), ctx->graphs.end(),
+                                    [](const tc_ctx::GraphEntry &x, const tc_ctx::GraphEntry &y) { return x.last_use < y.last_use; });
+        if (lru->exec) cudaGraphExecDestroy(lru->exec);
+        if (lru->graph) cudaGraphDestroy(lru->graph);
+        ctx->graphs.erase(lru);
+    }
+    tc_ctx::GraphEntry e;
+    e.key = key;
+    e.last_use = ++ctx->graph_clock;
+    CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    launch_desc(ctx->ix, d, ctx->stream);
+    bool ok = true;
+    e.launches = 1 + enqueue_kernels(ctx, a, KRec(), &ok);
+    const bool cap = cudaStreamEndCapture(ctx->stream, &e.graph) == cudaSuccess && e.graph;
+    if (!ok || !cap) {
+        if (e.graph) cudaGraphDestroy(e.graph);
+        return fail_cuda(ctx);
+    }
+    size_t n = 0;
+    CK(cudaGraphGetNodes(e.graph, nullptr, &n));
+    std::vector<cudaGraphNode_t> nodes(n);
+    CK(cudaGraphGetNodes(e.graph, nodes.data(), &n));
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        if (cudaGraphNodeGetType(nd, &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess && kp.func == desc_kernel()) e.desc_node = nd;
+    }
+    cudaGetLastError();
+    if (!e.desc_node || cudaGraphInstantiate(&e.exec, e.graph, 0) != cudaSuccess) {
+        cudaGraphDestroy(e.graph);
+        return fail_cuda(ctx);
+    }
+    ++ctx->graph_captures;
+    ctx->graphs.push_back(e);
+    *out = &ctx->graphs.back();
+    return TC_OK;
+}
+
 static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     IndexBufs &ix = ctx->ix;
     const int slot = (int)((ctx->b + 1) & 1u);
     BatchArgs a;
-    a.in = pp.in;
-    a.m_prev = ctx->m;
-    a.batch = ctx->b;
     a.first = ctx->first;
     a.seed = ctx->seed;
-    a.S_slot = slot;
-    a.S_reset = ctx->st.S + slot;
+    a.S = ctx->st.S;
     a.g = make_geometry((uint32_t)w, ctx->tune);
     a.small = ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax);
     if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
         CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
         ctx->ptag = 1;
     }
-    a.ptag = ctx->ptag;
-    // The batch's whole device sequence (counter resets + kernels) can be captured as one CUDA graph and the
-    // previous graph executable updated in place.
-    const bool graph = ctx->use_graph != 0 && !ctx->prof;  // profiling events need plain launches
-    KRec kr;
-    if (ctx->prof) {
-        kr.ev = &ctx->ev_pool[ctx->ev_used][2 * TC_NPHASES];
-        ctx->ev_kused[ctx->ev_used] = 0u;
-        kr.used = &ctx->ev_kused[ctx->ev_used];
+    BatchDesc d;
+    d.in = pp.in;
+    d.m_prev = ctx->m;
+    d.batch = ctx->b;
+    d.ptag = ctx->ptag;
+    d.slot = (uint32_t)slot;
+    d.pad = 0;
+    // the error word is sticky in asynchronous mode, and cleared (or set to the overflow error) here in strict
+    // mode -- stream operations ahead of the kernels, outside any graph
+    if (!ctx->async_errors) {
+        CK(cudaMemsetAsync(ix.ctr + kCtrErr, 0, 4, ctx->stream));
+        CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
+        if (pp.ovf) CK(cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ctx->stream));
     }
-    if (graph) CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    const bool graph = ctx->use_graph != 0 && !ctx->prof;  // profiling events need plain launches
     uint32_t launches = 0;
-    {
+    if (graph) {
+        tc_ctx::GraphEntry *ge = nullptr;
+        const int rc = graph_for(ctx, a, d, &ge);
+        if (rc != TC_OK) return rc;
+        BatchDesc *dst = ix.desc;
+        void *args[] = {&d, &dst};
+        cudaKernelNodeParams kp{};
+        kp.func = const_cast<void *>(desc_kernel());
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        CK(cudaGraphExecKernelNodeSetParams(ge->exec, ge->desc_node, &kp));
+        CK(cudaGraphLaunch(ge->exec, ctx->stream));
+        launches = ge->launches;
+    } else {
+        KRec kr;
+        if (ctx->prof) {
+            kr.ev = &ctx->ev_pool[ctx->ev_used][2 * TC_NPHASES];
+            ctx->ev_kused[ctx->ev_used] = 0u;
+            kr.used = &ctx->ev_kused[ctx->ev_used];
+        }
+        launch_desc(ix, d, ctx->stream);
         bool ok = true;
-        // profiled pushes run every kernel on the main stream, so each kernel's events time it alone
-        cudaStream_t ms = ctx->stream, ss = ctx->prof ? ms : ctx->side, s2 = ctx->prof ? ms : ctx->side2;
-        auto rec = [&](int e, cudaStream_t st) {
-            if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev_pool[ctx->ev_used][e], st) == cudaSuccess;
-        };
-        // k_count zeroes the counters and this batch's S; the error word is sticky in asynchronous mode and
-        // cleared (or set to the overflow error) here in strict mode
-        if (!ctx->async_errors)
-            ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, 0, 4, ms) == cudaSuccess &&
-                 cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ms) == cudaSuccess;
-        if (!ctx->async_errors && pp.ovf) ok = ok && cudaMemsetAsync(ix.ctr + kCtrErr, (int)kErrOvf, 1, ms) == cudaSuccess;
-        // a1: count, scans, scatter
-        rec(2 * TC_PHASE_PARTITION, ms);
-        launches += launch_partition(ix, a, ms, kr);
-        rec(2 * TC_PHASE_PARTITION + 1, ms);
-        // a3 (it reads only the raw batch) on the second stream, alongside the vertex phase
-        ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
-        ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
-        rec(2 * TC_PHASE_PAIRS, ss);
-        launches += launch_pairs(ix, a, ss, kr);
-        rec(2 * TC_PHASE_PAIRS + 1, ss);
-        ok = ok && cudaEventRecord(ctx->join, ss) == cudaSuccess;
-        ok = ok && cudaEventRecord(ctx->fork2, ms) == cudaSuccess;
-        // a2: the large vertex buckets on the third stream, the common ones on the main stream
-        ok = ok && cudaStreamWaitEvent(s2, ctx->fork2, 0) == cudaSuccess;
-        launches += launch_vertices_big(ix, a, s2, kr);
-        ok = ok && cudaEventRecord(ctx->join2, s2) == cudaSuccess;
-        rec(2 * TC_PHASE_VERTICES, ms);
-        launches += launch_vertices(ix, a, ms, kr);
-        ok = ok && cudaStreamWaitEvent(ms, ctx->join2, 0) == cudaSuccess;
-        rec(2 * TC_PHASE_VERTICES + 1, ms);
-        ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
-        rec(2 * TC_PHASE_UPDATE, ms);
-        if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
-        else launches += launch_update(ix, ctx->st, a, ms, kr);
-        rec(2 * TC_PHASE_UPDATE + 1, ms);
+        launches = 1 + enqueue_kernels(ctx, a, kr, &ok);
         if (ctx->prof)
             for (int p = 0; p < TC_NPHASES; ++p)
                 ctx->prof_launch[p] += (p == TC_PHASE_PARTITION ? 4 + (a.g.bs ? 1 : 0) : p == TC_PHASE_VERTICES ? 3 : 1);
-        if (graph) {
-            cudaGraph_t g = nullptr;
-            const bool cap = cudaStreamEndCapture(ctx->stream, &g) == cudaSuccess && g;
-            if (!ok || !cap) {
-                if (g) cudaGraphDestroy(g);
-                return fail_cuda(ctx);
-            }
-            cudaGraphExecUpdateResultInfo info;
-            if (!ctx->gexec || cudaGraphExecUpdate(ctx->gexec, g, &info) != cudaSuccess) {
-                cudaGetLastError();
-                if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
-                ctx->gexec = nullptr;
-                if (cudaGraphInstantiate(&ctx->gexec, g, 0) != cudaSuccess) {
-                    cudaGraphDestroy(g);
-                    return fail_cuda(ctx);
-                }
-            }
-            cudaGraphDestroy(g);
-            CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
-        } else if (!ok) {
-            return fail_cuda(ctx);
-        }
+        if (!ok) return fail_cuda(ctx);
     }
     if (ctx->prof) ++ctx->ev_used;
     CK(cudaGetLastError());
@@ -695,6 +768,7 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
     return each(ctx, [&](tc_ctx *c) -> int {
         int rc = settle(c);
         if (rc != TC_OK) return rc;
+        drop_graphs(c);  // the geometry of a batch shape may change
         switch (knob) {
             case TC_TUNE_VBUCKET_ARCS:
                 if (value < 1 || value > (1u << 30)) return TC_EINVAL;
@@ -1125,6 +1199,16 @@ int tc_stats(tc_ctx *ctx, uint64_t *out, int n) {
     CK(cudaMemcpy(v, ctx->st.stats, 8 * kNStats, cudaMemcpyDeviceToHost));
     for (int i = 0; i < n && i < kNStats; ++i) out[i] = v[i];
     return kNStats;
+}
+
+int tc_graph_captures(tc_ctx *ctx, uint64_t *captures) {
+    if (!ctx || !captures) return TC_EINVAL;
+    *captures = 0;
+    if (!ctx->peers.empty())
+        for (tc_ctx *p : ctx->peers) *captures += p->graph_captures;
+    else
+        *captures = ctx->graph_captures;
+    return TC_OK;
 }
 
 int tc_last_launches(tc_ctx *ctx, uint32_t *launches) {

@@ -60,6 +60,17 @@ constexpr int kCtrArcsBig = 7; // arcs grouped by the large-bucket kernels (k_vh
 constexpr int kCtrDBig = 8;    // distinct vertices of those buckets
 constexpr int kCtrWords = 16;
 
+// Per-batch values the kernels read from device memory (written by k_desc, the first node of every push), so
+// that one captured CUDA graph per batch shape is relaunched unchanged from batch to batch.
+struct __align__(32) BatchDesc {
+    const uint2 *in;             // the raw batch on this device
+    unsigned long long m_prev;   // |E| before the batch
+    uint32_t batch;              // index b of this non-empty batch (the Philox counter word)
+    uint32_t ptag;               // edge-pair slot tag of this push (1..254)
+    uint32_t slot;               // S accumulator slot of this batch
+    uint32_t pad;
+};
+
 struct __align__(16) VSlot {
     uint32_t key, deg, start, pad;
 };

@@ -108,7 +108,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *s
 // a1: bucket histograms
 
 struct PartArgs {
-    const uint2 *in;
+    const BatchDesc *d;  // in, ptag, slot (per batch)
     Geometry g;
     uint2 *E;
     uint4 *arcs;  // {vertex, k<<1|side, neighbour, 0}
@@ -117,19 +117,19 @@ struct PartArgs {
     uint16_t *arank;   // [2 w] in-tile ranks
     uint32_t *vstart;  // bucket sizes (k_scan_cols) -> exclusive prefixes (k_scan_tot)
     uint2 *pt;         // edge-pair table (G groups of 4 slots)
-    uint32_t G, ptag;
+    uint32_t G;
     uint32_t *ctr;
     uint32_t *filt;    // small batches: the vertex filter to fill (else null)
-    unsigned long long *S_reset;  // k_count zeroes this batch's S accumulator and the counters (not the error word)
+    unsigned long long *S;  // the two S accumulators: k_count zeroes this batch's (d->slot) and the counters
 };
 
 // a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
 // with room along its probe sequence (A, B, A+1, ...), by 64-bit CAS, so the live slots of a group form a
 // prefix.  Meeting the
 // same pair (confirmed against the raw batch, which is stable while E is being written) returns true.
-__device__ __forceinline__ bool pt_insert(const PartArgs &a, uint2 n, uint32_t k) {
+__device__ __forceinline__ bool pt_insert(const PartArgs &a, const uint2 *in, uint32_t ptag, uint2 n, uint32_t k) {
     const uint64_t h = hash_pair64(pair_key(n.x, n.y));
-    const uint32_t tf = (a.ptag << 24) | pfinger(h);
+    const uint32_t tf = (ptag << 24) | pfinger(h);
     const unsigned long long mine = (unsigned long long)k | ((unsigned long long)tf << 32);
     unsigned long long *t64 = reinterpret_cast<unsigned long long *>(a.pt);
     const uint32_t A = pgroup_start(h, a.G), B = pgroup_second(h, a.G, A);
@@ -141,13 +141,13 @@ __device__ __forceinline__ bool pt_insert(const PartArgs &a, uint2 n, uint32_t k
 #pragma unroll
         for (uint32_t i = 0; i < 4; ++i) {
             unsigned long long cur = cur4[i];
-            if ((uint32_t)(cur >> 56) != a.ptag) {
+            if ((uint32_t)(cur >> 56) != ptag) {
                 const unsigned long long old = atomicCAS(t64 + 4ull * g + i, cur, mine);
                 if (old == cur) return false;
                 cur = old;  // taken meanwhile (by this batch)
             }
             if ((uint32_t)(cur >> 32) == tf) {
-                const uint2 o = norm_edge(__ldg(a.in + (uint32_t)cur));
+                const uint2 o = norm_edge(__ldg(in + (uint32_t)cur));
                 if (o.x == n.x && o.y == n.y) return true;
             }
         }
@@ -157,12 +157,14 @@ __device__ __forceinline__ bool pt_insert(const PartArgs &a, uint2 n, uint32_t k
 __global__ void __launch_bounds__(256) k_pairs(PartArgs a) {
     if (a.ctr[kCtrErr] & (kErrStage | kErrDup)) return;  // sticky error of an earlier async batch
     const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint2 *in = a.d->in;
+    const uint32_t ptag = a.d->ptag;
     bool dup = false;
     if (k < a.g.w) {
-        const uint2 e = __ldg(a.in + k);
+        const uint2 e = __ldg(in + k);
         if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // k_count reports the rest
             const uint2 n = norm_edge(e);
-            dup = pt_insert(a, n, k);
+            dup = pt_insert(a, in, ptag, n, k);
             if (a.filt) {
                 const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
                 atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
@@ -187,9 +189,10 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
     if (blockIdx.x == 0) {  // per-batch resets (every later kernel of the batch starts after this one)
         if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
             a.ctr[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) *a.S_reset = 0ull;
+        if (threadIdx.x == 0) a.S[a.d->slot] = 0ull;
     }
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
+    const uint2 *in = a.d->in;
     extern __shared__ uint32_t dsh[];
     const uint32_t nV = 1u << a.g.bp1;
     uint16_t *wv = reinterpret_cast<uint16_t *>(dsh);  // [kTileWarps][nV]
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
     for (uint32_t j = 0; j < kEdgeRounds; ++j) {
         const uint32_t i = warp * kEdgesPerWarp + j * 32u + lane;
         if (i < ne) {
-            const uint2 e = __ldg(a.in + e0 + i);
+            const uint2 e = __ldg(in + e0 + i);
             a.E[e0 + i] = norm_edge(e);
             if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
             else if (e.x == e.y) bad |= kErrLoop;
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
         const bool valid = (ai >> 1) < ne;
         uint32_t d = 0;
         if (valid) {
-            const uint2 n = norm_edge(__ldg(a.in + e0 + (ai >> 1)));
+            const uint2 n = norm_edge(__ldg(in + e0 + (ai >> 1)));
             d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bp1);
         }
         const uint32_t peers = digit_peers_c<NB>(d, valid);
@@ -1215,9 +1218,17 @@ struct UpdateArgs {
     uint2 *r1s, *r2s;
     uint32_t *cfs, *p1s, *p2s;
     uint64_t count, first, seed;
-    uint32_t batch, w;
-    uint64_t m_prev;
+    uint32_t batch, w;          // batch: filled from the descriptor at kernel entry (with_desc)
+    uint64_t m_prev;            // likewise
+    const BatchDesc *d;
 };
+
+// The per-batch values of the descriptor into the kernel's own copies of its arguments.
+__device__ __forceinline__ void with_desc(UpdateArgs &u, Lookup &L) {
+    u.batch = u.d->batch;
+    u.m_prev = u.d->m_prev;
+    L.ptag = u.d->ptag;
+}
 
 template <bool kSmall>
 __device__ __forceinline__ EstState load_state(const UpdateArgs &u, uint64_t t) {
@@ -1376,6 +1387,8 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
 template <bool kSmall>
 __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
                                                    unsigned long long *stats, const uint32_t *filt) {
+    with_desc(u, ix.L);
+    S += u.d->slot;
     if (ix.ctr[kCtrErr]) {  // this batch (or, in asynchronous mode, an earlier one) was rejected: no update
         // the first batch to see the sticky error word is the one that set it: record its index so that the
         // host can restore m and the batch count of the last accepted batch
@@ -1456,6 +1469,8 @@ __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, Updat
 // Ku1 -- Step 1, level-1 reservoir: one Philox block per estimator; a replaced f1 resets
 // chi, f2 and the closed flag (readings R2, R3).
 __global__ void __launch_bounds__(256) k_u1_resample(UpdateArgs u, const uint2 *E, StepBufs sb, uint32_t *ctr) {
+    u.batch = u.d->batch;
+    u.m_prev = u.d->m_prev;
     if (ctr[kCtrErr]) {  // as k_update: the first batch to see the sticky error word records its index
         if (blockIdx.x == 0 && threadIdx.x == 0 && ctr[kCtrFailB] == 0xFFFFFFFFu) ctr[kCtrFailB] = u.batch;
         return;
@@ -1483,6 +1498,7 @@ __global__ void __launch_bounds__(256) k_u1_resample(UpdateArgs u, const uint2 *
 // Ku2 -- Step 2a, chi^+ = rank(u->v) + rank(v->u): a fresh f1's ranks from einfo, a retained
 // f1's from the vertex table (deg_W, footnote PAPER.md:818-821).
 __global__ void __launch_bounds__(256) k_u2_count(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
+    with_desc(u, ix.L);
     if (ix.ctr[kCtrErr]) return;
     TC_GRID_STRIDE(t, u.count) {
         const uint2 r1 = u.r1s[t];
@@ -1515,6 +1531,7 @@ __global__ void __launch_bounds__(256) k_u2_count(UpdateArgs u, UpdateIdx ix, St
 // Ku3 -- Step 2b, level-2 select (naming 761-767): one draw d2 over chi^- + chi^+ (reading
 // R4); phi = d2 - chi^- names the (phi)-th arc at u, else the (phi - ld)-th at v, by segment arithmetic.
 __global__ void __launch_bounds__(256) k_u3_select(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
+    with_desc(u, ix.L);
     if (ix.ctr[kCtrErr]) return;
     TC_GRID_STRIDE(t, u.count) {
         const uint32_t ld = sb.ld[t], rd = sb.rd[t], chim = sb.chim[t], chi_p = ld + rd;
@@ -1546,6 +1563,7 @@ __global__ void __launch_bounds__(256) k_u3_select(UpdateArgs u, UpdateIdx ix, S
 // Ku4 -- Step 3, closing edge: the wedge's closing pair in the edge-pair hash, after f2
 // (reading R6); skipped exactly when f1's endpoint x has no batch arc (the closing edge would touch x).
 __global__ void __launch_bounds__(256) k_u4_close(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
+    with_desc(u, ix.L);
     if (ix.ctr[kCtrErr]) return;
     TC_GRID_STRIDE(t, u.count) {
         const uint32_t cf = u.cfs[t];
@@ -1565,6 +1583,7 @@ __global__ void __launch_bounds__(256) k_u4_close(UpdateArgs u, UpdateIdx ix, St
 // Kr -- aggregation: S = sum of chi over closed estimators (exact u64) + the event counts.
 __global__ void __launch_bounds__(256) k_r_reduce(UpdateArgs u, StepBufs sb, unsigned long long *S,
                                                   unsigned long long *stats, const uint32_t *ctr) {
+    S += u.d->slot;
     if (ctr[kCtrErr]) return;
     unsigned long long contrib = 0;
     uint32_t n_fresh = 0, n_r2old = 0;
@@ -1616,6 +1635,16 @@ __global__ void k_group_sums(const uint32_t *__restrict__ cf, uint64_t count, ui
         atomicAdd(out + g, (unsigned long long)(v & kCMask));
     }
 }
+
+// The first node of every push: the batch's descriptor into device memory.
+__global__ void k_desc(BatchDesc d, BatchDesc *dst) { *dst = d; }
+
+int launch_desc(const IndexBufs &ix, const BatchDesc &d, cudaStream_t s) {
+    k_desc<<<1, 1, 0, s>>>(d, ix.desc);
+    return 1;
+}
+
+const void *desc_kernel() { return (const void *)k_desc; }
 
 // Test hooks (tc_test_draws / tc_test_philox): the estimator pass's own device functions on chosen inputs.
 __global__ void k_test_draws(const uint64_t *n, const uint64_t *x, const uint64_t *id, const uint32_t *b,
@@ -1687,8 +1716,8 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{a.in, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), a.ptag, ix.ctr,
-                    a.small ? ix.filt : nullptr, a.S_reset};
+    return PartArgs{ix.desc, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), ix.ctr,
+                    a.small ? ix.filt : nullptr, a.S};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
@@ -1757,14 +1786,14 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), a.ptag}, ix.einfo, ix.segS, ix.ctr};
-    UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.einfo, ix.segS, ix.ctr};
+    UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);
     if (a.small)
-        k_update<true><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, ix.filt);
+        k_update<true><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, ix.filt);
     else
-        k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S + a.S_slot, st.stats, nullptr);
+        k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, nullptr);
     kr.end(K_UPDATE, s);
     return 1;
 }
@@ -1772,8 +1801,8 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), a.ptag}, ix.einfo, ix.segS, ix.ctr};
-    UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, a.batch, a.g.w, a.m_prev};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.einfo, ix.segS, ix.ctr};
+    UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, 8);
     kr.beg(K_U1, s);
     k_u1_resample<<<grid, 256, 0, s>>>(u, ix.E, sb, ix.ctr);
@@ -1788,7 +1817,7 @@ int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs
     k_u4_close<<<grid, 256, 0, s>>>(u, ui, sb);
     kr.end(K_U4, s);
     kr.beg(K_R, s);
-    k_r_reduce<<<grid, 256, 0, s>>>(u, sb, st.S + a.S_slot, st.stats, ix.ctr);
+    k_r_reduce<<<grid, 256, 0, s>>>(u, sb, st.S, st.stats, ix.ctr);
     kr.end(K_R, s);
     return 5;
 }

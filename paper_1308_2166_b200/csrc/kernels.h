@@ -32,6 +32,7 @@ struct IndexBufs {
     uint32_t *filt = nullptr;      // [kFilterWords] small-batch filter over the batch's vertices
     uint2 *stage = nullptr;        // [wcap] H2D staging for host batches (two buffers, alternating)
     uint2 *stage2 = nullptr;
+    BatchDesc *desc = nullptr;     // the per-batch descriptor (k_desc writes it; every kernel reads it)
 };
 
 constexpr int kNStats = 7;
@@ -72,15 +73,13 @@ struct Geometry {
     uint32_t sortcap;  // k_vbig: buckets larger than this take the chunked global-memory path (<= kVChunk)
 };
 
+// Launch-time values of a push.  The per-batch values (input pointer, m, batch index, pair tag, S slot) are
+// NOT here: the kernels read them from the device descriptor (BatchDesc), so a captured graph of the launch
+// sequence depends only on the batch shape (w and the flags below).
 struct BatchArgs {
-    const uint2 *in;  // w raw edges (device)
-    uint64_t m_prev;
-    uint32_t batch;   // index b of this (non-empty) batch
     uint64_t first;   // global id of local estimator 0
     uint64_t seed;
-    int S_slot;
-    unsigned long long *S_reset;  // the S accumulator of this batch (zeroed by k_count)
-    uint32_t ptag;    // edge-pair table tag of this push (1..254)
+    unsigned long long *S;  // the two S accumulators (slot from the descriptor)
     bool small;       // small-batch estimator pass (filters built by k_pairs, k_update skips untouched estimators)
     Geometry g;
 };
@@ -127,6 +126,9 @@ constexpr uint32_t kBigCTAs = TC_BIG_CTAS;
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr = KRec());
+
+int launch_desc(const IndexBufs &ix, const BatchDesc &d, cudaStream_t s);  // the push's first node
+const void *desc_kernel();                                                  // its function (graph node lookup)
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
 int launch_group_sums(const StateBufs &st, uint64_t first, uint64_t N, uint32_t groups, unsigned long long *out,
