@@ -144,7 +144,7 @@ static bool alloc_steps(StepBufs &sb, uint64_t count) {
 }
 
 static void free_index(IndexBufs &ix) {
-    void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.einfo, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
+    void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.apos, ix.pslot, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
                     ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2, ix.filt, ix.desc};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
@@ -178,7 +178,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     IndexBufs &ix = ctx->ix;
     const uint64_t cap = std::max<uint64_t>(next_pow2(w), 1024);
     ix.tiles_cap = (cap + kTileEdges - 1) / kTileEdges;
-    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.einfo, 16 * cap) == cudaSuccess &&
+    bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.apos, 8 * cap) == cudaSuccess &&
+              cudaMalloc(&ix.pslot, 16 * cap) == cudaSuccess &&
               cudaMalloc(&ix.segS, 16 * cap) == cudaSuccess &&
               cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
               cudaMalloc(&ix.vt, 16 * 4 * cap) == cudaSuccess &&  // slices at 2 * (bucket start), <= 2 n_b slots

@@ -109,6 +109,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *s
 
 struct PartArgs {
     const BatchDesc *d;  // in, ptag, slot (per batch)
+    uint32_t *apos2;     // [2 w] partition position of every arc (by arc id k<<1|side)
     Geometry g;
     uint2 *E;
     uint4 *arcs;  // {vertex, k<<1|side, neighbour, 0}
@@ -370,7 +371,9 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
         const uint2 n = sE[ai >> 1];
         const uint32_t v = (ai & 1u) ? n.y : n.x, nb = (ai & 1u) ? n.x : n.y;
         const uint32_t d = vbucket_of(hash_vertex(v), a.g.bp1);
-        __stcs(a.arcs + soff[d] + (pos - toff[d]), make_uint4(v, 2u * e0 + ai, nb, 0u));
+        const uint32_t P = soff[d] + (pos - toff[d]);  // the arc's partition position (kept through k_split in .w)
+        __stcs(a.arcs + P, make_uint4(v, 2u * e0 + ai, nb, P));
+        a.apos2[2u * e0 + ai] = P;  // per arc, by arc id: the tile's own contiguous range (sectors fill in L2)
     }
 }
 
@@ -472,7 +475,8 @@ struct VertArgs {
     const uint2 *E;
     const uint32_t *vstart;
     uint2 *segS;        // [2 w] {k<<1|side, neighbour} grouped by vertex
-    uint2 *einfo2;      // [2 w]: einfo2[k<<1|side] = {sorted slot, segment end}
+    uint2 *pslot;       // [2 w]: pslot[partition position of an arc] = {its slot in segS, its segment's end}
+    const uint32_t *apos2;  // [2 w] partition position by arc id (the radix-sort paths carry arc ids only)
     VSlot *vt;
     uint2 *vslice;
     const uint32_t *vperm;
@@ -656,7 +660,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
             if (i == 0 || x.x != sbuf[i - 1].x) ++r;
             const uint32_t end = r < D ? run_start[r] : n;  // run r-1 ends where run r starts
             a.segS[base + i] = make_uint2(x.y, arc_neighbour(a.E, x.y));
-            a.einfo2[x.y] = make_uint2(base + i, base + end);
+            a.pslot[a.apos2[x.y]] = make_uint2(base + i, base + end);
         }
         // the slice, built in shared memory and written whole
         if (threadIdx.x == 0) {
@@ -791,7 +795,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
             const uint32_t run = r - 1;
             const uint32_t end = run + 1 < D ? gruns[run + 1] : n;
             a.segS[base + i] = make_uint2(x.y, arc_neighbour(a.E, x.y));
-            a.einfo2[x.y] = make_uint2(base + i, base + end);
+            a.pslot[a.apos2[x.y]] = make_uint2(base + i, base + end);
         }
         carry += tot;
     }
@@ -867,7 +871,7 @@ struct HL {
 // Arcs of a bucket as the hash path reads them: straight from the bucketed arcs, or (after a hub vertex
 // was peeled off) from a shared-memory list of the remaining arcs.
 struct ArcSrc {
-    const uint4 *g;                    // global {vertex, val, neighbour, 0} (g != nullptr), else:
+    const uint4 *g;                    // global {vertex, val, neighbour, partition position} (g != nullptr), else:
     const uint32_t *sv, *sval, *snb;   // shared-memory lists
     __device__ __forceinline__ uint32_t v(uint32_t i) const { return g ? g[i].x : sv[i]; }
     __device__ __forceinline__ uint2 vv(uint32_t i) const {
@@ -1002,7 +1006,9 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         const uint32_t l = pk[j] >> 16;
         const uint32_t pos = segst[l] + (pk[j] & 0xFFFFu);
         a.segS[b0 + pos] = make_uint2(val[j], nbv[j]);
-        a.einfo2[val[j]] = make_uint2(b0 + pos, b0 + segst[l + 1]);
+        // by the arc's partition position: this bucket's own range, so the writes fill whole sectors in L2
+        const uint32_t i = warp * 32u * R + j * 32u + lane;
+        a.pslot[src.g[i].w] = make_uint2(b0 + pos, b0 + segst[l + 1]);
     }
     // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole; the hub (if
     // any) is entry D
@@ -1180,7 +1186,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
             if (isH) {
                 const uint32_t pos = ph + __popc(bh & lt);
                 a.segS[base + pos] = make_uint2(x.y, x.z);
-                a.einfo2[x.y] = make_uint2(base + pos, base + H);
+                a.pslot[x.w] = make_uint2(base + pos, base + H);
             } else if (valid) {
                 rest[pr + __popc(br & lt)] = x;
             }
@@ -1204,7 +1210,8 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
 
 struct UpdateIdx {
     Lookup L;
-    const uint4 *einfo;
+    const uint2 *apos;   // [w] partition positions of edge k's two arcs
+    const uint2 *pslot;  // [2 w] by partition position: {slot in segS, segment end}
     const uint2 *segS;
     uint32_t *ctr;
 };
@@ -1277,14 +1284,17 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
         }
     }
     // ---- Step 2a: chi^+ = rank(u->v) + rank(v->u) ----
-    // fresh f1 = w_j: its ranks from einfo[j]; retained f1: rank(u->v) = deg_W(u) (footnote PAPER.md:818-821)
+    // fresh f1 = w_j: its ranks from its arcs' pslot entries (apos[j]); retained f1: rank(u->v) = deg_W(u) (footnote
+    // PAPER.md:818-821)
     uint2 r1 = old.r1;
     uint4 inf = make_uint4(0u, 0u, 0u, 0u);
     uint2 su = make_uint2(0u, 0u), sv = make_uint2(0u, 0u);
     const uint32_t hu = hash_vertex(r1.x), hv = hash_vertex(r1.y);
     if (fresh) {
         r1 = __ldg(ix.L.E + j);
-        inf = __ldg(ix.einfo + j);
+        const uint2 ap = __ldg(ix.apos + j);
+        const uint2 pu = __ldg(ix.pslot + ap.x), pv = __ldg(ix.pslot + ap.y);
+        inf = make_uint4(pu.x, pu.y, pv.x, pv.y);
     } else {
         su = __ldg(ix.L.vslice + vbucket_of(hu, ix.L.bv));
         sv = __ldg(ix.L.vslice + vbucket_of(hv, ix.L.bv));
@@ -1495,7 +1505,7 @@ __global__ void __launch_bounds__(256) k_u1_resample(UpdateArgs u, const uint2 *
     }
 }
 
-// Ku2 -- Step 2a, chi^+ = rank(u->v) + rank(v->u): a fresh f1's ranks from einfo, a retained
+// Ku2 -- Step 2a, chi^+ = rank(u->v) + rank(v->u): a fresh f1's ranks from pslot (via apos), a retained
 // f1's from the vertex table (deg_W, footnote PAPER.md:818-821).
 __global__ void __launch_bounds__(256) k_u2_count(UpdateArgs u, UpdateIdx ix, StepBufs sb) {
     with_desc(u, ix.L);
@@ -1505,7 +1515,9 @@ __global__ void __launch_bounds__(256) k_u2_count(UpdateArgs u, UpdateIdx ix, St
         const uint32_t j = sb.j[t];
         uint32_t ld, rd, endU, endV;
         if (j != kEmptyV) {
-            const uint4 inf = ix.einfo[j];
+            const uint2 ap = ix.apos[j];
+            const uint2 pu = ix.pslot[ap.x], pv = ix.pslot[ap.y];
+            const uint4 inf = make_uint4(pu.x, pu.y, pv.x, pv.y);
             ld = inf.y - 1u - inf.x;
             rd = inf.w - 1u - inf.z;
             endU = inf.y;
@@ -1716,7 +1728,7 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{ix.desc, a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), ix.ctr,
+    return PartArgs{ix.desc, reinterpret_cast<uint32_t *>(ix.apos), a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), ix.ctr,
                     a.small ? ix.filt : nullptr, a.S};
 }
 
@@ -1763,7 +1775,7 @@ int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const 
 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
     return VertArgs{a.g.bs ? ix.arcs2 : ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E,
-                    a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, reinterpret_cast<uint2 *>(ix.einfo), ix.vt, ix.vslice,
+                    a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, ix.pslot, reinterpret_cast<const uint32_t *>(ix.apos), ix.vt, ix.vslice,
                     ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 
@@ -1786,7 +1798,7 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.einfo, ix.segS, ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);
@@ -1801,7 +1813,7 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.einfo, ix.segS, ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, 8);
     kr.beg(K_U1, s);

@@ -18,7 +18,8 @@ struct IndexBufs {
     uint32_t *vstart2 = nullptr;   // [2^15 + 1] sub-bucket starts
     uint2 *scratch = nullptr;      // [2 wcap] sort scratch of oversized vertex buckets
     uint2 *segS = nullptr;         // [2 wcap] arcs {k<<1|side, neighbour} grouped by vertex
-    uint4 *einfo = nullptr;        // [wcap] {slot_lo, end_lo, slot_hi, end_hi}
+    uint2 *apos = nullptr;         // [wcap] partition positions of edge k's arcs {lo side, hi side} (k_scatter)
+    uint2 *pslot = nullptr;        // [2 wcap] by partition position: {slot in segS, segment end} (vertex kernels)
     VSlot *vt = nullptr;           // [4 wcap] vertex-table slices (bucket b at 2 * start_b)
     uint2 *vslice = nullptr;       // [4096] {offset, size}
     uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
