@@ -531,6 +531,17 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
     auto rec = [&](int e, cudaStream_t st) {
         if (ctx->prof) ok = ok && cudaEventRecord(ctx->ev_pool[ctx->ev_used][e], st) == cudaSuccess;
     };
+    if (a.g.small_index) {  // small batch: the whole index by one CTA, then the estimator pass
+        rec(2 * TC_PHASE_PARTITION, ms);
+        launches += launch_small_index(ix, a, ms, kr);
+        rec(2 * TC_PHASE_PARTITION + 1, ms);
+        rec(2 * TC_PHASE_UPDATE, ms);
+        if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
+        else launches += launch_update(ix, ctx->st, a, ms, kr);
+        rec(2 * TC_PHASE_UPDATE + 1, ms);
+        *ok_out = ok;
+        return launches;
+    }
     // a1: count, scans, scatter (k_count zeroes the counters and this batch's S)
     rec(2 * TC_PHASE_PARTITION, ms);
     launches += launch_partition(ix, a, ms, kr);
@@ -562,7 +573,8 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
 
 // The graph of a batch shape: found in the cache, or captured (k_desc + the kernels) and instantiated.
 static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx::GraphEntry **out) {
-    const uint64_t key = (uint64_t)a.g.w | ((uint64_t)a.small << 32) | ((uint64_t)ctx->tune.split << 33);
+    const uint64_t key = (uint64_t)a.g.w | ((uint64_t)a.small << 32) | ((uint64_t)ctx->tune.split << 33) |
+                         ((uint64_t)a.g.small_index << 34);
     for (auto &g : ctx->graphs)
         if (g.key == key) {
             g.last_use = ++ctx->graph_clock;
@@ -786,6 +798,10 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
             case TC_TUNE_VBUCKET_SORT_CAP:
                 if (value < 1 || value > kVChunk) return TC_EINVAL;
                 c->tune.sortcap = (uint32_t)value;
+                return TC_OK;
+            case TC_TUNE_SMALL_INDEX:
+                if (value > 2) return TC_EINVAL;
+                c->tune.small_index = (uint32_t)value;
                 return TC_OK;
             case TC_TUNE_SPLIT_KERNELS:
                 if (value > 1) return TC_EINVAL;
@@ -1177,7 +1193,8 @@ int tc_profile_kernels(tc_ctx *ctx, double *ms, uint64_t *launches, int n) {
 const char *tc_kernel_name(int k) {
     static const char *names[K_NKERNELS] = {"k_count", "k_scan_cols", "k_scan_tot", "k_scatter", "k_split",
                                             "k_pairs", "k_vhub", "k_vbig", "k_vhash", "k_update",
-                                            "k_u1_resample", "k_u2_count", "k_u3_select", "k_u4_close", "k_r_reduce"};
+                                            "k_u1_resample", "k_u2_count", "k_u3_select", "k_u4_close", "k_r_reduce",
+                                            "k_small_index"};
     return (k >= 0 && k < K_NKERNELS) ? names[k] : "";
 }
 

@@ -362,7 +362,9 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
     for (uint32_t ai = threadIdx.x; ai < 2 * ne; ai += kTileThreads) {
         const uint2 n = sE[ai >> 1];
         const uint32_t d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bp1);
-        idx[toff[d] + a.arank[2 * e0 + ai]] = (uint16_t)ai;
+        const uint32_t rk = a.arank[2 * e0 + ai];
+        idx[toff[d] + rk] = (uint16_t)ai;
+        a.apos2[2u * e0 + ai] = soff[d] + rk;  // the arc's partition position, written in arc order (coalesced)
     }
     __syncthreads();
     // consecutive threads write consecutive positions of the tile's bucket order: a bucket's run coalesces
@@ -373,7 +375,6 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
         const uint32_t d = vbucket_of(hash_vertex(v), a.g.bp1);
         const uint32_t P = soff[d] + (pos - toff[d]);  // the arc's partition position (kept through k_split in .w)
         __stcs(a.arcs + P, make_uint4(v, 2u * e0 + ai, nb, P));
-        a.apos2[2u * e0 + ai] = P;  // per arc, by arc id: the tile's own contiguous range (sectors fill in L2)
     }
 }
 
@@ -1206,6 +1207,60 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------------
+// a1..a3 for small batches (w <= kSmallIndexMax): ONE CTA builds the whole index -- validation, E, the arcs,
+// the edge-pair table (and the small-batch vertex filter), then all 2w arcs as a single vertex bucket through
+// the hash path -- instead of the eight launches of the partitioned build, whose fixed latency dominates small
+// batches.  Same tables, same lookups (the vertex table is one slice: bucket bits bv = 0).
+__global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, VertArgs v) {
+    extern __shared__ __align__(16) unsigned char hsm[];
+    __shared__ uint32_t ws[kHubWarps + 1];
+    __shared__ uint32_t sD;
+    if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
+        a.ctr[threadIdx.x] = 0u;
+    if (threadIdx.x == 0) a.S[a.d->slot] = 0ull;
+    if (a.filt)
+        for (uint32_t i = threadIdx.x; i < kFilterWords; i += blockDim.x) a.filt[i] = 0u;
+    const bool sticky = (a.ctr[kCtrErr] & kErrStage) != 0;  // an earlier asynchronous batch failed
+    __syncthreads();
+    if (sticky) return;
+    const uint2 *in = a.d->in;
+    const uint32_t ptag = a.d->ptag, w = a.g.w;
+    // validation and normalisation first: a rejected batch must not insert anything
+    uint32_t bad = 0;
+    for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
+        const uint2 e = __ldg(in + k);
+        if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
+        else if (e.x == e.y) bad |= kErrLoop;
+    }
+    bad = __reduce_or_sync(kFull, bad);
+    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], bad);
+    if (__syncthreads_or(bad != 0)) return;
+    bool dup = false;
+    for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
+        const uint2 n = norm_edge(__ldg(in + k));
+        a.E[k] = n;
+        // one bucket: an arc's partition position is its arc id
+        v.arcs[2 * k] = make_uint4(n.x, 2 * k, n.y, 2 * k);
+        v.arcs[2 * k + 1] = make_uint4(n.y, 2 * k + 1, n.x, 2 * k + 1);
+        a.apos2[2 * k] = 2 * k;
+        a.apos2[2 * k + 1] = 2 * k + 1;
+        dup |= pt_insert(a, in, ptag, n, k);
+        if (a.filt) {
+            const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
+            atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
+            atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
+        }
+    }
+    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+    __syncthreads();  // the arcs this CTA wrote are visible to all its threads
+    const uint32_t n = 2 * w;
+    const ArcSrc src{v.arcs, nullptr, nullptr, nullptr};
+    hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
+        vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(v, 0u, 0u, src, n, 0u, 0u, 0u, hsm, ws, &sD);
+    });
+}
+
+// ------------------------------------------------------------------------------------------------
 // a4..a8: the fused estimator update, one thread per estimator.
 
 struct UpdateIdx {
@@ -1718,12 +1773,14 @@ static inline uint32_t ceil_log2(uint64_t x) {
 Geometry make_geometry(uint32_t w, const Tuning &t) {
     Geometry g;
     g.w = w;
+    g.small_index = t.small_index == 2 ? (w <= kSmallIndexMax) : t.small_index == 1 ? false : (w <= kSmallIndexMax);
     g.tiles = (w + kTileEdges - 1) / kTileEdges;
     g.bv = std::min(kMaxBucketBits, ceil_log2((2ull * w + t.vbucket_arcs - 1) / t.vbucket_arcs));
     g.bp1 = std::min(g.bv, kMaxPartBits);
     g.bs = g.bv - g.bp1;
     g.vcap = std::min(t.vcap, kHCapSmall);
     g.sortcap = std::min(t.sortcap, kVChunk);
+    if (g.small_index) g.bv = g.bp1 = g.bs = 0;  // the whole batch is one vertex bucket
     return g;
 }
 
@@ -1777,6 +1834,13 @@ static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
     return VertArgs{a.g.bs ? ix.arcs2 : ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E,
                     a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, ix.pslot, reinterpret_cast<const uint32_t *>(ix.apos), ix.vt, ix.vslice,
                     ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
+}
+
+int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
+    kr.beg(K_SMALL, s);
+    k_small_index<<<1, kHubThreads, kVHubSmemBytes, s>>>(part_args(ix, a), vert_args(ix, a));
+    kr.end(K_SMALL, s);
+    return 1;
 }
 
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
@@ -1851,6 +1915,8 @@ int set_kernel_attributes() {
     cudaError_t e1 = cudaFuncSetAttribute(k_vbig, cudaFuncAttributeMaxDynamicSharedMemorySize, kVSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
+    if (e1 == cudaSuccess)
+        e1 = cudaFuncSetAttribute(k_small_index, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
     cudaError_t e2 = cudaSuccess;
     const void *counts[] = {(const void *)k_count<0>, (const void *)k_count<1>, (const void *)k_count<2>,
                             (const void *)k_count<3>, (const void *)k_count<4>, (const void *)k_count<5>,

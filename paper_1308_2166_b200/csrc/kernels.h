@@ -72,7 +72,10 @@ struct Geometry {
     uint32_t bs;       // split bits (k_split: each partition bucket into 2^bs sub-buckets; 0 = no split)
     uint32_t vcap;     // vertex buckets larger than this go to k_vhub (<= 2048)
     uint32_t sortcap;  // k_vbig: buckets larger than this take the chunked global-memory path (<= kVChunk)
+    bool small_index;  // the whole index by one CTA (k_small_index; w <= kSmallIndexMax)
 };
+
+constexpr uint32_t kSmallIndexMax = 4096;  // 2 w arcs must fit the one-CTA hash path (8192)
 
 // Launch-time values of a push.  The per-batch values (input pointer, m, batch index, pair tag, S slot) are
 // NOT here: the kernels read them from the device descriptor (BatchDesc), so a captured graph of the launch
@@ -94,13 +97,14 @@ struct Tuning {
     uint32_t vcap = 2048;
     uint32_t sortcap = kVChunk;
     uint32_t split = 0;            // 1: the estimator pass as the split per-step kernels
+    uint32_t small_index = 0;      // 0 auto (w <= kSmallIndexMax), 1 never, 2 always when w <= kSmallIndexMax
 };
 
 Geometry make_geometry(uint32_t w, const Tuning &t);
 
 // Per-kernel profiling (tc_profile_kernels): ids match include/tc.h TC_KERNEL_*.
 enum KernelId { K_COUNT = 0, K_SCAN_COLS, K_SCAN_TOT, K_SCATTER, K_SPLIT, K_PAIRS, K_VHUB, K_VBIG, K_VHASH, K_UPDATE,
-                K_U1, K_U2, K_U3, K_U4, K_R, K_NKERNELS };
+                K_U1, K_U2, K_U3, K_U4, K_R, K_SMALL, K_NKERNELS };
 struct KRec {
     cudaEvent_t *ev = nullptr;  // 2 K_NKERNELS events (begin, end) or null: no profiling
     uint32_t *used = nullptr;   // bit k set once kernel k's events were recorded in this push
@@ -119,6 +123,7 @@ struct KRec {
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());      // a3
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());   // a2
+int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1-a3
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a2 > vcap
 #ifndef TC_BIG_CTAS
 #define TC_BIG_CTAS 64

@@ -107,20 +107,23 @@ def test_hub_segments_multi_chunk():
     dict(vbucket_arcs=1 << 30),                    # one vertex bucket
     dict(small_batch=1),                           # the full estimator pass even for small batches
     dict(small_batch=2),                           # the filtered small-batch pass even for large batches
+    dict(small_index=1, small_batch=1),            # small batches through the partitioned build
+    dict(small_index=2, split_kernels=1),          # one-CTA index + split estimator pass
 ])
 def test_index_geometry_knobs(knobs):
-    """Results never depend on the index geometry (tc_tune): bit-exact against the oracle."""
+    """Results never depend on the index geometry (tc_tune): bit-exact against the oracle.  Batches of at most
+    4096 edges take the one-CTA index unless small_index=1, so the geometry knobs are also run with it off."""
     from paper_1308_2166_b200 import TriangleCounter
     s = _hub_stream()
-    for w in (len(s), 2500, 1):
+    for w, extra in ((len(s), {}), (2500, {}), (2500, {"small_index": 1}), (1, {}), (1, {"small_index": 1})):
         ww = w if w > 1 else 1
         tc = TriangleCounter(1500, 5 + w)
-        tc.tune(**knobs)
+        tc.tune(**{**knobs, **extra})
         n = len(s) if w > 1 else 300
         for k in range(0, n, ww):
             tc.push_batch(s[k:min(n, k + ww)])
         o = oracle_run(s[:n], 1500, 5 + w, ww)
-        assert_states_equal(tc.state(), o.state(), f"{knobs} w={w}")
+        assert_states_equal(tc.state(), o.state(), f"{knobs} {extra} w={w}")
 
 
 def test_device_pinned_pageable_inputs_agree():
@@ -439,6 +442,8 @@ def test_fuzz_configurations(case):
         knobs["vbucket_arcs"] = int(rng.choice([1, 16, 256, 4096]))
     if rng.random() < 0.3:
         knobs["vbucket_cap"] = int(rng.choice([1, 64, 2048]))
+    if rng.random() < 0.3:
+        knobs["small_index"] = int(rng.integers(0, 3))
     if knobs:
         tc.tune(**knobs)
     tc.set_graphs(bool(rng.random() < 0.5))
