@@ -13,9 +13,9 @@
 //                          memory, written as coalesced runs), so each bucket holds its arcs in arrival order
 //                          -- the F array of rankAll's proof, partitioned
 //   k_split      a1      : (w > 2^21 only) each bucket stably split again by the next hash bits
-//   k_pairs      a3      : (second stream, alongside the vertex phase) every edge of the raw batch into the
-//                          edge-pair table (64-bit CAS; a repeat is TC_EDUP); small batches also fill the
-//                          vertex filter
+//   (a3)                   the edge-pair table is built by the vertex kernels below, one region per vertex
+//                          bucket (build_pair_region: the pairs whose lo endpoint is in the bucket; a repeat is
+//                          TC_EDUP); small batches also fill the vertex filter there
 //   k_vhash      a2      : one CTA per vertex bucket: bucket-local vertex ids from a shared-memory hash
 //                          table, one stable ranking pass by local id (replaces rankAll's sort by (src, -pos),
 //                          PAPER.md:680-684), segment starts -> segS, per-arc {slot, segEnd} (rank = segEnd -
@@ -108,7 +108,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *s
 // a1: bucket histograms
 
 struct PartArgs {
-    const BatchDesc *d;  // in, ptag, slot (per batch)
+    const BatchDesc *d;  // in, slot (per batch)
     uint32_t *apos2;     // [2 w] partition position of every arc (by arc id k<<1|side)
     Geometry g;
     uint2 *E;
@@ -117,64 +117,10 @@ struct PartArgs {
     uint32_t *offV;    // [tiles][nV] the tile's offset inside the bucket
     uint16_t *arank;   // [2 w] in-tile ranks
     uint32_t *vstart;  // bucket sizes (k_scan_cols) -> exclusive prefixes (k_scan_tot)
-    uint2 *pt;         // edge-pair table (G groups of 4 slots)
-    uint32_t G;
     uint32_t *ctr;
-    uint32_t *filt;    // small batches: the vertex filter to fill (else null)
+    uint32_t *filt;    // small batches: the vertex filter (k_small_index zeroes it)
     unsigned long long *S;  // the two S accumulators: k_count zeroes this batch's (d->slot) and the counters
 };
-
-// a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
-// with room along its probe sequence (A, B, A+1, ...), by 64-bit CAS, so the live slots of a group form a
-// prefix.  Meeting the
-// same pair (confirmed against the raw batch, which is stable while E is being written) returns true.
-__device__ __forceinline__ bool pt_insert(const PartArgs &a, const uint2 *in, uint32_t ptag, uint2 n, uint32_t k) {
-    const uint64_t h = hash_pair64(pair_key(n.x, n.y));
-    const uint32_t tf = (ptag << 24) | pfinger(h);
-    const unsigned long long mine = (unsigned long long)k | ((unsigned long long)tf << 32);
-    unsigned long long *t64 = reinterpret_cast<unsigned long long *>(a.pt);
-    const uint32_t A = pgroup_start(h, a.G), B = pgroup_second(h, a.G, A);
-    for (uint32_t step = 0;; ++step) {
-        const uint32_t g = pgroup_at(A, B, step, a.G);
-        const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
-        const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
-        const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
-#pragma unroll
-        for (uint32_t i = 0; i < 4; ++i) {
-            unsigned long long cur = cur4[i];
-            if ((uint32_t)(cur >> 56) != ptag) {
-                const unsigned long long old = atomicCAS(t64 + 4ull * g + i, cur, mine);
-                if (old == cur) return false;
-                cur = old;  // taken meanwhile (by this batch)
-            }
-            if ((uint32_t)(cur >> 32) == tf) {
-                const uint2 o = norm_edge(__ldg(in + (uint32_t)cur));
-                if (o.x == n.x && o.y == n.y) return true;
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(256) k_pairs(PartArgs a) {
-    if (a.ctr[kCtrErr] & (kErrStage | kErrDup)) return;  // sticky error of an earlier async batch
-    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint2 *in = a.d->in;
-    const uint32_t ptag = a.d->ptag;
-    bool dup = false;
-    if (k < a.g.w) {
-        const uint2 e = __ldg(in + k);
-        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // k_count reports the rest
-            const uint2 n = norm_edge(e);
-            dup = pt_insert(a, in, ptag, n, k);
-            if (a.filt) {
-                const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
-                atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
-                atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
-            }
-        }
-    }
-    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
-}
 
 // Tile ranking: validate and normalise W, write E, and rank every arc (by vertex bucket) and every edge (by
 // pair bucket) inside its tile, stably in arrival order.  Arc a of the tile (a = 2 e + side) is owned by
@@ -486,7 +432,69 @@ struct VertArgs {
     uint32_t vcap;      // buckets with more arcs go to k_vbig
     uint32_t sortcap;   // k_vbig: buckets with more arcs take the chunked global-memory path
     uint32_t *ctr;
+    uint2 *pt;          // edge-pair table: one region per vertex bucket (build_pair_region)
+    uint32_t *filt;     // small batches: the vertex filter (bits of every arc's vertex), else null
 };
+
+// a3 inside the vertex phase: the edge-pair-table region of vertex bucket b (its arcs [st, en) of a.arcs) --
+// every pair {lo, hi} whose lo endpoint lies in the bucket (its side-0 arc), with its batch position k -- built
+// in shared memory (sm, cap slots) when it fits and then written out whole and coalesced, else in place in
+// global memory (the region is this CTA's alone).  A pair met twice is TC_EDUP (confirmed against E).  Small
+// batches also get the vertex-filter bit of every arc.  Called by the whole CTA; sm may alias dead scratch.
+template <int NT>
+__device__ __noinline__ void build_pair_region(const VertArgs &a, uint32_t b, uint32_t st, uint32_t en,
+                                               unsigned long long *sm, uint32_t cap) {
+    const uint32_t g0 = pr_first(st, b), G = pr_first(en, b + 1) - g0, S = 4 * G;
+    const bool in_sm = sm != nullptr && S <= cap;
+    unsigned long long *tab = in_sm ? sm : reinterpret_cast<unsigned long long *>(a.pt) + 4ull * g0;
+    constexpr unsigned long long kFreeSlot = 0x00000000FFFFFFFFull;  // k = kPairFree
+    for (uint32_t s = threadIdx.x; s < S; s += NT) tab[s] = kFreeSlot;
+    __syncthreads();
+    bool dup = false;
+    for (uint32_t i = st + threadIdx.x; i < en; i += NT) {
+        const uint4 x = a.arcs[i];
+        if (a.filt) {
+            const uint32_t bit = vfilter_bit(hash_vertex(x.x));
+            atomicOr(a.filt + (bit >> 5), 1u << (bit & 31u));
+        }
+        if (x.y & 1u) continue;  // the hi-side arc: its pair belongs to the lo endpoint's bucket
+        const uint64_t h = hash_pair64(pair_key(x.x, x.z));
+        const uint32_t fp = (uint32_t)h;
+        const unsigned long long mine = (unsigned long long)(x.y >> 1) | ((unsigned long long)fp << 32);
+        const uint32_t A = pgroup_start(h, G), B = pgroup_second(h, G, A);
+        bool done = false;
+        for (uint32_t step = 0; !done; ++step) {
+            volatile unsigned long long *grp = tab + 4ull * pgroup_at(A, B, step, G);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (done) break;
+                unsigned long long cur = grp[q];
+                if ((uint32_t)cur == kPairFree) {
+                    const unsigned long long old =
+                        atomicCAS(const_cast<unsigned long long *>(grp + q), kFreeSlot, mine);
+                    if (old == kFreeSlot) {
+                        done = true;
+                        break;
+                    }
+                    cur = old;  // taken meanwhile
+                }
+                if ((uint32_t)(cur >> 32) == fp) {
+                    const uint2 o = a.E[(uint32_t)cur];
+                    if (o.x == x.x && o.y == x.z) {
+                        dup = true;
+                        done = true;
+                    }
+                }
+            }
+        }
+    }
+    if (__syncthreads_or(dup) && threadIdx.x == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+    if (in_sm) {
+        uint4 *dst = reinterpret_cast<uint4 *>(a.pt + 4ull * g0);
+        const uint4 *src = reinterpret_cast<const uint4 *>(sm);
+        for (uint32_t s = threadIdx.x; s < S / 2; s += NT) dst[s] = src[s];
+    }
+}
 
 constexpr uint32_t kVWarps = kVBucketThreads / 32;
 constexpr uint32_t kVAux = kVChunk > kVWarps * 256 + 256 ? kVChunk : kVWarps * 256 + 256;
@@ -839,6 +847,9 @@ __global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
         const uint32_t b = s_b;
         __syncthreads();
         if (b == 0xFFFFFFFFu) return;
+        // the pair region first, in place in global memory: the chunked sort reuses the bucket's arc memory
+        build_pair_region<kVBucketThreads>(a, b, a.vstart[b], a.vstart[b + 1], nullptr, 0u);
+        __syncthreads();
         vbucket_sort(a, b, vsm, dtot, ws);
         __syncthreads();
     }
@@ -1064,6 +1075,8 @@ __global__ void __launch_bounds__(kHThreads, 4) k_vhash(VertArgs a) {
     hash_dispatch<kHCapSmall, kHThreads>(n, [&](auto r) {
         vbucket_hash<decltype(r)::value, kHCapSmall, kHThreads>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
     });
+    __syncthreads();  // the hash path's shared memory is dead: the bucket's pair region is built there
+    build_pair_region<kHThreads>(a, b, base, base + n, reinterpret_cast<unsigned long long *>(hsm), kVHashSmemBytes / 8);
 }
 
 // Large buckets (more than vcap arcs; at batch sizes of 2^22 and beyond, most buckets): 512-thread CTAs with
@@ -1104,6 +1117,9 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
             hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
                 vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
             });
+            __syncthreads();
+            build_pair_region<kHubThreads>(a, b, base, base + n, reinterpret_cast<unsigned long long *>(hsm),
+                                           kVHubSmemBytes / 8);
             __syncthreads();
             continue;
         }
@@ -1203,6 +1219,9 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
             vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD);
         });
         __syncthreads();
+        build_pair_region<kHubThreads>(a, b, base, base + n, reinterpret_cast<unsigned long long *>(hsm),
+                                       kVHubSmemBytes / 8);
+        __syncthreads();
     }
 }
 
@@ -1224,7 +1243,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
     __syncthreads();
     if (sticky) return;
     const uint2 *in = a.d->in;
-    const uint32_t ptag = a.d->ptag, w = a.g.w;
+    const uint32_t w = a.g.w;
     // validation and normalisation first: a rejected batch must not insert anything
     uint32_t bad = 0;
     for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
@@ -1235,7 +1254,6 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
     bad = __reduce_or_sync(kFull, bad);
     if (bad && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], bad);
     if (__syncthreads_or(bad != 0)) return;
-    bool dup = false;
     for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
         const uint2 n = norm_edge(__ldg(in + k));
         a.E[k] = n;
@@ -1244,20 +1262,19 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
         v.arcs[2 * k + 1] = make_uint4(n.y, 2 * k + 1, n.x, 2 * k + 1);
         a.apos2[2 * k] = 2 * k;
         a.apos2[2 * k + 1] = 2 * k + 1;
-        dup |= pt_insert(a, in, ptag, n, k);
-        if (a.filt) {
-            const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
-            atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
-            atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
-        }
     }
-    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+    if (threadIdx.x == 0) {  // the one bucket's arc range (the pair region and the lookups derive from it)
+        a.vstart[0] = 0u;
+        a.vstart[1] = 2 * w;
+    }
     __syncthreads();  // the arcs this CTA wrote are visible to all its threads
     const uint32_t n = 2 * w;
     const ArcSrc src{v.arcs, nullptr, nullptr, nullptr};
     hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
         vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(v, 0u, 0u, src, n, 0u, 0u, 0u, hsm, ws, &sD);
     });
+    __syncthreads();  // the hash path's shared memory is dead: the pair region is built there
+    build_pair_region<kHubThreads>(v, 0u, 0u, n, reinterpret_cast<unsigned long long *>(hsm), kVHubSmemBytes / 8);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1289,7 +1306,6 @@ struct UpdateArgs {
 __device__ __forceinline__ void with_desc(UpdateArgs &u, Lookup &L) {
     u.batch = u.d->batch;
     u.m_prev = u.d->m_prev;
-    L.ptag = u.d->ptag;
 }
 
 template <bool kSmall>
@@ -1785,14 +1801,15 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{ix.desc, reinterpret_cast<uint32_t *>(ix.apos), a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), ix.ctr,
-                    a.small ? ix.filt : nullptr, a.S};
+    return PartArgs{ix.desc, reinterpret_cast<uint32_t *>(ix.apos), a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart,
+                    ix.ctr, a.small ? ix.filt : nullptr, a.S};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     const Geometry &g = a.g;
     const uint32_t nV = 1u << g.bp1;
     const PartArgs p = part_args(ix, a);
+    if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
     kr.beg(K_COUNT, s);
     switch (g.bp1) {
 #define TC_COUNT_CASE(B) \
@@ -1822,18 +1839,12 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, co
     return 5;
 }
 
-int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
-    if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
-    kr.beg(K_PAIRS, s);
-    k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
-    kr.end(K_PAIRS, s);
-    return 1;
-}
+
 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
     return VertArgs{a.g.bs ? ix.arcs2 : ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E,
                     a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, ix.pslot, reinterpret_cast<const uint32_t *>(ix.apos), ix.vt, ix.vslice,
-                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
+                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr, ix.pt, a.small ? ix.filt : nullptr};
 }
 
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
@@ -1862,7 +1873,8 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, a.g.bs ? ix.vstart2 : ix.vstart}, ix.apos, ix.pslot, ix.segS,
+                 ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);
@@ -1877,7 +1889,8 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, a.g.bs ? ix.vstart2 : ix.vstart}, ix.apos, ix.pslot, ix.segS,
+                 ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, 8);
     kr.beg(K_U1, s);

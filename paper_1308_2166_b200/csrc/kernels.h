@@ -24,7 +24,7 @@ struct IndexBufs {
     uint2 *vslice = nullptr;       // [4096] {offset, size}
     uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
     uint32_t *vdefer = nullptr;    // [4096] large buckets k_vhub hands to k_vbig
-    uint2 *pt = nullptr;           // [4 ceil(wcap / 2)] pair slots {k, fp}, groups of 4
+    uint2 *pt = nullptr;           // pair slots {k, fp32}, groups of 4, one region per vertex bucket
     uint32_t *cntV = nullptr;      // [4096 * tiles] per-(bucket, tile) arc counts
     uint32_t *offV = nullptr;      // [4096 * tiles] the tile's offset inside the bucket
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
@@ -75,7 +75,8 @@ struct Geometry {
     bool small_index;  // the whole index by one CTA (k_small_index; w <= kSmallIndexMax)
 };
 
-constexpr uint32_t kSmallIndexMax = 4096;  // 2 w arcs must fit the one-CTA hash path (8192)
+constexpr uint32_t kSmallIndexMax = 2048;  // one CTA: measured faster than the partitioned build up to 2048 edges
+                                           // (C1: 39 us vs ~55), slower at 4096 (100 us vs ~65); hash path cap 8192
 
 // Launch-time values of a push.  The per-batch values (input pointer, m, batch index, pair tag, S slot) are
 // NOT here: the kernels read them from the device descriptor (BatchDesc), so a captured graph of the launch
@@ -84,7 +85,8 @@ struct BatchArgs {
     uint64_t first;   // global id of local estimator 0
     uint64_t seed;
     unsigned long long *S;  // the two S accumulators (slot from the descriptor)
-    bool small;       // small-batch estimator pass (filters built by k_pairs, k_update skips untouched estimators)
+    bool small;       // small-batch estimator pass (vertex filter built by the vertex kernels, k_update skips
+                      // untouched estimators)
     Geometry g;
 };
 
@@ -121,7 +123,6 @@ struct KRec {
 
 // Each returns the number of kernel launches issued.
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1
-int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());      // a3
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());   // a2
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1-a3
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a2 > vcap
