@@ -436,6 +436,35 @@ struct VertArgs {
     uint32_t *filt;     // small batches: the vertex filter (bits of every arc's vertex), else null
 };
 
+constexpr unsigned long long kFreeSlot = 0x00000000FFFFFFFFull;  // a free pair slot: k = kPairFree
+
+// Insert {lo, hi} -> k into a region of G groups (shared or global memory): the first free slot along its probe
+// sequence A, B, A+1, ..., by 64-bit CAS, so a group's filled slots form a prefix.  Returns true if the pair
+// is already there (a duplicate in the batch, confirmed against E).
+__device__ __forceinline__ bool pair_insert(unsigned long long *tab, uint32_t G, uint32_t lo, uint32_t hi, uint32_t k,
+                                            const uint2 *E) {
+    const uint64_t h = hash_pair64(pair_key(lo, hi));
+    const uint32_t fp = (uint32_t)h;
+    const unsigned long long mine = (unsigned long long)k | ((unsigned long long)fp << 32);
+    const uint32_t A = pgroup_start(h, G), B = pgroup_second(h, G, A);
+    for (uint32_t step = 0;; ++step) {
+        volatile unsigned long long *grp = tab + 4ull * pgroup_at(A, B, step, G);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            unsigned long long cur = grp[q];
+            if ((uint32_t)cur == kPairFree) {
+                const unsigned long long old = atomicCAS(const_cast<unsigned long long *>(grp + q), kFreeSlot, mine);
+                if (old == kFreeSlot) return false;
+                cur = old;  // taken meanwhile
+            }
+            if ((uint32_t)(cur >> 32) == fp) {
+                const uint2 o = E[(uint32_t)cur];
+                if (o.x == lo && o.y == hi) return true;
+            }
+        }
+    }
+}
+
 // a3 inside the vertex phase: the edge-pair-table region of vertex bucket b (its arcs [st, en) of a.arcs) --
 // every pair {lo, hi} whose lo endpoint lies in the bucket (its side-0 arc), with its batch position k -- built
 // in shared memory (sm, cap slots) when it fits and then written out whole and coalesced, else in place in
@@ -447,7 +476,6 @@ __device__ __noinline__ void build_pair_region(const VertArgs &a, uint32_t b, ui
     const uint32_t g0 = pr_first(st, b), G = pr_first(en, b + 1) - g0, S = 4 * G;
     const bool in_sm = sm != nullptr && S <= cap;
     unsigned long long *tab = in_sm ? sm : reinterpret_cast<unsigned long long *>(a.pt) + 4ull * g0;
-    constexpr unsigned long long kFreeSlot = 0x00000000FFFFFFFFull;  // k = kPairFree
     for (uint32_t s = threadIdx.x; s < S; s += NT) tab[s] = kFreeSlot;
     __syncthreads();
     bool dup = false;
@@ -458,35 +486,7 @@ __device__ __noinline__ void build_pair_region(const VertArgs &a, uint32_t b, ui
             atomicOr(a.filt + (bit >> 5), 1u << (bit & 31u));
         }
         if (x.y & 1u) continue;  // the hi-side arc: its pair belongs to the lo endpoint's bucket
-        const uint64_t h = hash_pair64(pair_key(x.x, x.z));
-        const uint32_t fp = (uint32_t)h;
-        const unsigned long long mine = (unsigned long long)(x.y >> 1) | ((unsigned long long)fp << 32);
-        const uint32_t A = pgroup_start(h, G), B = pgroup_second(h, G, A);
-        bool done = false;
-        for (uint32_t step = 0; !done; ++step) {
-            volatile unsigned long long *grp = tab + 4ull * pgroup_at(A, B, step, G);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (done) break;
-                unsigned long long cur = grp[q];
-                if ((uint32_t)cur == kPairFree) {
-                    const unsigned long long old =
-                        atomicCAS(const_cast<unsigned long long *>(grp + q), kFreeSlot, mine);
-                    if (old == kFreeSlot) {
-                        done = true;
-                        break;
-                    }
-                    cur = old;  // taken meanwhile
-                }
-                if ((uint32_t)(cur >> 32) == fp) {
-                    const uint2 o = a.E[(uint32_t)cur];
-                    if (o.x == x.x && o.y == x.z) {
-                        dup = true;
-                        done = true;
-                    }
-                }
-            }
-        }
+        dup |= pair_insert(tab, G, x.x, x.z, x.y >> 1, a.E);
     }
     if (__syncthreads_or(dup) && threadIdx.x == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
     if (in_sm) {
@@ -1047,6 +1047,33 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         else if (l == D) o = make_uint4(hub, hubn, base, 0u);
         reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
     }
+    // the 1024-thread callers (hub buckets, the one-CTA small index) build the pair region from global memory
+    // afterwards (build_pair_region): keeping R items live to here would spill their registers
+    if (hubn || NT != kHThreads) return;
+    // phase 6 (a3): the bucket's edge-pair region from the arcs still in registers (vertex = vkey[local id]), in
+    // the dead hash-path memory when it fits, then written out whole; the small-batch filter bits of its vertices
+    const uint32_t g0 = pr_first(base, b), G = pr_first(base + n, b + 1) - g0, SP = 4 * G;
+    if (a.filt)
+        for (uint32_t l = threadIdx.x; l < D; l += NT) {
+            const uint32_t bit = vfilter_bit(hash_vertex(vkey[l]));
+            atomicOr(a.filt + (bit >> 5), 1u << (bit & 31u));
+        }
+    const bool in_sm = SP * 8 <= L::R1;
+    unsigned long long *tab =
+        in_sm ? reinterpret_cast<unsigned long long *>(sm) : reinterpret_cast<unsigned long long *>(a.pt) + 4ull * g0;
+    __syncthreads();  // the slice loop above is done with the shared table
+    for (uint32_t s = threadIdx.x; s < SP; s += NT) tab[s] = kFreeSlot;
+    __syncthreads();
+    bool dup = false;
+#pragma unroll
+    for (int j = 0; j < R; ++j)
+        if (pk[j] != 0xFFFFFFFFu && !(val[j] & 1u)) dup |= pair_insert(tab, G, vkey[pk[j] >> 16], nbv[j], val[j] >> 1, a.E);
+    if (__syncthreads_or(dup) && threadIdx.x == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+    if (in_sm) {
+        uint4 *dst = reinterpret_cast<uint4 *>(a.pt + 4ull * g0);
+        const uint4 *src4 = reinterpret_cast<const uint4 *>(sm);
+        for (uint32_t s = threadIdx.x; s < SP / 2; s += NT) dst[s] = src4[s];
+    }
 }
 
 template <uint32_t CAP, int NT, typename F>
@@ -1075,8 +1102,6 @@ __global__ void __launch_bounds__(kHThreads, 4) k_vhash(VertArgs a) {
     hash_dispatch<kHCapSmall, kHThreads>(n, [&](auto r) {
         vbucket_hash<decltype(r)::value, kHCapSmall, kHThreads>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
     });
-    __syncthreads();  // the hash path's shared memory is dead: the bucket's pair region is built there
-    build_pair_region<kHThreads>(a, b, base, base + n, reinterpret_cast<unsigned long long *>(hsm), kVHashSmemBytes / 8);
 }
 
 // Large buckets (more than vcap arcs; at batch sizes of 2^22 and beyond, most buckets): 512-thread CTAs with

@@ -39,7 +39,7 @@ def test_b200_arm_json_line():
     r = d["roofline"]
     for k in ("bound", "achieved", "peak", "unit", "frac", "traffic", "kernel", "kernels", "whole_step"):
         assert k in r, k
-    assert 0 < r["frac"] < 1 and d["gpu_launches"] >= 6 * 9 and d["value"] > 0
+    assert 0 < r["frac"] < 1 and d["gpu_launches"] >= 6 * 3 and d["value"] > 0  # C1: desc + small index + update
     # the dominant kernel is the one with the largest measured time, and the shares add up
     ks = r["kernels"]
     assert r["kernel"] == max(ks, key=lambda k: ks[k]["ms_per_launch"] * ks[k]["launches"])
