@@ -174,8 +174,7 @@ def cpu_info():
 # Algorithmic bytes (SURVEY 8(d) byte model): what each kernel MUST move, per launch.
 #   Ke (staging): read the batch 8 B/edge, write E 8 B/edge  -> k_count; write 2 arcs x 8 B -> k_scatter
 #   Ki (index)  : 8 B per arc grouped + 16 B per distinct vertex (16w + 16D)  -> k_vhash, k_vhub (+k_vbig)
-#   Kp (pairs)  : read E 8 B/edge + one 16 B pair slot per edge (24w): built by the vertex kernels (one region
-#                 per vertex bucket, the pairs of its lo-side arcs) -> 12 B per arc they group
+#   Kp (pairs)  : read E 8 B/edge + one 16 B pair slot per edge (24w)        -> k_pairs
 #   Ku (update) : 24 B per estimator (read r1, c, r2 20 B, write c 4 B) + 16 B per replaced r1 (r1, p1)
 #                 + 16 B per replaced r2 (r2, p2): B_est = 24 + 16 (P_r1 + P_r2)
 #   k_scan_*, k_split: 0 (implementation overhead of the grouping; it shows up as a lower fraction)
@@ -186,12 +185,12 @@ def kernel_bytes(kernel, w, st, R):
         return 16 * w
     if kernel == "k_scatter":
         return 16 * w
+    if kernel == "k_pairs":
+        return 24 * w
     if kernel == "k_vhash":
-        return 20 * (arcs - st["arcs_big"]) + 16 * (st["vertices"] - st["vertices_big"])
+        return 8 * (arcs - st["arcs_big"]) + 16 * (st["vertices"] - st["vertices_big"])
     if kernel == "k_vhub":
-        return 20 * st["arcs_big"] + 16 * st["vertices_big"]
-    if kernel == "k_small_index":  # the whole index of a small batch: Ke + Ki + Kp
-        return 32 * w + 16 * w + 16 * st["vertices"] + 24 * w
+        return 8 * st["arcs_big"] + 16 * st["vertices_big"]
     if kernel == "k_update":
         return 24 * R + 32 * st["fresh"] + 16 * st["r2_replaced_retained"] - 4 * st["skipped"]
     return 0
@@ -368,9 +367,8 @@ def run_b200(args):
                 "frac": rows[dom].get("frac"), "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": rows[dom]["algorithmic_bytes_per_launch"],
                 "launch_ms": rows[dom]["ms_per_launch"],
-                "byte_model": "SURVEY 8(d): Ke 16w (k_count) + 16w (k_scatter); Ki 8 B/arc + 16 B/vertex and Kp 24w "
-                              "(12 B/arc) in the vertex kernels; Ku 24 B/estimator + 16 B per replaced r1 + 16 B "
-                              "per replaced r2",
+                "byte_model": "SURVEY 8(d): Ke 16w (k_count) + 16w (k_scatter); Ki 8 B/arc + 16 B/vertex; "
+                              "Kp 24w; Ku 24 B/estimator + 16 B per replaced r1 + 16 B per replaced r2",
                 "kernels": rows,
                 "whole_step": {"algorithmic_bytes": B_step, "ms": step_ms,
                                "achieved_GBps": B_step / (step_ms / 1e3) / 1e9,

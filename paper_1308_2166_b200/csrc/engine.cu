@@ -42,6 +42,7 @@ struct tc_ctx {
     uint64_t r = 0, seed = 0, first = 0, count = 0;
     uint64_t m = 0;
     uint32_t b = 0;
+    uint32_t ptag = 0;  // edge-pair table tag of the last push
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -180,7 +181,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.apos, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.pslot, 16 * cap) == cudaSuccess &&
               cudaMalloc(&ix.segS, 16 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.pt, 32ull * pair_groups_total(cap, kMaxBuckets)) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
               cudaMalloc(&ix.vt, 16 * 4 * cap) == cudaSuccess &&  // slices at 2 * (bucket start), <= 2 n_b slots
               cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess;
     ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.vstart2, 4 * kStartWords) == cudaSuccess &&
@@ -211,6 +212,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     ix.wcap = cap;
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
     CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
+    CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)cap), ctx->stream));  // tag 0: free
+    ctx->ptag = 0;
     return TC_OK;
 }
 
@@ -543,8 +546,13 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
     rec(2 * TC_PHASE_PARTITION, ms);
     launches += launch_partition(ix, a, ms, kr);
     rec(2 * TC_PHASE_PARTITION + 1, ms);
-    // (a3, the edge-pair table, is built by the vertex kernels: one region per vertex bucket)
-    (void)ss;
+    // a3 (it reads only the raw batch) on the second stream, alongside the vertex phase
+    ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
+    ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
+    rec(2 * TC_PHASE_PAIRS, ss);
+    launches += launch_pairs(ix, a, ss, kr);
+    rec(2 * TC_PHASE_PAIRS + 1, ss);
+    ok = ok && cudaEventRecord(ctx->join, ss) == cudaSuccess;
     ok = ok && cudaEventRecord(ctx->fork2, ms) == cudaSuccess;
     // a2: the large vertex buckets on the third stream, the common ones on the main stream
     ok = ok && cudaStreamWaitEvent(s2, ctx->fork2, 0) == cudaSuccess;
@@ -554,6 +562,7 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
     launches += launch_vertices(ix, a, ms, kr);
     ok = ok && cudaStreamWaitEvent(ms, ctx->join2, 0) == cudaSuccess;
     rec(2 * TC_PHASE_VERTICES + 1, ms);
+    ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
     rec(2 * TC_PHASE_UPDATE, ms);
     if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
     else launches += launch_update(ix, ctx->st, a, ms, kr);
@@ -621,11 +630,15 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     a.S = ctx->st.S;
     a.g = make_geometry((uint32_t)w, ctx->tune);
     a.small = ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax);
+    if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
+        CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
+        ctx->ptag = 1;
+    }
     BatchDesc d;
     d.in = pp.in;
     d.m_prev = ctx->m;
     d.batch = ctx->b;
-    d.reserved = 0;
+    d.ptag = ctx->ptag;
     d.slot = (uint32_t)slot;
     d.pad = 0;
     // the error word is sticky in asynchronous mode, and cleared (or set to the overflow error) here in strict

@@ -13,14 +13,10 @@
 //             2 * (the bucket's first arc slot) -- slices never overlap and need no prefix sum;
 //             vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
-//   edge-pair table: partitioned by VERTEX BUCKET -- the pairs whose lo endpoint lies in bucket b own groups
-//             [pr_first(st_b, b), pr_first(en_b, b + 1)) (st_b, en_b: the bucket's arc range; 3/8 group per arc
-//             plus one, so load <= 2/3 and ~1/3 typically), built whole by the bucket's vertex CTA every batch
-//             (in shared memory when it fits, then written out coalesced).  Groups of four 8-byte slots {k, fp32}
-//             (one 32-byte sector), k = 0xFFFFFFFF free; a pair probes its home group A, then (A full) an
-//             independent group B, then A+1, A+2, ... within the region; Step 3's (src,dst)-sorted "edges" array
-//             with its multisearch becomes one sector read (a fingerprint hit is verified
-//             against E[k]).
+//   edge-pair table: ceil(3w / 4) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
+//             <= 1/3); a pair probes its home group A, then (if A is full) an independent group B, then
+//             A+1, A+2, ...; Step 3's (src,dst)-sorted "edges" array with its
+//             multisearch becomes one sector read (a fingerprint hit is verified against E[k]).
 #pragma once
 #include <cstdint>
 
@@ -70,7 +66,7 @@ struct __align__(32) BatchDesc {
     const uint2 *in;             // the raw batch on this device
     unsigned long long m_prev;   // |E| before the batch
     uint32_t batch;              // index b of this non-empty batch (the Philox counter word)
-    uint32_t reserved;
+    uint32_t ptag;               // edge-pair slot tag of this push (1..254)
     uint32_t slot;               // S accumulator slot of this batch
     uint32_t pad;
 };
@@ -111,8 +107,11 @@ __host__ __device__ __forceinline__ uint64_t pair_key(uint32_t lo, uint32_t hi) 
 }
 
 __host__ __device__ __forceinline__ uint32_t vbucket_of(uint32_t h, uint32_t bv) { return bv ? h >> (32 - bv) : 0u; }
-// slot position word (bits 20..51) of a pair hash; the fingerprint is its low 32 bits
+// slot position word (bits 20..51) and 24-bit fingerprint (bits 0..23) of a pair hash; a slot is
+// {k, tag << 24 | fingerprint} and is live only when its tag is the batch's (1..254), so the table is
+// cleared once per 254 batches, not per batch
 __host__ __device__ __forceinline__ uint32_t pslot_word(uint64_t h) { return (uint32_t)(h >> 20); }
+__host__ __device__ __forceinline__ uint32_t pfinger(uint64_t h) { return (uint32_t)h & 0xFFFFFFu; }
 __host__ __device__ __forceinline__ uint32_t pgroup_start(uint64_t h, uint32_t groups) {
     return (uint32_t)(((uint64_t)pslot_word(h) * groups) >> 32);
 }
@@ -149,19 +148,19 @@ __host__ __device__ __forceinline__ uint32_t vfilter_bit(uint32_t hv) { return h
 struct Lookup {
     const uint2 *E;
     const VSlot *vt;
-    const uint2 *vslice;     // [BV] {offset, size}
+    const uint2 *vslice;   // [BV] {offset, size}
     uint32_t bv;
-    const uint2 *pt;         // pair slots {k, fp32}, groups of 4, one region per vertex bucket
-    const uint32_t *bstart;  // [BV + 1] the vertex buckets' arc ranges (their pair regions follow from them)
+    const uint2 *pt;       // pair slots {k, tag << 24 | fp}, groups of 4
+    uint32_t G;            // pair-table groups
+    uint32_t ptag;         // this batch's slot tag
 };
 
-// Pair-table regions: bucket b with arcs [st, en) owns groups [pr_first(st, b), pr_first(en, b + 1)).
-__host__ __device__ __forceinline__ uint32_t pr_first(uint32_t arc_start, uint32_t b) {
-    return (uint32_t)((3ull * arc_start) >> 3) + b;
+#ifndef TC_PT_GROUPS_PER_8
+#define TC_PT_GROUPS_PER_8 6  // groups of 4 slots per 8 edges: 6 -> load 1/3
+#endif
+__host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) {
+    return (uint32_t)(((uint64_t)w * TC_PT_GROUPS_PER_8 + 7) / 8);
 }
-// Groups of the whole table for batches of up to w edges in up to nb vertex buckets.
-__host__ __device__ __forceinline__ uint64_t pair_groups_total(uint64_t w, uint64_t nb) { return ((6ull * w) >> 3) + nb + 1; }
-constexpr uint32_t kPairFree = 0xFFFFFFFFu;  // k of a free slot
 
 // Continue a vertex probe at slot pair b of slice sl (after the first pair missed without an empty slot).
 static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uint32_t b, uint32_t v) {
@@ -175,36 +174,32 @@ static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uin
     }
 }
 
-// Pair probe split in two so that its load can be issued together with other probes: pt_issue() locates the
-// lo endpoint's bucket region and reads the home group A (one 32-byte sector); pt_resolve() scans it and, only
-// when A is full (rare), goes on to B, A+1, ...  Inside a group the filled slots form a prefix, so the first free
-// slot ends the search.  Result: batch position of {lo, hi} (lo < hi), or -1.
+// Pair probe split in two so that its load can be issued together with other probes: pt_issue() reads
+// the home group A (one 32-byte sector); pt_resolve() scans it and, only when A is full (rare at load
+// 1/3), goes on to B, A+1, ...  Inside a group the filled slots form a prefix, so the first empty slot
+// ends the search.  Result: batch position of {lo, hi} (lo < hi), or -1.
 struct PairProbe {
-    uint32_t lo, hi, fp, A, B, G;
-    const uint2 *sl;  // the region's first slot
-    uint4 a0, a1;     // group A
+    uint32_t lo, hi, fp, A, B, ng;
+    const uint2 *sl;
+    uint4 a0, a1;  // group A
 };
 
 __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t hi, bool active, PairProbe &P) {
     const uint64_t h = hash_pair64(pair_key(lo, hi));
+    const uint32_t ng = active ? L.G : 0u;
     P.lo = lo;
     P.hi = hi;
-    P.fp = (uint32_t)h;
-    P.G = 0;
-    P.A = P.B = 0;
-    P.a0 = P.a1 = make_uint4(kPairFree, 0u, kPairFree, 0u);
-    P.sl = L.pt;
-    if (!active) return;
-    const uint32_t b = vbucket_of(hash_vertex(lo), L.bv);
-    const uint32_t st = __ldg(L.bstart + b), en = __ldg(L.bstart + b + 1);
-    const uint32_t g0 = pr_first(st, b);
-    P.G = pr_first(en, b + 1) - g0;
-    P.sl = L.pt + 4ull * g0;
-    P.A = pgroup_start(h, P.G);
-    P.B = pgroup_second(h, P.G, P.A);
-    const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
-    P.a0 = __ldg(qa);
-    P.a1 = __ldg(qa + 1);
+    P.fp = (L.ptag << 24) | pfinger(h);
+    P.ng = ng;
+    P.sl = L.pt;  // 32-byte aligned
+    P.A = ng ? pgroup_start(h, ng) : 0u;
+    P.B = ng ? pgroup_second(h, ng, P.A) : 0u;
+    P.a0 = P.a1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
+    if (ng) {
+        const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
+        P.a0 = __ldg(qa);
+        P.a1 = __ldg(qa + 1);
+    }
 }
 
 // 0: not in the group and the group has room (absent); 1: found (*k set); 2: group full, go on.
@@ -212,7 +207,7 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
     const uint32_t ks[4] = {q0.x, q0.z, q1.x, q1.z}, fs[4] = {q0.y, q0.w, q1.y, q1.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        if (ks[i] == kPairFree) return 0;
+        if ((fs[i] >> 24) != L.ptag) return 0;  // free slot (stale tag)
         if (fs[i] == P.fp) {
             const uint2 e = __ldg(L.E + ks[i]);
             if (e.x == P.lo && e.y == P.hi) {
@@ -225,21 +220,20 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
 }
 
 static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
-    for (uint32_t i = 2; i <= P.G; ++i) {
-        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * pgroup_at(P.A, P.B, i, P.G));
+    for (uint32_t i = 2;; ++i) {
+        const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * pgroup_at(P.A, P.B, i, P.ng));
         uint32_t k;
         const int r = pt_group(L, P, __ldg(q), __ldg(q + 1), &k);
         if (r == 0) return -1;
         if (r == 1) return (int64_t)k;
     }
-    return -1;
 }
 
 __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &P) {
-    if (P.G == 0) return -1;
+    if (P.ng == 0) return -1;
     uint32_t k;
     int r = pt_group(L, P, P.a0, P.a1, &k);
-    if (r == 2) {  // group A full (rare): read B now
+    if (r == 2) {  // group A full (rare at load 1/3): read B now
         const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
         r = pt_group(L, P, __ldg(qb), __ldg(qb + 1), &k);
         if (r == 2) return pt_walk(L, P);

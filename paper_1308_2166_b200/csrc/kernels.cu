@@ -13,9 +13,9 @@
 //                          memory, written as coalesced runs), so each bucket holds its arcs in arrival order
 //                          -- the F array of rankAll's proof, partitioned
 //   k_split      a1      : (w > 2^21 only) each bucket stably split again by the next hash bits
-//   (a3)                   the edge-pair table is built by the vertex kernels below, one region per vertex
-//                          bucket (build_pair_region: the pairs whose lo endpoint is in the bucket; a repeat is
-//                          TC_EDUP); small batches also fill the vertex filter there
+//   k_pairs      a3      : (second stream, alongside the vertex phase) every edge of the raw batch into the
+//                          edge-pair table (64-bit CAS; a repeat is TC_EDUP); small batches also fill the
+//                          vertex filter
 //   k_vhash      a2      : one CTA per vertex bucket: bucket-local vertex ids from a shared-memory hash
 //                          table, one stable ranking pass by local id (replaces rankAll's sort by (src, -pos),
 //                          PAPER.md:680-684), segment starts -> segS, per-arc {slot, segEnd} (rank = segEnd -
@@ -108,7 +108,7 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t x, uint32_t *s
 // a1: bucket histograms
 
 struct PartArgs {
-    const BatchDesc *d;  // in, slot (per batch)
+    const BatchDesc *d;  // in, ptag, slot (per batch)
     uint32_t *apos2;     // [2 w] partition position of every arc (by arc id k<<1|side)
     Geometry g;
     uint2 *E;
@@ -117,10 +117,64 @@ struct PartArgs {
     uint32_t *offV;    // [tiles][nV] the tile's offset inside the bucket
     uint16_t *arank;   // [2 w] in-tile ranks
     uint32_t *vstart;  // bucket sizes (k_scan_cols) -> exclusive prefixes (k_scan_tot)
+    uint2 *pt;         // edge-pair table (G groups of 4 slots)
+    uint32_t G;
     uint32_t *ctr;
-    uint32_t *filt;    // small batches: the vertex filter (k_small_index zeroes it)
+    uint32_t *filt;    // small batches: the vertex filter to fill (else null)
     unsigned long long *S;  // the two S accumulators: k_count zeroes this batch's (d->slot) and the counters
 };
+
+// a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
+// with room along its probe sequence (A, B, A+1, ...), by 64-bit CAS, so the live slots of a group form a
+// prefix.  Meeting the
+// same pair (confirmed against the raw batch, which is stable while E is being written) returns true.
+__device__ __forceinline__ bool pt_insert(const PartArgs &a, const uint2 *in, uint32_t ptag, uint2 n, uint32_t k) {
+    const uint64_t h = hash_pair64(pair_key(n.x, n.y));
+    const uint32_t tf = (ptag << 24) | pfinger(h);
+    const unsigned long long mine = (unsigned long long)k | ((unsigned long long)tf << 32);
+    unsigned long long *t64 = reinterpret_cast<unsigned long long *>(a.pt);
+    const uint32_t A = pgroup_start(h, a.G), B = pgroup_second(h, a.G, A);
+    for (uint32_t step = 0;; ++step) {
+        const uint32_t g = pgroup_at(A, B, step, a.G);
+        const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
+        const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
+        const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
+#pragma unroll
+        for (uint32_t i = 0; i < 4; ++i) {
+            unsigned long long cur = cur4[i];
+            if ((uint32_t)(cur >> 56) != ptag) {
+                const unsigned long long old = atomicCAS(t64 + 4ull * g + i, cur, mine);
+                if (old == cur) return false;
+                cur = old;  // taken meanwhile (by this batch)
+            }
+            if ((uint32_t)(cur >> 32) == tf) {
+                const uint2 o = norm_edge(__ldg(in + (uint32_t)cur));
+                if (o.x == n.x && o.y == n.y) return true;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_pairs(PartArgs a) {
+    if (a.ctr[kCtrErr] & (kErrStage | kErrDup)) return;  // sticky error of an earlier async batch
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint2 *in = a.d->in;
+    const uint32_t ptag = a.d->ptag;
+    bool dup = false;
+    if (k < a.g.w) {
+        const uint2 e = __ldg(in + k);
+        if (e.x != kEmptyV && e.y != kEmptyV && e.x != e.y) {  // k_count reports the rest
+            const uint2 n = norm_edge(e);
+            dup = pt_insert(a, in, ptag, n, k);
+            if (a.filt) {
+                const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
+                atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
+                atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
+            }
+        }
+    }
+    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+}
 
 // Tile ranking: validate and normalise W, write E, and rank every arc (by vertex bucket) and every edge (by
 // pair bucket) inside its tile, stably in arrival order.  Arc a of the tile (a = 2 e + side) is owned by
@@ -432,69 +486,7 @@ struct VertArgs {
     uint32_t vcap;      // buckets with more arcs go to k_vbig
     uint32_t sortcap;   // k_vbig: buckets with more arcs take the chunked global-memory path
     uint32_t *ctr;
-    uint2 *pt;          // edge-pair table: one region per vertex bucket (build_pair_region)
-    uint32_t *filt;     // small batches: the vertex filter (bits of every arc's vertex), else null
 };
-
-constexpr unsigned long long kFreeSlot = 0x00000000FFFFFFFFull;  // a free pair slot: k = kPairFree
-
-// Insert {lo, hi} -> k into a region of G groups (shared or global memory): the first free slot along its probe
-// sequence A, B, A+1, ..., by 64-bit CAS, so a group's filled slots form a prefix.  Returns true if the pair
-// is already there (a duplicate in the batch, confirmed against E).
-__device__ __forceinline__ bool pair_insert(unsigned long long *tab, uint32_t G, uint32_t lo, uint32_t hi, uint32_t k,
-                                            const uint2 *E) {
-    const uint64_t h = hash_pair64(pair_key(lo, hi));
-    const uint32_t fp = (uint32_t)h;
-    const unsigned long long mine = (unsigned long long)k | ((unsigned long long)fp << 32);
-    const uint32_t A = pgroup_start(h, G), B = pgroup_second(h, G, A);
-    for (uint32_t step = 0;; ++step) {
-        volatile unsigned long long *grp = tab + 4ull * pgroup_at(A, B, step, G);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            unsigned long long cur = grp[q];
-            if ((uint32_t)cur == kPairFree) {
-                const unsigned long long old = atomicCAS(const_cast<unsigned long long *>(grp + q), kFreeSlot, mine);
-                if (old == kFreeSlot) return false;
-                cur = old;  // taken meanwhile
-            }
-            if ((uint32_t)(cur >> 32) == fp) {
-                const uint2 o = E[(uint32_t)cur];
-                if (o.x == lo && o.y == hi) return true;
-            }
-        }
-    }
-}
-
-// a3 inside the vertex phase: the edge-pair-table region of vertex bucket b (its arcs [st, en) of a.arcs) --
-// every pair {lo, hi} whose lo endpoint lies in the bucket (its side-0 arc), with its batch position k -- built
-// in shared memory (sm, cap slots) when it fits and then written out whole and coalesced, else in place in
-// global memory (the region is this CTA's alone).  A pair met twice is TC_EDUP (confirmed against E).  Small
-// batches also get the vertex-filter bit of every arc.  Called by the whole CTA; sm may alias dead scratch.
-template <int NT>
-__device__ __noinline__ void build_pair_region(const VertArgs &a, uint32_t b, uint32_t st, uint32_t en,
-                                               unsigned long long *sm, uint32_t cap) {
-    const uint32_t g0 = pr_first(st, b), G = pr_first(en, b + 1) - g0, S = 4 * G;
-    const bool in_sm = sm != nullptr && S <= cap;
-    unsigned long long *tab = in_sm ? sm : reinterpret_cast<unsigned long long *>(a.pt) + 4ull * g0;
-    for (uint32_t s = threadIdx.x; s < S; s += NT) tab[s] = kFreeSlot;
-    __syncthreads();
-    bool dup = false;
-    for (uint32_t i = st + threadIdx.x; i < en; i += NT) {
-        const uint4 x = a.arcs[i];
-        if (a.filt) {
-            const uint32_t bit = vfilter_bit(hash_vertex(x.x));
-            atomicOr(a.filt + (bit >> 5), 1u << (bit & 31u));
-        }
-        if (x.y & 1u) continue;  // the hi-side arc: its pair belongs to the lo endpoint's bucket
-        dup |= pair_insert(tab, G, x.x, x.z, x.y >> 1, a.E);
-    }
-    if (__syncthreads_or(dup) && threadIdx.x == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
-    if (in_sm) {
-        uint4 *dst = reinterpret_cast<uint4 *>(a.pt + 4ull * g0);
-        const uint4 *src = reinterpret_cast<const uint4 *>(sm);
-        for (uint32_t s = threadIdx.x; s < S / 2; s += NT) dst[s] = src[s];
-    }
-}
 
 constexpr uint32_t kVWarps = kVBucketThreads / 32;
 constexpr uint32_t kVAux = kVChunk > kVWarps * 256 + 256 ? kVChunk : kVWarps * 256 + 256;
@@ -847,9 +839,6 @@ __global__ void __launch_bounds__(kVBucketThreads, 1) k_vbig(VertArgs a) {
         const uint32_t b = s_b;
         __syncthreads();
         if (b == 0xFFFFFFFFu) return;
-        // the pair region first, in place in global memory: the chunked sort reuses the bucket's arc memory
-        build_pair_region<kVBucketThreads>(a, b, a.vstart[b], a.vstart[b + 1], nullptr, 0u);
-        __syncthreads();
         vbucket_sort(a, b, vsm, dtot, ws);
         __syncthreads();
     }
@@ -1047,33 +1036,6 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         else if (l == D) o = make_uint4(hub, hubn, base, 0u);
         reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
     }
-    // the 1024-thread callers (hub buckets, the one-CTA small index) build the pair region from global memory
-    // afterwards (build_pair_region): keeping R items live to here would spill their registers
-    if (hubn || NT != kHThreads) return;
-    // phase 6 (a3): the bucket's edge-pair region from the arcs still in registers (vertex = vkey[local id]), in
-    // the dead hash-path memory when it fits, then written out whole; the small-batch filter bits of its vertices
-    const uint32_t g0 = pr_first(base, b), G = pr_first(base + n, b + 1) - g0, SP = 4 * G;
-    if (a.filt)
-        for (uint32_t l = threadIdx.x; l < D; l += NT) {
-            const uint32_t bit = vfilter_bit(hash_vertex(vkey[l]));
-            atomicOr(a.filt + (bit >> 5), 1u << (bit & 31u));
-        }
-    const bool in_sm = SP * 8 <= L::R1;
-    unsigned long long *tab =
-        in_sm ? reinterpret_cast<unsigned long long *>(sm) : reinterpret_cast<unsigned long long *>(a.pt) + 4ull * g0;
-    __syncthreads();  // the slice loop above is done with the shared table
-    for (uint32_t s = threadIdx.x; s < SP; s += NT) tab[s] = kFreeSlot;
-    __syncthreads();
-    bool dup = false;
-#pragma unroll
-    for (int j = 0; j < R; ++j)
-        if (pk[j] != 0xFFFFFFFFu && !(val[j] & 1u)) dup |= pair_insert(tab, G, vkey[pk[j] >> 16], nbv[j], val[j] >> 1, a.E);
-    if (__syncthreads_or(dup) && threadIdx.x == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
-    if (in_sm) {
-        uint4 *dst = reinterpret_cast<uint4 *>(a.pt + 4ull * g0);
-        const uint4 *src4 = reinterpret_cast<const uint4 *>(sm);
-        for (uint32_t s = threadIdx.x; s < SP / 2; s += NT) dst[s] = src4[s];
-    }
 }
 
 template <uint32_t CAP, int NT, typename F>
@@ -1142,9 +1104,6 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
             hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
                 vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(a, b, base, src, n, 0u, 0u, 0u, hsm, ws, &sD);
             });
-            __syncthreads();
-            build_pair_region<kHubThreads>(a, b, base, base + n, reinterpret_cast<unsigned long long *>(hsm),
-                                           kVHubSmemBytes / 8);
             __syncthreads();
             continue;
         }
@@ -1244,9 +1203,6 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
             vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(a, b, base, src, n - H, H, h, H, hsm, ws, &sD);
         });
         __syncthreads();
-        build_pair_region<kHubThreads>(a, b, base, base + n, reinterpret_cast<unsigned long long *>(hsm),
-                                       kVHubSmemBytes / 8);
-        __syncthreads();
     }
 }
 
@@ -1268,7 +1224,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
     __syncthreads();
     if (sticky) return;
     const uint2 *in = a.d->in;
-    const uint32_t w = a.g.w;
+    const uint32_t ptag = a.d->ptag, w = a.g.w;
     // validation and normalisation first: a rejected batch must not insert anything
     uint32_t bad = 0;
     for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
@@ -1279,6 +1235,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
     bad = __reduce_or_sync(kFull, bad);
     if (bad && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], bad);
     if (__syncthreads_or(bad != 0)) return;
+    bool dup = false;
     for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
         const uint2 n = norm_edge(__ldg(in + k));
         a.E[k] = n;
@@ -1287,19 +1244,20 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
         v.arcs[2 * k + 1] = make_uint4(n.y, 2 * k + 1, n.x, 2 * k + 1);
         a.apos2[2 * k] = 2 * k;
         a.apos2[2 * k + 1] = 2 * k + 1;
+        dup |= pt_insert(a, in, ptag, n, k);
+        if (a.filt) {
+            const uint32_t b0 = vfilter_bit(hash_vertex(n.x)), b1 = vfilter_bit(hash_vertex(n.y));
+            atomicOr(a.filt + (b0 >> 5), 1u << (b0 & 31u));
+            atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
+        }
     }
-    if (threadIdx.x == 0) {  // the one bucket's arc range (the pair region and the lookups derive from it)
-        a.vstart[0] = 0u;
-        a.vstart[1] = 2 * w;
-    }
+    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
     __syncthreads();  // the arcs this CTA wrote are visible to all its threads
     const uint32_t n = 2 * w;
     const ArcSrc src{v.arcs, nullptr, nullptr, nullptr};
     hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
         vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(v, 0u, 0u, src, n, 0u, 0u, 0u, hsm, ws, &sD);
     });
-    __syncthreads();  // the hash path's shared memory is dead: the pair region is built there
-    build_pair_region<kHubThreads>(v, 0u, 0u, n, reinterpret_cast<unsigned long long *>(hsm), kVHubSmemBytes / 8);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1331,6 +1289,7 @@ struct UpdateArgs {
 __device__ __forceinline__ void with_desc(UpdateArgs &u, Lookup &L) {
     u.batch = u.d->batch;
     u.m_prev = u.d->m_prev;
+    L.ptag = u.d->ptag;
 }
 
 template <bool kSmall>
@@ -1826,15 +1785,14 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 }
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
-    return PartArgs{ix.desc, reinterpret_cast<uint32_t *>(ix.apos), a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart,
-                    ix.ctr, a.small ? ix.filt : nullptr, a.S};
+    return PartArgs{ix.desc, reinterpret_cast<uint32_t *>(ix.apos), a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), ix.ctr,
+                    a.small ? ix.filt : nullptr, a.S};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     const Geometry &g = a.g;
     const uint32_t nV = 1u << g.bp1;
     const PartArgs p = part_args(ix, a);
-    if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
     kr.beg(K_COUNT, s);
     switch (g.bp1) {
 #define TC_COUNT_CASE(B) \
@@ -1864,12 +1822,18 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, co
     return 5;
 }
 
-
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
+    if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
+    kr.beg(K_PAIRS, s);
+    k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
+    kr.end(K_PAIRS, s);
+    return 1;
+}
 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
     return VertArgs{a.g.bs ? ix.arcs2 : ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E,
                     a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, ix.pslot, reinterpret_cast<const uint32_t *>(ix.apos), ix.vt, ix.vslice,
-                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr, ix.pt, a.small ? ix.filt : nullptr};
+                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
 }
 
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
@@ -1898,8 +1862,7 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, a.g.bs ? ix.vstart2 : ix.vstart}, ix.apos, ix.pslot, ix.segS,
-                 ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);
@@ -1914,8 +1877,7 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, a.g.bs ? ix.vstart2 : ix.vstart}, ix.apos, ix.pslot, ix.segS,
-                 ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, 8);
     kr.beg(K_U1, s);

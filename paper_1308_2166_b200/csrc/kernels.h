@@ -24,7 +24,7 @@ struct IndexBufs {
     uint2 *vslice = nullptr;       // [4096] {offset, size}
     uint32_t *vperm = nullptr;     // [4096] vertex buckets in processing order (oversized first)
     uint32_t *vdefer = nullptr;    // [4096] large buckets k_vhub hands to k_vbig
-    uint2 *pt = nullptr;           // pair slots {k, fp32}, groups of 4, one region per vertex bucket
+    uint2 *pt = nullptr;           // [4 ceil(wcap / 2)] pair slots {k, fp}, groups of 4
     uint32_t *cntV = nullptr;      // [4096 * tiles] per-(bucket, tile) arc counts
     uint32_t *offV = nullptr;      // [4096 * tiles] the tile's offset inside the bucket
     uint16_t *arank = nullptr;     // [2 wcap] rank of each arc among its tile's arcs of the same vertex bucket
@@ -85,8 +85,7 @@ struct BatchArgs {
     uint64_t first;   // global id of local estimator 0
     uint64_t seed;
     unsigned long long *S;  // the two S accumulators (slot from the descriptor)
-    bool small;       // small-batch estimator pass (vertex filter built by the vertex kernels, k_update skips
-                      // untouched estimators)
+    bool small;       // small-batch estimator pass (filters built by k_pairs, k_update skips untouched estimators)
     Geometry g;
 };
 
@@ -123,6 +122,7 @@ struct KRec {
 
 // Each returns the number of kernel launches issued.
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1
+int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());      // a3
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());   // a2
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1-a3
 int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a2 > vcap
