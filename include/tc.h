@@ -49,7 +49,8 @@ enum {
                             handle poisoned                                                 */
     TC_ESTATE = -8,      /* handle poisoned by an earlier asynchronous error               */
     TC_EPARSE = -9,      /* malformed edge-list line (tc_parse_edges / tc_ingest_file)      */
-    TC_EIO = -10         /* the edge-list file cannot be opened or read                     */
+    TC_EIO = -10,        /* the edge-list file cannot be opened or read                     */
+    TC_EINTERNAL = -11   /* a bounds check of a -DTC_CHECKED build failed (never in release) */
 };
 
 /* tc_create -- r estimators (ids 0..r-1) on the current CUDA device, all "empty" (f1 = f2 = f3 =

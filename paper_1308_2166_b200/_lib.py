@@ -20,6 +20,7 @@ TC_ENCCL = -7
 TC_ESTATE = -8
 TC_EPARSE = -9
 TC_EIO = -10
+TC_EINTERNAL = -11
 TC_INGEST_SKIP_LOOPS = 1
 TC_NPHASES = 4
 PHASES = ("partition", "pairs", "vertices", "update")

@@ -354,6 +354,7 @@ tc_ctx *tc_create(uint64_t r, uint64_t seed) { return tc_create_shard(r, seed, 0
 void tc_destroy(tc_ctx *ctx) { destroy_ctx(ctx); }
 
 static int decode_err(uint32_t e) {
+    if (e & kErrInternal) return TC_EINTERNAL;
     if (e & kErrInval) return TC_EINVAL;
     if (e & kErrLoop) return TC_ESELFLOOP;
     if (e & kErrDup) return TC_EDUP;
@@ -1450,6 +1451,7 @@ const char *tc_strerror(int code) {
         case TC_ECUDA: return "CUDA error";
         case TC_ESTATE: return "handle poisoned by an earlier asynchronous error";
         case TC_ENCCL: return "NCCL error (communicator aborted)";
+        case TC_EINTERNAL: return "internal bounds check failed (TC_CHECKED build)";
         case TC_EPARSE: return "malformed edge-list line";
         case TC_EIO: return "cannot open or read the edge-list file";
         default: return "unknown error";

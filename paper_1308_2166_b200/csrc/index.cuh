@@ -31,6 +31,7 @@ constexpr uint32_t kErrInval = 1u;
 constexpr uint32_t kErrLoop = 2u;
 constexpr uint32_t kErrDup = 4u;
 constexpr uint32_t kErrOvf = 8u;
+constexpr uint32_t kErrInternal = 16u;  // a TC_CHECKED build's device bounds check failed (TC_EINTERNAL)
 // errors found while counting (they stop the index build); a duplicate (found by the pair-bucket kernel,
 // concurrently with the vertex buckets) or an overflow (set by the host) only stop the estimator update
 constexpr uint32_t kErrStage = kErrInval | kErrLoop;
@@ -62,6 +63,20 @@ constexpr int kCtrWords = 16;
 
 // Per-batch values the kernels read from device memory (written by k_desc, the first node of every push), so
 // that one captured CUDA graph per batch shape is relaunched unchanged from batch to batch.
+// Bounds checks of computed indices (the substitute for compute-sanitizer, which this GPU pool refuses):
+// compiled in with -DTC_CHECKED (tests/test_checked_build.py), a violation sets kErrInternal in the error word
+// and the push fails with TC_EINTERNAL; compiled out otherwise.
+#ifdef TC_CHECKED
+#define TC_CHECK(cond, ctr)                                                  \
+    do {                                                                     \
+        if (!(cond)) atomicOr(const_cast<uint32_t *>(&(ctr)[kCtrErr]), kErrInternal); \
+    } while (0)
+#else
+#define TC_CHECK(cond, ctr) \
+    do {                    \
+    } while (0)
+#endif
+
 struct __align__(32) BatchDesc {
     const uint2 *in;             // the raw batch on this device
     unsigned long long m_prev;   // |E| before the batch

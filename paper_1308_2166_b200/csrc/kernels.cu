@@ -136,6 +136,7 @@ __device__ __forceinline__ bool pt_insert(const PartArgs &a, const uint2 *in, ui
     const uint32_t A = pgroup_start(h, a.G), B = pgroup_second(h, a.G, A);
     for (uint32_t step = 0;; ++step) {
         const uint32_t g = pgroup_at(A, B, step, a.G);
+        TC_CHECK(g < a.G && step <= a.G, a.ctr);
         const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
         const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
         const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
         const uint32_t v = (ai & 1u) ? n.y : n.x, nb = (ai & 1u) ? n.x : n.y;
         const uint32_t d = vbucket_of(hash_vertex(v), a.g.bp1);
         const uint32_t P = soff[d] + (pos - toff[d]);  // the arc's partition position (kept through k_split in .w)
+        TC_CHECK(P < 2 * a.g.w, a.ctr);
         __stcs(a.arcs + P, make_uint4(v, 2u * e0 + ai, nb, P));
     }
 }
@@ -459,6 +461,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
             tot[threadIdx.x] = r;  // this chunk's count
         }
         __syncthreads();
+        TC_CHECK(!valid || soff[sb] + run[sb] + wc[warp][sb] + mine < n, a.ctr);
         if (valid) a.arcs2[base + soff[sb] + run[sb] + wc[warp][sb] + mine] = x4;
         __syncthreads();
         if (threadIdx.x < S) run[threadIdx.x] += tot[threadIdx.x];
@@ -486,6 +489,7 @@ struct VertArgs {
     uint32_t vcap;      // buckets with more arcs go to k_vbig
     uint32_t sortcap;   // k_vbig: buckets with more arcs take the chunked global-memory path
     uint32_t *ctr;
+    uint32_t narcs;     // 2 w (TC_CHECKED bounds)
 };
 
 constexpr uint32_t kVWarps = kVBucketThreads / 32;
@@ -660,6 +664,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
             const uint2 x = sbuf[i];
             if (i == 0 || x.x != sbuf[i - 1].x) ++r;
             const uint32_t end = r < D ? run_start[r] : n;  // run r-1 ends where run r starts
+            TC_CHECK(base + end <= a.narcs && x.y < a.narcs && a.apos2[x.y] < a.narcs, a.ctr);
             a.segS[base + i] = make_uint2(x.y, arc_neighbour(a.E, x.y));
             a.pslot[a.apos2[x.y]] = make_uint2(base + i, base + end);
         }
@@ -795,6 +800,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
             if (i == 0 || x.x != src[i - 1].x) ++r;
             const uint32_t run = r - 1;
             const uint32_t end = run + 1 < D ? gruns[run + 1] : n;
+            TC_CHECK(base + end <= a.narcs && x.y < a.narcs && a.apos2[x.y] < a.narcs, a.ctr);
             a.segS[base + i] = make_uint2(x.y, arc_neighbour(a.E, x.y));
             a.pslot[a.apos2[x.y]] = make_uint2(base + i, base + end);
         }
@@ -1006,9 +1012,11 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         if (pk[j] == 0xFFFFFFFFu) continue;
         const uint32_t l = pk[j] >> 16;
         const uint32_t pos = segst[l] + (pk[j] & 0xFFFFu);
+        TC_CHECK(pos < n && b0 + segst[l + 1] <= a.narcs && val[j] < a.narcs, a.ctr);
         a.segS[b0 + pos] = make_uint2(val[j], nbv[j]);
         // by the arc's partition position: this bucket's own range, so the writes fill whole sectors in L2
         const uint32_t i = warp * 32u * R + j * 32u + lane;
+        TC_CHECK(src.g[i].w < a.narcs, a.ctr);
         a.pslot[src.g[i].w] = make_uint2(b0 + pos, b0 + segst[l + 1]);
     }
     // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole; the hub (if
@@ -1186,6 +1194,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
             }
             if (isH) {
                 const uint32_t pos = ph + __popc(bh & lt);
+                TC_CHECK(pos < H && base + H <= a.narcs && x.w < a.narcs, a.ctr);
                 a.segS[base + pos] = make_uint2(x.y, x.z);
                 a.pslot[x.w] = make_uint2(base + pos, base + H);
             } else if (valid) {
@@ -1348,7 +1357,9 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
     if (fresh) {
         r1 = __ldg(ix.L.E + j);
         const uint2 ap = __ldg(ix.apos + j);
+        TC_CHECK(j < u.w && ap.x < 2 * u.w && ap.y < 2 * u.w, ix.ctr);
         const uint2 pu = __ldg(ix.pslot + ap.x), pv = __ldg(ix.pslot + ap.y);
+        TC_CHECK(pu.x < pu.y && pu.y <= 2 * u.w && pv.x < pv.y && pv.y <= 2 * u.w, ix.ctr);
         inf = make_uint4(pu.x, pu.y, pv.x, pv.y);
     } else {
         su = __ldg(ix.L.vslice + vbucket_of(hu, ix.L.bv));
@@ -1399,6 +1410,7 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
         const uint32_t phi = (uint32_t)(d2 - (c - chi_p));
         const bool atU = phi < ld;  // (src = u, rank = phi) or (src = v, rank = phi - ld)
         if (r2new) {
+            TC_CHECK((atU ? endU : endV) - 1u - (atU ? phi : phi - ld) < 2 * u.w, ix.ctr);
             const uint2 arc = __ldg(ix.segS + ((atU ? endU : endV) - 1u - (atU ? phi : phi - ld)));
             const uint32_t src = atU ? r1.x : r1.y;
             k2 = arc.x >> 1;
@@ -1833,7 +1845,7 @@ int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const 
 static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
     return VertArgs{a.g.bs ? ix.arcs2 : ix.arcs, ix.scratch, reinterpret_cast<uint4 *>(ix.scratch), ix.E,
                     a.g.bs ? ix.vstart2 : ix.vstart, ix.segS, ix.pslot, reinterpret_cast<const uint32_t *>(ix.apos), ix.vt, ix.vslice,
-                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr};
+                    ix.vperm, ix.vdefer, a.g.bv, a.g.vcap, a.g.sortcap, ix.ctr, 2 * a.g.w};
 }
 
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {

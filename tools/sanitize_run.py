@@ -34,6 +34,13 @@ def main():
                 t.push_batch(hub[k:k + 6000])
             assert t.sync() == 0
             assert_states_equal(t.state(), oracle_run(hub, 700, 5, 6000).state(), f"{knobs} graphs={graphs}")
+    # the one-CTA index and the partitioned build at the same small batch size
+    for si in (2, 1):
+        t = TriangleCounter(900, 7)
+        t.tune(small_index=si)
+        for k in range(0, len(hub), 2000):
+            t.push_batch(hub[k:k + 2000])
+        assert_states_equal(t.state(), oracle_run(hub, 900, 7, 2000).state(), f"small_index={si}")
     bad = np.array([[1, 2], [3, 3]], np.uint32)
     assert tc.push_batch(bad, check=False) != 0
     if os.environ.get("TC_SANITIZE_NCCL", "1") == "1":
