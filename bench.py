@@ -191,6 +191,8 @@ def kernel_bytes(kernel, w, st, R):
         return 8 * (arcs - st["arcs_big"]) + 16 * (st["vertices"] - st["vertices_big"])
     if kernel == "k_vhub":
         return 8 * st["arcs_big"] + 16 * st["vertices_big"]
+    if kernel == "k_small_index":  # the whole index of a small batch in one kernel: Ke 32w + Ki 16w + 16D + Kp 24w
+        return 72 * w + 16 * st["vertices"]
     if kernel == "k_update":
         return 24 * R + 32 * st["fresh"] + 16 * st["r2_replaced_retained"] - 4 * st["skipped"]
     return 0
