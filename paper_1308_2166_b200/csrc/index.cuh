@@ -42,9 +42,12 @@ constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 #endif
 constexpr uint32_t kTileEdges = TC_TILE_EDGES;  // edges per count/scatter tile
 constexpr uint32_t kTileThreads = 512;
-constexpr uint32_t kMaxPartBits = 12;     // the partition kernels: at most 4096 vertex buckets
-constexpr uint32_t kMaxSplitBits = 3;     // k_split: each of them into at most 8 sub-buckets
-constexpr uint32_t kMaxBucketBits = kMaxPartBits + kMaxSplitBits;
+#ifndef TC_PART_BITS
+#define TC_PART_BITS 12
+#endif
+constexpr uint32_t kMaxBucketBits = 15;   // at most 2^15 vertex buckets
+constexpr uint32_t kMaxPartBits = TC_PART_BITS;  // the partition kernels: at most 2^12 vertex buckets
+constexpr uint32_t kMaxSplitBits = kMaxBucketBits - kMaxPartBits;  // k_split: each into at most 2^3 sub-buckets
 constexpr uint32_t kVBucketThreads = 256; // vertex-bucket CTA
 constexpr uint32_t kVItems = 24;          // arcs per thread held in registers by the vertex-bucket sort
 constexpr uint32_t kVChunk = kVBucketThreads * kVItems;  // 6144 arcs: larger buckets take the chunked path
@@ -179,7 +182,7 @@ __host__ __device__ __forceinline__ uint32_t pair_groups(uint32_t w) {
 
 // Continue a vertex probe at slot pair b of slice sl (after the first pair missed without an empty slot).
 static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uint32_t b, uint32_t v) {
-    while (true) {
+    for (uint32_t it = 0; it < sl.y / 2; ++it) {  // every slot pair once (slices are at most half full)
         b = vslot_next(b, sl.y);
         const uint4 *p = reinterpret_cast<const uint4 *>(L.vt + sl.x + b);
         const uint4 s0 = __ldg(p), s1 = __ldg(p + 1);
@@ -187,6 +190,7 @@ static __device__ __noinline__ uint2 vt_find_from(const Lookup &L, uint2 sl, uin
         if (s1.x == v) return make_uint2(s1.y, s1.z);
         if (s0.x == kEmptyV || s1.x == kEmptyV) return make_uint2(0u, 0u);
     }
+    return make_uint2(0u, 0u);
 }
 
 // Pair probe split in two so that its load can be issued together with other probes: pt_issue() reads
@@ -235,13 +239,14 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
 }
 
 static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
-    for (uint32_t i = 2;; ++i) {
+    for (uint32_t i = 2; i <= P.ng; ++i) {  // every group once
         const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * pgroup_at(P.A, P.B, i, P.ng));
         uint32_t k;
         const int r = pt_group(L, P, __ldg(q), __ldg(q + 1), &k);
         if (r == 0) return -1;
         if (r == 1) return (int64_t)k;
     }
+    return -1;
 }
 
 __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &P) {

@@ -135,8 +135,12 @@ __device__ __forceinline__ bool pt_insert(const PartArgs &a, const uint2 *in, ui
     unsigned long long *t64 = reinterpret_cast<unsigned long long *>(a.pt);
     const uint32_t A = pgroup_start(h, a.G), B = pgroup_second(h, a.G, A);
     for (uint32_t step = 0;; ++step) {
+        if (step > a.G) {  // every group visited: cannot happen at load <= 1/3 -- an internal error, not a hang
+            atomicOr(&a.ctr[kCtrErr], kErrInternal);
+            return false;
+        }
         const uint32_t g = pgroup_at(A, B, step, a.G);
-        TC_CHECK(g < a.G && step <= a.G, a.ctr);
+        TC_CHECK(g < a.G, a.ctr);
         const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(t64 + 4ull * g);
         const ulonglong2 a0 = __ldcg(q), a1 = __ldcg(q + 1);
         const unsigned long long cur4[4] = {a0.x, a0.y, a1.x, a1.y};
@@ -422,6 +426,11 @@ __global__ void __launch_bounds__(kSplitThreads, 1) k_split(SplitArgs a) {
         tot[threadIdx.x] = 0;
         run[threadIdx.x] = 0;
     }
+    if (n == 0) {  // an empty bucket: its sub-buckets are empty too (their starts must still be written)
+        if (threadIdx.x < S) a.vstart2[(b << a.bs) + threadIdx.x] = base;
+        if (threadIdx.x == 0 && b == gridDim.x - 1) a.vstart2[gridDim.x << a.bs] = base;
+        return;
+    }
     const bool one_chunk = n <= kSplitChunk;
     if (!one_chunk) {  // sub-bucket sizes of a multi-chunk bucket first
         __syncthreads();
@@ -595,12 +604,13 @@ __device__ __forceinline__ void rank_pass(const uint32_t (&key)[kVItems], uint32
 
 // Table insert of run r (vertex hash h) into a power-of-two table of u16 run indices, 2-slot aligned
 // linear probing (the probe order vt_find assumes).
-__device__ __forceinline__ void stable_insert16(uint16_t *table, uint32_t S, uint32_t h, uint32_t r) {
+__device__ __forceinline__ void stable_insert16(uint16_t *table, uint32_t S, uint32_t h, uint32_t r, uint32_t *ctr) {
     uint32_t s = vslot_start(h, S);
-    while (true) {
+    for (uint32_t it = 0; it < S; ++it) {
         if (table[s] == 0xFFFFu && atomicCAS(&table[s], (unsigned short)0xFFFFu, (unsigned short)r) == 0xFFFFu) return;
         if (++s == S) s = 0;
     }
+    atomicOr(&ctr[kCtrErr], kErrInternal);  // a full table: an internal error, never a hang
 }
 
 // The other endpoint of the edge of arc val = k<<1 | side (side 0 = the lo endpoint).
@@ -701,7 +711,7 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         uint16_t *table = reinterpret_cast<uint16_t *>(sbuf);
         for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) table[s] = 0xFFFFu;
         __syncthreads();
-        for (uint32_t q = threadIdx.x; q < D; q += kVBucketThreads) stable_insert16(table, S, run_key[q], q);
+        for (uint32_t q = threadIdx.x; q < D; q += kVBucketThreads) stable_insert16(table, S, run_key[q], q, a.ctr);
         __syncthreads();
         for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) {
             const uint32_t q = table[s];
@@ -844,9 +854,14 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         const uint32_t st = gruns[q], en = q + 1 < D ? gruns[q + 1] : n;
         const uint32_t h = src[st].x;
         const u128 v = (u128)unhash_vertex(h) | ((u128)(en - st) << 32) | ((u128)(base + st) << 64);
-        uint32_t s = vslot_start(h, S);
-        while (atomicCAS(reinterpret_cast<u128 *>(sl + s), empty, v) != empty)
+        uint32_t s = vslot_start(h, S), it = 0;
+        while (atomicCAS(reinterpret_cast<u128 *>(sl + s), empty, v) != empty) {
             if (++s == S) s = 0;
+            if (++it == S) {
+                atomicOr(&a.ctr[kCtrErr], kErrInternal);
+                break;
+            }
+        }
     }
 }
 
@@ -950,7 +965,11 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
             val[j] = x.y;
             nbv[j] = x.z;
             uint32_t s = hash_vertex(x.x) & (Tb - 1);
-            while (true) {
+            for (uint32_t it = 0;; ++it) {
+                if (it == Tb) {  // a full table: an internal error, never a hang
+                    atomicOr(&a.ctr[kCtrErr], kErrInternal);
+                    break;
+                }
                 uint32_t k = hkey[s];
                 if (k == kEmptyV) {
                     k = atomicCAS(&hkey[s], kEmptyV, x.x);
@@ -1054,9 +1073,14 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     for (uint32_t s = threadIdx.x; s < S; s += NT) table[s] = kEmptyV;
     __syncthreads();
     for (uint32_t l = threadIdx.x; l < Dt; l += NT) {
-        uint32_t s = vslot_start(hash_vertex(l < D ? vkey[l] : hub), S);
-        while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV)
+        uint32_t s = vslot_start(hash_vertex(l < D ? vkey[l] : hub), S), it = 0;
+        while (atomicCAS(&table[s], kEmptyV, l) != kEmptyV) {
             if (++s == S) s = 0;
+            if (++it == S) {
+                atomicOr(&a.ctr[kCtrErr], kErrInternal);
+                break;
+            }
+        }
     }
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < S; s += NT) {
@@ -1147,7 +1171,7 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
         {
             const uint32_t v = arcs[(uint32_t)(((uint64_t)threadIdx.x * n) / kHubSample)].x;
             uint32_t s = hash_vertex(v) & (2 * kHubSample - 1);
-            while (true) {
+            for (uint32_t it = 0; it < 2 * kHubSample; ++it) {  // 1024 samples in 2048 slots: always room
                 const uint32_t k = atomicCAS(&skey[s], kEmptyV, v);
                 if (k == kEmptyV || k == v) break;
                 s = (s + 1) & (2 * kHubSample - 1);
