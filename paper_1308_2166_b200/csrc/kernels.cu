@@ -404,99 +404,72 @@ struct SplitArgs {
 };
 
 constexpr int kSplitThreads = 1024;
-constexpr uint32_t kSplitItems = 8;                                  // arcs per thread per chunk
-constexpr uint32_t kSplitChunk = kSplitThreads * kSplitItems;       // 8192: most partition buckets are one chunk
 
-// One partition bucket per CTA.  A chunk of up to 8192 arcs is held in registers (warp w owns chunk items
-// [256 w, 256 (w+1)), round j lane l = item 256 w + 32 j + l, so (warp, round, lane) order is arrival order);
-// each item's stable rank inside its sub-bucket comes from ballots over the split bits and per-warp running
-// counts in shared memory.  A bucket of one chunk is read once; a larger one is counted first, then placed
-// chunk by chunk.
-__global__ void __launch_bounds__(kSplitThreads, 1) k_split(SplitArgs a) {
+__global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
-    constexpr uint32_t NW = kSplitThreads / 32, SMAX = 1u << kMaxSplitBits;
-    __shared__ uint32_t wc[NW][SMAX];  // per-warp running counts -> the warp's offset inside the chunk's digit
-    __shared__ uint32_t tot[SMAX], soff[SMAX], run[SMAX], ccnt[SMAX];
+    constexpr uint32_t NW = kSplitThreads / 32;
+    __shared__ uint32_t wc[NW][1u << kMaxSplitBits];
+    __shared__ uint32_t tot[1u << kMaxSplitBits], soff[1u << kMaxSplitBits], run[1u << kMaxSplitBits];
     const uint32_t b = blockIdx.x, S = 1u << a.bs;
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
     const uint32_t sh = 32 - a.bp1 - a.bs, smask = S - 1u;
-    auto digit_of = [&](uint32_t v) { return (hash_vertex(v) >> sh) & smask; };
-    if (threadIdx.x < SMAX) {
+    if (threadIdx.x < S) {
         tot[threadIdx.x] = 0;
         run[threadIdx.x] = 0;
     }
-    if (n == 0) {  // an empty bucket: its sub-buckets are empty too (their starts must still be written)
-        if (threadIdx.x < S) a.vstart2[(b << a.bs) + threadIdx.x] = base;
-        if (threadIdx.x == 0 && b == gridDim.x - 1) a.vstart2[gridDim.x << a.bs] = base;
-        return;
-    }
-    const bool one_chunk = n <= kSplitChunk;
-    if (!one_chunk) {  // sub-bucket sizes of a multi-chunk bucket first
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n + ((32 - n % 32) % 32); i += kSplitThreads) {
-            const bool valid = i < n;
-            const uint32_t d = valid ? digit_of(a.arcs[base + i].x) : 0u;
-            for (uint32_t x = 0; x < S; ++x) {
-                const uint32_t c = __popc(__ballot_sync(kFull, valid && d == x));
-                if (lane == 0 && c) atomicAdd(&tot[x], c);
-            }
+    __syncthreads();
+    // pass A: sub-bucket sizes
+    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
+        const uint32_t i = q0 + threadIdx.x;
+        const bool valid = i < n;
+        const uint32_t sb = valid ? (hash_vertex(a.arcs[base + i].x) >> sh) & smask : 0u;
+        for (uint32_t x = 0; x < S; ++x) {
+            const uint32_t c = __popc(__ballot_sync(kFull, valid && sb == x));
+            if (lane == 0 && c) atomicAdd(&tot[x], c);
         }
     }
-    for (uint32_t c0 = 0; c0 < n; c0 += kSplitChunk) {
-        uint4 x4[kSplitItems];
-        uint32_t pk[kSplitItems];  // digit << 16 | rank inside the warp's items of that digit (0xFFFFFFFF: none)
-        if (threadIdx.x < SMAX)
-            for (uint32_t w2 = 0; w2 < NW; ++w2) wc[w2][threadIdx.x] = 0;
-        __syncthreads();
-#pragma unroll
-        for (uint32_t j = 0; j < kSplitItems; ++j) {
-            const uint32_t i = c0 + warp * 32u * kSplitItems + j * 32u + lane;
-            const bool valid = i < n;
-            x4[j] = valid ? a.arcs[base + i] : make_uint4(0u, 0u, 0u, 0u);
-            const uint32_t d = valid ? digit_of(x4[j].x) : 0u;
-            const uint32_t peers = digit_peers(d, valid, a.bs);
-            const uint32_t before = __popc(peers & lt);
-            uint32_t c = 0;
-            if (valid) c = wc[warp][d];
-            __syncwarp();
-            if (valid && before == 0) wc[warp][d] = c + __popc(peers);
-            __syncwarp();
-            pk[j] = valid ? (d << 16) | (c + before) : 0xFFFFFFFFu;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t r = 0;
+        for (uint32_t x = 0; x < S; ++x) {
+            soff[x] = r;
+            a.vstart2[(b << a.bs) + x] = base + r;
+            if (tot[x] > a.vcap) a.vperm[atomicAdd(&a.ctr[kCtrBig], 1u)] = (b << a.bs) + x;
+            r += tot[x];
+        }
+        if (b == gridDim.x - 1) a.vstart2[gridDim.x << a.bs] = base + n;
+    }
+    __syncthreads();
+    // pass B: stable ranks chunk by chunk (chunk order, then warp order, then lane order = arrival order)
+    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
+        const uint32_t i = q0 + threadIdx.x;
+        const bool valid = i < n;
+        uint4 x4 = make_uint4(0u, 0u, 0u, 0u);
+        if (valid) x4 = a.arcs[base + i];
+        const uint32_t sb = valid ? (hash_vertex(x4.x) >> sh) & smask : 0u;
+        uint32_t mine = 0;
+        for (uint32_t x = 0; x < S; ++x) {
+            const uint32_t m = __ballot_sync(kFull, valid && sb == x);
+            if (lane == 0) wc[warp][x] = __popc(m);
+            if (sb == x) mine = __popc(m & lt);
         }
         __syncthreads();
-        if (threadIdx.x < S) {  // per digit: exclusive prefix over warps; this chunk's count
+        if (threadIdx.x < S) {  // per sub-bucket: exclusive prefix over warps
             uint32_t r = 0;
             for (uint32_t w2 = 0; w2 < NW; ++w2) {
                 const uint32_t c = wc[w2][threadIdx.x];
                 wc[w2][threadIdx.x] = r;
                 r += c;
             }
-            if (one_chunk) tot[threadIdx.x] = r;
-            else ccnt[threadIdx.x] = r;
+            tot[threadIdx.x] = r;  // this chunk's count
         }
         __syncthreads();
-        if (c0 == 0 && threadIdx.x == 0) {  // sub-bucket starts (and the large ones for k_vhub)
-            uint32_t r = 0;
-            for (uint32_t x = 0; x < S; ++x) {
-                soff[x] = r;
-                a.vstart2[(b << a.bs) + x] = base + r;
-                if (tot[x] > a.vcap) a.vperm[atomicAdd(&a.ctr[kCtrBig], 1u)] = (b << a.bs) + x;
-                r += tot[x];
-            }
-            if (b == gridDim.x - 1) a.vstart2[gridDim.x << a.bs] = base + n;
-        }
+        TC_CHECK(!valid || soff[sb] + run[sb] + wc[warp][sb] + mine < n, a.ctr);
+        if (valid) a.arcs2[base + soff[sb] + run[sb] + wc[warp][sb] + mine] = x4;
         __syncthreads();
-#pragma unroll
-        for (uint32_t j = 0; j < kSplitItems; ++j) {
-            if (pk[j] == 0xFFFFFFFFu) continue;
-            const uint32_t d = pk[j] >> 16;
-            const uint32_t dst = soff[d] + run[d] + wc[warp][d] + (pk[j] & 0xFFFFu);
-            TC_CHECK(dst < n, a.ctr);
-            a.arcs2[base + dst] = x4[j];
-        }
+        if (threadIdx.x < S) run[threadIdx.x] += tot[threadIdx.x];
         __syncthreads();
-        if (!one_chunk && threadIdx.x < S) run[threadIdx.x] += ccnt[threadIdx.x];  // offsets for the next chunk
     }
 }
 
