@@ -43,11 +43,11 @@ constexpr uint32_t kErrStage = kErrInval | kErrLoop;
 constexpr uint32_t kTileEdges = TC_TILE_EDGES;  // edges per count/scatter tile
 constexpr uint32_t kTileThreads = 512;
 #ifndef TC_PART_BITS
-#define TC_PART_BITS 12
+#define TC_PART_BITS 11  // 12 measured 5 % slower at C3: k_count's per-warp counters need 128 KB (1 CTA/SM)
 #endif
 constexpr uint32_t kMaxBucketBits = 15;   // at most 2^15 vertex buckets
-constexpr uint32_t kMaxPartBits = TC_PART_BITS;  // the partition kernels: at most 2^12 vertex buckets
-constexpr uint32_t kMaxSplitBits = kMaxBucketBits - kMaxPartBits;  // k_split: each into at most 2^3 sub-buckets
+constexpr uint32_t kMaxPartBits = TC_PART_BITS;  // the partition kernels: at most 2^11 vertex buckets
+constexpr uint32_t kMaxSplitBits = kMaxBucketBits - kMaxPartBits;  // k_split: each into at most 2^4 sub-buckets
 constexpr uint32_t kVBucketThreads = 256; // vertex-bucket CTA
 constexpr uint32_t kVItems = 24;          // arcs per thread held in registers by the vertex-bucket sort
 constexpr uint32_t kVChunk = kVBucketThreads * kVItems;  // 6144 arcs: larger buckets take the chunked path

@@ -419,15 +419,13 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
         run[threadIdx.x] = 0;
     }
     __syncthreads();
-    // pass A: sub-bucket sizes
+    // pass A: sub-bucket sizes (the lanes of each sub-bucket value found with bs ballots; its first lane adds)
     for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
         const uint32_t i = q0 + threadIdx.x;
         const bool valid = i < n;
         const uint32_t sb = valid ? (hash_vertex(a.arcs[base + i].x) >> sh) & smask : 0u;
-        for (uint32_t x = 0; x < S; ++x) {
-            const uint32_t c = __popc(__ballot_sync(kFull, valid && sb == x));
-            if (lane == 0 && c) atomicAdd(&tot[x], c);
-        }
+        const uint32_t peers = digit_peers(sb, valid, a.bs);
+        if (valid && (peers & lt) == 0) atomicAdd(&tot[sb], __popc(peers));
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -448,12 +446,11 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
         uint4 x4 = make_uint4(0u, 0u, 0u, 0u);
         if (valid) x4 = a.arcs[base + i];
         const uint32_t sb = valid ? (hash_vertex(x4.x) >> sh) & smask : 0u;
-        uint32_t mine = 0;
-        for (uint32_t x = 0; x < S; ++x) {
-            const uint32_t m = __ballot_sync(kFull, valid && sb == x);
-            if (lane == 0) wc[warp][x] = __popc(m);
-            if (sb == x) mine = __popc(m & lt);
-        }
+        const uint32_t peers = digit_peers(sb, valid, a.bs);  // lanes with my sub-bucket value (bs ballots)
+        const uint32_t mine = __popc(peers & lt);
+        if (lane < S) wc[warp][lane] = 0u;
+        __syncwarp();
+        if (valid && mine == 0) wc[warp][sb] = __popc(peers);
         __syncthreads();
         if (threadIdx.x < S) {  // per sub-bucket: exclusive prefix over warps
             uint32_t r = 0;
