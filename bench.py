@@ -359,6 +359,12 @@ def run_b200(args):
                 torch.distributed.all_gather_object(per_rank, {k: v["ms_per_launch"] for k, v in rows.items()})
             ncu = committed_ncu(args.config)
             traffic = (ncu.get("kernels", {}).get(dom) or {}).get("dram_bytes_per_launch")
+            for name, row in rows.items():  # the pipeline's own DRAM bytes per launch (ncu), as a rate
+                t_ = (ncu.get("kernels", {}).get(name) or {}).get("dram_bytes_per_launch")
+                if t_:
+                    row["dram_bytes_per_launch_ncu"] = t_
+                    row["dram_GBps"] = t_ / (row["ms_per_launch"] / 1e3) / 1e9
+                    row["dram_frac"] = row["dram_GBps"] / peak
             D_avg = stats["vertices"] / nsteps
             B_step = (40 * prof_edges + 16 * stats["vertices"]) / nsteps + \
                 kernel_bytes("k_update", prof_edges, stats, R_total) / nsteps
@@ -369,6 +375,10 @@ def run_b200(args):
                 "frac": rows[dom].get("frac"), "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": rows[dom]["algorithmic_bytes_per_launch"],
                 "launch_ms": rows[dom]["ms_per_launch"],
+                "dram_frac": rows[dom].get("dram_frac"),
+                "dram_frac_note": "traffic (ncu pipeline capture, DRAM bytes actually moved per launch) / this run's "
+                                  "launch time / peak: how close the kernel is to HBM on the accesses it makes "
+                                  "(random 8-32 B probes cost a 32-64 B DRAM access each)",
                 "byte_model": "SURVEY 8(d): Ke 16w (k_count) + 16w (k_scatter); Ki 8 B/arc + 16 B/vertex; "
                               "Kp 24w; Ku 24 B/estimator + 16 B per replaced r1 + 16 B per replaced r2",
                 "kernels": rows,
