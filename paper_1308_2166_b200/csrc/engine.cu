@@ -593,7 +593,7 @@ static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx
     e.key = key;
     e.last_use = ++ctx->graph_clock;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    launch_desc(ctx->ix, d, ctx->stream);
+    launch_desc(ctx->ix, a, d, ctx->stream);
     bool ok = true;
     e.launches = 1 + enqueue_kernels(ctx, a, KRec(), &ok);
     const bool cap = cudaStreamEndCapture(ctx->stream, &e.graph) == cudaSuccess && e.graph;
@@ -656,11 +656,14 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
         const int rc = graph_for(ctx, a, d, &ge);
         if (rc != TC_OK) return rc;
         BatchDesc *dst = ix.desc;
-        void *args[] = {&d, &dst};
+        uint32_t *ctr = ix.ctr;
+        unsigned long long *S = a.S;
+        uint32_t *filt = a.small ? ix.filt : nullptr;
+        void *args[] = {&d, &dst, &ctr, &S, &filt};
         cudaKernelNodeParams kp{};
         kp.func = const_cast<void *>(desc_kernel());
         kp.gridDim = dim3(1);
-        kp.blockDim = dim3(1);
+        kp.blockDim = dim3(256);
         kp.kernelParams = args;
         CK(cudaGraphExecKernelNodeSetParams(ge->exec, ge->desc_node, &kp));
         CK(cudaGraphLaunch(ge->exec, ctx->stream));
@@ -672,7 +675,7 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
             ctx->ev_kused[ctx->ev_used] = 0u;
             kr.used = &ctx->ev_kused[ctx->ev_used];
         }
-        launch_desc(ix, d, ctx->stream);
+        launch_desc(ix, a, d, ctx->stream);
         bool ok = true;
         launches = 1 + enqueue_kernels(ctx, a, kr, &ok);
         if (ctx->prof)

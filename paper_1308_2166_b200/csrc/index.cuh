@@ -62,6 +62,7 @@ constexpr int kCtrTicket2 = 5; // k_vbig's bucket ticket
 constexpr int kCtrFailB = 6;   // batch index of the first batch that found the error word set (async mode)
 constexpr int kCtrArcsBig = 7; // arcs grouped by the large-bucket kernels (k_vhub / k_vbig)
 constexpr int kCtrDBig = 8;    // distinct vertices of those buckets
+constexpr int kCtrCursor = 9;  // k_small_index: next free segment slot (each bucket CTA takes its range)
 constexpr int kCtrWords = 16;
 
 // Per-batch values the kernels read from device memory (written by k_desc, the first node of every push), so

@@ -902,6 +902,9 @@ struct ArcSrc {
         }
         return make_uint3(sv[i], sval[i], snb[i]);
     }
+    // the arc's partition position (pslot index): carried in .w by the partitioned build; the shared-memory
+    // lists belong to k_small_index, where it is the arc id itself
+    __device__ __forceinline__ uint32_t pre(uint32_t i) const { return g ? g[i].w : sval[i]; }
 };
 
 // Hash-path grouping of n arcs (src) of bucket b whose segments start at slot base + off0; `hub` (if
@@ -1027,8 +1030,9 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         a.segS[b0 + pos] = make_uint2(val[j], nbv[j]);
         // by the arc's partition position: this bucket's own range, so the writes fill whole sectors in L2
         const uint32_t i = warp * 32u * R + j * 32u + lane;
-        TC_CHECK(src.g[i].w < a.narcs, a.ctr);
-        a.pslot[src.g[i].w] = make_uint2(b0 + pos, b0 + segst[l + 1]);
+        const uint32_t pre = src.pre(i);
+        TC_CHECK(pre < a.narcs, a.ctr);
+        a.pslot[pre] = make_uint2(b0 + pos, b0 + segst[l + 1]);
     }
     // phase 5: the vertex-table slice, built in shared memory (over whist) and written whole; the hub (if
     // any) is entry D
@@ -1232,41 +1236,42 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------------
-// a1..a3 for small batches (w <= kSmallIndexMax): ONE CTA builds the whole index -- validation, E, the arcs,
-// the edge-pair table (and the small-batch vertex filter), then all 2w arcs as a single vertex bucket through
-// the hash path -- instead of the eight launches of the partitioned build, whose fixed latency dominates small
-// batches.  Same tables, same lookups (the vertex table is one slice: bucket bits bv = 0).
-__global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, VertArgs v) {
-    extern __shared__ __align__(16) unsigned char hsm[];
-    __shared__ uint32_t ws[kHubWarps + 1];
-    __shared__ uint32_t sD;
-    if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
-        a.ctr[threadIdx.x] = 0u;
-    if (threadIdx.x == 0) a.S[a.d->slot] = 0ull;
-    if (a.filt)
-        for (uint32_t i = threadIdx.x; i < kFilterWords; i += blockDim.x) a.filt[i] = 0u;
-    const bool sticky = (a.ctr[kCtrErr] & kErrStage) != 0;  // an earlier asynchronous batch failed
-    __syncthreads();
-    if (sticky) return;
+// a1..a3 for small batches (w <= kSmallIndexMax): ONE kernel instead of the partitioned build's eight launches,
+// whose fixed latency dominates small batches.  CTA b of 2^bv: validates the whole batch (it is small), writes
+// E / apos / the edge-pair table for its slice of the edges, compacts the arcs of vertex bucket b in arrival
+// order into shared memory (a block-wide stable prefix), takes its segment range with one atomic, and groups
+// them through the hash path.  Same tables and lookups as the partitioned build (a bucket's partition position
+// of an arc is its arc id here).  The per-batch counter resets are done by k_desc, ahead of every CTA.
+constexpr uint32_t kSmallThreads = 256;
+constexpr uint32_t kSmallCap = 2 * kSmallIndexMax;  // a bucket may hold every arc of the batch
+constexpr uint32_t kSmallHashBytes = HL<kSmallCap, kSmallThreads>::BYTES;
+constexpr uint32_t kSmallSmemBytes = kSmallHashBytes + 3 * kSmallCap * 4;
+
+__global__ void __launch_bounds__(kSmallThreads) k_small_index(PartArgs a, VertArgs v) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint32_t *sv = reinterpret_cast<uint32_t *>(smem + kSmallHashBytes), *sval = sv + kSmallCap, *snb = sval + kSmallCap;
+    __shared__ uint32_t ws[kSmallThreads / 32 + 1];
+    __shared__ uint32_t sD, s_base, s_cnt;
+    if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier asynchronous batch
     const uint2 *in = a.d->in;
-    const uint32_t ptag = a.d->ptag, w = a.g.w;
-    // validation and normalisation first: a rejected batch must not insert anything
+    const uint32_t ptag = a.d->ptag, w = a.g.w, b = blockIdx.x, bv = a.g.bv, NB = gridDim.x;
+    const uint32_t lane = threadIdx.x & 31u;
+    // validation first (every CTA, the batch is small): a rejected batch must not insert anything
     uint32_t bad = 0;
-    for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
+    for (uint32_t k = threadIdx.x; k < w; k += kSmallThreads) {
         const uint2 e = __ldg(in + k);
         if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
         else if (e.x == e.y) bad |= kErrLoop;
     }
     bad = __reduce_or_sync(kFull, bad);
-    if (bad && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], bad);
+    if (bad && lane == 0) atomicOr(&a.ctr[kCtrErr], bad);
     if (__syncthreads_or(bad != 0)) return;
+    // this CTA's slice of the edges: E, partition positions (= arc ids), pair table, small-batch filter
     bool dup = false;
-    for (uint32_t k = threadIdx.x; k < w; k += blockDim.x) {
+    for (uint32_t k = (uint32_t)((uint64_t)b * w / NB) + threadIdx.x, k1 = (uint32_t)((uint64_t)(b + 1) * w / NB);
+         k < k1; k += kSmallThreads) {
         const uint2 n = norm_edge(__ldg(in + k));
         a.E[k] = n;
-        // one bucket: an arc's partition position is its arc id
-        v.arcs[2 * k] = make_uint4(n.x, 2 * k, n.y, 2 * k);
-        v.arcs[2 * k + 1] = make_uint4(n.y, 2 * k + 1, n.x, 2 * k + 1);
         a.apos2[2 * k] = 2 * k;
         a.apos2[2 * k + 1] = 2 * k + 1;
         dup |= pt_insert(a, in, ptag, n, k);
@@ -1276,12 +1281,40 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_small_index(PartArgs a, Vert
             atomicOr(a.filt + (b1 >> 5), 1u << (b1 & 31u));
         }
     }
-    if (__any_sync(kFull, dup) && (threadIdx.x & 31u) == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
-    __syncthreads();  // the arcs this CTA wrote are visible to all its threads
-    const uint32_t n = 2 * w;
-    const ArcSrc src{v.arcs, nullptr, nullptr, nullptr};
-    hash_dispatch<kHubCap, kHubThreads>(n, [&](auto r) {
-        vbucket_hash<decltype(r)::value, kHubCap, kHubThreads>(v, 0u, 0u, src, n, 0u, 0u, 0u, hsm, ws, &sD);
+    if (__any_sync(kFull, dup) && lane == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
+    // bucket b's arcs in arrival order (arc a = 2k + side), compacted by a block-wide stable prefix
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (uint32_t a0 = 0; a0 < 2 * w; a0 += kSmallThreads) {
+        const uint32_t ai = a0 + threadIdx.x;
+        uint32_t vx = 0, nb = 0;
+        bool mine = false;
+        if (ai < 2 * w) {
+            const uint2 n = norm_edge(__ldg(in + (ai >> 1)));
+            vx = (ai & 1u) ? n.y : n.x;
+            nb = (ai & 1u) ? n.x : n.y;
+            mine = vbucket_of(hash_vertex(vx), bv) == b;
+        }
+        uint32_t tot;
+        const uint32_t pre = block_exclusive_scan<kSmallThreads>(mine ? 1u : 0u, ws, &tot);
+        if (mine) {
+            const uint32_t q = s_cnt + pre;
+            sv[q] = vx;
+            sval[q] = ai;
+            snb[q] = nb;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_cnt += tot;
+    }
+    __syncthreads();
+    const uint32_t n = s_cnt;
+    if (threadIdx.x == 0) s_base = atomicAdd(&a.ctr[kCtrCursor], n);  // segments: any bucket order will do
+    __syncthreads();
+    const uint32_t base = s_base;
+    TC_CHECK(n <= kSmallCap && base + n <= 2 * w, a.ctr);
+    const ArcSrc src{nullptr, sv, sval, snb};
+    hash_dispatch<kSmallCap, kSmallThreads>(n, [&](auto r) {
+        vbucket_hash<decltype(r)::value, kSmallCap, kSmallThreads>(v, b, base, src, n, 0u, 0u, 0u, smem, ws, &sD);
     });
 }
 
@@ -1731,11 +1764,23 @@ __global__ void k_group_sums(const uint32_t *__restrict__ cf, uint64_t count, ui
     }
 }
 
-// The first node of every push: the batch's descriptor into device memory.
-__global__ void k_desc(BatchDesc d, BatchDesc *dst) { *dst = d; }
+// The first node of every push: the batch's descriptor into device memory, and the per-batch resets (the
+// counters except the sticky error word and the failed-batch index, this batch's S, the small-batch filter)
+// ahead of every kernel of the batch.
+__global__ void __launch_bounds__(256) k_desc(BatchDesc d, BatchDesc *dst, uint32_t *ctr, unsigned long long *S,
+                                              uint32_t *filt) {
+    if (threadIdx.x == 0) {
+        *dst = d;
+        S[d.slot] = 0ull;
+    }
+    if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
+        ctr[threadIdx.x] = 0u;
+    if (filt)
+        for (uint32_t i = threadIdx.x; i < kFilterWords; i += blockDim.x) filt[i] = 0u;
+}
 
-int launch_desc(const IndexBufs &ix, const BatchDesc &d, cudaStream_t s) {
-    k_desc<<<1, 1, 0, s>>>(d, ix.desc);
+int launch_desc(const IndexBufs &ix, const BatchArgs &a, const BatchDesc &d, cudaStream_t s) {
+    k_desc<<<1, 256, 0, s>>>(d, ix.desc, ix.ctr, a.S, a.small ? ix.filt : nullptr);
     return 1;
 }
 
@@ -1808,7 +1853,10 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
     g.bs = g.bv - g.bp1;
     g.vcap = std::min(t.vcap, kHCapSmall);
     g.sortcap = std::min(t.sortcap, kVChunk);
-    if (g.small_index) g.bv = g.bp1 = g.bs = 0;  // the whole batch is one vertex bucket
+    if (g.small_index) {  // one CTA per vertex bucket of ~512 arcs, at most 16 (no partition kernels)
+        g.bv = std::min<uint32_t>(4, ceil_log2((2ull * w + 511) / 512));
+        g.bp1 = g.bs = 0;
+    }
     return g;
 }
 
@@ -1851,7 +1899,6 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, co
 }
 
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
-    if (a.small && cudaMemsetAsync(ix.filt, 0, 4ull * kFilterWords, s) != cudaSuccess) return 0;
     kr.beg(K_PAIRS, s);
     k_pairs<<<(a.g.w + 255) / 256, 256, 0, s>>>(part_args(ix, a));
     kr.end(K_PAIRS, s);
@@ -1866,7 +1913,7 @@ static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
 
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     kr.beg(K_SMALL, s);
-    k_small_index<<<1, kHubThreads, kVHubSmemBytes, s>>>(part_args(ix, a), vert_args(ix, a));
+    k_small_index<<<1u << a.g.bv, kSmallThreads, kSmallSmemBytes, s>>>(part_args(ix, a), vert_args(ix, a));
     kr.end(K_SMALL, s);
     return 1;
 }
@@ -1944,7 +1991,7 @@ int set_kernel_attributes() {
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
     if (e1 == cudaSuccess)
-        e1 = cudaFuncSetAttribute(k_small_index, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
+        e1 = cudaFuncSetAttribute(k_small_index, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSmemBytes);
     cudaError_t e2 = cudaSuccess;
     const void *counts[] = {(const void *)k_count<0>, (const void *)k_count<1>, (const void *)k_count<2>,
                             (const void *)k_count<3>, (const void *)k_count<4>, (const void *)k_count<5>,

@@ -134,7 +134,7 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr = KRec());
 
-int launch_desc(const IndexBufs &ix, const BatchDesc &d, cudaStream_t s);  // the push's first node
+int launch_desc(const IndexBufs &ix, const BatchArgs &a, const BatchDesc &d, cudaStream_t s);  // the push's first node
 const void *desc_kernel();                                                  // its function (graph node lookup)
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
