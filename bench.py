@@ -360,10 +360,11 @@ def run_b200(args):
             ncu = committed_ncu(args.config)
             traffic = (ncu.get("kernels", {}).get(dom) or {}).get("dram_bytes_per_launch")
             for name, row in rows.items():  # the pipeline's own DRAM bytes per launch (ncu), as a rate
-                t_ = (ncu.get("kernels", {}).get(name) or {}).get("dram_bytes_per_launch")
-                if t_:
+                kn = ncu.get("kernels", {}).get(name) or {}
+                t_, d_ = kn.get("dram_bytes_per_launch"), kn.get("duration_us")
+                if t_ and d_:  # bytes and time from the same capture (ncu serialises the kernels)
                     row["dram_bytes_per_launch_ncu"] = t_
-                    row["dram_GBps"] = t_ / (row["ms_per_launch"] / 1e3) / 1e9
+                    row["dram_GBps"] = t_ / (d_ / 1e6) / 1e9
                     row["dram_frac"] = row["dram_GBps"] / peak
             D_avg = stats["vertices"] / nsteps
             B_step = (40 * prof_edges + 16 * stats["vertices"]) / nsteps + \
@@ -376,9 +377,10 @@ def run_b200(args):
                 "algorithmic_bytes_per_launch": rows[dom]["algorithmic_bytes_per_launch"],
                 "launch_ms": rows[dom]["ms_per_launch"],
                 "dram_frac": rows[dom].get("dram_frac"),
-                "dram_frac_note": "traffic (ncu pipeline capture, DRAM bytes actually moved per launch) / this run's "
-                                  "launch time / peak: how close the kernel is to HBM on the accesses it makes "
-                                  "(random 8-32 B probes cost a 32-64 B DRAM access each)",
+                "dram_frac_note": "traffic / duration, both from the ncu pipeline capture (DRAM bytes the kernel "
+                                  "actually moves, application replay without cache control), over peak: how close "
+                                  "the kernel is to HBM on the accesses it makes (random 8-32 B probes cost a 32-64 B "
+                                  "DRAM access each)",
                 "byte_model": "SURVEY 8(d): Ke 16w (k_count) + 16w (k_scatter); Ki 8 B/arc + 16 B/vertex; "
                               "Kp 24w; Ku 24 B/estimator + 16 B per replaced r1 + 16 B per replaced r2",
                 "kernels": rows,

@@ -248,9 +248,9 @@ int tc_graph_captures(tc_ctx *ctx, uint64_t *captures);
  *                        a7), k_r_reduce (aggregation, a8) -- instead of the fused k_update, keeping every step's
  *                        values per estimator (tc_get_steps) for per-step parity and per-step timing; 0 (default):
  *                        fused.  The states are identical either way.
- *  TC_TUNE_SMALL_INDEX   batches of at most 2048 edges build the whole index in ONE kernel (one CTA: validation,
- *                        pair table, grouping of all 2w arcs as a single vertex bucket) instead of the eight
- *                        launches of the partitioned build: 0 = auto (default), 1 = never, 2 = always (same).
+ *  TC_TUNE_SMALL_INDEX   batches of at most 4096 edges build the whole index in ONE kernel (one CTA per vertex
+ *                        bucket of ~512 arcs: validation, pair table, grouping) instead of the eight launches of
+ *                        the partitioned build: 0 = auto (default), 1 = never, 2 = always (same).
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
 enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6,
        TC_TUNE_SPLIT_KERNELS = 8, TC_TUNE_SMALL_INDEX = 10 };

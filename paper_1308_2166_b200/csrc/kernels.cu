@@ -1242,12 +1242,17 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
 // order into shared memory (a block-wide stable prefix), takes its segment range with one atomic, and groups
 // them through the hash path.  Same tables and lookups as the partitioned build (a bucket's partition position
 // of an arc is its arc id here).  The per-batch counter resets are done by k_desc, ahead of every CTA.
-constexpr uint32_t kSmallThreads = 256;
-constexpr uint32_t kSmallCap = 2 * kSmallIndexMax;  // a bucket may hold every arc of the batch
-constexpr uint32_t kSmallHashBytes = HL<kSmallCap, kSmallThreads>::BYTES;
-constexpr uint32_t kSmallSmemBytes = kSmallHashBytes + 3 * kSmallCap * 4;
+// Two instances: <256 threads, 4096-arc buckets> up to w = 2048, <512, 8192> up to w = 4096 (a bucket may hold
+// every arc of the batch).
+template <int kSmallThreads, uint32_t kSmallCap>
+struct SmallIndexCfg {
+    static constexpr uint32_t kHashBytes = HL<kSmallCap, kSmallThreads>::BYTES;
+    static constexpr uint32_t kSmemBytes = kHashBytes + 3 * kSmallCap * 4;
+};
 
+template <int kSmallThreads, uint32_t kSmallCap>
 __global__ void __launch_bounds__(kSmallThreads) k_small_index(PartArgs a, VertArgs v) {
+    constexpr uint32_t kSmallHashBytes = SmallIndexCfg<kSmallThreads, kSmallCap>::kHashBytes;
     extern __shared__ __align__(16) unsigned char smem[];
     uint32_t *sv = reinterpret_cast<uint32_t *>(smem + kSmallHashBytes), *sval = sv + kSmallCap, *snb = sval + kSmallCap;
     __shared__ uint32_t ws[kSmallThreads / 32 + 1];
@@ -1282,30 +1287,42 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_index(PartArgs a, VertA
         }
     }
     if (__any_sync(kFull, dup) && lane == 0) atomicOr(&a.ctr[kCtrErr], kErrDup);
-    // bucket b's arcs in arrival order (arc a = 2k + side), compacted by a block-wide stable prefix
-    if (threadIdx.x == 0) s_cnt = 0;
-    __syncthreads();
-    for (uint32_t a0 = 0; a0 < 2 * w; a0 += kSmallThreads) {
-        const uint32_t ai = a0 + threadIdx.x;
+    // bucket b's arcs in arrival order (arc a = 2k + side), compacted stably: warp w owns the contiguous arcs
+    // [w C, (w+1) C); it counts its matches with ballots, one block scan turns the counts into offsets, and a
+    // second sweep (the batch is in L1/L2 by now) writes them
+    constexpr uint32_t NWS = kSmallThreads / 32;
+    const uint32_t warp = threadIdx.x >> 5, C = (2 * w + NWS - 1) / NWS;
+    const uint32_t c0 = min(2 * w, warp * C), c1 = min(2 * w, c0 + C);
+    auto arc_at = [&](uint32_t ai, uint32_t &vx, uint32_t &nb) {
+        const uint2 n = norm_edge(__ldg(in + (ai >> 1)));
+        vx = (ai & 1u) ? n.y : n.x;
+        nb = (ai & 1u) ? n.x : n.y;
+        return vbucket_of(hash_vertex(vx), bv) == b;
+    };
+    uint32_t cnt = 0;
+    for (uint32_t ai0 = c0; ai0 < c1; ai0 += 32) {
+        const uint32_t ai = ai0 + lane;
+        uint32_t vx, nb;
+        cnt += __popc(__ballot_sync(kFull, ai < c1 && arc_at(ai, vx, nb)));
+    }
+    uint32_t tot;
+    const uint32_t wpre = block_exclusive_scan<kSmallThreads>(lane == 0 ? cnt : 0u, ws, &tot);
+    const uint32_t woff = __shfl_sync(kFull, wpre, 0);
+    uint32_t run = 0;
+    for (uint32_t ai0 = c0; ai0 < c1; ai0 += 32) {
+        const uint32_t ai = ai0 + lane;
         uint32_t vx = 0, nb = 0;
-        bool mine = false;
-        if (ai < 2 * w) {
-            const uint2 n = norm_edge(__ldg(in + (ai >> 1)));
-            vx = (ai & 1u) ? n.y : n.x;
-            nb = (ai & 1u) ? n.x : n.y;
-            mine = vbucket_of(hash_vertex(vx), bv) == b;
-        }
-        uint32_t tot;
-        const uint32_t pre = block_exclusive_scan<kSmallThreads>(mine ? 1u : 0u, ws, &tot);
+        const bool mine = ai < c1 && arc_at(ai, vx, nb);
+        const uint32_t m = __ballot_sync(kFull, mine);
         if (mine) {
-            const uint32_t q = s_cnt + pre;
+            const uint32_t q = woff + run + __popc(m & ((1u << lane) - 1u));
             sv[q] = vx;
             sval[q] = ai;
             snb[q] = nb;
         }
-        __syncthreads();
-        if (threadIdx.x == 0) s_cnt += tot;
+        run += __popc(m);
     }
+    if (threadIdx.x == 0) s_cnt = tot;
     __syncthreads();
     const uint32_t n = s_cnt;
     if (threadIdx.x == 0) s_base = atomicAdd(&a.ctr[kCtrCursor], n);  // segments: any bucket order will do
@@ -1913,7 +1930,12 @@ static VertArgs vert_args(const IndexBufs &ix, const BatchArgs &a) {
 
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     kr.beg(K_SMALL, s);
-    k_small_index<<<1u << a.g.bv, kSmallThreads, kSmallSmemBytes, s>>>(part_args(ix, a), vert_args(ix, a));
+    if (a.g.w <= 2048)
+        k_small_index<256, 4096><<<1u << a.g.bv, 256, SmallIndexCfg<256, 4096>::kSmemBytes, s>>>(part_args(ix, a),
+                                                                                             vert_args(ix, a));
+    else
+        k_small_index<512, 8192><<<1u << a.g.bv, 512, SmallIndexCfg<512, 8192>::kSmemBytes, s>>>(part_args(ix, a),
+                                                                                             vert_args(ix, a));
     kr.end(K_SMALL, s);
     return 1;
 }
@@ -1991,7 +2013,11 @@ int set_kernel_attributes() {
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
     if (e1 == cudaSuccess)
-        e1 = cudaFuncSetAttribute(k_small_index, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmallSmemBytes);
+        e1 = cudaFuncSetAttribute(k_small_index<256, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SmallIndexCfg<256, 4096>::kSmemBytes);
+    if (e1 == cudaSuccess)
+        e1 = cudaFuncSetAttribute(k_small_index<512, 8192>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  SmallIndexCfg<512, 8192>::kSmemBytes);
     cudaError_t e2 = cudaSuccess;
     const void *counts[] = {(const void *)k_count<0>, (const void *)k_count<1>, (const void *)k_count<2>,
                             (const void *)k_count<3>, (const void *)k_count<4>, (const void *)k_count<5>,

@@ -75,8 +75,8 @@ struct Geometry {
     bool small_index;  // the whole index by one CTA (k_small_index; w <= kSmallIndexMax)
 };
 
-constexpr uint32_t kSmallIndexMax = 2048;  // one CTA: measured faster than the partitioned build up to 2048 edges
-                                           // (C1: 39 us vs ~55), slower at 4096 (100 us vs ~65); hash path cap 8192
+constexpr uint32_t kSmallIndexMax = 4096;  // k_small_index: one CTA per vertex bucket of ~512 arcs (a bucket may
+                                           // hold all 2 w arcs: hash path caps 4096 / 8192 at 256 / 512 threads)
 
 // Launch-time values of a push.  The per-batch values (input pointer, m, batch index, pair tag, S slot) are
 // NOT here: the kernels read them from the device descriptor (BatchDesc), so a captured graph of the launch
