@@ -1781,107 +1781,6 @@ __global__ void __launch_bounds__(256) k_r_reduce(UpdateArgs u, StepBufs sb, uns
     }
 }
 
-// The small-batch estimator pass (a.small).  Per CTA round of 1024 estimators: phase 1 streams their state,
-// draws Step 1 and tests f1's endpoints against the batch's vertex filter; only the estimators the batch can
-// change (a fresh f1, or an endpoint in the batch) are queued in shared memory with the state already loaded;
-// phase 2 runs Steps 2-3 over the queue with full warps.  (The filtered pass of round 1 skipped untouched lanes
-// inside the warp, so with hubs touching ~1/3 of the estimators almost every warp still ran the full path.)
-constexpr uint32_t kQThreads = 256, kQPer = 4, kQChunk = kQThreads * kQPer;
-constexpr uint32_t kQSmemBytes = 4 * kFilterWords + kQChunk * (8 + 8 + 8 + 8 + 4 + 4);
-
-__global__ void __launch_bounds__(kQThreads, 3) k_update_small(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
-                                                              unsigned long long *stats, const uint32_t *filt) {
-    with_desc(u, ix.L);
-    S += u.d->slot;
-    if (ix.ctr[kCtrErr]) {  // as k_update: record the batch that first saw the sticky error word
-        if (blockIdx.x == 0 && threadIdx.x == 0 && ix.ctr[kCtrFailB] == 0xFFFFFFFFu) ix.ctr[kCtrFailB] = u.batch;
-        return;
-    }
-    extern __shared__ __align__(16) unsigned char qsm[];
-    uint32_t *sf = reinterpret_cast<uint32_t *>(qsm);
-    unsigned long long *q_d1 = reinterpret_cast<unsigned long long *>(qsm + 4 * kFilterWords), *q_xhi = q_d1 + kQChunk;
-    uint2 *q_r1 = reinterpret_cast<uint2 *>(q_xhi + kQChunk), *q_r2 = q_r1 + kQChunk;
-    uint32_t *q_cf = reinterpret_cast<uint32_t *>(q_r2 + kQChunk), *q_t = q_cf + kQChunk;
-    __shared__ uint32_t qn;
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(filt);
-        for (uint32_t i = threadIdx.x; i < kFilterWords / 4; i += kQThreads) reinterpret_cast<uint4 *>(sf)[i] = __ldg(src + i);
-    }
-    const uint32_t lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
-    unsigned long long contrib = 0;
-    uint32_t n_fresh = 0, n_r2old = 0, n_skip = 0;
-    for (uint64_t c0 = (uint64_t)blockIdx.x * kQChunk; c0 < u.count; c0 += (uint64_t)gridDim.x * kQChunk) {
-        if (threadIdx.x == 0) qn = 0;
-        __syncthreads();  // (also: the filter is loaded; the previous round's queue is consumed)
-#pragma unroll
-        for (uint32_t k = 0; k < kQPer; ++k) {
-            const uint64_t t = c0 + k * kQThreads + threadIdx.x;
-            bool take = false;
-            Step1 s1{0, 0, false};
-            EstState e;
-            if (t < u.count) {
-                e.r1 = __ldcs(u.r1s + t);
-                e.cf = __ldcs(u.cfs + t);
-                e.r2 = __ldcs(u.r2s + t);
-                s1 = step1_draw(u, t);
-                take = s1.fresh || touched_by(sf, e.r1);
-                if (!take) {
-                    ++n_skip;
-                    if (e.cf & kClosedBit) contrib += e.cf & kCMask;
-                }
-            }
-            const uint32_t m = __ballot_sync(kFull, take);
-            uint32_t base = 0;
-            if (lane == 0 && m) base = atomicAdd(&qn, __popc(m));
-            base = __shfl_sync(kFull, base, 0);
-            if (take) {
-                const uint32_t q = base + __popc(m & lt);
-                q_t[q] = (uint32_t)(t - c0);
-                q_r1[q] = e.r1;
-                q_r2[q] = e.r2;
-                q_cf[q] = e.cf;
-                q_d1[q] = s1.d1;
-                q_xhi[q] = s1.xhi;
-            }
-        }
-        __syncthreads();
-        const uint32_t n = qn;
-        for (uint32_t q = threadIdx.x; q < n; q += kQThreads) {
-            EstState old;
-            old.r1 = q_r1[q];
-            old.r2 = q_r2[q];
-            old.cf = q_cf[q];
-            old.p1 = old.p2 = 0u;  // never read by the small-batch writes
-            Step1 s1;
-            s1.d1 = q_d1[q];
-            s1.xhi = q_xhi[q];
-            s1.fresh = s1.d1 >= u.m_prev;
-            contrib += update_rest<true>(u, ix, c0 + q_t[q], old, s1, n_fresh, n_r2old);
-        }
-        __syncthreads();
-    }
-    // ---- a8: partial sum of chi over closed estimators (+ event counts for the byte model) ----
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
-        contrib += __shfl_xor_sync(kFull, contrib, off);
-        n_fresh += __shfl_xor_sync(kFull, n_fresh, off);
-        n_r2old += __shfl_xor_sync(kFull, n_r2old, off);
-        n_skip += __shfl_xor_sync(kFull, n_skip, off);
-    }
-    if (lane == 0) {
-        if (contrib) atomicAdd(S, contrib);
-        if (n_fresh) atomicAdd(stats + 0, (unsigned long long)n_fresh);
-        if (n_r2old) atomicAdd(stats + 1, (unsigned long long)n_r2old);
-        if (n_skip) atomicAdd(stats + 4, (unsigned long long)n_skip);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        atomicAdd(stats + 2, (unsigned long long)ix.ctr[kCtrD]);
-        atomicAdd(stats + 3, 1ull);
-        atomicAdd(stats + 5, (unsigned long long)ix.ctr[kCtrArcsBig]);
-        atomicAdd(stats + 6, (unsigned long long)ix.ctr[kCtrDBig]);
-    }
-}
-
 __global__ void k_init_state(uint2 *r1, uint2 *r2, uint32_t *cf, uint32_t *p1, uint32_t *p2, uint64_t count) {
     for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count; t += (uint64_t)gridDim.x * blockDim.x) {
         r1[t] = make_uint2(kEmptyV, kEmptyV);
@@ -2088,7 +1987,7 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);
     if (a.small)
-        k_update_small<<<grid_for(st.count, kQChunk, 3), kQThreads, kQSmemBytes, s>>>(u, ui, st.S, st.stats, ix.filt);
+        k_update<true><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, ix.filt);
     else
         k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, nullptr);
     kr.end(K_UPDATE, s);
@@ -2136,8 +2035,7 @@ int set_kernel_attributes() {
     cudaError_t e1 = cudaFuncSetAttribute(k_vbig, cudaFuncAttributeMaxDynamicSharedMemorySize, kVSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhash, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHashSmemBytes);
     if (e1 == cudaSuccess) e1 = cudaFuncSetAttribute(k_vhub, cudaFuncAttributeMaxDynamicSharedMemorySize, kVHubSmemBytes);
-    if (e1 == cudaSuccess)
-        e1 = cudaFuncSetAttribute(k_update_small, cudaFuncAttributeMaxDynamicSharedMemorySize, kQSmemBytes);
+
     if (e1 == cudaSuccess)
         e1 = cudaFuncSetAttribute(k_small_index<256, 4096>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   SmallIndexCfg<256, 4096>::kSmemBytes);
