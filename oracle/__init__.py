@@ -22,6 +22,12 @@ Contents (each function cites the PAPER.md passage it follows):
                     OpenMP over estimators.  This is the oracle timed as the
                     CPU baseline.
 
+* ``ed``         -- the event-driven mode (reading R17): the sequential
+                    neighborhood-sampling rule per edge, with the two reservoir coins
+                    replaced by skip-sampled replacement times; exact enumeration of its outcome law.
+* ``edc``        -- ctypes front end of ``ed.c``: the same mode walked event by event per estimator
+                    (OpenMP), the GPU event mode's parity oracle at full size.
+
 The two oracles (``nbsi`` brute force, ``indexed.c`` bulk) are independent of
 each other and are required to agree bit-for-bit; both are pinned by the tests
 in ``tests/test_oracle_*.py``.
