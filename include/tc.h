@@ -256,6 +256,37 @@ enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_C
        TC_TUNE_SPLIT_KERNELS = 8, TC_TUNE_SMALL_INDEX = 10 };
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
 
+/* tc_set_mode -- the estimator update rule (reading R17, §10 row 4).
+ *  TC_MODE_BULK  (default) the paper's bulkUpdateAll (§4): every estimator takes one Step-1
+ *                draw per batch, O(r + w) work per batch.
+ *  TC_MODE_EVENT the sequential neighborhood-sampling rule (batch size 1 of bulkUpdateAll is
+ *                reservoir sampling) with skip-sampled reservoirs: each estimator draws, when
+ *                f1 (f2) is taken, the stream time J (the adjacency count K) of its next replacement, with
+ *                P(J > s) = t1/s (P(K > k) = chi/k) -- exactly the per-edge coins' law, so NBSI holds after every
+ *                batch and E[X] = tau as in the bulk mode, but the random draws differ (the two modes' states are
+ *                different samples of the same law).  A batch processes only the estimators it changes (watch
+ *                lists keyed by J, by (vertex, degree threshold) and by the closing pair; O(w + events) per
+ *                batch after the first few), and the state after a stream prefix does not depend on the batching.
+ *                chi is kept as deg(u) + deg(v) - B with persistent vertex degrees; a batch that would give a
+ *                vertex degree > 2^30 - 1 is rejected with TC_EOVERFLOW (reading R17c).  tc_set_state and
+ *                tc_set_counters return TC_EINVAL in this mode.
+ * Only on a handle that has seen no batch (fresh or after tc_reset), else TC_EINVAL.  The event mode allocates
+ * about 1 KB per estimator of watch tables (12 watch nodes, 16-byte map slots at load <= 1/2) plus 32 bytes per
+ * distinct vertex seen.  Synchronises. */
+enum { TC_MODE_BULK = 0, TC_MODE_EVENT = 1 };
+int tc_set_mode(tc_ctx *ctx, int mode);
+
+/* tc_get_event_state -- event mode: for local estimators [first, first+count), HOST arrays (any may be NULL):
+ * J = the 1-based stream time of the next f1 replacement, K = the adjacency count at which f2 is next replaced
+ * (0xFFFFFFFF: beyond 2^31 - 1, i.e. never; K = 0xFFFFFFFF also for an estimator without f1), ev = random words
+ * used.  The NBSI fields come from tc_get_state.  TC_EINVAL in the bulk mode.  Synchronises. */
+int tc_get_event_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *J, uint32_t *K, uint32_t *ev);
+
+/* tc_event_counters -- event mode, totals since the mode was set / the last reset: out[0] estimators processed,
+ * out[1] f1 and f2 replacements, out[2] full sweeps, out[3] distinct vertices seen.  Returns 4 (TC_EINVAL in the
+ * bulk mode).  Synchronises. */
+int tc_event_counters(tc_ctx *ctx, uint64_t *out, int n);
+
 /* tc_get_steps -- with TC_TUNE_SPLIT_KERNELS on: the per-step values of the last batch for local estimators
  * [first, first+count), HOST arrays (any may be NULL): j = Step 1's replacement index in W (0xFFFFFFFF: f1
  * retained), chim = chi^- after Step 1, ld / rd = rank(u->v) / rank(v->u) (chi^+ = ld + rd; u = min endpoint,

@@ -304,6 +304,29 @@ class TriangleCounter:
         self._ck(_lib.load().tc_graph_captures(self._h, C.byref(out)), "tc_graph_captures")
         return int(out.value)
 
+    def set_mode(self, mode: str):
+        """tc_set_mode: "bulk" (the paper's bulkUpdateAll, default) or "event" (skip-sampled neighborhood
+        sampling that visits only the estimators a batch changes).  Fresh handles only."""
+        code = {"bulk": 0, "event": 1}[mode]
+        self._ck(_lib.load().tc_set_mode(self._h, code), "tc_set_mode")
+
+    def event_state(self, first: int = 0, count: int | None = None) -> dict:
+        """tc_get_event_state: J (next f1 replacement time, 1-based), K (adjacency count of the next f2
+        replacement), ev (random words used); 0xFFFFFFFF = never."""
+        n = self.count - first if count is None else count
+        out = dict(J=np.empty(n, np.uint32), K=np.empty(n, np.uint32), ev=np.empty(n, np.uint32))
+        P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+        self._ck(_lib.load().tc_get_event_state(self._h, int(first), int(n), P(out["J"]), P(out["K"]), P(out["ev"])),
+                 "tc_get_event_state")
+        return out
+
+    def event_counters(self) -> dict:
+        v = np.zeros(4, np.uint64)
+        rc = _lib.load().tc_event_counters(self._h, v.ctypes.data_as(C.c_void_p), 4)
+        if rc < 0:
+            self._ck(rc, "tc_event_counters")
+        return dict(visited=int(v[0]), events=int(v[1]), sweeps=int(v[2]), vertices=int(v[3]))
+
     def tune(self, **knobs):
         """Index-geometry knobs (tc_tune): vbucket_arcs, vbucket_cap, vbucket_sort_cap."""
         for k, v in knobs.items():

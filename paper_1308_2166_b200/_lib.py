@@ -89,6 +89,9 @@ def load(path: str = LIB_PATH):
         "tc_set_graphs": (i32, [vp, i32]),
         "tc_graph_captures": (i32, [vp, C.POINTER(u64)]),
         "tc_tune": (i32, [vp, i32, u64]),
+        "tc_set_mode": (i32, [vp, i32]),
+        "tc_get_event_state": (i32, [vp, u64, u64, vp, vp, vp]),
+        "tc_event_counters": (i32, [vp, vp, i32]),
         "tc_get_steps": (i32, [vp, u64, u64, vp, vp, vp, vp, vp, vp]),
         "tc_sync": (i32, [vp]),
         "tc_stream": (vp, [vp]),

@@ -8,8 +8,8 @@ import subprocess
 PKG = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtc_b200.so")
-SOURCES = ["kernels.cu", "engine.cu", "exact.cu", "ingest.cpp"]
-HEADERS = ["kernels.h", "index.cuh", "philox.cuh", os.path.join("..", "..", "include", "tc.h")]
+SOURCES = ["kernels.cu", "event.cu", "engine.cu", "exact.cu", "ingest.cpp"]
+HEADERS = ["kernels.h", "event.h", "index.cuh", "philox.cuh", os.path.join("..", "..", "include", "tc.h")]
 
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-pthread", "-shared", "-Xptxas", "-v"]

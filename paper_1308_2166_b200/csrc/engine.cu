@@ -15,6 +15,7 @@
 #include <thread>
 
 #include "../../include/tc.h"
+#include "event.h"
 #include "kernels.h"
 #include "nccl_api.h"
 
@@ -98,6 +99,12 @@ struct tc_ctx {
     StepBufs steps;  // split estimator pass (TC_TUNE_SPLIT_KERNELS): per-step values of the last batch
     // a tc_create_ex handle over several GPUs of this process: the peers (rank handles) do all the work
     std::vector<tc_ctx *> peers;
+    // event-driven mode (tc_set_mode TC_MODE_EVENT): its device tables, and an upper bound
+    // on the persistent vertex count (exact at m = ed_m_known, + 2 per edge pushed since) that decides when the
+    // vertex table must grow
+    int mode = TC_MODE_BULK;
+    EdDev ed;
+    uint64_t ed_pv_known = 0, ed_m_known = 0;
 };
 
 // what a call on a poisoned handle returns: the CUDA / NCCL failure itself, else TC_ESTATE (a rejected batch)
@@ -209,6 +216,10 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
             }
         }
     }
+    if (ctx->mode == TC_MODE_EVENT && !ed_alloc_seg(ctx->ed, cap)) {
+        free_index(ix);
+        return TC_ENOMEM;
+    }
     ix.wcap = cap;
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
     CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
@@ -240,6 +251,7 @@ static void destroy_ctx(tc_ctx *ctx) {
     cudaFree(ctx->d_red);
     free_steps(ctx->steps);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    ed_free(ctx->ed);
     free_index(ctx->ix);
     cudaFree(ctx->st.r1);
     cudaFree(ctx->st.r2);
@@ -522,6 +534,13 @@ static int push_prepare(tc_ctx *ctx, const tc_edge *edges, uint64_t w, PushPrep 
     return TC_OK;
 }
 
+// a4-a8: the bulk estimator pass (fused, or split per step), or the event mode's four kernels
+static uint32_t estimator_pass(tc_ctx *ctx, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
+    if (ctx->mode == TC_MODE_EVENT) return launch_ed_batch(ctx->ix, a, ctx->ed, s, kr);
+    if (ctx->tune.split) return launch_update_split(ctx->ix, ctx->st, ctx->steps, a, s, kr);
+    return launch_update(ctx->ix, ctx->st, a, s, kr);
+}
+
 // The kernels of one push (after k_desc), on the handle's streams; returns the number of launches.
 static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr, bool *ok_out) {
     IndexBufs &ix = ctx->ix;
@@ -537,8 +556,7 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
         launches += launch_small_index(ix, a, ms, kr);
         rec(2 * TC_PHASE_PARTITION + 1, ms);
         rec(2 * TC_PHASE_UPDATE, ms);
-        if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
-        else launches += launch_update(ix, ctx->st, a, ms, kr);
+        launches += estimator_pass(ctx, a, ms, kr);
         rec(2 * TC_PHASE_UPDATE + 1, ms);
         *ok_out = ok;
         return launches;
@@ -565,17 +583,18 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
     rec(2 * TC_PHASE_VERTICES + 1, ms);
     ok = ok && cudaStreamWaitEvent(ms, ctx->join, 0) == cudaSuccess;
     rec(2 * TC_PHASE_UPDATE, ms);
-    if (ctx->tune.split) launches += launch_update_split(ix, ctx->st, ctx->steps, a, ms, kr);
-    else launches += launch_update(ix, ctx->st, a, ms, kr);
+    launches += estimator_pass(ctx, a, ms, kr);
     rec(2 * TC_PHASE_UPDATE + 1, ms);
     *ok_out = ok;
     return launches;
 }
 
+static uint32_t *ed_ctr(const tc_ctx *ctx) { return ctx->mode == TC_MODE_EVENT ? ctx->ed.ctr : nullptr; }
+
 // The graph of a batch shape: found in the cache, or captured (k_desc + the kernels) and instantiated.
 static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx::GraphEntry **out) {
     const uint64_t key = (uint64_t)a.g.w | ((uint64_t)a.small << 32) | ((uint64_t)ctx->tune.split << 33) |
-                         ((uint64_t)a.g.small_index << 34);
+                         ((uint64_t)a.g.small_index << 34) | ((uint64_t)ctx->mode << 35);
     for (auto &g : ctx->graphs)
         if (g.key == key) {
             g.last_use = ++ctx->graph_clock;
@@ -593,7 +612,7 @@ static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx
     e.key = key;
     e.last_use = ++ctx->graph_clock;
     CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    launch_desc(ctx->ix, a, d, ctx->stream);
+    launch_desc(ctx->ix, a, d, ed_ctr(ctx), ctx->stream);
     bool ok = true;
     e.launches = 1 + enqueue_kernels(ctx, a, KRec(), &ok);
     const bool cap = cudaStreamEndCapture(ctx->stream, &e.graph) == cudaSuccess && e.graph;
@@ -622,6 +641,24 @@ static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx
     return TC_OK;
 }
 
+// Event mode: the persistent vertex table keeps load <= 1/2.  Its count is known exactly at the last settle; each
+// edge adds at most 2 vertices, so only when that bound could pass half the capacity does the host settle, read
+// the exact count and, if needed, rehash into a larger table (drops the captured graphs: they hold the table).
+static int ed_reserve_vertices(tc_ctx *ctx, uint64_t w) {
+    const uint64_t cap = (uint64_t)ctx->ed.pv_mask + 1;
+    if (ctx->ed_pv_known + 2 * (ctx->m - ctx->ed_m_known) + 2 * w <= cap / 2) return TC_OK;
+    int rc = settle(ctx);
+    if (rc != TC_OK) return rc;
+    uint32_t n = 0;
+    CK(cudaMemcpy(&n, ctx->ed.ctr + kEdPVN, 4, cudaMemcpyDeviceToHost));
+    ctx->ed_pv_known = n;
+    ctx->ed_m_known = ctx->m;
+    if (n + 2 * w <= cap / 2) return TC_OK;
+    drop_graphs(ctx);
+    if (ed_rehash_pv(ctx->ed, 8 * (n + 2 * w), ctx->stream) != 0) return TC_ENOMEM;
+    return TC_OK;
+}
+
 static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     IndexBufs &ix = ctx->ix;
     const int slot = (int)((ctx->b + 1) & 1u);
@@ -630,7 +667,7 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     a.seed = ctx->seed;
     a.S = ctx->st.S;
     a.g = make_geometry((uint32_t)w, ctx->tune);
-    a.small = ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax);
+    a.small = ctx->mode == TC_MODE_BULK && (ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax));
     if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
         CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
         ctx->ptag = 1;
@@ -642,6 +679,14 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     d.ptag = ctx->ptag;
     d.slot = (uint32_t)slot;
     d.pad = 0;
+    if (ctx->mode == TC_MODE_EVENT) {
+        // S carries over; a full sweep early in the stream, where most estimators change anyway (and the watch
+        // lists of the first stream times would be long)
+        const bool full = ctx->m < 8 * w || ctx->m < ctx->count / 8;
+        d.pad = 1u | (full ? 2u : 0u);
+        const int rc = ed_reserve_vertices(ctx, w);
+        if (rc != TC_OK) return rc;
+    }
     // the error word is sticky in asynchronous mode, and cleared (or set to the overflow error) here in strict
     // mode -- stream operations ahead of the kernels, outside any graph
     if (!ctx->async_errors) {
@@ -659,7 +704,8 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
         uint32_t *ctr = ix.ctr;
         unsigned long long *S = a.S;
         uint32_t *filt = a.small ? ix.filt : nullptr;
-        void *args[] = {&d, &dst, &ctr, &S, &filt};
+        uint32_t *edctr = ed_ctr(ctx);
+        void *args[] = {&d, &dst, &ctr, &S, &filt, &edctr};
         cudaKernelNodeParams kp{};
         kp.func = const_cast<void *>(desc_kernel());
         kp.gridDim = dim3(1);
@@ -675,7 +721,7 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
             ctx->ev_kused[ctx->ev_used] = 0u;
             kr.used = &ctx->ev_kused[ctx->ev_used];
         }
-        launch_desc(ix, a, d, ctx->stream);
+        launch_desc(ix, a, d, ed_ctr(ctx), ctx->stream);
         bool ok = true;
         launches = 1 + enqueue_kernels(ctx, a, kr, &ok);
         if (ctx->prof)
@@ -837,6 +883,8 @@ int tc_reset(tc_ctx *ctx) {
         if (rc != TC_OK) return rc;
         tc_ctx *ctx = c;  // for CK
         launch_init_state(ctx->st, ctx->stream);
+        if (ctx->mode == TC_MODE_EVENT) launch_ed_init(ctx->ed, ctx->stream);
+        ctx->ed_pv_known = ctx->ed_m_known = 0;
         CK(cudaGetLastError());
         CK(cudaMemsetAsync(ctx->st.S, 0, 16, ctx->stream));
         if (ctx->ix.ctr) {
@@ -868,7 +916,6 @@ int tc_sync(tc_ctx *ctx) {
 static int red_scratch(tc_ctx *ctx, uint64_t words) {
     if (ctx->d_red_words >= words) return TC_OK;
     cudaFree(ctx->d_red);
-    free_steps(ctx->steps);
     ctx->d_red = nullptr;
     ctx->d_red_words = 0;
     if (cudaMalloc(&ctx->d_red, 8 * words) != cudaSuccess) {
@@ -974,6 +1021,7 @@ static int group_sums_one(tc_ctx *ctx, uint32_t groups, uint64_t *S_g) {
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     unsigned long long *d = nullptr;
+    if (ctx->mode == TC_MODE_EVENT) launch_ed_export(ctx->ed, ctx->st, ctx->stream);
     CK(cudaMalloc(&d, 8ull * groups));
     bool ok = cudaMemsetAsync(d, 0, 8ull * groups, ctx->stream) == cudaSuccess;
     if (ok) {
@@ -1054,6 +1102,10 @@ int tc_get_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *r1, uint
     int rc = settle_allow_poisoned(ctx);
     if (rc != TC_OK) return rc;
     if (count == 0) return TC_OK;
+    if (ctx->mode == TC_MODE_EVENT) {
+        launch_ed_export(ctx->ed, ctx->st, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
     if (r1) CK(cudaMemcpy(r1, ctx->st.r1 + first, 8 * count, cudaMemcpyDeviceToHost));
     if (r2) CK(cudaMemcpy(r2, ctx->st.r2 + first, 8 * count, cudaMemcpyDeviceToHost));
     if (p1 || p2) {  // stored as u32 (positions < 2^31, reading R13); 0xFFFFFFFF -> UINT64_MAX
@@ -1083,6 +1135,7 @@ static int recompute_S(tc_ctx *ctx) {
         return TC_OK;
     }
     const int slot = (int)(ctx->b & 1u);
+    if (ctx->mode == TC_MODE_EVENT) launch_ed_export(ctx->ed, ctx->st, ctx->stream);
     CK(cudaMemsetAsync(ctx->st.S + slot, 0, 8, ctx->stream));
     launch_group_sums(ctx->st, 0, 1, 1, ctx->st.S + slot, ctx->stream);
     CK(cudaGetLastError());
@@ -1095,6 +1148,7 @@ int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1
                  const uint32_t *r2, const uint64_t *p2, const uint32_t *c, const uint8_t *closed) {
     if (!ctx || !ctx->peers.empty() || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
     if (count && (!r1 || !p1 || !r2 || !p2 || !c || !closed)) return TC_EINVAL;
+    if (ctx->mode == TC_MODE_EVENT) return TC_EINVAL;  // the event mode's state has more than the NBSI fields
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     std::vector<uint32_t> q1(count), q2(count), cf(count);
@@ -1132,6 +1186,7 @@ int tc_set_state(tc_ctx *ctx, uint64_t first, uint64_t count, const uint32_t *r1
 
 int tc_set_counters(tc_ctx *ctx, uint64_t m, uint32_t batches) {
     if (!ctx || !ctx->peers.empty() || m > 0x7FFFFFFFull || (batches == 0) != (m == 0)) return TC_EINVAL;
+    if (ctx->mode == TC_MODE_EVENT) return TC_EINVAL;
     int rc = settle(ctx);
     if (rc != TC_OK) return rc;
     ctx->m = m;
@@ -1159,6 +1214,68 @@ int tc_set_async(tc_ctx *ctx, int async_errors) {
         c->async_errors = async_errors ? 1 : 0;
         return TC_OK;
     });
+}
+
+int tc_set_mode(tc_ctx *ctx, int mode) {
+    if (!ctx || (mode != TC_MODE_BULK && mode != TC_MODE_EVENT)) return TC_EINVAL;
+    return each(ctx, [&](tc_ctx *c) -> int {
+        int rc = settle(c);
+        if (rc != TC_OK) return rc;
+        if (c->m != 0 || c->b != 0) return TC_EINVAL;
+        if (mode == c->mode) return TC_OK;
+        tc_ctx *ctx = c;  // for CK
+        drop_graphs(c);
+        ed_free(c->ed);
+        c->mode = TC_MODE_BULK;
+        if (mode == TC_MODE_EVENT) {
+            const uint64_t pv_cap = 8 * std::max<uint64_t>(2 * c->ix.wcap, 2048);
+            if (!ed_alloc(c->ed, c->count, c->first, c->seed, pv_cap) || (c->ix.wcap && !ed_alloc_seg(c->ed, c->ix.wcap))) {
+                ed_free(c->ed);
+                return TC_ENOMEM;
+            }
+            launch_ed_init(c->ed, c->stream);
+            CK(cudaGetLastError());
+            CK(cudaMemsetAsync(c->st.S, 0, 16, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            c->ed_pv_known = c->ed_m_known = 0;
+            c->mode = TC_MODE_EVENT;
+        }
+        return TC_OK;
+    });
+}
+
+int tc_get_event_state(tc_ctx *ctx, uint64_t first, uint64_t count, uint32_t *J, uint32_t *K, uint32_t *ev) {
+    if (ctx && !ctx->peers.empty()) {
+        if (first > ctx->r || count > ctx->r - first) return TC_EINVAL;
+        for (tc_ctx *p : ctx->peers) {
+            const uint64_t lo = std::max(first, p->first), hi = std::min(first + count, p->first + p->count);
+            if (lo >= hi) continue;
+            const uint64_t o = lo - first;
+            const int rc = tc_get_event_state(p, lo - p->first, hi - lo, J ? J + o : nullptr, K ? K + o : nullptr,
+                                              ev ? ev + o : nullptr);
+            if (rc != TC_OK) return rc;
+        }
+        return TC_OK;
+    }
+    if (!ctx || ctx->mode != TC_MODE_EVENT || first > ctx->count || count > ctx->count - first) return TC_EINVAL;
+    int rc = settle_allow_poisoned(ctx);
+    if (rc != TC_OK) return rc;
+    if (count == 0) return TC_OK;
+    if (J) CK(cudaMemcpy(J, ctx->ed.J + first, 4 * count, cudaMemcpyDeviceToHost));
+    if (K) CK(cudaMemcpy(K, ctx->ed.K + first, 4 * count, cudaMemcpyDeviceToHost));
+    if (ev) CK(cudaMemcpy(ev, ctx->ed.ev + first, 4 * count, cudaMemcpyDeviceToHost));
+    return TC_OK;
+}
+
+int tc_event_counters(tc_ctx *ctx, uint64_t *out, int n) {
+    if (!ctx || !out || !ctx->peers.empty() || ctx->mode != TC_MODE_EVENT) return TC_EINVAL;
+    int rc = settle_allow_poisoned(ctx);
+    if (rc != TC_OK) return rc;
+    uint32_t v[kEdWords];
+    CK(cudaMemcpy(v, ctx->ed.ctr, 4 * kEdWords, cudaMemcpyDeviceToHost));
+    const uint64_t vals[4] = {v[kEdVisited], v[kEdEvents], v[kEdSweeps], v[kEdPVN]};
+    for (int i = 0; i < n && i < 4; ++i) out[i] = vals[i];
+    return 4;
 }
 
 void *tc_stream(tc_ctx *ctx) {
@@ -1198,7 +1315,8 @@ const char *tc_kernel_name(int k) {
     static const char *names[K_NKERNELS] = {"k_count", "k_scan_cols", "k_scan_tot", "k_scatter", "k_split",
                                             "k_pairs", "k_vhub", "k_vbig", "k_vhash", "k_update",
                                             "k_u1_resample", "k_u2_count", "k_u3_select", "k_u4_close", "k_r_reduce",
-                                            "k_small_index"};
+                                            "k_small_index", "k_ed_pre", "k_ed_trigger", "k_ed_process",
+                                            "k_ed_post"};
     return (k >= 0 && k < K_NKERNELS) ? names[k] : "";
 }
 

@@ -1,0 +1,670 @@
+// event.cu -- the event-driven estimator mode (reading R17, §10 row 4).
+//
+// The sequential neighborhood-sampling rule (batch size 1 of bulkUpdateAll is reservoir
+// sampling) with both reservoir coins replaced by skip-sampled replacement points:
+//   J = next_after(t1)  the stream time at which f1 is next replaced (P(J > s) = t1 / s),
+//   K = next_after(chi) the adjacency count at which f2 is next replaced (P(K > k) = chi / k), K = 1 for a new f1.
+// chi is never stored: chi = deg(u) + deg(v) - B with persistent vertex degrees and B = deg_t1(u) + deg_t1(v)
+// (no edge but f1 touches both u and v in a simple graph).  A batch processes only the estimators it can change:
+//   * f1 is replaced          <=> the batch holds stream time J             -> watch (kJKey, J)
+//   * chi reaches K           <=> deg(u) + deg(v) reaches B + K             -> watches (u, du + a), (v, dv + b)
+//     with a + b = Delta + 1, Delta = B + K - du - dv: one of them fires at or before the event (re-armed with
+//     the halved remainder otherwise, O(log Delta) firings per event);
+//   * the closing edge arrives <=> the batch holds the pair                 -> watch (closing pair)
+// and processes each of them once, replaying every event of the batch in time order against the batch index
+// (vertex segments in arrival order, the edge-pair table) -- the same tables the bulk pass probes.
+//
+// Random words: estimator i's 64-bit word stream n = 0, 1, ...: Philox4x32-10 block ctr = (i lo, i hi, n >> 1,
+// 0xED5A0000), key = (seed lo, seed hi); word x | y << 32 for even n, z | w << 32 for odd n.  U[0, n) is Lemire's
+// multiply-shift, a rejected word replaced by the next word.  next_after(t): t = 0 -> 1; else epoch k = trailing
+// zeros of a word (0 -> INF), L = t 2^k (> HMAX -> INF), then proposals s = L + 1 + U[0, L) accepted when
+// U[0, s-1) < L and U[0, s) < L + 1; s > HMAX -> INF.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "event.h"
+#include "philox.cuh"
+
+namespace tcb {
+
+namespace {
+
+constexpr uint32_t kFullMask = 0xffffffffu;
+
+// ---- the random words of one estimator ----------------------------------------------------------------------
+struct EdWords {
+    uint32_t id_lo, id_hi, n;  // next word index
+    PhiloxKey key;
+    uint64_t spare;            // the odd word of the last block (valid when n is odd and have_spare)
+    bool have_spare;
+};
+
+__device__ __forceinline__ uint64_t ed_word(EdWords &w) {
+    const uint32_t n = w.n++;
+    if ((n & 1u) && w.have_spare) {
+        w.have_spare = false;
+        return w.spare;
+    }
+    const uint4 o = philox4x32_10(make_uint4(w.id_lo, w.id_hi, n >> 1, 0xED5A0000u), w.key);
+    if (n & 1u) return (uint64_t)o.z | ((uint64_t)o.w << 32);
+    w.spare = (uint64_t)o.z | ((uint64_t)o.w << 32);
+    w.have_spare = true;
+    return (uint64_t)o.x | ((uint64_t)o.y << 32);
+}
+
+__device__ __forceinline__ uint64_t ed_uniform(uint64_t n, EdWords &w) {
+    uint64_t x = ed_word(w);
+    uint64_t lo = x * n;
+    uint64_t hi = __umul64hi(x, n);
+    if (lo < n) {
+        const uint64_t thr = (0ull - n) % n;
+        while (lo < thr) {
+            x = ed_word(w);
+            lo = x * n;
+            hi = __umul64hi(x, n);
+        }
+    }
+    return hi;
+}
+
+__device__ uint32_t ed_next_after(uint32_t t, EdWords &w) {
+    if (t == 0) return 1u;
+    const uint64_t x = ed_word(w);
+    if (x == 0) return kEdInf;
+    const int k = __ffsll((long long)x) - 1;
+    if (k >= 31) return kEdInf;
+    const uint64_t L = (uint64_t)t << k;
+    if (L > kEdHMax) return kEdInf;
+    for (;;) {
+        const uint64_t s = L + 1 + ed_uniform(L, w);
+        if (ed_uniform(s - 1, w) >= L) continue;
+        if (ed_uniform(s, w) >= L + 1) continue;
+        return s <= kEdHMax ? (uint32_t)s : kEdInf;
+    }
+}
+
+// ---- hash tables ----------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t pv_find(const EdDev &e, uint32_t x) {
+    uint32_t i = hash_vertex(x) & e.pv_mask;
+    for (uint32_t n = 0; n <= e.pv_mask; ++n) {
+        const uint32_t k = e.pv[i].x;
+        if (k == x) return i;
+        if (k == kEmptyV) return kEdNil;
+        i = (i + 1) & e.pv_mask;
+    }
+    return kEdNil;
+}
+
+__device__ uint32_t pv_insert(const EdDev &e, uint32_t x, uint32_t *ixctr) {
+    uint32_t i = hash_vertex(x) & e.pv_mask;
+    for (uint32_t n = 0; n <= e.pv_mask; ++n) {
+        const uint32_t k = *reinterpret_cast<volatile uint32_t *>(&e.pv[i].x);
+        if (k == x) return i;
+        if (k == kEmptyV) {
+            const uint32_t prev = atomicCAS(&e.pv[i].x, kEmptyV, x);
+            if (prev == kEmptyV) {
+                atomicAdd(&e.ctr[kEdPVN], 1u);
+                return i;
+            }
+            if (prev == x) return i;
+        }
+        i = (i + 1) & e.pv_mask;
+    }
+    atomicOr(&ixctr[kCtrErr], kErrInternal);  // a full table: never a hang
+    return kEdNil;
+}
+
+__device__ __forceinline__ uint64_t key64(uint32_t k0, uint32_t k1) { return ((uint64_t)k1 << 32) | k0; }
+
+__device__ __forceinline__ uint32_t map_find(const uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1) {
+    const uint64_t key = key64(k0, k1);
+    uint32_t i = (uint32_t)hash_pair64(key) & mask;
+    for (uint32_t n = 0; n <= mask; ++n) {
+        const uint4 s = map[i];
+        if (s.x == k0 && s.y == k1) return i;
+        if (s.x == kEmptyV && s.y == kEmptyV) return kEdNil;
+        i = (i + 1) & mask;
+    }
+    return kEdNil;
+}
+
+__device__ uint32_t map_insert(uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1, uint32_t *ixctr) {
+    const uint64_t key = key64(k0, k1);
+    uint32_t i = (uint32_t)hash_pair64(key) & mask;
+    for (uint32_t n = 0; n <= mask; ++n) {
+        unsigned long long *kp = reinterpret_cast<unsigned long long *>(&map[i]);
+        const unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(kp);
+        if (cur == key) return i;
+        if (cur == ~0ull) {
+            const unsigned long long prev = atomicCAS(kp, ~0ull, (unsigned long long)key);
+            if (prev == ~0ull || prev == key) return i;
+        }
+        i = (i + 1) & mask;
+    }
+    atomicOr(&ixctr[kCtrErr], kErrInternal);
+    return kEdNil;
+}
+
+// push watch node (est, ver) onto the list of key (k0, k1)
+__device__ void watch(const EdDev &e, uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1, uint32_t est, uint32_t ver,
+                      uint32_t *ixctr) {
+    const uint32_t s = map_insert(map, mask, k0, k1, ixctr);
+    if (s == kEdNil) return;
+    const uint32_t node = atomicAdd(&e.ctr[kEdPool], 1u);
+    if (node >= e.pool_cap) {
+        atomicOr(&ixctr[kCtrErr], kErrInternal);
+        return;
+    }
+    const uint32_t prev = atomicExch(&map[s].z, node);
+    e.pool[node] = make_uint4(est, ver, prev, 0u);
+}
+
+// detach the list at slot s and queue its live estimators (each at most once per batch)
+__device__ void fire(const EdDev &e, uint4 *map, uint32_t s, uint32_t tag) {
+    uint32_t h = atomicExch(&map[s].z, kEdNil);
+    for (uint32_t n = 0; h != kEdNil && n < e.pool_cap; ++n) {
+        const uint4 nd = e.pool[h];
+        if (nd.y == e.ver[nd.x] && atomicExch(&e.stamp[nd.x], tag) != tag) {
+            const uint32_t q = atomicAdd(&e.ctr[kEdQueue], 1u);
+            e.queue[q] = nd.x;
+        }
+        h = nd.z;
+    }
+}
+
+// ---- the batch index as the event mode reads it --------------------------------------------------------------
+struct EdIdx {
+    Lookup L;
+    const uint2 *segS;   // arcs {k << 1 | side, neighbour} grouped by vertex, arrival order
+    const uint2 *apos;   // edge k -> partition positions of its two arcs
+    const uint2 *pslot;  // partition position -> {slot in segS, segment end}
+    uint32_t *ctr;
+    const BatchDesc *d;
+    uint32_t w;
+};
+
+__device__ __forceinline__ uint32_t arc_vertex(const uint2 *E, uint32_t val) {
+    const uint2 e = E[val >> 1];
+    return (val & 1u) ? e.y : e.x;
+}
+
+// a vertex as this batch sees it
+struct VInfo {
+    uint32_t dold, pvs, dW, start;  // degree before the batch, pv slot, arcs in the batch, segment start
+};
+
+__device__ __forceinline__ VInfo vinfo(const EdIdx &I, const EdDev &e, uint32_t x) {
+    VertProbe P;
+    vt_issue(I.L, x, P);
+    const uint2 r = vt_resolve(I.L, P, x);  // {deg_W, segment start} or {0, 0}
+    VInfo v;
+    if (r.x) {
+        const uint4 s = e.seg[r.y];
+        v.dold = s.x;
+        v.pvs = s.y;
+        v.dW = r.x;
+        v.start = r.y;
+    } else {
+        const uint32_t p = pv_find(e, x);
+        v.pvs = p;
+        v.dold = p == kEdNil ? 0u : e.pv[p].y;
+        v.dW = 0;
+        v.start = 0;
+    }
+    return v;
+}
+
+// arcs of vertex v in the batch with batch index <= kmax (kmax = -1: none)
+__device__ __forceinline__ uint32_t cnt_le(const EdIdx &I, const VInfo &v, int32_t kmax) {
+    uint32_t a = 0, b = v.dW;
+    while (a < b) {
+        const uint32_t mid = (a + b) >> 1;
+        if ((int32_t)(I.segS[v.start + mid].x >> 1) <= kmax) a = mid + 1;
+        else b = mid;
+    }
+    return a;
+}
+
+// batch index of the n-th (n >= 1) arc of u or v after batch index kq (the caller knows it exists)
+__device__ int32_t kth_after(const EdIdx &I, const VInfo &u, const VInfo &v, int32_t kq, uint32_t n) {
+    const uint32_t cu = cnt_le(I, u, kq), cv = cnt_le(I, v, kq);
+    int32_t lo = kq + 1, hi = (int32_t)I.w - 1;
+    while (lo < hi) {
+        const int32_t mid = (lo + hi) >> 1;
+        if ((cnt_le(I, u, mid) - cu) + (cnt_le(I, v, mid) - cv) >= n) hi = mid;
+        else lo = mid + 1;
+    }
+    return lo;
+}
+
+// ---- kernels ---------------------------------------------------------------------------------------------------
+
+// Persistent vertices of the batch: find-or-insert, degree limit (reading R17c), per-segment info, and S's growth
+// from every closed estimator whose f1 touches a batch vertex (sum over batch arcs of ncl(x)).
+__global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long long *S) {
+    const BatchDesc d = *I.d;
+    if (I.ctr[kCtrErr]) {  // rejected (this batch or an earlier asynchronous one): record the first, change nothing
+        if (blockIdx.x == 0 && threadIdx.x == 0 && I.ctr[kCtrFailB] == 0xFFFFFFFFu) I.ctr[kCtrFailB] = d.batch;
+        return;
+    }
+    unsigned long long grow = 0;
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < 2 * I.w; s += gridDim.x * blockDim.x) {
+        const uint32_t val = I.segS[s].x;
+        const uint32_t x = arc_vertex(I.L.E, val);
+        if (s > 0 && arc_vertex(I.L.E, I.segS[s - 1].x) == x) continue;  // not the first arc of x's segment
+        VertProbe P;
+        vt_issue(I.L, x, P);
+        const uint32_t dW = vt_resolve(I.L, P, x).x;
+        const uint32_t p = pv_insert(e, x, I.ctr);
+        if (p == kEdNil) continue;
+        const uint4 pv = e.pv[p];
+        if ((uint64_t)pv.y + dW > kEdDegMax) atomicOr(&I.ctr[kCtrErr], kErrOvf);
+        e.seg[s] = make_uint4(pv.y, p, dW, s);
+        grow += (unsigned long long)dW * pv.z;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) grow += __shfl_xor_sync(kFullMask, grow, off);
+    if ((threadIdx.x & 31u) == 0 && grow) atomicAdd(S + d.slot, grow);
+}
+
+// Watches that fire in this batch -> the queue.  A full sweep instead clears the watch maps (every estimator is
+// processed and re-armed).
+__global__ void __launch_bounds__(256) k_ed_trigger(EdIdx I, EdDev e) {
+    if (I.ctr[kCtrErr]) return;
+    const BatchDesc d = *I.d;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    if (e.ctr[kEdFull]) {
+        const uint4 empty = make_uint4(kEmptyV, kEmptyV, kEdNil, kEmptyV);
+        for (uint64_t i = tid; i <= e.a_mask; i += nth) e.amap[i] = empty;
+        for (uint64_t i = tid; i <= e.p_mask; i += nth) e.pmap[i] = empty;
+        if (tid == 0) {
+            e.ctr[kEdPool] = 0u;
+            atomicAdd(&e.ctr[kEdSweeps], 1u);
+        }
+        return;
+    }
+    const uint32_t tag = d.batch + 1u;
+    const uint32_t t0 = (uint32_t)d.m_prev + 1u;  // stream time of batch edge 0
+    for (uint32_t k = tid; k < I.w; k += nth) {
+        const uint32_t sj = map_find(e.amap, e.a_mask, kJKey, t0 + k);
+        if (sj != kEdNil) fire(e, e.amap, sj, tag);
+        const uint2 ed = I.L.E[k];
+        const uint32_t sp = map_find(e.pmap, e.p_mask, ed.x, ed.y);
+        if (sp != kEdNil) fire(e, e.pmap, sp, tag);
+        const uint2 ap = I.apos[k];
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+            const uint32_t x = side ? ed.y : ed.x;
+            const uint2 ps = I.pslot[side ? ap.y : ap.x];  // {slot, segment end}
+            VertProbe P;
+            vt_issue(I.L, x, P);
+            const uint2 r = vt_resolve(I.L, P, x);  // {deg_W, start}
+            const uint32_t theta = e.seg[r.y].x + (ps.x - r.y) + 1u;  // x's degree once this arc has arrived
+            const uint32_t st = map_find(e.amap, e.a_mask, x, theta);
+            if (st != kEdNil) fire(e, e.amap, st, tag);
+        }
+    }
+}
+
+// Each queued estimator (every estimator in a full sweep): replay its events of this batch in time order, update
+// S and the closed counts, re-arm its watches.
+__global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned long long *S) {
+    if (I.ctr[kCtrErr]) return;
+    const BatchDesc d = *I.d;
+    const bool full = e.ctr[kEdFull] != 0;
+    const uint32_t nq = full ? (uint32_t)e.count : e.ctr[kEdQueue];
+    const uint32_t P0 = (uint32_t)d.m_prev, Pend = P0 + I.w;
+    Lookup L = I.L;
+    L.ptag = d.ptag;
+    unsigned long long dS = 0;
+    uint32_t visited = 0, events = 0;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+        const uint32_t t = full ? q : e.queue[q];
+        ++visited;
+        const uint64_t gid = e.first + t;
+        EdWords W{(uint32_t)gid, (uint32_t)(gid >> 32), e.ev[t], PhiloxKey{(uint32_t)e.seed, (uint32_t)(e.seed >> 32)},
+                  0ull, false};
+        uint32_t J = e.J[t], t1 = e.t1[t], u = e.u[t], v = e.v[t], B = e.B[t], K = e.K[t], t2 = e.t2[t], y = e.y[t],
+                 fl = e.fl[t];
+        const uint32_t uo = u, vo = v, Bo = B, t1o = t1;
+        const bool closed_o = (fl & 1u) != 0;
+        // the batch in time order, one f1 epoch at a time: f2 events (clause 3) of the current f1 up to the next f1
+        // replacement (clause 1) inside the batch, then that replacement -- the random words are used in event
+        // order, as the per-edge rule uses them
+        VInfo iu, iv;
+        if (t1) {
+            iu = vinfo(I, e, u);
+            iv = vinfo(I, e, v);
+        }
+        int32_t kq = -1;  // events of the current f1 are after batch index kq
+        for (;;) {
+            const bool jin = J != kEdInf && J <= Pend;
+            const int32_t kh = jin ? (int32_t)(J - P0) - 2 : (int32_t)I.w - 1;  // the epoch's last batch index
+            if (t1 && K != kEdInf) {
+                const uint32_t chi_h = iu.dold + cnt_le(I, iu, kh) + iv.dold + cnt_le(I, iv, kh) - B;
+                if (K <= chi_h) {  // chi reaches K at an arc of this epoch
+                    const uint32_t chi_q = iu.dold + cnt_le(I, iu, kq) + iv.dold + cnt_le(I, iv, kq) - B;
+                    do {
+                        const int32_t k2 = kth_after(I, iu, iv, kq, K - chi_q);
+                        const uint2 ed = L.E[k2];
+                        const bool at_u = ed.x == u || ed.y == u;
+                        const uint32_t sh = at_u ? u : v;
+                        y = ed.x == sh ? ed.y : ed.x;
+                        t2 = P0 + 1u + (uint32_t)k2;
+                        fl = at_u ? 0u : 2u;  // a new f2 is not closed
+                        K = ed_next_after(K, W);
+                        ++events;
+                    } while (K != kEdInf && K <= chi_h);
+                }
+            }
+            if (!jin) break;
+            t1 = J;  // clause 1: f1 <- e_J
+            J = ed_next_after(t1, W);
+            ++events;
+            kq = (int32_t)(t1 - P0 - 1u);
+            const uint2 ed = L.E[kq];
+            u = ed.x;
+            v = ed.y;
+            iu = vinfo(I, e, u);
+            iv = vinfo(I, e, v);
+            B = iu.dold + cnt_le(I, iu, kq) + iv.dold + cnt_le(I, iv, kq);
+            K = 1u;
+            t2 = 0u;
+            y = kEmptyV;
+            fl = 0u;
+        }
+        uint32_t du_end = 0, dv_end = 0;
+        if (t1) {
+            du_end = iu.dold + iu.dW;
+            dv_end = iv.dold + iv.dW;
+            if (t2 && !(fl & 1u)) {  // clause 4: the closing edge in this batch, after f2
+                const uint32_t z = (fl & 2u) ? u : v;
+                const int64_t kc = pt_find(L, min(z, y), max(z, y));
+                if (kc >= 0 && P0 + 1u + (uint32_t)kc > t2) fl |= 1u;
+            }
+        }
+        const bool closed = (fl & 1u) != 0;
+        // S and the closed counts: the old contribution at the end of the batch out, the new one in
+        if (closed_o) {
+            uint32_t c_old;
+            if (t1 == t1o) {
+                c_old = du_end + dv_end - Bo;
+            } else {
+                const VInfo a = vinfo(I, e, uo), b = vinfo(I, e, vo);
+                c_old = a.dold + a.dW + b.dold + b.dW - Bo;
+                atomicSub(&e.pv[a.pvs].z, 1u);
+                atomicSub(&e.pv[b.pvs].z, 1u);
+            }
+            dS -= c_old;
+            if (t1 == t1o && !closed) {
+                atomicSub(&e.pv[iu.pvs].z, 1u);
+                atomicSub(&e.pv[iv.pvs].z, 1u);
+            }
+        }
+        if (closed) {
+            dS += du_end + dv_end - B;
+            if (!(closed_o && t1 == t1o)) {
+                atomicAdd(&e.pv[iu.pvs].z, 1u);
+                atomicAdd(&e.pv[iv.pvs].z, 1u);
+            }
+        }
+        // re-arm
+        const uint32_t ver = e.ver[t] + 1u;
+        if (J != kEdInf) watch(e, e.amap, e.a_mask, kJKey, J, t, ver, I.ctr);
+        if (t1 && K != kEdInf) {
+            const uint32_t delta = B + K - du_end - dv_end;  // >= 1
+            const uint32_t a = (delta + 1u) >> 1, b = delta + 1u - a;
+            watch(e, e.amap, e.a_mask, u, du_end + a, t, ver, I.ctr);
+            watch(e, e.amap, e.a_mask, v, dv_end + b, t, ver, I.ctr);
+        }
+        if (t2 && !closed) {
+            const uint32_t z = (fl & 2u) ? u : v;
+            watch(e, e.pmap, e.p_mask, min(z, y), max(z, y), t, ver, I.ctr);
+        }
+        e.ver[t] = ver;
+        e.J[t] = J;
+        e.t1[t] = t1;
+        e.u[t] = u;
+        e.v[t] = v;
+        e.B[t] = B;
+        e.K[t] = t1 ? K : kEdInf;
+        e.t2[t] = t2;
+        e.y[t] = y;
+        e.fl[t] = fl;
+        e.ev[t] = W.n;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        dS += __shfl_xor_sync(kFullMask, dS, off);
+        visited += __shfl_xor_sync(kFullMask, visited, off);
+        events += __shfl_xor_sync(kFullMask, events, off);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (dS) atomicAdd(S + d.slot, dS);
+        if (visited) atomicAdd(&e.ctr[kEdVisited], visited);
+        if (events) atomicAdd(&e.ctr[kEdEvents], events);
+    }
+}
+
+// The batch's degrees into the persistent table.
+__global__ void __launch_bounds__(256) k_ed_post(EdIdx I, EdDev e) {
+    if (I.ctr[kCtrErr]) return;
+    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < 2 * I.w; s += gridDim.x * blockDim.x) {
+        const uint32_t x = arc_vertex(I.L.E, I.segS[s].x);
+        if (s > 0 && arc_vertex(I.L.E, I.segS[s - 1].x) == x) continue;
+        const uint4 sg = e.seg[s];
+        e.pv[sg.y].y = sg.x + sg.z;
+    }
+}
+
+__global__ void k_ed_init(EdDev e) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t t = tid; t < e.count; t += nth) {
+        e.J[t] = 1u;
+        e.t1[t] = 0u;
+        e.u[t] = kEmptyV;
+        e.v[t] = kEmptyV;
+        e.B[t] = 0u;
+        e.K[t] = kEdInf;
+        e.t2[t] = 0u;
+        e.y[t] = kEmptyV;
+        e.fl[t] = 0u;
+        e.ver[t] = 0u;
+        e.stamp[t] = 0u;
+        e.ev[t] = 0u;
+    }
+    const uint4 empty = make_uint4(kEmptyV, kEmptyV, kEdNil, kEmptyV);
+    for (uint64_t i = tid; i <= e.a_mask; i += nth) e.amap[i] = empty;
+    for (uint64_t i = tid; i <= e.p_mask; i += nth) e.pmap[i] = empty;
+    for (uint64_t i = tid; i <= e.pv_mask; i += nth) e.pv[i] = make_uint4(kEmptyV, 0u, 0u, 0u);
+    if (tid < (uint64_t)kEdWords) e.ctr[tid] = 0u;
+}
+
+__global__ void k_ed_set_thr(uint32_t *ctr, uint32_t thr) { ctr[kEdThr] = thr; }
+
+__global__ void k_ed_rehash(uint4 *old_pv, uint64_t old_n, uint4 *pv, uint32_t mask, uint32_t *err) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < old_n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 s = old_pv[i];
+        if (s.x == kEmptyV) continue;
+        uint32_t j = hash_vertex(s.x) & mask;
+        uint32_t n = 0;
+        for (; n <= mask; ++n) {
+            if (atomicCAS(&pv[j].x, kEmptyV, s.x) == kEmptyV) {
+                pv[j].y = s.y;
+                pv[j].z = s.z;
+                break;
+            }
+            j = (j + 1) & mask;
+        }
+        if (n > mask) atomicOr(err, 1u);
+    }
+}
+
+__global__ void k_ed_fill_pv(uint4 *pv, uint64_t n) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        pv[i] = make_uint4(kEmptyV, 0u, 0u, 0u);
+}
+
+__global__ void k_ed_export(EdDev e, uint2 *r1, uint32_t *p1, uint2 *r2, uint32_t *p2, uint32_t *cf) {
+    for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < e.count; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t1 = e.t1[t];
+        if (!t1) {
+            r1[t] = r2[t] = make_uint2(kEmptyV, kEmptyV);
+            p1[t] = p2[t] = kEmptyV;
+            cf[t] = 0u;
+            continue;
+        }
+        const uint32_t u = e.u[t], v = e.v[t];
+        const uint32_t pu = pv_find(e, u), pv = pv_find(e, v);
+        const uint32_t chi = e.pv[pu].y + e.pv[pv].y - e.B[t];
+        const uint32_t fl = e.fl[t], t2 = e.t2[t];
+        r1[t] = make_uint2(u, v);
+        p1[t] = t1 - 1u;
+        if (t2) {
+            const uint32_t sh = (fl & 2u) ? v : u, y = e.y[t];
+            r2[t] = make_uint2(min(sh, y), max(sh, y));
+            p2[t] = t2 - 1u;
+        } else {
+            r2[t] = make_uint2(kEmptyV, kEmptyV);
+            p2[t] = kEmptyV;
+        }
+        cf[t] = chi | ((fl & 1u) ? kClosedBit : 0u);
+    }
+}
+
+uint32_t grid_of(uint64_t items, uint32_t per_sm) {
+    const uint64_t want = (items + 255) / 256;
+    const uint64_t cap = (uint64_t)sm_count() * per_sm;
+    return (uint32_t)std::max<uint64_t>(1, std::min(want, cap));
+}
+
+uint64_t pow2_at_least(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+}  // namespace
+
+bool ed_alloc(EdDev &e, uint64_t count, uint64_t first, uint64_t seed, uint64_t pv_cap) {
+    e = EdDev();
+    e.count = count;
+    e.first = first;
+    e.seed = seed;
+    const uint64_t n = std::max<uint64_t>(count, 1);
+    // watch nodes: a full sweep arms at most 4 per estimator, a batch at most 4 per estimator; a rebuild is due
+    // once more than 8 n are in use, so 12 n + slack always suffice
+    const uint64_t pool = 12 * n + 4096;
+    if (pool > 0xFFFFFFF0ull) return false;
+    e.pool_cap = (uint32_t)pool;
+    const uint64_t acap = pow2_at_least(2 * (9 * n + 4096)), pcap = pow2_at_least(2 * (3 * n + 4096));
+    const uint64_t vcap = pow2_at_least(std::max<uint64_t>(pv_cap, 1024));
+    if (acap > (1ull << 32) || pcap > (1ull << 32) || vcap > (1ull << 32)) return false;
+    e.a_mask = (uint32_t)(acap - 1);
+    e.p_mask = (uint32_t)(pcap - 1);
+    e.pv_mask = (uint32_t)(vcap - 1);
+    uint32_t **soa[] = {&e.J, &e.t1, &e.u, &e.v, &e.B, &e.K, &e.t2, &e.y, &e.fl, &e.ver, &e.stamp, &e.ev, &e.queue};
+    bool ok = true;
+    for (uint32_t **p : soa) ok = ok && cudaMalloc(p, 4 * n) == cudaSuccess;
+    ok = ok && cudaMalloc(&e.pool, 16 * pool) == cudaSuccess && cudaMalloc(&e.amap, 16 * acap) == cudaSuccess &&
+         cudaMalloc(&e.pmap, 16 * pcap) == cudaSuccess && cudaMalloc(&e.pv, 16 * vcap) == cudaSuccess &&
+         cudaMalloc(&e.ctr, 4 * kEdWords) == cudaSuccess;
+    if (!ok) {
+        cudaGetLastError();
+        ed_free(e);
+    }
+    return ok;
+}
+
+void ed_free(EdDev &e) {
+    void *bufs[] = {e.J, e.t1, e.u, e.v, e.B, e.K, e.t2, e.y, e.fl, e.ver, e.stamp, e.ev, e.queue,
+                    e.pool, e.amap, e.pmap, e.pv, e.ctr, e.seg};
+    for (void *p : bufs) cudaFree(p);
+    e = EdDev();
+}
+
+bool ed_alloc_seg(EdDev &e, uint64_t wcap) {
+    cudaFree(e.seg);
+    e.seg = nullptr;
+    if (cudaMalloc(&e.seg, 16 * 2 * std::max<uint64_t>(wcap, 1)) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return true;
+}
+
+int launch_ed_init(const EdDev &e, cudaStream_t s) {
+    const uint64_t items = std::max<uint64_t>({e.count, (uint64_t)e.a_mask + 1, (uint64_t)e.p_mask + 1,
+                                               (uint64_t)e.pv_mask + 1});
+    k_ed_init<<<grid_of(items, 16), 256, 0, s>>>(e);
+    // rebuild threshold: more than 8 nodes per estimator in use (see ed_alloc)
+    k_ed_set_thr<<<1, 1, 0, s>>>(e.ctr, (uint32_t)std::min<uint64_t>(8 * std::max<uint64_t>(e.count, 1) + 1024,
+                                                                     e.pool_cap - 4 * std::max<uint64_t>(e.count, 1)));
+    return 2;
+}
+
+int ed_rehash_pv(EdDev &e, uint64_t new_cap, cudaStream_t s) {
+    new_cap = pow2_at_least(new_cap);
+    if (new_cap > (1ull << 32)) return -1;
+    uint4 *pv = nullptr;
+    if (cudaMalloc(&pv, 16 * new_cap) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    uint32_t *err = nullptr;
+    if (cudaMalloc(&err, 4) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(pv);
+        return -1;
+    }
+    cudaMemsetAsync(err, 0, 4, s);
+    k_ed_fill_pv<<<grid_of(new_cap, 16), 256, 0, s>>>(pv, new_cap);
+    const uint64_t old_n = (uint64_t)e.pv_mask + 1;
+    k_ed_rehash<<<grid_of(old_n, 16), 256, 0, s>>>(e.pv, old_n, pv, (uint32_t)(new_cap - 1), err);
+    uint32_t h = 0;
+    const bool ok = cudaMemcpyAsync(&h, err, 4, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+                    cudaStreamSynchronize(s) == cudaSuccess && h == 0;
+    cudaFree(err);
+    if (!ok) {
+        cudaGetLastError();
+        cudaFree(pv);
+        return -1;
+    }
+    cudaFree(e.pv);
+    e.pv = pv;
+    e.pv_mask = (uint32_t)(new_cap - 1);
+    return 0;
+}
+
+static EdIdx ed_idx(const IndexBufs &ix, const BatchArgs &a) {
+    return EdIdx{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.segS, ix.apos, ix.pslot,
+                 ix.ctr, ix.desc, a.g.w};
+}
+
+int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, cudaStream_t s, const KRec &kr) {
+    const EdIdx I = ed_idx(ix, a);
+    const uint32_t g_arcs = grid_of(2ull * a.g.w, 8);
+    kr.beg(K_ED_PRE, s);
+    k_ed_pre<<<g_arcs, 256, 0, s>>>(I, e, a.S);
+    kr.end(K_ED_PRE, s);
+    kr.beg(K_ED_TRIGGER, s);
+    k_ed_trigger<<<std::max<uint32_t>(grid_of(a.g.w, 8), (uint32_t)sm_count() * 4), 256, 0, s>>>(I, e);
+    kr.end(K_ED_TRIGGER, s);
+    kr.beg(K_ED_PROCESS, s);
+    k_ed_process<<<(uint32_t)sm_count() * 4, 256, 0, s>>>(I, e, a.S);
+    kr.end(K_ED_PROCESS, s);
+    kr.beg(K_ED_POST, s);
+    k_ed_post<<<g_arcs, 256, 0, s>>>(I, e);
+    kr.end(K_ED_POST, s);
+    return 4;
+}
+
+int launch_ed_export(const EdDev &e, const StateBufs &st, cudaStream_t s) {
+    if (!e.count) return 0;
+    k_ed_export<<<grid_of(e.count, 16), 256, 0, s>>>(e, st.r1, st.p1, st.r2, st.p2, st.cf);
+    return 1;
+}
+
+}  // namespace tcb

@@ -32,6 +32,7 @@
 
 #include "index.cuh"
 #include "kernels.h"
+#include "event.h"
 #include "philox.cuh"
 
 namespace tcb {
@@ -192,10 +193,10 @@ constexpr uint32_t kArcsPerWarp = kArcRounds * 32, kEdgesPerWarp = kEdgeRounds *
 
 template <int NB>  // the partition bits a.g.bp1, as a compile-time constant
 __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
-    if (blockIdx.x == 0) {  // per-batch resets (every later kernel of the batch starts after this one)
+    if (blockIdx.x == 0) {  // per-batch resets (every later kernel of the batch starts after this one); this
+                            // batch's S slot is k_desc's (zeroed, or carried over in the event mode)
         if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
             a.ctr[threadIdx.x] = 0u;
-        if (threadIdx.x == 0) a.S[a.d->slot] = 0ull;
     }
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     const uint2 *in = a.d->in;
@@ -1806,12 +1807,18 @@ __global__ void k_group_sums(const uint32_t *__restrict__ cf, uint64_t count, ui
 
 // The first node of every push: the batch's descriptor into device memory, and the per-batch resets (the
 // counters except the sticky error word and the failed-batch index, this batch's S, the small-batch filter)
-// ahead of every kernel of the batch.
+// ahead of every kernel of the batch.  Event mode (edctr != null): S is carried over from the
+// previous batch (d.pad bit 0), the queue is emptied, and the batch becomes a full sweep when the host asks for one
+// (d.pad bit 1) or the watch-node pool has passed its rebuild threshold.
 __global__ void __launch_bounds__(256) k_desc(BatchDesc d, BatchDesc *dst, uint32_t *ctr, unsigned long long *S,
-                                              uint32_t *filt) {
+                                              uint32_t *filt, uint32_t *edctr) {
     if (threadIdx.x == 0) {
         *dst = d;
-        S[d.slot] = 0ull;
+        S[d.slot] = (d.pad & 1u) ? S[d.slot ^ 1u] : 0ull;
+        if (edctr) {
+            edctr[kEdQueue] = 0u;
+            edctr[kEdFull] = ((d.pad & 2u) || edctr[kEdPool] > edctr[kEdThr]) ? 1u : 0u;
+        }
     }
     if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
         ctr[threadIdx.x] = 0u;
@@ -1819,8 +1826,8 @@ __global__ void __launch_bounds__(256) k_desc(BatchDesc d, BatchDesc *dst, uint3
         for (uint32_t i = threadIdx.x; i < kFilterWords; i += blockDim.x) filt[i] = 0u;
 }
 
-int launch_desc(const IndexBufs &ix, const BatchArgs &a, const BatchDesc &d, cudaStream_t s) {
-    k_desc<<<1, 256, 0, s>>>(d, ix.desc, ix.ctr, a.S, a.small ? ix.filt : nullptr);
+int launch_desc(const IndexBufs &ix, const BatchArgs &a, const BatchDesc &d, uint32_t *edctr, cudaStream_t s) {
+    k_desc<<<1, 256, 0, s>>>(d, ix.desc, ix.ctr, a.S, a.small ? ix.filt : nullptr, edctr);
     return 1;
 }
 

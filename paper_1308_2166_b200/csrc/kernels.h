@@ -105,7 +105,7 @@ Geometry make_geometry(uint32_t w, const Tuning &t);
 
 // Per-kernel profiling (tc_profile_kernels): ids match include/tc.h TC_KERNEL_*.
 enum KernelId { K_COUNT = 0, K_SCAN_COLS, K_SCAN_TOT, K_SCATTER, K_SPLIT, K_PAIRS, K_VHUB, K_VBIG, K_VHASH, K_UPDATE,
-                K_U1, K_U2, K_U3, K_U4, K_R, K_SMALL, K_NKERNELS };
+                K_U1, K_U2, K_U3, K_U4, K_R, K_SMALL, K_ED_PRE, K_ED_TRIGGER, K_ED_PROCESS, K_ED_POST, K_NKERNELS };
 struct KRec {
     cudaEvent_t *ev = nullptr;  // 2 K_NKERNELS events (begin, end) or null: no profiling
     uint32_t *used = nullptr;   // bit k set once kernel k's events were recorded in this push
@@ -134,7 +134,8 @@ int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, 
 int launch_update_split(const IndexBufs &ix, const StateBufs &st, const StepBufs &sb, const BatchArgs &a, cudaStream_t s,
                         const KRec &kr = KRec());
 
-int launch_desc(const IndexBufs &ix, const BatchArgs &a, const BatchDesc &d, cudaStream_t s);  // the push's first node
+// the push's first node; edctr: the event mode's counters (null in the bulk mode)
+int launch_desc(const IndexBufs &ix, const BatchArgs &a, const BatchDesc &d, uint32_t *edctr, cudaStream_t s);
 const void *desc_kernel();                                                  // its function (graph node lookup)
 
 int launch_init_state(const StateBufs &st, cudaStream_t s);
