@@ -51,6 +51,11 @@ def parse():
     ap.add_argument("--no-graphs", action="store_true", help="plain stream launches instead of one CUDA graph per push")
     ap.add_argument("--no-profile-pass", action="store_true", help="skip the per-kernel attribution pass")
     ap.add_argument("--cpu-batches", type=int, default=0, help="batches in the cpu_baseline sample (0: auto)")
+    ap.add_argument("--mode", default="bulk", choices=["bulk", "event"],
+                    help="estimator update rule (tc_set_mode): the paper's bulkUpdateAll, or the event-driven mode "
+                         "(SURVEY 8(f) row 4)")
+    ap.add_argument("--whole-stream", action="store_true",
+                    help="time every batch of one pass over the stream (steps = batches per stream)")
     return ap.parse_args()
 
 
@@ -195,6 +200,18 @@ def kernel_bytes(kernel, w, st, R):
         return 72 * w + 16 * st["vertices"]
     if kernel == "k_update":
         return 24 * R + 32 * st["fresh"] + 16 * st["r2_replaced_retained"] - 4 * st["skipped"]
+    # event mode (DESIGN.md section 10 row 4): per arc the segment read, per distinct vertex a persistent-table
+    # probe and the 16-byte segment record; per edge the trigger lookups (time, pair, two degree thresholds:
+    # 4 x 16-byte slots) and the edge / arc records; per visited estimator its 48-byte state read and written and
+    # about 4 watch nodes + map slots armed (4 x 32 B)
+    if kernel == "k_ed_pre":
+        return 16 * w + 48 * st["vertices"]
+    if kernel == "k_ed_trigger":
+        return 96 * w
+    if kernel == "k_ed_process":
+        return (96 + 128) * st.get("visited", 0)
+    if kernel == "k_ed_post":
+        return 16 * w + 32 * st["vertices"]
     return 0
 
 
@@ -221,6 +238,8 @@ def run_b200(args):
     t_gen = time.perf_counter() - t_gen
     m_total = len(stream)
     nb = (m_total + w - 1) // w
+    if args.whole_stream:
+        args.steps = nb
     first = rank * r // world
     count = (rank + 1) * r // world - first
 
@@ -241,6 +260,8 @@ def run_b200(args):
     else:
         tc = TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
     assert (tc.first, tc.count) == (first, count)
+    if args.mode == "event":
+        tc.set_mode("event")
     tc.set_async(True)
     if knobs:
         tc.tune(**knobs)
@@ -291,6 +312,10 @@ def run_b200(args):
                         acc[1] += n
                 for kk, v in tc.stats().items():
                     stats[kk] = stats.get(kk, 0) + v
+                if args.mode == "event":
+                    ec = tc.event_counters()
+                    for kk in ("visited", "events", "sweeps"):
+                        stats[kk] = stats.get(kk, 0) + ec[kk]
 
             barrier()
             torch.cuda.synchronize()
@@ -389,7 +414,10 @@ def run_b200(args):
                                "frac": B_step / (step_ms / 1e3) / 1e9 / peak,
                                "model": "w (40 + 16 D/w) + R (24 + 16 (P_r1 + P_r2)) bytes (SURVEY 8(d) minimal)"},
                 "events_per_batch": {"D": D_avg, "fresh_r1": stats["fresh"] / nsteps,
-                                     "r2_replaced_retained": stats["r2_replaced_retained"] / nsteps},
+                                     "r2_replaced_retained": stats["r2_replaced_retained"] / nsteps,
+                                     **({"visited": stats.get("visited", 0) / nsteps,
+                                         "events": stats.get("events", 0) / nsteps,
+                                         "full_sweeps": stats.get("sweeps", 0)} if args.mode == "event" else {})},
                 "from": "CUDA events around every kernel, a second pass over the stream (plain launches); shares "
                         "agree with the committed ncu launch list profiles/launches_r02_<config>.csv",
                 "per_rank_kernel_ms": per_rank,
@@ -397,6 +425,8 @@ def run_b200(args):
                 "ncu_source": ncu.get("source")}
 
     out["config"] = {"workload": f"{args.config}: {cfg['desc']}", "r": r, "w": w, "stream_edges": m_total,
+                     "mode": args.mode, "steps_from": "stream start (one whole pass)" if args.whole_stream else
+                     "stream start, consecutive batches",
                      "batches_per_stream": nb, "estimators_per_gpu": count,
                      "parallelism": f"estimator-shard x{world}",
                      "l2": "flushed before every step (256 MiB read, outside the step events)",
@@ -416,6 +446,8 @@ def run_b200(args):
         if not resident:
             tc.set_graphs(not args.no_graphs)
         tc2 = tc if not resident else TriangleCounter(r, args.seed, device=dev.index, w_max_hint=w)
+        if resident and args.mode == "event":
+            tc2.set_mode("event")
         tc2.set_async(True)
         tc2.set_graphs(not args.no_graphs)
         ext2 = torch.cuda.ExternalStream(tc2.stream_ptr, device=dev)
@@ -463,7 +495,8 @@ def run_b200(args):
     # ---- CPU baseline: the oracle as it stands, on this host's cores (rank 0, N = 1 only) ----
     if not args.no_cpu_baseline and world == 1:
         nbat = args.cpu_batches or max(1, min(8, (1 << 24) // max(w, r)))
-        out["cpu_baseline"] = cpu_baseline(stream, r, w, args.seed, nbatches=min(nbat, nb))
+        out["cpu_baseline"] = (cpu_baseline_event(stream, r, w, args.seed) if args.mode == "event" else
+                               cpu_baseline(stream, r, w, args.seed, nbatches=min(nbat, nb)))
 
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -486,6 +519,22 @@ def cpu_baseline(stream, r, w, seed, nbatches):
             "cpu_model": model, "host_cpus": ncpu, "omp_num_threads_env": os.environ.get("OMP_NUM_THREADS"),
             "sample": f"first {nbatches} batch(es) ({edges} edges) of the same stream at full r={r}, w={w}; "
                       f"oracle/indexed.c (qsort + binary-search multisearch, OpenMP over estimators), {dt:.1f} s"}
+
+
+def cpu_baseline_event(stream, r, w, seed):
+    """The event mode's oracle (oracle/ed.c: every estimator walked event by event, OpenMP) on a stream prefix
+    of about 2^21 edges at full r (its cost is per estimator event, so the sample is a prefix, not a batch)."""
+    from oracle.edc import EventOracleC, threads
+    m = min(len(stream), max(w, 1 << 21))
+    o = EventOracleC(r, seed)
+    t0 = time.perf_counter()
+    o.push_batch(stream[:m], validate=False)
+    o.closed_sum()
+    dt = time.perf_counter() - t0
+    model, ncpu = cpu_info()
+    return {"value": m / dt, "unit": "edges/s", "cores": threads(), "kind": "oracle", "cpu_model": model,
+            "host_cpus": ncpu, "sample": f"the first {m} edges of the same stream at full r={r} through oracle/ed.c "
+                                         f"(event mode), {dt:.1f} s"}
 
 
 def run_reference(args):

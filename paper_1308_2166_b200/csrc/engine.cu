@@ -536,7 +536,7 @@ static int push_prepare(tc_ctx *ctx, const tc_edge *edges, uint64_t w, PushPrep 
 
 // a4-a8: the bulk estimator pass (fused, or split per step), or the event mode's four kernels
 static uint32_t estimator_pass(tc_ctx *ctx, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
-    if (ctx->mode == TC_MODE_EVENT) return launch_ed_batch(ctx->ix, a, ctx->ed, s, kr);
+    if (ctx->mode == TC_MODE_EVENT) return launch_ed_batch(ctx->ix, a, ctx->ed, ctx->st.stats, s, kr);
     if (ctx->tune.split) return launch_update_split(ctx->ix, ctx->st, ctx->steps, a, s, kr);
     return launch_update(ctx->ix, ctx->st, a, s, kr);
 }
@@ -680,9 +680,8 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     d.slot = (uint32_t)slot;
     d.pad = 0;
     if (ctx->mode == TC_MODE_EVENT) {
-        // S carries over; a full sweep early in the stream, where most estimators change anyway (and the watch
-        // lists of the first stream times would be long)
-        const bool full = ctx->m < 8 * w || ctx->m < ctx->count / 8;
+        // S carries over; a full sweep early in the stream (m < 8 w), where most estimators change anyway
+        const bool full = ctx->m < 8 * w;
         d.pad = 1u | (full ? 2u : 0u);
         const int rc = ed_reserve_vertices(ctx, w);
         if (rc != TC_OK) return rc;

@@ -147,9 +147,23 @@ __device__ uint32_t map_insert(uint4 *map, uint32_t mask, uint32_t k0, uint32_t 
     return kEdNil;
 }
 
-// push watch node (est, ver) onto the list of key (k0, k1)
+// Watch versions, one per kind, packed in one word per estimator: a node is live while its kind's version is the
+// estimator's current one.  A stale node that looks live (the 10/11-bit field wrapped) only queues the estimator
+// once more -- processing an estimator without events in the batch is harmless -- so the check is a filter, and
+// correctness needs only that a live watch is never missed.
+enum WatchKind : uint32_t { kWJ = 0, kWT = 1, kWP = 2 };
+__device__ __forceinline__ uint32_t ver_of(uint32_t ver, uint32_t kind) {
+    return kind == kWJ ? (ver & 0x3FFu) : kind == kWT ? ((ver >> 10) & 0x7FFu) : (ver >> 21);
+}
+__device__ __forceinline__ uint32_t ver_bump(uint32_t ver, uint32_t kind) {
+    const uint32_t f = ver_of(ver, kind) + 1u;
+    return kind == kWJ ? ((ver & ~0x3FFu) | (f & 0x3FFu))
+                       : kind == kWT ? ((ver & ~(0x7FFu << 10)) | ((f & 0x7FFu) << 10)) : ((ver & 0x1FFFFFu) | (f << 21));
+}
+
+// push watch node (est, kind, version) onto the list of key (k0, k1)
 __device__ void watch(const EdDev &e, uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1, uint32_t est, uint32_t ver,
-                      uint32_t *ixctr) {
+                      uint32_t kind, uint32_t *ixctr) {
     const uint32_t s = map_insert(map, mask, k0, k1, ixctr);
     if (s == kEdNil) return;
     const uint32_t node = atomicAdd(&e.ctr[kEdPool], 1u);
@@ -158,7 +172,7 @@ __device__ void watch(const EdDev &e, uint4 *map, uint32_t mask, uint32_t k0, ui
         return;
     }
     const uint32_t prev = atomicExch(&map[s].z, node);
-    e.pool[node] = make_uint4(est, ver, prev, 0u);
+    e.pool[node] = make_uint4(est, ver_of(ver, kind), prev, kind);
 }
 
 // detach the list at slot s and queue its live estimators (each at most once per batch)
@@ -166,7 +180,7 @@ __device__ void fire(const EdDev &e, uint4 *map, uint32_t s, uint32_t tag) {
     uint32_t h = atomicExch(&map[s].z, kEdNil);
     for (uint32_t n = 0; h != kEdNil && n < e.pool_cap; ++n) {
         const uint4 nd = e.pool[h];
-        if (nd.y == e.ver[nd.x] && atomicExch(&e.stamp[nd.x], tag) != tag) {
+        if (nd.y == ver_of(e.ver[nd.x], nd.w) && atomicExch(&e.stamp[nd.x], tag) != tag) {
             const uint32_t q = atomicAdd(&e.ctr[kEdQueue], 1u);
             e.queue[q] = nd.x;
         }
@@ -227,29 +241,34 @@ __device__ __forceinline__ uint32_t cnt_le(const EdIdx &I, const VInfo &v, int32
     return a;
 }
 
-// batch index of the n-th (n >= 1) arc of u or v after batch index kq (the caller knows it exists)
+// batch index of the n-th (n >= 1) arc of u or v after batch index kq (the caller knows it exists): the two
+// segments are sorted by batch index and disjoint, so a binary search over how many come from u's (merge path)
 __device__ int32_t kth_after(const EdIdx &I, const VInfo &u, const VInfo &v, int32_t kq, uint32_t n) {
-    const uint32_t cu = cnt_le(I, u, kq), cv = cnt_le(I, v, kq);
-    int32_t lo = kq + 1, hi = (int32_t)I.w - 1;
-    while (lo < hi) {
-        const int32_t mid = (lo + hi) >> 1;
-        if ((cnt_le(I, u, mid) - cu) + (cnt_le(I, v, mid) - cv) >= n) hi = mid;
-        else lo = mid + 1;
+    const uint32_t a0 = cnt_le(I, u, kq), b0 = cnt_le(I, v, kq);
+    const uint32_t la = u.dW - a0, lb = v.dW - b0;
+    const uint2 *A = I.segS + u.start + a0, *Bs = I.segS + v.start + b0;
+    uint32_t lo = n > lb ? n - lb : 0u, hi = min(n, la);
+    while (lo < hi) {  // smallest i whose A[i] comes after B[n - i - 1]
+        const uint32_t i = (lo + hi) >> 1;
+        if ((A[i].x >> 1) < (Bs[n - i - 1].x >> 1)) lo = i + 1;
+        else hi = i;
     }
-    return lo;
+    const int32_t ka = lo ? (int32_t)(A[lo - 1].x >> 1) : -1, kb = n - lo ? (int32_t)(Bs[n - lo - 1].x >> 1) : -1;
+    return max(ka, kb);
 }
 
 // ---- kernels ---------------------------------------------------------------------------------------------------
 
 // Persistent vertices of the batch: find-or-insert, degree limit (reading R17c), per-segment info, and S's growth
 // from every closed estimator whose f1 touches a batch vertex (sum over batch arcs of ncl(x)).
-__global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long long *S) {
+__global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long long *S, unsigned long long *stats) {
     const BatchDesc d = *I.d;
     if (I.ctr[kCtrErr]) {  // rejected (this batch or an earlier asynchronous one): record the first, change nothing
         if (blockIdx.x == 0 && threadIdx.x == 0 && I.ctr[kCtrFailB] == 0xFFFFFFFFu) I.ctr[kCtrFailB] = d.batch;
         return;
     }
     unsigned long long grow = 0;
+    uint32_t nv = 0;  // distinct vertices (the bench's byte model: tc_stats out[2], out[3])
     for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < 2 * I.w; s += gridDim.x * blockDim.x) {
         const uint32_t val = I.segS[s].x;
         const uint32_t x = arc_vertex(I.L.E, val);
@@ -257,6 +276,7 @@ __global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long 
         VertProbe P;
         vt_issue(I.L, x, P);
         const uint32_t dW = vt_resolve(I.L, P, x).x;
+        ++nv;
         const uint32_t p = pv_insert(e, x, I.ctr);
         if (p == kEdNil) continue;
         const uint4 pv = e.pv[p];
@@ -265,8 +285,15 @@ __global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long 
         grow += (unsigned long long)dW * pv.z;
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) grow += __shfl_xor_sync(kFullMask, grow, off);
-    if ((threadIdx.x & 31u) == 0 && grow) atomicAdd(S + d.slot, grow);
+    for (int off = 16; off > 0; off >>= 1) {
+        grow += __shfl_xor_sync(kFullMask, grow, off);
+        nv += __shfl_xor_sync(kFullMask, nv, off);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (grow) atomicAdd(S + d.slot, grow);
+        if (nv) atomicAdd(stats + 2, (unsigned long long)nv);
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats + 3, 1ull);
+    }
 }
 
 // Watches that fire in this batch -> the queue.  A full sweep instead clears the watch maps (every estimator is
@@ -328,7 +355,7 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
                   0ull, false};
         uint32_t J = e.J[t], t1 = e.t1[t], u = e.u[t], v = e.v[t], B = e.B[t], K = e.K[t], t2 = e.t2[t], y = e.y[t],
                  fl = e.fl[t];
-        const uint32_t uo = u, vo = v, Bo = B, t1o = t1;
+        const uint32_t uo = u, vo = v, Bo = B, t1o = t1, J_o = J, t2o = t2;
         const bool closed_o = (fl & 1u) != 0;
         // the batch in time order, one f1 epoch at a time: f2 events (clause 3) of the current f1 up to the next f1
         // replacement (clause 1) inside the batch, then that replacement -- the random words are used in event
@@ -410,18 +437,31 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
                 atomicAdd(&e.pv[iv.pvs].z, 1u);
             }
         }
-        // re-arm
-        const uint32_t ver = e.ver[t] + 1u;
-        if (J != kEdInf) watch(e, e.amap, e.a_mask, kJKey, J, t, ver, I.ctr);
-        if (t1 && K != kEdInf) {
-            const uint32_t delta = B + K - du_end - dv_end;  // >= 1
-            const uint32_t a = (delta + 1u) >> 1, b = delta + 1u - a;
-            watch(e, e.amap, e.a_mask, u, du_end + a, t, ver, I.ctr);
-            watch(e, e.amap, e.a_mask, v, dv_end + b, t, ver, I.ctr);
+        // re-arm: the degree watches always (their split depends on the degrees now); the time and pair watches only
+        // when they changed (the old node is still armed otherwise), or after a full sweep cleared the maps
+        uint32_t ver = e.ver[t];
+        if (full || J != J_o) {
+            ver = ver_bump(ver, kWJ);
+            if (J != kEdInf) watch(e, e.amap, e.a_mask, kJKey, J, t, ver, kWJ, I.ctr);
         }
-        if (t2 && !closed) {
-            const uint32_t z = (fl & 2u) ? u : v;
-            watch(e, e.pmap, e.p_mask, min(z, y), max(z, y), t, ver, I.ctr);
+        ver = ver_bump(ver, kWT);
+        if (t1 && K != kEdInf) {
+            // chi reaches K once deg(u) + deg(v) has grown by delta more: split delta + 1 between u and v in
+            // proportion to their degrees (a proxy of their arrival rates), so that the first watch to fire tends to
+            // be close to the event itself; any split with a, b >= 1 and a + b = delta + 1 is exact
+            const uint32_t delta = B + K - du_end - dv_end;  // >= 1
+            uint32_t a = (uint32_t)((uint64_t)(delta + 1u) * du_end / ((uint64_t)du_end + dv_end));
+            a = min(max(a, 1u), delta);
+            const uint32_t b = delta + 1u - a;
+            watch(e, e.amap, e.a_mask, u, du_end + a, t, ver, kWT, I.ctr);
+            watch(e, e.amap, e.a_mask, v, dv_end + b, t, ver, kWT, I.ctr);
+        }
+        if (full || t2 != t2o || closed != closed_o) {
+            ver = ver_bump(ver, kWP);
+            if (t2 && !closed) {
+                const uint32_t z = (fl & 2u) ? u : v;
+                watch(e, e.pmap, e.p_mask, min(z, y), max(z, y), t, ver, kWP, I.ctr);
+            }
         }
         e.ver[t] = ver;
         e.J[t] = J;
@@ -643,11 +683,12 @@ static EdIdx ed_idx(const IndexBufs &ix, const BatchArgs &a) {
                  ix.ctr, ix.desc, a.g.w};
 }
 
-int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, cudaStream_t s, const KRec &kr) {
+int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, cudaStream_t s,
+                    const KRec &kr) {
     const EdIdx I = ed_idx(ix, a);
     const uint32_t g_arcs = grid_of(2ull * a.g.w, 8);
     kr.beg(K_ED_PRE, s);
-    k_ed_pre<<<g_arcs, 256, 0, s>>>(I, e, a.S);
+    k_ed_pre<<<g_arcs, 256, 0, s>>>(I, e, a.S, stats);
     kr.end(K_ED_PRE, s);
     kr.beg(K_ED_TRIGGER, s);
     k_ed_trigger<<<std::max<uint32_t>(grid_of(a.g.w, 8), (uint32_t)sm_count() * 4), 256, 0, s>>>(I, e);

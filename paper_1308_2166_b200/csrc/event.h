@@ -8,7 +8,7 @@
 //   (kJKey, J)           -- the batch contains stream time J;
 //   (x, theta)           -- vertex x reaches degree theta (the two halves of the remaining adjacency count);
 //   closing pair (a, b)  -- the batch contains the closing edge of (f1, f2).
-// Batches early in the stream (m < 8 w, or m < r / 8, where most estimators change anyway) and every batch after
+// Batches early in the stream (m < 8 w, where most estimators change anyway) and every batch after
 // the watch-node pool passed its threshold are full sweeps: every estimator is processed and all watch lists are
 // rebuilt.
 #pragma once
@@ -65,8 +65,10 @@ bool ed_alloc_seg(EdDev &e, uint64_t wcap);  // with the index (2 wcap entries)
 int launch_ed_init(const EdDev &e, cudaStream_t s);
 // Re-insert the persistent vertices into a table of new_cap slots (replaces e.pv / e.pv_mask on success).
 int ed_rehash_pv(EdDev &e, uint64_t new_cap, cudaStream_t s);
-// The four kernels of a batch (after the index): k_ed_pre, k_ed_trigger, k_ed_process, k_ed_post.
-int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, cudaStream_t s, const KRec &kr);
+// The four kernels of a batch (after the index): k_ed_pre, k_ed_trigger, k_ed_process, k_ed_post.  stats: the bulk
+// state's event counters (tc_stats): out[2] += distinct vertices of the batch, out[3] += 1.
+int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, cudaStream_t s,
+                    const KRec &kr);
 // The NBSI view of the state (r1, p1, r2, p2, chi | closed) into the bulk state buffers.
 int launch_ed_export(const EdDev &e, const StateBufs &st, cudaStream_t s);
 
