@@ -271,8 +271,8 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
  *                vertex degree > 2^30 - 1 is rejected with TC_EOVERFLOW (reading R17c).  tc_set_state and
  *                tc_set_counters return TC_EINVAL in this mode.
  * Only on a handle that has seen no batch (fresh or after tc_reset), else TC_EINVAL.  The event mode allocates
- * about 1 KB per estimator of watch tables (12 watch nodes, 16-byte map slots at load <= 1/2) plus 32 bytes per
- * distinct vertex seen.  Synchronises. */
+ * about 2.1 KB per estimator of watch tables (16 64-byte watch chunks, two maps of 16-byte slots at load <= 1/2)
+ * plus 32 bytes per distinct vertex seen (table load <= 1/2).  Synchronises. */
 enum { TC_MODE_BULK = 0, TC_MODE_EVENT = 1 };
 int tc_set_mode(tc_ctx *ctx, int mode);
 

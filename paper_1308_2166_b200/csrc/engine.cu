@@ -534,9 +534,13 @@ static int push_prepare(tc_ctx *ctx, const tc_edge *edges, uint64_t w, PushPrep 
     return TC_OK;
 }
 
-// a4-a8: the bulk estimator pass (fused, or split per step), or the event mode's four kernels
+// Event mode: can a vertex degree reach the limit in this batch (m + w > 2^30 - 1)?  Then the degrees are checked
+// first and applied by a separate kernel once the batch is accepted.
+static bool ed_post(const tc_ctx *ctx, uint64_t w) { return ctx->m + w > (uint64_t)kEdDegMax; }
+
+// a4-a8: the bulk estimator pass (fused, or split per step), or the event mode's kernels
 static uint32_t estimator_pass(tc_ctx *ctx, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
-    if (ctx->mode == TC_MODE_EVENT) return launch_ed_batch(ctx->ix, a, ctx->ed, ctx->st.stats, s, kr);
+    if (ctx->mode == TC_MODE_EVENT) return launch_ed_batch(ctx->ix, a, ctx->ed, ctx->st.stats, ed_post(ctx, a.g.w), s, kr);
     if (ctx->tune.split) return launch_update_split(ctx->ix, ctx->st, ctx->steps, a, s, kr);
     return launch_update(ctx->ix, ctx->st, a, s, kr);
 }
@@ -594,7 +598,8 @@ static uint32_t *ed_ctr(const tc_ctx *ctx) { return ctx->mode == TC_MODE_EVENT ?
 // The graph of a batch shape: found in the cache, or captured (k_desc + the kernels) and instantiated.
 static int graph_for(tc_ctx *ctx, const BatchArgs &a, const BatchDesc &d, tc_ctx::GraphEntry **out) {
     const uint64_t key = (uint64_t)a.g.w | ((uint64_t)a.small << 32) | ((uint64_t)ctx->tune.split << 33) |
-                         ((uint64_t)a.g.small_index << 34) | ((uint64_t)ctx->mode << 35);
+                         ((uint64_t)a.g.small_index << 34) | ((uint64_t)ctx->mode << 35) |
+                         ((uint64_t)(ctx->mode == TC_MODE_EVENT && ed_post(ctx, a.g.w)) << 36);
     for (auto &g : ctx->graphs)
         if (g.key == key) {
             g.last_use = ++ctx->graph_clock;
@@ -682,7 +687,7 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     if (ctx->mode == TC_MODE_EVENT) {
         // S carries over; a full sweep early in the stream (m < 8 w), where most estimators change anyway
         const bool full = ctx->m < 8 * w;
-        d.pad = 1u | (full ? 2u : 0u);
+        d.pad = 1u | (full ? 2u : 0u) | (ed_post(ctx, w) ? 0u : 4u);
         const int rc = ed_reserve_vertices(ctx, w);
         if (rc != TC_OK) return rc;
     }

@@ -161,30 +161,98 @@ __device__ __forceinline__ uint32_t ver_bump(uint32_t ver, uint32_t kind) {
                        : kind == kWT ? ((ver & ~(0x7FFu << 10)) | ((f & 0x7FFu) << 10)) : ((ver & 0x1FFFFFu) | (f << 21));
 }
 
-// push watch node (est, kind, version) onto the list of key (k0, k1)
+// One slot per active lane of the calling (possibly divergent) warp: lanes with want get consecutive indices from
+// *ctr (one atomic per warp), others get kEdNil.
+__device__ __forceinline__ uint32_t warp_take(uint32_t *ctr, bool want) {
+    const uint32_t mask = __activemask();
+    const uint32_t b = __ballot_sync(mask, want);
+    if (!b) return kEdNil;
+    const uint32_t lane = threadIdx.x & 31u, leader = __ffs(b) - 1u;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(ctr, (uint32_t)__popc(b));
+    base = __shfl_sync(mask, base, leader);
+    return want ? base + (uint32_t)__popc(b & ((1u << lane) - 1u)) : kEdNil;
+}
+
+// n[lane] <= 7 consecutive slots per active lane (one atomic per warp): returns the lane's first slot.
+__device__ __forceinline__ uint32_t warp_take_n(uint32_t *ctr, uint32_t n) {
+    const uint32_t mask = __activemask();
+    const uint32_t lane = threadIdx.x & 31u, lt = (1u << lane) - 1u;
+    const uint32_t b0 = __ballot_sync(mask, n & 1u), b1 = __ballot_sync(mask, n & 2u), b2 = __ballot_sync(mask, n & 4u);
+    const uint32_t total = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+    if (!total) return 0u;
+    const uint32_t leader = __ffs(mask) - 1u;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(ctr, total);
+    base = __shfl_sync(mask, base, leader);
+    return base + __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+}
+
+// Watch lists are stacks of 64-byte chunks of kChunkNodes nodes {estimator, kind << 30 | version} with the next chunk
+// in word 14, so a list is walked one DRAM access per chunk.  The key's slot holds {head chunk, fill of the head}
+// as one 64-bit word (slot .z = head, .w = fill); a full or missing head gets a fresh chunk by CAS.
+constexpr uint32_t kChunkNodes = 7;
+
+// spare: a chunk taken for this watch in advance (it stays unused when the node fits the key's head chunk)
 __device__ void watch(const EdDev &e, uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1, uint32_t est, uint32_t ver,
-                      uint32_t kind, uint32_t *ixctr) {
+                      uint32_t kind, uint32_t spare, uint32_t *ixctr) {
     const uint32_t s = map_insert(map, mask, k0, k1, ixctr);
     if (s == kEdNil) return;
-    const uint32_t node = atomicAdd(&e.ctr[kEdPool], 1u);
-    if (node >= e.pool_cap) {
+    unsigned long long *hf = reinterpret_cast<unsigned long long *>(&map[s].z);
+    const uint2 node = make_uint2(est, (kind << 30) | ver_of(ver, kind));
+    if (spare >= e.pool_cap) {
         atomicOr(&ixctr[kCtrErr], kErrInternal);
         return;
     }
-    const uint32_t prev = atomicExch(&map[s].z, node);
-    e.pool[node] = make_uint4(est, ver_of(ver, kind), prev, kind);
+    // a key just created has the cleared {NIL, ~0} or detached {NIL, 0} word: try installing the chunk directly
+    reinterpret_cast<uint32_t *>(e.pool + 4ull * spare)[14] = kEdNil;
+    if (atomicCAS(hf, ~0ull, (1ull << 32) | spare) == ~0ull ||
+        atomicCAS(hf, (unsigned long long)kEdNil, (1ull << 32) | spare) == (unsigned long long)kEdNil) {
+        reinterpret_cast<uint2 *>(e.pool + 4ull * spare)[0] = node;
+        return;
+    }
+    for (uint32_t it = 0; it < 1024u; ++it) {
+        const unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(hf);
+        const uint32_t head = (uint32_t)old, fill = (uint32_t)(old >> 32);
+        if (head != kEdNil && fill < kChunkNodes) {
+            if (atomicCAS(hf, old, old + (1ull << 32)) == old) {
+                reinterpret_cast<uint2 *>(e.pool + 4ull * head)[fill] = node;
+                return;
+            }
+        } else {
+            reinterpret_cast<uint32_t *>(e.pool + 4ull * spare)[14] = head;
+            if (atomicCAS(hf, old, (1ull << 32) | spare) == old) {
+                reinterpret_cast<uint2 *>(e.pool + 4ull * spare)[0] = node;
+                return;
+            }
+        }
+    }
+    atomicOr(&ixctr[kCtrErr], kErrInternal);  // never: a bounded retry loop instead of a possible hang
 }
 
 // detach the list at slot s and queue its live estimators (each at most once per batch)
 __device__ void fire(const EdDev &e, uint4 *map, uint32_t s, uint32_t tag) {
-    uint32_t h = atomicExch(&map[s].z, kEdNil);
-    for (uint32_t n = 0; h != kEdNil && n < e.pool_cap; ++n) {
-        const uint4 nd = e.pool[h];
-        if (nd.y == ver_of(e.ver[nd.x], nd.w) && atomicExch(&e.stamp[nd.x], tag) != tag) {
-            const uint32_t q = atomicAdd(&e.ctr[kEdQueue], 1u);
-            e.queue[q] = nd.x;
+    const unsigned long long old = atomicExch(reinterpret_cast<unsigned long long *>(&map[s].z), (unsigned long long)kEdNil);
+    uint32_t c = (uint32_t)old, n = min((uint32_t)(old >> 32), kChunkNodes);
+    for (uint32_t hops = 0; c != kEdNil && hops < e.pool_cap; ++hops) {
+        const uint4 *ch = e.pool + 4ull * c;
+        const uint4 q0 = ch[0], q1 = ch[1], q2 = ch[2], q3 = ch[3];
+        const uint32_t w[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+        uint2 vs[kChunkNodes];
+#pragma unroll
+        for (uint32_t j = 0; j < kChunkNodes; ++j)  // the versions of all nodes of the chunk in flight together
+            if (j < n) vs[j] = e.vs[w[2 * j]];
+#pragma unroll
+        for (uint32_t j = 0; j < kChunkNodes; ++j) {
+            if (j >= n) continue;
+            const uint32_t est = w[2 * j], kv = w[2 * j + 1];
+            const bool want = (kv & 0x3FFFFFFFu) == ver_of(vs[j].x, kv >> 30) && vs[j].y != tag &&
+                              atomicExch(&e.vs[est].y, tag) != tag;
+            const uint32_t q = warp_take(&e.ctr[kEdQueue], want);
+            if (want) e.queue[q] = est;
         }
-        h = nd.z;
+        c = w[14];
+        n = kChunkNodes;
     }
 }
 
@@ -209,10 +277,7 @@ struct VInfo {
     uint32_t dold, pvs, dW, start;  // degree before the batch, pv slot, arcs in the batch, segment start
 };
 
-__device__ __forceinline__ VInfo vinfo(const EdIdx &I, const EdDev &e, uint32_t x) {
-    VertProbe P;
-    vt_issue(I.L, x, P);
-    const uint2 r = vt_resolve(I.L, P, x);  // {deg_W, segment start} or {0, 0}
+__device__ __forceinline__ VInfo vinfo_of(const EdDev &e, uint32_t x, uint2 r) {
     VInfo v;
     if (r.x) {
         const uint4 s = e.seg[r.y];
@@ -230,8 +295,26 @@ __device__ __forceinline__ VInfo vinfo(const EdIdx &I, const EdDev &e, uint32_t 
     return v;
 }
 
+__device__ __forceinline__ VInfo vinfo(const EdIdx &I, const EdDev &e, uint32_t x) {
+    VertProbe P;
+    vt_issue(I.L, x, P);
+    return vinfo_of(e, x, vt_resolve(I.L, P, x));  // {deg_W, segment start} or {0, 0}
+}
+
+// both endpoints, their probes issued together
+__device__ __forceinline__ void vinfo2(const EdIdx &I, const EdDev &e, uint32_t x, uint32_t y, VInfo &ix, VInfo &iy) {
+    VertProbe P, Q;
+    vt_issue(I.L, x, P);
+    vt_issue(I.L, y, Q);
+    const uint2 rx = vt_resolve(I.L, P, x), ry = vt_resolve(I.L, Q, y);
+    ix = vinfo_of(e, x, rx);
+    iy = vinfo_of(e, y, ry);
+}
+
 // arcs of vertex v in the batch with batch index <= kmax (kmax = -1: none)
 __device__ __forceinline__ uint32_t cnt_le(const EdIdx &I, const VInfo &v, int32_t kmax) {
+    if (kmax < 0) return 0u;
+    if (kmax >= (int32_t)I.w - 1) return v.dW;  // the whole batch: no search
     uint32_t a = 0, b = v.dW;
     while (a < b) {
         const uint32_t mid = (a + b) >> 1;
@@ -258,6 +341,17 @@ __device__ int32_t kth_after(const EdIdx &I, const VInfo &u, const VInfo &v, int
 }
 
 // ---- kernels ---------------------------------------------------------------------------------------------------
+// The per-batch kernels are latency chains with little data each (a few thousand items over 148 SMs): items are
+// dealt lane-major -- item i to warp i mod W, lane i / W for the W warps of the grid -- so that a small batch puts
+// one or two items in each of many warps rather than 32 divergent lanes in a few.
+struct Spread {
+    uint32_t first, step;
+};
+__device__ __forceinline__ Spread spread() {
+    const uint32_t nw = gridDim.x * (blockDim.x >> 5), wid = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    return Spread{(threadIdx.x & 31u) * nw + wid, 32u * nw};
+}
+
 
 // Persistent vertices of the batch: find-or-insert, degree limit (reading R17c), per-segment info, and S's growth
 // from every closed estimator whose f1 touches a batch vertex (sum over batch arcs of ncl(x)).
@@ -269,7 +363,8 @@ __global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long 
     }
     unsigned long long grow = 0;
     uint32_t nv = 0;  // distinct vertices (the bench's byte model: tc_stats out[2], out[3])
-    for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < 2 * I.w; s += gridDim.x * blockDim.x) {
+    const Spread sp = spread();
+    for (uint32_t s = sp.first; s < 2 * I.w; s += sp.step) {
         const uint32_t val = I.segS[s].x;
         const uint32_t x = arc_vertex(I.L.E, val);
         if (s > 0 && arc_vertex(I.L.E, I.segS[s - 1].x) == x) continue;  // not the first arc of x's segment
@@ -280,7 +375,8 @@ __global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long 
         const uint32_t p = pv_insert(e, x, I.ctr);
         if (p == kEdNil) continue;
         const uint4 pv = e.pv[p];
-        if ((uint64_t)pv.y + dW > kEdDegMax) atomicOr(&I.ctr[kCtrErr], kErrOvf);
+        if (d.pad & 4u) e.pv[p].y = pv.y + dW;  // no degree can pass the limit (host): the update is done here
+        else if ((uint64_t)pv.y + dW > kEdDegMax) atomicOr(&I.ctr[kCtrErr], kErrOvf);
         e.seg[s] = make_uint4(pv.y, p, dW, s);
         grow += (unsigned long long)dW * pv.z;
     }
@@ -314,24 +410,29 @@ __global__ void __launch_bounds__(256) k_ed_trigger(EdIdx I, EdDev e) {
     }
     const uint32_t tag = d.batch + 1u;
     const uint32_t t0 = (uint32_t)d.m_prev + 1u;  // stream time of batch edge 0
-    for (uint32_t k = tid; k < I.w; k += nth) {
-        const uint32_t sj = map_find(e.amap, e.a_mask, kJKey, t0 + k);
-        if (sj != kEdNil) fire(e, e.amap, sj, tag);
-        const uint2 ed = I.L.E[k];
-        const uint32_t sp = map_find(e.pmap, e.p_mask, ed.x, ed.y);
-        if (sp != kEdNil) fire(e, e.pmap, sp, tag);
-        const uint2 ap = I.apos[k];
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-            const uint32_t x = side ? ed.y : ed.x;
-            const uint2 ps = I.pslot[side ? ap.y : ap.x];  // {slot, segment end}
+    const Spread sp = spread();
+    for (uint32_t i = sp.first; i < 4 * I.w; i += sp.step) {  // item (edge k, kind): time, pair, lo arc, hi arc
+        const uint32_t k = i >> 2, kind = i & 3u;
+        uint32_t sl;
+        uint4 *map = e.amap;
+        if (kind == 0) {
+            sl = map_find(e.amap, e.a_mask, kJKey, t0 + k);
+        } else if (kind == 1) {
+            const uint2 ed = I.L.E[k];
+            map = e.pmap;
+            sl = map_find(e.pmap, e.p_mask, ed.x, ed.y);
+        } else {
+            const uint2 ed = I.L.E[k];
+            const uint32_t x = kind == 3 ? ed.y : ed.x;
+            const uint2 ap = I.apos[k];
+            const uint2 ps = I.pslot[kind == 3 ? ap.y : ap.x];  // {slot, segment end}
             VertProbe P;
             vt_issue(I.L, x, P);
             const uint2 r = vt_resolve(I.L, P, x);  // {deg_W, start}
             const uint32_t theta = e.seg[r.y].x + (ps.x - r.y) + 1u;  // x's degree once this arc has arrived
-            const uint32_t st = map_find(e.amap, e.a_mask, x, theta);
-            if (st != kEdNil) fire(e, e.amap, st, tag);
+            sl = map_find(e.amap, e.a_mask, x, theta);
         }
+        if (sl != kEdNil) fire(e, map, sl, tag);
     }
 }
 
@@ -347,7 +448,8 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
     L.ptag = d.ptag;
     unsigned long long dS = 0;
     uint32_t visited = 0, events = 0;
-    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const Spread sp = full ? Spread{blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x} : spread();
+    for (uint32_t q = sp.first; q < nq; q += sp.step) {
         const uint32_t t = full ? q : e.queue[q];
         ++visited;
         const uint64_t gid = e.first + t;
@@ -361,10 +463,7 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
         // replacement (clause 1) inside the batch, then that replacement -- the random words are used in event
         // order, as the per-edge rule uses them
         VInfo iu, iv;
-        if (t1) {
-            iu = vinfo(I, e, u);
-            iv = vinfo(I, e, v);
-        }
+        if (t1) vinfo2(I, e, u, v, iu, iv);
         int32_t kq = -1;  // events of the current f1 are after batch index kq
         for (;;) {
             const bool jin = J != kEdInf && J <= Pend;
@@ -392,10 +491,10 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             ++events;
             kq = (int32_t)(t1 - P0 - 1u);
             const uint2 ed = L.E[kq];
+ 
             u = ed.x;
             v = ed.y;
-            iu = vinfo(I, e, u);
-            iv = vinfo(I, e, v);
+            vinfo2(I, e, u, v, iu, iv);
             B = iu.dold + cnt_le(I, iu, kq) + iv.dold + cnt_le(I, iv, kq);
             K = 1u;
             t2 = 0u;
@@ -419,7 +518,8 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             if (t1 == t1o) {
                 c_old = du_end + dv_end - Bo;
             } else {
-                const VInfo a = vinfo(I, e, uo), b = vinfo(I, e, vo);
+                VInfo a, b;
+                vinfo2(I, e, uo, vo, a, b);
                 c_old = a.dold + a.dW + b.dold + b.dW - Bo;
                 atomicSub(&e.pv[a.pvs].z, 1u);
                 atomicSub(&e.pv[b.pvs].z, 1u);
@@ -439,13 +539,16 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
         }
         // re-arm: the degree watches always (their split depends on the degrees now); the time and pair watches only
         // when they changed (the old node is still armed otherwise), or after a full sweep cleared the maps
-        uint32_t ver = e.ver[t];
+        uint32_t ver = e.vs[t].x;
+        const bool armJ = (full || J != J_o) && J != kEdInf, armT = t1 && K != kEdInf,
+                   newP = full || t2 != t2o || closed != closed_o, armP = newP && t2 && !closed;
+        uint32_t chunk = warp_take_n(&e.ctr[kEdPool], (armJ ? 1u : 0u) + (armT ? 2u : 0u) + (armP ? 1u : 0u));
         if (full || J != J_o) {
             ver = ver_bump(ver, kWJ);
-            if (J != kEdInf) watch(e, e.amap, e.a_mask, kJKey, J, t, ver, kWJ, I.ctr);
+            if (armJ) watch(e, e.amap, e.a_mask, kJKey, J, t, ver, kWJ, chunk++, I.ctr);
         }
         ver = ver_bump(ver, kWT);
-        if (t1 && K != kEdInf) {
+        if (armT) {
             // chi reaches K once deg(u) + deg(v) has grown by delta more: split delta + 1 between u and v in
             // proportion to their degrees (a proxy of their arrival rates), so that the first watch to fire tends to
             // be close to the event itself; any split with a, b >= 1 and a + b = delta + 1 is exact
@@ -453,17 +556,17 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             uint32_t a = (uint32_t)((uint64_t)(delta + 1u) * du_end / ((uint64_t)du_end + dv_end));
             a = min(max(a, 1u), delta);
             const uint32_t b = delta + 1u - a;
-            watch(e, e.amap, e.a_mask, u, du_end + a, t, ver, kWT, I.ctr);
-            watch(e, e.amap, e.a_mask, v, dv_end + b, t, ver, kWT, I.ctr);
+            watch(e, e.amap, e.a_mask, u, du_end + a, t, ver, kWT, chunk++, I.ctr);
+            watch(e, e.amap, e.a_mask, v, dv_end + b, t, ver, kWT, chunk++, I.ctr);
         }
-        if (full || t2 != t2o || closed != closed_o) {
+        if (newP) {
             ver = ver_bump(ver, kWP);
-            if (t2 && !closed) {
+            if (armP) {
                 const uint32_t z = (fl & 2u) ? u : v;
-                watch(e, e.pmap, e.p_mask, min(z, y), max(z, y), t, ver, kWP, I.ctr);
+                watch(e, e.pmap, e.p_mask, min(z, y), max(z, y), t, ver, kWP, chunk++, I.ctr);
             }
         }
-        e.ver[t] = ver;
+        e.vs[t].x = ver;
         e.J[t] = J;
         e.t1[t] = t1;
         e.u[t] = u;
@@ -511,8 +614,7 @@ __global__ void k_ed_init(EdDev e) {
         e.t2[t] = 0u;
         e.y[t] = kEmptyV;
         e.fl[t] = 0u;
-        e.ver[t] = 0u;
-        e.stamp[t] = 0u;
+        e.vs[t] = make_uint2(0u, 0u);
         e.ev[t] = 0u;
     }
     const uint4 empty = make_uint4(kEmptyV, kEmptyV, kEdNil, kEmptyV);
@@ -594,21 +696,24 @@ bool ed_alloc(EdDev &e, uint64_t count, uint64_t first, uint64_t seed, uint64_t 
     e.first = first;
     e.seed = seed;
     const uint64_t n = std::max<uint64_t>(count, 1);
-    // watch nodes: a full sweep arms at most 4 per estimator, a batch at most 4 per estimator; a rebuild is due
-    // once more than 8 n are in use, so 12 n + slack always suffice
-    const uint64_t pool = 12 * n + 4096;
-    if (pool > 0xFFFFFFF0ull) return false;
+    // watch chunks (64 B, 7 nodes; every armed watch takes one): a sweep arms at most 4 per estimator, a batch at
+    // most 4 per estimator it visits; a rebuild is due once more than 12 n are in use, so 16 n + slack always
+    // suffice.  Every key owns at least one chunk, so the maps (load <= 1/2) get 2 slots per chunk.  (~1.5 KB per
+    // estimator in all: the rebuilds -- a full sweep, O(r) -- stay rare.)
+    const uint64_t pool = 16 * n + 4096;
+    if (pool > 0x7FFFFFF0ull) return false;
     e.pool_cap = (uint32_t)pool;
-    const uint64_t acap = pow2_at_least(2 * (9 * n + 4096)), pcap = pow2_at_least(2 * (3 * n + 4096));
+    const uint64_t acap = pow2_at_least(2 * pool), pcap = acap;
     const uint64_t vcap = pow2_at_least(std::max<uint64_t>(pv_cap, 1024));
     if (acap > (1ull << 32) || pcap > (1ull << 32) || vcap > (1ull << 32)) return false;
     e.a_mask = (uint32_t)(acap - 1);
     e.p_mask = (uint32_t)(pcap - 1);
     e.pv_mask = (uint32_t)(vcap - 1);
-    uint32_t **soa[] = {&e.J, &e.t1, &e.u, &e.v, &e.B, &e.K, &e.t2, &e.y, &e.fl, &e.ver, &e.stamp, &e.ev, &e.queue};
+    uint32_t **soa[] = {&e.J, &e.t1, &e.u, &e.v, &e.B, &e.K, &e.t2, &e.y, &e.fl, &e.ev, &e.queue};
     bool ok = true;
     for (uint32_t **p : soa) ok = ok && cudaMalloc(p, 4 * n) == cudaSuccess;
-    ok = ok && cudaMalloc(&e.pool, 16 * pool) == cudaSuccess && cudaMalloc(&e.amap, 16 * acap) == cudaSuccess &&
+    ok = ok && cudaMalloc(&e.vs, 8 * n) == cudaSuccess &&
+         cudaMalloc(&e.pool, 64 * pool) == cudaSuccess && cudaMalloc(&e.amap, 16 * acap) == cudaSuccess &&
          cudaMalloc(&e.pmap, 16 * pcap) == cudaSuccess && cudaMalloc(&e.pv, 16 * vcap) == cudaSuccess &&
          cudaMalloc(&e.ctr, 4 * kEdWords) == cudaSuccess;
     if (!ok) {
@@ -619,7 +724,7 @@ bool ed_alloc(EdDev &e, uint64_t count, uint64_t first, uint64_t seed, uint64_t 
 }
 
 void ed_free(EdDev &e) {
-    void *bufs[] = {e.J, e.t1, e.u, e.v, e.B, e.K, e.t2, e.y, e.fl, e.ver, e.stamp, e.ev, e.queue,
+    void *bufs[] = {e.J, e.t1, e.u, e.v, e.B, e.K, e.t2, e.y, e.fl, e.vs, e.ev, e.queue,
                     e.pool, e.amap, e.pmap, e.pv, e.ctr, e.seg};
     for (void *p : bufs) cudaFree(p);
     e = EdDev();
@@ -639,9 +744,9 @@ int launch_ed_init(const EdDev &e, cudaStream_t s) {
     const uint64_t items = std::max<uint64_t>({e.count, (uint64_t)e.a_mask + 1, (uint64_t)e.p_mask + 1,
                                                (uint64_t)e.pv_mask + 1});
     k_ed_init<<<grid_of(items, 16), 256, 0, s>>>(e);
-    // rebuild threshold: more than 8 nodes per estimator in use (see ed_alloc)
-    k_ed_set_thr<<<1, 1, 0, s>>>(e.ctr, (uint32_t)std::min<uint64_t>(8 * std::max<uint64_t>(e.count, 1) + 1024,
-                                                                     e.pool_cap - 4 * std::max<uint64_t>(e.count, 1)));
+    // rebuild threshold: more than 12 chunks per estimator in use (see ed_alloc)
+    const uint64_t n = std::max<uint64_t>(e.count, 1);
+    k_ed_set_thr<<<1, 1, 0, s>>>(e.ctr, (uint32_t)std::min<uint64_t>(12 * n + 1024, e.pool_cap - 4 * n));
     return 2;
 }
 
@@ -683,19 +788,20 @@ static EdIdx ed_idx(const IndexBufs &ix, const BatchArgs &a) {
                  ix.ctr, ix.desc, a.g.w};
 }
 
-int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, cudaStream_t s,
-                    const KRec &kr) {
+int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, bool post,
+                    cudaStream_t s, const KRec &kr) {
     const EdIdx I = ed_idx(ix, a);
-    const uint32_t g_arcs = grid_of(2ull * a.g.w, 8);
+    const uint32_t g_arcs = grid_of(2ull * a.g.w, 8), g_spread = std::max<uint32_t>(g_arcs, (uint32_t)sm_count() * 4);
     kr.beg(K_ED_PRE, s);
-    k_ed_pre<<<g_arcs, 256, 0, s>>>(I, e, a.S, stats);
+    k_ed_pre<<<g_spread, 256, 0, s>>>(I, e, a.S, stats);
     kr.end(K_ED_PRE, s);
     kr.beg(K_ED_TRIGGER, s);
-    k_ed_trigger<<<std::max<uint32_t>(grid_of(a.g.w, 8), (uint32_t)sm_count() * 4), 256, 0, s>>>(I, e);
+    k_ed_trigger<<<std::max<uint32_t>(grid_of(4ull * a.g.w, 8), (uint32_t)sm_count() * 4), 256, 0, s>>>(I, e);
     kr.end(K_ED_TRIGGER, s);
     kr.beg(K_ED_PROCESS, s);
     k_ed_process<<<(uint32_t)sm_count() * 4, 256, 0, s>>>(I, e, a.S);
     kr.end(K_ED_PROCESS, s);
+    if (!post) return 3;
     kr.beg(K_ED_POST, s);
     k_ed_post<<<g_arcs, 256, 0, s>>>(I, e);
     kr.end(K_ED_POST, s);

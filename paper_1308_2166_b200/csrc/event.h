@@ -27,7 +27,7 @@ constexpr uint32_t kEdNil = 0xFFFFFFFFu;
 constexpr uint32_t kJKey = 0xFFFFFFFFu;    // the reserved vertex id: (kJKey, t) watches stream time t
 
 // counters (EdDev::ctr)
-constexpr int kEdPool = 0;     // watch nodes in use
+constexpr int kEdPool = 0;     // watch chunks in use
 constexpr int kEdQueue = 1;    // estimators queued in this batch
 constexpr int kEdFull = 2;     // this batch is a full sweep (set by k_desc)
 constexpr int kEdPVN = 3;      // vertices in the persistent table
@@ -39,9 +39,10 @@ constexpr int kEdWords = 8;
 
 struct EdDev {
     // estimator SoA: J, f1 = (u, v) at time t1 (0: none), B = deg_t1(u) + deg_t1(v), K, f2 at time t2 = (shared,
-    // y) with fl bit 1 = "shared is v", fl bit 0 = closed; ver = watch version, stamp = last batch queued,
-    // ev = random words used
-    uint32_t *J, *t1, *u, *v, *B, *K, *t2, *y, *fl, *ver, *stamp, *ev;
+    // y) with fl bit 1 = "shared is v", fl bit 0 = closed; ev = random words used; vs = {watch versions (time,
+    // degree, pair: 10 / 11 / 11 bits), last batch the estimator was queued in}
+    uint32_t *J, *t1, *u, *v, *B, *K, *t2, *y, *fl, *ev;
+    uint2 *vs;
     uint64_t count, first, seed;
     uint4 *pv;        // persistent vertices {id, degree, closed estimators with it as an f1 endpoint, 0}
     uint32_t pv_mask;
@@ -49,8 +50,8 @@ struct EdDev {
     uint32_t a_mask;
     uint4 *pmap;      // closing-pair watches
     uint32_t p_mask;
-    uint4 *pool;      // watch nodes {estimator, version, next, 0}
-    uint32_t pool_cap;
+    uint4 *pool;      // watch chunks: 64 B = 7 nodes {estimator, kind << 30 | version} + the next chunk (word 14)
+    uint32_t pool_cap;  // chunks
     uint32_t *queue;  // [count] estimators to process in this batch
     uint4 *seg;       // [2 wcap] at each vertex segment's first slot: {degree before the batch, pv slot, degree in
                       // the batch, segment start}
@@ -65,10 +66,12 @@ bool ed_alloc_seg(EdDev &e, uint64_t wcap);  // with the index (2 wcap entries)
 int launch_ed_init(const EdDev &e, cudaStream_t s);
 // Re-insert the persistent vertices into a table of new_cap slots (replaces e.pv / e.pv_mask on success).
 int ed_rehash_pv(EdDev &e, uint64_t new_cap, cudaStream_t s);
-// The four kernels of a batch (after the index): k_ed_pre, k_ed_trigger, k_ed_process, k_ed_post.  stats: the bulk
-// state's event counters (tc_stats): out[2] += distinct vertices of the batch, out[3] += 1.
-int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, cudaStream_t s,
-                    const KRec &kr);
+// The kernels of a batch (after the index): k_ed_pre, k_ed_trigger, k_ed_process, and k_ed_post when `post` (the
+// degree limit can be reached: k_ed_pre only checks it, k_ed_post applies the degrees once the batch is accepted;
+// otherwise k_ed_pre applies them and the descriptor has pad bit 2).  stats: the bulk state's event counters
+// (tc_stats): out[2] += distinct vertices of the batch, out[3] += 1.
+int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, bool post,
+                    cudaStream_t s, const KRec &kr);
 // The NBSI view of the state (r1, p1, r2, p2, chi | closed) into the bulk state buffers.
 int launch_ed_export(const EdDev &e, const StateBufs &st, cudaStream_t s);
 
