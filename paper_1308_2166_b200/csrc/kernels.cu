@@ -1262,12 +1262,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_index(PartArgs a, VertA
     const uint2 *in = a.d->in;
     const uint32_t ptag = a.d->ptag, w = a.g.w, b = blockIdx.x, bv = a.g.bv, NB = gridDim.x;
     const uint32_t lane = threadIdx.x & 31u;
-    // validation first (every CTA, the batch is small): a rejected batch must not insert anything
+    // one coalesced pass over the batch (every CTA, the batch is small): validation -- a rejected batch must not
+    // insert anything -- and the vertex bucket of every arc into shared memory (the hash path's region, free
+    // until the grouping), so that the compaction below scans shared memory instead of the batch twice
+    uint16_t *sbk = reinterpret_cast<uint16_t *>(smem);
+    static_assert(2 * kSmallCap * 2 <= kSmallHashBytes, "arc bucket ids must fit the hash region");
     uint32_t bad = 0;
     for (uint32_t k = threadIdx.x; k < w; k += kSmallThreads) {
         const uint2 e = __ldg(in + k);
         if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
         else if (e.x == e.y) bad |= kErrLoop;
+        const uint2 n = norm_edge(e);
+        sbk[2 * k] = (uint16_t)vbucket_of(hash_vertex(n.x), bv);
+        sbk[2 * k + 1] = (uint16_t)vbucket_of(hash_vertex(n.y), bv);
     }
     bad = __reduce_or_sync(kFull, bad);
     if (bad && lane == 0) atomicOr(&a.ctr[kCtrErr], bad);
@@ -1294,17 +1301,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_index(PartArgs a, VertA
     constexpr uint32_t NWS = kSmallThreads / 32;
     const uint32_t warp = threadIdx.x >> 5, C = (2 * w + NWS - 1) / NWS;
     const uint32_t c0 = min(2 * w, warp * C), c1 = min(2 * w, c0 + C);
-    auto arc_at = [&](uint32_t ai, uint32_t &vx, uint32_t &nb) {
-        const uint2 n = norm_edge(__ldg(in + (ai >> 1)));
-        vx = (ai & 1u) ? n.y : n.x;
-        nb = (ai & 1u) ? n.x : n.y;
-        return vbucket_of(hash_vertex(vx), bv) == b;
-    };
     uint32_t cnt = 0;
     for (uint32_t ai0 = c0; ai0 < c1; ai0 += 32) {
         const uint32_t ai = ai0 + lane;
-        uint32_t vx, nb;
-        cnt += __popc(__ballot_sync(kFull, ai < c1 && arc_at(ai, vx, nb)));
+        cnt += __popc(__ballot_sync(kFull, ai < c1 && sbk[ai] == b));
     }
     uint32_t tot;
     const uint32_t wpre = block_exclusive_scan<kSmallThreads>(lane == 0 ? cnt : 0u, ws, &tot);
@@ -1312,10 +1312,11 @@ __global__ void __launch_bounds__(kSmallThreads) k_small_index(PartArgs a, VertA
     uint32_t run = 0;
     for (uint32_t ai0 = c0; ai0 < c1; ai0 += 32) {
         const uint32_t ai = ai0 + lane;
-        uint32_t vx = 0, nb = 0;
-        const bool mine = ai < c1 && arc_at(ai, vx, nb);
+        const bool mine = ai < c1 && sbk[ai] == b;
         const uint32_t m = __ballot_sync(kFull, mine);
         if (mine) {
+            const uint2 ne = norm_edge(__ldg(in + (ai >> 1)));
+            const uint32_t vx = (ai & 1u) ? ne.y : ne.x, nb = (ai & 1u) ? ne.x : ne.y;
             const uint32_t q = woff + run + __popc(m & ((1u << lane) - 1u));
             sv[q] = vx;
             sval[q] = ai;
