@@ -48,3 +48,20 @@ def test_b200_arm_json_line():
     assert d["cpu_baseline"]["cpu_model"] if "cpu_baseline" in d else True
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d.get("e2e_results_match_tc_estimate") is True
+
+
+@pytest.mark.gpu
+def test_b200_arm_event_mode_json_line():
+    """--mode event: the same contract, the event kernels attributed, the event oracle as cpu_baseline."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C1", "--mode", "event",
+                          "--whole-stream", "--warmup", "3"], capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["config"]["mode"] == "event" and d["steps"] == d["config"]["batches_per_stream"]
+    ks = d["roofline"]["kernels"]
+    assert {"k_ed_pre", "k_ed_trigger", "k_ed_process"} <= set(ks) and "k_update" not in ks
+    assert d["roofline"]["events_per_batch"]["visited"] > 0
+    assert "oracle/ed.c" in d["cpu_baseline"]["sample"] and d["value"] > 0
+    assert d.get("e2e_results_match_tc_estimate") is True
