@@ -326,8 +326,8 @@ __device__ __forceinline__ uint32_t cnt_le(const EdIdx &I, const VInfo &v, int32
 
 // batch index of the n-th (n >= 1) arc of u or v after batch index kq (the caller knows it exists): the two
 // segments are sorted by batch index and disjoint, so a binary search over how many come from u's (merge path)
-__device__ int32_t kth_after(const EdIdx &I, const VInfo &u, const VInfo &v, int32_t kq, uint32_t n) {
-    const uint32_t a0 = cnt_le(I, u, kq), b0 = cnt_le(I, v, kq);
+// a0, b0: the arcs of u and v at or before kq (cnt_le, computed once per f1 epoch)
+__device__ int32_t kth_after(const EdIdx &I, const VInfo &u, const VInfo &v, uint32_t a0, uint32_t b0, uint32_t n) {
     const uint32_t la = u.dW - a0, lb = v.dW - b0;
     const uint2 *A = I.segS + u.start + a0, *Bs = I.segS + v.start + b0;
     uint32_t lo = n > lb ? n - lb : 0u, hi = min(n, la);
@@ -471,9 +471,10 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             if (t1 && K != kEdInf) {
                 const uint32_t chi_h = iu.dold + cnt_le(I, iu, kh) + iv.dold + cnt_le(I, iv, kh) - B;
                 if (K <= chi_h) {  // chi reaches K at an arc of this epoch
-                    const uint32_t chi_q = iu.dold + cnt_le(I, iu, kq) + iv.dold + cnt_le(I, iv, kq) - B;
+                    const uint32_t cu = cnt_le(I, iu, kq), cv = cnt_le(I, iv, kq);
+                    const uint32_t chi_q = iu.dold + cu + iv.dold + cv - B;
                     do {
-                        const int32_t k2 = kth_after(I, iu, iv, kq, K - chi_q);
+                        const int32_t k2 = kth_after(I, iu, iv, cu, cv, K - chi_q);
                         const uint2 ed = L.E[k2];
                         const bool at_u = ed.x == u || ed.y == u;
                         const uint32_t sh = at_u ? u : v;
