@@ -133,6 +133,11 @@ __device__ __forceinline__ uint32_t map_find(const uint4 *map, uint32_t mask, ui
 __device__ uint32_t map_insert(uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1, uint32_t *ixctr) {
     const uint64_t key = key64(k0, k1);
     uint32_t i = (uint32_t)hash_pair64(key) & mask;
+    {  // most keys are new and their home slot free: claim it in one round trip
+        const unsigned long long prev = atomicCAS(reinterpret_cast<unsigned long long *>(&map[i]), ~0ull,
+                                                  (unsigned long long)key);
+        if (prev == ~0ull || prev == key) return i;
+    }
     for (uint32_t n = 0; n <= mask; ++n) {
         unsigned long long *kp = reinterpret_cast<unsigned long long *>(&map[i]);
         const unsigned long long cur = *reinterpret_cast<volatile unsigned long long *>(kp);
@@ -193,24 +198,9 @@ __device__ __forceinline__ uint32_t warp_take_n(uint32_t *ctr, uint32_t n) {
 // as one 64-bit word (slot .z = head, .w = fill); a full or missing head gets a fresh chunk by CAS.
 constexpr uint32_t kChunkNodes = 7;
 
-// spare: a chunk taken for this watch in advance (it stays unused when the node fits the key's head chunk)
-__device__ void watch(const EdDev &e, uint4 *map, uint32_t mask, uint32_t k0, uint32_t k1, uint32_t est, uint32_t ver,
-                      uint32_t kind, uint32_t spare, uint32_t *ixctr) {
-    const uint32_t s = map_insert(map, mask, k0, k1, ixctr);
-    if (s == kEdNil) return;
+// The slow path of a watch: key slot s known, spare chunk taken; push the node (CAS loop on {head, fill}).
+__device__ void watch_push(const EdDev &e, uint4 *map, uint32_t s, uint2 node, uint32_t spare, uint32_t *ixctr) {
     unsigned long long *hf = reinterpret_cast<unsigned long long *>(&map[s].z);
-    const uint2 node = make_uint2(est, (kind << 30) | ver_of(ver, kind));
-    if (spare >= e.pool_cap) {
-        atomicOr(&ixctr[kCtrErr], kErrInternal);
-        return;
-    }
-    // a key just created has the cleared {NIL, ~0} or detached {NIL, 0} word: try installing the chunk directly
-    reinterpret_cast<uint32_t *>(e.pool + 4ull * spare)[14] = kEdNil;
-    if (atomicCAS(hf, ~0ull, (1ull << 32) | spare) == ~0ull ||
-        atomicCAS(hf, (unsigned long long)kEdNil, (1ull << 32) | spare) == (unsigned long long)kEdNil) {
-        reinterpret_cast<uint2 *>(e.pool + 4ull * spare)[0] = node;
-        return;
-    }
     for (uint32_t it = 0; it < 1024u; ++it) {
         const unsigned long long old = *reinterpret_cast<volatile unsigned long long *>(hf);
         const uint32_t head = (uint32_t)old, fill = (uint32_t)(old >> 32);
@@ -228,6 +218,49 @@ __device__ void watch(const EdDev &e, uint4 *map, uint32_t mask, uint32_t k0, ui
         }
     }
     atomicOr(&ixctr[kCtrErr], kErrInternal);  // never: a bounded retry loop instead of a possible hang
+}
+
+// Arm up to 4 watches of one estimator.  Their round trips are independent, so each step is issued for all of
+// them before any result is used: claim the keys' home slots (most keys are new), then install each spare chunk
+// on a fresh key's {head, fill} word; only a taken home slot or an existing list takes the looping paths.
+struct WatchReq {
+    uint4 *map;
+    uint32_t mask, k0, k1, kind, spare;
+};
+
+__device__ __forceinline__ void watch_many(const EdDev &e, const WatchReq *rq, uint32_t n, uint32_t est, uint32_t ver,
+                                           uint32_t *ixctr) {
+    uint32_t slot[4];
+    unsigned long long prev[4];
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) {
+        if (i >= n) continue;
+        slot[i] = (uint32_t)hash_pair64(key64(rq[i].k0, rq[i].k1)) & rq[i].mask;
+        prev[i] = atomicCAS(reinterpret_cast<unsigned long long *>(&rq[i].map[slot[i]]), ~0ull,
+                            (unsigned long long)key64(rq[i].k0, rq[i].k1));
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) {
+        if (i >= n) continue;
+        if (prev[i] != ~0ull && prev[i] != key64(rq[i].k0, rq[i].k1))
+            slot[i] = map_insert(rq[i].map, rq[i].mask, rq[i].k0, rq[i].k1, ixctr);
+        if (rq[i].spare >= e.pool_cap) {
+            atomicOr(&ixctr[kCtrErr], kErrInternal);
+            slot[i] = kEdNil;
+        }
+        if (slot[i] == kEdNil) continue;
+        reinterpret_cast<uint32_t *>(e.pool + 4ull * rq[i].spare)[14] = kEdNil;
+        // a key just created has the cleared {NIL, ~0} word: install the chunk directly
+        prev[i] = atomicCAS(reinterpret_cast<unsigned long long *>(&rq[i].map[slot[i]].z), ~0ull,
+                            (1ull << 32) | rq[i].spare);
+    }
+#pragma unroll
+    for (uint32_t i = 0; i < 4; ++i) {
+        if (i >= n || slot[i] == kEdNil) continue;
+        const uint2 node = make_uint2(est, (rq[i].kind << 30) | ver_of(ver, rq[i].kind));
+        if (prev[i] == ~0ull) reinterpret_cast<uint2 *>(e.pool + 4ull * rq[i].spare)[0] = node;
+        else watch_push(e, rq[i].map, slot[i], node, rq[i].spare, ixctr);
+    }
 }
 
 // detach the list at slot s and queue its live estimators (each at most once per batch)
@@ -324,6 +357,26 @@ __device__ __forceinline__ uint32_t cnt_le(const EdIdx &I, const VInfo &v, int32
     return a;
 }
 
+// cnt_le of two vertices at once, the two binary searches interleaved so that their loads overlap
+__device__ __forceinline__ uint2 cnt_le2(const EdIdx &I, const VInfo &u, const VInfo &v, int32_t kmax) {
+    if (kmax < 0) return make_uint2(0u, 0u);
+    if (kmax >= (int32_t)I.w - 1) return make_uint2(u.dW, v.dW);
+    uint32_t a0 = 0, b0 = u.dW, a1 = 0, b1 = v.dW;
+    while (a0 < b0 || a1 < b1) {
+        const uint32_t m0 = (a0 + b0) >> 1, m1 = (a1 + b1) >> 1;
+        const uint32_t x0 = a0 < b0 ? I.segS[u.start + m0].x : 0u, x1 = a1 < b1 ? I.segS[v.start + m1].x : 0u;
+        if (a0 < b0) {
+            if ((int32_t)(x0 >> 1) <= kmax) a0 = m0 + 1;
+            else b0 = m0;
+        }
+        if (a1 < b1) {
+            if ((int32_t)(x1 >> 1) <= kmax) a1 = m1 + 1;
+            else b1 = m1;
+        }
+    }
+    return make_uint2(a0, a1);
+}
+
 // batch index of the n-th (n >= 1) arc of u or v after batch index kq (the caller knows it exists): the two
 // segments are sorted by batch index and disjoint, so a binary search over how many come from u's (merge path)
 // a0, b0: the arcs of u and v at or before kq (cnt_le, computed once per f1 epoch)
@@ -341,6 +394,18 @@ __device__ int32_t kth_after(const EdIdx &I, const VInfo &u, const VInfo &v, uin
 }
 
 // ---- kernels ---------------------------------------------------------------------------------------------------
+#ifdef TC_ED_CLOCKS  // timing instrumentation of k_ed_process (tools/dbg, never in the product build)
+__device__ uint32_t g_edclk[1 << 22][8];
+__device__ uint32_t g_edclk_n;
+#define TC_EDCLK_BEGIN                                                 \
+    const long long clk0_ = clock64();                                 \
+    const uint32_t ci_ = atomicAdd(&g_edclk_n, 1u) & ((1u << 22) - 1u); \
+    g_edclk[ci_][7] = events;
+#define TC_EDCLK(k) g_edclk[ci_][k] = (uint32_t)(clock64() - clk0_);
+#else
+#define TC_EDCLK_BEGIN
+#define TC_EDCLK(k)
+#endif
 // The per-batch kernels are latency chains with little data each (a few thousand items over 148 SMs): items are
 // dealt lane-major -- item i to warp i mod W, lane i / W for the W warps of the grid -- so that a small batch puts
 // one or two items in each of many warps rather than 32 divergent lanes in a few.
@@ -403,7 +468,7 @@ __global__ void __launch_bounds__(256) k_ed_trigger(EdIdx I, EdDev e) {
         for (uint64_t i = tid; i <= e.a_mask; i += nth) e.amap[i] = empty;
         for (uint64_t i = tid; i <= e.p_mask; i += nth) e.pmap[i] = empty;
         if (tid == 0) {
-            e.ctr[kEdPool] = 0u;
+            for (uint32_t i = 0; i < kEdStripes; ++i) e.ctr[kEdStripe0 + i] = 0u;
             atomicAdd(&e.ctr[kEdSweeps], 1u);
         }
         return;
@@ -451,6 +516,7 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
     const Spread sp = full ? Spread{blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x} : spread();
     for (uint32_t q = sp.first; q < nq; q += sp.step) {
         const uint32_t t = full ? q : e.queue[q];
+        TC_EDCLK_BEGIN
         ++visited;
         const uint64_t gid = e.first + t;
         EdWords W{(uint32_t)gid, (uint32_t)(gid >> 32), e.ev[t], PhiloxKey{(uint32_t)e.seed, (uint32_t)(e.seed >> 32)},
@@ -464,26 +530,33 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
         // order, as the per-edge rule uses them
         VInfo iu, iv;
         if (t1) vinfo2(I, e, u, v, iu, iv);
+        TC_EDCLK(0)
         int32_t kq = -1;  // events of the current f1 are after batch index kq
         for (;;) {
             const bool jin = J != kEdInf && J <= Pend;
             const int32_t kh = jin ? (int32_t)(J - P0) - 2 : (int32_t)I.w - 1;  // the epoch's last batch index
             if (t1 && K != kEdInf) {
-                const uint32_t chi_h = iu.dold + cnt_le(I, iu, kh) + iv.dold + cnt_le(I, iv, kh) - B;
+                const uint2 ch = cnt_le2(I, iu, iv, kh);
+                const uint32_t chi_h = iu.dold + ch.x + iv.dold + ch.y - B;
                 if (K <= chi_h) {  // chi reaches K at an arc of this epoch
-                    const uint32_t cu = cnt_le(I, iu, kq), cv = cnt_le(I, iv, kq);
-                    const uint32_t chi_q = iu.dold + cu + iv.dold + cv - B;
+                    // every replacement of the epoch draws the next K (the words are used in event order), but
+                    // only the last one's arc is the epoch's f2: locate that one alone
+                    uint32_t Klast;
                     do {
-                        const int32_t k2 = kth_after(I, iu, iv, cu, cv, K - chi_q);
-                        const uint2 ed = L.E[k2];
-                        const bool at_u = ed.x == u || ed.y == u;
-                        const uint32_t sh = at_u ? u : v;
-                        y = ed.x == sh ? ed.y : ed.x;
-                        t2 = P0 + 1u + (uint32_t)k2;
-                        fl = at_u ? 0u : 2u;  // a new f2 is not closed
+                        Klast = K;
                         K = ed_next_after(K, W);
                         ++events;
                     } while (K != kEdInf && K <= chi_h);
+                    const uint2 cq = cnt_le2(I, iu, iv, kq);
+                    const uint32_t cu = cq.x, cv = cq.y;
+                    const uint32_t chi_q = iu.dold + cu + iv.dold + cv - B;
+                    const int32_t k2 = kth_after(I, iu, iv, cu, cv, Klast - chi_q);
+                    const uint2 ed = L.E[k2];
+                    const bool at_u = ed.x == u || ed.y == u;
+                    const uint32_t sh = at_u ? u : v;
+                    y = ed.x == sh ? ed.y : ed.x;
+                    t2 = P0 + 1u + (uint32_t)k2;
+                    fl = at_u ? 0u : 2u;  // a new f2 is not closed
                 }
             }
             if (!jin) break;
@@ -496,12 +569,14 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             u = ed.x;
             v = ed.y;
             vinfo2(I, e, u, v, iu, iv);
-            B = iu.dold + cnt_le(I, iu, kq) + iv.dold + cnt_le(I, iv, kq);
+            const uint2 cb = cnt_le2(I, iu, iv, kq);
+            B = iu.dold + cb.x + iv.dold + cb.y;
             K = 1u;
             t2 = 0u;
             y = kEmptyV;
             fl = 0u;
         }
+        TC_EDCLK(1)
         uint32_t du_end = 0, dv_end = 0;
         if (t1) {
             du_end = iu.dold + iu.dW;
@@ -513,6 +588,7 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             }
         }
         const bool closed = (fl & 1u) != 0;
+        TC_EDCLK(2)
         // S and the closed counts: the old contribution at the end of the batch out, the new one in
         if (closed_o) {
             uint32_t c_old;
@@ -538,15 +614,21 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
                 atomicAdd(&e.pv[iv.pvs].z, 1u);
             }
         }
+        TC_EDCLK(3)
         // re-arm: the degree watches always (their split depends on the degrees now); the time and pair watches only
         // when they changed (the old node is still armed otherwise), or after a full sweep cleared the maps
         uint32_t ver = e.vs[t].x;
         const bool armJ = (full || J != J_o) && J != kEdInf, armT = t1 && K != kEdInf,
                    newP = full || t2 != t2o || closed != closed_o, armP = newP && t2 && !closed;
-        uint32_t chunk = warp_take_n(&e.ctr[kEdPool], (armJ ? 1u : 0u) + (armT ? 2u : 0u) + (armP ? 1u : 0u));
+        const uint32_t stripe = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) % kEdStripes;
+        const uint32_t nch = (armJ ? 1u : 0u) + (armT ? 2u : 0u) + (armP ? 1u : 0u);
+        const uint32_t l = warp_take_n(&e.ctr[kEdStripe0 + stripe], nch), stripe_cap = e.pool_cap / kEdStripes;
+        uint32_t chunk = l + nch <= stripe_cap ? stripe * stripe_cap + l : e.pool_cap;  // past the stripe: kErrInternal
+        WatchReq rq[4];
+        uint32_t nrq = 0;
         if (full || J != J_o) {
             ver = ver_bump(ver, kWJ);
-            if (armJ) watch(e, e.amap, e.a_mask, kJKey, J, t, ver, kWJ, chunk++, I.ctr);
+            if (armJ) rq[nrq++] = WatchReq{e.amap, e.a_mask, kJKey, J, kWJ, chunk++};
         }
         ver = ver_bump(ver, kWT);
         if (armT) {
@@ -557,16 +639,21 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
             uint32_t a = (uint32_t)((uint64_t)(delta + 1u) * du_end / ((uint64_t)du_end + dv_end));
             a = min(max(a, 1u), delta);
             const uint32_t b = delta + 1u - a;
-            watch(e, e.amap, e.a_mask, u, du_end + a, t, ver, kWT, chunk++, I.ctr);
-            watch(e, e.amap, e.a_mask, v, dv_end + b, t, ver, kWT, chunk++, I.ctr);
+            rq[nrq++] = WatchReq{e.amap, e.a_mask, u, du_end + a, kWT, chunk++};
+            rq[nrq++] = WatchReq{e.amap, e.a_mask, v, dv_end + b, kWT, chunk++};
         }
         if (newP) {
             ver = ver_bump(ver, kWP);
             if (armP) {
                 const uint32_t z = (fl & 2u) ? u : v;
-                watch(e, e.pmap, e.p_mask, min(z, y), max(z, y), t, ver, kWP, chunk++, I.ctr);
+                rq[nrq++] = WatchReq{e.pmap, e.p_mask, min(z, y), max(z, y), kWP, chunk++};
             }
         }
+        watch_many(e, rq, nrq, t, ver, I.ctr);
+        TC_EDCLK(4)
+#ifdef TC_ED_CLOCKS
+        g_edclk[ci_][6] = events;
+#endif
         e.vs[t].x = ver;
         e.J[t] = J;
         e.t1[t] = t1;
@@ -701,7 +788,7 @@ bool ed_alloc(EdDev &e, uint64_t count, uint64_t first, uint64_t seed, uint64_t 
     // most 4 per estimator it visits; a rebuild is due once more than 12 n are in use, so 16 n + slack always
     // suffice.  Every key owns at least one chunk, so the maps (load <= 1/2) get 2 slots per chunk.  (~1.5 KB per
     // estimator in all: the rebuilds -- a full sweep, O(r) -- stay rare.)
-    const uint64_t pool = 16 * n + 4096;
+    const uint64_t pool = 16 * n + 32 * 1024;
     if (pool > 0x7FFFFFF0ull) return false;
     e.pool_cap = (uint32_t)pool;
     const uint64_t acap = pow2_at_least(2 * pool), pcap = acap;
@@ -745,9 +832,9 @@ int launch_ed_init(const EdDev &e, cudaStream_t s) {
     const uint64_t items = std::max<uint64_t>({e.count, (uint64_t)e.a_mask + 1, (uint64_t)e.p_mask + 1,
                                                (uint64_t)e.pv_mask + 1});
     k_ed_init<<<grid_of(items, 16), 256, 0, s>>>(e);
-    // rebuild threshold: more than 12 chunks per estimator in use (see ed_alloc)
+    // rebuild threshold: more than 12 chunks per estimator in use in any stripe (see ed_alloc)
     const uint64_t n = std::max<uint64_t>(e.count, 1);
-    k_ed_set_thr<<<1, 1, 0, s>>>(e.ctr, (uint32_t)std::min<uint64_t>(12 * n + 1024, e.pool_cap - 4 * n));
+    k_ed_set_thr<<<1, 1, 0, s>>>(e.ctr, (uint32_t)((12 * n + 1024) / kEdStripes));
     return 2;
 }
 
@@ -808,6 +895,20 @@ int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, uns
     kr.end(K_ED_POST, s);
     return 4;
 }
+
+#ifdef TC_ED_CLOCKS
+extern "C" int tc_debug_ed_clocks(uint32_t *out, uint32_t cap, int reset) {
+    uint32_t n = 0;
+    cudaMemcpyFromSymbol(&n, g_edclk_n, 4);
+    n = n < cap ? n : cap;
+    cudaMemcpyFromSymbol(out, g_edclk, 32ull * n);
+    if (reset) {
+        const uint32_t z = 0;
+        cudaMemcpyToSymbol(g_edclk_n, &z, 4);
+    }
+    return (int)n;
+}
+#endif
 
 int launch_ed_export(const EdDev &e, const StateBufs &st, cudaStream_t s) {
     if (!e.count) return 0;

@@ -27,15 +27,17 @@ constexpr uint32_t kEdNil = 0xFFFFFFFFu;
 constexpr uint32_t kJKey = 0xFFFFFFFFu;    // the reserved vertex id: (kJKey, t) watches stream time t
 
 // counters (EdDev::ctr)
-constexpr int kEdPool = 0;     // watch chunks in use
+constexpr int kEdPool = 0;     // (unused: the chunk pool is striped, kEdStripe0 ..)
 constexpr int kEdQueue = 1;    // estimators queued in this batch
 constexpr int kEdFull = 2;     // this batch is a full sweep (set by k_desc)
 constexpr int kEdPVN = 3;      // vertices in the persistent table
-constexpr int kEdThr = 4;      // pool threshold of a rebuild
+constexpr int kEdThr = 4;      // per-stripe chunk threshold of a rebuild
 constexpr int kEdVisited = 5;  // estimators processed (all batches)
 constexpr int kEdEvents = 6;   // f1 / f2 replacements (all batches)
 constexpr int kEdSweeps = 7;   // full sweeps
-constexpr int kEdWords = 8;
+constexpr int kEdStripe0 = 8;  // chunks in use per stripe: the pool is 32 stripes of pool_cap / 32 chunks, warp w
+constexpr uint32_t kEdStripes = 32;  // allocating from stripe w mod 32 (one hot counter would serialise them)
+constexpr int kEdWords = kEdStripe0 + (int)kEdStripes;
 
 struct EdDev {
     // estimator SoA: J, f1 = (u, v) at time t1 (0: none), B = deg_t1(u) + deg_t1(v), K, f2 at time t2 = (shared,
@@ -51,7 +53,7 @@ struct EdDev {
     uint4 *pmap;      // closing-pair watches
     uint32_t p_mask;
     uint4 *pool;      // watch chunks: 64 B = 7 nodes {estimator, kind << 30 | version} + the next chunk (word 14)
-    uint32_t pool_cap;  // chunks
+    uint32_t pool_cap;  // chunks (kEdStripes stripes of pool_cap / kEdStripes)
     uint32_t *queue;  // [count] estimators to process in this batch
     uint4 *seg;       // [2 wcap] at each vertex segment's first slot: {degree before the batch, pv slot, degree in
                       // the batch, segment start}

@@ -1818,7 +1818,9 @@ __global__ void __launch_bounds__(256) k_desc(BatchDesc d, BatchDesc *dst, uint3
         S[d.slot] = (d.pad & 1u) ? S[d.slot ^ 1u] : 0ull;
         if (edctr) {
             edctr[kEdQueue] = 0u;
-            edctr[kEdFull] = ((d.pad & 2u) || edctr[kEdPool] > edctr[kEdThr]) ? 1u : 0u;
+            uint32_t used = 0;  // the fullest stripe of the watch-chunk pool
+            for (uint32_t i = 0; i < kEdStripes; ++i) used = max(used, edctr[kEdStripe0 + i]);
+            edctr[kEdFull] = ((d.pad & 2u) || used > edctr[kEdThr]) ? 1u : 0u;
         }
     }
     if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
