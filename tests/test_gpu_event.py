@@ -225,3 +225,38 @@ def test_rank_handle_world1_event_mode():
     o.push_batch(s, validate=False)
     compare(tc, o, "rank handle")
     assert tc.estimate() == o.estimate()
+
+
+def test_event_mode_group_handle_graphs_and_async_sums():
+    """tc_create_ex (one device) in the event mode; one graph capture per batch shape; tc_closed_sum_async per
+    batch equal to the oracle's S after that prefix; median of means from the oracle's state."""
+    from paper_1308_2166_b200 import TriangleCounter
+    from synth import rmat
+    s = np.ascontiguousarray(rmat(12, 8, 21)[:24000], dtype=np.uint32)
+    w, r = 3000, 2500
+    tc = TriangleCounter.multi(r, 17, [0], strict=False, graphs=True, w_max_hint=w)
+    tc.set_mode("event")
+    solo = event_counter(r, 17, graphs=True, async_=True, w_max_hint=w)
+    Sbuf = torch.zeros(16, dtype=torch.int64).pin_memory()
+    o = oracle(r, 17)
+    ref = []
+    for i, k in enumerate(range(0, len(s), w)):
+        tc.push_batch(s[k:k + w])
+        solo.push_batch(s[k:k + w])
+        solo.closed_sum_async(Sbuf, i)
+        o.push_batch(s[k:k + w], validate=False)
+        ref.append(o.closed_sum())
+    assert tc.sync() == 0 and solo.sync() == 0
+    assert Sbuf[: len(ref)].tolist() == ref
+    assert solo.graph_captures() <= 2  # the full-sweep and watch batches share one shape
+    compare(tc, o, "tc_create_ex(1) event mode")
+    compare(solo, o, "solo event mode")
+    ost = o.state()
+    m = len(s)
+    for g in (1, 5, 50):
+        means = []
+        for j in range(g):
+            lo, hi = j * r // g, (j + 1) * r // g
+            Sg = int(ost["c"][lo:hi][ost["closed"][lo:hi] == 1].astype(np.int64).sum())
+            means.append(float(m) * float(Sg) / float(hi - lo))
+        assert tc.estimate_mom(g) == sorted(means)[(g - 1) // 2]
