@@ -264,7 +264,7 @@ __device__ __forceinline__ void watch_many(const EdDev &e, const WatchReq *rq, u
 }
 
 // detach the list at slot s and queue its live estimators (each at most once per batch)
-__device__ void fire(const EdDev &e, uint4 *map, uint32_t s, uint32_t tag) {
+__device__ void fire(const EdDev &e, uint4 *map, uint32_t s, uint32_t tag, uint32_t *ixctr) {
     const unsigned long long old = atomicExch(reinterpret_cast<unsigned long long *>(&map[s].z), (unsigned long long)kEdNil);
     uint32_t c = (uint32_t)old, n = min((uint32_t)(old >> 32), kChunkNodes);
     for (uint32_t hops = 0; c != kEdNil && hops < e.pool_cap; ++hops) {
@@ -282,6 +282,7 @@ __device__ void fire(const EdDev &e, uint4 *map, uint32_t s, uint32_t tag) {
             const bool want = (kv & 0x3FFFFFFFu) == ver_of(vs[j].x, kv >> 30) && vs[j].y != tag &&
                               atomicExch(&e.vs[est].y, tag) != tag;
             const uint32_t q = warp_take(&e.ctr[kEdQueue], want);
+            TC_CHECK(!want || (q < e.count && est < e.count), ixctr);
             if (want) e.queue[q] = est;
         }
         c = w[14];
@@ -494,10 +495,11 @@ __global__ void __launch_bounds__(256) k_ed_trigger(EdIdx I, EdDev e) {
             VertProbe P;
             vt_issue(I.L, x, P);
             const uint2 r = vt_resolve(I.L, P, x);  // {deg_W, start}
+            TC_CHECK(r.x > 0 && r.y <= ps.x && ps.x < r.y + r.x && ps.x < 2 * I.w, I.ctr);
             const uint32_t theta = e.seg[r.y].x + (ps.x - r.y) + 1u;  // x's degree once this arc has arrived
             sl = map_find(e.amap, e.a_mask, x, theta);
         }
-        if (sl != kEdNil) fire(e, map, sl, tag);
+        if (sl != kEdNil) fire(e, map, sl, tag, I.ctr);
     }
 }
 
@@ -516,6 +518,7 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
     const Spread sp = full ? Spread{blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x} : spread();
     for (uint32_t q = sp.first; q < nq; q += sp.step) {
         const uint32_t t = full ? q : e.queue[q];
+        TC_CHECK(t < e.count, I.ctr);
         TC_EDCLK_BEGIN
         ++visited;
         const uint64_t gid = e.first + t;
@@ -551,6 +554,7 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
                     const uint32_t cu = cq.x, cv = cq.y;
                     const uint32_t chi_q = iu.dold + cu + iv.dold + cv - B;
                     const int32_t k2 = kth_after(I, iu, iv, cu, cv, Klast - chi_q);
+                    TC_CHECK(k2 > kq && k2 <= kh, I.ctr);
                     const uint2 ed = L.E[k2];
                     const bool at_u = ed.x == u || ed.y == u;
                     const uint32_t sh = at_u ? u : v;

@@ -1,8 +1,8 @@
 """A small workload that drives every kernel path of the library, for compute-sanitizer
 (tests/test_sanitizers.py runs it under ONE tool per process): C1 batches, a hub stream through every
 vertex-bucket path (hash, hub peeling, radix sort in shared and global memory, split partition), the
-small-batch and the split per-step estimator passes, asynchronous and strict errors, CUDA graphs, and a
-world-1 NCCL rank handle.  Exits non-zero if a result differs from the oracle."""
+small-batch and the split per-step estimator passes, the event-driven mode, asynchronous and strict errors,
+CUDA graphs, and a world-1 NCCL rank handle.  Exits non-zero if a result differs from the oracle."""
 import os
 import sys
 
@@ -41,6 +41,20 @@ def main():
         for k in range(0, len(hub), 2000):
             t.push_batch(hub[k:k + 2000])
         assert_states_equal(t.state(), oracle_run(hub, 900, 7, 2000).state(), f"small_index={si}")
+    # the event-driven mode: small (one-CTA) and partitioned index, strict and graphs + asynchronous errors
+    from oracle.edc import EventOracleC
+    for w, graphs in ((2000, False), (6000, True), (333, True)):
+        t = TriangleCounter(800, 11)
+        t.set_mode("event")
+        t.set_graphs(graphs)
+        t.set_async(graphs)
+        o = EventOracleC(800, 11)
+        for k in range(0, len(hub), w):
+            t.push_batch(hub[k:k + w])
+            o.push_batch(hub[k:k + w], validate=False)
+        assert t.sync() == 0
+        assert_states_equal(t.state(), o.state(), f"event mode w={w}")
+        assert t.closed_sum() == o.closed_sum()
     bad = np.array([[1, 2], [3, 3]], np.uint32)
     assert tc.push_batch(bad, check=False) != 0
     if os.environ.get("TC_SANITIZE_NCCL", "1") == "1":
