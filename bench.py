@@ -208,6 +208,8 @@ def kernel_bytes(kernel, w, st, R):
         return 16 * w + 48 * st["vertices"]
     if kernel == "k_ed_trigger":
         return 96 * w
+    if kernel == "k_ed_front":  # k_ed_pre + k_ed_trigger in one kernel
+        return 16 * w + 48 * st["vertices"] + 96 * w
     if kernel == "k_ed_process":
         return (96 + 128) * st.get("visited", 0)
     if kernel == "k_ed_post":

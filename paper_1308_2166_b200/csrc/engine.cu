@@ -536,7 +536,7 @@ static int push_prepare(tc_ctx *ctx, const tc_edge *edges, uint64_t w, PushPrep 
 
 // Event mode: can a vertex degree reach the limit in this batch (m + w > 2^30 - 1)?  Then the degrees are checked
 // first and applied by a separate kernel once the batch is accepted.
-static bool ed_post(const tc_ctx *ctx, uint64_t w) { return ctx->m + w > (uint64_t)kEdDegMax; }
+static bool ed_post(const tc_ctx *ctx, uint64_t w) { return ctx->tune.event_checked || ctx->m + w > (uint64_t)kEdDegMax; }
 
 // a4-a8: the bulk estimator pass (fused, or split per step), or the event mode's kernels
 static uint32_t estimator_pass(tc_ctx *ctx, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
@@ -856,6 +856,10 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
             case TC_TUNE_SMALL_INDEX:
                 if (value > 2) return TC_EINVAL;
                 c->tune.small_index = (uint32_t)value;
+                return TC_OK;
+            case TC_TUNE_EVENT_CHECKED:
+                if (value > 1) return TC_EINVAL;
+                c->tune.event_checked = (uint32_t)value;
                 return TC_OK;
             case TC_TUNE_SPLIT_KERNELS:
                 if (value > 1) return TC_EINVAL;
@@ -1320,7 +1324,7 @@ const char *tc_kernel_name(int k) {
                                             "k_pairs", "k_vhub", "k_vbig", "k_vhash", "k_update",
                                             "k_u1_resample", "k_u2_count", "k_u3_select", "k_u4_close", "k_r_reduce",
                                             "k_small_index", "k_ed_pre", "k_ed_trigger", "k_ed_process",
-                                            "k_ed_post"};
+                                            "k_ed_post", "k_ed_front"};
     return (k >= 0 && k < K_NKERNELS) ? names[k] : "";
 }
 

@@ -441,10 +441,85 @@ __global__ void __launch_bounds__(256) k_ed_pre(EdIdx I, EdDev e, unsigned long 
         const uint32_t p = pv_insert(e, x, I.ctr);
         if (p == kEdNil) continue;
         const uint4 pv = e.pv[p];
-        if (d.pad & 4u) e.pv[p].y = pv.y + dW;  // no degree can pass the limit (host): the update is done here
-        else if ((uint64_t)pv.y + dW > kEdDegMax) atomicOr(&I.ctr[kCtrErr], kErrOvf);
+        if ((uint64_t)pv.y + dW > kEdDegMax) atomicOr(&I.ctr[kCtrErr], kErrOvf);
         e.seg[s] = make_uint4(pv.y, p, dW, s);
         grow += (unsigned long long)dW * pv.z;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        grow += __shfl_xor_sync(kFullMask, grow, off);
+        nv += __shfl_xor_sync(kFullMask, nv, off);
+    }
+    if ((threadIdx.x & 31u) == 0) {
+        if (grow) atomicAdd(S + d.slot, grow);
+        if (nv) atomicAdd(stats + 2, (unsigned long long)nv);
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(stats + 3, 1ull);
+    }
+}
+
+// The fast path (no vertex degree can reach the limit in this batch, so nothing after the index can reject it):
+// k_ed_pre's vertex work and k_ed_trigger's lookups in ONE kernel over 4w items -- arc slot s < 2w: the vertex's
+// persistent record (inserted at its segment's first slot, with the segment record and S's growth) and the degree
+// watch (x, deg_old(x) + rank + 1) that the arc reaches; edge item: the time and pair watches.  The degrees
+// themselves are applied by k_ed_process (nothing reads a batch vertex's persistent degree before that).
+__global__ void __launch_bounds__(256) k_ed_front(EdIdx I, EdDev e, unsigned long long *S, unsigned long long *stats) {
+    const BatchDesc d = *I.d;
+    if (I.ctr[kCtrErr]) {  // rejected (this batch or an earlier asynchronous one): record the first, change nothing
+        if (blockIdx.x == 0 && threadIdx.x == 0 && I.ctr[kCtrFailB] == 0xFFFFFFFFu) I.ctr[kCtrFailB] = d.batch;
+        return;
+    }
+    const bool full = e.ctr[kEdFull] != 0;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    if (full) {  // a full sweep: every estimator is processed and re-armed into cleared maps
+        const uint4 empty = make_uint4(kEmptyV, kEmptyV, kEdNil, kEmptyV);
+        for (uint64_t i = tid; i <= e.a_mask; i += nth) e.amap[i] = empty;
+        for (uint64_t i = tid; i <= e.p_mask; i += nth) e.pmap[i] = empty;
+        if (tid == 0) {
+            for (uint32_t i = 0; i < kEdStripes; ++i) e.ctr[kEdStripe0 + i] = 0u;
+            atomicAdd(&e.ctr[kEdSweeps], 1u);
+        }
+    }
+    const uint32_t tag = d.batch + 1u;
+    const uint32_t t0 = (uint32_t)d.m_prev + 1u;  // stream time of batch edge 0
+    unsigned long long grow = 0;
+    uint32_t nv = 0;
+    const Spread sp = spread();
+    for (uint32_t i = sp.first; i < 4 * I.w; i += sp.step) {
+        uint32_t sl = kEdNil;
+        uint4 *map = e.amap;
+        if (i < 2 * I.w) {
+            const uint32_t s = i;
+            const uint32_t x = arc_vertex(I.L.E, I.segS[s].x);
+            const bool first = s == 0 || arc_vertex(I.L.E, I.segS[s - 1].x) != x;
+            VertProbe P;
+            vt_issue(I.L, x, P);
+            const uint2 r = vt_resolve(I.L, P, x);  // {deg_W, segment start}
+            TC_CHECK(r.x > 0 && r.y <= s && s < r.y + r.x, I.ctr);
+            uint32_t dold;
+            if (first) {
+                const uint32_t p = pv_insert(e, x, I.ctr);
+                if (p == kEdNil) continue;
+                const uint4 pv = e.pv[p];
+                dold = pv.y;
+                e.seg[s] = make_uint4(pv.y, p, r.x, s);
+                grow += (unsigned long long)r.x * pv.z;
+                ++nv;
+            } else {
+                const uint32_t p = full ? kEdNil : pv_find(e, x);  // a vertex new in this batch has no watches
+                dold = p == kEdNil ? 0u : e.pv[p].y;
+            }
+            if (!full && dold) sl = map_find(e.amap, e.a_mask, x, dold + (s - r.y) + 1u);
+        } else if (!full) {
+            const uint32_t j = i - 2 * I.w, k = j >> 1;
+            if (j & 1u) {
+                const uint2 ed = I.L.E[k];
+                map = e.pmap;
+                sl = map_find(e.pmap, e.p_mask, ed.x, ed.y);
+            } else {
+                sl = map_find(e.amap, e.a_mask, kJKey, t0 + k);
+            }
+        }
+        if (sl != kEdNil) fire(e, map, sl, tag, I.ctr);
     }
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -515,6 +590,15 @@ __global__ void __launch_bounds__(256) k_ed_process(EdIdx I, EdDev e, unsigned l
     L.ptag = d.ptag;
     unsigned long long dS = 0;
     uint32_t visited = 0, events = 0;
+    if (d.pad & 4u) {  // the fast path: the batch's vertex degrees (k_ed_front left them to this kernel; the
+                       // estimators below read the persistent degree of non-batch vertices only)
+        for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < 2 * I.w; s += gridDim.x * blockDim.x) {
+            const uint32_t x = arc_vertex(I.L.E, I.segS[s].x);
+            if (s > 0 && arc_vertex(I.L.E, I.segS[s - 1].x) == x) continue;
+            const uint4 sg = e.seg[s];
+            e.pv[sg.y].y = sg.x + sg.z;
+        }
+    }
     const Spread sp = full ? Spread{blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x} : spread();
     for (uint32_t q = sp.first; q < nq; q += sp.step) {
         const uint32_t t = full ? q : e.queue[q];
@@ -884,16 +968,25 @@ int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, uns
                     cudaStream_t s, const KRec &kr) {
     const EdIdx I = ed_idx(ix, a);
     const uint32_t g_arcs = grid_of(2ull * a.g.w, 8), g_spread = std::max<uint32_t>(g_arcs, (uint32_t)sm_count() * 4);
+    const uint32_t g_items = std::max<uint32_t>(grid_of(4ull * a.g.w, 8), (uint32_t)sm_count() * 4);
+    if (!post) {  // fast path: vertex work and watch lookups in one kernel, the degrees applied by k_ed_process
+        kr.beg(K_ED_FRONT, s);
+        k_ed_front<<<g_items, 256, 0, s>>>(I, e, a.S, stats);
+        kr.end(K_ED_FRONT, s);
+        kr.beg(K_ED_PROCESS, s);
+        k_ed_process<<<(uint32_t)sm_count() * 4, 256, 0, s>>>(I, e, a.S);
+        kr.end(K_ED_PROCESS, s);
+        return 2;
+    }
     kr.beg(K_ED_PRE, s);
     k_ed_pre<<<g_spread, 256, 0, s>>>(I, e, a.S, stats);
     kr.end(K_ED_PRE, s);
     kr.beg(K_ED_TRIGGER, s);
-    k_ed_trigger<<<std::max<uint32_t>(grid_of(4ull * a.g.w, 8), (uint32_t)sm_count() * 4), 256, 0, s>>>(I, e);
+    k_ed_trigger<<<g_items, 256, 0, s>>>(I, e);
     kr.end(K_ED_TRIGGER, s);
     kr.beg(K_ED_PROCESS, s);
     k_ed_process<<<(uint32_t)sm_count() * 4, 256, 0, s>>>(I, e, a.S);
     kr.end(K_ED_PROCESS, s);
-    if (!post) return 3;
     kr.beg(K_ED_POST, s);
     k_ed_post<<<g_arcs, 256, 0, s>>>(I, e);
     kr.end(K_ED_POST, s);

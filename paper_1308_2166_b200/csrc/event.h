@@ -68,9 +68,10 @@ bool ed_alloc_seg(EdDev &e, uint64_t wcap);  // with the index (2 wcap entries)
 int launch_ed_init(const EdDev &e, cudaStream_t s);
 // Re-insert the persistent vertices into a table of new_cap slots (replaces e.pv / e.pv_mask on success).
 int ed_rehash_pv(EdDev &e, uint64_t new_cap, cudaStream_t s);
-// The kernels of a batch (after the index): k_ed_pre, k_ed_trigger, k_ed_process, and k_ed_post when `post` (the
-// degree limit can be reached: k_ed_pre only checks it, k_ed_post applies the degrees once the batch is accepted;
-// otherwise k_ed_pre applies them and the descriptor has pad bit 2).  stats: the bulk state's event counters
+// The kernels of a batch (after the index).  Fast path (no vertex degree can reach the limit; descriptor pad bit
+// 2): k_ed_front (vertex records + every watch lookup) and k_ed_process (which also applies the degrees).  When
+// `post` (the limit can be reached, so the batch may still be rejected after the index): k_ed_pre checks it,
+// k_ed_trigger looks the watches up, k_ed_process, and k_ed_post applies the degrees once the batch is accepted.  stats: the bulk state's event counters
 // (tc_stats): out[2] += distinct vertices of the batch, out[3] += 1.
 int launch_ed_batch(const IndexBufs &ix, const BatchArgs &a, const EdDev &e, unsigned long long *stats, bool post,
                     cudaStream_t s, const KRec &kr);

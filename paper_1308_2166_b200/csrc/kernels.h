@@ -99,13 +99,14 @@ struct Tuning {
     uint32_t sortcap = kVChunk;
     uint32_t split = 0;            // 1: the estimator pass as the split per-step kernels
     uint32_t small_index = 0;      // 0 auto (w <= kSmallIndexMax), 1 never, 2 always when w <= kSmallIndexMax
+    uint32_t event_checked = 0;    // event mode: 1 = always the four-kernel path that checks the degree limit
 };
 
 Geometry make_geometry(uint32_t w, const Tuning &t);
 
 // Per-kernel profiling (tc_profile_kernels): ids match include/tc.h TC_KERNEL_*.
 enum KernelId { K_COUNT = 0, K_SCAN_COLS, K_SCAN_TOT, K_SCATTER, K_SPLIT, K_PAIRS, K_VHUB, K_VBIG, K_VHASH, K_UPDATE,
-                K_U1, K_U2, K_U3, K_U4, K_R, K_SMALL, K_ED_PRE, K_ED_TRIGGER, K_ED_PROCESS, K_ED_POST, K_NKERNELS };
+                K_U1, K_U2, K_U3, K_U4, K_R, K_SMALL, K_ED_PRE, K_ED_TRIGGER, K_ED_PROCESS, K_ED_POST, K_ED_FRONT, K_NKERNELS };
 struct KRec {
     cudaEvent_t *ev = nullptr;  // 2 K_NKERNELS events (begin, end) or null: no profiling
     uint32_t *used = nullptr;   // bit k set once kernel k's events were recorded in this push

@@ -61,7 +61,7 @@ def test_b200_arm_event_mode_json_line():
     d = json.loads(lines[0])
     assert d["config"]["mode"] == "event" and d["steps"] == d["config"]["batches_per_stream"]
     ks = d["roofline"]["kernels"]
-    assert {"k_ed_pre", "k_ed_trigger", "k_ed_process"} <= set(ks) and "k_update" not in ks
+    assert {"k_ed_front", "k_ed_process"} <= set(ks) and "k_update" not in ks
     assert d["roofline"]["events_per_batch"]["visited"] > 0
     assert "oracle/ed.c" in d["cpu_baseline"]["sample"] and d["value"] > 0
     assert d.get("e2e_results_match_tc_estimate") is True

@@ -23,10 +23,12 @@ def lib():
     return pkg.load_library()
 
 
-def event_counter(r, seed, first=0, count=None, graphs=False, async_=False, w_max_hint=0):
+def event_counter(r, seed, first=0, count=None, graphs=False, async_=False, w_max_hint=0, checked=False):
     from paper_1308_2166_b200 import TriangleCounter
     tc = TriangleCounter(r, seed, first=first, count=count, w_max_hint=w_max_hint)
     tc.set_mode("event")
+    if checked:  # the four-kernel path that checks the degree limit first (else only past m + w > 2^30 - 1)
+        tc.tune(event_checked=1)
     tc.set_graphs(graphs)
     tc.set_async(async_)
     return tc
@@ -66,7 +68,7 @@ def test_every_batch_random(case):
     s = np.ascontiguousarray(s, dtype=np.uint32)
     r = [1, 37, 2000, 5000][case % 4]
     graphs, async_ = case % 3 == 1, case % 3 == 2
-    tc = event_counter(r, 100 + case, graphs=graphs, async_=async_)
+    tc = event_counter(r, 100 + case, graphs=graphs, async_=async_, checked=case >= 3)
     o = oracle(r, 100 + case)
     for lo, hi in _batchings(rng, len(s), [1, 7, 64, 500, 1500, 4096]):
         tc.push_batch(s[lo:hi])
@@ -100,12 +102,15 @@ def test_C1_and_watch_path_used():
     from synth import config_stream
     s = config_stream("C1")
     tc = event_counter(4096, 42, graphs=True, async_=True, w_max_hint=2048)
+    tc2 = event_counter(4096, 42, graphs=True, async_=True, w_max_hint=2048, checked=True)
     o = oracle(4096, 42)
     for k in range(0, len(s), 2048):
         tc.push_batch(s[k:k + 2048])
+        tc2.push_batch(s[k:k + 2048])
         o.push_batch(s[k:k + 2048], validate=False)
-    assert tc.sync() == 0
+    assert tc.sync() == 0 and tc2.sync() == 0
     st = compare(tc, o, "C1")
+    compare(tc2, o, "C1 checked path")
     check_properties(s, st, len(s))
     cnt = tc.event_counters()
     nb = (len(s) + 2047) // 2048
@@ -121,7 +126,7 @@ def test_C5_prefix(lw):
     w, r = 1 << lw, 1 << 22
     m = (1 << 21) + 777
     s = np.ascontiguousarray(s[:m])
-    tc = event_counter(r, 9, graphs=True, async_=True, w_max_hint=w)
+    tc = event_counter(r, 9, graphs=True, async_=True, w_max_hint=w, checked=lw == 16)
     dev = torch.from_numpy(s.view(np.int32)).cuda()
     for k in range(0, m, w):
         tc.push_batch(dev[k:k + w])

@@ -43,9 +43,10 @@ def main():
         assert_states_equal(t.state(), oracle_run(hub, 900, 7, 2000).state(), f"small_index={si}")
     # the event-driven mode: small (one-CTA) and partitioned index, strict and graphs + asynchronous errors
     from oracle.edc import EventOracleC
-    for w, graphs in ((2000, False), (6000, True), (333, True)):
+    for w, graphs, checked in ((2000, False, 0), (6000, True, 0), (333, True, 0), (2000, True, 1), (6000, False, 1)):
         t = TriangleCounter(800, 11)
         t.set_mode("event")
+        t.tune(event_checked=checked)
         t.set_graphs(graphs)
         t.set_async(graphs)
         o = EventOracleC(800, 11)
