@@ -255,9 +255,14 @@ int tc_graph_captures(tc_ctx *ctx, uint64_t *captures);
  *                        limit before applying anything (k_ed_pre, k_ed_trigger, k_ed_process, k_ed_post); 0
  *                        (default) = that path only when a degree could reach the limit (m + w > 2^30 - 1),
  *                        else the two-kernel path (k_ed_front, k_ed_process).  Same results.
+ *  TC_TUNE_PAIR_FILTER   bulk mode, fused estimator pass: a Bloom filter over the batch's pairs (16 bits per edge,
+ *                        filled by the pair-table kernel) that Step 3's closing-edge probe
+ *                        reads before the edge-pair table; it has no false negatives.  0 = auto (default;
+ *                        batches of at least 2^21 edges, where the table no longer stays in L2), 1 = never,
+ *                        2 = always (partitioned index).  Same results.
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
 enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6,
-       TC_TUNE_SPLIT_KERNELS = 8, TC_TUNE_SMALL_INDEX = 10, TC_TUNE_EVENT_CHECKED = 12 };
+       TC_TUNE_SPLIT_KERNELS = 8, TC_TUNE_SMALL_INDEX = 10, TC_TUNE_EVENT_CHECKED = 12, TC_TUNE_PAIR_FILTER = 14 };
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
 
 /* tc_set_mode -- the estimator update rule (reading R17, §10 row 4).

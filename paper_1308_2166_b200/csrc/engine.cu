@@ -44,6 +44,7 @@ struct tc_ctx {
     uint64_t m = 0;
     uint32_t b = 0;
     uint32_t ptag = 0;  // edge-pair table tag of the last push
+    uint32_t pf_zeroed[2] = {0, 0};  // pair filters: leading words known to be zero (k_count zeroes the other one)
     int async_errors = 0;
     int poisoned = 0;  // 0 or the TC_E* code that poisoned the handle
     int S_slot = -1;   // accumulator slot holding S of the last accepted batch (-1: none yet)
@@ -152,7 +153,7 @@ static bool alloc_steps(StepBufs &sb, uint64_t count) {
 
 static void free_index(IndexBufs &ix) {
     void *bufs[] = {ix.arcs2, ix.vstart2, ix.E, ix.apos, ix.pslot, ix.segS, ix.pt, ix.vt, ix.vslice, ix.arcs, ix.scratch, ix.vperm, ix.vdefer,
-                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2, ix.filt, ix.desc};
+                    ix.cntV, ix.offV, ix.arank, ix.vstart, ix.ctr, ix.stage, ix.stage2, ix.filt, ix.pf, ix.desc};
     for (void *p : bufs) cudaFree(p);
     ix = IndexBufs();
 }
@@ -199,6 +200,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
          cudaMalloc(&ix.arank, 4 * cap) == cudaSuccess && cudaMalloc(&ix.vstart, 4 * kStartWords) == cudaSuccess &&
          cudaMalloc(&ix.ctr, 4 * kCtrWords) == cudaSuccess && cudaMalloc(&ix.stage, 8 * cap) == cudaSuccess &&
          cudaMalloc(&ix.stage2, 8 * cap) == cudaSuccess && cudaMalloc(&ix.filt, 4ull * kFilterWords) == cudaSuccess &&
+         cudaMalloc(&ix.pf, 8ull * pf_words((uint32_t)cap)) == cudaSuccess &&  // two filters
          cudaMalloc(&ix.desc, sizeof(BatchDesc)) == cudaSuccess;
     if (!ok) {
         cudaGetLastError();
@@ -224,6 +226,8 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
     CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
     CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)cap), ctx->stream));  // tag 0: free
+    CK(cudaMemsetAsync(ix.pf, 0, 8ull * pf_words((uint32_t)cap), ctx->stream));
+    ctx->pf_zeroed[0] = ctx->pf_zeroed[1] = pf_words((uint32_t)cap);
     ctx->ptag = 0;
     return TC_OK;
 }
@@ -673,6 +677,15 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
     a.S = ctx->st.S;
     a.g = make_geometry((uint32_t)w, ctx->tune);
     a.small = ctx->mode == TC_MODE_BULK && (ctx->tune.small == 2 || (ctx->tune.small == 0 && w <= kSmallBatchMax));
+    a.pfilt = ctx->mode == TC_MODE_BULK && !ctx->tune.split && !a.g.small_index &&
+              (ctx->tune.pair_filter == 2 || (ctx->tune.pair_filter == 0 && w >= kPairFilterMin));
+    if (a.pfilt) {  // this batch fills filter `slot`, which must start zeroed; k_count zeroes the other one
+        const uint32_t need = pf_words((uint32_t)w);
+        if (ctx->pf_zeroed[slot] < need)
+            CK(cudaMemsetAsync(ix.pf + (size_t)slot * pf_words((uint32_t)ix.wcap), 0, 4ull * need, ctx->stream));
+        ctx->pf_zeroed[slot] = 0;
+        ctx->pf_zeroed[slot ^ 1] = std::max(ctx->pf_zeroed[slot ^ 1], need);
+    }
     if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
         CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
         ctx->ptag = 1;
@@ -860,6 +873,10 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
             case TC_TUNE_EVENT_CHECKED:
                 if (value > 1) return TC_EINVAL;
                 c->tune.event_checked = (uint32_t)value;
+                return TC_OK;
+            case TC_TUNE_PAIR_FILTER:
+                if (value > 2) return TC_EINVAL;
+                c->tune.pair_filter = (uint32_t)value;
                 return TC_OK;
             case TC_TUNE_SPLIT_KERNELS:
                 if (value > 1) return TC_EINVAL;

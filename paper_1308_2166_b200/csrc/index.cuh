@@ -8,9 +8,9 @@
 //             Vertices are grouped by BUCKET (the top bv bits of hash_vertex), each bucket owns the slot
 //             range of its arcs; inside a bucket vertices appear in hash order.
 //   einfo[k]  uint4  {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
-//   vertex table: one open-addressing slice per vertex bucket, min(next_pow2(2 D_b), 2 n_b) slots for the
-//             bucket's D_b distinct vertices (n_b arcs), 16 B slots {x, deg_W(x), segment start, 0}, at offset
-//             2 * (the bucket's first arc slot) -- slices never overlap and need no prefix sum;
+//   vertex table: one open-addressing slice per vertex bucket, min(next_pow2(2 D_b), 2 n_b) slots (load <= 1/2)
+//             for the bucket's D_b distinct vertices (n_b arcs), 16 B slots {x, deg_W(x), segment start, 0}, at
+//             offset 2 * (the bucket's first arc slot) -- slices never overlap and need no prefix sum;
 //             vslice[b] = {offset, size}.
 //             Slices are written whole every batch (empty slots included), so the table needs no tags.
 //   edge-pair table: ceil(3w / 4) groups of four 8-byte slots {k, tag|fp} (one 32-byte sector per group, load
@@ -149,7 +149,7 @@ __host__ __device__ __forceinline__ uint32_t pgroup_at(uint32_t A, uint32_t B, u
 
 // Vertex-table slices: bucket b (n_b arcs, D_b distinct vertices) owns the S_b = min(next_pow2(2 D_b), 2 n_b)
 // slots at offset 2 * (its first arc slot) (load <= 1/2, slices disjoint).  A vertex with hash h probes the
-// slot pairs from vslot_start(h, S) on, wrapping at S (S is even).
+// slot pairs (one 32-byte sector) from vslot_start(h, S) on, wrapping at S (S is even).
 __host__ __device__ __forceinline__ uint32_t vslot_start(uint32_t h, uint32_t S) {
     // the bucket is the top bits of h: remix so that the low bits choose the slot
     return (uint32_t)(((uint64_t)(h * 0x9E3779B9u) * S) >> 32) & ~1u;
@@ -164,6 +164,48 @@ constexpr uint32_t kFilterBits = 1u << 18;                 // 32 KB
 constexpr uint32_t kFilterWords = kFilterBits / 32;
 __host__ __device__ __forceinline__ uint32_t vfilter_bit(uint32_t hv) { return hv & (kFilterBits - 1u); }
 
+// Read-only loads of one-shot random probes (the edge-pair table, segS, pslot / apos / E of a fresh f1) with
+// an L2 evict-first policy, so that the tables every estimator probes (the vertex table, the pair filter, vslice) stay in L2
+// while ~1 GB of probe lines per C3 batch pass through it.  Measured (tools/l2hint.cu): a 48 MB table probed
+// alongside random misses into 1 GB stays resident only when the misses are marked evict-first (DRAM bytes per
+// probe pair 168 -> 127, time -18 %); marking the hot table evict-last does nothing.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// ef: the batch is large (kPairFilterMin edges or more) -- below that the whole index stays in L2 and the hint only
+// costs hits (C2: k_update 68 vs 63 us with it)
+__device__ __forceinline__ uint4 ldf(const uint4 *p, uint32_t ef) {
+    if (!ef) return __ldg(p);
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_evict_first()));
+    return v;
+}
+__device__ __forceinline__ uint2 ldf(const uint2 *p, uint32_t ef) {
+    if (!ef) return __ldg(p);
+    uint2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_evict_first()));
+    return v;
+}
+
+// Large batches: a blocked Bloom filter over the batch's pairs (16 bits per edge, one 32-bit word per pair with
+// four of its bits set), filled by k_count as it normalises the edges (two filters alternate by batch parity:
+// k_count zeroes the next batch's while it fills this one's).  The filter is ~w·2 bytes
+// (17 MB at w = 2^23), so it stays in L2, whereas the pair table (24 B per edge) does not: Step 3's closing
+// probe reads the filter word first and goes to the table only when all four bits are set (every pair of the
+// batch; ~0.8 % of the others).  No false negatives, so results are unchanged.  On this part a random read that
+// misses L2 costs a whole 128-byte line of DRAM traffic (tools/randbench.cu, profiles/randbench_r02.txt), so
+// the filter turns most closing probes from a DRAM line into an L2 hit.
+__host__ __device__ __forceinline__ uint32_t pf_words(uint32_t w) { return w < 2 ? 1u : w / 2; }
+__host__ __device__ __forceinline__ uint32_t pf_word(uint64_t h, uint32_t nw) {
+    return (uint32_t)(((h >> 32) * (uint64_t)nw) >> 32);
+}
+__host__ __device__ __forceinline__ uint32_t pf_mask(uint64_t h) {
+    return (1u << (h & 31u)) | (1u << ((h >> 5) & 31u)) | (1u << ((h >> 10) & 31u)) | (1u << ((h >> 15) & 31u));
+}
+
 struct Lookup {
     const uint2 *E;
     const VSlot *vt;
@@ -172,6 +214,10 @@ struct Lookup {
     const uint2 *pt;       // pair slots {k, tag << 24 | fp}, groups of 4
     uint32_t G;            // pair-table groups
     uint32_t ptag;         // this batch's slot tag
+    const uint32_t *pf;    // pair filters (large batches; this batch's at pf + slot * pfs) or null
+    uint32_t pfw;          // words of a filter at this batch's size (0: no filter)
+    uint32_t pfs;          // stride between the two filters
+    uint32_t ef;           // 1: one-shot probes read with the L2 evict-first policy (large batches)
 };
 
 #ifndef TC_PT_GROUPS_PER_8
@@ -217,8 +263,8 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
     P.a0 = P.a1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
     if (ng) {
         const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
-        P.a0 = __ldg(qa);
-        P.a1 = __ldg(qa + 1);
+        P.a0 = ldf(qa, L.ef);
+        P.a1 = ldf(qa + 1, L.ef);
     }
 }
 
@@ -229,7 +275,7 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
     for (int i = 0; i < 4; ++i) {
         if ((fs[i] >> 24) != L.ptag) return 0;  // free slot (stale tag)
         if (fs[i] == P.fp) {
-            const uint2 e = __ldg(L.E + ks[i]);
+            const uint2 e = ldf(L.E + ks[i], L.ef);
             if (e.x == P.lo && e.y == P.hi) {
                 *k = ks[i];
                 return 1;
@@ -243,7 +289,7 @@ static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
     for (uint32_t i = 2; i <= P.ng; ++i) {  // every group once
         const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * pgroup_at(P.A, P.B, i, P.ng));
         uint32_t k;
-        const int r = pt_group(L, P, __ldg(q), __ldg(q + 1), &k);
+        const int r = pt_group(L, P, ldf(q, L.ef), ldf(q + 1, L.ef), &k);
         if (r == 0) return -1;
         if (r == 1) return (int64_t)k;
     }
@@ -256,7 +302,7 @@ __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &
     int r = pt_group(L, P, P.a0, P.a1, &k);
     if (r == 2) {  // group A full (rare at load 1/3): read B now
         const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
-        r = pt_group(L, P, __ldg(qb), __ldg(qb + 1), &k);
+        r = pt_group(L, P, ldf(qb, L.ef), ldf(qb + 1, L.ef), &k);
         if (r == 2) return pt_walk(L, P);
     }
     if (r == 0) return -1;
@@ -267,6 +313,17 @@ __device__ __forceinline__ int64_t pt_find(const Lookup &L, uint32_t lo, uint32_
     PairProbe P;
     pt_issue(L, lo, hi, true, P);
     return pt_resolve(L, P);
+}
+
+// pt_find behind the pair filter (when the batch has one): a pair whose four filter bits are not all set is not
+// in the batch.
+__device__ __forceinline__ int64_t pt_find_filtered(const Lookup &L, uint32_t lo, uint32_t hi) {
+    if (L.pfw) {
+        const uint64_t h = hash_pair64(pair_key(lo, hi));
+        const uint32_t m = pf_mask(h);
+        if ((__ldg(L.pf + pf_word(h, L.pfw)) & m) != m) return -1;
+    }
+    return pt_find(L, lo, hi);
 }
 
 // Vertex probe split likewise: first sector (two 16-byte slots) of each of u and v.
@@ -285,6 +342,7 @@ __device__ __forceinline__ void vt_issue(const Lookup &L, uint32_t v, VertProbe 
     P.s1 = __ldg(p + 1);
 }
 
+// {deg_W(v), segment start of v}, or {0, 0} when v has no batch arc
 __device__ __forceinline__ uint2 vt_resolve(const Lookup &L, const VertProbe &P, uint32_t v) {
     if (P.sl.y == 0) return make_uint2(0u, 0u);
     if (P.s0.x == v) return make_uint2(P.s0.y, P.s0.z);

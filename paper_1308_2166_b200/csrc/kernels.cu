@@ -123,6 +123,9 @@ struct PartArgs {
     uint32_t *ctr;
     uint32_t *filt;    // small batches: the vertex filter to fill (else null)
     unsigned long long *S;  // the two S accumulators: k_count zeroes this batch's (d->slot) and the counters
+    uint32_t *pf;      // large batches: the two pair filters (k_count fills this batch's, d->slot, and zeroes the other), else null
+    uint32_t pfw;      // words of a filter at this batch's size
+    uint32_t pfs;      // stride between the two filters
 };
 
 // a3: insert edge k = {lo, hi} into the edge-pair table: the first free slot (stale tag) of the first group
@@ -198,6 +201,14 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
         if (threadIdx.x < (uint32_t)kCtrWords && threadIdx.x != (uint32_t)kCtrErr && threadIdx.x != (uint32_t)kCtrFailB)
             a.ctr[threadIdx.x] = 0u;
     }
+    uint32_t *pfill = nullptr;
+    if (a.pf) {  // pair filters: this batch's is filled below; the other one (the next batch's) is zeroed here,
+                 // its tile's share (the host zeroes a filter itself when no earlier batch did)
+        const uint32_t slot = a.d->slot, lo = blockIdx.x * (kTileEdges / 2), hi = min(a.pfw, lo + kTileEdges / 2);
+        uint32_t *clr = a.pf + (size_t)(slot ^ 1u) * a.pfs;
+        for (uint32_t i = lo + threadIdx.x; i < hi; i += kTileThreads) clr[i] = 0u;
+        pfill = a.pf + (size_t)slot * a.pfs;
+    }
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     const uint2 *in = a.d->in;
     extern __shared__ uint32_t dsh[];
@@ -215,9 +226,14 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
         const uint32_t i = warp * kEdgesPerWarp + j * 32u + lane;
         if (i < ne) {
             const uint2 e = __ldg(in + e0 + i);
-            a.E[e0 + i] = norm_edge(e);
+            const uint2 n = norm_edge(e);
+            a.E[e0 + i] = n;
             if (e.x == kEmptyV || e.y == kEmptyV) bad |= kErrInval;
             else if (e.x == e.y) bad |= kErrLoop;
+            else if (pfill) {  // (filled in k_scatter instead: C3 step +9 us)
+                const uint64_t h = hash_pair64(pair_key(n.x, n.y));
+                atomicOr(pfill + pf_word(h, a.pfw), pf_mask(h));
+            }
         }
     }
     bad = __reduce_or_sync(kFull, bad);
@@ -504,7 +520,14 @@ __device__ __forceinline__ uint32_t pow2_ceil(uint32_t x) { return x <= 1 ? 1u :
 __device__ __forceinline__ uint32_t log2_ceil(uint32_t x) { return x <= 1 ? 0u : 32 - __clz(x - 1); }
 
 // vertex-table slice of D vertices in a bucket of n arcs (D <= n): load <= 1/2, at most 2 n slots
+// (A load-0.6 sizing, min(13 D / 8 + 2, 2 n) -- 64 MB instead of ~120 MB at C3 -- measured slower: k_update
+// 383 vs 329 us and k_vhash 351 vs 334 us at C3, the longer probe runs costing more than the L2 hits gained.)
 __device__ __forceinline__ uint32_t slice_size(uint32_t D, uint32_t n) { return D ? min(pow2_ceil(2 * D), 2 * n) : 0u; }
+
+// one vertex-table slot {x, deg_W(x), segment start}
+__device__ __forceinline__ void vt_put(const VertArgs &a, uint64_t s, uint32_t x, uint32_t deg, uint32_t start) {
+    reinterpret_cast<uint4 *>(a.vt)[s] = make_uint4(x, deg, start, 0u);
+}
 
 // One LSD pass over the items held in registers (warp-blocked layout, R rounds): stable rank by the digit
 // (key >> shift) & ((1 << bits) - 1); returns the destination index of every item in `dst`.
@@ -686,12 +709,12 @@ __device__ __forceinline__ void vbucket_sort(const VertArgs &a, uint32_t b, unsi
         __syncthreads();
         for (uint32_t s = threadIdx.x; s < S; s += kVBucketThreads) {
             const uint32_t q = table[s];
-            uint4 o = make_uint4(kEmptyV, 0u, 0u, 0u);
             if (q != 0xFFFFu) {
                 const uint32_t st = run_start[q], en = q + 1 < D ? run_start[q + 1] : n;
-                o = make_uint4(unhash_vertex(run_key[q]), en - st, base + st, 0u);
+                vt_put(a, off + s, unhash_vertex(run_key[q]), en - st, base + st);
+            } else {
+                vt_put(a, off + s, kEmptyV, 0u, 0u);
             }
-            reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
         }
         return;
     }
@@ -1060,10 +1083,9 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     __syncthreads();
     for (uint32_t s = threadIdx.x; s < S; s += NT) {
         const uint32_t l = table[s];
-        uint4 o = make_uint4(kEmptyV, 0u, 0u, 0u);
-        if (l < D) o = make_uint4(vkey[l], segst[l + 1] - segst[l], b0 + segst[l], 0u);
-        else if (l == D) o = make_uint4(hub, hubn, base, 0u);
-        reinterpret_cast<uint4 *>(a.vt)[off + s] = o;
+        if (l < D) vt_put(a, off + s, vkey[l], segst[l + 1] - segst[l], b0 + segst[l]);
+        else if (l == D) vt_put(a, off + s, hub, hubn, base);
+        else vt_put(a, off + s, kEmptyV, 0u, 0u);
     }
 }
 
@@ -1367,6 +1389,7 @@ __device__ __forceinline__ void with_desc(UpdateArgs &u, Lookup &L) {
     u.batch = u.d->batch;
     u.m_prev = u.d->m_prev;
     L.ptag = u.d->ptag;
+    if (L.pf) L.pf += (size_t)u.d->slot * L.pfs;  // this batch's pair filter
 }
 
 template <bool kSmall>
@@ -1446,10 +1469,10 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
     uint2 su = make_uint2(0u, 0u), sv = make_uint2(0u, 0u);
     const uint32_t hu = hash_vertex(r1.x), hv = hash_vertex(r1.y);
     if (fresh) {
-        r1 = __ldg(ix.L.E + j);
-        const uint2 ap = __ldg(ix.apos + j);
+        r1 = ldf(ix.L.E + j, ix.L.ef);
+        const uint2 ap = ldf(ix.apos + j, ix.L.ef);
         TC_CHECK(j < u.w && ap.x < 2 * u.w && ap.y < 2 * u.w, ix.ctr);
-        const uint2 pu = __ldg(ix.pslot + ap.x), pv = __ldg(ix.pslot + ap.y);
+        const uint2 pu = ldf(ix.pslot + ap.x, ix.L.ef), pv = ldf(ix.pslot + ap.y, ix.L.ef);
         TC_CHECK(pu.x < pu.y && pu.y <= 2 * u.w && pv.x < pv.y && pv.y <= 2 * u.w, ix.ctr);
         inf = make_uint4(pu.x, pu.y, pv.x, pv.y);
     } else {
@@ -1502,7 +1525,7 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
         const bool atU = phi < ld;  // (src = u, rank = phi) or (src = v, rank = phi - ld)
         if (r2new) {
             TC_CHECK((atU ? endU : endV) - 1u - (atU ? phi : phi - ld) < 2 * u.w, ix.ctr);
-            const uint2 arc = __ldg(ix.segS + ((atU ? endU : endV) - 1u - (atU ? phi : phi - ld)));
+            const uint2 arc = ldf(ix.segS + ((atU ? endU : endV) - 1u - (atU ? phi : phi - ld)), ix.L.ef);
             const uint32_t src = atU ? r1.x : r1.y;
             k2 = arc.x >> 1;
             r2 = make_uint2(min(src, arc.y), max(src, arc.y));
@@ -1520,7 +1543,7 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
     // fresh): ld / rd count exactly those arcs, so x without any needs no probe
     const uint32_t degx = x == r1.x ? ld : rd;
     if ((r2new || had_r2) && !closed && degx) {
-        const int64_t kk = pt_find(ix.L, min(x, z), max(x, z));
+        const int64_t kk = pt_find_filtered(ix.L, min(x, z), max(x, z));
         if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
     }
     const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
@@ -1912,7 +1935,8 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
 
 static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
     return PartArgs{ix.desc, reinterpret_cast<uint32_t *>(ix.apos), a.g, ix.E, ix.arcs, ix.cntV, ix.offV, ix.arank, ix.vstart, ix.pt, pair_groups(a.g.w), ix.ctr,
-                    a.small ? ix.filt : nullptr, a.S};
+                    a.small ? ix.filt : nullptr, a.S, a.pfilt ? ix.pf : nullptr, pf_words(a.g.w),
+                    pf_words((uint32_t)ix.wcap)};
 }
 
 int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
@@ -1992,7 +2016,9 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
-    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u}, ix.apos, ix.pslot, ix.segS, ix.ctr};
+    UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u, a.pfilt ? ix.pf : nullptr,
+                        a.pfilt ? pf_words(a.g.w) : 0u, pf_words((uint32_t)ix.wcap), a.g.w >= kPairFilterMin ? 1u : 0u},
+                 ix.apos, ix.pslot, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);

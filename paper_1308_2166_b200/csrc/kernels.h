@@ -31,6 +31,7 @@ struct IndexBufs {
     uint32_t *vstart = nullptr;    // [4097] vertex-bucket totals -> exclusive prefix
     uint32_t *ctr = nullptr;       // device counters (index.cuh kCtr*)
     uint32_t *filt = nullptr;      // [kFilterWords] small-batch filter over the batch's vertices
+    uint32_t *pf = nullptr;        // [pf_words(wcap)] large-batch pair filter (index.cuh)
     uint2 *stage = nullptr;        // [wcap] H2D staging for host batches (two buffers, alternating)
     uint2 *stage2 = nullptr;
     BatchDesc *desc = nullptr;     // the per-batch descriptor (k_desc writes it; every kernel reads it)
@@ -87,6 +88,7 @@ struct BatchArgs {
     unsigned long long *S;  // the two S accumulators (slot from the descriptor)
     bool small;       // small-batch estimator pass (filters built by k_pairs, k_update skips untouched estimators)
     Geometry g;
+    bool pfilt = false;  // the pair filter: k_pairs fills it, Step 3 of k_update reads it before the pair table
 };
 
 // Batches of at most this many edges take the filtered small-batch estimator pass (filter load <= 1/16)
@@ -100,7 +102,11 @@ struct Tuning {
     uint32_t split = 0;            // 1: the estimator pass as the split per-step kernels
     uint32_t small_index = 0;      // 0 auto (w <= kSmallIndexMax), 1 never, 2 always when w <= kSmallIndexMax
     uint32_t event_checked = 0;    // event mode: 1 = always the four-kernel path that checks the degree limit
+    uint32_t pair_filter = 0;      // 0 auto (w >= kPairFilterMin), 1 never, 2 always (bulk fused pass, partitioned index)
 };
+
+// Batches of at least this many edges get the pair filter (below it the pair table is mostly L2-resident)
+constexpr uint32_t kPairFilterMin = 1u << 21;
 
 Geometry make_geometry(uint32_t w, const Tuning &t);
 

@@ -109,6 +109,8 @@ def test_hub_segments_multi_chunk():
     dict(small_batch=2),                           # the filtered small-batch pass even for large batches
     dict(small_index=1, small_batch=1),            # small batches through the partitioned build
     dict(small_index=2, split_kernels=1),          # one-CTA index + split estimator pass
+    dict(pair_filter=2),                           # Step 3 behind the pair filter at every size
+    dict(pair_filter=2, small_batch=2, vbucket_arcs=2),  # pair filter + filtered pass + split partition
 ])
 def test_index_geometry_knobs(knobs):
     """Results never depend on the index geometry (tc_tune): bit-exact against the oracle.  Batches of at most
@@ -478,3 +480,33 @@ def test_graph_relaunch_steady_stream():
     assert tc.sync() == 0
     assert tc.graph_captures() == (1 if len(s) % 3000 == 0 else 2)
     assert_states_equal(tc.state(), oracle_run(s, 4000, 6, 3000).state(), "graph relaunch")
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pair_filter_mixed_sizes(graphs):
+    """Step 3 behind the pair filter (tc_tune pair_filter=2): the two filters alternate by batch parity and k_count
+    zeroes the next one, so batches of changing size, one-CTA-index batches (no filter) in between and a
+    rejected batch must all leave the oracle's exact state."""
+    from paper_1308_2166_b200 import TCError, TriangleCounter
+    s = rmat(14, 12, 77)
+    sizes = [9000, 300, 12000, 1, 7000, 5000, 4097, 20000, 2, 15000]
+    tc = TriangleCounter(3000, 21)
+    tc.tune(pair_filter=2)
+    tc.set_graphs(graphs)
+    o_bounds, k = [], 0
+    for i, w in enumerate(sizes * 3):
+        if k >= len(s):
+            break
+        if i == 7:  # a rejected batch (self-loop) changes nothing
+            bad = np.array(s[k:k + 5000])
+            bad[17] = [bad[17][0], bad[17][0]]
+            with pytest.raises(TCError):
+                tc.push_batch(bad)
+        tc.push_batch(s[k:k + w])
+        o_bounds.append((k, min(len(s), k + w)))
+        k += w
+    from oracle.indexed import IndexedOracle
+    o = IndexedOracle(3000, 21, 0, None)
+    for a, b in o_bounds:
+        assert o.push_batch(s[a:b]) == 0
+    assert_states_equal(tc.state(), o.state(), f"pair filter, graphs={graphs}")
