@@ -174,17 +174,19 @@ __device__ __forceinline__ uint64_t l2_evict_first() {
     asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
-// ef: the batch is large (kPairFilterMin edges or more) -- below that the whole index stays in L2 and the hint only
-// costs hits (C2: k_update 68 vs 63 us with it)
-__device__ __forceinline__ uint4 ldf(const uint4 *p, uint32_t ef) {
-    if (!ef) return __ldg(p);
+// EF: the batch is large (kPairFilterMin edges or more) -- below that the whole index stays in L2 and the hint only
+// costs hits (C2: k_update 68 vs 63 us with it).  A template parameter, so the other instantiations carry nothing.
+template <bool EF>
+__device__ __forceinline__ uint4 ldf(const uint4 *p) {
+    if (!EF) return __ldg(p);
     uint4 v;
     asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_evict_first()));
     return v;
 }
-__device__ __forceinline__ uint2 ldf(const uint2 *p, uint32_t ef) {
-    if (!ef) return __ldg(p);
+template <bool EF>
+__device__ __forceinline__ uint2 ldf(const uint2 *p) {
+    if (!EF) return __ldg(p);
     uint2 v;
     asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_evict_first()));
     return v;
@@ -217,7 +219,6 @@ struct Lookup {
     const uint32_t *pf;    // pair filters (large batches; this batch's at pf + slot * pfs) or null
     uint32_t pfw;          // words of a filter at this batch's size (0: no filter)
     uint32_t pfs;          // stride between the two filters
-    uint32_t ef;           // 1: one-shot probes read with the L2 evict-first policy (large batches)
 };
 
 #ifndef TC_PT_GROUPS_PER_8
@@ -250,6 +251,7 @@ struct PairProbe {
     uint4 a0, a1;  // group A
 };
 
+template <bool EF = false>
 __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t hi, bool active, PairProbe &P) {
     const uint64_t h = hash_pair64(pair_key(lo, hi));
     const uint32_t ng = active ? L.G : 0u;
@@ -263,19 +265,20 @@ __device__ __forceinline__ void pt_issue(const Lookup &L, uint32_t lo, uint32_t 
     P.a0 = P.a1 = make_uint4(0u, 0u, 0u, 0u);  // tag 0: free
     if (ng) {
         const uint4 *qa = reinterpret_cast<const uint4 *>(P.sl + 4 * P.A);
-        P.a0 = ldf(qa, L.ef);
-        P.a1 = ldf(qa + 1, L.ef);
+        P.a0 = ldf<EF>(qa);
+        P.a1 = ldf<EF>(qa + 1);
     }
 }
 
 // 0: not in the group and the group has room (absent); 1: found (*k set); 2: group full, go on.
+template <bool EF = false>
 __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uint4 q0, uint4 q1, uint32_t *k) {
     const uint32_t ks[4] = {q0.x, q0.z, q1.x, q1.z}, fs[4] = {q0.y, q0.w, q1.y, q1.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         if ((fs[i] >> 24) != L.ptag) return 0;  // free slot (stale tag)
         if (fs[i] == P.fp) {
-            const uint2 e = ldf(L.E + ks[i], L.ef);
+            const uint2 e = ldf<EF>(L.E + ks[i]);
             if (e.x == P.lo && e.y == P.hi) {
                 *k = ks[i];
                 return 1;
@@ -285,45 +288,49 @@ __device__ __forceinline__ int pt_group(const Lookup &L, const PairProbe &P, uin
     return 2;
 }
 
+template <bool EF = false>
 static __device__ __noinline__ int64_t pt_walk(const Lookup &L, PairProbe P) {
     for (uint32_t i = 2; i <= P.ng; ++i) {  // every group once
         const uint4 *q = reinterpret_cast<const uint4 *>(P.sl + 4 * pgroup_at(P.A, P.B, i, P.ng));
         uint32_t k;
-        const int r = pt_group(L, P, ldf(q, L.ef), ldf(q + 1, L.ef), &k);
+        const int r = pt_group<EF>(L, P, ldf<EF>(q), ldf<EF>(q + 1), &k);
         if (r == 0) return -1;
         if (r == 1) return (int64_t)k;
     }
     return -1;
 }
 
+template <bool EF = false>
 __device__ __forceinline__ int64_t pt_resolve(const Lookup &L, const PairProbe &P) {
     if (P.ng == 0) return -1;
     uint32_t k;
-    int r = pt_group(L, P, P.a0, P.a1, &k);
+    int r = pt_group<EF>(L, P, P.a0, P.a1, &k);
     if (r == 2) {  // group A full (rare at load 1/3): read B now
         const uint4 *qb = reinterpret_cast<const uint4 *>(P.sl + 4 * P.B);
-        r = pt_group(L, P, ldf(qb, L.ef), ldf(qb + 1, L.ef), &k);
-        if (r == 2) return pt_walk(L, P);
+        r = pt_group<EF>(L, P, ldf<EF>(qb), ldf<EF>(qb + 1), &k);
+        if (r == 2) return pt_walk<EF>(L, P);
     }
     if (r == 0) return -1;
     return (int64_t)k;
 }
 
+template <bool EF = false>
 __device__ __forceinline__ int64_t pt_find(const Lookup &L, uint32_t lo, uint32_t hi) {
     PairProbe P;
-    pt_issue(L, lo, hi, true, P);
-    return pt_resolve(L, P);
+    pt_issue<EF>(L, lo, hi, true, P);
+    return pt_resolve<EF>(L, P);
 }
 
 // pt_find behind the pair filter (when the batch has one): a pair whose four filter bits are not all set is not
 // in the batch.
+template <bool EF>
 __device__ __forceinline__ int64_t pt_find_filtered(const Lookup &L, uint32_t lo, uint32_t hi) {
     if (L.pfw) {
         const uint64_t h = hash_pair64(pair_key(lo, hi));
         const uint32_t m = pf_mask(h);
         if ((__ldg(L.pf + pf_word(h, L.pfw)) & m) != m) return -1;
     }
-    return pt_find(L, lo, hi);
+    return pt_find<EF>(L, lo, hi);
 }
 
 // Vertex probe split likewise: first sector (two 16-byte slots) of each of u and v.

@@ -1437,11 +1437,11 @@ __device__ __forceinline__ bool touched_by(const uint32_t *sf, uint2 r1) {
     return filter_has(sf, vfilter_bit(hash_vertex(r1.x))) || filter_has(sf, vfilter_bit(hash_vertex(r1.y)));
 }
 
-template <bool kSmall>
+template <bool kSmall, bool kEF>
 __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const UpdateIdx &ix, uint64_t t, const EstState &old,
                                                 const Step1 &s1, uint32_t &n_fresh, uint32_t &n_r2old);
 
-template <bool kSmall>
+template <bool kSmall, bool kEF>
 __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const UpdateIdx &ix, uint64_t t, const EstState &old,
                                                uint32_t &n_fresh, uint32_t &n_r2old, uint32_t &n_skip, const uint32_t *sf) {
     const Step1 s1 = step1_draw(u, t);
@@ -1449,11 +1449,11 @@ __device__ __forceinline__ uint32_t update_one(const UpdateArgs &u, const Update
         ++n_skip;
         return (old.cf & kClosedBit) ? (old.cf & kCMask) : 0u;
     }
-    return update_rest<kSmall>(u, ix, t, old, s1, n_fresh, n_r2old);
+    return update_rest<kSmall, kEF>(u, ix, t, old, s1, n_fresh, n_r2old);
 }
 
 // Steps 2-3 and the state writes, after Step 1's draw (s1).  Returns chi if the estimator ends closed.
-template <bool kSmall>
+template <bool kSmall, bool kEF>
 __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const UpdateIdx &ix, uint64_t t, const EstState &old,
                                                 const Step1 &s1, uint32_t &n_fresh, uint32_t &n_r2old) {
     const uint64_t gid = u.first + t;
@@ -1469,10 +1469,10 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
     uint2 su = make_uint2(0u, 0u), sv = make_uint2(0u, 0u);
     const uint32_t hu = hash_vertex(r1.x), hv = hash_vertex(r1.y);
     if (fresh) {
-        r1 = ldf(ix.L.E + j, ix.L.ef);
-        const uint2 ap = ldf(ix.apos + j, ix.L.ef);
+        r1 = ldf<kEF>(ix.L.E + j);
+        const uint2 ap = ldf<kEF>(ix.apos + j);
         TC_CHECK(j < u.w && ap.x < 2 * u.w && ap.y < 2 * u.w, ix.ctr);
-        const uint2 pu = ldf(ix.pslot + ap.x, ix.L.ef), pv = ldf(ix.pslot + ap.y, ix.L.ef);
+        const uint2 pu = ldf<kEF>(ix.pslot + ap.x), pv = ldf<kEF>(ix.pslot + ap.y);
         TC_CHECK(pu.x < pu.y && pu.y <= 2 * u.w && pv.x < pv.y && pv.y <= 2 * u.w, ix.ctr);
         inf = make_uint4(pu.x, pu.y, pv.x, pv.y);
     } else {
@@ -1525,7 +1525,7 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
         const bool atU = phi < ld;  // (src = u, rank = phi) or (src = v, rank = phi - ld)
         if (r2new) {
             TC_CHECK((atU ? endU : endV) - 1u - (atU ? phi : phi - ld) < 2 * u.w, ix.ctr);
-            const uint2 arc = ldf(ix.segS + ((atU ? endU : endV) - 1u - (atU ? phi : phi - ld)), ix.L.ef);
+            const uint2 arc = ldf<kEF>(ix.segS + ((atU ? endU : endV) - 1u - (atU ? phi : phi - ld)));
             const uint32_t src = atU ? r1.x : r1.y;
             k2 = arc.x >> 1;
             r2 = make_uint2(min(src, arc.y), max(src, arc.y));
@@ -1543,7 +1543,7 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
     // fresh): ld / rd count exactly those arcs, so x without any needs no probe
     const uint32_t degx = x == r1.x ? ld : rd;
     if ((r2new || had_r2) && !closed && degx) {
-        const int64_t kk = pt_find_filtered(ix.L, min(x, z), max(x, z));
+        const int64_t kk = pt_find_filtered<kEF>(ix.L, min(x, z), max(x, z));
         if (kk >= 0 && (!r2new || (uint32_t)kk > k2)) closed = true;
     }
     const uint32_t cf_new = c | (closed ? kClosedBit : 0u);
@@ -1575,7 +1575,9 @@ __device__ __forceinline__ uint32_t update_rest(const UpdateArgs &u, const Updat
 #ifndef TC_UPD_MINB
 #define TC_UPD_MINB 4
 #endif
-template <bool kSmall>
+// kEF: a large batch (kPairFilterMin edges or more): one-shot probes evict-first in L2, as a compile-time
+// constant so that the small instantiations carry no trace of it (C2: +3.5 us when it was a runtime flag)
+template <bool kSmall, bool kEF>
 __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, UpdateIdx ix, unsigned long long *S,
                                                    unsigned long long *stats, const uint32_t *filt) {
     with_desc(u, ix.L);
@@ -1603,7 +1605,7 @@ __global__ void __launch_bounds__(256, TC_UPD_MINB) k_update(UpdateArgs u, Updat
         const uint64_t tn = t + stride;
         EstState nxt;
         if (tn < u.count) nxt = load_state<kSmall>(u, tn);
-        contrib += update_one<kSmall>(u, ix, t, cur, n_fresh, n_r2old, n_skip, sf);
+        contrib += update_one<kSmall, kEF>(u, ix, t, cur, n_fresh, n_r2old, n_skip, sf);
         cur = nxt;
         t = tn;
     }
@@ -1902,7 +1904,7 @@ int sm_count() {
 #ifndef TC_UPD_WAVES
 #define TC_UPD_WAVES 1
 #endif
-constexpr uint32_t kUpdateCTAsPerSM = 4, kUpdateWaves = TC_UPD_WAVES;  // k_update grid
+constexpr uint32_t kUpdateCTAsPerSM = TC_UPD_MINB, kUpdateWaves = TC_UPD_WAVES;  // k_update grid
 
 static inline uint32_t grid_for(uint64_t items, uint32_t threads, uint32_t per_sm) {
     const uint64_t want = (items + threads - 1) / threads;
@@ -2017,15 +2019,17 @@ int launch_vertices_big(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s,
 int launch_update(const IndexBufs &ix, const StateBufs &st, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     if (st.count == 0) return 0;
     UpdateIdx ui{Lookup{ix.E, ix.vt, ix.vslice, a.g.bv, ix.pt, pair_groups(a.g.w), 0u, a.pfilt ? ix.pf : nullptr,
-                        a.pfilt ? pf_words(a.g.w) : 0u, pf_words((uint32_t)ix.wcap), a.g.w >= kPairFilterMin ? 1u : 0u},
+                        a.pfilt ? pf_words(a.g.w) : 0u, pf_words((uint32_t)ix.wcap)},
                  ix.apos, ix.pslot, ix.segS, ix.ctr};
     UpdateArgs u{st.r1, st.r2, st.cf, st.p1, st.p2, st.count, a.first, a.seed, 0u, a.g.w, 0ull, ix.desc};
     const uint32_t grid = grid_for(st.count, 256, kUpdateCTAsPerSM * kUpdateWaves);
     kr.beg(K_UPDATE, s);
     if (a.small)
-        k_update<true><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, ix.filt);
+        k_update<true, false><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, ix.filt);
+    else if (a.g.w >= kPairFilterMin)
+        k_update<false, true><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, nullptr);
     else
-        k_update<false><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, nullptr);
+        k_update<false, false><<<grid, 256, 0, s>>>(u, ui, st.S, st.stats, nullptr);
     kr.end(K_UPDATE, s);
     return 1;
 }
