@@ -189,7 +189,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     bool ok = cudaMalloc(&ix.E, 8 * cap) == cudaSuccess && cudaMalloc(&ix.apos, 8 * cap) == cudaSuccess &&
               cudaMalloc(&ix.pslot, 16 * cap) == cudaSuccess &&
               cudaMalloc(&ix.segS, 16 * cap) == cudaSuccess &&
-              cudaMalloc(&ix.pt, 32ull * pair_groups((uint32_t)cap)) == cudaSuccess &&
+              cudaMalloc(&ix.pt, 32ull * pair_groups_alloc((uint32_t)cap)) == cudaSuccess &&
               cudaMalloc(&ix.vt, 16 * 4 * cap) == cudaSuccess &&  // slices at 2 * (bucket start), <= 2 n_b slots
               cudaMalloc(&ix.vslice, 8 * kMaxBuckets) == cudaSuccess;
     ok = ok && cudaMalloc(&ix.arcs, 32 * cap) == cudaSuccess && cudaMalloc(&ix.vstart2, 4 * kStartWords) == cudaSuccess &&
@@ -225,7 +225,7 @@ static int grow_index(tc_ctx *ctx, uint64_t w) {
     ix.wcap = cap;
     CK(cudaMemsetAsync(ix.ctr, 0, 4 * kCtrWords, ctx->stream));
     CK(cudaMemsetAsync(ix.ctr + kCtrFailB, 0xFF, 4, ctx->stream));
-    CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)cap), ctx->stream));  // tag 0: free
+    CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups_alloc((uint32_t)cap), ctx->stream));  // tag 0: free
     CK(cudaMemsetAsync(ix.pf, 0, 8ull * pf_words((uint32_t)cap), ctx->stream));
     ctx->pf_zeroed[0] = ctx->pf_zeroed[1] = pf_words((uint32_t)cap);
     ctx->ptag = 0;
@@ -687,7 +687,7 @@ static int push_launch(tc_ctx *ctx, uint64_t w, const PushPrep &pp) {
         ctx->pf_zeroed[slot ^ 1] = std::max(ctx->pf_zeroed[slot ^ 1], need);
     }
     if (++ctx->ptag == 255) {  // edge-pair slot tags 1..254: clear the table once per 254 pushes
-        CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups((uint32_t)ix.wcap), ctx->stream));
+        CK(cudaMemsetAsync(ix.pt, 0, 32ull * pair_groups_alloc((uint32_t)ix.wcap), ctx->stream));
         ctx->ptag = 1;
     }
     BatchDesc d;

@@ -105,8 +105,8 @@ struct Tuning {
     uint32_t pair_filter = 0;      // 0 auto (w >= kPairFilterMin), 1 never, 2 always (bulk fused pass, partitioned index)
 };
 
-// Batches of at least this many edges get the pair filter (below it the pair table is mostly L2-resident)
-constexpr uint32_t kPairFilterMin = 1u << 21;
+// Batches of at least kPairFilterMin (index.cuh) edges get the pair filter (below it the pair table is mostly
+// L2-resident)
 
 Geometry make_geometry(uint32_t w, const Tuning &t);
 
