@@ -425,7 +425,10 @@ constexpr int kSplitThreads = 1024;
 __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     constexpr uint32_t NW = kSplitThreads / 32;
-    __shared__ uint32_t wc[NW][1u << kMaxSplitBits];
+    static_assert(NW == 32, "the per-sub-bucket scan over warps is one warp of shuffles");
+    // wc: per chunk, each warp's count of every sub-bucket value, then (after the scan) its output offset inside
+    // the sub-bucket; two buffers alternate by chunk parity, so a chunk needs two barriers, not four
+    __shared__ uint32_t wc[2][NW][1u << kMaxSplitBits];
     __shared__ uint32_t tot[1u << kMaxSplitBits], soff[1u << kMaxSplitBits], run[1u << kMaxSplitBits];
     const uint32_t b = blockIdx.x, S = 1u << a.bs;
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
@@ -457,7 +460,8 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     }
     __syncthreads();
     // pass B: stable ranks chunk by chunk (chunk order, then warp order, then lane order = arrival order)
-    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
+    uint32_t par = 0;
+    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads, par ^= 1u) {
         const uint32_t i = q0 + threadIdx.x;
         const bool valid = i < n;
         uint4 x4 = make_uint4(0u, 0u, 0u, 0u);
@@ -465,25 +469,25 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
         const uint32_t sb = valid ? (hash_vertex(x4.x) >> sh) & smask : 0u;
         const uint32_t peers = digit_peers(sb, valid, a.bs);  // lanes with my sub-bucket value (bs ballots)
         const uint32_t mine = __popc(peers & lt);
-        if (lane < S) wc[warp][lane] = 0u;
+        if (lane < S) wc[par][warp][lane] = 0u;
         __syncwarp();
-        if (valid && mine == 0) wc[warp][sb] = __popc(peers);
+        if (valid && mine == 0) wc[par][warp][sb] = __popc(peers);
         __syncthreads();
-        if (threadIdx.x < S) {  // per sub-bucket: exclusive prefix over warps
-            uint32_t r = 0;
-            for (uint32_t w2 = 0; w2 < NW; ++w2) {
-                const uint32_t c = wc[w2][threadIdx.x];
-                wc[w2][threadIdx.x] = r;
-                r += c;
+        if (warp < S) {  // warp x scans sub-bucket x over the 32 warps: exclusive prefix + the running offset
+            const uint32_t c = wc[par][lane][warp];
+            uint32_t inc = c;
+#pragma unroll
+            for (uint32_t o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, inc, o);
+                if (lane >= o) inc += y;
             }
-            tot[threadIdx.x] = r;  // this chunk's count
+            const uint32_t r0 = run[warp];
+            wc[par][lane][warp] = soff[warp] + r0 + inc - c;
+            if (lane == 31) run[warp] = r0 + inc;  // only this warp touches run[warp]
         }
         __syncthreads();
-        TC_CHECK(!valid || soff[sb] + run[sb] + wc[warp][sb] + mine < n, a.ctr);
-        if (valid) a.arcs2[base + soff[sb] + run[sb] + wc[warp][sb] + mine] = x4;
-        __syncthreads();
-        if (threadIdx.x < S) run[threadIdx.x] += tot[threadIdx.x];
-        __syncthreads();
+        TC_CHECK(!valid || wc[par][warp][sb] + mine < n, a.ctr);
+        if (valid) a.arcs2[base + wc[par][warp][sb] + mine] = x4;
     }
 }
 
