@@ -406,8 +406,9 @@ def run_b200(args):
                 "dram_frac": rows[dom].get("dram_frac"),
                 "dram_frac_note": "traffic / duration, both from the ncu pipeline capture (DRAM bytes the kernel "
                                   "actually moves, application replay without cache control), over peak: how close "
-                                  "the kernel is to HBM on the accesses it makes (random 8-32 B probes cost a 32-64 B "
-                                  "DRAM access each)",
+                                  "the kernel is to HBM on the accesses it makes (a random 8-32 B probe that misses "
+                                  "L2 moves a whole 128-byte line from DRAM on this part, whatever the load flavour: "
+                                  "profiles/randbench_r02.txt)",
                 "byte_model": "SURVEY 8(d): Ke 16w (k_count) + 16w (k_scatter); Ki 8 B/arc + 16 B/vertex; "
                               "Kp 24w; Ku 24 B/estimator + 16 B per replaced r1 + 16 B per replaced r2",
                 "kernels": rows,

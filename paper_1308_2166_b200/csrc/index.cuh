@@ -7,7 +7,8 @@
 //             rank(x->y) of the arc at slot s = segEnd(x) - 1 - s (Definition Rank).
 //             Vertices are grouped by BUCKET (the top bv bits of hash_vertex), each bucket owns the slot
 //             range of its arcs; inside a bucket vertices appear in hash order.
-//   einfo[k]  uint4  {slot of the lo-arc, segEnd(lo), slot of the hi-arc, segEnd(hi)}
+//   apos[k]   uint2  partition positions of edge k's two arcs; pslot[p] uint2 {slot in segS, segment end} of the
+//             arc at partition position p (a fresh f1 = W[j] reads apos[j], then its two pslot entries)
 //   vertex table: one open-addressing slice per vertex bucket, min(next_pow2(2 D_b), 2 n_b) slots (load <= 1/2)
 //             for the bucket's D_b distinct vertices (n_b arcs), 16 B slots {x, deg_W(x), segment start, 0}, at
 //             offset 2 * (the bucket's first arc slot) -- slices never overlap and need no prefix sum;
@@ -63,6 +64,7 @@ constexpr int kCtrFailB = 6;   // batch index of the first batch that found the 
 constexpr int kCtrArcsBig = 7; // arcs grouped by the large-bucket kernels (k_vhub / k_vbig)
 constexpr int kCtrDBig = 8;    // distinct vertices of those buckets
 constexpr int kCtrCursor = 9;  // k_small_index: next free segment slot (each bucket CTA takes its range)
+constexpr int kCtrQ = 10;      // large batches: Step 3 queries queued by k_update for k_close_q
 constexpr int kCtrWords = 16;
 
 // Per-batch values the kernels read from device memory (written by k_desc, the first node of every push), so
