@@ -422,6 +422,7 @@ struct SplitArgs {
 
 constexpr int kSplitThreads = 1024;
 
+template <int BS>  // the split bits (1..kMaxSplitBits) as a compile-time constant: BS ballots per arc
 __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     constexpr uint32_t NW = kSplitThreads / 32;
@@ -430,10 +431,10 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     // the sub-bucket; two buffers alternate by chunk parity, so a chunk needs two barriers, not four
     __shared__ uint32_t wc[2][NW][1u << kMaxSplitBits];
     __shared__ uint32_t tot[1u << kMaxSplitBits], soff[1u << kMaxSplitBits], run[1u << kMaxSplitBits];
-    const uint32_t b = blockIdx.x, S = 1u << a.bs;
+    const uint32_t b = blockIdx.x, S = 1u << BS;
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
-    const uint32_t sh = 32 - a.bp1 - a.bs, smask = S - 1u;
+    const uint32_t sh = 32 - a.bp1 - BS, smask = S - 1u;
     if (threadIdx.x < S) {
         tot[threadIdx.x] = 0;
         run[threadIdx.x] = 0;
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
         const uint32_t i = q0 + threadIdx.x;
         const bool valid = i < n;
         const uint32_t sb = valid ? (hash_vertex(a.arcs[base + i].x) >> sh) & smask : 0u;
-        const uint32_t peers = digit_peers(sb, valid, a.bs);
+        const uint32_t peers = digit_peers_c<BS>(sb, valid);
         if (valid && (peers & lt) == 0) atomicAdd(&tot[sb], __popc(peers));
     }
     __syncthreads();
@@ -452,11 +453,11 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
         uint32_t r = 0;
         for (uint32_t x = 0; x < S; ++x) {
             soff[x] = r;
-            a.vstart2[(b << a.bs) + x] = base + r;
-            if (tot[x] > a.vcap) a.vperm[atomicAdd(&a.ctr[kCtrBig], 1u)] = (b << a.bs) + x;
+            a.vstart2[(b << BS) + x] = base + r;
+            if (tot[x] > a.vcap) a.vperm[atomicAdd(&a.ctr[kCtrBig], 1u)] = (b << BS) + x;
             r += tot[x];
         }
-        if (b == gridDim.x - 1) a.vstart2[gridDim.x << a.bs] = base + n;
+        if (b == gridDim.x - 1) a.vstart2[gridDim.x << BS] = base + n;
     }
     __syncthreads();
     // pass B: stable ranks chunk by chunk (chunk order, then warp order, then lane order = arrival order)
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
         uint4 x4 = make_uint4(0u, 0u, 0u, 0u);
         if (valid) x4 = a.arcs[base + i];
         const uint32_t sb = valid ? (hash_vertex(x4.x) >> sh) & smask : 0u;
-        const uint32_t peers = digit_peers(sb, valid, a.bs);  // lanes with my sub-bucket value (bs ballots)
+        const uint32_t peers = digit_peers_c<BS>(sb, valid);  // lanes with my sub-bucket value (bs ballots)
         const uint32_t mine = __popc(peers & lt);
         if (lane < S) wc[par][warp][lane] = 0u;
         __syncwarp();
@@ -1973,7 +1974,12 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, co
     if (!g.bs) return 4;
     SplitArgs sa{ix.arcs, ix.arcs2, ix.vstart, ix.vstart2, g.bp1, g.bs, g.vcap, ix.vperm, ix.ctr};
     kr.beg(K_SPLIT, s);
-    k_split<<<nV, kSplitThreads, 0, s>>>(sa);
+    switch (g.bs) {
+        case 1: k_split<1><<<nV, kSplitThreads, 0, s>>>(sa); break;
+        case 2: k_split<2><<<nV, kSplitThreads, 0, s>>>(sa); break;
+        case 3: k_split<3><<<nV, kSplitThreads, 0, s>>>(sa); break;
+        default: k_split<kMaxSplitBits><<<nV, kSplitThreads, 0, s>>>(sa); break;
+    }
     kr.end(K_SPLIT, s);
     return 5;
 }

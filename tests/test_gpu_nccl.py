@@ -57,6 +57,24 @@ def test_rank_handle_world1_matches_oracle(async_, graphs):
         assert tc.estimate_mom(groups) == plain.estimate_mom(groups)
 
 
+@pytest.mark.parametrize("graphs", [False, True])
+def test_rank_handle_world1_pair_filter(graphs):
+    """The large-batch path (pair filter filled by k_count, evict-first probes, half-full edge-pair table) through
+    a rank handle: batches broadcast on the comm stream into alternating receive buffers while the filters
+    alternate by batch parity."""
+    from paper_1308_2166_b200 import TriangleCounter, nccl_unique_id
+    s = rmat(14, 16, 9)
+    r, w = 4000, 20000
+    tc = TriangleCounter.rank(r, 3, 0, 1, nccl_unique_id(), device=0, w_max_hint=w)
+    tc.tune(pair_filter=2, small_batch=1)
+    tc.set_graphs(graphs)
+    for k in range(0, len(s), w):
+        tc.push_batch(s[k:k + w])
+    o = oracle_run(s, r, 3, w)
+    assert_states_equal(tc.state(), o.state(), f"rank handle + pair filter, graphs={graphs}")
+    assert tc.closed_sum() == o.closed_sum()
+
+
 def test_rank_handle_rejects_bad_batch_and_large_w():
     from paper_1308_2166_b200 import TriangleCounter, nccl_unique_id
     from paper_1308_2166_b200._lib import TC_EDUP, TC_EINVAL
