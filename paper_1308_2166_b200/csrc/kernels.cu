@@ -351,21 +351,28 @@ __global__ void __launch_bounds__(kScanWarps * 32) k_scan_cols(const uint32_t *c
 
 // Tile scatter: arc {vertex, k<<1|side, neighbour} -> arcs[start(bucket) + offset(bucket, tile) + rank in
 // tile].  Pure streaming: the ranks come from k_count.
+// kSmemE: the tile's edges staged in shared memory (12 B of shared memory per tile edge), else read from E through
+// L1 (4 B per tile edge: more CTAs per SM).  Measured: staging wins at C2 (20.7 vs 25.0 us), E through L1 at C3
+// (174 vs 180 us), so batches of 2^22 edges and more take the second.
+constexpr uint32_t kScatterGlobalEMin = 1u << 22;
+template <bool kSmemE>
 __global__ void __launch_bounds__(kTileThreads) k_scatter(PartArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;
     extern __shared__ uint32_t dsh[];
     __shared__ uint32_t ws[kTileThreads / 32 + 1];
     const uint32_t nV = 1u << a.g.bp1;
     uint32_t *soff = dsh, *toff = dsh + nV;                            // [nV] each
-    uint2 *sE = reinterpret_cast<uint2 *>(dsh + 2 * nV);               // [kTileEdges] the tile's edges
-    uint16_t *idx = reinterpret_cast<uint16_t *>(sE + kTileEdges);    // [2 kTileEdges] arcs in bucket order
     const uint32_t t = blockIdx.x, e0 = t * kTileEdges;
+    uint2 *sEs = reinterpret_cast<uint2 *>(dsh + 2 * nV);              // [kTileEdges] the tile's edges (kSmemE)
+    const uint2 *sE = kSmemE ? sEs : a.E + e0;
+    uint16_t *idx = reinterpret_cast<uint16_t *>(dsh + 2 * nV + (kSmemE ? 2 * kTileEdges : 0));  // arcs in bucket order
     const uint32_t ne = min(kTileEdges, a.g.w - e0);
     for (uint32_t d = threadIdx.x; d < nV; d += kTileThreads) {
         soff[d] = a.vstart[d] + a.offV[(size_t)t * nV + d];
         toff[d] = a.cntV[(size_t)t * nV + d];
     }
-    for (uint32_t i = threadIdx.x; i < ne; i += kTileThreads) sE[i] = a.E[e0 + i];
+    if (kSmemE)
+        for (uint32_t i = threadIdx.x; i < ne; i += kTileThreads) sEs[i] = a.E[e0 + i];
     __syncthreads();
     {  // where each bucket's run starts in the tile's bucket order
         const uint32_t per = (nV + kTileThreads - 1) / kTileThreads;
@@ -429,8 +436,8 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     static_assert(NW == 32, "the per-sub-bucket scan over warps is one warp of shuffles");
     // wc: per chunk, each warp's count of every sub-bucket value, then (after the scan) its output offset inside
     // the sub-bucket; two buffers alternate by chunk parity, so a chunk needs two barriers, not four
-    __shared__ uint32_t wc[2][NW][1u << kMaxSplitBits];
-    __shared__ uint32_t tot[1u << kMaxSplitBits], soff[1u << kMaxSplitBits], run[1u << kMaxSplitBits];
+    __shared__ uint32_t wc[2][NW][1u << BS];
+    __shared__ uint32_t tot[1u << BS], soff[1u << BS], run[1u << BS];
     const uint32_t b = blockIdx.x, S = 1u << BS;
     const uint32_t base = a.vstart[b], n = a.vstart[b + 1] - base;
     const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5, lt = (1u << lane) - 1u;
@@ -441,10 +448,14 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     }
     __syncthreads();
     // pass A: sub-bucket sizes (the lanes of each sub-bucket value found with bs ballots; its first lane adds)
-    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads) {
+    // the sub-bucket values of this thread's first kCache chunks are kept (BS bits each) for pass B
+    constexpr uint32_t kCache = 32 / BS;
+    uint32_t sbc = 0;
+    for (uint32_t q0 = 0, c = 0; q0 < n; q0 += kSplitThreads, ++c) {
         const uint32_t i = q0 + threadIdx.x;
         const bool valid = i < n;
         const uint32_t sb = valid ? (hash_vertex(a.arcs[base + i].x) >> sh) & smask : 0u;
+        if (c < kCache) sbc |= sb << (c * BS);
         const uint32_t peers = digit_peers_c<BS>(sb, valid);
         if (valid && (peers & lt) == 0) atomicAdd(&tot[sb], __popc(peers));
     }
@@ -462,12 +473,12 @@ __global__ void __launch_bounds__(kSplitThreads) k_split(SplitArgs a) {
     __syncthreads();
     // pass B: stable ranks chunk by chunk (chunk order, then warp order, then lane order = arrival order)
     uint32_t par = 0;
-    for (uint32_t q0 = 0; q0 < n; q0 += kSplitThreads, par ^= 1u) {
+    for (uint32_t q0 = 0, c = 0; q0 < n; q0 += kSplitThreads, par ^= 1u, ++c) {
         const uint32_t i = q0 + threadIdx.x;
         const bool valid = i < n;
         uint4 x4 = make_uint4(0u, 0u, 0u, 0u);
         if (valid) x4 = a.arcs[base + i];
-        const uint32_t sb = valid ? (hash_vertex(x4.x) >> sh) & smask : 0u;
+        const uint32_t sb = !valid ? 0u : c < kCache ? (sbc >> (c * BS)) & smask : (hash_vertex(x4.x) >> sh) & smask;
         const uint32_t peers = digit_peers_c<BS>(sb, valid);  // lanes with my sub-bucket value (bs ballots)
         const uint32_t mine = __popc(peers & lt);
         if (lane < S) wc[par][warp][lane] = 0u;
@@ -1969,16 +1980,21 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, co
     k_scan_tot<<<1, 1024, 0, s>>>(ix.vstart, nV, g.bs ? 0xFFFFFFFFu : g.vcap, ix.vperm, ix.ctr);
     kr.end(K_SCAN_TOT, s);
     kr.beg(K_SCATTER, s);
-    k_scatter<<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
+    if (g.w >= kScatterGlobalEMin)
+        k_scatter<false><<<g.tiles, kTileThreads, 8 * nV + 4 * kTileEdges, s>>>(p);
+    else
+        k_scatter<true><<<g.tiles, kTileThreads, 8 * nV + 12 * kTileEdges, s>>>(p);
     kr.end(K_SCATTER, s);
     if (!g.bs) return 4;
     SplitArgs sa{ix.arcs, ix.arcs2, ix.vstart, ix.vstart2, g.bp1, g.bs, g.vcap, ix.vperm, ix.ctr};
     kr.beg(K_SPLIT, s);
+    static_assert(kMaxSplitBits <= 5, "k_split scans each sub-bucket with one of its 32 warps");
     switch (g.bs) {
         case 1: k_split<1><<<nV, kSplitThreads, 0, s>>>(sa); break;
         case 2: k_split<2><<<nV, kSplitThreads, 0, s>>>(sa); break;
         case 3: k_split<3><<<nV, kSplitThreads, 0, s>>>(sa); break;
-        default: k_split<kMaxSplitBits><<<nV, kSplitThreads, 0, s>>>(sa); break;
+        case 4: k_split<4><<<nV, kSplitThreads, 0, s>>>(sa); break;
+        default: k_split<5><<<nV, kSplitThreads, 0, s>>>(sa); break;
     }
     kr.end(K_SPLIT, s);
     return 5;
@@ -2101,7 +2117,9 @@ int set_kernel_attributes() {
     for (int b = 0; b <= 12 && e2 == cudaSuccess; ++b)
         e2 = cudaFuncSetAttribute(counts[b], cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kTileWarps * (1 << b));
     if (e2 == cudaSuccess)
-        e2 = cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 + 12 * kTileEdges);
+        e2 = cudaFuncSetAttribute(k_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 + 12 * kTileEdges);
+    if (e2 == cudaSuccess)
+        e2 = cudaFuncSetAttribute(k_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 4096 + 4 * kTileEdges);
     return (e1 == cudaSuccess && e2 == cudaSuccess) ? 0 : -1;
 }
 
