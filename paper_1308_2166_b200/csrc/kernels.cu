@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
     if (a.ctr[kCtrErr] & kErrStage) return;  // sticky error of an earlier async batch
     const uint2 *in = a.d->in;
     extern __shared__ uint32_t dsh[];
-    const uint32_t nV = 1u << a.g.bp1;
+    constexpr uint32_t nV = 1u << NB;  // == 1 << a.g.bp1 (the launch dispatches on it)
     uint16_t *wv = reinterpret_cast<uint16_t *>(dsh);  // [kTileWarps][nV]
     for (uint32_t i = threadIdx.x; i < kTileWarps * nV / 2; i += kTileThreads) dsh[i] = 0;
     __syncthreads();
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kTileThreads) k_count(PartArgs a) {
         uint32_t d = 0;
         if (valid) {
             const uint2 n = norm_edge(__ldg(in + e0 + (ai >> 1)));
-            d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), a.g.bp1);
+            d = vbucket_of(hash_vertex((ai & 1u) ? n.y : n.x), (uint32_t)NB);
         }
         const uint32_t peers = digit_peers_c<NB>(d, valid);
         const uint32_t before = __popc(peers & lt);
