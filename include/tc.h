@@ -249,8 +249,10 @@ int tc_graph_captures(tc_ctx *ctx, uint64_t *captures);
  *                        values per estimator (tc_get_steps) for per-step parity and per-step timing; 0 (default):
  *                        fused.  The states are identical either way.
  *  TC_TUNE_SMALL_INDEX   batches of at most 4096 edges build the whole index in ONE kernel (one CTA per vertex
- *                        bucket of ~512 arcs: validation, pair table, grouping) instead of the eight launches of
+ *                        bucket of ~64 arcs, TC_TUNE_SMALL_INDEX_ARCS: validation, pair table, grouping) instead of the eight launches of
  *                        the partitioned build: 0 = auto (default), 1 = never, 2 = always (same).
+ *  TC_TUNE_SMALL_INDEX_ARCS  target arcs per k_small_index CTA (16..8192, default 64; at most 256 CTAs).  Same
+ *                        results (the segment order in segS may differ; every probe goes through the tables).
  *  TC_TUNE_EVENT_CHECKED event mode: 1 = every batch through the four-kernel path that checks the vertex degree
  *                        limit before applying anything (k_ed_pre, k_ed_trigger, k_ed_process, k_ed_post); 0
  *                        (default) = that path only when a degree could reach the limit (m + w > 2^30 - 1),
@@ -262,7 +264,8 @@ int tc_graph_captures(tc_ctx *ctx, uint64_t *captures);
  *                        2 = always (partitioned index).  Same results.
  * Returns TC_EINVAL for an unknown knob or a value out of range.  Synchronises. */
 enum { TC_TUNE_VBUCKET_ARCS = 0, TC_TUNE_VBUCKET_CAP = 2, TC_TUNE_VBUCKET_SORT_CAP = 4, TC_TUNE_SMALL_BATCH = 6,
-       TC_TUNE_SPLIT_KERNELS = 8, TC_TUNE_SMALL_INDEX = 10, TC_TUNE_EVENT_CHECKED = 12, TC_TUNE_PAIR_FILTER = 14 };
+       TC_TUNE_SPLIT_KERNELS = 8, TC_TUNE_SMALL_INDEX = 10, TC_TUNE_EVENT_CHECKED = 12, TC_TUNE_PAIR_FILTER = 14,
+       TC_TUNE_SMALL_INDEX_ARCS = 16 };
 int tc_tune(tc_ctx *ctx, int knob, uint64_t value);
 
 /* tc_set_mode -- the estimator update rule (reading R17, §10 row 4).

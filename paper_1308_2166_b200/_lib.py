@@ -24,7 +24,7 @@ TC_EINTERNAL = -11
 TC_INGEST_SKIP_LOOPS = 1
 TC_NPHASES = 4
 PHASES = ("partition", "pairs", "vertices", "update")
-TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4, "small_batch": 6, "split_kernels": 8, "small_index": 10, "event_checked": 12, "pair_filter": 14}
+TUNE = {"vbucket_arcs": 0, "vbucket_cap": 2, "vbucket_sort_cap": 4, "small_batch": 6, "split_kernels": 8, "small_index": 10, "event_checked": 12, "pair_filter": 14, "small_index_arcs": 16}
 
 EXPORTS = ["tc_create", "tc_create_shard", "tc_create_rank", "tc_create_ex", "tc_nccl_unique_id", "tc_rank_info", "tc_push_batch", "tc_push_batch_after", "tc_test_draws", "tc_test_philox", "tc_estimate", "tc_reset", "tc_destroy", "tc_closed_sum",
            "tc_estimate_mom", "tc_closed_sum_async", "tc_required_estimators", "tc_group_sums", "tc_get_state", "tc_set_state", "tc_set_counters", "tc_counters", "tc_set_async", "tc_set_graphs", "tc_graph_captures", "tc_tune", "tc_set_mode", "tc_get_event_state", "tc_event_counters", "tc_get_steps", "tc_sync",

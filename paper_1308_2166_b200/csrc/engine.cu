@@ -870,6 +870,10 @@ int tc_tune(tc_ctx *ctx, int knob, uint64_t value) {
                 if (value > 2) return TC_EINVAL;
                 c->tune.small_index = (uint32_t)value;
                 return TC_OK;
+            case TC_TUNE_SMALL_INDEX_ARCS:
+                if (value < 16 || value > 8192) return TC_EINVAL;
+                c->tune.small_index_arcs = (uint32_t)value;
+                return TC_OK;
             case TC_TUNE_EVENT_CHECKED:
                 if (value > 1) return TC_EINVAL;
                 c->tune.event_checked = (uint32_t)value;

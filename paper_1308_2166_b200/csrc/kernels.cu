@@ -1282,7 +1282,9 @@ __global__ void __launch_bounds__(kHubThreads, 1) k_vhub(VertArgs a) {
 // them through the hash path.  Same tables and lookups as the partitioned build (a bucket's partition position
 // of an arc is its arc id here).  The per-batch counter resets are done by k_desc, ahead of every CTA.
 // Two instances: <256 threads, 4096-arc buckets> up to w = 2048, <512, 8192> up to w = 4096 (a bucket may hold
-// every arc of the batch).
+// every arc of the batch).  2w / 64 CTAs (Tuning::small_index_arcs; measured 16..512 arcs per CTA): at w = 4096
+// 128 CTAs take 20.0 us vs 25.2 for the 16 CTAs of ~512 arcs (256 CTAs: 29.2), at w = 2048 16.8 vs 22.9 us --
+// the kernel is a chain of dependent phases, and a CTA with fewer arcs finishes its hash path sooner.
 template <int kSmallThreads, uint32_t kSmallCap>
 struct SmallIndexCfg {
     static constexpr uint32_t kHashBytes = HL<kSmallCap, kSmallThreads>::BYTES;
@@ -1944,8 +1946,8 @@ Geometry make_geometry(uint32_t w, const Tuning &t) {
     g.bs = g.bv - g.bp1;
     g.vcap = std::min(t.vcap, kHCapSmall);
     g.sortcap = std::min(t.sortcap, kVChunk);
-    if (g.small_index) {  // one CTA per vertex bucket of ~512 arcs, at most 16 (no partition kernels)
-        g.bv = std::min<uint32_t>(4, ceil_log2((2ull * w + 511) / 512));
+    if (g.small_index) {  // one CTA per vertex bucket of ~small_index_arcs arcs (no partition kernels)
+        g.bv = std::min<uint32_t>(kSmallIndexMaxBits, ceil_log2((2ull * w + t.small_index_arcs - 1) / t.small_index_arcs));
         g.bp1 = g.bs = 0;
     }
     return g;

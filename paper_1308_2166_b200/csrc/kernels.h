@@ -76,7 +76,8 @@ struct Geometry {
     bool small_index;  // the whole index by one CTA (k_small_index; w <= kSmallIndexMax)
 };
 
-constexpr uint32_t kSmallIndexMax = 4096;  // k_small_index: one CTA per vertex bucket of ~512 arcs (a bucket may
+constexpr uint32_t kSmallIndexMaxBits = 8;  // k_small_index: at most 256 CTAs
+constexpr uint32_t kSmallIndexMax = 4096;  // k_small_index: one CTA per vertex bucket of ~Tuning::small_index_arcs arcs (a bucket may
                                            // hold all 2 w arcs: hash path caps 4096 / 8192 at 256 / 512 threads)
 
 // Launch-time values of a push.  The per-batch values (input pointer, m, batch index, pair tag, S slot) are
@@ -103,6 +104,7 @@ struct Tuning {
     uint32_t small_index = 0;      // 0 auto (w <= kSmallIndexMax), 1 never, 2 always when w <= kSmallIndexMax
     uint32_t event_checked = 0;    // event mode: 1 = always the four-kernel path that checks the degree limit
     uint32_t pair_filter = 0;      // 0 auto (w >= kPairFilterMin), 1 never, 2 always (bulk fused pass, partitioned index)
+    uint32_t small_index_arcs = 64;   // k_small_index: target arcs per CTA (vertex bucket), at most 2^kSmallIndexMaxBits CTAs
 };
 
 // Batches of at least kPairFilterMin (index.cuh) edges get the pair filter (below it the pair table is mostly

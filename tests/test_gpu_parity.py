@@ -111,6 +111,8 @@ def test_hub_segments_multi_chunk():
     dict(small_index=2, split_kernels=1),          # one-CTA index + split estimator pass
     dict(pair_filter=2),                           # Step 3 behind the pair filter at every size
     dict(pair_filter=2, small_batch=2, vbucket_arcs=2),  # pair filter + filtered pass + split partition
+    dict(small_index_arcs=16),                     # one-CTA index on its maximum of 256 CTAs
+    dict(small_index_arcs=8192, small_batch=2),    # one-CTA index on a single CTA
 ])
 def test_index_geometry_knobs(knobs):
     """Results never depend on the index geometry (tc_tune): bit-exact against the oracle.  Batches of at most
