@@ -935,16 +935,12 @@ struct ArcSrc {
         }
         return make_uint2(sv[i], sval[i]);
     }
-    __device__ __forceinline__ uint3 vvn(uint32_t i) const {
-        if (g) {
-            const uint4 x = g[i];
-            return make_uint3(x.x, x.y, x.z);
-        }
-        return make_uint3(sv[i], sval[i], snb[i]);
+    // {vertex, val, neighbour, partition position (pslot index)}: the position is carried in .w by the
+    // partitioned build; the shared-memory lists belong to k_small_index, where it is the arc id itself
+    __device__ __forceinline__ uint4 all(uint32_t i) const {
+        if (g) return g[i];
+        return make_uint4(sv[i], sval[i], snb[i], sval[i]);
     }
-    // the arc's partition position (pslot index): carried in .w by the partitioned build; the shared-memory
-    // lists belong to k_small_index, where it is the arc id itself
-    __device__ __forceinline__ uint32_t pre(uint32_t i) const { return g ? g[i].w : sval[i]; }
 };
 
 // Hash-path grouping of n arcs (src) of bucket b whose segments start at slot base + off0; `hub` (if
@@ -969,12 +965,14 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
     __syncthreads();
     // phase 1: local ids (claim order) through the shared hash table; warp w owns items [w 32 R, (w+1) 32 R)
     uint32_t val[R], pk[R], nbv[R];
+    uint32_t prw[R];  // the arc's partition position, kept from the one read of the arc
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const uint32_t i = warp * 32u * R + j * 32u + lane;
         pk[j] = 0xFFFFFFFFu;
         if (i < n) {
-            const uint3 x = src.vvn(i);
+            const uint4 x = src.all(i);
+            prw[j] = x.w;
             val[j] = x.y;
             nbv[j] = x.z;
             uint32_t s = hash_vertex(x.x) & (Tb - 1);
@@ -1069,8 +1067,7 @@ __device__ __forceinline__ void vbucket_hash(const VertArgs &a, uint32_t b, uint
         TC_CHECK(pos < n && b0 + segst[l + 1] <= a.narcs && val[j] < a.narcs, a.ctr);
         a.segS[b0 + pos] = make_uint2(val[j], nbv[j]);
         // by the arc's partition position: this bucket's own range, so the writes fill whole sectors in L2
-        const uint32_t i = warp * 32u * R + j * 32u + lane;
-        const uint32_t pre = src.pre(i);
+        const uint32_t pre = prw[j];
         TC_CHECK(pre < a.narcs, a.ctr);
         a.pslot[pre] = make_uint2(b0 + pos, b0 + segst[l + 1]);
     }
