@@ -571,15 +571,10 @@ static uint32_t enqueue_kernels(tc_ctx *ctx, const BatchArgs &a, const KRec &kr,
     }
     // a1: count, scans, scatter (k_count zeroes the counters and this batch's S)
     rec(2 * TC_PHASE_PARTITION, ms);
-#ifdef TC_EXP_EARLY_PAIRS
-    launches += launch_partition(ix, a, ms, kr, ctx->fork);
-    rec(2 * TC_PHASE_PARTITION + 1, ms);
-#else
     launches += launch_partition(ix, a, ms, kr);
     rec(2 * TC_PHASE_PARTITION + 1, ms);
     // a3 (it reads only the raw batch) on the second stream, alongside the vertex phase
     ok = ok && cudaEventRecord(ctx->fork, ms) == cudaSuccess;
-#endif
     ok = ok && cudaStreamWaitEvent(ss, ctx->fork, 0) == cudaSuccess;
     rec(2 * TC_PHASE_PAIRS, ss);
     launches += launch_pairs(ix, a, ss, kr);

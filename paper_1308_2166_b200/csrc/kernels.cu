@@ -1956,7 +1956,7 @@ static PartArgs part_args(const IndexBufs &ix, const BatchArgs &a) {
                     pf_words((uint32_t)ix.wcap)};
 }
 
-int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr, cudaEvent_t after_count) {
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr) {
     const Geometry &g = a.g;
     const uint32_t nV = 1u << g.bp1;
     const PartArgs p = part_args(ix, a);
@@ -1971,7 +1971,6 @@ int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, co
         default: return 0;
     }
     kr.end(K_COUNT, s);
-    if (after_count) cudaEventRecord(after_count, s);
     kr.beg(K_SCAN_COLS, s);
     k_scan_cols<<<(nV + 31) / 32, kScanWarps * 32, 0, s>>>(ix.cntV, ix.offV, ix.vstart, g.tiles, nV, ix.ctr);
     kr.end(K_SCAN_COLS, s);

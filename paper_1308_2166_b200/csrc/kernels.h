@@ -130,9 +130,7 @@ struct KRec {
 };
 
 // Each returns the number of kernel launches issued.
-// a1; after_count (optional) is recorded behind k_count: k_pairs needs nothing later than that
-int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec(),
-                     cudaEvent_t after_count = nullptr);
+int launch_partition(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1
 int launch_pairs(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());      // a3
 int launch_vertices(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());   // a2
 int launch_small_index(const IndexBufs &ix, const BatchArgs &a, cudaStream_t s, const KRec &kr = KRec());  // a1-a3
